@@ -1,0 +1,311 @@
+"""Seeded synthetic inputs shared by tests, bench.py and the oracle harness.
+
+This module holds NO arithmetic of the method (no series, no walks, no bounds):
+only graph structure, query pairs and the preprocessing input lambda.  Both the
+CUDA path and the oracle consume what it produces; neither is imported here.
+
+Recipes:
+
+* ``tiny_er``      BASELINE config 0: G(n=1000, p=8/(n-1)) + a random spanning
+                   path (connectivity) + the triangle {0,1,2} (non-bipartite).
+* ``rmat``         BASELINE configs 1-4: R-MAT (Chakrabarti et al.) edges with
+                   quadrant probabilities (a,b,c,d), symmetrise, drop self-loops,
+                   dedupe, keep the largest connected component, random relabel,
+                   CSR with every adjacency list sorted ascending.
+* ``query_pairs``  the paper's protocol: half uniform random node pairs,
+                   half uniform random edges, each edge oriented by a fair coin.
+* ``lambda_of``    lambda = max(|lambda_2|, |lambda_n|) of P (Eq. 6) by
+                   ARPACK (scipy ``eigsh``) on N = D^-1/2 A D^-1/2 with the known
+                   top eigenvector sqrt(d/2m) deflated -- the same preprocessing
+                   the paper runs outside its timings.
+* closed-form fixtures (K_n, C_n, paths, Petersen, Fig. 3 toy graph, lollipop).
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+
+@dataclass
+class Graph:
+    n: int
+    offsets: np.ndarray  # int64 [n+1]
+    cols: np.ndarray     # int32 [offsets[n]]
+    name: str = ""
+    lam: float | None = None
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.offsets[-1])
+
+    @property
+    def m(self) -> int:
+        return self.nnz // 2
+
+    def degrees(self) -> np.ndarray:
+        return np.diff(self.offsets)
+
+    def neighbors(self, v: int) -> np.ndarray:
+        return self.cols[self.offsets[v]:self.offsets[v + 1]]
+
+
+def from_edges(n: int, edges, name: str = "", sort_adj: bool = True) -> Graph:
+    """Simple undirected graph from an undirected edge list (symmetrised, deduped,
+    self-loops dropped); adjacency lists sorted ascending."""
+    e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+    e = e[e[:, 0] != e[:, 1]]
+    u = np.concatenate([e[:, 0], e[:, 1]])
+    v = np.concatenate([e[:, 1], e[:, 0]])
+    key = np.unique(u * n + v)
+    u = key // n
+    v = (key % n).astype(np.int32)
+    counts = np.bincount(u, minlength=n)
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=off[1:])
+    return Graph(n, off, v, name)
+
+
+# ------------------------------------------------------------ closed-form fixtures
+def complete(n: int) -> Graph:
+    return from_edges(n, [(i, j) for i in range(n) for j in range(i + 1, n)], f"K{n}")
+
+
+def cycle(n: int) -> Graph:
+    return from_edges(n, [(i, (i + 1) % n) for i in range(n)], f"C{n}")
+
+
+def path(n: int) -> Graph:
+    return from_edges(n, [(i, i + 1) for i in range(n - 1)], f"P{n}")
+
+
+def petersen() -> Graph:
+    outer = [(i, (i + 1) % 5) for i in range(5)]
+    spokes = [(i, i + 5) for i in range(5)]
+    inner = [(5 + i, 5 + (i + 2) % 5) for i in range(5)]
+    return from_edges(10, outer + spokes + inner, "petersen")
+
+
+def toy_fig3() -> tuple[Graph, dict]:
+    """Fig. 3 running example: edges t-{v1..v7}, v2-v8, v8-s, v1-v9, v9-s.
+    Node ids: t=0, v1..v9 = 1..9, s=10.  It is bipartite."""
+    t, s = 0, 10
+    E = [(t, i) for i in range(1, 8)] + [(2, 8), (8, s), (1, 9), (9, s)]
+    return from_edges(11, E, "fig3"), {"s": s, "t": t}
+
+
+def lollipop(path_len: int) -> Graph:
+    """Triangle {0,1,2} with a path 2-3-...-(2+path_len) attached; non-bipartite."""
+    E = [(0, 1), (1, 2), (0, 2)] + [(2 + i, 3 + i) for i in range(path_len)]
+    return from_edges(3 + path_len, E, f"lollipop{path_len}")
+
+
+def star_triangle(leaves: int) -> Graph:
+    """Star centre 0 with leaves 1..L, plus the edge (1,2) closing a triangle."""
+    E = [(0, i) for i in range(1, leaves + 1)] + [(1, 2)]
+    return from_edges(leaves + 1, E, f"star{leaves}tri")
+
+
+def _connected(g: Graph) -> bool:
+    seen = np.zeros(g.n, bool)
+    stack = [0]
+    seen[0] = True
+    while stack:
+        v = stack.pop()
+        for w in g.neighbors(v):
+            if not seen[w]:
+                seen[w] = True
+                stack.append(int(w))
+    return bool(seen.all())
+
+
+def _bipartite(g: Graph) -> bool:
+    col = -np.ones(g.n, dtype=np.int64)
+    for r in range(g.n):
+        if col[r] >= 0:
+            continue
+        col[r] = 0
+        stack = [r]
+        while stack:
+            v = stack.pop()
+            for w in g.neighbors(v):
+                if col[w] < 0:
+                    col[w] = 1 - col[v]
+                    stack.append(int(w))
+                elif col[w] == col[v]:
+                    return False
+    return True
+
+
+def random_small(seed: int, n: int, p: float) -> Graph:
+    """Connected, non-bipartite G(n,p) + spanning path + triangle {0,1,2}."""
+    rng = np.random.default_rng(seed)
+    iu, ju = np.triu_indices(n, 1)
+    keep = rng.random(len(iu)) < p
+    E = list(zip(iu[keep], ju[keep]))
+    perm = rng.permutation(n)
+    E += [(perm[i], perm[i + 1]) for i in range(n - 1)]
+    E += [(0, 1), (1, 2), (0, 2)]
+    g = from_edges(n, E, f"rand{n}_{seed}")
+    assert _connected(g) and not _bipartite(g)
+    return g
+
+
+# ------------------------------------------------------------ BASELINE config 0
+def tiny_er(seed: int = 20231210, n: int = 1000, avg_deg: float = 8.0) -> Graph:
+    rng = np.random.default_rng(seed)
+    p = avg_deg / (n - 1)
+    iu, ju = np.triu_indices(n, 1)
+    keep = rng.random(len(iu)) < p
+    E = np.stack([iu[keep], ju[keep]], 1)
+    perm = rng.permutation(n)
+    Ep = np.stack([perm[:-1], perm[1:]], 1)
+    Et = np.array([[0, 1], [1, 2], [0, 2]])
+    g = from_edges(n, np.concatenate([E, Ep, Et]), f"tiny_er_n{n}_d{avg_deg:g}_s{seed}")
+    return g
+
+
+# ------------------------------------------------------------ R-MAT configs
+def _rmat_edges(scale: int, nedges: int, a: float, b: float, c: float, rng) -> np.ndarray:
+    u = np.zeros(nedges, dtype=np.int64)
+    v = np.zeros(nedges, dtype=np.int64)
+    ab, abc = a + b, a + b + c
+    chunk = 1 << 24
+    for lo in range(0, nedges, chunk):
+        hi = min(nedges, lo + chunk)
+        uu = np.zeros(hi - lo, dtype=np.int64)
+        vv = np.zeros(hi - lo, dtype=np.int64)
+        for _ in range(scale):
+            r = rng.random(hi - lo)
+            ubit = (r >= ab).astype(np.int64)
+            vbit = (((r >= a) & (r < ab)) | (r >= abc)).astype(np.int64)
+            uu = (uu << 1) | ubit
+            vv = (vv << 1) | vbit
+        u[lo:hi] = uu
+        v[lo:hi] = vv
+    return np.stack([u, v], 1)
+
+
+def rmat(scale: int, edge_factor: float, a=0.57, b=0.19, c=0.19, d=0.05, seed: int = 20231211,
+         name: str | None = None) -> Graph:
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import connected_components
+    assert abs(a + b + c + d - 1.0) < 1e-9
+    rng = np.random.default_rng(seed)
+    N = 1 << scale
+    ne = int(edge_factor * N)
+    E = _rmat_edges(scale, ne, a, b, c, rng)
+    E = E[E[:, 0] != E[:, 1]]
+    u = np.concatenate([E[:, 0], E[:, 1]])
+    v = np.concatenate([E[:, 1], E[:, 0]])
+    del E
+    key = np.unique(u * N + v)
+    del u, v
+    u = key // N
+    v = key % N
+    del key
+    A = sp.csr_matrix((np.ones(len(u), dtype=np.int8), (u, v)), shape=(N, N))
+    ncomp, lab = connected_components(A, directed=False)
+    big = np.argmax(np.bincount(lab))
+    keepn = np.nonzero(lab == big)[0]
+    n = len(keepn)
+    relabel = -np.ones(N, dtype=np.int64)
+    relabel[keepn] = rng.permutation(n)
+    m = (relabel[u] >= 0)
+    u2 = relabel[u[m]]
+    v2 = relabel[v[m]]
+    del u, v, A
+    key = np.sort(u2 * n + v2)
+    del u2, v2
+    uu = key // n
+    cols = (key % n).astype(np.int32)
+    counts = np.bincount(uu, minlength=n)
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=off[1:])
+    nm = name or f"rmat_s{scale}_ef{edge_factor:g}_{a:g}_{b:g}_{c:g}_{d:g}_seed{seed}"
+    return Graph(n, off, cols, nm, meta={"scale": scale, "edge_factor": edge_factor,
+                                        "abcd": [a, b, c, d], "seed": seed})
+
+
+# ------------------------------------------------------------ queries
+def query_pairs(g: Graph, nq: int, seed: int) -> np.ndarray:
+    """P:616 protocol: first half uniform random node pairs, second half uniform
+    random edges (fair-coin orientation).  Returns int32 [nq, 2]."""
+    rng = np.random.default_rng(seed)
+    nr = nq // 2
+    ne = nq - nr
+    rp = rng.integers(0, g.n, size=(nr, 2))
+    eidx = rng.integers(0, g.nnz, size=ne)
+    src = np.searchsorted(g.offsets, eidx, side="right") - 1
+    dst = g.cols[eidx].astype(np.int64)
+    flip = rng.random(ne) < 0.5
+    ep = np.stack([np.where(flip, dst, src), np.where(flip, src, dst)], 1)
+    return np.ascontiguousarray(np.concatenate([rp, ep]).astype(np.int32))
+
+
+# ------------------------------------------------------------ lambda (preprocessing input)
+def lambda_of(g: Graph, tol: float = 1e-10) -> float:
+    """max(|lambda_2|, |lambda_n|) of P via ARPACK on the deflated symmetric operator."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as sla
+    d = g.degrees().astype(np.float64)
+    rows = np.repeat(np.arange(g.n), g.degrees())
+    isd = 1.0 / np.sqrt(d)
+    N = sp.csr_matrix((isd[rows] * isd[g.cols], g.cols, g.offsets), shape=(g.n, g.n))
+    u1 = np.sqrt(d / d.sum())
+
+    def mv(x):
+        x = np.asarray(x).ravel()
+        y = N @ x
+        return y - u1 * (u1 @ x)
+
+    op = sla.LinearOperator((g.n, g.n), matvec=mv, dtype=np.float64)
+    vals = sla.eigsh(op, k=2, which="LM", tol=tol, return_eigenvectors=False,
+                     v0=np.random.default_rng(1).random(g.n))
+    return float(np.max(np.abs(vals)))
+
+
+# ------------------------------------------------------------ BASELINE configs
+CONFIGS = {
+    # name: (kind, params, nq, eps list)
+    "tiny": ("tiny_er", dict(seed=20231210), 100, [0.1, 0.5]),
+    "rmat20": ("rmat", dict(scale=20, edge_factor=5, seed=20231211), 10_000, [0.5, 0.2, 0.1, 0.05]),
+    "lj": ("rmat", dict(scale=23, edge_factor=4.5, seed=20231212), 100_000, [0.1]),
+    "orkut": ("rmat", dict(scale=18, edge_factor=40, a=0.45, b=0.22, c=0.22, d=0.11, seed=20231213),
+              100_000, [0.2, 0.1]),
+}
+
+
+def cache_dir() -> Path:
+    p = Path(os.environ.get("GEER_WORKLOAD_CACHE", "/tmp/geer_workloads"))
+    p.mkdir(parents=True, exist_ok=True)
+    return p
+
+
+def load_config(name: str, with_lambda: bool = True) -> tuple[Graph, np.ndarray, list]:
+    """Generate (or load from the cache) a BASELINE config: graph, query pairs, eps list.
+    The cache is only a speed-up; it is regenerated when absent."""
+    kind, params, nq, eps = CONFIGS[name]
+    tag = hashlib.sha1(repr((kind, sorted(params.items()), nq, 3)).encode()).hexdigest()[:12]
+    f = cache_dir() / f"{name}_{tag}.npz"
+    if f.exists():
+        z = np.load(f)
+        g = Graph(int(z["n"]), z["offsets"], z["cols"], str(z["name"]),
+                  float(z["lam"]) if float(z["lam"]) > 0 else None)
+        pairs = z["pairs"]
+    else:
+        g = tiny_er(**params) if kind == "tiny_er" else rmat(**params)
+        pairs = query_pairs(g, nq, seed=params["seed"] + 1)
+        g.lam = None
+    if with_lambda and g.lam is None:
+        g.lam = lambda_of(g)
+    if not f.exists() or (with_lambda and g.lam is not None):
+        tmp = f.with_suffix(".tmp%d.npz" % os.getpid())
+        np.savez(tmp, n=g.n, offsets=g.offsets, cols=g.cols, name=g.name,
+                 lam=g.lam if g.lam is not None else -1.0, pairs=pairs)
+        os.replace(tmp, f)
+    return g, pairs, eps
