@@ -1,0 +1,361 @@
+"""bench.py -- GEER epsilon-approximate PER queries/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE configs[1]): R-MAT scale 20, edge factor 5, (a,b,c,d) = (.57,.19,.19,.05),
+symmetrised, deduped, self-loops dropped, largest connected component, random relabel;
+10,000 queries per GPU (half uniform random pairs, half uniform random edges);
+eps = 0.1, delta = 0.01, tau = 5.  lambda from the library's device Lanczos
+estimate (preprocessing, untimed like the paper's ARPACK step).
+
+A step = one er_query_batch_ex over the rank's queries (inputs resident in HBM, results
+left in HBM), followed by the NCCL all-gather of results when N > 1.  W untimed warm-up
+steps, then K steps, each bracketed by CUDA events on the library's launch stream, with
+L2 flushed between steps (a 256 MiB write, outside the events).  value = queries of all
+ranks / max-over-ranks of the summed step time.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+        torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "eps-approx PER queries/sec (1/2/4/8 B200); SpMM HBM GB/s vs peak"
+CONFIG = "rmat20"
+WALK_BYTES_PER_STEP = 24   # off[v], off[v+1] (16 B) + cols[idx] (4 B) + y-key probe (4 B)
+SPMM_Q = 16                # columns of the K9 dense-block measurement
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_uuid: str | None):
+        self.lines: list[str] = []
+        cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200"]
+        if dev_uuid:
+            cmd += ["-i", dev_uuid]
+        try:
+            self.p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self, min_samples=3, timeout=2.0):
+        if not self.p:
+            return None
+        t0 = time.time()
+        while len(self.lines) < min_samples and time.time() - t0 < timeout:
+            time.sleep(0.05)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=2)
+        except Exception:
+            self.p.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ncu_traffic_per_step():
+    """dram bytes per walk step of K6 from the committed ncu --set full summary, if any."""
+    for p in sorted((ROOT / "profiles").glob("ncu_k_walks_*.json"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+            return float(d["dram_bytes_per_walk_step"]), p.name
+        except Exception:
+            continue
+    return None, None
+
+
+def cpu_baseline_leg(g, lam, pairs, eps, target_s=10.0):
+    """The oracle as it stands, on the host cores, over a bounded sample of the workload."""
+    import oracle
+    oracle.build()
+    k = len(pairs)
+    half = k // 2
+    n = 250
+    while True:
+        idx = np.concatenate([np.arange(0, min(n, half)), np.arange(half, half + min(n, k - half))])
+        sub = pairs[idx]
+        t0 = time.perf_counter()
+        oracle.geer_batch(g, lam, sub, eps, delta=0.01, with_stats=False)
+        dt = time.perf_counter() - t0
+        if dt >= target_s or n >= half:
+            break
+        n = min(half, int(n * max(2.0, target_s / max(dt, 1e-3) * 1.1)))
+    return {"value": len(sub) / dt, "unit": "queries/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"{len(sub)} of the {k} queries (first {len(sub)//2} random pairs + first "
+                      f"{len(sub) - len(sub)//2} edges), eps={eps}, delta=0.01, tau=5, {dt:.1f} s"}
+
+
+def reference_arm(args):
+    """--impl reference: the oracle (CPU, host cores) on the same workload, metric and unit."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    import workloads as W
+    oracle.build()
+    g, pairs_all, _ = W.load_config(CONFIG, with_lambda=True)
+    pairs = pairs_all[: args.queries]
+    half = len(pairs) // 2
+    ns = args.ref_sample // 2
+    sub = np.concatenate([pairs[:ns], pairs[half:half + ns]])
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.geer_batch(g, g.lam, sub, args.eps, delta=0.01, with_stats=False,
+                          query_index_base=0)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = len(sub) * len(times) / tot
+    cores = oracle.max_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(g, args),
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{len(sub)} of the {len(pairs)} queries per step "
+                                   f"({ns} random pairs + {ns} edges)"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(g, args):
+    return {"workload": f"R-MAT s20 ef5 (.57,.19,.19,.05) LCC, {args.queries} queries/GPU "
+                        f"(50% random pairs, 50% edges), eps={args.eps}, delta=0.01, tau=5",
+            "n": int(g.n), "m": int(g.m), "max_degree": int(g.degrees().max()),
+            "lambda": float(g.lam) if g.lam is not None else None,
+            "queries_per_gpu": args.queries, "eps": args.eps, "delta": 0.01, "tau": 5,
+            "parallelism": f"queries sharded over {args.gpus} GPU(s), CSR replicated",
+            "l2": "flushed between steps (256 MiB device write outside the timed events)",
+            "seeds": {"graph": 20231211, "queries": 20231212, "walks": "0x2312061232DEC0DE"}}
+
+
+def spmm_measure(G, h, g, torch, q=SPMM_Q, reps=10):
+    """K9 (er_spmm) on a dense n x q fp64 block: algorithmic bytes / event time."""
+    X = torch.rand((g.n, q), dtype=torch.float64, device="cuda")
+    Y = torch.empty_like(X)
+    st = torch.cuda.Stream()
+    for _ in range(3):
+        G.er_spmm(h, X, Y, stream=st)
+    st.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        G.er_spmm(h, X, Y, stream=st)
+    e1.record(st)
+    st.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    # algorithmic bytes: offsets (8 B/row) + cols (4 B/arc) + X gathers (8q B/arc) + Y writes (8q B/row)
+    byts = 8 * (g.n + 1) + 4 * g.nnz + 8 * q * g.nnz + 8 * q * g.n
+    return {"q": q, "ms": ms, "achieved_gbs": byts / ms / 1e6, "algorithmic_bytes": byts}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--eps", type=float, default=0.1)
+    ap.add_argument("--queries", type=int, default=10_000)
+    ap.add_argument("--ref-sample", type=int, default=1000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    assert world == args.gpus or world == 1, "--gpus must match the launched world size"
+
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("geer_build", ROOT / "paper_2312_06123_b200" / "build.py")
+    bm = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bm)
+    if rank == 0:
+        bm.build()
+    if dist:
+        dist.barrier()
+    import paper_2312_06123_b200 as G
+    import workloads as W
+    from paper_2312_06123_b200.dist import gather_results
+
+    g, _, _ = W.load_config(CONFIG, with_lambda=False)
+    nq = args.queries
+    # rank r answers its own 10k-query set (weak scaling); rank 0's set is the N=1 set
+    pairs = np.ascontiguousarray(W.query_pairs(g, nq, seed=20231212 + rank))
+    lo = rank * nq
+    h = G.er_graph_create(g.n, g.offsets, g.cols)
+    g.lam = G.er_graph_estimate_lambda(h)
+
+    st = torch.cuda.Stream()
+    pairs_d = torch.from_numpy(pairs).cuda()
+    out_d = torch.zeros(nq, dtype=torch.float64, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
+
+    def step():
+        G.er_query_batch_ex(h, pairs_d, args.eps, 0.01, out=out_d, stream=st, query_index_base=lo)
+        if dist:
+            with torch.cuda.stream(st):
+                gather_results(out_d, nq * world)
+
+    for _ in range(args.warmup):
+        step()
+    st.synchronize()
+
+    uuid = None
+    try:
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+    except Exception:
+        pass
+    clocks = ClockSampler(uuid)
+    G.er_graph_profile(h, True)
+    l0 = G.er_graph_kernel_launches(h)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = 0.0
+    for _ in range(args.steps):
+        with torch.cuda.stream(st):
+            flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        step()
+        e1.record(st)
+        st.synchronize()
+        total_ms += e0.elapsed_time(e1)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = G.er_graph_kernel_launches(h) - l0
+    prof = G.er_graph_profile_read(h)
+    G.er_graph_profile(h, False)
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = nq * world * args.steps / (max_ms / 1000.0)
+
+    # ---- e2e: the plain C-ABI call with HOST buffers (H2D pairs + D2H results inside)
+    host_pairs = pairs.copy()
+    e2e_times = []
+    for _ in range(args.steps):
+        with torch.cuda.stream(st):
+            flush.fill_(2)
+        st.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        r = G.er_query_batch_ex(h, host_pairs, args.eps, 0.01, query_index_base=lo)[0]
+        if dist:
+            gather_results(torch.from_numpy(r).cuda(), nq * world).cpu()
+        e2e_times.append(time.perf_counter() - t0)
+    te = torch.tensor([sum(e2e_times)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = nq * world * args.steps / float(te.item())
+
+    if rank == 0:
+        hbm, how = peaks()
+        walk_launch_ms = prof["walk_ms"] / max(prof["walk_launches"], 1)
+        bytes_per_launch = WALK_BYTES_PER_STEP * prof["walk_steps"] / max(prof["walk_launches"], 1)
+        achieved = bytes_per_launch / (walk_launch_ms / 1e3) / 1e9 if walk_launch_ms > 0 else 0.0
+        tps, tsrc = ncu_traffic_per_step()
+        traffic = tps * prof["walk_steps"] / max(prof["walk_launches"], 1) if tps else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(g, args),
+            "roofline": {"bound": "hbm", "kernel": "k_walks (K6, AMC walks)", "achieved": achieved,
+                         "peak": hbm, "peak_kind": how, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": traffic, "traffic_source": tsrc,
+                         "algorithmic_bytes_per_step": WALK_BYTES_PER_STEP,
+                         "walk_steps_per_launch": prof["walk_steps"] / max(prof["walk_launches"], 1),
+                         "avg_launch_ms": walk_launch_ms,
+                         "walk_share_of_step": prof["walk_ms"] / max(max_ms, 1e-9)},
+            "phases_ms_per_step": {"smm_head": prof["smm_ms"] / args.steps,
+                                   "walks": prof["walk_ms"] / args.steps,
+                                   "amc_reduce_etc": prof["amc_other_ms"] / args.steps},
+            "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(pairs.nbytes),
+                    "d2h_bytes_per_step": int(nq * 8)},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        try:
+            sp = spmm_measure(G, h, g, torch)
+            sp.update({"peak": hbm, "frac": sp["achieved_gbs"] / hbm})
+            line["spmm"] = sp
+        except Exception as ex:  # noqa: BLE001
+            line["spmm"] = {"error": str(ex)}
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_leg(g, g.lam, pairs, args.eps)
+        print(json.dumps(line), flush=True)
+    G.er_graph_destroy(h)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,64 @@
+"""Build libgeer.so in-tree with nvcc for sm_100a (B200).
+
+Usage: python -m paper_2312_06123_b200.build [--force]
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libgeer.so"
+SOURCES = ["pipeline.cu", "abi.cu", "lambda.cu"]
+HEADERS = ["geer_internal.h", "geer_device.cuh"]
+INCLUDE = PKG.parent / "include" / "geer.h"
+
+NVCC_FLAGS = [
+    "-O3", "-std=c++17", "-lineinfo",
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    # No FMA contraction: the decision arithmetic (Eq. 6/8/9/10, sigma^2) must round
+    # exactly as written, like the oracle (gcc -ffp-contract=off).
+    "-fmad=false",
+    "-Xcompiler", "-fPIC,-fopenmp,-O3",
+    "-Xptxas", "-v",
+    "--expt-relaxed-constexpr",
+]
+
+
+def nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc"):
+        if c and Path(c).exists():
+            return c
+    return "nvcc"
+
+
+def needs_build() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [INCLUDE]
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not needs_build():
+        return LIB
+    tmp = LIB.with_suffix(".so.tmp%d" % os.getpid())
+    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-o", str(tmp), *[str(CSRC / s) for s in SOURCES], "-lgomp"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libgeer.so")
+    (PKG / "build_ptxas.log").write_text(r.stderr)
+    if verbose:
+        sys.stderr.write(r.stderr)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv)
+    print(LIB)

@@ -1,0 +1,370 @@
+// abi.cu -- the extern "C" boundary of libgeer.so (include/geer.h).
+// Argument checking, error codes, graph creation/validation, handle lifetime.
+
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "geer_internal.h"
+
+namespace geer {
+
+static thread_local int t_code = ER_OK;
+static thread_local std::string t_msg = "ok";
+
+void set_error(int code, const std::string &msg)
+{
+    t_code = code;
+    t_msg = msg;
+}
+
+int cuda_fail(cudaError_t e, const char *what)
+{
+    const int code = (e == cudaErrorMemoryAllocation) ? ER_ENOMEM : ER_ECUDA;
+    set_error(code, std::string(what) + ": " + cudaGetErrorString(e));
+    cudaGetLastError();
+    return code;
+}
+
+static void clear_error()
+{
+    t_code = ER_OK;
+    t_msg = "ok";
+}
+
+// Host-side validation of the CSR (graph creation is not on the query path; the
+// paper also loads and preprocesses graphs outside its timings).
+static int validate(int64_t n, const int64_t *off, const int32_t *cols, bool *rows_sorted, int32_t *max_deg,
+                    int *spectral_code, bool spmm_only)
+{
+    if (n < 2 || n > (int64_t)INT32_MAX) {
+        set_error(ER_EINVAL, "n must be in [2, 2^31-1]");
+        return ER_EINVAL;
+    }
+    if (!off || !cols) {
+        set_error(ER_EINVAL, "offsets/cols must be non-NULL");
+        return ER_EINVAL;
+    }
+    if (off[0] != 0) {
+        set_error(ER_EINVAL, "offsets[0] != 0");
+        return ER_EINVAL;
+    }
+    for (int64_t v = 0; v < n; v++) {
+        if (off[v + 1] < off[v]) {
+            set_error(ER_EINVAL, "offsets not non-decreasing at node " + std::to_string(v));
+            return ER_EINVAL;
+        }
+    }
+    const int64_t nnz = off[n];
+    int bad = -1;          // first failure class found
+    int64_t bad_node = -1;
+    bool sorted = true;
+    int32_t md = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(&& : sorted) reduction(max : md)
+    for (int64_t v = 0; v < n; v++) {
+        const int64_t e0 = off[v], e1 = off[v + 1];
+        md = std::max(md, (int32_t)(e1 - e0));
+        int cls = -1;
+        for (int64_t e = e0; e < e1; e++) {
+            const int32_t u = cols[e];
+            if (u < 0 || u >= n) { cls = 0; break; }
+            if (u == v) { cls = 1; break; }
+            if (e > e0 && cols[e - 1] >= u) sorted = false;
+        }
+        if (cls < 0) {
+            // duplicates: sorted copy of the row
+            std::vector<int32_t> row(cols + e0, cols + e1);
+            std::sort(row.begin(), row.end());
+            for (size_t i = 1; i < row.size(); i++)
+                if (row[i] == row[i - 1]) { cls = 2; break; }
+        }
+        if (cls >= 0) {
+#pragma omp critical
+            {
+                if (bad < 0 || cls < bad || (cls == bad && v < bad_node)) {
+                    bad = cls;
+                    bad_node = v;
+                }
+            }
+        }
+    }
+    if (bad == 0) { set_error(ER_EINVAL, "col id out of range in row " + std::to_string(bad_node)); return ER_EINVAL; }
+    if (bad == 1) { set_error(ER_ESELFLOOP, "self-loop at node " + std::to_string(bad_node)); return ER_ESELFLOOP; }
+    if (bad == 2) { set_error(ER_EDUP, "duplicate neighbour in row " + std::to_string(bad_node)); return ER_EDUP; }
+    // symmetry: every (v,u) has (u,v); rows are searched through sorted copies when unsorted
+    std::vector<int32_t> sc;
+    const int32_t *S = cols;
+    if (!sorted) {
+        sc.assign(cols, cols + nnz);
+#pragma omp parallel for schedule(dynamic, 4096)
+        for (int64_t v = 0; v < n; v++) std::sort(sc.begin() + off[v], sc.begin() + off[v + 1]);
+        S = sc.data();
+    }
+    int64_t asym = -1;
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t v = 0; v < n; v++) {
+        for (int64_t e = off[v]; e < off[v + 1]; e++) {
+            const int32_t u = cols[e];
+            if (!std::binary_search(S + off[u], S + off[u + 1], (int32_t)v)) {
+#pragma omp critical
+                if (asym < 0 || v < asym) asym = v;
+                break;
+            }
+        }
+    }
+    if (asym >= 0) { set_error(ER_EASYM, "adjacency not symmetric at node " + std::to_string(asym)); return ER_EASYM; }
+    // connectivity + 2-colouring (BFS from node 0)
+    std::vector<int8_t> colr(n, -1);
+    std::vector<int32_t> queue;
+    queue.reserve(n);
+    colr[0] = 0;
+    queue.push_back(0);
+    bool bip = true;
+    for (size_t h = 0; h < queue.size(); h++) {
+        const int32_t v = queue[h];
+        for (int64_t e = off[v]; e < off[v + 1]; e++) {
+            const int32_t u = cols[e];
+            if (colr[u] < 0) {
+                colr[u] = 1 - colr[v];
+                queue.push_back(u);
+            } else if (colr[u] == colr[v]) {
+                bip = false;
+            }
+        }
+    }
+    *spectral_code = ER_OK;
+    if ((int64_t)queue.size() != n) *spectral_code = ER_EDISCONNECTED;
+    else if (bip) *spectral_code = ER_EBIPARTITE;
+    if (*spectral_code != ER_OK && !spmm_only) {
+        if (*spectral_code == ER_EDISCONNECTED) set_error(ER_EDISCONNECTED, "graph is not connected");
+        else set_error(ER_EBIPARTITE, "graph is bipartite (lambda = 1)");
+        return *spectral_code;
+    }
+    *rows_sorted = sorted;
+    *max_deg = md;
+    return ER_OK;
+}
+
+}  // namespace geer
+
+using namespace geer;
+
+extern "C" {
+
+int er_last_error(void) { return t_code; }
+const char *er_last_error_message(void) { return t_msg.c_str(); }
+
+void er_opts_default(er_opts *o)
+{
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->tau = 5;
+    o->force_ell_b = -1;
+    o->seed = ER_DEFAULT_SEED;
+    o->query_index_base = 0;
+    o->cuda_stream = nullptr;
+    o->pairs_on_device = 0;
+    o->out_on_device = 0;
+    o->ell_variant = 0;
+    o->synchronous = 1;
+}
+
+er_graph *er_graph_create(int64_t n, const int64_t *offsets, const int32_t *cols)
+{
+    return er_graph_create_ex(n, offsets, cols, 0u);
+}
+
+er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *cols, uint32_t flags)
+{
+    clear_error();
+    bool sorted = false;
+    int32_t md = 0;
+    int spec = ER_OK;
+    if (flags & ~ER_CREATE_SPMM_ONLY) {
+        set_error(ER_EINVAL, "unknown flags");
+        return nullptr;
+    }
+    if (validate(n, offsets, cols, &sorted, &md, &spec, (flags & ER_CREATE_SPMM_ONLY) != 0) != ER_OK) return nullptr;
+    er_graph *g = new (std::nothrow) er_graph();
+    if (!g) {
+        set_error(ER_ENOMEM, "host allocation failed");
+        return nullptr;
+    }
+    cudaError_t e = cudaGetDevice(&g->device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+    g->n = n;
+    g->nnz = offsets[n];
+    g->rows_sorted = sorted;
+    g->max_deg = md;
+    g->query_block = spec;
+    int nb = 1;
+    while ((1ll << nb) < n) nb++;
+    g->nbits = nb;
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_off, sizeof(int64_t) * (n + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_cols, sizeof(int32_t) * std::max<int64_t>(g->nnz, 1));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_off, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_cols, cols, sizeof(int32_t) * g->nnz, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "er_graph_create");
+        er_graph_destroy(g);
+        return nullptr;
+    }
+    return g;
+}
+
+void er_graph_destroy(er_graph *g)
+{
+    if (!g) return;
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(g->device);
+        if (g->stream) cudaStreamSynchronize(g->stream);
+        g->ws.release();
+        if (g->d_off) cudaFree(g->d_off);
+        if (g->d_cols) cudaFree(g->d_cols);
+        if (g->d_steps) cudaFree(g->d_steps);
+        if (g->stream) cudaStreamDestroy(g->stream);
+        cudaSetDevice(cur);
+    }
+    delete g;
+}
+
+int er_graph_lambda(const er_graph *g, double *lambda_out)
+{
+    clear_error();
+    if (!g || !lambda_out) { set_error(ER_EINVAL, "NULL argument"); return ER_EINVAL; }
+    if (!g->lambda_set) { set_error(ER_ESPECTRAL, "lambda not set"); return ER_ESPECTRAL; }
+    *lambda_out = g->lambda;
+    return ER_OK;
+}
+
+int er_graph_set_lambda(er_graph *g, double lambda)
+{
+    clear_error();
+    if (!g) { set_error(ER_EINVAL, "NULL graph"); return ER_EINVAL; }
+    if (!(lambda > 0.0 && lambda <= 1.0 - 1e-12)) {
+        set_error(ER_ESPECTRAL, "lambda must be in (0, 1-1e-12]");
+        return ER_ESPECTRAL;
+    }
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->lambda = lambda;
+    g->lambda_set = true;
+    return ER_OK;
+}
+
+int64_t er_graph_num_nodes(const er_graph *g) { return g ? g->n : -1; }
+int64_t er_graph_num_arcs(const er_graph *g) { return g ? g->nnz : -1; }
+int64_t er_graph_kernel_launches(const er_graph *g) { return g ? g->launches : -1; }
+
+int er_query_batch_ex(er_graph *g, const int32_t *pairs, int64_t k, double eps, double p_fail, const er_opts *o,
+                      double *out_r, er_query_stats *stats)
+{
+    clear_error();
+    er_opts opt;
+    if (o) opt = *o;
+    else er_opts_default(&opt);
+    if (!g) { set_error(ER_EINVAL, "NULL graph"); return ER_EINVAL; }
+    if (k < 0) { set_error(ER_EINVAL, "k < 0"); return ER_EINVAL; }
+    if (k > 0 && (!pairs || !out_r)) { set_error(ER_EINVAL, "NULL pairs/out_r"); return ER_EINVAL; }
+    if (!(eps > 0.0) || !std::isfinite(eps)) { set_error(ER_EINVAL, "eps must be > 0"); return ER_EINVAL; }
+    if (!(p_fail > 0.0 && p_fail < 1.0)) { set_error(ER_EINVAL, "p_fail must be in (0,1)"); return ER_EINVAL; }
+    if (opt.tau < 1 || opt.tau > 8) { set_error(ER_EINVAL, "tau must be in [1,8]"); return ER_EINVAL; }
+    if (opt.ell_variant != 0 && opt.ell_variant != 1) { set_error(ER_EINVAL, "ell_variant must be 0 or 1"); return ER_EINVAL; }
+    if (opt.force_ell_b < -1) { set_error(ER_EINVAL, "force_ell_b must be >= -1"); return ER_EINVAL; }
+    if (opt.query_index_base < 0 || opt.query_index_base + k > ((int64_t)1 << 32)) {
+        set_error(ER_EINVAL, "query indices must fit in 32 bits");
+        return ER_EINVAL;
+    }
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->query_block != ER_OK) { set_error(g->query_block, "graph created ER_CREATE_SPMM_ONLY: not connected or bipartite"); return g->query_block; }
+    if (!g->lambda_set) { set_error(ER_ESPECTRAL, "lambda not set (er_graph_set_lambda / er_graph_estimate_lambda)"); return ER_ESPECTRAL; }
+    if (k == 0) return ER_OK;
+    if (!opt.pairs_on_device) {
+        for (int64_t i = 0; i < 2 * k; i++) {
+            if (pairs[i] < 0 || pairs[i] >= g->n) {
+                set_error(ER_EINVAL, "node id out of range at pairs[" + std::to_string(i) + "]");
+                return ER_EINVAL;
+            }
+        }
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != g->device) cudaSetDevice(g->device);
+    const int rc = run_query_batch(g, pairs, k, eps, p_fail, opt, out_r, stats);
+    if (cur != g->device) cudaSetDevice(cur);
+    return rc;
+}
+
+int er_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, double p_fail, double *out_r)
+{
+    return er_query_batch_ex(g, pairs, k, eps, p_fail, nullptr, out_r, nullptr);
+}
+
+int er_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, void *stream)
+{
+    clear_error();
+    if (!g || !X || !Y || X == Y) { set_error(ER_EINVAL, "bad arguments"); return ER_EINVAL; }
+    if (q < 1 || q > 256) { set_error(ER_EINVAL, "q must be in [1,256]"); return ER_EINVAL; }
+    std::lock_guard<std::mutex> lk(g->mu);
+    return run_spmm(g, X, Y, q, normalize, stream ? (cudaStream_t)stream : g->stream);
+}
+
+int er_graph_estimate_lambda(er_graph *g, int iters, double *lambda_out)
+{
+    clear_error();
+    if (!g) { set_error(ER_EINVAL, "NULL graph"); return ER_EINVAL; }
+    if (g->query_block != ER_OK) { set_error(g->query_block, "graph is not connected or bipartite"); return g->query_block; }
+    if (iters < 0 || iters > 2000) { set_error(ER_EINVAL, "iters must be in [0,2000]"); return ER_EINVAL; }
+    std::lock_guard<std::mutex> lk(g->mu);
+    double lam = 0.0;
+    const int rc = run_estimate_lambda(g, iters == 0 ? 120 : iters, &lam);
+    if (rc) return rc;
+    if (!(lam > 0.0 && lam <= 1.0 - 1e-12)) {
+        set_error(ER_ESPECTRAL, "estimated lambda outside (0, 1-1e-12]");
+        return ER_ESPECTRAL;
+    }
+    g->lambda = lam;
+    g->lambda_set = true;
+    if (lambda_out) *lambda_out = lam;
+    return ER_OK;
+}
+
+int er_graph_profile(er_graph *g, int enable)
+{
+    clear_error();
+    if (!g) { set_error(ER_EINVAL, "NULL graph"); return ER_EINVAL; }
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (!g->d_steps) {
+        cudaError_t e = cudaMalloc(&g->d_steps, sizeof(int64_t));
+        if (e != cudaSuccess) return cuda_fail(e, "er_graph_profile");
+    }
+    cudaError_t e = cudaMemsetAsync(g->d_steps, 0, sizeof(int64_t), g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "er_graph_profile");
+    g->prof = er_profile{};
+    g->profiling = enable != 0;
+    return ER_OK;
+}
+
+int er_graph_profile_read(er_graph *g, er_profile *out)
+{
+    clear_error();
+    if (!g || !out) { set_error(ER_EINVAL, "NULL argument"); return ER_EINVAL; }
+    std::lock_guard<std::mutex> lk(g->mu);
+    *out = g->prof;
+    if (g->d_steps) {
+        int64_t steps = 0;
+        cudaError_t e = cudaMemcpy(&steps, g->d_steps, sizeof(int64_t), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(e, "er_graph_profile_read");
+        out->walk_steps = steps;
+    }
+    return ER_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+// geer_internal.h -- internal declarations shared by the libgeer.so translation units.
+// Product code only: nothing here is shared with oracle/ (see DESIGN.md "Independence").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/geer.h"
+
+namespace geer {
+
+// Query phases.
+enum : int32_t { PH_DONE = 0, PH_SMM = 1, PH_AMC = 2 };
+
+// Per-query device state (AoS; one thread/warp per query touches it).
+struct QState {
+    er_query_stats st;     // public diagnostics, copied out at the end
+    int32_t s, t;          // query endpoints
+    int32_t ds, dt;        // degrees d(s), d(t)
+    int32_t phase;         // PH_*
+    int32_t ylog2;         // log2 of the y-table capacity (0 if no table)
+    int64_t yoff;          // offset (in entries) of this query's y-table in the pool
+    double z;              // last batch mean Z (= r_f)
+};
+
+// y-table entry: 16 B, so a probe and its value share one 32 B sector.
+struct YEntry {
+    int32_t key;           // node id, -1 = empty
+    int32_t pad;
+    double val;            // y(v) = s*(v)/d(s) - t*(v)/d(t)
+};
+
+// Per-segment statistics of an SMM iterate (segment = one side of one query).
+struct SegStat {
+    int64_t vol;           // sum of d(v) over the support (Eq. 15 left side)
+    double max1, max2;     // top-2 entries (R5)
+    double at_s, at_t;     // x(s), x(t) of the segment's query
+};
+
+// Per-tile partial sums of one AMC batch (tile = 32 walk pairs of one query).
+struct TilePart {
+    double s1, s2;         // sum Z_k, sum Z_k^2 over the tile's lanes
+    uint64_t ck;           // walk checksum partial
+    uint64_t pad;
+};
+
+// Scalars every kernel of a batch needs (passed by value).
+struct BatchParams {
+    double eps, delta, lambda;
+    double log_inv_lambda;  // log(1/lambda), host-computed
+    double L_eta;           // log(2 tau / delta), host-computed (Eq. 9)
+    double L_bern;          // log(3 / (delta / tau)), host-computed (Eq. 8 with delta/tau)
+    int32_t tau;
+    int32_t force_ell_b;
+    int32_t ell_variant;
+    int32_t nbits;          // bits of a node id (sort keys)
+    uint64_t seed;
+    int64_t qbase;          // global index of query 0
+    int64_t n;
+};
+
+// Grow-only device buffer.
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes, bool keep, cudaStream_t st);
+    template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+    void release();
+};
+
+struct Workspace {
+    DevBuf qs, pairs, out, stats;
+    DevBuf act, act2, cont, idx;                    // active lists / flags / scan outputs
+    DevBuf fr_id, fr_val, fr_seg, fr_off;           // current frontier
+    DevBuf nf_id, nf_val, nf_seg, nf_off;           // next frontier
+    DevBuf ent_off;                                 // emission offsets per frontier entry
+    DevBuf keys, vals, keys2, vals2;                // emitted (key, value) pairs + sort buffers
+    DevBuf head, runidx, runstart;                  // run-length reduction
+    DevBuf segstat;                                 // SegStat per segment
+    DevBuf ycap, yoff, ypool;                       // y-tables
+    DevBuf tiles, parts;                            // AMC tiles
+    DevBuf cub_tmp;                                 // CUB temp storage
+    DevBuf scalars;                                 // small device scalars
+    DevBuf ids, seglen;                             // 0..k-1 ids; compaction lengths
+    void *host_pinned = nullptr;                    // small pinned host scalars
+    size_t host_pinned_cap = 0;
+    void release();
+};
+
+}  // namespace geer
+
+struct er_graph {
+    int device = 0;
+    int64_t n = 0, nnz = 0;
+    int64_t *d_off = nullptr;
+    int32_t *d_cols = nullptr;
+    int32_t max_deg = 0;
+    bool rows_sorted = false;
+    int query_block = 0;  // ER_OK, or the validation code that forbids queries (ER_CREATE_SPMM_ONLY)
+    double lambda = 0.0;
+    bool lambda_set = false;
+    int nbits = 1;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    int64_t launches = 0;
+    bool profiling = false;
+    er_profile prof{};
+    int64_t *d_steps = nullptr;  // device walk-step counter (profiling)
+    geer::Workspace ws;
+};
+
+namespace geer {
+
+void set_error(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+
+// Pipeline entry (pipeline.cu).
+int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, double p_fail,
+                    const er_opts &o, double *out_r, er_query_stats *stats);
+int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st);
+int run_estimate_lambda(er_graph *g, int iters, double *lambda_out);
+
+}  // namespace geer

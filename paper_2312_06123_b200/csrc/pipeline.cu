@@ -1,0 +1,1087 @@
+// pipeline.cu -- the GEER query pipeline on one B200 (sm_100a).
+//
+// Per batch of k queries:
+//   K1 k_setup            ell (Eq. 6), r_b^0, phase per query            Alg. 3 L1-L4
+//   SMM waves, each:      s* <- P s*, t* <- P t* for every active query   Alg. 3 L6-L8
+//     K2 k_emit           push (u, x(v)) for v in frontier, u in N(v)
+//        CUB radix sort   stable sort by (segment, u)
+//     K3 k_run_reduce     ordered sequential sum per (segment, u), / d(u)
+//     K4 k_seg_stats      vol, top-2, x(s), x(t) per segment              Eq. 10, Eq. 15
+//        k_decide         r_b += term; psi -> eta* -> eta0 -> h; switch   Alg. 3 L7, L9
+//     K5 k_yinsert        y = s*/d_s - t*/d_t into a per-query hash table Alg. 1 L7
+//        compaction       frontier + active list of continuing queries
+//   AMC waves b = 0..tau-1:
+//     K6 k_walks          32 walk pairs per warp, Philox keyed by (q,b,side,k,step)  Alg. 1 L5-L9
+//     K7 k_amc_reduce     Z, sigma^2, Bernstein f, stop or double         Alg. 1 L11-L14
+//   K8 k_finalize         r' = r_f + r_b                                  Alg. 3 L11
+//
+// Everything is deterministic: no floating-point atomics, fixed reduction orders.
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "geer_device.cuh"
+#include "geer_internal.h"
+
+namespace geer {
+
+#define CK(call)                                            \
+    do {                                                    \
+        cudaError_t _e = (call);                            \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+#define LAUNCHED(g) ((g)->launches++)
+
+static inline unsigned blocks_for(int64_t n, int per) { return (unsigned)((n + per - 1) / per); }
+
+// ============================================================================ kernels
+
+// K1: per-query setup.
+__global__ void k_setup(int64_t k, const int32_t *__restrict__ pairs, const int64_t *__restrict__ off,
+                        BatchParams P, QState *__restrict__ qs)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    QState Q;
+    memset(&Q, 0, sizeof(Q));
+    const int32_t s = pairs[2 * i], t = pairs[2 * i + 1];
+    Q.s = s;
+    Q.t = t;
+    Q.ds = (int32_t)(off[s + 1] - off[s]);
+    Q.dt = (int32_t)(off[t + 1] - off[t]);
+    Q.phase = PH_DONE;
+    if (s != t) {
+        const double dsf = (double)Q.ds, dtf = (double)Q.dt;
+        // Eq. 6 or Eq. 5; natural log (R2); clamp at 0 (R3).
+        double arg;
+        if (P.ell_variant == 1) arg = 4.0 / (P.eps - P.eps * P.lambda);
+        else arg = (2.0 / dsf + 2.0 / dtf) / (P.eps * (1.0 - P.lambda));
+        const double x = log(arg) / P.log_inv_lambda - 1.0;
+        double c = ceil(x);
+        if (c < 0.0) c = 0.0;
+        const int64_t ell = (int64_t)c;
+        if (x > 0.0 && near_int(x)) Q.st.tie_flags |= 1u;
+        Q.st.ell = (int32_t)ell;
+        // Alg. 3 L4 with s* = e_s, t* = e_t.
+        const double xs_s = 1.0, xt_t = 1.0, xs_t = 0.0, xt_s = 0.0;
+        Q.st.r_b = xs_s / dsf + xt_t / dtf - xs_t / dsf - xt_s / dtf;
+        if (ell > 0) {
+            if (P.force_ell_b == 0) {
+                // AMC alone (Thm 3.4 setting): s = e_s, t = e_t, lf = ell.
+                const double psi = psi_eq10(ell, 1.0, 0.0, 1.0, 0.0, dsf, dtf);
+                const double es = 2.0 * psi * psi * P.L_eta / (P.eps * P.eps);
+                double e0 = ceil(es / (double)(1u << (P.tau - 1)));
+                if (e0 < 1.0) e0 = 1.0;
+                Q.st.ell_f = (int32_t)ell;
+                Q.st.psi = psi;
+                Q.st.eta0 = (int64_t)e0;
+                Q.phase = PH_AMC;
+            } else {
+                Q.phase = PH_SMM;
+            }
+        }
+    }
+    qs[i] = Q;
+}
+
+__global__ void k_flag_phase(int64_t k, const QState *__restrict__ qs, int32_t phase, int32_t *__restrict__ flags,
+                             int32_t *__restrict__ ids)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    flags[i] = qs[i].phase == phase ? 1 : 0;
+    ids[i] = (int32_t)i;
+}
+
+// Initial frontier of an active list: segment 2i = {(s, 1.0)}, 2i+1 = {(t, 1.0)} (Alg. 3 L3).
+__global__ void k_init_frontier(int32_t na, const int32_t *__restrict__ act, const QState *__restrict__ qs,
+                                int32_t *__restrict__ id, double *__restrict__ val, int32_t *__restrict__ seg,
+                                int64_t *__restrict__ segoff)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na) {
+        const QState &Q = qs[act[i]];
+        id[2 * i] = Q.s;
+        id[2 * i + 1] = Q.t;
+        val[2 * i] = 1.0;
+        val[2 * i + 1] = 1.0;
+        seg[2 * i] = 2 * i;
+        seg[2 * i + 1] = 2 * i + 1;
+    }
+    if (i <= 2 * na) segoff[i] = i;
+}
+
+// Degree of every frontier entry (emission count of the push).
+__global__ void k_ent_deg(int64_t F, const int32_t *__restrict__ id, const int64_t *__restrict__ off,
+                          int64_t *__restrict__ deg)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= F) return;
+    const int32_t v = id[e];
+    deg[e] = off[v + 1] - off[v];
+}
+
+// K2: push.  Output position p belongs to entry e = max{e : ent_off[e] <= p}; the pair is
+// (key = seg << nbits | u, value = x(v)) with u the (p - ent_off[e])-th neighbour of v.
+// Pairs are written in frontier order (ascending v within a segment).
+__global__ void k_emit(int64_t E, int64_t F, const int64_t *__restrict__ ent_off, const int32_t *__restrict__ id,
+                       const double *__restrict__ val, const int32_t *__restrict__ seg,
+                       const int64_t *__restrict__ off, const int32_t *__restrict__ cols, int nbits,
+                       uint64_t *__restrict__ keys, double *__restrict__ vals)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= E) return;
+    int64_t lo = 0, hi = F;  // ent_off[lo] <= p < ent_off[hi]
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ent_off[mid] <= p) lo = mid;
+        else hi = mid;
+    }
+    const int32_t v = id[lo];
+    const int32_t u = cols[off[v] + (p - ent_off[lo])];
+    keys[p] = ((uint64_t)(uint32_t)seg[lo] << nbits) | (uint64_t)(uint32_t)u;
+    vals[p] = val[lo];
+}
+
+// Run heads of the sorted keys; the last thread also records the run count.
+__global__ void k_heads(int64_t E, const uint64_t *__restrict__ keys, int32_t *__restrict__ head)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= E) return;
+    head[p] = (p == 0 || keys[p] != keys[p - 1]) ? 1 : 0;
+}
+
+// runidx = inclusive scan of heads; runstart[r] = first position of run r; runstart[U] = E.
+__global__ void k_runstart(int64_t E, const int32_t *__restrict__ head, const int64_t *__restrict__ runincl,
+                           int64_t *__restrict__ runstart, int64_t *__restrict__ dU)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= E) return;
+    if (head[p]) runstart[runincl[p] - 1] = p;
+    if (p == E - 1) {
+        runstart[runincl[p]] = E;
+        *dU = runincl[p];
+    }
+}
+
+// K3: x'(u) = (sum of the run, sequential in ascending source order) / d(u)   (R1, R13).
+__global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const int64_t *__restrict__ runstart,
+                             const uint64_t *__restrict__ keys, const double *__restrict__ vals,
+                             const int64_t *__restrict__ off, int nbits, int32_t *__restrict__ nid,
+                             double *__restrict__ nval, int32_t *__restrict__ nseg)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= Emax || r >= *dU) return;
+    const int64_t p0 = runstart[r], p1 = runstart[r + 1];
+    const uint64_t key = keys[p0];
+    const int32_t u = (int32_t)(key & ((1ull << nbits) - 1));
+    double sum = 0.0;
+    for (int64_t p = p0; p < p1; p++) sum += vals[p];
+    nid[r] = u;
+    nval[r] = sum / (double)(off[u + 1] - off[u]);
+    nseg[r] = (int32_t)(key >> nbits);
+}
+
+// Segment offsets of the (sorted) next frontier: segoff[g] = lower_bound(seg, g).
+__global__ void k_seg_off(int32_t nseg, const int64_t *__restrict__ dU, const int32_t *__restrict__ seg,
+                          int64_t *__restrict__ segoff)
+{
+    const int32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g > nseg) return;
+    const int64_t U = *dU;
+    int64_t lo = 0, hi = U;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (seg[mid] < g) lo = mid + 1;
+        else hi = mid;
+    }
+    segoff[g] = lo;
+}
+
+// K4: per-segment statistics, one warp per segment.
+__global__ void k_seg_stats(int32_t nseg, const int64_t *__restrict__ segoff, const int32_t *__restrict__ id,
+                            const double *__restrict__ val, const int64_t *__restrict__ off,
+                            const int32_t *__restrict__ act, const QState *__restrict__ qs,
+                            SegStat *__restrict__ out)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= nseg) return;
+    const QState &Q = qs[act[g >> 1]];
+    const int32_t s = Q.s, t = Q.t;
+    int64_t vol = 0;
+    double m1 = 0.0, m2 = 0.0, as = 0.0, at = 0.0;
+    for (int64_t e = segoff[g] + lane; e < segoff[g + 1]; e += 32) {
+        const int32_t v = id[e];
+        const double x = val[e];
+        vol += off[v + 1] - off[v];
+        if (x > m1) { m2 = m1; m1 = x; }
+        else if (x > m2) { m2 = x; }
+        if (v == s) as = x;
+        if (v == t) at = x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        vol += __shfl_xor_sync(0xffffffffu, vol, o);
+        const double b1 = __shfl_xor_sync(0xffffffffu, m1, o);
+        const double b2 = __shfl_xor_sync(0xffffffffu, m2, o);
+        const double lo1 = fmin(m1, b1);
+        m1 = fmax(m1, b1);
+        m2 = fmax(lo1, fmax(m2, b2));
+        as = fmax(as, __shfl_xor_sync(0xffffffffu, as, o));
+        at = fmax(at, __shfl_xor_sync(0xffffffffu, at, o));
+    }
+    if (lane == 0) {
+        SegStat S;
+        S.vol = vol;
+        S.max1 = m1;
+        S.max2 = m2;
+        S.at_s = as;
+        S.at_t = at;
+        out[g] = S;
+    }
+}
+
+// Alg. 3 L7-L9 for every active query: r_b increment, Eq. 10 -> Eq. 9 -> eta0 -> h, Eq. 15.
+__global__ void k_decide(int32_t na, const int32_t *__restrict__ act, const SegStat *__restrict__ ss, BatchParams P,
+                         QState *__restrict__ qs, int32_t *__restrict__ cont)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    QState &Q = qs[act[i]];
+    const SegStat S = ss[2 * i], T = ss[2 * i + 1];
+    const double dsf = (double)Q.ds, dtf = (double)Q.dt;
+    const double term = S.at_s / dsf + T.at_t / dtf - S.at_t / dsf - T.at_s / dtf;
+    Q.st.r_b = Q.st.r_b + term;
+    const int32_t lb = Q.st.ell_b;
+    if (lb < 8) Q.st.rb_terms[lb] = term;
+    const int32_t ell_b = lb + 1;
+    Q.st.ell_b = ell_b;
+    const int64_t ell = Q.st.ell;
+    const int64_t vol = S.vol + T.vol;
+    const double psi = psi_eq10(ell - ell_b, S.max1, S.max2, T.max1, T.max2, dsf, dtf);
+    const double es = 2.0 * psi * psi * P.L_eta / (P.eps * P.eps);
+    const double ratio = es / (double)(1u << (P.tau - 1));
+    double e0 = ceil(ratio);
+    if (e0 < 1.0) e0 = 1.0;
+    if (ell - ell_b > 0 && near_int(ratio)) Q.st.tie_flags |= 2u;
+    const int64_t eta0 = (int64_t)e0;
+    const int64_t h = (((int64_t)1 << P.tau) - 1) * eta0;
+    Q.st.vol_last = vol;
+    Q.st.h_last = h;
+    const int64_t maxit = P.force_ell_b >= 0 ? (P.force_ell_b < ell ? P.force_ell_b : ell) : ell;
+    const bool go = ell_b < maxit && !(P.force_ell_b < 0 && vol > h);
+    cont[i] = go ? 1 : 0;
+    if (!go) {
+        const int64_t lf = ell - ell_b;
+        Q.st.ell_f = (int32_t)lf;
+        if (lf > 0) {
+            Q.st.psi = psi;
+            Q.st.eta0 = eta0;
+            Q.phase = PH_AMC;
+        } else {
+            Q.phase = PH_DONE;
+        }
+    }
+}
+
+// y-table capacity for queries that leave the SMM head for AMC in this wave.
+__global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState *__restrict__ qs,
+                       const int32_t *__restrict__ cont, const int64_t *__restrict__ segoff,
+                       int64_t *__restrict__ ycap)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    int64_t cap = 0;
+    if ((cont == nullptr || !cont[i]) && qs[act[i]].phase == PH_AMC) {
+        const int64_t len = segoff[2 * i + 2] - segoff[2 * i];
+        cap = 16;
+        while (cap < 2 * len) cap <<= 1;
+    }
+    ycap[i] = cap;
+}
+
+__global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__ ycap,
+                          const int64_t *__restrict__ yincl, int64_t base, QState *__restrict__ qs,
+                          YEntry *__restrict__ pool)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na || ycap[i] == 0) return;
+    QState &Q = qs[act[i]];
+    const int64_t cap = ycap[i];
+    Q.yoff = base + yincl[i] - cap;
+    int lg = 0;
+    while ((1ll << lg) < cap) lg++;
+    Q.ylog2 = lg;
+    (void)pool;
+}
+
+__global__ void k_yfill(int64_t Y, YEntry *__restrict__ tab)
+{
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= Y) return;
+    YEntry e;
+    e.key = -1;
+    e.pad = 0;
+    e.val = 0.0;
+    tab[j] = e;
+}
+
+// K5: y(v) = s*(v)/d(s) - t*(v)/d(t) for v in supp(s*) U supp(t*) (Alg. 1 L7 with s = s*, t = t*).
+__global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
+                          const int32_t *__restrict__ id, const double *__restrict__ val,
+                          const int64_t *__restrict__ segoff, const int32_t *__restrict__ act,
+                          const int64_t *__restrict__ ycap, const QState *__restrict__ qs, YEntry *__restrict__ pool)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
+    const int32_t g = seg[e];
+    const int32_t i = g >> 1;
+    if (ycap[i] == 0) return;
+    const QState &Q = qs[act[i]];
+    const int32_t v = id[e];
+    const double x = val[e];
+    const int32_t og = g ^ 1;
+    int64_t lo = segoff[og], hi = segoff[og + 1];
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (id[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    const bool found = lo < segoff[og + 1] && id[lo] == v;
+    double a, b;
+    if ((g & 1) == 0) {
+        a = x;
+        b = found ? val[lo] : 0.0;
+    } else {
+        if (found) return;  // inserted by the s-side entry
+        a = 0.0;
+        b = x;
+    }
+    const double y = a / (double)Q.ds - b / (double)Q.dt;
+    YEntry *tab = pool + Q.yoff;
+    const int lg = Q.ylog2;
+    const uint32_t mask = (1u << lg) - 1u;
+    uint32_t h = yslot(v, lg);
+    while (true) {
+        const int32_t prev = atomicCAS(&tab[h].key, -1, v);
+        if (prev == -1) {
+            tab[h].val = y;
+            return;
+        }
+        h = (h + 1) & mask;
+    }
+}
+
+// Continuing segments: new lengths (for the compaction scan).
+__global__ void k_seglen(int32_t nseg, const int32_t *__restrict__ cont, const int64_t *__restrict__ segoff,
+                         int64_t *__restrict__ len)
+{
+    const int32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nseg) return;
+    len[g] = cont[g >> 1] ? segoff[g + 1] - segoff[g] : 0;
+}
+
+__global__ void k_compact_entries(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
+                                  const int32_t *__restrict__ id, const double *__restrict__ val,
+                                  const int64_t *__restrict__ segoff, const int32_t *__restrict__ cont,
+                                  const int32_t *__restrict__ newidx_incl, const int64_t *__restrict__ segnew_incl,
+                                  const int64_t *__restrict__ seglen, int32_t *__restrict__ oid,
+                                  double *__restrict__ oval, int32_t *__restrict__ oseg)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= Fmax || e >= *dF) return;
+    const int32_t g = seg[e];
+    const int32_t i = g >> 1;
+    if (!cont[i]) return;
+    const int64_t dst = segnew_incl[g] - seglen[g] + (e - segoff[g]);
+    oid[dst] = id[e];
+    oval[dst] = val[e];
+    oseg[dst] = 2 * (newidx_incl[i] - 1) + (g & 1);
+}
+
+__global__ void k_compact_lists(int32_t na, const int32_t *__restrict__ cont, const int32_t *__restrict__ newidx_incl,
+                                const int32_t *__restrict__ act, const int64_t *__restrict__ segnew_incl,
+                                const int64_t *__restrict__ seglen, int32_t *__restrict__ act2,
+                                int64_t *__restrict__ segoff2)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    if (cont[i]) {
+        const int32_t j = newidx_incl[i] - 1;
+        act2[j] = act[i];
+        segoff2[2 * j] = segnew_incl[2 * i] - seglen[2 * i];
+        segoff2[2 * j + 1] = segnew_incl[2 * i + 1] - seglen[2 * i + 1];
+    }
+    if (i == na - 1) segoff2[2 * newidx_incl[i]] = segnew_incl[2 * na - 1];
+}
+
+// ---------------------------------------------------------------------------- AMC
+
+__device__ __forceinline__ double ylookup(const YEntry *__restrict__ tab, int lg, int32_t v)
+{
+    const uint32_t mask = (1u << lg) - 1u;
+    uint32_t h = yslot(v, lg);
+    while (true) {
+        const longlong2 e = __ldg(reinterpret_cast<const longlong2 *>(tab + h));
+        const int32_t key = (int32_t)(uint32_t)(unsigned long long)e.x;
+        if (key == v) return __longlong_as_double(e.y);
+        if (key < 0) return 0.0;
+        h = (h + 1) & mask;
+    }
+}
+
+__global__ void k_tiles(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs, int b,
+                        int64_t *__restrict__ ntiles)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    const int64_t eta = qs[amc[i]].st.eta0 << b;
+    ntiles[i] = (eta + 31) / 32;
+}
+
+constexpr int WALK_WARPS = 8;
+
+// K6: one warp = one tile = 32 walk pairs (S_k from s, T_k from t) of one query; both chains
+// are advanced in the same loop (two independent dependent-load chains per thread).
+__global__ void __launch_bounds__(WALK_WARPS * 32)
+k_walks(int64_t T, int32_t na, const int64_t *__restrict__ tile_incl, const int32_t *__restrict__ amc,
+        const QState *__restrict__ qs, const int64_t *__restrict__ off, const int32_t *__restrict__ cols,
+        const YEntry *__restrict__ pool, int b, uint32_t key0, uint32_t key1, int64_t qbase,
+        TilePart *__restrict__ parts)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t tile = (int64_t)blockIdx.x * WALK_WARPS + (threadIdx.x >> 5);
+    if (tile >= T) return;
+    // query of this tile: smallest i with tile_incl[i] > tile
+    int32_t lo = 0, hi = na - 1;
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (tile_incl[mid] > tile) hi = mid;
+        else lo = mid + 1;
+    }
+    const int32_t qi = amc[lo];
+    const int64_t first = lo == 0 ? 0 : tile_incl[lo - 1];
+    const QState &Q = qs[qi];
+    const int32_t lf = Q.st.ell_f;
+    const int64_t eta = Q.st.eta0 << b;
+    const uint64_t k = (uint64_t)(tile - first) * 32u + (uint64_t)lane;
+    const bool active = k < (uint64_t)eta;
+    const uint32_t q = (uint32_t)(qbase + qi);
+    const YEntry *tab = pool + Q.yoff;
+    const int lg = Q.ylog2;
+    int32_t vS = Q.s, vT = Q.t;
+    double aS = 0.0, aT = 0.0;
+    if (active) {
+        const uint32_t c3S = ((uint32_t)b << 29) | (0u << 28) | (uint32_t)(k >> 32);
+        const uint32_t c3T = ((uint32_t)b << 29) | (1u << 28) | (uint32_t)(k >> 32);
+        U4 rS = {0, 0, 0, 0}, rT = {0, 0, 0, 0};
+        for (int32_t j = 1; j <= lf; j++) {
+            uint64_t r64S, r64T;
+            if (j & 1) {
+                const uint32_t c = (uint32_t)((j - 1) >> 1);
+                rS = philox4x32_10(U4{c, (uint32_t)k, q, c3S}, key0, key1);
+                rT = philox4x32_10(U4{c, (uint32_t)k, q, c3T}, key0, key1);
+                r64S = ((uint64_t)rS.y << 32) | rS.x;
+                r64T = ((uint64_t)rT.y << 32) | rT.x;
+            } else {
+                r64S = ((uint64_t)rS.w << 32) | rS.z;
+                r64T = ((uint64_t)rT.w << 32) | rT.z;
+            }
+            const int64_t oS = __ldg(off + vS), oT = __ldg(off + vT);
+            const uint64_t dS = (uint64_t)(__ldg(off + vS + 1) - oS);
+            const uint64_t dT = (uint64_t)(__ldg(off + vT + 1) - oT);
+            vS = __ldg(cols + oS + (int64_t)__umul64hi(r64S, dS));
+            vT = __ldg(cols + oT + (int64_t)__umul64hi(r64T, dT));
+            aS += ylookup(tab, lg, vS);
+            aT += ylookup(tab, lg, vT);
+        }
+    }
+    double z = active ? aS - aT : 0.0;
+    double s1 = z, s2 = z * z;
+    uint64_t ck = active ? walk_hash(q, (uint32_t)b, 0u, k, vS) + walk_hash(q, (uint32_t)b, 1u, k, vT) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        ck += __shfl_xor_sync(0xffffffffu, ck, o);
+    }
+    if (lane == 0) {
+        TilePart tp;
+        tp.s1 = s1;
+        tp.s2 = s2;
+        tp.ck = ck;
+        tp.pad = 0;
+        parts[tile] = tp;
+    }
+}
+
+// K7: one warp per active query: sum its tiles, Alg. 1 L11-L14.
+__global__ void k_amc_reduce(int32_t na, const int32_t *__restrict__ amc, const int64_t *__restrict__ tile_incl,
+                             const TilePart *__restrict__ parts, int b, BatchParams P, QState *__restrict__ qs,
+                             int32_t *__restrict__ cont, unsigned long long *__restrict__ steps_counter)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= na) return;
+    const int64_t t0 = i == 0 ? 0 : tile_incl[i - 1], t1 = tile_incl[i];
+    double s1 = 0.0, s2 = 0.0;
+    uint64_t ck = 0;
+    for (int64_t t = t0 + lane; t < t1; t += 32) {
+        s1 += parts[t].s1;
+        s2 += parts[t].s2;
+        ck += parts[t].ck;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        ck += __shfl_xor_sync(0xffffffffu, ck, o);
+    }
+    if (lane != 0) return;
+    QState &Q = qs[amc[i]];
+    const int64_t eta = Q.st.eta0 << b;
+    const double etaf = (double)eta;
+    const double Z = s1 / etaf;
+    double var = s2 / etaf - Z * Z;
+    if (var < 0.0) var = 0.0;
+    const double f = sqrt(2.0 * var * P.L_bern / etaf) + 3.0 * Q.st.psi * P.L_bern / etaf;
+    Q.st.batches_run = b + 1;
+    Q.st.walks_total += eta;
+    Q.st.steps_total += 2 * eta * (int64_t)Q.st.ell_f;
+    if (steps_counter) atomicAdd(steps_counter, (unsigned long long)(2 * eta * (int64_t)Q.st.ell_f));
+    Q.st.walk_checksum += ck;
+    Q.st.f_last = f;
+    Q.st.sigma2_last = var;
+    Q.z = Z;
+    if (fabs(f - P.eps / 2.0) <= 1e-12 * P.eps) Q.st.tie_flags |= 4u;
+    const bool stop = f <= P.eps / 2.0 || b == P.tau - 1;
+    if (stop) Q.phase = PH_DONE;
+    cont[i] = stop ? 0 : 1;
+}
+
+// K8: r' = r_f + r_b (Alg. 3 L11); s = t -> 0.
+__global__ void k_finalize(int64_t k, const QState *__restrict__ qs, double *__restrict__ out,
+                           er_query_stats *__restrict__ stats)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    const QState &Q = qs[i];
+    er_query_stats st = Q.st;
+    double r;
+    if (Q.s == Q.t) {
+        memset(&st, 0, sizeof(st));
+        r = 0.0;
+    } else {
+        st.r_f = st.batches_run > 0 ? Q.z : 0.0;
+        r = st.r_f + st.r_b;
+    }
+    out[i] = r;
+    if (stats) stats[i] = st;
+}
+
+__global__ void k_select(int32_t n, const int32_t *__restrict__ in, const int32_t *__restrict__ flag,
+                         const int32_t *__restrict__ incl, int32_t *__restrict__ out)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) out[incl[i] - 1] = in[i];
+}
+
+// ============================================================================ K9: dense SpMM
+// Y[v, c] = (sum_{w in N(v)} X[w, c]) [/ d(v)], sequential over the row in CSR order.
+// One thread per (row, column); consecutive threads = consecutive columns of one row.
+__global__ void k_spmm_simple(int64_t n, int32_t q, const int64_t *__restrict__ off, const int32_t *__restrict__ cols,
+                              const double *__restrict__ X, double *__restrict__ Y, int normalize)
+{
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= n * q) return;
+    const int64_t v = tid / q;
+    const int32_t c = (int32_t)(tid - v * q);
+    const int64_t e0 = off[v], e1 = off[v + 1];
+    double sum = 0.0;
+    for (int64_t e = e0; e < e1; e++) sum += X[(int64_t)__ldg(cols + e) * q + c];
+    Y[tid] = normalize ? sum / (double)(e1 - e0) : sum;
+}
+
+// ============================================================================ host side
+
+cudaError_t DevBuf::ensure(size_t bytes, bool keep, cudaStream_t st)
+{
+    if (bytes <= cap) return cudaSuccess;
+    size_t ncap = std::max(bytes, cap + cap / 2);
+    ncap = (ncap + 255) & ~(size_t)255;
+    void *np = nullptr;
+    cudaError_t e = cudaMalloc(&np, ncap);
+    if (e != cudaSuccess) {
+        ncap = (bytes + 255) & ~(size_t)255;
+        cudaGetLastError();
+        e = cudaMalloc(&np, ncap);
+        if (e != cudaSuccess) return e;
+    }
+    if (keep && p && cap) {
+        e = cudaMemcpyAsync(np, p, cap, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return e;
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return e;
+    }
+    if (p) {
+        cudaStreamSynchronize(st);
+        cudaFree(p);
+    }
+    p = np;
+    cap = ncap;
+    return cudaSuccess;
+}
+
+void DevBuf::release()
+{
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+}
+
+void Workspace::release()
+{
+    DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
+                     &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2, &head,
+                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen};
+    for (DevBuf *b : all) b->release();
+    if (host_pinned) cudaFreeHost(host_pinned);
+    host_pinned = nullptr;
+    host_pinned_cap = 0;
+}
+
+namespace {
+
+struct Ctx {
+    er_graph *g;
+    cudaStream_t st;
+    Workspace &ws;
+    int64_t *hp;  // pinned host scalars
+};
+
+#define ENSURE(buf, bytes, keep) CK((buf).ensure((bytes), (keep), c.st))
+
+template <class F>
+int cub_call(Ctx &c, F &&f)
+{
+    size_t bytes = 0;
+    CK(f((void *)nullptr, bytes));
+    ENSURE(c.ws.cub_tmp, bytes + 16, false);
+    size_t b2 = c.ws.cub_tmp.cap;
+    CK(f(c.ws.cub_tmp.p, b2));
+    c.g->launches += 2;
+    return ER_OK;
+}
+
+// out[0] = 0, out[1..n] = inclusive prefix sums of in[0..n).
+template <class T>
+int scan_offsets(Ctx &c, const T *in, T *out, int64_t n)
+{
+    CK(cudaMemsetAsync(out, 0, sizeof(T), c.st));
+    if (n == 0) return ER_OK;
+    return cub_call(c, [&](void *tmp, size_t &bytes) {
+        return cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, c.st);
+    });
+}
+
+template <class T>
+int scan_incl(Ctx &c, const T *in, T *out, int64_t n)
+{
+    if (n == 0) return ER_OK;
+    return cub_call(c, [&](void *tmp, size_t &bytes) {
+        return cub::DeviceScan::InclusiveSum(tmp, bytes, in, out, n, c.st);
+    });
+}
+
+int read_scalars(Ctx &c, std::initializer_list<const int64_t *> src)
+{
+    int j = 0;
+    for (const int64_t *p : src) {
+        CK(cudaMemcpyAsync(c.hp + j, p, sizeof(int64_t), cudaMemcpyDeviceToHost, c.st));
+        j++;
+    }
+    CK(cudaStreamSynchronize(c.st));
+    return ER_OK;
+}
+
+// Select ids[i] for which flag[i] != 0, in order.  Returns the count through *cnt.
+int select_list(Ctx &c, const int32_t *ids, const int32_t *flag, int32_t n, int32_t *out, int32_t *incl_tmp,
+                int64_t *cnt)
+{
+    if (n == 0) {
+        *cnt = 0;
+        return ER_OK;
+    }
+    int rc = scan_incl(c, flag, incl_tmp, n);
+    if (rc) return rc;
+    k_select<<<blocks_for(n, 256), 256, 0, c.st>>>(n, ids, flag, incl_tmp, out);
+    LAUNCHED(c.g);
+    int32_t h = 0;
+    CK(cudaMemcpyAsync(&h, incl_tmp + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    *cnt = h;
+    return ER_OK;
+}
+
+// Build y-tables for the queries of `act` with ycap > 0 from frontier (segoff,id,val,seg; nF entries,
+// device count dF).  `cont` may be null (all queries of the list leave the head).
+int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, const int64_t *segoff,
+                  const int32_t *id, const double *val, const int32_t *seg, int64_t Fmax, const int64_t *dF,
+                  int64_t &pool_used, const BatchParams &P)
+{
+    (void)P;
+    Workspace &ws = c.ws;
+    ENSURE(ws.ycap, sizeof(int64_t) * (na + 1), false);
+    ENSURE(ws.yoff, sizeof(int64_t) * (na + 1), false);
+    int64_t *ycap = ws.ycap.as<int64_t>(), *yincl = ws.yoff.as<int64_t>();
+    k_ycap<<<blocks_for(na, 256), 256, 0, c.st>>>(na, act, ws.qs.as<QState>(), cont, segoff, ycap);
+    LAUNCHED(c.g);
+    int rc = scan_incl(c, ycap, yincl, na);
+    if (rc) return rc;
+    rc = read_scalars(c, {yincl + (na - 1)});
+    if (rc) return rc;
+    const int64_t Y = c.hp[0];
+    if (Y == 0) return ER_OK;
+    ENSURE(ws.ypool, sizeof(YEntry) * (size_t)(pool_used + Y), true);
+    k_yfill<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, ws.ypool.as<YEntry>() + pool_used);
+    LAUNCHED(c.g);
+    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, ycap, yincl, pool_used, ws.qs.as<QState>(),
+                                                    ws.ypool.as<YEntry>());
+    LAUNCHED(c.g);
+    k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, segoff, act, ycap,
+                                                      ws.qs.as<QState>(), ws.ypool.as<YEntry>());
+    LAUNCHED(c.g);
+    pool_used += Y;
+    return ER_OK;
+}
+
+}  // namespace
+
+int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, double p_fail, const er_opts &o,
+                    double *out_r, er_query_stats *stats)
+{
+    Workspace &ws = g->ws;
+    cudaStream_t st = o.cuda_stream ? (cudaStream_t)o.cuda_stream : g->stream;
+    if (!ws.host_pinned) {
+        CK(cudaMallocHost(&ws.host_pinned, 4096));
+        ws.host_pinned_cap = 4096;
+    }
+    Ctx c{g, st, ws, reinterpret_cast<int64_t *>(ws.host_pinned)};
+    if (k == 0) return ER_OK;
+    if (k > (int64_t)INT32_MAX / 4) {
+        set_error(ER_EINVAL, "k too large for one batch (max 536870911)");
+        return ER_EINVAL;
+    }
+
+    BatchParams P;
+    P.eps = eps;
+    P.delta = p_fail;
+    P.lambda = g->lambda;
+    P.log_inv_lambda = std::log(1.0 / g->lambda);
+    P.L_eta = std::log(2.0 * (double)o.tau / p_fail);
+    P.L_bern = std::log(3.0 / (p_fail / (double)o.tau));
+    P.tau = o.tau;
+    P.force_ell_b = o.force_ell_b;
+    P.ell_variant = o.ell_variant;
+    P.nbits = g->nbits;
+    P.seed = o.seed;
+    P.qbase = o.query_index_base;
+    P.n = g->n;
+
+    // ---- inputs
+    const int32_t *d_pairs = pairs;
+    if (!o.pairs_on_device) {
+        ENSURE(ws.pairs, sizeof(int32_t) * 2 * k, false);
+        CK(cudaMemcpyAsync(ws.pairs.p, pairs, sizeof(int32_t) * 2 * k, cudaMemcpyHostToDevice, st));
+        d_pairs = ws.pairs.as<int32_t>();
+    }
+    ENSURE(ws.qs, sizeof(QState) * k, false);
+    QState *qs = ws.qs.as<QState>();
+    k_setup<<<blocks_for(k, 128), 128, 0, st>>>(k, d_pairs, g->d_off, P, qs);
+    LAUNCHED(g);
+
+    const int32_t K = (int32_t)k;
+    ENSURE(ws.cont, sizeof(int32_t) * (k + 1), false);
+    ENSURE(ws.idx, sizeof(int32_t) * (k + 1), false);
+    ENSURE(ws.act, sizeof(int32_t) * (k + 1), false);
+    ENSURE(ws.act2, sizeof(int32_t) * (k + 1), false);
+    int64_t pool_used = 0;
+    int64_t smm_pairs = 0;
+    int rc;
+
+    // ---- profiling events: [0] SMM start, [1] SMM end, [2+2j] walk j start, [3+2j] walk j end
+    const bool prof = g->profiling;
+    cudaEvent_t ev[2 + 2 * 8 + 1] = {};
+    int nwalk = 0;
+    if (prof) {
+        for (auto &e : ev) CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(ev[0], st));
+    }
+
+    // ---- SMM head
+    {
+        // all-query ids and phase flags
+        ENSURE(ws.ids, sizeof(int32_t) * (k + 1), false);
+        int32_t *ids = ws.ids.as<int32_t>();
+        k_flag_phase<<<blocks_for(k, 256), 256, 0, st>>>(k, qs, PH_SMM, ws.cont.as<int32_t>(), ids);
+        LAUNCHED(g);
+        int64_t na = 0;
+        rc = select_list(c, ids, ws.cont.as<int32_t>(), K, ws.act.as<int32_t>(), ws.idx.as<int32_t>(), &na);
+        if (rc) return rc;
+        // AMC-only queries (force_ell_b == 0) need tables built from e_s, e_t.
+        if (P.force_ell_b == 0) {
+            k_flag_phase<<<blocks_for(k, 256), 256, 0, st>>>(k, qs, PH_AMC, ws.cont.as<int32_t>(), ids);
+            LAUNCHED(g);
+            int64_t n0 = 0;
+            rc = select_list(c, ids, ws.cont.as<int32_t>(), K, ws.act.as<int32_t>(), ws.idx.as<int32_t>(), &n0);
+            if (rc) return rc;
+            if (n0 > 0) {
+                const int64_t F0 = 2 * n0;
+                ENSURE(ws.fr_id, sizeof(int32_t) * F0, false);
+                ENSURE(ws.fr_val, sizeof(double) * F0, false);
+                ENSURE(ws.fr_seg, sizeof(int32_t) * F0, false);
+                ENSURE(ws.fr_off, sizeof(int64_t) * (F0 + 1), false);
+                k_init_frontier<<<blocks_for(F0 + 1, 256), 256, 0, st>>>((int32_t)n0, ws.act.as<int32_t>(), qs,
+                                                                       ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(),
+                                                                       ws.fr_seg.as<int32_t>(), ws.fr_off.as<int64_t>());
+                LAUNCHED(g);
+                rc = build_ytables(c, (int32_t)n0, ws.act.as<int32_t>(), nullptr, ws.fr_off.as<int64_t>(),
+                                   ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(), ws.fr_seg.as<int32_t>(), F0, nullptr,
+                                   pool_used, P);
+                if (rc) return rc;
+            }
+            na = 0;
+        }
+
+        int64_t F = 2 * na;
+        if (na > 0) {
+            ENSURE(ws.fr_id, sizeof(int32_t) * F, false);
+            ENSURE(ws.fr_val, sizeof(double) * F, false);
+            ENSURE(ws.fr_seg, sizeof(int32_t) * F, false);
+            ENSURE(ws.fr_off, sizeof(int64_t) * (F + 1), false);
+            k_init_frontier<<<blocks_for(F + 1, 256), 256, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), qs,
+                                                                   ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(),
+                                                                   ws.fr_seg.as<int32_t>(), ws.fr_off.as<int64_t>());
+            LAUNCHED(g);
+        }
+        while (na > 0) {
+            const int32_t nseg = (int32_t)(2 * na);
+            int gb = 1;
+            while ((1ll << gb) < nseg) gb++;
+            const int end_bit = P.nbits + gb;
+            if (end_bit > 64) {
+                set_error(ER_EINVAL, "sort key exceeds 64 bits");
+                return ER_EINVAL;
+            }
+            // emission offsets
+            ENSURE(ws.ent_off, sizeof(int64_t) * (2 * F + 2), false);
+            int64_t *ent_deg = ws.ent_off.as<int64_t>() + (F + 1);
+            int64_t *ent_off = ws.ent_off.as<int64_t>();
+            k_ent_deg<<<blocks_for(F, 256), 256, 0, st>>>(F, ws.fr_id.as<int32_t>(), g->d_off, ent_deg);
+            LAUNCHED(g);
+            rc = scan_offsets(c, ent_deg, ent_off, F);
+            if (rc) return rc;
+            rc = read_scalars(c, {ent_off + F});
+            if (rc) return rc;
+            const int64_t E = c.hp[0];
+            smm_pairs += E;
+            if (E > (int64_t)INT32_MAX) {
+                set_error(ER_ENOMEM, "SMM wave emits more than 2^31 pairs");
+                return ER_ENOMEM;
+            }
+            ENSURE(ws.keys, sizeof(uint64_t) * E, false);
+            ENSURE(ws.keys2, sizeof(uint64_t) * E, false);
+            ENSURE(ws.vals, sizeof(double) * E, false);
+            ENSURE(ws.vals2, sizeof(double) * E, false);
+            k_emit<<<blocks_for(E, 256), 256, 0, st>>>(E, F, ent_off, ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(),
+                                                       ws.fr_seg.as<int32_t>(), g->d_off, g->d_cols, P.nbits,
+                                                       ws.keys.as<uint64_t>(), ws.vals.as<double>());
+            LAUNCHED(g);
+            cub::DoubleBuffer<uint64_t> dk(ws.keys.as<uint64_t>(), ws.keys2.as<uint64_t>());
+            cub::DoubleBuffer<double> dv(ws.vals.as<double>(), ws.vals2.as<double>());
+            rc = cub_call(c, [&](void *tmp, size_t &bytes) {
+                return cub::DeviceRadixSort::SortPairs(tmp, bytes, dk, dv, (int)E, 0, end_bit, st);
+            });
+            if (rc) return rc;
+            const uint64_t *skeys = dk.Current();
+            const double *svals = dv.Current();
+            // run-length reduction
+            ENSURE(ws.head, sizeof(int32_t) * E, false);
+            ENSURE(ws.runidx, sizeof(int64_t) * E, false);
+            ENSURE(ws.runstart, sizeof(int64_t) * (E + 1), false);
+            ENSURE(ws.scalars, sizeof(int64_t) * 8, false);
+            int64_t *dU = ws.scalars.as<int64_t>();
+            k_heads<<<blocks_for(E, 256), 256, 0, st>>>(E, skeys, ws.head.as<int32_t>());
+            LAUNCHED(g);
+            // inclusive scan of heads into int64 runidx
+            rc = cub_call(c, [&](void *tmp, size_t &bytes) {
+                return cub::DeviceScan::InclusiveSum(tmp, bytes, ws.head.as<int32_t>(), ws.runidx.as<int64_t>(), E, st);
+            });
+            if (rc) return rc;
+            k_runstart<<<blocks_for(E, 256), 256, 0, st>>>(E, ws.head.as<int32_t>(), ws.runidx.as<int64_t>(),
+                                                           ws.runstart.as<int64_t>(), dU);
+            LAUNCHED(g);
+            ENSURE(ws.nf_id, sizeof(int32_t) * E, false);
+            ENSURE(ws.nf_val, sizeof(double) * E, false);
+            ENSURE(ws.nf_seg, sizeof(int32_t) * E, false);
+            ENSURE(ws.nf_off, sizeof(int64_t) * (nseg + 1), false);
+            k_run_reduce<<<blocks_for(E, 256), 256, 0, st>>>(E, dU, ws.runstart.as<int64_t>(), skeys, svals, g->d_off,
+                                                             P.nbits, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
+                                                             ws.nf_seg.as<int32_t>());
+            LAUNCHED(g);
+            k_seg_off<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, dU, ws.nf_seg.as<int32_t>(),
+                                                                 ws.nf_off.as<int64_t>());
+            LAUNCHED(g);
+            ENSURE(ws.segstat, sizeof(SegStat) * nseg, false);
+            k_seg_stats<<<blocks_for((int64_t)nseg * 32, 256), 256, 0, st>>>(
+                nseg, ws.nf_off.as<int64_t>(), ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(), g->d_off,
+                ws.act.as<int32_t>(), qs, ws.segstat.as<SegStat>());
+            LAUNCHED(g);
+            int32_t *cont = ws.cont.as<int32_t>();
+            k_decide<<<blocks_for(na, 128), 128, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), ws.segstat.as<SegStat>(),
+                                                          P, qs, cont);
+            LAUNCHED(g);
+            // y-tables for queries leaving the head now
+            rc = build_ytables(c, (int32_t)na, ws.act.as<int32_t>(), cont, ws.nf_off.as<int64_t>(),
+                               ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), E, dU,
+                               pool_used, P);
+            if (rc) return rc;
+            // compaction of continuing queries
+            int32_t *newidx = ws.idx.as<int32_t>();
+            rc = scan_incl(c, cont, newidx, na);
+            if (rc) return rc;
+            ENSURE(ws.seglen, sizeof(int64_t) * (2 * nseg + 2), false);  // seglen | segnew_incl
+            int64_t *seglen = ws.seglen.as<int64_t>();
+            int64_t *segnew = seglen + nseg;
+            k_seglen<<<blocks_for(nseg, 256), 256, 0, st>>>(nseg, cont, ws.nf_off.as<int64_t>(), seglen);
+            LAUNCHED(g);
+            rc = scan_incl(c, seglen, segnew, nseg);
+            if (rc) return rc;
+            CK(cudaMemcpyAsync(c.hp + 0, newidx + (na - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(c.hp + 1, segnew + (nseg - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            const int64_t na2 = (int64_t)(*reinterpret_cast<int32_t *>(c.hp + 0));
+            const int64_t F2 = c.hp[1];
+            if (na2 > 0) {
+                ENSURE(ws.fr_id, sizeof(int32_t) * F2, false);
+                ENSURE(ws.fr_val, sizeof(double) * F2, false);
+                ENSURE(ws.fr_seg, sizeof(int32_t) * F2, false);
+                ENSURE(ws.fr_off, sizeof(int64_t) * (2 * na2 + 1), false);
+                k_compact_entries<<<blocks_for(E, 256), 256, 0, st>>>(
+                    E, dU, ws.nf_seg.as<int32_t>(), ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
+                    ws.nf_off.as<int64_t>(), cont, newidx, segnew, seglen, ws.fr_id.as<int32_t>(),
+                    ws.fr_val.as<double>(), ws.fr_seg.as<int32_t>());
+                LAUNCHED(g);
+                k_compact_lists<<<blocks_for(na, 256), 256, 0, st>>>((int32_t)na, cont, newidx, ws.act.as<int32_t>(),
+                                                                     segnew, seglen, ws.act2.as<int32_t>(),
+                                                                     ws.fr_off.as<int64_t>());
+                LAUNCHED(g);
+                std::swap(ws.act, ws.act2);
+            }
+            na = na2;
+            F = F2;
+        }
+    }
+
+    if (prof) CK(cudaEventRecord(ev[1], st));
+
+    // ---- AMC tail
+    {
+        int32_t *ids = ws.ids.as<int32_t>();
+        k_flag_phase<<<blocks_for(k, 256), 256, 0, st>>>(k, qs, PH_AMC, ws.cont.as<int32_t>(), ids);
+        LAUNCHED(g);
+        int64_t na = 0;
+        rc = select_list(c, ids, ws.cont.as<int32_t>(), K, ws.act.as<int32_t>(), ws.idx.as<int32_t>(), &na);
+        if (rc) return rc;
+        const uint32_t key0 = (uint32_t)P.seed, key1 = (uint32_t)(P.seed >> 32);
+        for (int b = 0; b < P.tau && na > 0; b++) {
+            ENSURE(ws.tiles, sizeof(int64_t) * 2 * (na + 1), false);
+            int64_t *ntiles = ws.tiles.as<int64_t>();
+            int64_t *tincl = ntiles + (na + 1);
+            k_tiles<<<blocks_for(na, 256), 256, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), qs, b, ntiles);
+            LAUNCHED(g);
+            rc = scan_incl(c, ntiles, tincl, na);
+            if (rc) return rc;
+            rc = read_scalars(c, {tincl + (na - 1)});
+            if (rc) return rc;
+            const int64_t T = c.hp[0];
+            ENSURE(ws.parts, sizeof(TilePart) * T, false);
+            if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk], st));
+            k_walks<<<blocks_for(T, WALK_WARPS), WALK_WARPS * 32, 0, st>>>(
+                T, (int32_t)na, tincl, ws.act.as<int32_t>(), qs, g->d_off, g->d_cols, ws.ypool.as<YEntry>(), b, key0,
+                key1, P.qbase, ws.parts.as<TilePart>());
+            LAUNCHED(g);
+            if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk + 1], st));
+            k_amc_reduce<<<blocks_for(na * 32, 256), 256, 0, st>>>(
+                (int32_t)na, ws.act.as<int32_t>(), tincl, ws.parts.as<TilePart>(), b, P, qs, ws.cont.as<int32_t>(),
+                prof ? reinterpret_cast<unsigned long long *>(g->d_steps) : nullptr);
+            nwalk++;
+            LAUNCHED(g);
+            int64_t na2 = 0;
+            rc = select_list(c, ws.act.as<int32_t>(), ws.cont.as<int32_t>(), (int32_t)na, ws.act2.as<int32_t>(),
+                             ws.idx.as<int32_t>(), &na2);
+            if (rc) return rc;
+            std::swap(ws.act, ws.act2);
+            na = na2;
+        }
+    }
+
+    // ---- results
+    double *d_out = out_r;
+    er_query_stats *d_stats = stats;
+    if (!o.out_on_device) {
+        ENSURE(ws.out, sizeof(double) * k, false);
+        d_out = ws.out.as<double>();
+        if (stats) {
+            ENSURE(ws.stats, sizeof(er_query_stats) * k, false);
+            d_stats = ws.stats.as<er_query_stats>();
+        }
+    }
+    k_finalize<<<blocks_for(k, 128), 128, 0, st>>>(k, qs, d_out, d_stats);
+    LAUNCHED(g);
+    CK(cudaGetLastError());
+    if (!o.out_on_device) {
+        CK(cudaMemcpyAsync(out_r, d_out, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+        if (stats) CK(cudaMemcpyAsync(stats, d_stats, sizeof(er_query_stats) * k, cudaMemcpyDeviceToHost, st));
+    }
+    if (prof) CK(cudaEventRecord(ev[18], st));
+    if (o.synchronous || !o.out_on_device || prof) CK(cudaStreamSynchronize(st));
+    if (prof) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        g->prof.smm_ms += ms;
+        for (int j = 0; j < nwalk; j++) {
+            CK(cudaEventElapsedTime(&ms, ev[2 + 2 * j], ev[3 + 2 * j]));
+            g->prof.walk_ms += ms;
+        }
+        float amc_all = 0.f;
+        CK(cudaEventElapsedTime(&amc_all, ev[1], ev[18]));
+        double walk_this = 0.0;
+        for (int j = 0; j < nwalk; j++) {
+            CK(cudaEventElapsedTime(&ms, ev[2 + 2 * j], ev[3 + 2 * j]));
+            walk_this += ms;
+        }
+        g->prof.amc_other_ms += amc_all - walk_this;
+        g->prof.walk_launches += nwalk;
+        g->prof.smm_pairs += smm_pairs;
+        g->prof.batches += 1;
+        for (auto &e : ev) cudaEventDestroy(e);
+    }
+    return ER_OK;
+}
+
+int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st)
+{
+    const int64_t total = g->n * (int64_t)q;
+    k_spmm_simple<<<blocks_for(total, 256), 256, 0, st>>>(g->n, q, g->d_off, g->d_cols, X, Y, normalize);
+    LAUNCHED(g);
+    CK(cudaGetLastError());
+    return ER_OK;
+}
+
+}  // namespace geer

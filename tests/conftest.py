@@ -17,5 +17,30 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def tiny():
     import workloads as W
-    g, pairs, _ = W.load_config("tiny")
+    g, pairs, _ = W.load_config("tiny", with_lambda=True)
     return g, pairs
+
+
+@pytest.fixture(scope="session")
+def geer():
+    """The built CUDA library (fails loudly without a device: there is no fallback)."""
+    import importlib.util
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    spec = importlib.util.spec_from_file_location("geer_build", ROOT / "paper_2312_06123_b200" / "build.py")
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    m.build()
+    import paper_2312_06123_b200 as G
+    return G
+
+
+@pytest.fixture(scope="session")
+def rmat20(geer):
+    """BASELINE config 1 (R-MAT s20 ef5, 10k queries) with lambda from the device Lanczos
+    estimate, pinned for both the library and the oracle (R12)."""
+    import workloads as W
+    g, pairs, eps = W.load_config("rmat20", with_lambda=False)
+    h = geer.er_graph_create(g.n, g.offsets, g.cols)
+    g.lam = geer.er_graph_estimate_lambda(h)
+    return g, pairs, eps, h

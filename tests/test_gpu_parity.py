@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Acceptance (BASELINE north_star), per query, same (lambda, seed,
+tau, query_index_base) on both sides:
+  decisions         ell, ell_b, ell_f, batches_run, eta0, vol_last, h_last equal
+  walks             walks_total, steps_total, walk_checksum equal (endpoints bit-exact)
+  series terms      rb_terms / r_b within 1e-10 * max(|term|, 1/d_s + 1/d_t);
+                    bit-exact on sorted-adjacency graphs (strict summation order, R13)
+  final estimate    |r'_gpu - r'_oracle| <= 1e-9
+  tiny graph        |r'_gpu - r_exact| <= eps on every pair
+Queries whose tie_flags are set on either side are excluded from the exact
+decision comparison (R15); the test asserts there are none on these inputs.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from oracle import exact
+
+pytestmark = pytest.mark.gpu
+
+DECISIONS = ["ell", "ell_b", "ell_f", "batches_run", "eta0", "vol_last", "h_last",
+             "walks_total", "steps_total", "walk_checksum"]
+
+
+def compare(g, pairs, r_gpu, st_gpu, r_or, st_or, sorted_adj=True):
+    ties = (st_gpu["tie_flags"] | st_or["tie_flags"]) != 0
+    assert ties.sum() == 0, f"{ties.sum()} decision ties"
+    for f in DECISIONS:
+        bad = np.nonzero(st_gpu[f] != st_or[f])[0]
+        assert len(bad) == 0, f"{f} differs at {bad[:5]}: gpu {st_gpu[f][bad[:5]]} oracle {st_or[f][bad[:5]]}"
+    d = g.degrees()
+    scale = 1.0 / d[pairs[:, 0]] + 1.0 / d[pairs[:, 1]]
+    tol = 1e-10 * np.maximum(np.abs(st_or["rb_terms"]), scale[:, None])
+    assert (np.abs(st_gpu["rb_terms"] - st_or["rb_terms"]) <= tol).all()
+    assert (np.abs(st_gpu["r_b"] - st_or["r_b"]) <= 1e-10 * np.maximum(np.abs(st_or["r_b"]), scale)).all()
+    if sorted_adj:
+        assert np.array_equal(st_gpu["r_b"], st_or["r_b"]) and np.array_equal(st_gpu["psi"], st_or["psi"])
+    err = np.abs(r_gpu - r_or)
+    assert err.max() <= 1e-9, f"max |r_gpu - r_oracle| = {err.max()}"
+    return err.max()
+
+
+def run_both(G, h, g, pairs, eps, **kw):
+    r, st = G.er_query_batch_ex(h, pairs, eps, 0.01, stats=True, **kw)
+    okw = {k: v for k, v in kw.items() if k in ("tau", "seed", "query_index_base", "force_ell_b", "ell_variant")}
+    ro, so = oracle.geer_batch(g, g.lam, pairs, eps, delta=0.01, **okw)
+    return r, st, ro, so
+
+
+@pytest.fixture(scope="module")
+def tiny_h(geer, tiny):
+    g, pairs = tiny
+    h = geer.er_graph_create(g.n, g.offsets, g.cols)
+    geer.er_graph_set_lambda(h, g.lam)
+    yield h
+    geer.er_graph_destroy(h)
+
+
+@pytest.mark.parametrize("eps", [0.5, 0.1, 0.05])
+def test_tiny_parity_and_exact(geer, tiny, tiny_h, eps):
+    g, pairs = tiny
+    r, st, ro, so = run_both(geer, tiny_h, g, pairs, eps)
+    compare(g, pairs, r, st, ro, so)
+    ex = exact.er_pinv(g, pairs)
+    assert np.abs(r - ex).max() <= eps
+    assert (st["steps_total"] > 0).any()
+
+
+@pytest.mark.parametrize("kw", [dict(tau=1), dict(tau=8), dict(force_ell_b=0), dict(force_ell_b=3),
+                                dict(ell_variant=1), dict(seed=12345, query_index_base=777)])
+def test_tiny_parity_options(geer, tiny, tiny_h, kw):
+    g, pairs = tiny
+    r, st, ro, so = run_both(geer, tiny_h, g, pairs, 0.2, **kw)
+    compare(g, pairs, r, st, ro, so)
+
+
+def test_tiny_determinism_sharding_device_pointers(geer, tiny, tiny_h):
+    import torch
+    g, pairs = tiny
+    a, _ = geer.er_query_batch_ex(tiny_h, pairs, 0.1)
+    b, _ = geer.er_query_batch_ex(tiny_h, pairs, 0.1)
+    assert a.tobytes() == b.tobytes()
+    # sharding by query_index_base reproduces the unsharded batch bit for bit
+    parts = [geer.er_query_batch_ex(tiny_h, pairs[lo:hi], 0.1, query_index_base=lo)[0]
+             for lo, hi in [(0, 37), (37, 64), (64, 100)]]
+    assert np.concatenate(parts).tobytes() == a.tobytes()
+    # device pointers (pairs, out, stats on the GPU)
+    dp = torch.from_numpy(pairs).cuda()
+    dout = torch.zeros(len(pairs), dtype=torch.float64, device="cuda")
+    dst = torch.zeros(len(pairs) * geer.STATS_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    geer.er_query_batch_ex(tiny_h, dp, 0.1, out=dout, stats=dst)
+    torch.cuda.synchronize()
+    assert dout.cpu().numpy().tobytes() == a.tobytes()
+    # plain 3-call API
+    c = geer.er_query_batch(tiny_h, pairs, 0.1, 0.01)
+    assert c.tobytes() == a.tobytes()
+
+
+def test_edge_cases(geer, tiny, tiny_h):
+    g, pairs = tiny
+    out, st = geer.er_query_batch_ex(tiny_h, np.zeros((0, 2), np.int32), 0.1)
+    assert out.shape == (0,)
+    same = np.array([[5, 5], [0, 0]], dtype=np.int32)
+    out, st = geer.er_query_batch_ex(tiny_h, same, 0.1, stats=True)
+    assert (out == 0.0).all() and (st["ell"] == 0).all()
+    with pytest.raises(geer.GeerError) as e:
+        geer.er_query_batch(tiny_h, np.array([[0, g.n]], np.int32), 0.1)
+    assert e.value.code == geer.ER_EINVAL
+    with pytest.raises(geer.GeerError):
+        geer.er_query_batch(tiny_h, pairs, -0.1)
+    with pytest.raises(geer.GeerError):
+        geer.er_query_batch(tiny_h, pairs, 0.1, 1.5)
+    # ell = 0 (huge eps): r' = 1/d_s + 1/d_t exactly (R3)
+    out, st = geer.er_query_batch_ex(tiny_h, pairs[:10], 50.0, stats=True)
+    d = g.degrees()
+    assert (st["ell"] == 0).all()
+    assert np.array_equal(out, 1.0 / d[pairs[:10, 0]] + 1.0 / d[pairs[:10, 1]])
+    # lambda must be set before queries
+    h2 = geer.er_graph_create(g.n, g.offsets, g.cols)
+    with pytest.raises(geer.GeerError) as e:
+        geer.er_query_batch(h2, pairs, 0.1)
+    assert e.value.code == geer.ER_ESPECTRAL
+    geer.er_graph_destroy(h2)
+
+
+def test_fig3_integer_spmm(geer):
+    import torch
+    from pathlib import Path
+    gold = {}
+    for line in (Path(__file__).parent / "golden" / "fig3_paths.txt").read_text().splitlines():
+        if line.strip() and not line.startswith("#"):
+            k, *v = line.split()
+            gold[k] = [int(x) for x in v]
+    g, idx = W.toy_fig3()
+    h = geer.er_graph_create(g.n, g.offsets, g.cols, flags=geer.ER_CREATE_SPMM_ONLY)
+    X = torch.zeros((g.n, 2), dtype=torch.float64, device="cuda")
+    X[idx["s"], 0] = 1.0
+    X[idx["t"], 1] = 1.0
+    rows_s, rows_t = [], []
+    for _ in range(8):
+        Y = torch.empty_like(X)
+        geer.er_spmm(h, X, Y, normalize=False)
+        X = Y
+        tot = X.sum(0).cpu().numpy()
+        rows_s.append(int(tot[0]))
+        rows_t.append(int(tot[1]))
+    assert rows_s == gold["path_s"] and rows_t == gold["path_t"]
+    with pytest.raises(geer.GeerError) as e:
+        geer.er_query_batch(h, [[0, 1]], 0.1)
+    assert e.value.code == geer.ER_EBIPARTITE
+    geer.er_graph_destroy(h)
+
+
+def test_spmm_matches_dense_and_series(geer):
+    import torch
+    g = W.random_small(3, 60, 0.08)
+    h = geer.er_graph_create(g.n, g.offsets, g.cols)
+    X = np.random.default_rng(0).random((g.n, 7))
+    Y = torch.empty((g.n, 7), dtype=torch.float64, device="cuda")
+    geer.er_spmm(h, torch.from_numpy(X).cuda(), Y)
+    assert np.allclose(Y.cpu().numpy(), exact.dense_P(g) @ X, atol=1e-13)
+    # oracle's own dense propagation is bit-identical (same CSR-order sums)
+    assert np.array_equal(Y.cpu().numpy()[:, 3], oracle.propagate_dense(g, X[:, 3]))
+    geer.er_graph_destroy(h)
+
+
+@pytest.mark.parametrize("n", [5, 10])
+def test_complete_graph_series_on_gpu(geer, n):
+    g = W.complete(n)
+    h = geer.er_graph_create(g.n, g.offsets, g.cols)
+    geer.er_graph_set_lambda(h, 1.0 / (n - 1))
+    out, st = geer.er_query_batch_ex(h, [[0, 1], [2, 4]], 1e-9, force_ell_b=1000, stats=True)
+    ell = int(st["ell"][0])
+    assert ell >= 4 and (st["ell_f"] == 0).all()
+    want = (2 / n) * (1 - (-1 / (n - 1)) ** (ell + 1))
+    assert np.abs(out - want).max() < 1e-14
+    terms = st["rb_terms"][0][:min(ell, 8)]
+    i = np.arange(1, len(terms) + 1)
+    # term_i = r_i - r_{i-1} = (2/n) (-1/(n-1))^i (1 + 1/(n-1))
+    assert np.allclose(terms, (2 / n) * (-1 / (n - 1)) ** i * (1 + 1 / (n - 1)), rtol=1e-12, atol=1e-16)
+    geer.er_graph_destroy(h)
+
+
+def test_lanczos_lambda(geer, tiny):
+    g, _ = tiny
+    h = geer.er_graph_create(g.n, g.offsets, g.cols)
+    lam = geer.er_graph_estimate_lambda(h)
+    true = exact.lambda_dense(g)
+    assert true - 1e-12 <= lam <= true + 1e-6
+    assert geer.er_graph_lambda(h) == lam
+    for gg, want in [(W.petersen(), 2 / 3), (W.complete(6), 1 / 5), (W.cycle(9), np.cos(np.pi / 9))]:
+        hh = geer.er_graph_create(gg.n, gg.offsets, gg.cols)
+        assert abs(geer.er_graph_estimate_lambda(hh) - want) < 1e-6
+        geer.er_graph_destroy(hh)
+    geer.er_graph_destroy(h)
+
+
+def test_rmat20_lambda_vs_arpack(rmat20):
+    g, _, _, _ = rmat20
+    assert abs(g.lam - W.lambda_of(g)) < 1e-6
+
+
+@pytest.mark.parametrize("eps", [0.5, 0.2, 0.1])
+def test_rmat20_parity_full(geer, rmat20, eps):
+    g, pairs, _, h = rmat20
+    r, st, ro, so = run_both(geer, h, g, pairs, eps)
+    compare(g, pairs, r, st, ro, so)
+    a, _ = geer.er_query_batch_ex(h, pairs, eps)
+    assert a.tobytes() == r.tobytes()
+
+
+def test_rmat20_parity_eps005_subset(geer, rmat20):
+    g, pairs, _, h = rmat20
+    sub = pairs[::10]
+    r, st, ro, so = run_both(geer, h, g, sub, 0.05, query_index_base=3)
+    compare(g, sub, r, st, ro, so)
+
+
+def test_launch_counter(geer, tiny, tiny_h):
+    g, pairs = tiny
+    n0 = geer.er_graph_kernel_launches(tiny_h)
+    geer.er_query_batch(tiny_h, pairs, 0.1)
+    assert geer.er_graph_kernel_launches(tiny_h) > n0
