@@ -335,7 +335,9 @@ def main():
                          "walk_share_of_step": prof["walk_ms"] / max(max_ms, 1e-9)},
             "phases_ms_per_step": {"smm_head": prof["smm_ms"] / args.steps,
                                    "walks": prof["walk_ms"] / args.steps,
-                                   "amc_reduce_etc": prof["amc_other_ms"] / args.steps},
+                                   "amc_reduce_etc": prof["amc_other_ms"] / args.steps,
+                                   "smm_pairs_per_step": prof["smm_pairs"] / args.steps,
+                                   "walk_steps_per_step": prof["walk_steps"] / args.steps},
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(pairs.nbytes),
                     "d2h_bytes_per_step": int(nq * 8)},
             "gpu_launches": int(launches),

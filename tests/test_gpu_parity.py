@@ -198,8 +198,10 @@ def test_lanczos_lambda(geer, tiny):
 
 
 def test_rmat20_lambda_vs_arpack(rmat20):
+    # the device estimate is widened by its Ritz residual: an upper estimate (R12), close to ARPACK
     g, _, _, _ = rmat20
-    assert abs(g.lam - W.lambda_of(g)) < 1e-6
+    ref = W.lambda_of(g)
+    assert ref - 1e-9 <= g.lam <= ref + 2e-5
 
 
 @pytest.mark.parametrize("eps", [0.5, 0.2, 0.1])
