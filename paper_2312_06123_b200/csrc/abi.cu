@@ -60,6 +60,10 @@ static int validate(int64_t n, const int64_t *off, const int32_t *cols, bool *ro
         }
     }
     const int64_t nnz = off[n];
+    if (nnz >= ((int64_t)1 << 32)) {
+        set_error(ER_EINVAL, "graphs with 2^32 or more arcs are not supported (32-bit node records)");
+        return ER_EINVAL;
+    }
     int bad = -1;          // first failure class found
     int64_t bad_node = -1;
     bool sorted = true;
@@ -208,6 +212,14 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
     if (e == cudaSuccess) e = cudaMalloc(&g->d_cols, sizeof(int32_t) * std::max<int64_t>(g->nnz, 1));
     if (e == cudaSuccess) e = cudaMemcpy(g->d_off, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g->d_cols, cols, sizeof(int32_t) * g->nnz, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        // 8-byte node records {offset, degree} for the walk kernel (one sector per step)
+        std::vector<uint2> rec(n);
+#pragma omp parallel for schedule(static)
+        for (int64_t v = 0; v < n; v++) rec[v] = make_uint2((uint32_t)offsets[v], (uint32_t)(offsets[v + 1] - offsets[v]));
+        e = cudaMalloc(&g->d_rec, sizeof(uint2) * n);
+        if (e == cudaSuccess) e = cudaMemcpy(g->d_rec, rec.data(), sizeof(uint2) * n, cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) {
         cuda_fail(e, "er_graph_create");
         er_graph_destroy(g);
@@ -228,6 +240,7 @@ void er_graph_destroy(er_graph *g)
         g->ws.release();
         if (g->d_off) cudaFree(g->d_off);
         if (g->d_cols) cudaFree(g->d_cols);
+        if (g->d_rec) cudaFree(g->d_rec);
         if (g->d_steps) cudaFree(g->d_steps);
         if (g->stream) cudaStreamDestroy(g->stream);
         cudaSetDevice(cur);

@@ -37,8 +37,9 @@ struct YEntry {
 // Per-segment statistics of an SMM iterate (segment = one side of one query).
 struct SegStat {
     int64_t vol;           // sum of d(v) over the support (Eq. 15 left side)
-    double max1, max2;     // top-2 entries (R5)
+    double max1, max2;     // top-2 entries (R5); accumulated as uint64 bit patterns (x >= 0)
     double at_s, at_t;     // x(s), x(t) of the segment's query
+    unsigned long long n_max1;  // occurrences of max1
 };
 
 // Per-tile partial sums of one AMC batch (tile = 32 walk pairs of one query).
@@ -85,7 +86,7 @@ struct Workspace {
     DevBuf tiles, parts;                            // AMC tiles
     DevBuf cub_tmp;                                 // CUB temp storage
     DevBuf scalars;                                 // small device scalars
-    DevBuf ids, seglen;                             // 0..k-1 ids; compaction lengths
+    DevBuf ids, seglen, segbeg, lfkey;              // 0..k-1 ids; compaction lengths; sort segments; AMC order
     void *host_pinned = nullptr;                    // small pinned host scalars
     size_t host_pinned_cap = 0;
     void release();
@@ -98,6 +99,7 @@ struct er_graph {
     int64_t n = 0, nnz = 0;
     int64_t *d_off = nullptr;
     int32_t *d_cols = nullptr;
+    uint2 *d_rec = nullptr;       // {offset, degree} per node (offsets < 2^32)
     int32_t max_deg = 0;
     bool rows_sorted = false;
     int query_block = 0;  // ER_OK, or the validation code that forbids queries (ER_CREATE_SPMM_ONLY)

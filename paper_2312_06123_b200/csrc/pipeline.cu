@@ -4,14 +4,14 @@
 //   K1 k_setup            ell (Eq. 6), r_b^0, phase per query            Alg. 3 L1-L4
 //   SMM waves, each:      s* <- P s*, t* <- P t* for every active query   Alg. 3 L6-L8
 //     K2 k_emit           push (u, x(v)) for v in frontier, u in N(v)
-//        CUB radix sort   stable sort by (segment, u)
+//        CUB radix sort   stable sort by (segment, u) on packed keys, chunked by segments
 //     K3 k_run_reduce     ordered sequential sum per (segment, u), / d(u)
-//     K4 k_seg_stats      vol, top-2, x(s), x(t) per segment              Eq. 10, Eq. 15
+//     K4 (fused in K3) + k_seg_max2  vol, top-2, x(s), x(t) per segment  Eq. 10, Eq. 15
 //        k_decide         r_b += term; psi -> eta* -> eta0 -> h; switch   Alg. 3 L7, L9
 //     K5 k_yinsert        y = s*/d_s - t*/d_t into a per-query hash table Alg. 1 L7
 //        compaction       frontier + active list of continuing queries
 //   AMC waves b = 0..tau-1:
-//     K6 k_walks          32 walk pairs per warp, Philox keyed by (q,b,side,k,step)  Alg. 1 L5-L9
+//     K6 k_walks          thread = walk pair, flattened over queries; Philox (q,b,side,k,step)  Alg. 1 L5-L9
 //     K7 k_amc_reduce     Z, sigma^2, Bernstein f, stop or double         Alg. 1 L11-L14
 //   K8 k_finalize         r' = r_f + r_b                                  Alg. 3 L11
 //
@@ -125,13 +125,24 @@ __global__ void k_ent_deg(int64_t F, const int32_t *__restrict__ id, const int64
     deg[e] = off[v + 1] - off[v];
 }
 
+// Segment begins in the emission order: segbeg[g] = ent_off[segoff[g]] (g = 0..nseg).
+__global__ void k_segbeg(int32_t nseg, const int64_t *__restrict__ segoff, const int64_t *__restrict__ ent_off,
+                         int32_t *__restrict__ segbeg)
+{
+    const int32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g > nseg) return;
+    segbeg[g] = (int32_t)ent_off[segoff[g]];
+}
+
 // K2: push.  Output position p belongs to entry e = max{e : ent_off[e] <= p}; the pair is
-// (key = seg << nbits | u, value = x(v)) with u the (p - ent_off[e])-th neighbour of v.
-// Pairs are written in frontier order (ascending v within a segment).
+// (key = (seg mod spc) << nbits | u, value = x(v)) with u the (p - ent_off[e])-th neighbour of
+// v.  Pairs are written in frontier order: segment by segment, ascending v inside a segment.
+// Segments are sorted in chunks of spc segments, so the chunk-local segment id fits the key.
+template <class KeyT>
 __global__ void k_emit(int64_t E, int64_t F, const int64_t *__restrict__ ent_off, const int32_t *__restrict__ id,
-                       const double *__restrict__ val, const int32_t *__restrict__ seg,
-                       const int64_t *__restrict__ off, const int32_t *__restrict__ cols, int nbits,
-                       uint64_t *__restrict__ keys, double *__restrict__ vals)
+                       const double *__restrict__ val, const int32_t *__restrict__ seg, int64_t spc, int nbits,
+                       const int64_t *__restrict__ off, const int32_t *__restrict__ cols, KeyT *__restrict__ keys,
+                       double *__restrict__ vals)
 {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= E) return;
@@ -142,17 +153,24 @@ __global__ void k_emit(int64_t E, int64_t F, const int64_t *__restrict__ ent_off
         else hi = mid;
     }
     const int32_t v = id[lo];
-    const int32_t u = cols[off[v] + (p - ent_off[lo])];
-    keys[p] = ((uint64_t)(uint32_t)seg[lo] << nbits) | (uint64_t)(uint32_t)u;
+    const uint32_t u = (uint32_t)cols[off[v] + (p - ent_off[lo])];
+    keys[p] = ((KeyT)(seg[lo] % spc) << nbits) | (KeyT)u;
     vals[p] = val[lo];
 }
 
-// Run heads of the sorted keys; the last thread also records the run count.
-__global__ void k_heads(int64_t E, const uint64_t *__restrict__ keys, int32_t *__restrict__ head)
+// Run heads of the (per-segment) sorted keys: a key change or a segment start.
+template <class KeyT>
+__global__ void k_heads(int64_t E, const KeyT *__restrict__ keys, int32_t *__restrict__ head)
 {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= E) return;
     head[p] = (p == 0 || keys[p] != keys[p - 1]) ? 1 : 0;
+}
+
+__global__ void k_mark_segbeg(int32_t nseg, const int32_t *__restrict__ segbeg, int32_t *__restrict__ head)
+{
+    const int32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < nseg && segbeg[g] < segbeg[g + 1]) head[segbeg[g]] = 1;
 }
 
 // runidx = inclusive scan of heads; runstart[r] = first position of run r; runstart[U] = E.
@@ -168,22 +186,94 @@ __global__ void k_runstart(int64_t E, const int32_t *__restrict__ head, const in
     }
 }
 
-// K3: x'(u) = (sum of the run, sequential in ascending source order) / d(u)   (R1, R13).
+// Segmented warp reduction over lanes sorted by g: the first lane of each run of equal g
+// ends up holding op over that run's lanes (order-independent ops only: +, max).
+template <class T, class Op>
+__device__ __forceinline__ T warp_seg_reduce(T v, int32_t g, Op op)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T ov = __shfl_down_sync(0xffffffffu, v, o);
+        const int32_t og = __shfl_down_sync(0xffffffffu, g, o);
+        if (lane + o < 32 && og == g) v = op(v, ov);
+    }
+    return v;
+}
+
+__device__ __forceinline__ bool warp_seg_head(int32_t g)
+{
+    const int32_t pg = __shfl_up_sync(0xffffffffu, g, 1);
+    return (threadIdx.x & 31) == 0 || pg != g;
+}
+
+// K3 + K4a: x'(u) = (sum of the run, sequential in ascending source order) / d(u) (R1, R13),
+// fused with the segment statistics that are order-independent: vol = sum d(u) (int64 add),
+// max1 (max of non-negative doubles as uint64 bit patterns), x(s), x(t) (single writers).
+template <class KeyT>
 __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const int64_t *__restrict__ runstart,
-                             const uint64_t *__restrict__ keys, const double *__restrict__ vals,
-                             const int64_t *__restrict__ off, int nbits, int32_t *__restrict__ nid,
-                             double *__restrict__ nval, int32_t *__restrict__ nseg)
+                             const KeyT *__restrict__ keys, int nbits, const double *__restrict__ vals,
+                             const int32_t *__restrict__ segbeg, int32_t nseg, const int64_t *__restrict__ off,
+                             const int32_t *__restrict__ act, const QState *__restrict__ qs,
+                             int32_t *__restrict__ nid, double *__restrict__ nval, int32_t *__restrict__ nseg_out,
+                             SegStat *__restrict__ ss)
 {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= Emax || r >= *dU) return;
-    const int64_t p0 = runstart[r], p1 = runstart[r + 1];
-    const uint64_t key = keys[p0];
-    const int32_t u = (int32_t)(key & ((1ull << nbits) - 1));
-    double sum = 0.0;
-    for (int64_t p = p0; p < p1; p++) sum += vals[p];
-    nid[r] = u;
-    nval[r] = sum / (double)(off[u + 1] - off[u]);
-    nseg[r] = (int32_t)(key >> nbits);
+    const bool live = r < Emax && r < *dU;
+    int32_t g = 0x7fffffff;
+    unsigned long long deg = 0, bits = 0;
+    if (live) {
+        const int64_t p0 = runstart[r], p1 = runstart[r + 1];
+        const int32_t u = (int32_t)(keys[p0] & (((KeyT)1 << nbits) - 1));
+        int32_t lo = 0, hi = nseg;  // segbeg[lo] <= p0 < segbeg[hi]
+        while (hi - lo > 1) {
+            const int32_t mid = (lo + hi) >> 1;
+            if (segbeg[mid] <= p0) lo = mid;
+            else hi = mid;
+        }
+        g = lo;
+        double sum = 0.0;
+        for (int64_t p = p0; p < p1; p++) sum += vals[p];
+        const int64_t d = off[u + 1] - off[u];
+        const double x = sum / (double)d;
+        nid[r] = u;
+        nval[r] = x;
+        nseg_out[r] = g;
+        deg = (unsigned long long)d;
+        bits = (unsigned long long)__double_as_longlong(x);
+        const QState &Q = qs[act[g >> 1]];
+        if (u == Q.s) ss[g].at_s = x;
+        if (u == Q.t) ss[g].at_t = x;
+    }
+    const unsigned long long vsum = warp_seg_reduce(deg, g, [](unsigned long long a, unsigned long long b) { return a + b; });
+    const unsigned long long vmax = warp_seg_reduce(bits, g, [](unsigned long long a, unsigned long long b) { return a > b ? a : b; });
+    if (live && warp_seg_head(g)) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(&ss[g].vol), vsum);
+        atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max1), vmax);
+    }
+}
+
+// K4b: max2 of each segment = max1 if max1 occurs twice, else the largest entry below max1 (R5).
+__global__ void k_seg_max2(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
+                           const double *__restrict__ val, SegStat *__restrict__ ss)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = e < Fmax && e < *dF;
+    int32_t g = 0x7fffffff;
+    unsigned long long below = 0, eq = 0;
+    if (live) {
+        g = seg[e];
+        const unsigned long long b = (unsigned long long)__double_as_longlong(val[e]);
+        const unsigned long long m1 = *reinterpret_cast<const unsigned long long *>(&ss[g].max1);
+        if (b < m1) below = b;
+        else eq = 1;
+    }
+    const unsigned long long vb = warp_seg_reduce(below, g, [](unsigned long long a, unsigned long long b) { return a > b ? a : b; });
+    const unsigned long long ve = warp_seg_reduce(eq, g, [](unsigned long long a, unsigned long long b) { return a + b; });
+    if (live && warp_seg_head(g)) {
+        if (vb) atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max2), vb);
+        if (ve) atomicAdd(&ss[g].n_max1, ve);
+    }
 }
 
 // Segment offsets of the (sorted) next frontier: segoff[g] = lower_bound(seg, g).
@@ -202,50 +292,6 @@ __global__ void k_seg_off(int32_t nseg, const int64_t *__restrict__ dU, const in
     segoff[g] = lo;
 }
 
-// K4: per-segment statistics, one warp per segment.
-__global__ void k_seg_stats(int32_t nseg, const int64_t *__restrict__ segoff, const int32_t *__restrict__ id,
-                            const double *__restrict__ val, const int64_t *__restrict__ off,
-                            const int32_t *__restrict__ act, const QState *__restrict__ qs,
-                            SegStat *__restrict__ out)
-{
-    const int lane = threadIdx.x & 31;
-    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (g >= nseg) return;
-    const QState &Q = qs[act[g >> 1]];
-    const int32_t s = Q.s, t = Q.t;
-    int64_t vol = 0;
-    double m1 = 0.0, m2 = 0.0, as = 0.0, at = 0.0;
-    for (int64_t e = segoff[g] + lane; e < segoff[g + 1]; e += 32) {
-        const int32_t v = id[e];
-        const double x = val[e];
-        vol += off[v + 1] - off[v];
-        if (x > m1) { m2 = m1; m1 = x; }
-        else if (x > m2) { m2 = x; }
-        if (v == s) as = x;
-        if (v == t) at = x;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        vol += __shfl_xor_sync(0xffffffffu, vol, o);
-        const double b1 = __shfl_xor_sync(0xffffffffu, m1, o);
-        const double b2 = __shfl_xor_sync(0xffffffffu, m2, o);
-        const double lo1 = fmin(m1, b1);
-        m1 = fmax(m1, b1);
-        m2 = fmax(lo1, fmax(m2, b2));
-        as = fmax(as, __shfl_xor_sync(0xffffffffu, as, o));
-        at = fmax(at, __shfl_xor_sync(0xffffffffu, at, o));
-    }
-    if (lane == 0) {
-        SegStat S;
-        S.vol = vol;
-        S.max1 = m1;
-        S.max2 = m2;
-        S.at_s = as;
-        S.at_t = at;
-        out[g] = S;
-    }
-}
-
 // Alg. 3 L7-L9 for every active query: r_b increment, Eq. 10 -> Eq. 9 -> eta0 -> h, Eq. 15.
 __global__ void k_decide(int32_t na, const int32_t *__restrict__ act, const SegStat *__restrict__ ss, BatchParams P,
                          QState *__restrict__ qs, int32_t *__restrict__ cont)
@@ -253,7 +299,9 @@ __global__ void k_decide(int32_t na, const int32_t *__restrict__ act, const SegS
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
     QState &Q = qs[act[i]];
-    const SegStat S = ss[2 * i], T = ss[2 * i + 1];
+    SegStat S = ss[2 * i], T = ss[2 * i + 1];
+    if (S.n_max1 >= 2) S.max2 = S.max1;   // R5: a repeated maximum is also the second largest
+    if (T.n_max1 >= 2) T.max2 = T.max1;
     const double dsf = (double)Q.ds, dtf = (double)Q.dt;
     const double term = S.at_s / dsf + T.at_t / dtf - S.at_t / dsf - T.at_s / dtf;
     Q.st.r_b = Q.st.r_b + term;
@@ -435,93 +483,173 @@ __device__ __forceinline__ double ylookup(const YEntry *__restrict__ tab, int lg
     }
 }
 
-__global__ void k_tiles(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs, int b,
-                        int64_t *__restrict__ ntiles)
+// Walk pairs of batch b per AMC query, and the AMC sort key (descending ell_f) used to order
+// the flattened walk space so warps mostly see one trip count.
+__global__ void k_npairs(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs, int b,
+                         int64_t *__restrict__ npairs)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
-    const int64_t eta = qs[amc[i]].st.eta0 << b;
-    ntiles[i] = (eta + 31) / 32;
+    npairs[i] = qs[amc[i]].st.eta0 << b;
 }
 
-constexpr int WALK_WARPS = 8;
-
-// K6: one warp = one tile = 32 walk pairs (S_k from s, T_k from t) of one query; both chains
-// are advanced in the same loop (two independent dependent-load chains per thread).
-__global__ void __launch_bounds__(WALK_WARPS * 32)
-k_walks(int64_t T, int32_t na, const int64_t *__restrict__ tile_incl, const int32_t *__restrict__ amc,
-        const QState *__restrict__ qs, const int64_t *__restrict__ off, const int32_t *__restrict__ cols,
-        const YEntry *__restrict__ pool, int b, uint32_t key0, uint32_t key1, int64_t qbase,
-        TilePart *__restrict__ parts)
+__global__ void k_lf_key(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs,
+                         uint32_t *__restrict__ key)
 {
-    const int lane = threadIdx.x & 31;
-    const int64_t tile = (int64_t)blockIdx.x * WALK_WARPS + (threadIdx.x >> 5);
-    if (tile >= T) return;
-    // query of this tile: smallest i with tile_incl[i] > tile
-    int32_t lo = 0, hi = na - 1;
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    key[i] = ~(uint32_t)qs[amc[i]].st.ell_f;
+}
+
+// Warps of the flattened walk space touched by each query: [P_{i-1}/32, (P_i - 1)/32].
+__global__ void k_nwarps(int32_t na, const int64_t *__restrict__ pincl, int64_t *__restrict__ nw)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    const int64_t p0 = i == 0 ? 0 : pincl[i - 1], p1 = pincl[i];
+    nw[i] = (p1 - 1) / 32 - p0 / 32 + 1;
+}
+
+constexpr int WALK_THREADS = 256;
+constexpr int WALK_SMEM_ENTRIES = 2048;   // 32 KB of staged y-table entries per CTA
+
+__device__ __forceinline__ int32_t find_query(const int64_t *__restrict__ pincl, int32_t lo, int32_t hi, int64_t p)
+{
+    // smallest i in [lo, hi] with pincl[i] > p
     while (lo < hi) {
         const int32_t mid = (lo + hi) >> 1;
-        if (tile_incl[mid] > tile) hi = mid;
+        if (pincl[mid] > p) hi = mid;
         else lo = mid + 1;
     }
-    const int32_t qi = amc[lo];
-    const int64_t first = lo == 0 ? 0 : tile_incl[lo - 1];
-    const QState &Q = qs[qi];
-    const int32_t lf = Q.st.ell_f;
-    const int64_t eta = Q.st.eta0 << b;
-    const uint64_t k = (uint64_t)(tile - first) * 32u + (uint64_t)lane;
-    const bool active = k < (uint64_t)eta;
-    const uint32_t q = (uint32_t)(qbase + qi);
-    const YEntry *tab = pool + Q.yoff;
-    const int lg = Q.ylog2;
-    int32_t vS = Q.s, vT = Q.t;
-    double aS = 0.0, aT = 0.0;
+    return lo;
+}
+
+// K6: thread = one walk pair (S_k from s, T_k from t) of the flattened walk space of batch b
+// (queries ordered by descending ell_f); both chains advance in the same loop.  The y-tables of
+// the CTA's queries are staged in shared memory when they fit (WALK_SMEM_ENTRIES), otherwise
+// probed in global memory.  Node records are 8-byte {offset, degree}: one sector per step.
+// Each (warp, query) run writes one partial {sum Z, sum Z^2, checksum} at a fixed slot.
+__global__ void __launch_bounds__(WALK_THREADS, 5)
+k_walks(int64_t W, int32_t na, const int64_t *__restrict__ pincl, const int64_t *__restrict__ pwincl,
+        const int32_t *__restrict__ amc, const QState *__restrict__ qs, const uint2 *__restrict__ rec,
+        const int32_t *__restrict__ cols, const YEntry *__restrict__ pool, int b, uint32_t key0, uint32_t key1,
+        int64_t qbase, TilePart *__restrict__ parts)
+{
+    __shared__ YEntry sm_tab[WALK_SMEM_ENTRIES];
+    __shared__ int32_t s_q0, s_q1;
+    __shared__ int32_t s_soff[WALK_THREADS];
+    __shared__ int32_t s_cap[WALK_THREADS];
+    __shared__ int64_t s_yoff[WALK_THREADS];
+    const int tid = threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * WALK_THREADS;
+    if (tid == 0) {
+        const int64_t last = min(base + WALK_THREADS, W) - 1;
+        s_q0 = find_query(pincl, 0, na - 1, base);
+        s_q1 = find_query(pincl, 0, na - 1, last);
+    }
+    __syncthreads();
+    const int32_t q0 = s_q0, nq = s_q1 - s_q0 + 1;
+    // staging plan: table j goes to shared memory if the tables 0..j fit
+    int32_t cap = 0;
+    if (tid < nq) {
+        const QState &Q = qs[amc[q0 + tid]];
+        cap = 1 << Q.ylog2;
+        s_yoff[tid] = Q.yoff;
+    }
+    {
+        typedef cub::BlockScan<int32_t, WALK_THREADS> Scan;
+        __shared__ typename Scan::TempStorage tmp;
+        int32_t excl;
+        Scan(tmp).ExclusiveSum(cap, excl);
+        if (tid < nq) {
+            s_cap[tid] = cap;
+            s_soff[tid] = (excl + cap <= WALK_SMEM_ENTRIES) ? excl : -1;
+        }
+    }
+    __syncthreads();
+    for (int32_t j = 0; j < nq; j++) {
+        const int32_t so = s_soff[j];
+        if (so < 0) break;
+        const int32_t cj = s_cap[j];
+        const YEntry *src = pool + s_yoff[j];
+        for (int32_t e = tid; e < cj; e += WALK_THREADS) sm_tab[so + e] = src[e];
+    }
+    __syncthreads();
+
+    const int64_t p = base + tid;
+    const bool active = p < W;
+    const int32_t i = active ? find_query(pincl, q0, q0 + nq - 1, p) : 0x7fffffff;
+    double z = 0.0;
+    uint64_t ck = 0;
     if (active) {
+        const int32_t j = i - q0;
+        const int32_t qi = amc[i];
+        const QState &Q = qs[qi];
+        const int32_t lf = Q.st.ell_f;
+        const int64_t first = i == 0 ? 0 : pincl[i - 1];
+        const uint64_t k = (uint64_t)(p - first);
+        const uint32_t q = (uint32_t)(qbase + qi);
+        const int lg = Q.ylog2;
+        const YEntry *tab = s_soff[j] >= 0 ? sm_tab + s_soff[j] : pool + s_yoff[j];
+        const uint32_t mask = (1u << lg) - 1u;
+        int32_t vS = Q.s, vT = Q.t;
+        double aS = 0.0, aT = 0.0;
         const uint32_t c3S = ((uint32_t)b << 29) | (0u << 28) | (uint32_t)(k >> 32);
         const uint32_t c3T = ((uint32_t)b << 29) | (1u << 28) | (uint32_t)(k >> 32);
         U4 rS = {0, 0, 0, 0}, rT = {0, 0, 0, 0};
-        for (int32_t j = 1; j <= lf; j++) {
+        for (int32_t jj = 1; jj <= lf; jj++) {
             uint64_t r64S, r64T;
-            if (j & 1) {
-                const uint32_t c = (uint32_t)((j - 1) >> 1);
-                rS = philox4x32_10(U4{c, (uint32_t)k, q, c3S}, key0, key1);
-                rT = philox4x32_10(U4{c, (uint32_t)k, q, c3T}, key0, key1);
+            if (jj & 1) {
+                const uint32_t cc = (uint32_t)((jj - 1) >> 1);
+                rS = philox4x32_10(U4{cc, (uint32_t)k, q, c3S}, key0, key1);
+                rT = philox4x32_10(U4{cc, (uint32_t)k, q, c3T}, key0, key1);
                 r64S = ((uint64_t)rS.y << 32) | rS.x;
                 r64T = ((uint64_t)rT.y << 32) | rT.x;
             } else {
                 r64S = ((uint64_t)rS.w << 32) | rS.z;
                 r64T = ((uint64_t)rT.w << 32) | rT.z;
             }
-            const int64_t oS = __ldg(off + vS), oT = __ldg(off + vT);
-            const uint64_t dS = (uint64_t)(__ldg(off + vS + 1) - oS);
-            const uint64_t dT = (uint64_t)(__ldg(off + vT + 1) - oT);
-            vS = __ldg(cols + oS + (int64_t)__umul64hi(r64S, dS));
-            vT = __ldg(cols + oT + (int64_t)__umul64hi(r64T, dT));
-            aS += ylookup(tab, lg, vS);
-            aT += ylookup(tab, lg, vT);
+            const uint2 RS = __ldg(rec + vS), RT = __ldg(rec + vT);
+            vS = __ldg(cols + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
+            vT = __ldg(cols + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
+            // y probes (shared or global table); y(v) = 0 off the support
+            uint32_t h = yslot(vS, lg);
+            while (true) {
+                const YEntry e = tab[h];
+                if (e.key == vS) { aS += e.val; break; }
+                if (e.key < 0) { aS += 0.0; break; }
+                h = (h + 1) & mask;
+            }
+            h = yslot(vT, lg);
+            while (true) {
+                const YEntry e = tab[h];
+                if (e.key == vT) { aT += e.val; break; }
+                if (e.key < 0) { aT += 0.0; break; }
+                h = (h + 1) & mask;
+            }
         }
+        z = aS - aT;
+        ck = walk_hash(q, (uint32_t)b, 0u, k, vS) + walk_hash(q, (uint32_t)b, 1u, k, vT);
     }
-    double z = active ? aS - aT : 0.0;
-    double s1 = z, s2 = z * z;
-    uint64_t ck = active ? walk_hash(q, (uint32_t)b, 0u, k, vS) + walk_hash(q, (uint32_t)b, 1u, k, vT) : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-        ck += __shfl_xor_sync(0xffffffffu, ck, o);
-    }
-    if (lane == 0) {
+    // per-(warp, query) partials
+    const double s1 = warp_seg_reduce(z, i, [](double x, double y) { return x + y; });
+    const double s2 = warp_seg_reduce(z * z, i, [](double x, double y) { return x + y; });
+    const uint64_t c1 = warp_seg_reduce(ck, i, [](uint64_t x, uint64_t y) { return x + y; });
+    if (active && warp_seg_head(i)) {
+        const int64_t first = i == 0 ? 0 : pincl[i - 1];
+        const int64_t w = p >> 5;
+        const int64_t slot = (i == 0 ? 0 : pwincl[i - 1]) + (w - (first >> 5));
         TilePart tp;
         tp.s1 = s1;
         tp.s2 = s2;
-        tp.ck = ck;
+        tp.ck = c1;
         tp.pad = 0;
-        parts[tile] = tp;
+        parts[slot] = tp;
     }
 }
 
 // K7: one warp per active query: sum its tiles, Alg. 1 L11-L14.
-__global__ void k_amc_reduce(int32_t na, const int32_t *__restrict__ amc, const int64_t *__restrict__ tile_incl,
+__global__ void k_amc_reduce(int32_t na, const int32_t *__restrict__ amc, const int64_t *__restrict__ tile_incl,  // partial slots
                              const TilePart *__restrict__ parts, int b, BatchParams P, QState *__restrict__ qs,
                              int32_t *__restrict__ cont, unsigned long long *__restrict__ steps_counter)
 {
@@ -648,7 +776,7 @@ void Workspace::release()
 {
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2, &head,
-                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen};
+                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey};
     for (DevBuf *b : all) b->release();
     if (host_pinned) cudaFreeHost(host_pinned);
     host_pinned = nullptr;
@@ -757,6 +885,67 @@ int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, c
                                                       ws.qs.as<QState>(), ws.ypool.as<YEntry>());
     LAUNCHED(c.g);
     pool_used += Y;
+    return ER_OK;
+}
+
+// Emit + group one SMM wave: pairs (key, x(v)) sorted by (segment, u), stable (ascending v
+// kept inside each (segment, u) run), then run heads / starts.  Segments are sorted in chunks
+// of spc = 2^(keybits - nbits) segments with one radix sort per chunk over only the
+// significant key bits; the result is in ws.keys2 / ws.vals2.
+template <class KeyT>
+int smm_group(Ctx &c, int64_t E, int64_t F, int32_t nseg, const int64_t *ent_off, const int32_t *segbeg, int nbits,
+              int64_t *dU)
+{
+    Workspace &ws = c.ws;
+    er_graph *g = c.g;
+    cudaStream_t st = c.st;
+    const int keybits = (int)(8 * sizeof(KeyT));
+    int gb = 1;
+    while ((1ll << gb) < nseg) gb++;
+    const int cbits = std::min(gb, keybits - nbits);
+    const int64_t spc = (int64_t)1 << cbits;
+    ENSURE(ws.keys, sizeof(KeyT) * E, false);
+    ENSURE(ws.keys2, sizeof(KeyT) * E, false);
+    ENSURE(ws.vals, sizeof(double) * E, false);
+    ENSURE(ws.vals2, sizeof(double) * E, false);
+    KeyT *k1 = ws.keys.as<KeyT>(), *k2 = ws.keys2.as<KeyT>();
+    double *v1 = ws.vals.as<double>(), *v2 = ws.vals2.as<double>();
+    k_emit<KeyT><<<blocks_for(E, 256), 256, 0, st>>>(E, F, ent_off, ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(),
+                                                     ws.fr_seg.as<int32_t>(), spc, nbits, g->d_off, g->d_cols, k1, v1);
+    LAUNCHED(g);
+    // chunk boundaries in emission order (segbeg on the host: nseg+1 int32)
+    const int32_t nchunks = (int32_t)((nseg + spc - 1) / spc);
+    std::vector<int32_t> hb(nchunks + 1);
+    for (int32_t ch = 0; ch <= nchunks; ch++) {
+        const int64_t gs = std::min<int64_t>((int64_t)ch * spc, nseg);
+        CK(cudaMemcpyAsync(&hb[ch], segbeg + gs, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    for (int32_t ch = 0; ch < nchunks; ch++) {
+        const int64_t lo = hb[ch], n = (int64_t)hb[ch + 1] - hb[ch];
+        if (n <= 0) continue;
+        const int64_t segs = std::min<int64_t>(spc, nseg - (int64_t)ch * spc);
+        int cb = 1;
+        while ((1ll << cb) < segs) cb++;
+        const int end_bit = nbits + cb;
+        int rc = cub_call(c, [&](void *tmp, size_t &bytes) {
+            return cub::DeviceRadixSort::SortPairs(tmp, bytes, k1 + lo, k2 + lo, v1 + lo, v2 + lo, (int)n, 0, end_bit, st);
+        });
+        if (rc) return rc;
+    }
+    ENSURE(ws.runidx, sizeof(int64_t) * E, false);
+    ENSURE(ws.runstart, sizeof(int64_t) * (E + 1), false);
+    k_heads<KeyT><<<blocks_for(E, 256), 256, 0, st>>>(E, k2, ws.head.as<int32_t>());
+    LAUNCHED(g);
+    k_mark_segbeg<<<blocks_for(nseg, 256), 256, 0, st>>>(nseg, segbeg, ws.head.as<int32_t>());
+    LAUNCHED(g);
+    int rc = cub_call(c, [&](void *tmp, size_t &bytes) {
+        return cub::DeviceScan::InclusiveSum(tmp, bytes, ws.head.as<int32_t>(), ws.runidx.as<int64_t>(), E, st);
+    });
+    if (rc) return rc;
+    k_runstart<<<blocks_for(E, 256), 256, 0, st>>>(E, ws.head.as<int32_t>(), ws.runidx.as<int64_t>(),
+                                                   ws.runstart.as<int64_t>(), dU);
+    LAUNCHED(g);
     return ER_OK;
 }
 
@@ -871,13 +1060,6 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         }
         while (na > 0) {
             const int32_t nseg = (int32_t)(2 * na);
-            int gb = 1;
-            while ((1ll << gb) < nseg) gb++;
-            const int end_bit = P.nbits + gb;
-            if (end_bit > 64) {
-                set_error(ER_EINVAL, "sort key exceeds 64 bits");
-                return ER_EINVAL;
-            }
             // emission offsets
             ENSURE(ws.ent_off, sizeof(int64_t) * (2 * F + 2), false);
             int64_t *ent_deg = ws.ent_off.as<int64_t>() + (F + 1);
@@ -894,53 +1076,38 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                 set_error(ER_ENOMEM, "SMM wave emits more than 2^31 pairs");
                 return ER_ENOMEM;
             }
-            ENSURE(ws.keys, sizeof(uint64_t) * E, false);
-            ENSURE(ws.keys2, sizeof(uint64_t) * E, false);
-            ENSURE(ws.vals, sizeof(double) * E, false);
-            ENSURE(ws.vals2, sizeof(double) * E, false);
-            k_emit<<<blocks_for(E, 256), 256, 0, st>>>(E, F, ent_off, ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(),
-                                                       ws.fr_seg.as<int32_t>(), g->d_off, g->d_cols, P.nbits,
-                                                       ws.keys.as<uint64_t>(), ws.vals.as<double>());
+            ENSURE(ws.segbeg, sizeof(int32_t) * (nseg + 1), false);
+            int32_t *segbeg = ws.segbeg.as<int32_t>();
+            k_segbeg<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, ws.fr_off.as<int64_t>(), ent_off, segbeg);
             LAUNCHED(g);
-            cub::DoubleBuffer<uint64_t> dk(ws.keys.as<uint64_t>(), ws.keys2.as<uint64_t>());
-            cub::DoubleBuffer<double> dv(ws.vals.as<double>(), ws.vals2.as<double>());
-            rc = cub_call(c, [&](void *tmp, size_t &bytes) {
-                return cub::DeviceRadixSort::SortPairs(tmp, bytes, dk, dv, (int)E, 0, end_bit, st);
-            });
-            if (rc) return rc;
-            const uint64_t *skeys = dk.Current();
-            const double *svals = dv.Current();
-            // run-length reduction
-            ENSURE(ws.head, sizeof(int32_t) * E, false);
-            ENSURE(ws.runidx, sizeof(int64_t) * E, false);
-            ENSURE(ws.runstart, sizeof(int64_t) * (E + 1), false);
             ENSURE(ws.scalars, sizeof(int64_t) * 8, false);
             int64_t *dU = ws.scalars.as<int64_t>();
-            k_heads<<<blocks_for(E, 256), 256, 0, st>>>(E, skeys, ws.head.as<int32_t>());
-            LAUNCHED(g);
-            // inclusive scan of heads into int64 runidx
-            rc = cub_call(c, [&](void *tmp, size_t &bytes) {
-                return cub::DeviceScan::InclusiveSum(tmp, bytes, ws.head.as<int32_t>(), ws.runidx.as<int64_t>(), E, st);
-            });
+            ENSURE(ws.head, sizeof(int32_t) * E, false);
+            if (P.nbits <= 24) rc = smm_group<uint32_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU);
+            else rc = smm_group<uint64_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU);
             if (rc) return rc;
-            k_runstart<<<blocks_for(E, 256), 256, 0, st>>>(E, ws.head.as<int32_t>(), ws.runidx.as<int64_t>(),
-                                                           ws.runstart.as<int64_t>(), dU);
-            LAUNCHED(g);
             ENSURE(ws.nf_id, sizeof(int32_t) * E, false);
             ENSURE(ws.nf_val, sizeof(double) * E, false);
             ENSURE(ws.nf_seg, sizeof(int32_t) * E, false);
             ENSURE(ws.nf_off, sizeof(int64_t) * (nseg + 1), false);
-            k_run_reduce<<<blocks_for(E, 256), 256, 0, st>>>(E, dU, ws.runstart.as<int64_t>(), skeys, svals, g->d_off,
-                                                             P.nbits, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
-                                                             ws.nf_seg.as<int32_t>());
+            ENSURE(ws.segstat, sizeof(SegStat) * nseg, false);
+            CK(cudaMemsetAsync(ws.segstat.p, 0, sizeof(SegStat) * nseg, st));
+            if (P.nbits <= 24)
+                k_run_reduce<uint32_t><<<blocks_for(E, 256), 256, 0, st>>>(
+                    E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint32_t>(), P.nbits, ws.vals2.as<double>(), segbeg,
+                    nseg, g->d_off, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
+                    ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>());
+            else
+                k_run_reduce<uint64_t><<<blocks_for(E, 256), 256, 0, st>>>(
+                    E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint64_t>(), P.nbits, ws.vals2.as<double>(), segbeg,
+                    nseg, g->d_off, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
+                    ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>());
+            LAUNCHED(g);
+            k_seg_max2<<<blocks_for(E, 256), 256, 0, st>>>(E, dU, ws.nf_seg.as<int32_t>(), ws.nf_val.as<double>(),
+                                                           ws.segstat.as<SegStat>());
             LAUNCHED(g);
             k_seg_off<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, dU, ws.nf_seg.as<int32_t>(),
                                                                  ws.nf_off.as<int64_t>());
-            LAUNCHED(g);
-            ENSURE(ws.segstat, sizeof(SegStat) * nseg, false);
-            k_seg_stats<<<blocks_for((int64_t)nseg * 32, 256), 256, 0, st>>>(
-                nseg, ws.nf_off.as<int64_t>(), ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(), g->d_off,
-                ws.act.as<int32_t>(), qs, ws.segstat.as<SegStat>());
             LAUNCHED(g);
             int32_t *cont = ws.cont.as<int32_t>();
             k_decide<<<blocks_for(na, 128), 128, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), ws.segstat.as<SegStat>(),
@@ -999,26 +1166,45 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         rc = select_list(c, ids, ws.cont.as<int32_t>(), K, ws.act.as<int32_t>(), ws.idx.as<int32_t>(), &na);
         if (rc) return rc;
         const uint32_t key0 = (uint32_t)P.seed, key1 = (uint32_t)(P.seed >> 32);
-        for (int b = 0; b < P.tau && na > 0; b++) {
-            ENSURE(ws.tiles, sizeof(int64_t) * 2 * (na + 1), false);
-            int64_t *ntiles = ws.tiles.as<int64_t>();
-            int64_t *tincl = ntiles + (na + 1);
-            k_tiles<<<blocks_for(na, 256), 256, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), qs, b, ntiles);
+        if (na > 1) {
+            // order the AMC queries by descending ell_f (stable): warps then see one trip count
+            ENSURE(ws.lfkey, sizeof(uint32_t) * 2 * na, false);
+            uint32_t *kk = ws.lfkey.as<uint32_t>();
+            k_lf_key<<<blocks_for(na, 256), 256, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), qs, kk);
             LAUNCHED(g);
-            rc = scan_incl(c, ntiles, tincl, na);
+            rc = cub_call(c, [&](void *tmp, size_t &bytes) {
+                return cub::DeviceRadixSort::SortPairs(tmp, bytes, kk, kk + na, ws.act.as<int32_t>(),
+                                                       ws.act2.as<int32_t>(), (int)na, 0, 32, st);
+            });
             if (rc) return rc;
-            rc = read_scalars(c, {tincl + (na - 1)});
+            std::swap(ws.act, ws.act2);
+        }
+        for (int b = 0; b < P.tau && na > 0; b++) {
+            ENSURE(ws.tiles, sizeof(int64_t) * 4 * (na + 1), false);
+            int64_t *npairs = ws.tiles.as<int64_t>();
+            int64_t *pincl = npairs + (na + 1);
+            int64_t *nw = pincl + (na + 1);
+            int64_t *pwincl = nw + (na + 1);
+            k_npairs<<<blocks_for(na, 256), 256, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), qs, b, npairs);
+            LAUNCHED(g);
+            rc = scan_incl(c, npairs, pincl, na);
             if (rc) return rc;
-            const int64_t T = c.hp[0];
-            ENSURE(ws.parts, sizeof(TilePart) * T, false);
+            k_nwarps<<<blocks_for(na, 256), 256, 0, st>>>((int32_t)na, pincl, nw);
+            LAUNCHED(g);
+            rc = scan_incl(c, nw, pwincl, na);
+            if (rc) return rc;
+            rc = read_scalars(c, {pincl + (na - 1), pwincl + (na - 1)});
+            if (rc) return rc;
+            const int64_t W = c.hp[0], NP = c.hp[1];
+            ENSURE(ws.parts, sizeof(TilePart) * NP, false);
             if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk], st));
-            k_walks<<<blocks_for(T, WALK_WARPS), WALK_WARPS * 32, 0, st>>>(
-                T, (int32_t)na, tincl, ws.act.as<int32_t>(), qs, g->d_off, g->d_cols, ws.ypool.as<YEntry>(), b, key0,
-                key1, P.qbase, ws.parts.as<TilePart>());
+            k_walks<<<blocks_for(W, WALK_THREADS), WALK_THREADS, 0, st>>>(
+                W, (int32_t)na, pincl, pwincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_cols, ws.ypool.as<YEntry>(), b,
+                key0, key1, P.qbase, ws.parts.as<TilePart>());
             LAUNCHED(g);
             if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk + 1], st));
             k_amc_reduce<<<blocks_for(na * 32, 256), 256, 0, st>>>(
-                (int32_t)na, ws.act.as<int32_t>(), tincl, ws.parts.as<TilePart>(), b, P, qs, ws.cont.as<int32_t>(),
+                (int32_t)na, ws.act.as<int32_t>(), pwincl, ws.parts.as<TilePart>(), b, P, qs, ws.cont.as<int32_t>(),
                 prof ? reinterpret_cast<unsigned long long *>(g->d_steps) : nullptr);
             nwalk++;
             LAUNCHED(g);

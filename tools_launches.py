@@ -1,0 +1,15 @@
+import csv, collections, sys
+rows=list(csv.reader(open(sys.argv[1])))
+hi=[i for i,r in enumerate(rows) if 'Kernel Name' in r][0]
+h=rows[hi]; R=rows[hi+1:]
+ki=h.index('Kernel Name'); mi=h.index('Metric Value')
+seq=[(r[ki],float(r[mi].replace(',',''))) for r in R if len(r)>mi]
+idxs=[i for i,(n,v) in enumerate(seq) if 'k_setup' in n]
+b0=idxs[-2]; b1=idxs[-1]
+agg=collections.defaultdict(float); c=collections.Counter()
+for n,v in seq[b0:b1]:
+    n=n.split('(')[0][:90]; agg[n]+=v; c[n]+=1
+T=sum(agg.values())
+for n,v in sorted(agg.items(), key=lambda x:-x[1])[:int(sys.argv[2]) if len(sys.argv)>2 else 40]:
+    print(f"{v/1e3:9.1f} us {100*v/T:5.1f}% x{c[n]:3d} {n}")
+print('total us', T/1e3, 'launches', b1-b0)
