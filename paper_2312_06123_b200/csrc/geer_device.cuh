@@ -49,10 +49,13 @@ __device__ __forceinline__ uint64_t walk_hash(uint32_t q, uint32_t b, uint32_t s
     return fmix64(h ^ (uint64_t)(uint32_t)end);
 }
 
-// y-table slot of node v in a table of 2^lg entries (multiplicative hash, top bits).
-__device__ __forceinline__ uint32_t yslot(int32_t v, int lg)
+// y-tables: buckets of YB = 8 int32 keys (one 32-byte sector); bucket of node v in a table of
+// 2^lgb buckets (multiplicative hash, top bits).
+constexpr int YB = 8;
+constexpr int YB_LOG = 3;
+__device__ __forceinline__ uint32_t ybucket(int32_t v, int lgb)
 {
-    return ((uint32_t)v * 0x9E3779B1u) >> (32 - lg);
+    return lgb == 0 ? 0u : ((uint32_t)v * 0x9E3779B1u) >> (32 - lgb);
 }
 
 // Eq. 10.

@@ -22,17 +22,11 @@ struct QState {
     int32_t s, t;          // query endpoints
     int32_t ds, dt;        // degrees d(s), d(t)
     int32_t phase;         // PH_*
-    int32_t ylog2;         // log2 of the y-table capacity (0 if no table)
-    int64_t yoff;          // offset (in entries) of this query's y-table in the pool
+    int32_t ylog2;         // log2 of the y-table capacity in slots (>= 3)
+    int64_t yoff;          // offset (in slots) of this query's y-table in the pools
     double z;              // last batch mean Z (= r_f)
 };
 
-// y-table entry: 16 B, so a probe and its value share one 32 B sector.
-struct YEntry {
-    int32_t key;           // node id, -1 = empty
-    int32_t pad;
-    double val;            // y(v) = s*(v)/d(s) - t*(v)/d(t)
-};
 
 // Per-segment statistics of an SMM iterate (segment = one side of one query).
 struct SegStat {
@@ -82,7 +76,7 @@ struct Workspace {
     DevBuf keys, vals, keys2, vals2;                // emitted (key, value) pairs + sort buffers
     DevBuf head, runidx, runstart;                  // run-length reduction
     DevBuf segstat;                                 // SegStat per segment
-    DevBuf ycap, yoff, ypool;                       // y-tables
+    DevBuf ycap, yoff, ypool, yvals;                // y-tables: int32 keys (8 per bucket) | fp64 values
     DevBuf tiles, parts;                            // AMC tiles
     DevBuf cub_tmp;                                 // CUB temp storage
     DevBuf scalars;                                 // small device scalars

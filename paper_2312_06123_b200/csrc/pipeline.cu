@@ -337,7 +337,8 @@ __global__ void k_decide(int32_t na, const int32_t *__restrict__ act, const SegS
     }
 }
 
-// y-table capacity for queries that leave the SMM head for AMC in this wave.
+// y-table capacity (slots) for queries that leave the SMM head for AMC in this wave:
+// next power of two >= 2 |supp(s*)| + 2 |supp(t*)| (load <= 1/2), at least one 8-slot bucket.
 __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState *__restrict__ qs,
                        const int32_t *__restrict__ cont, const int64_t *__restrict__ segoff,
                        int64_t *__restrict__ ycap)
@@ -347,15 +348,14 @@ __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState
     int64_t cap = 0;
     if ((cont == nullptr || !cont[i]) && qs[act[i]].phase == PH_AMC) {
         const int64_t len = segoff[2 * i + 2] - segoff[2 * i];
-        cap = 16;
+        cap = YB;
         while (cap < 2 * len) cap <<= 1;
     }
     ycap[i] = cap;
 }
 
 __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__ ycap,
-                          const int64_t *__restrict__ yincl, int64_t base, QState *__restrict__ qs,
-                          YEntry *__restrict__ pool)
+                          const int64_t *__restrict__ yincl, int64_t base, QState *__restrict__ qs)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na || ycap[i] == 0) return;
@@ -365,25 +365,22 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int
     int lg = 0;
     while ((1ll << lg) < cap) lg++;
     Q.ylog2 = lg;
-    (void)pool;
 }
 
-__global__ void k_yfill(int64_t Y, YEntry *__restrict__ tab)
+__global__ void k_yfill(int64_t Y, int32_t *__restrict__ keys)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= Y) return;
-    YEntry e;
-    e.key = -1;
-    e.pad = 0;
-    e.val = 0.0;
-    tab[j] = e;
+    if (j < Y) keys[j] = -1;
 }
 
 // K5: y(v) = s*(v)/d(s) - t*(v)/d(t) for v in supp(s*) U supp(t*) (Alg. 1 L7 with s = s*, t = t*).
+// Bucketed open addressing: 8 int32 keys per 32-byte bucket, buckets probed linearly, slots in
+// order inside a bucket; values in a parallel fp64 array.
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                           const int32_t *__restrict__ id, const double *__restrict__ val,
                           const int64_t *__restrict__ segoff, const int32_t *__restrict__ act,
-                          const int64_t *__restrict__ ycap, const QState *__restrict__ qs, YEntry *__restrict__ pool)
+                          const int64_t *__restrict__ ycap, const QState *__restrict__ qs, int32_t *__restrict__ ykeys,
+                          double *__restrict__ yvals)
 {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
@@ -411,17 +408,21 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
         b = x;
     }
     const double y = a / (double)Q.ds - b / (double)Q.dt;
-    YEntry *tab = pool + Q.yoff;
-    const int lg = Q.ylog2;
-    const uint32_t mask = (1u << lg) - 1u;
-    uint32_t h = yslot(v, lg);
+    int32_t *keys = ykeys + Q.yoff;
+    double *vals = yvals + Q.yoff;
+    const int lgb = Q.ylog2 - YB_LOG;
+    const uint32_t bmask = (1u << lgb) - 1u;
+    uint32_t bk = ybucket(v, lgb);
     while (true) {
-        const int32_t prev = atomicCAS(&tab[h].key, -1, v);
-        if (prev == -1) {
-            tab[h].val = y;
-            return;
+        for (int j = 0; j < YB; j++) {
+            const uint32_t slot = bk * YB + j;
+            if (keys[slot] != -1) continue;
+            if (atomicCAS(&keys[slot], -1, v) == -1) {
+                vals[slot] = y;
+                return;
+            }
         }
-        h = (h + 1) & mask;
+        bk = (bk + 1) & bmask;
     }
 }
 
@@ -470,27 +471,14 @@ __global__ void k_compact_lists(int32_t na, const int32_t *__restrict__ cont, co
 
 // ---------------------------------------------------------------------------- AMC
 
-__device__ __forceinline__ double ylookup(const YEntry *__restrict__ tab, int lg, int32_t v)
-{
-    const uint32_t mask = (1u << lg) - 1u;
-    uint32_t h = yslot(v, lg);
-    while (true) {
-        const longlong2 e = __ldg(reinterpret_cast<const longlong2 *>(tab + h));
-        const int32_t key = (int32_t)(uint32_t)(unsigned long long)e.x;
-        if (key == v) return __longlong_as_double(e.y);
-        if (key < 0) return 0.0;
-        h = (h + 1) & mask;
-    }
-}
-
 // Walk pairs of batch b per AMC query, and the AMC sort key (descending ell_f) used to order
 // the flattened walk space so warps mostly see one trip count.
-__global__ void k_npairs(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs, int b,
-                         int64_t *__restrict__ npairs)
+__global__ void k_nchunks(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs, int b,
+                          int64_t *__restrict__ nch)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
-    npairs[i] = qs[amc[i]].st.eta0 << b;
+    nch[i] = ((qs[amc[i]].st.eta0 << b) + 31) / 32;
 }
 
 __global__ void k_lf_key(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs,
@@ -501,150 +489,214 @@ __global__ void k_lf_key(int32_t na, const int32_t *__restrict__ amc, const QSta
     key[i] = ~(uint32_t)qs[amc[i]].st.ell_f;
 }
 
-// Warps of the flattened walk space touched by each query: [P_{i-1}/32, (P_i - 1)/32].
-__global__ void k_nwarps(int32_t na, const int64_t *__restrict__ pincl, int64_t *__restrict__ nw)
-{
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= na) return;
-    const int64_t p0 = i == 0 ? 0 : pincl[i - 1], p1 = pincl[i];
-    nw[i] = (p1 - 1) / 32 - p0 / 32 + 1;
-}
+constexpr int WALK_WARPS = 8;
+constexpr int WALK_THREADS = 32 * WALK_WARPS;
+constexpr int WALK_SMEM_SLOTS = 8192;      // 32 KB of staged y-table keys per CTA
 
-constexpr int WALK_THREADS = 256;
-constexpr int WALK_SMEM_ENTRIES = 2048;   // 32 KB of staged y-table entries per CTA
-
-__device__ __forceinline__ int32_t find_query(const int64_t *__restrict__ pincl, int32_t lo, int32_t hi, int64_t p)
+__device__ __forceinline__ int32_t find_chunk_query(const int64_t *__restrict__ cincl, int32_t n, int64_t c)
 {
-    // smallest i in [lo, hi] with pincl[i] > p
+    int32_t lo = 0, hi = n - 1;  // smallest i with cincl[i] > c
     while (lo < hi) {
         const int32_t mid = (lo + hi) >> 1;
-        if (pincl[mid] > p) hi = mid;
+        if (cincl[mid] > c) hi = mid;
         else lo = mid + 1;
     }
     return lo;
 }
 
-// K6: thread = one walk pair (S_k from s, T_k from t) of the flattened walk space of batch b
-// (queries ordered by descending ell_f); both chains advance in the same loop.  The y-tables of
-// the CTA's queries are staged in shared memory when they fit (WALK_SMEM_ENTRIES), otherwise
-// probed in global memory.  Node records are 8-byte {offset, degree}: one sector per step.
-// Each (warp, query) run writes one partial {sum Z, sum Z^2, checksum} at a fixed slot.
-__global__ void __launch_bounds__(WALK_THREADS, 5)
-k_walks(int64_t W, int32_t na, const int64_t *__restrict__ pincl, const int64_t *__restrict__ pwincl,
-        const int32_t *__restrict__ amc, const QState *__restrict__ qs, const uint2 *__restrict__ rec,
-        const int32_t *__restrict__ cols, const YEntry *__restrict__ pool, int b, uint32_t key0, uint32_t key1,
+// 8 keys of a bucket: index of v, or -1; *empty = the bucket has a free slot.
+__device__ __forceinline__ int bucket_match(const int4 a, const int4 b, int32_t v, bool *empty)
+{
+    int m = -1;
+    m = (b.w == v) ? 7 : m;
+    m = (b.z == v) ? 6 : m;
+    m = (b.y == v) ? 5 : m;
+    m = (b.x == v) ? 4 : m;
+    m = (a.w == v) ? 3 : m;
+    m = (a.z == v) ? 2 : m;
+    m = (a.y == v) ? 1 : m;
+    m = (a.x == v) ? 0 : m;
+    *empty = (a.x < 0) | (a.y < 0) | (a.z < 0) | (a.w < 0) | (b.x < 0) | (b.y < 0) | (b.z < 0) | (b.w < 0);
+    return m;
+}
+
+template <bool SMEM>
+__device__ __forceinline__ void load_bucket(const int32_t *keys, uint32_t bk, int4 &a, int4 &b)
+{
+    const int4 *p = reinterpret_cast<const int4 *>(keys + (size_t)bk * YB);
+    if (SMEM) {
+        a = p[0];
+        b = p[1];
+    } else {
+        a = __ldg(p);
+        b = __ldg(p + 1);
+    }
+}
+
+// Slow path: v not in its first bucket and the bucket is full -> probe the following buckets.
+template <bool SMEM>
+__device__ __noinline__ double probe_rest(const int32_t *keys, const double *__restrict__ vals, uint32_t bk,
+                                          uint32_t bmask, int32_t v)
+{
+    while (true) {
+        bk = (bk + 1) & bmask;
+        int4 a, b;
+        load_bucket<SMEM>(keys, bk, a, b);
+        bool empty;
+        const int m = bucket_match(a, b, v, &empty);
+        if (m >= 0) return __ldg(vals + (size_t)bk * YB + m);
+        if (empty) return 0.0;
+    }
+}
+
+// One walk pair (S_k from s, T_k from t), both chains advanced in one loop.  Software
+// pipelined: step j issues the node-record load for step j+1 before it resolves the y probe of
+// step j-1's node, and a hit's value load is consumed one step later, so only the
+// record -> column chain is serial.  y values are added in step order (R9, R13).
+template <bool SMEM>
+__device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const int32_t *__restrict__ cols,
+                                          const int32_t *keys, const double *__restrict__ vals, int lgb,
+                                          int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b, uint64_t k,
+                                          uint32_t key0, uint32_t key1, double &accS, double &accT,
+                                          int32_t &endS, int32_t &endT)
+{
+    const uint32_t bmask = (1u << lgb) - 1u;
+    const uint32_t c3S = (b << 29) | (0u << 28) | (uint32_t)(k >> 32);
+    const uint32_t c3T = (b << 29) | (1u << 28) | (uint32_t)(k >> 32);
+    int32_t vS = s, vT = t;
+    double aS = 0.0, aT = 0.0;
+    double pvS = 0.0, pvT = 0.0;        // pending hit values (added one step later)
+    int4 kS0, kS1, kT0, kT1;            // bucket keys of the current nodes
+    U4 rS = {0, 0, 0, 0}, rT = {0, 0, 0, 0};
+    for (int32_t j = 1; j <= lf; j++) {
+        const uint2 RS = __ldg(rec + vS), RT = __ldg(rec + vT);
+        if (j > 1) {
+            aS += pvS;
+            aT += pvT;
+            bool eS, eT;
+            const uint32_t bS = ybucket(vS, lgb), bT = ybucket(vT, lgb);
+            const int mS = bucket_match(kS0, kS1, vS, &eS);
+            const int mT = bucket_match(kT0, kT1, vT, &eT);
+            pvS = 0.0;
+            pvT = 0.0;
+            if (mS >= 0) pvS = __ldg(vals + (size_t)bS * YB + mS);
+            else if (!eS) aS += probe_rest<SMEM>(keys, vals, bS, bmask, vS);
+            if (mT >= 0) pvT = __ldg(vals + (size_t)bT * YB + mT);
+            else if (!eT) aT += probe_rest<SMEM>(keys, vals, bT, bmask, vT);
+        }
+        uint64_t r64S, r64T;
+        if (j & 1) {
+            const uint32_t cc = (uint32_t)((j - 1) >> 1);
+            rS = philox4x32_10(U4{cc, (uint32_t)k, q, c3S}, key0, key1);
+            rT = philox4x32_10(U4{cc, (uint32_t)k, q, c3T}, key0, key1);
+            r64S = ((uint64_t)rS.y << 32) | rS.x;
+            r64T = ((uint64_t)rT.y << 32) | rT.x;
+        } else {
+            r64S = ((uint64_t)rS.w << 32) | rS.z;
+            r64T = ((uint64_t)rT.w << 32) | rT.z;
+        }
+        vS = __ldg(cols + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
+        vT = __ldg(cols + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
+        load_bucket<SMEM>(keys, ybucket(vS, lgb), kS0, kS1);
+        load_bucket<SMEM>(keys, ybucket(vT, lgb), kT0, kT1);
+    }
+    // resolve the last step
+    aS += pvS;
+    aT += pvT;
+    if (lf > 0) {
+        bool eS, eT;
+        const uint32_t bS = ybucket(vS, lgb), bT = ybucket(vT, lgb);
+        const int mS = bucket_match(kS0, kS1, vS, &eS);
+        const int mT = bucket_match(kT0, kT1, vT, &eT);
+        if (mS >= 0) aS += __ldg(vals + (size_t)bS * YB + mS);
+        else if (!eS) aS += probe_rest<SMEM>(keys, vals, bS, bmask, vS);
+        if (mT >= 0) aT += __ldg(vals + (size_t)bT * YB + mT);
+        else if (!eT) aT += probe_rest<SMEM>(keys, vals, bT, bmask, vT);
+    }
+    accS = aS;
+    accT = aT;
+    endS = vS;
+    endT = vT;
+}
+
+// K6: warp = one chunk of 32 walk pairs of one query (chunks of all AMC queries are laid out
+// query after query, queries ordered by descending ell_f).  The CTA stages the y-table keys of
+// its (<= 8) queries in shared memory when they fit; otherwise the warp probes global memory.
+// Each warp writes the canonical partial {sum Z, sum Z^2, checksum} of its chunk.
+__global__ void __launch_bounds__(WALK_THREADS, 4)
+k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
+        const QState *__restrict__ qs, const uint2 *__restrict__ rec, const int32_t *__restrict__ cols,
+        const int32_t *__restrict__ ykeys, const double *__restrict__ yvals, int b, uint32_t key0, uint32_t key1,
         int64_t qbase, TilePart *__restrict__ parts)
 {
-    __shared__ YEntry sm_tab[WALK_SMEM_ENTRIES];
-    __shared__ int32_t s_q0, s_q1;
-    __shared__ int32_t s_soff[WALK_THREADS];
-    __shared__ int32_t s_cap[WALK_THREADS];
-    __shared__ int64_t s_yoff[WALK_THREADS];
-    const int tid = threadIdx.x;
-    const int64_t base = (int64_t)blockIdx.x * WALK_THREADS;
-    if (tid == 0) {
-        const int64_t last = min(base + WALK_THREADS, W) - 1;
-        s_q0 = find_query(pincl, 0, na - 1, base);
-        s_q1 = find_query(pincl, 0, na - 1, last);
-    }
+    __shared__ __align__(16) int32_t sm_keys[WALK_SMEM_SLOTS];
+    __shared__ int32_t s_qi[WALK_WARPS];
+    __shared__ int32_t s_soff[WALK_WARPS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t chunk = (int64_t)blockIdx.x * WALK_WARPS + warp;
+    const bool wvalid = chunk < nchunks;
+    const int32_t i = wvalid ? find_chunk_query(cincl, na, chunk) : -1;
+    if (lane == 0) s_qi[warp] = i;
     __syncthreads();
-    const int32_t q0 = s_q0, nq = s_q1 - s_q0 + 1;
-    // staging plan: table j goes to shared memory if the tables 0..j fit
-    int32_t cap = 0;
-    if (tid < nq) {
-        const QState &Q = qs[amc[q0 + tid]];
-        cap = 1 << Q.ylog2;
-        s_yoff[tid] = Q.yoff;
-    }
-    {
-        typedef cub::BlockScan<int32_t, WALK_THREADS> Scan;
-        __shared__ typename Scan::TempStorage tmp;
-        int32_t excl;
-        Scan(tmp).ExclusiveSum(cap, excl);
-        if (tid < nq) {
-            s_cap[tid] = cap;
-            s_soff[tid] = (excl + cap <= WALK_SMEM_ENTRIES) ? excl : -1;
+    if (threadIdx.x == 0) {
+        // prefix-fit staging plan over the distinct queries of this CTA (consecutive warps)
+        int32_t used = 0;
+        for (int w = 0; w < WALK_WARPS; w++) {
+            const int32_t qi = s_qi[w];
+            if (qi < 0) { s_soff[w] = -1; continue; }
+            if (w > 0 && s_qi[w - 1] == qi) { s_soff[w] = s_soff[w - 1]; continue; }
+            const int32_t cap = 1 << qs[amc[qi]].ylog2;
+            if (used + cap <= WALK_SMEM_SLOTS) { s_soff[w] = used; used += cap; }
+            else s_soff[w] = -1;
         }
     }
     __syncthreads();
-    for (int32_t j = 0; j < nq; j++) {
-        const int32_t so = s_soff[j];
-        if (so < 0) break;
-        const int32_t cj = s_cap[j];
-        const YEntry *src = pool + s_yoff[j];
-        for (int32_t e = tid; e < cj; e += WALK_THREADS) sm_tab[so + e] = src[e];
+    for (int w = 0; w < WALK_WARPS; w++) {
+        if (s_soff[w] < 0 || (w > 0 && s_qi[w - 1] == s_qi[w])) continue;
+        const QState &Q = qs[amc[s_qi[w]]];
+        const int32_t cap = 1 << Q.ylog2;
+        const int4 *src = reinterpret_cast<const int4 *>(ykeys + Q.yoff);
+        int4 *dst = reinterpret_cast<int4 *>(sm_keys + s_soff[w]);
+        for (int32_t e = threadIdx.x; e < cap / 4; e += WALK_THREADS) dst[e] = __ldg(src + e);
     }
     __syncthreads();
+    if (!wvalid) return;
 
-    const int64_t p = base + tid;
-    const bool active = p < W;
-    const int32_t i = active ? find_query(pincl, q0, q0 + nq - 1, p) : 0x7fffffff;
-    double z = 0.0;
-    uint64_t ck = 0;
+    const int32_t qi = amc[i];
+    const QState &Q = qs[qi];
+    const int64_t c0 = i == 0 ? 0 : cincl[i - 1];
+    const uint64_t k = (uint64_t)(chunk - c0) * 32u + (uint64_t)lane;
+    const int64_t eta = Q.st.eta0 << b;
+    const bool active = k < (uint64_t)eta;
+    const uint32_t q = (uint32_t)(qbase + qi);
+    const int lgb = Q.ylog2 - YB_LOG;
+    const double *vals = yvals + Q.yoff;
+    double aS = 0.0, aT = 0.0;
+    int32_t eS = 0, eT = 0;
     if (active) {
-        const int32_t j = i - q0;
-        const int32_t qi = amc[i];
-        const QState &Q = qs[qi];
-        const int32_t lf = Q.st.ell_f;
-        const int64_t first = i == 0 ? 0 : pincl[i - 1];
-        const uint64_t k = (uint64_t)(p - first);
-        const uint32_t q = (uint32_t)(qbase + qi);
-        const int lg = Q.ylog2;
-        const YEntry *tab = s_soff[j] >= 0 ? sm_tab + s_soff[j] : pool + s_yoff[j];
-        const uint32_t mask = (1u << lg) - 1u;
-        int32_t vS = Q.s, vT = Q.t;
-        double aS = 0.0, aT = 0.0;
-        const uint32_t c3S = ((uint32_t)b << 29) | (0u << 28) | (uint32_t)(k >> 32);
-        const uint32_t c3T = ((uint32_t)b << 29) | (1u << 28) | (uint32_t)(k >> 32);
-        U4 rS = {0, 0, 0, 0}, rT = {0, 0, 0, 0};
-        for (int32_t jj = 1; jj <= lf; jj++) {
-            uint64_t r64S, r64T;
-            if (jj & 1) {
-                const uint32_t cc = (uint32_t)((jj - 1) >> 1);
-                rS = philox4x32_10(U4{cc, (uint32_t)k, q, c3S}, key0, key1);
-                rT = philox4x32_10(U4{cc, (uint32_t)k, q, c3T}, key0, key1);
-                r64S = ((uint64_t)rS.y << 32) | rS.x;
-                r64T = ((uint64_t)rT.y << 32) | rT.x;
-            } else {
-                r64S = ((uint64_t)rS.w << 32) | rS.z;
-                r64T = ((uint64_t)rT.w << 32) | rT.z;
-            }
-            const uint2 RS = __ldg(rec + vS), RT = __ldg(rec + vT);
-            vS = __ldg(cols + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
-            vT = __ldg(cols + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
-            // y probes (shared or global table); y(v) = 0 off the support
-            uint32_t h = yslot(vS, lg);
-            while (true) {
-                const YEntry e = tab[h];
-                if (e.key == vS) { aS += e.val; break; }
-                if (e.key < 0) { aS += 0.0; break; }
-                h = (h + 1) & mask;
-            }
-            h = yslot(vT, lg);
-            while (true) {
-                const YEntry e = tab[h];
-                if (e.key == vT) { aT += e.val; break; }
-                if (e.key < 0) { aT += 0.0; break; }
-                h = (h + 1) & mask;
-            }
-        }
-        z = aS - aT;
-        ck = walk_hash(q, (uint32_t)b, 0u, k, vS) + walk_hash(q, (uint32_t)b, 1u, k, vT);
+        if (s_soff[warp] >= 0)
+            walk_pair<true>(rec, cols, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k,
+                            key0, key1, aS, aT, eS, eT);
+        else
+            walk_pair<false>(rec, cols, ykeys + Q.yoff, vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k, key0,
+                             key1, aS, aT, eS, eT);
     }
-    // per-(warp, query) partials
-    const double s1 = warp_seg_reduce(z, i, [](double x, double y) { return x + y; });
-    const double s2 = warp_seg_reduce(z * z, i, [](double x, double y) { return x + y; });
-    const uint64_t c1 = warp_seg_reduce(ck, i, [](uint64_t x, uint64_t y) { return x + y; });
-    if (active && warp_seg_head(i)) {
-        const int64_t first = i == 0 ? 0 : pincl[i - 1];
-        const int64_t w = p >> 5;
-        const int64_t slot = (i == 0 ? 0 : pwincl[i - 1]) + (w - (first >> 5));
+    const double z = active ? aS - aT : 0.0;
+    double s1 = z, s2 = z * z;
+    uint64_t ck = active ? walk_hash(q, (uint32_t)b, 0u, k, eS) + walk_hash(q, (uint32_t)b, 1u, k, eT) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        ck += __shfl_xor_sync(0xffffffffu, ck, o);
+    }
+    if (lane == 0) {
         TilePart tp;
         tp.s1 = s1;
         tp.s2 = s2;
-        tp.ck = c1;
+        tp.ck = ck;
         tp.pad = 0;
-        parts[slot] = tp;
+        parts[chunk] = tp;
     }
 }
 
@@ -776,7 +828,7 @@ void Workspace::release()
 {
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2, &head,
-                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey};
+                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals};
     for (DevBuf *b : all) b->release();
     if (host_pinned) cudaFreeHost(host_pinned);
     host_pinned = nullptr;
@@ -875,14 +927,14 @@ int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, c
     if (rc) return rc;
     const int64_t Y = c.hp[0];
     if (Y == 0) return ER_OK;
-    ENSURE(ws.ypool, sizeof(YEntry) * (size_t)(pool_used + Y), true);
-    k_yfill<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, ws.ypool.as<YEntry>() + pool_used);
+    ENSURE(ws.ypool, sizeof(int32_t) * (size_t)(pool_used + Y), true);
+    ENSURE(ws.yvals, sizeof(double) * (size_t)(pool_used + Y), true);
+    k_yfill<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, ws.ypool.as<int32_t>() + pool_used);
     LAUNCHED(c.g);
-    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, ycap, yincl, pool_used, ws.qs.as<QState>(),
-                                                    ws.ypool.as<YEntry>());
+    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, ycap, yincl, pool_used, ws.qs.as<QState>());
     LAUNCHED(c.g);
     k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, segoff, act, ycap,
-                                                      ws.qs.as<QState>(), ws.ypool.as<YEntry>());
+                                                      ws.qs.as<QState>(), ws.ypool.as<int32_t>(), ws.yvals.as<double>());
     LAUNCHED(c.g);
     pool_used += Y;
     return ER_OK;
@@ -1180,31 +1232,25 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             std::swap(ws.act, ws.act2);
         }
         for (int b = 0; b < P.tau && na > 0; b++) {
-            ENSURE(ws.tiles, sizeof(int64_t) * 4 * (na + 1), false);
-            int64_t *npairs = ws.tiles.as<int64_t>();
-            int64_t *pincl = npairs + (na + 1);
-            int64_t *nw = pincl + (na + 1);
-            int64_t *pwincl = nw + (na + 1);
-            k_npairs<<<blocks_for(na, 256), 256, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), qs, b, npairs);
+            ENSURE(ws.tiles, sizeof(int64_t) * 2 * (na + 1), false);
+            int64_t *nch = ws.tiles.as<int64_t>();
+            int64_t *cincl = nch + (na + 1);
+            k_nchunks<<<blocks_for(na, 256), 256, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), qs, b, nch);
             LAUNCHED(g);
-            rc = scan_incl(c, npairs, pincl, na);
+            rc = scan_incl(c, nch, cincl, na);
             if (rc) return rc;
-            k_nwarps<<<blocks_for(na, 256), 256, 0, st>>>((int32_t)na, pincl, nw);
-            LAUNCHED(g);
-            rc = scan_incl(c, nw, pwincl, na);
+            rc = read_scalars(c, {cincl + (na - 1)});
             if (rc) return rc;
-            rc = read_scalars(c, {pincl + (na - 1), pwincl + (na - 1)});
-            if (rc) return rc;
-            const int64_t W = c.hp[0], NP = c.hp[1];
-            ENSURE(ws.parts, sizeof(TilePart) * NP, false);
+            const int64_t NC = c.hp[0];
+            ENSURE(ws.parts, sizeof(TilePart) * NC, false);
             if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk], st));
-            k_walks<<<blocks_for(W, WALK_THREADS), WALK_THREADS, 0, st>>>(
-                W, (int32_t)na, pincl, pwincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_cols, ws.ypool.as<YEntry>(), b,
-                key0, key1, P.qbase, ws.parts.as<TilePart>());
+            k_walks<<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(
+                NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_cols, ws.ypool.as<int32_t>(),
+                ws.yvals.as<double>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>());
             LAUNCHED(g);
             if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk + 1], st));
             k_amc_reduce<<<blocks_for(na * 32, 256), 256, 0, st>>>(
-                (int32_t)na, ws.act.as<int32_t>(), pwincl, ws.parts.as<TilePart>(), b, P, qs, ws.cont.as<int32_t>(),
+                (int32_t)na, ws.act.as<int32_t>(), cincl, ws.parts.as<TilePart>(), b, P, qs, ws.cont.as<int32_t>(),
                 prof ? reinterpret_cast<unsigned long long *>(g->d_steps) : nullptr);
             nwalk++;
             LAUNCHED(g);
