@@ -219,6 +219,8 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         for (int64_t v = 0; v < n; v++) rec[v] = make_uint2((uint32_t)offsets[v], (uint32_t)(offsets[v + 1] - offsets[v]));
         e = cudaMalloc(&g->d_rec, sizeof(uint2) * n);
         if (e == cudaSuccess) e = cudaMemcpy(g->d_rec, rec.data(), sizeof(uint2) * n, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMalloc(&g->d_arcs, sizeof(uint4) * std::max<int64_t>(g->nnz, 1));
+        if (e == cudaSuccess) e = geer::build_arcs(g);
     }
     if (e != cudaSuccess) {
         cuda_fail(e, "er_graph_create");
@@ -241,6 +243,7 @@ void er_graph_destroy(er_graph *g)
         if (g->d_off) cudaFree(g->d_off);
         if (g->d_cols) cudaFree(g->d_cols);
         if (g->d_rec) cudaFree(g->d_rec);
+        if (g->d_arcs) cudaFree(g->d_arcs);
         if (g->d_steps) cudaFree(g->d_steps);
         if (g->stream) cudaStreamDestroy(g->stream);
         cudaSetDevice(cur);

@@ -94,6 +94,7 @@ struct er_graph {
     int64_t *d_off = nullptr;
     int32_t *d_cols = nullptr;
     uint2 *d_rec = nullptr;       // {offset, degree} per node (offsets < 2^32)
+    uint4 *d_arcs = nullptr;      // {u, offset(u), degree(u), 0} per arc, in CSR order (walk chain)
     int32_t max_deg = 0;
     bool rows_sorted = false;
     int query_block = 0;  // ER_OK, or the validation code that forbids queries (ER_CREATE_SPMM_ONLY)
@@ -119,5 +120,6 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                     const er_opts &o, double *out_r, er_query_stats *stats);
 int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st);
 int run_estimate_lambda(er_graph *g, int iters, double *lambda_out);
+cudaError_t build_arcs(er_graph *g);
 
 }  // namespace geer

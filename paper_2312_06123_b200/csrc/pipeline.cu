@@ -523,13 +523,15 @@ __device__ __forceinline__ int bucket_match(const int4 a, const int4 b, int32_t 
 template <bool SMEM>
 __device__ __forceinline__ void load_bucket(const int32_t *keys, uint32_t bk, int4 &a, int4 &b)
 {
-    const int4 *p = reinterpret_cast<const int4 *>(keys + (size_t)bk * YB);
+    const int32_t *p = keys + (size_t)bk * YB;
     if (SMEM) {
-        a = p[0];
-        b = p[1];
+        a = reinterpret_cast<const int4 *>(p)[0];
+        b = reinterpret_cast<const int4 *>(p)[1];
     } else {
-        a = __ldg(p);
-        b = __ldg(p + 1);
+        // one 32-byte sector in one instruction (LDG.E.ENL2.256 on sm_100a)
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                     : "l"(p));
     }
 }
 
@@ -550,11 +552,12 @@ __device__ __noinline__ double probe_rest(const int32_t *keys, const double *__r
 }
 
 // One walk pair (S_k from s, T_k from t), both chains advanced in one loop.  Software
-// pipelined: step j issues the node-record load for step j+1 before it resolves the y probe of
-// step j-1's node, and a hit's value load is consumed one step later, so only the
-// record -> column chain is serial.  y values are added in step order (R9, R13).
+// pipelined: step j issues the load of step j's arc before it resolves the y probe of step
+// j-1's node, and a hit's value load is consumed one step later, so only the arc chain is
+// serial.  Arc records {u, off(u), d(u), -} make the chain one 16-byte load per step.
+// y values are added in step order (R9, R13).
 template <bool SMEM>
-__device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const int32_t *__restrict__ cols,
+__device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
                                           const int32_t *keys, const double *__restrict__ vals, int lgb,
                                           int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b, uint64_t k,
                                           uint32_t key0, uint32_t key1, double &accS, double &accT,
@@ -563,13 +566,26 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const i
     const uint32_t bmask = (1u << lgb) - 1u;
     const uint32_t c3S = (b << 29) | (0u << 28) | (uint32_t)(k >> 32);
     const uint32_t c3T = (b << 29) | (1u << 28) | (uint32_t)(k >> 32);
+    uint2 RS = __ldg(rec + s), RT = __ldg(rec + t);   // {offset, degree} of the current nodes
     int32_t vS = s, vT = t;
     double aS = 0.0, aT = 0.0;
     double pvS = 0.0, pvT = 0.0;        // pending hit values (added one step later)
     int4 kS0, kS1, kT0, kT1;            // bucket keys of the current nodes
     U4 rS = {0, 0, 0, 0}, rT = {0, 0, 0, 0};
     for (int32_t j = 1; j <= lf; j++) {
-        const uint2 RS = __ldg(rec + vS), RT = __ldg(rec + vT);
+        uint64_t r64S, r64T;
+        if (j & 1) {
+            const uint32_t cc = (uint32_t)((j - 1) >> 1);
+            rS = philox4x32_10(U4{cc, (uint32_t)k, q, c3S}, key0, key1);
+            rT = philox4x32_10(U4{cc, (uint32_t)k, q, c3T}, key0, key1);
+            r64S = ((uint64_t)rS.y << 32) | rS.x;
+            r64T = ((uint64_t)rT.y << 32) | rT.x;
+        } else {
+            r64S = ((uint64_t)rS.w << 32) | rS.z;
+            r64T = ((uint64_t)rT.w << 32) | rT.z;
+        }
+        const uint4 AS = __ldg(arcs + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
+        const uint4 AT = __ldg(arcs + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
         if (j > 1) {
             aS += pvS;
             aT += pvT;
@@ -584,19 +600,10 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const i
             if (mT >= 0) pvT = __ldg(vals + (size_t)bT * YB + mT);
             else if (!eT) aT += probe_rest<SMEM>(keys, vals, bT, bmask, vT);
         }
-        uint64_t r64S, r64T;
-        if (j & 1) {
-            const uint32_t cc = (uint32_t)((j - 1) >> 1);
-            rS = philox4x32_10(U4{cc, (uint32_t)k, q, c3S}, key0, key1);
-            rT = philox4x32_10(U4{cc, (uint32_t)k, q, c3T}, key0, key1);
-            r64S = ((uint64_t)rS.y << 32) | rS.x;
-            r64T = ((uint64_t)rT.y << 32) | rT.x;
-        } else {
-            r64S = ((uint64_t)rS.w << 32) | rS.z;
-            r64T = ((uint64_t)rT.w << 32) | rT.z;
-        }
-        vS = __ldg(cols + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
-        vT = __ldg(cols + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
+        vS = (int32_t)AS.x;
+        vT = (int32_t)AT.x;
+        RS = make_uint2(AS.y, AS.z);
+        RT = make_uint2(AT.y, AT.z);
         load_bucket<SMEM>(keys, ybucket(vS, lgb), kS0, kS1);
         load_bucket<SMEM>(keys, ybucket(vT, lgb), kT0, kT1);
     }
@@ -625,11 +632,11 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const i
 // Each warp writes the canonical partial {sum Z, sum Z^2, checksum} of its chunk.
 __global__ void __launch_bounds__(WALK_THREADS, 4)
 k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
-        const QState *__restrict__ qs, const uint2 *__restrict__ rec, const int32_t *__restrict__ cols,
+        const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
         const int32_t *__restrict__ ykeys, const double *__restrict__ yvals, int b, uint32_t key0, uint32_t key1,
         int64_t qbase, TilePart *__restrict__ parts)
 {
-    __shared__ __align__(16) int32_t sm_keys[WALK_SMEM_SLOTS];
+    __shared__ __align__(32) int32_t sm_keys[WALK_SMEM_SLOTS];
     __shared__ int32_t s_qi[WALK_WARPS];
     __shared__ int32_t s_soff[WALK_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -675,10 +682,10 @@ k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const in
     int32_t eS = 0, eT = 0;
     if (active) {
         if (s_soff[warp] >= 0)
-            walk_pair<true>(rec, cols, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k,
+            walk_pair<true>(rec, arcs, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k,
                             key0, key1, aS, aT, eS, eT);
         else
-            walk_pair<false>(rec, cols, ykeys + Q.yoff, vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k, key0,
+            walk_pair<false>(rec, arcs, ykeys + Q.yoff, vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k, key0,
                              key1, aS, aT, eS, eT);
     }
     const double z = active ? aS - aT : 0.0;
@@ -1245,7 +1252,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             ENSURE(ws.parts, sizeof(TilePart) * NC, false);
             if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk], st));
             k_walks<<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(
-                NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_cols, ws.ypool.as<int32_t>(),
+                NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_arcs, ws.ypool.as<int32_t>(),
                 ws.yvals.as<double>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>());
             LAUNCHED(g);
             if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk + 1], st));
@@ -1305,6 +1312,25 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         for (auto &e : ev) cudaEventDestroy(e);
     }
     return ER_OK;
+}
+
+__global__ void k_build_arcs(int64_t nnz, const int32_t *__restrict__ cols, const uint2 *__restrict__ rec,
+                             uint4 *__restrict__ arcs)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    const int32_t u = cols[e];
+    const uint2 r = rec[u];
+    arcs[e] = make_uint4((uint32_t)u, r.x, r.y, 0u);
+}
+
+cudaError_t build_arcs(er_graph *g)
+{
+    k_build_arcs<<<blocks_for(g->nnz, 256), 256>>>(g->nnz, g->d_cols, g->d_rec, g->d_arcs);
+    g->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    return e;
 }
 
 int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st)
