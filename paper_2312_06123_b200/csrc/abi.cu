@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -219,8 +220,20 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         for (int64_t v = 0; v < n; v++) rec[v] = make_uint2((uint32_t)offsets[v], (uint32_t)(offsets[v + 1] - offsets[v]));
         e = cudaMalloc(&g->d_rec, sizeof(uint2) * n);
         if (e == cudaSuccess) e = cudaMemcpy(g->d_rec, rec.data(), sizeof(uint2) * n, cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMalloc(&g->d_arcs, sizeof(uint4) * std::max<int64_t>(g->nnz, 1));
-        if (e == cudaSuccess) e = geer::build_arcs(g);
+        // walk layout: {off, d} node records + columns while they stay well inside L2;
+        // 16-byte arc records (one random access per step) once the graph is DRAM-resident anyway
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
+        const double foot = 4.0 * (double)g->nnz + 8.0 * (double)n;
+        bool use_arcs = foot > 0.5 * (double)l2;
+        if (const char *env = getenv("GEER_WALK_LAYOUT")) {
+            if (!strcmp(env, "arcs")) use_arcs = true;
+            if (!strcmp(env, "cols")) use_arcs = false;
+        }
+        if (use_arcs && e == cudaSuccess) {
+            e = cudaMalloc(&g->d_arcs, sizeof(uint4) * std::max<int64_t>(g->nnz, 1));
+            if (e == cudaSuccess) e = geer::build_arcs(g);
+        }
     }
     if (e != cudaSuccess) {
         cuda_fail(e, "er_graph_create");

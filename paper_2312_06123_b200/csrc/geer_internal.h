@@ -76,7 +76,7 @@ struct Workspace {
     DevBuf keys, vals, keys2, vals2;                // emitted (key, value) pairs + sort buffers
     DevBuf head, runidx, runstart;                  // run-length reduction
     DevBuf segstat;                                 // SegStat per segment
-    DevBuf ycap, yoff, ypool, yvals;                // y-tables: int32 keys (8 per bucket) | fp64 values
+    DevBuf ycap, yoff, ypool, yvals, ytmp;          // y-tables: int32 keys (8 per bucket) | fp64 values | t* scratch
     DevBuf tiles, parts;                            // AMC tiles
     DevBuf cub_tmp;                                 // CUB temp storage
     DevBuf scalars;                                 // small device scalars

@@ -253,6 +253,50 @@ __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const
     }
 }
 
+// K2/K3 for the first SMM iteration when every adjacency row is sorted: from s* = e_s the
+// iterate is s*(u) = (0.0 + 1.0)/d(u) on N(s) (one contribution per u), already in ascending u
+// order, so no push/sort is needed.  Same statistics as k_run_reduce.
+__global__ void k_first_wave(int64_t E, int32_t nseg, const int64_t *__restrict__ ent_off,
+                             const int32_t *__restrict__ fr_id, const int64_t *__restrict__ off,
+                             const int32_t *__restrict__ cols, const int32_t *__restrict__ act,
+                             const QState *__restrict__ qs, int32_t *__restrict__ nid, double *__restrict__ nval,
+                             int32_t *__restrict__ nseg_out, SegStat *__restrict__ ss, int64_t *__restrict__ dU)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = p < E;
+    int32_t g = 0x7fffffff;
+    unsigned long long deg = 0, bits = 0;
+    if (live) {
+        int32_t lo = 0, hi = nseg;  // ent_off[lo] <= p < ent_off[hi]
+        while (hi - lo > 1) {
+            const int32_t mid = (lo + hi) >> 1;
+            if (ent_off[mid] <= p) lo = mid;
+            else hi = mid;
+        }
+        g = lo;
+        const int32_t v = fr_id[g];
+        const int32_t u = cols[off[v] + (p - ent_off[g])];
+        const int64_t d = off[u + 1] - off[u];
+        const double sum = 0.0 + 1.0;
+        const double x = sum / (double)d;
+        nid[p] = u;
+        nval[p] = x;
+        nseg_out[p] = g;
+        deg = (unsigned long long)d;
+        bits = (unsigned long long)__double_as_longlong(x);
+        const QState &Q = qs[act[g >> 1]];
+        if (u == Q.s) ss[g].at_s = x;
+        if (u == Q.t) ss[g].at_t = x;
+        if (p == 0) *dU = E;
+    }
+    const unsigned long long vsum = warp_seg_reduce(deg, g, [](unsigned long long a, unsigned long long b) { return a + b; });
+    const unsigned long long vmax = warp_seg_reduce(bits, g, [](unsigned long long a, unsigned long long b) { return a > b ? a : b; });
+    if (live && warp_seg_head(g)) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(&ss[g].vol), vsum);
+        atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max1), vmax);
+    }
+}
+
 // K4b: max2 of each segment = max1 if max1 occurs twice, else the largest entry below max1 (R5).
 __global__ void k_seg_max2(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                            const double *__restrict__ val, SegStat *__restrict__ ss)
@@ -367,20 +411,24 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int
     Q.ylog2 = lg;
 }
 
-__global__ void k_yfill(int64_t Y, int32_t *__restrict__ keys)
+__global__ void k_yfill(int64_t Y, int32_t *__restrict__ keys, double *__restrict__ ys, double *__restrict__ yt)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < Y) keys[j] = -1;
+    if (j >= Y) return;
+    keys[j] = -1;
+    ys[j] = 0.0;
+    yt[j] = 0.0;
 }
 
-// K5: y(v) = s*(v)/d(s) - t*(v)/d(t) for v in supp(s*) U supp(t*) (Alg. 1 L7 with s = s*, t = t*).
+// K5a: insert every support node of a leaving query into its y-table (find-or-insert; the node
+// may come from both sides) and record s*(v) (side 0) or t*(v) (side 1) at its slot.
 // Bucketed open addressing: 8 int32 keys per 32-byte bucket, buckets probed linearly, slots in
-// order inside a bucket; values in a parallel fp64 array.
+// order inside a bucket.
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                           const int32_t *__restrict__ id, const double *__restrict__ val,
-                          const int64_t *__restrict__ segoff, const int32_t *__restrict__ act,
-                          const int64_t *__restrict__ ycap, const QState *__restrict__ qs, int32_t *__restrict__ ykeys,
-                          double *__restrict__ yvals)
+                          const int32_t *__restrict__ act, const int64_t *__restrict__ ycap,
+                          const QState *__restrict__ qs, int32_t *__restrict__ ykeys, double *__restrict__ ys,
+                          double *__restrict__ yt, int64_t tbase)
 {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
@@ -389,41 +437,45 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
     if (ycap[i] == 0) return;
     const QState &Q = qs[act[i]];
     const int32_t v = id[e];
-    const double x = val[e];
-    const int32_t og = g ^ 1;
-    int64_t lo = segoff[og], hi = segoff[og + 1];
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (id[mid] < v) lo = mid + 1;
-        else hi = mid;
-    }
-    const bool found = lo < segoff[og + 1] && id[lo] == v;
-    double a, b;
-    if ((g & 1) == 0) {
-        a = x;
-        b = found ? val[lo] : 0.0;
-    } else {
-        if (found) return;  // inserted by the s-side entry
-        a = 0.0;
-        b = x;
-    }
-    const double y = a / (double)Q.ds - b / (double)Q.dt;
     int32_t *keys = ykeys + Q.yoff;
-    double *vals = yvals + Q.yoff;
     const int lgb = Q.ylog2 - YB_LOG;
     const uint32_t bmask = (1u << lgb) - 1u;
     uint32_t bk = ybucket(v, lgb);
     while (true) {
         for (int j = 0; j < YB; j++) {
             const uint32_t slot = bk * YB + j;
-            if (keys[slot] != -1) continue;
-            if (atomicCAS(&keys[slot], -1, v) == -1) {
-                vals[slot] = y;
+            int32_t k = keys[slot];
+            if (k == -1) k = atomicCAS(&keys[slot], -1, v);
+            if (k == -1 || k == v) {
+                if (g & 1) yt[Q.yoff - tbase + slot] = val[e];
+                else ys[Q.yoff + slot] = val[e];
                 return;
             }
         }
         bk = (bk + 1) & bmask;
     }
+}
+
+// K5b: y(v) = s*(v)/d(s) - t*(v)/d(t) at every occupied slot of the new tables (Alg. 1 L7 with
+// s = s*, t = t*); a side the node is not on contributes 0.0 (its value stayed 0).
+__global__ void k_yfinal(int64_t Y, int64_t tbase, int32_t na, const int32_t *__restrict__ act,
+                         const int64_t *__restrict__ ycap, const int64_t *__restrict__ yincl,
+                         const QState *__restrict__ qs, const int32_t *__restrict__ ykeys, double *__restrict__ ys,
+                         const double *__restrict__ yt)
+{
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= Y) return;
+    const int64_t slot = tbase + j;
+    if (ykeys[slot] < 0) return;
+    int32_t lo = 0, hi = na - 1;  // owner: smallest i with yincl[i] > j
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (yincl[mid] > j) hi = mid;
+        else lo = mid + 1;
+    }
+    const QState &Q = qs[act[lo]];
+    const double a = ys[slot], b = yt[j];
+    ys[slot] = a / (double)Q.ds - b / (double)Q.dt;
 }
 
 // Continuing segments: new lengths (for the compaction scan).
@@ -529,7 +581,7 @@ __device__ __forceinline__ void load_bucket(const int32_t *keys, uint32_t bk, in
         b = reinterpret_cast<const int4 *>(p)[1];
     } else {
         // one 32-byte sector in one instruction (LDG.E.ENL2.256 on sm_100a)
-        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
                      : "l"(p));
     }
@@ -537,7 +589,7 @@ __device__ __forceinline__ void load_bucket(const int32_t *keys, uint32_t bk, in
 
 // Slow path: v not in its first bucket and the bucket is full -> probe the following buckets.
 template <bool SMEM>
-__device__ __noinline__ double probe_rest(const int32_t *keys, const double *__restrict__ vals, uint32_t bk,
+__device__ __forceinline__ double probe_rest(const int32_t *keys, const double *__restrict__ vals, uint32_t bk,
                                           uint32_t bmask, int32_t v)
 {
     while (true) {
@@ -556,8 +608,9 @@ __device__ __noinline__ double probe_rest(const int32_t *keys, const double *__r
 // j-1's node, and a hit's value load is consumed one step later, so only the arc chain is
 // serial.  Arc records {u, off(u), d(u), -} make the chain one 16-byte load per step.
 // y values are added in step order (R9, R13).
-template <bool SMEM>
+template <bool SMEM, bool ARC>
 __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
+                                          const int32_t *__restrict__ cols,
                                           const int32_t *keys, const double *__restrict__ vals, int lgb,
                                           int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b, uint64_t k,
                                           uint32_t key0, uint32_t key1, double &accS, double &accT,
@@ -584,8 +637,14 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
             r64S = ((uint64_t)rS.w << 32) | rS.z;
             r64T = ((uint64_t)rT.w << 32) | rT.z;
         }
-        const uint4 AS = __ldg(arcs + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
-        const uint4 AT = __ldg(arcs + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
+        uint4 AS, AT;
+        if (ARC) {
+            AS = __ldg(arcs + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
+            AT = __ldg(arcs + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
+        } else {
+            AS.x = (uint32_t)__ldg(cols + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
+            AT.x = (uint32_t)__ldg(cols + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
+        }
         if (j > 1) {
             aS += pvS;
             aT += pvT;
@@ -602,8 +661,13 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
         }
         vS = (int32_t)AS.x;
         vT = (int32_t)AT.x;
-        RS = make_uint2(AS.y, AS.z);
-        RT = make_uint2(AT.y, AT.z);
+        if (ARC) {
+            RS = make_uint2(AS.y, AS.z);
+            RT = make_uint2(AT.y, AT.z);
+        } else {
+            RS = __ldg(rec + vS);
+            RT = __ldg(rec + vT);
+        }
         load_bucket<SMEM>(keys, ybucket(vS, lgb), kS0, kS1);
         load_bucket<SMEM>(keys, ybucket(vT, lgb), kT0, kT1);
     }
@@ -630,9 +694,11 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
 // query after query, queries ordered by descending ell_f).  The CTA stages the y-table keys of
 // its (<= 8) queries in shared memory when they fit; otherwise the warp probes global memory.
 // Each warp writes the canonical partial {sum Z, sum Z^2, checksum} of its chunk.
+template <bool ARC>
 __global__ void __launch_bounds__(WALK_THREADS, 4)
 k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
         const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
+        const int32_t *__restrict__ cols,
         const int32_t *__restrict__ ykeys, const double *__restrict__ yvals, int b, uint32_t key0, uint32_t key1,
         int64_t qbase, TilePart *__restrict__ parts)
 {
@@ -682,10 +748,10 @@ k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const in
     int32_t eS = 0, eT = 0;
     if (active) {
         if (s_soff[warp] >= 0)
-            walk_pair<true>(rec, arcs, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k,
+            walk_pair<true, ARC>(rec, arcs, cols, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k,
                             key0, key1, aS, aT, eS, eT);
         else
-            walk_pair<false>(rec, arcs, ykeys + Q.yoff, vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k, key0,
+            walk_pair<false, ARC>(rec, arcs, cols, ykeys + Q.yoff, vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k, key0,
                              key1, aS, aT, eS, eT);
     }
     const double z = active ? aS - aT : 0.0;
@@ -835,7 +901,7 @@ void Workspace::release()
 {
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2, &head,
-                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals};
+                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals, &ytmp};
     for (DevBuf *b : all) b->release();
     if (host_pinned) cudaFreeHost(host_pinned);
     host_pinned = nullptr;
@@ -936,12 +1002,19 @@ int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, c
     if (Y == 0) return ER_OK;
     ENSURE(ws.ypool, sizeof(int32_t) * (size_t)(pool_used + Y), true);
     ENSURE(ws.yvals, sizeof(double) * (size_t)(pool_used + Y), true);
-    k_yfill<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, ws.ypool.as<int32_t>() + pool_used);
+    ENSURE(ws.ytmp, sizeof(double) * (size_t)Y, false);
+    (void)segoff;
+    k_yfill<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, ws.ypool.as<int32_t>() + pool_used,
+                                                  ws.yvals.as<double>() + pool_used, ws.ytmp.as<double>());
     LAUNCHED(c.g);
     k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, ycap, yincl, pool_used, ws.qs.as<QState>());
     LAUNCHED(c.g);
-    k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, segoff, act, ycap,
-                                                      ws.qs.as<QState>(), ws.ypool.as<int32_t>(), ws.yvals.as<double>());
+    k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, act, ycap, ws.qs.as<QState>(),
+                                                      ws.ypool.as<int32_t>(), ws.yvals.as<double>(),
+                                                      ws.ytmp.as<double>(), pool_used);
+    LAUNCHED(c.g);
+    k_yfinal<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, pool_used, na, act, ycap, yincl, ws.qs.as<QState>(),
+                                                  ws.ypool.as<int32_t>(), ws.yvals.as<double>(), ws.ytmp.as<double>());
     LAUNCHED(c.g);
     pool_used += Y;
     return ER_OK;
@@ -1117,6 +1190,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                                                                    ws.fr_seg.as<int32_t>(), ws.fr_off.as<int64_t>());
             LAUNCHED(g);
         }
+        bool first_wave = true;
         while (na > 0) {
             const int32_t nseg = (int32_t)(2 * na);
             // emission offsets
@@ -1135,22 +1209,32 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                 set_error(ER_ENOMEM, "SMM wave emits more than 2^31 pairs");
                 return ER_ENOMEM;
             }
-            ENSURE(ws.segbeg, sizeof(int32_t) * (nseg + 1), false);
-            int32_t *segbeg = ws.segbeg.as<int32_t>();
-            k_segbeg<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, ws.fr_off.as<int64_t>(), ent_off, segbeg);
-            LAUNCHED(g);
             ENSURE(ws.scalars, sizeof(int64_t) * 8, false);
             int64_t *dU = ws.scalars.as<int64_t>();
-            ENSURE(ws.head, sizeof(int32_t) * E, false);
-            if (P.nbits <= 24) rc = smm_group<uint32_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU);
-            else rc = smm_group<uint64_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU);
-            if (rc) return rc;
+            const bool fast_first = first_wave && g->rows_sorted;
+            int32_t *segbeg = nullptr;
+            if (!fast_first) {
+                ENSURE(ws.segbeg, sizeof(int32_t) * (nseg + 1), false);
+                segbeg = ws.segbeg.as<int32_t>();
+                k_segbeg<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, ws.fr_off.as<int64_t>(), ent_off, segbeg);
+                LAUNCHED(g);
+                ENSURE(ws.head, sizeof(int32_t) * E, false);
+                if (P.nbits <= 24) rc = smm_group<uint32_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU);
+                else rc = smm_group<uint64_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU);
+                if (rc) return rc;
+            }
             ENSURE(ws.nf_id, sizeof(int32_t) * E, false);
             ENSURE(ws.nf_val, sizeof(double) * E, false);
             ENSURE(ws.nf_seg, sizeof(int32_t) * E, false);
             ENSURE(ws.nf_off, sizeof(int64_t) * (nseg + 1), false);
             ENSURE(ws.segstat, sizeof(SegStat) * nseg, false);
             CK(cudaMemsetAsync(ws.segstat.p, 0, sizeof(SegStat) * nseg, st));
+            if (fast_first) {
+                k_first_wave<<<blocks_for(E, 256), 256, 0, st>>>(E, nseg, ent_off, ws.fr_id.as<int32_t>(), g->d_off,
+                                                                 g->d_cols, ws.act.as<int32_t>(), qs,
+                                                                 ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
+                                                                 ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>(), dU);
+            } else
             if (P.nbits <= 24)
                 k_run_reduce<uint32_t><<<blocks_for(E, 256), 256, 0, st>>>(
                     E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint32_t>(), P.nbits, ws.vals2.as<double>(), segbeg,
@@ -1211,6 +1295,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             }
             na = na2;
             F = F2;
+            first_wave = false;
         }
     }
 
@@ -1251,9 +1336,14 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             const int64_t NC = c.hp[0];
             ENSURE(ws.parts, sizeof(TilePart) * NC, false);
             if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk], st));
-            k_walks<<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(
-                NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_arcs, ws.ypool.as<int32_t>(),
-                ws.yvals.as<double>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>());
+            if (g->d_arcs)
+                k_walks<true><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(
+                    NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_arcs, g->d_cols,
+                    ws.ypool.as<int32_t>(), ws.yvals.as<double>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>());
+            else
+                k_walks<false><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(
+                    NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_arcs, g->d_cols,
+                    ws.ypool.as<int32_t>(), ws.yvals.as<double>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>());
             LAUNCHED(g);
             if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk + 1], st));
             k_amc_reduce<<<blocks_for(na * 32, 256), 256, 0, st>>>(

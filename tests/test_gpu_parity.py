@@ -225,3 +225,21 @@ def test_launch_counter(geer, tiny, tiny_h):
     n0 = geer.er_graph_kernel_launches(tiny_h)
     geer.er_query_batch(tiny_h, pairs, 0.1)
     assert geer.er_graph_kernel_launches(tiny_h) > n0
+
+
+def test_unsorted_rows_parity(geer, tiny):
+    # adjacency rows in a random order: walks index rows in input order on both sides (R10);
+    # SMM sums differ from the oracle's CSR-order sums only by rounding (R13, 1e-10 relative)
+    g0, pairs = tiny
+    rng = np.random.default_rng(5)
+    cols = g0.cols.copy()
+    for v in range(g0.n):
+        a, b = g0.offsets[v], g0.offsets[v + 1]
+        cols[a:b] = rng.permutation(cols[a:b])
+    g = W.Graph(g0.n, g0.offsets.copy(), cols, "tiny_shuffled", g0.lam)
+    h = geer.er_graph_create(g.n, g.offsets, g.cols)
+    geer.er_graph_set_lambda(h, g.lam)
+    for eps in (0.1, 0.3):
+        r, st, ro, so = run_both(geer, h, g, pairs, eps)
+        compare(g, pairs, r, st, ro, so, sorted_adj=False)
+    geer.er_graph_destroy(h)
