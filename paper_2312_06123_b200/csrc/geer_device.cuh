@@ -58,14 +58,6 @@ __device__ __forceinline__ uint32_t ybucket(int32_t v, int lgb)
     return lgb == 0 ? 0u : ((uint32_t)v * 0x9E3779B1u) >> (32 - lgb);
 }
 
-// 8-bit fingerprint of node v (1..255; 0 marks an empty slot), from hash bits independent of
-// the bucket index.
-__device__ __forceinline__ uint8_t yfinger(int32_t v)
-{
-    const uint32_t h = (uint32_t)v * 0x85EBCA6Bu;
-    return (uint8_t)(1u + ((h ^ (h >> 13)) & 0xffu) % 255u);
-}
-
 // Eq. 10.
 __device__ __forceinline__ double psi_eq10(int64_t lf, double m1s, double m2s, double m1t, double m2t,
                                            double ds, double dt)

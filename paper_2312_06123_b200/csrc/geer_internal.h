@@ -28,13 +28,6 @@ struct QState {
 };
 
 
-// y-table slot: 16 B, so a confirmed probe reads key and value in one access.
-struct YEntry {
-    int32_t key;   // node id, -1 = empty
-    int32_t pad;
-    double val;    // y(v) = s*(v)/d(s) - t*(v)/d(t)
-};
-
 // Per-segment statistics of an SMM iterate (segment = one side of one query).
 struct SegStat {
     int64_t vol;           // sum of d(v) over the support (Eq. 15 left side)
@@ -83,7 +76,7 @@ struct Workspace {
     DevBuf keys, vals, keys2, vals2;                // emitted (key, value) pairs + sort buffers
     DevBuf head, runidx, runstart;                  // run-length reduction
     DevBuf segstat;                                 // SegStat per segment
-    DevBuf ycap, yoff, ypool, yvals, ytmp, yfp;     // y-tables: YEntry slots | (unused) | t* scratch | fingerprints
+    DevBuf ycap, yoff, ypool, yvals, ytmp;          // y-tables: int32 keys (8 per bucket) | fp64 values | t* scratch
     DevBuf tiles, parts;                            // AMC tiles
     DevBuf cub_tmp;                                 // CUB temp storage
     DevBuf scalars;                                 // small device scalars

@@ -411,23 +411,23 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int
     Q.ylog2 = lg;
 }
 
-__global__ void k_yfill(int64_t Y, YEntry *__restrict__ tab, uint8_t *__restrict__ fps, double *__restrict__ yt)
+__global__ void k_yfill(int64_t Y, int32_t *__restrict__ keys, double *__restrict__ ys, double *__restrict__ yt)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= Y) return;
-    tab[j] = YEntry{-1, 0, 0.0};
-    fps[j] = 0;
+    keys[j] = -1;
+    ys[j] = 0.0;
     yt[j] = 0.0;
 }
 
 // K5a: insert every support node of a leaving query into its y-table (find-or-insert; the node
-// may come from both sides).  Side 0 stores s*(v)/d(s) in the entry, side 1 stores t*(v)/d(t)
-// in a scratch array; the slot's fingerprint byte is set.  Bucketed open addressing: buckets of
-// 8 slots probed linearly, slots in order inside a bucket, claimed by CAS on the key.
+// may come from both sides) and record s*(v) (side 0) or t*(v) (side 1) at its slot.
+// Bucketed open addressing: 8 int32 keys per 32-byte bucket, buckets probed linearly, slots in
+// order inside a bucket.
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                           const int32_t *__restrict__ id, const double *__restrict__ val,
                           const int32_t *__restrict__ act, const int64_t *__restrict__ ycap,
-                          const QState *__restrict__ qs, YEntry *__restrict__ tab_pool, uint8_t *__restrict__ fp_pool,
+                          const QState *__restrict__ qs, int32_t *__restrict__ ykeys, double *__restrict__ ys,
                           double *__restrict__ yt, int64_t tbase)
 {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -437,22 +437,18 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
     if (ycap[i] == 0) return;
     const QState &Q = qs[act[i]];
     const int32_t v = id[e];
-    YEntry *tab = tab_pool + Q.yoff;
+    int32_t *keys = ykeys + Q.yoff;
     const int lgb = Q.ylog2 - YB_LOG;
     const uint32_t bmask = (1u << lgb) - 1u;
     uint32_t bk = ybucket(v, lgb);
     while (true) {
-        int32_t k[YB];
-#pragma unroll
-        for (int j = 0; j < YB; j++) k[j] = *(volatile int32_t *)&tab[bk * YB + j].key;
         for (int j = 0; j < YB; j++) {
             const uint32_t slot = bk * YB + j;
-            int32_t kk = k[j];
-            if (kk == -1) kk = atomicCAS(&tab[slot].key, -1, v);
-            if (kk == -1 || kk == v) {
-                if (g & 1) yt[Q.yoff - tbase + slot] = val[e] / (double)Q.dt;
-                else tab[slot].val = val[e] / (double)Q.ds;
-                fp_pool[Q.yoff + slot] = yfinger(v);
+            int32_t k = keys[slot];
+            if (k == -1) k = atomicCAS(&keys[slot], -1, v);
+            if (k == -1 || k == v) {
+                if (g & 1) yt[Q.yoff - tbase + slot] = val[e];
+                else ys[Q.yoff + slot] = val[e];
                 return;
             }
         }
@@ -461,13 +457,25 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
 }
 
 // K5b: y(v) = s*(v)/d(s) - t*(v)/d(t) at every occupied slot of the new tables (Alg. 1 L7 with
-// s = s*, t = t*); a side the node is not on contributes 0.0 (its term stayed 0).
-__global__ void k_yfinal(int64_t Y, int64_t tbase, YEntry *__restrict__ tab, const double *__restrict__ yt)
+// s = s*, t = t*); a side the node is not on contributes 0.0 (its value stayed 0).
+__global__ void k_yfinal(int64_t Y, int64_t tbase, int32_t na, const int32_t *__restrict__ act,
+                         const int64_t *__restrict__ ycap, const int64_t *__restrict__ yincl,
+                         const QState *__restrict__ qs, const int32_t *__restrict__ ykeys, double *__restrict__ ys,
+                         const double *__restrict__ yt)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= Y) return;
-    YEntry &E = tab[tbase + j];
-    if (E.key >= 0) E.val = E.val - yt[j];
+    const int64_t slot = tbase + j;
+    if (ykeys[slot] < 0) return;
+    int32_t lo = 0, hi = na - 1;  // owner: smallest i with yincl[i] > j
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (yincl[mid] > j) hi = mid;
+        else lo = mid + 1;
+    }
+    const QState &Q = qs[act[lo]];
+    const double a = ys[slot], b = yt[j];
+    ys[slot] = a / (double)Q.ds - b / (double)Q.dt;
 }
 
 // Continuing segments: new lengths (for the compaction scan).
@@ -535,7 +543,7 @@ __global__ void k_lf_key(int32_t na, const int32_t *__restrict__ amc, const QSta
 
 constexpr int WALK_WARPS = 8;
 constexpr int WALK_THREADS = 32 * WALK_WARPS;
-constexpr int WALK_SMEM_FP = 32768;        // 32 KB of staged fingerprint bytes (slots) per CTA
+constexpr int WALK_SMEM_SLOTS = 8192;      // 32 KB of staged y-table keys per CTA
 
 __device__ __forceinline__ int32_t find_chunk_query(const int64_t *__restrict__ cincl, int32_t n, int64_t c)
 {
@@ -548,67 +556,65 @@ __device__ __forceinline__ int32_t find_chunk_query(const int64_t *__restrict__ 
     return lo;
 }
 
-// Fingerprint bucket (8 bytes) from shared or global memory.
-template <bool SMEM>
-__device__ __forceinline__ uint2 load_fp(const uint8_t *fps, uint32_t bk)
+// 8 keys of a bucket: index of v, or -1; *empty = the bucket has a free slot.
+__device__ __forceinline__ int bucket_match(const int4 a, const int4 b, int32_t v, bool *empty)
 {
-    const uint2 *p = reinterpret_cast<const uint2 *>(fps + (size_t)bk * YB);
-    return SMEM ? *p : __ldg(p);
+    int m = -1;
+    m = (b.w == v) ? 7 : m;
+    m = (b.z == v) ? 6 : m;
+    m = (b.y == v) ? 5 : m;
+    m = (b.x == v) ? 4 : m;
+    m = (a.w == v) ? 3 : m;
+    m = (a.z == v) ? 2 : m;
+    m = (a.y == v) ? 1 : m;
+    m = (a.x == v) ? 0 : m;
+    *empty = (a.x < 0) | (a.y < 0) | (a.z < 0) | (a.w < 0) | (b.x < 0) | (b.y < 0) | (b.z < 0) | (b.w < 0);
+    return m;
 }
 
-// Byte-match masks of a fingerprint bucket: bit j set if slot j's fingerprint equals f
-// (resp. is 0 = empty).
-__device__ __forceinline__ uint32_t fp_mask(uint2 F, uint32_t f4)
-{
-    const uint32_t lo = __vcmpeq4(F.x, f4), hi = __vcmpeq4(F.y, f4);
-    // 0xff per equal byte -> one bit per byte
-    const uint32_t ml = ((lo >> 7) & 1u) | ((lo >> 14) & 2u) | ((lo >> 21) & 4u) | ((lo >> 28) & 8u);
-    const uint32_t mh = ((hi >> 7) & 1u) | ((hi >> 14) & 2u) | ((hi >> 21) & 4u) | ((hi >> 28) & 8u);
-    return ml | (mh << 4);
-}
-
-// Full lookup of y(v) (blocking): used for the rare cases (fingerprint false positive,
-// second fingerprint match, full bucket).
 template <bool SMEM>
-__device__ __noinline__ double ylookup_slow(const uint8_t *fps, const YEntry *__restrict__ tab, uint32_t bk,
-                                            uint32_t bmask, int32_t v)
+__device__ __forceinline__ void load_bucket(const int32_t *keys, uint32_t bk, int4 &a, int4 &b)
 {
-    const uint32_t f4 = (uint32_t)yfinger(v) * 0x01010101u;
-    while (true) {
-        const uint2 F = load_fp<SMEM>(fps, bk);
-        uint32_t m = fp_mask(F, f4);
-        while (m) {
-            const int j = __ffs(m) - 1;
-            m &= m - 1;
-            const longlong2 E = __ldg(reinterpret_cast<const longlong2 *>(tab + (size_t)bk * YB + j));
-            if ((int32_t)(uint32_t)(unsigned long long)E.x == v) return __longlong_as_double(E.y);
-        }
-        if (fp_mask(F, 0u)) return 0.0;
-        bk = (bk + 1) & bmask;
+    const int32_t *p = keys + (size_t)bk * YB;
+    if (SMEM) {
+        a = reinterpret_cast<const int4 *>(p)[0];
+        b = reinterpret_cast<const int4 *>(p)[1];
+    } else {
+        // one 32-byte sector in one instruction (LDG.E.ENL2.256 on sm_100a)
+        asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                     : "l"(p));
     }
 }
 
-// Pipelined probe state of one chain: the node, its first-bucket fingerprint word, and the
-// speculative entry load of the first fingerprint match.
-struct Probe {
-    int32_t v;
-    uint32_t bk;
-    uint32_t match;  // fingerprint-match mask (after stage 2)
-    uint32_t empty;  // empty-slot mask
-    longlong2 e;     // entry of the first match (valid if match)
-};
+// Slow path: v not in its first bucket and the bucket is full -> probe the following buckets.
+template <bool SMEM>
+__device__ __forceinline__ double probe_rest(const int32_t *keys, const double *__restrict__ vals, uint32_t bk,
+                                          uint32_t bmask, int32_t v)
+{
+    while (true) {
+        bk = (bk + 1) & bmask;
+        int4 a, b;
+        load_bucket<SMEM>(keys, bk, a, b);
+        bool empty;
+        const int m = bucket_match(a, b, v, &empty);
+        if (m >= 0) return __ldg(vals + (size_t)bk * YB + m);
+        if (empty) return 0.0;
+    }
+}
 
-// One walk pair (S_k from s, T_k from t), both chains advanced in one loop.  Per step: the
-// chain load (node record + column, or one arc record), then the y probe of the new node in
-// three pipelined stages -- fingerprint bucket (shared memory when staged), entry load of the
-// first fingerprint match, key check + accumulate -- spread over the following steps, so only
-// the chain loads are serial.  y values are added in step order (R9, R13).
+// One walk pair (S_k from s, T_k from t), both chains advanced in one loop.  Software
+// pipelined: step j issues the load of step j's arc before it resolves the y probe of step
+// j-1's node, and a hit's value load is consumed one step later, so only the arc chain is
+// serial.  Arc records {u, off(u), d(u), -} make the chain one 16-byte load per step.
+// y values are added in step order (R9, R13).
 template <bool SMEM, bool ARC>
 __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
-                                          const int32_t *__restrict__ cols, const uint8_t *fps,
-                                          const YEntry *__restrict__ tab, int lgb, int32_t s, int32_t t, int32_t lf,
-                                          uint32_t q, uint32_t b, uint64_t k, uint32_t key0, uint32_t key1,
-                                          double &accS, double &accT, int32_t &endS, int32_t &endT)
+                                          const int32_t *__restrict__ cols,
+                                          const int32_t *keys, const double *__restrict__ vals, int lgb,
+                                          int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b, uint64_t k,
+                                          uint32_t key0, uint32_t key1, double &accS, double &accT,
+                                          int32_t &endS, int32_t &endT)
 {
     const uint32_t bmask = (1u << lgb) - 1u;
     const uint32_t c3S = (b << 29) | (0u << 28) | (uint32_t)(k >> 32);
@@ -616,30 +622,9 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
     uint2 RS = __ldg(rec + s), RT = __ldg(rec + t);   // {offset, degree} of the current nodes
     int32_t vS = s, vT = t;
     double aS = 0.0, aT = 0.0;
-    // stage-2 state (entry load in flight) and stage-1 state (fingerprint word in flight)
-    Probe pS2 = {0, 0, 0, 1, {0, 0}}, pT2 = {0, 0, 0, 1, {0, 0}};
-    uint2 FS = {0, 0}, FT = {0, 0};
+    double pvS = 0.0, pvT = 0.0;        // pending hit values (added one step later)
+    int4 kS0, kS1, kT0, kT1;            // bucket keys of the current nodes
     U4 rS = {0, 0, 0, 0}, rT = {0, 0, 0, 0};
-    auto finish = [&](Probe &P, double &acc) {
-        // stage 3: key check of the speculative entry
-        if (P.match) {
-            if ((int32_t)(uint32_t)(unsigned long long)P.e.x == P.v) acc += __longlong_as_double(P.e.y);
-            else acc += ylookup_slow<SMEM>(fps, tab, P.bk, bmask, P.v);
-        } else if (!P.empty) {
-            acc += ylookup_slow<SMEM>(fps, tab, (P.bk + 1) & bmask, bmask, P.v);
-        }
-    };
-    auto stage2 = [&](Probe &P, int32_t v, uint2 F) {
-        P.v = v;
-        P.bk = ybucket(v, lgb);
-        const uint32_t f4 = (uint32_t)yfinger(v) * 0x01010101u;
-        P.match = fp_mask(F, f4);
-        P.empty = fp_mask(F, 0u);
-        if (P.match) {
-            const int j = __ffs(P.match) - 1;
-            P.e = __ldg(reinterpret_cast<const longlong2 *>(tab + (size_t)P.bk * YB + j));
-        }
-    };
     for (int32_t j = 1; j <= lf; j++) {
         uint64_t r64S, r64T;
         if (j & 1) {
@@ -660,14 +645,19 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
             AS.x = (uint32_t)__ldg(cols + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
             AT.x = (uint32_t)__ldg(cols + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
         }
-        // probe pipeline: finish step j-2, start entry load of step j-1
-        if (j > 2) {
-            finish(pS2, aS);
-            finish(pT2, aT);
-        }
         if (j > 1) {
-            stage2(pS2, vS, FS);
-            stage2(pT2, vT, FT);
+            aS += pvS;
+            aT += pvT;
+            bool eS, eT;
+            const uint32_t bS = ybucket(vS, lgb), bT = ybucket(vT, lgb);
+            const int mS = bucket_match(kS0, kS1, vS, &eS);
+            const int mT = bucket_match(kT0, kT1, vT, &eT);
+            pvS = 0.0;
+            pvT = 0.0;
+            if (mS >= 0) pvS = __ldg(vals + (size_t)bS * YB + mS);
+            else if (!eS) aS += probe_rest<SMEM>(keys, vals, bS, bmask, vS);
+            if (mT >= 0) pvT = __ldg(vals + (size_t)bT * YB + mT);
+            else if (!eT) aT += probe_rest<SMEM>(keys, vals, bT, bmask, vT);
         }
         vS = (int32_t)AS.x;
         vT = (int32_t)AT.x;
@@ -678,19 +668,21 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
             RS = __ldg(rec + vS);
             RT = __ldg(rec + vT);
         }
-        FS = load_fp<SMEM>(fps, ybucket(vS, lgb));
-        FT = load_fp<SMEM>(fps, ybucket(vT, lgb));
+        load_bucket<SMEM>(keys, ybucket(vS, lgb), kS0, kS1);
+        load_bucket<SMEM>(keys, ybucket(vT, lgb), kT0, kT1);
     }
-    // drain the pipeline in step order
-    if (lf > 1) {
-        finish(pS2, aS);
-        finish(pT2, aT);
-    }
+    // resolve the last step
+    aS += pvS;
+    aT += pvT;
     if (lf > 0) {
-        stage2(pS2, vS, FS);
-        stage2(pT2, vT, FT);
-        finish(pS2, aS);
-        finish(pT2, aT);
+        bool eS, eT;
+        const uint32_t bS = ybucket(vS, lgb), bT = ybucket(vT, lgb);
+        const int mS = bucket_match(kS0, kS1, vS, &eS);
+        const int mT = bucket_match(kT0, kT1, vT, &eT);
+        if (mS >= 0) aS += __ldg(vals + (size_t)bS * YB + mS);
+        else if (!eS) aS += probe_rest<SMEM>(keys, vals, bS, bmask, vS);
+        if (mT >= 0) aT += __ldg(vals + (size_t)bT * YB + mT);
+        else if (!eT) aT += probe_rest<SMEM>(keys, vals, bT, bmask, vT);
     }
     accS = aS;
     accT = aT;
@@ -699,18 +691,18 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
 }
 
 // K6: warp = one chunk of 32 walk pairs of one query (chunks of all AMC queries are laid out
-// query after query, queries ordered by descending ell_f).  The CTA stages the y-table
-// fingerprints of its (<= 8) queries in shared memory when they fit; otherwise the warp reads
-// them from global memory.  Each warp writes the canonical partial {sum Z, sum Z^2, checksum}
-// of its chunk (sums over the chunk's lanes in a fixed tree: independent of batch layout).
+// query after query, queries ordered by descending ell_f).  The CTA stages the y-table keys of
+// its (<= 8) queries in shared memory when they fit; otherwise the warp probes global memory.
+// Each warp writes the canonical partial {sum Z, sum Z^2, checksum} of its chunk.
 template <bool ARC>
 __global__ void __launch_bounds__(WALK_THREADS, 4)
 k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
         const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
-        const int32_t *__restrict__ cols, const YEntry *__restrict__ tab_pool, const uint8_t *__restrict__ fp_pool,
-        int b, uint32_t key0, uint32_t key1, int64_t qbase, TilePart *__restrict__ parts)
+        const int32_t *__restrict__ cols,
+        const int32_t *__restrict__ ykeys, const double *__restrict__ yvals, int b, uint32_t key0, uint32_t key1,
+        int64_t qbase, TilePart *__restrict__ parts)
 {
-    __shared__ __align__(16) uint8_t sm_fp[WALK_SMEM_FP];
+    __shared__ __align__(32) int32_t sm_keys[WALK_SMEM_SLOTS];
     __shared__ int32_t s_qi[WALK_WARPS];
     __shared__ int32_t s_soff[WALK_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -727,7 +719,7 @@ k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const in
             if (qi < 0) { s_soff[w] = -1; continue; }
             if (w > 0 && s_qi[w - 1] == qi) { s_soff[w] = s_soff[w - 1]; continue; }
             const int32_t cap = 1 << qs[amc[qi]].ylog2;
-            if (used + cap <= WALK_SMEM_FP) { s_soff[w] = used; used += cap; }
+            if (used + cap <= WALK_SMEM_SLOTS) { s_soff[w] = used; used += cap; }
             else s_soff[w] = -1;
         }
     }
@@ -736,9 +728,9 @@ k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const in
         if (s_soff[w] < 0 || (w > 0 && s_qi[w - 1] == s_qi[w])) continue;
         const QState &Q = qs[amc[s_qi[w]]];
         const int32_t cap = 1 << Q.ylog2;
-        const uint2 *src = reinterpret_cast<const uint2 *>(fp_pool + Q.yoff);
-        uint2 *dst = reinterpret_cast<uint2 *>(sm_fp + s_soff[w]);
-        for (int32_t e = threadIdx.x; e < cap / 8; e += WALK_THREADS) dst[e] = __ldg(src + e);
+        const int4 *src = reinterpret_cast<const int4 *>(ykeys + Q.yoff);
+        int4 *dst = reinterpret_cast<int4 *>(sm_keys + s_soff[w]);
+        for (int32_t e = threadIdx.x; e < cap / 4; e += WALK_THREADS) dst[e] = __ldg(src + e);
     }
     __syncthreads();
     if (!wvalid) return;
@@ -751,16 +743,16 @@ k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const in
     const bool active = k < (uint64_t)eta;
     const uint32_t q = (uint32_t)(qbase + qi);
     const int lgb = Q.ylog2 - YB_LOG;
-    const YEntry *tab = tab_pool + Q.yoff;
+    const double *vals = yvals + Q.yoff;
     double aS = 0.0, aT = 0.0;
     int32_t eS = 0, eT = 0;
     if (active) {
         if (s_soff[warp] >= 0)
-            walk_pair<true, ARC>(rec, arcs, cols, sm_fp + s_soff[warp], tab, lgb, Q.s, Q.t, Q.st.ell_f, q,
-                                 (uint32_t)b, k, key0, key1, aS, aT, eS, eT);
+            walk_pair<true, ARC>(rec, arcs, cols, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k,
+                            key0, key1, aS, aT, eS, eT);
         else
-            walk_pair<false, ARC>(rec, arcs, cols, fp_pool + Q.yoff, tab, lgb, Q.s, Q.t, Q.st.ell_f, q,
-                                  (uint32_t)b, k, key0, key1, aS, aT, eS, eT);
+            walk_pair<false, ARC>(rec, arcs, cols, ykeys + Q.yoff, vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k, key0,
+                             key1, aS, aT, eS, eT);
     }
     const double z = active ? aS - aT : 0.0;
     double s1 = z, s2 = z * z;
@@ -909,7 +901,7 @@ void Workspace::release()
 {
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2, &head,
-                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals, &ytmp, &yfp};
+                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals, &ytmp};
     for (DevBuf *b : all) b->release();
     if (host_pinned) cudaFreeHost(host_pinned);
     host_pinned = nullptr;
@@ -1008,20 +1000,21 @@ int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, c
     if (rc) return rc;
     const int64_t Y = c.hp[0];
     if (Y == 0) return ER_OK;
-    ENSURE(ws.ypool, sizeof(YEntry) * (size_t)(pool_used + Y), true);
-    ENSURE(ws.yfp, (size_t)(pool_used + Y), true);
+    ENSURE(ws.ypool, sizeof(int32_t) * (size_t)(pool_used + Y), true);
+    ENSURE(ws.yvals, sizeof(double) * (size_t)(pool_used + Y), true);
     ENSURE(ws.ytmp, sizeof(double) * (size_t)Y, false);
     (void)segoff;
-    k_yfill<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, ws.ypool.as<YEntry>() + pool_used, ws.yfp.as<uint8_t>() + pool_used,
-                                                  ws.ytmp.as<double>());
+    k_yfill<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, ws.ypool.as<int32_t>() + pool_used,
+                                                  ws.yvals.as<double>() + pool_used, ws.ytmp.as<double>());
     LAUNCHED(c.g);
     k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, ycap, yincl, pool_used, ws.qs.as<QState>());
     LAUNCHED(c.g);
     k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, act, ycap, ws.qs.as<QState>(),
-                                                      ws.ypool.as<YEntry>(), ws.yfp.as<uint8_t>(),
+                                                      ws.ypool.as<int32_t>(), ws.yvals.as<double>(),
                                                       ws.ytmp.as<double>(), pool_used);
     LAUNCHED(c.g);
-    k_yfinal<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, pool_used, ws.ypool.as<YEntry>(), ws.ytmp.as<double>());
+    k_yfinal<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, pool_used, na, act, ycap, yincl, ws.qs.as<QState>(),
+                                                  ws.ypool.as<int32_t>(), ws.yvals.as<double>(), ws.ytmp.as<double>());
     LAUNCHED(c.g);
     pool_used += Y;
     return ER_OK;
@@ -1346,11 +1339,11 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             if (g->d_arcs)
                 k_walks<true><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(
                     NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_arcs, g->d_cols,
-                    ws.ypool.as<YEntry>(), ws.yfp.as<uint8_t>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>());
+                    ws.ypool.as<int32_t>(), ws.yvals.as<double>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>());
             else
                 k_walks<false><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(
                     NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_arcs, g->d_cols,
-                    ws.ypool.as<YEntry>(), ws.yfp.as<uint8_t>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>());
+                    ws.ypool.as<int32_t>(), ws.yvals.as<double>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>());
             LAUNCHED(g);
             if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk + 1], st));
             k_amc_reduce<<<blocks_for(na * 32, 256), 256, 0, st>>>(
