@@ -220,19 +220,34 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         for (int64_t v = 0; v < n; v++) rec[v] = make_uint2((uint32_t)offsets[v], (uint32_t)(offsets[v + 1] - offsets[v]));
         e = cudaMalloc(&g->d_rec, sizeof(uint2) * n);
         if (e == cudaSuccess) e = cudaMemcpy(g->d_rec, rec.data(), sizeof(uint2) * n, cudaMemcpyHostToDevice);
-        // walk layout: {off, d} node records + columns while they stay well inside L2;
-        // 16-byte arc records (one random access per step) once the graph is DRAM-resident anyway
+        // Walk layout: packed 8-byte arc records {u | off(u) | d(u)} when the
+        // three fields fit 64 bits and the array stays inside L2 (one random access per step);
+        // else 16-byte arc records when the graph is DRAM-resident anyway; else node records
+        // {off, d} + columns.
         int l2 = 0;
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
-        const double foot = 4.0 * (double)g->nnz + 8.0 * (double)n;
-        bool use_arcs = foot > 0.5 * (double)l2;
+        auto bits = [](uint64_t x) { int b = 1; while (b < 64 && (1ull << b) <= x) b++; return b; };
+        const int bu = bits((uint64_t)(n - 1)), bo = bits((uint64_t)g->nnz), bd = bits((uint64_t)md);
+        const bool packable = bu + bo + bd <= 64;
+        const double cols_foot = 4.0 * (double)g->nnz + 8.0 * (double)n;
+        const double pack_foot = 8.0 * (double)g->nnz;
+        int layout = 0;  // 0 cols, 1 arcs16, 2 packed
+        if (packable && pack_foot <= 0.75 * (double)l2) layout = 2;
+        else if (cols_foot > 0.5 * (double)l2) layout = 1;
         if (const char *env = getenv("GEER_WALK_LAYOUT")) {
-            if (!strcmp(env, "arcs")) use_arcs = true;
-            if (!strcmp(env, "cols")) use_arcs = false;
+            if (!strcmp(env, "arcs")) layout = 1;
+            if (!strcmp(env, "cols")) layout = 0;
+            if (!strcmp(env, "packed") && packable) layout = 2;
         }
-        if (use_arcs && e == cudaSuccess) {
+        g->pack.bo = bo;
+        g->pack.bd = bd;
+        if (layout == 1 && e == cudaSuccess) {
             e = cudaMalloc(&g->d_arcs, sizeof(uint4) * std::max<int64_t>(g->nnz, 1));
             if (e == cudaSuccess) e = geer::build_arcs(g);
+        }
+        if (layout == 2 && e == cudaSuccess) {
+            e = cudaMalloc(&g->d_parcs, sizeof(unsigned long long) * std::max<int64_t>(g->nnz, 1));
+            if (e == cudaSuccess) e = geer::build_parcs(g);
         }
     }
     if (e != cudaSuccess) {
@@ -257,6 +272,7 @@ void er_graph_destroy(er_graph *g)
         if (g->d_cols) cudaFree(g->d_cols);
         if (g->d_rec) cudaFree(g->d_rec);
         if (g->d_arcs) cudaFree(g->d_arcs);
+        if (g->d_parcs) cudaFree(g->d_parcs);
         if (g->d_steps) cudaFree(g->d_steps);
         if (g->stream) cudaStreamDestroy(g->stream);
         cudaSetDevice(cur);

@@ -28,6 +28,24 @@ struct QState {
 };
 
 
+// 64-bit packed arc record: u | offset(u) | degree(u) in bu + bo + bd <= 64 bits.
+struct PackSpec {
+    int bo = 0, bd = 0;  // bit widths of offset and degree (u takes the high bits)
+    __host__ __device__ unsigned long long pack(uint32_t u, uint32_t off, uint32_t deg) const
+    {
+        return ((unsigned long long)u << (bo + bd)) | ((unsigned long long)off << bd) | (unsigned long long)deg;
+    }
+    __host__ __device__ uint4 unpack(unsigned long long a) const
+    {
+        uint4 r;
+        r.z = (uint32_t)(a & ((1ull << bd) - 1));
+        r.y = (uint32_t)((a >> bd) & ((1ull << bo) - 1));
+        r.x = (uint32_t)(a >> (bo + bd));
+        r.w = 0;
+        return r;
+    }
+};
+
 // Per-segment statistics of an SMM iterate (segment = one side of one query).
 struct SegStat {
     int64_t vol;           // sum of d(v) over the support (Eq. 15 left side)
@@ -95,6 +113,8 @@ struct er_graph {
     int32_t *d_cols = nullptr;
     uint2 *d_rec = nullptr;       // {offset, degree} per node (offsets < 2^32)
     uint4 *d_arcs = nullptr;      // {u, offset(u), degree(u), 0} per arc, in CSR order (walk chain)
+    unsigned long long *d_parcs = nullptr;  // packed 8-byte arc records (when they fit 64 bits)
+    geer::PackSpec pack;
     int32_t max_deg = 0;
     bool rows_sorted = false;
     int query_block = 0;  // ER_OK, or the validation code that forbids queries (ER_CREATE_SPMM_ONLY)
@@ -121,5 +141,6 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
 int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st);
 int run_estimate_lambda(er_graph *g, int iters, double *lambda_out);
 cudaError_t build_arcs(er_graph *g);
+cudaError_t build_parcs(er_graph *g);
 
 }  // namespace geer

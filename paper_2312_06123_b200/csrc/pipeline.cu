@@ -421,9 +421,9 @@ __global__ void k_yfill(int64_t Y, int32_t *__restrict__ keys, double *__restric
 }
 
 // K5a: insert every support node of a leaving query into its y-table (find-or-insert; the node
-// may come from both sides) and record s*(v) (side 0) or t*(v) (side 1) at its slot.
-// Bucketed open addressing: 8 int32 keys per 32-byte bucket, buckets probed linearly, slots in
-// order inside a bucket.
+// may come from both sides).  Side 0 stores s*(v)/d(s) at the slot, side 1 stores t*(v)/d(t) in a
+// scratch array.  Bucketed open addressing: 8 int32 keys per 32-byte bucket, buckets probed
+// linearly, slots in order inside a bucket, claimed by CAS.
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                           const int32_t *__restrict__ id, const double *__restrict__ val,
                           const int32_t *__restrict__ act, const int64_t *__restrict__ ycap,
@@ -442,13 +442,18 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
     const uint32_t bmask = (1u << lgb) - 1u;
     uint32_t bk = ybucket(v, lgb);
     while (true) {
+        const int4 *bp = reinterpret_cast<const int4 *>(keys + bk * YB);
+        int4 A, B;
+        asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(A.x), "=r"(A.y), "=r"(A.z), "=r"(A.w) : "l"(bp));
+        asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(B.x), "=r"(B.y), "=r"(B.z), "=r"(B.w) : "l"(bp + 1));
+        const int32_t kk[YB] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
         for (int j = 0; j < YB; j++) {
             const uint32_t slot = bk * YB + j;
-            int32_t k = keys[slot];
+            int32_t k = kk[j];
             if (k == -1) k = atomicCAS(&keys[slot], -1, v);
             if (k == -1 || k == v) {
-                if (g & 1) yt[Q.yoff - tbase + slot] = val[e];
-                else ys[Q.yoff + slot] = val[e];
+                if (g & 1) yt[Q.yoff - tbase + slot] = val[e] / (double)Q.dt;
+                else ys[Q.yoff + slot] = val[e] / (double)Q.ds;
                 return;
             }
         }
@@ -456,26 +461,13 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
     }
 }
 
-// K5b: y(v) = s*(v)/d(s) - t*(v)/d(t) at every occupied slot of the new tables (Alg. 1 L7 with
-// s = s*, t = t*); a side the node is not on contributes 0.0 (its value stayed 0).
-__global__ void k_yfinal(int64_t Y, int64_t tbase, int32_t na, const int32_t *__restrict__ act,
-                         const int64_t *__restrict__ ycap, const int64_t *__restrict__ yincl,
-                         const QState *__restrict__ qs, const int32_t *__restrict__ ykeys, double *__restrict__ ys,
-                         const double *__restrict__ yt)
+// K5b: y(v) = s*(v)/d(s) - t*(v)/d(t) at every slot of the new tables (Alg. 1 L7 with s = s*,
+// t = t*); a side the node is not on contributes 0.0 (its term stayed 0; empty slots stay 0).
+__global__ void k_yfinal(int64_t Y, int64_t tbase, double *__restrict__ ys, const double *__restrict__ yt)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= Y) return;
-    const int64_t slot = tbase + j;
-    if (ykeys[slot] < 0) return;
-    int32_t lo = 0, hi = na - 1;  // owner: smallest i with yincl[i] > j
-    while (lo < hi) {
-        const int32_t mid = (lo + hi) >> 1;
-        if (yincl[mid] > j) hi = mid;
-        else lo = mid + 1;
-    }
-    const QState &Q = qs[act[lo]];
-    const double a = ys[slot], b = yt[j];
-    ys[slot] = a / (double)Q.ds - b / (double)Q.dt;
+    ys[tbase + j] = ys[tbase + j] - yt[j];
 }
 
 // Continuing segments: new lengths (for the compaction scan).
@@ -608,9 +600,10 @@ __device__ __forceinline__ double probe_rest(const int32_t *keys, const double *
 // j-1's node, and a hit's value load is consumed one step later, so only the arc chain is
 // serial.  Arc records {u, off(u), d(u), -} make the chain one 16-byte load per step.
 // y values are added in step order (R9, R13).
-template <bool SMEM, bool ARC>
+template <bool SMEM, int ARC>
 __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
-                                          const int32_t *__restrict__ cols,
+                                          const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs,
+                                          PackSpec pk,
                                           const int32_t *keys, const double *__restrict__ vals, int lgb,
                                           int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b, uint64_t k,
                                           uint32_t key0, uint32_t key1, double &accS, double &accT,
@@ -638,9 +631,14 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
             r64T = ((uint64_t)rT.w << 32) | rT.z;
         }
         uint4 AS, AT;
-        if (ARC) {
+        if (ARC == 1) {
             AS = __ldg(arcs + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
             AT = __ldg(arcs + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
+        } else if (ARC == 2) {
+            const unsigned long long PS = __ldg(parcs + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
+            const unsigned long long PT = __ldg(parcs + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
+            AS = pk.unpack(PS);
+            AT = pk.unpack(PT);
         } else {
             AS.x = (uint32_t)__ldg(cols + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
             AT.x = (uint32_t)__ldg(cols + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
@@ -694,11 +692,11 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
 // query after query, queries ordered by descending ell_f).  The CTA stages the y-table keys of
 // its (<= 8) queries in shared memory when they fit; otherwise the warp probes global memory.
 // Each warp writes the canonical partial {sum Z, sum Z^2, checksum} of its chunk.
-template <bool ARC>
+template <int ARC>
 __global__ void __launch_bounds__(WALK_THREADS, 4)
 k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
         const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
-        const int32_t *__restrict__ cols,
+        const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs, PackSpec pk,
         const int32_t *__restrict__ ykeys, const double *__restrict__ yvals, int b, uint32_t key0, uint32_t key1,
         int64_t qbase, TilePart *__restrict__ parts)
 {
@@ -748,10 +746,10 @@ k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const in
     int32_t eS = 0, eT = 0;
     if (active) {
         if (s_soff[warp] >= 0)
-            walk_pair<true, ARC>(rec, arcs, cols, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k,
+            walk_pair<true, ARC>(rec, arcs, cols, parcs, pk, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k,
                             key0, key1, aS, aT, eS, eT);
         else
-            walk_pair<false, ARC>(rec, arcs, cols, ykeys + Q.yoff, vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k, key0,
+            walk_pair<false, ARC>(rec, arcs, cols, parcs, pk, ykeys + Q.yoff, vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k, key0,
                              key1, aS, aT, eS, eT);
     }
     const double z = active ? aS - aT : 0.0;
@@ -1013,8 +1011,7 @@ int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, c
                                                       ws.ypool.as<int32_t>(), ws.yvals.as<double>(),
                                                       ws.ytmp.as<double>(), pool_used);
     LAUNCHED(c.g);
-    k_yfinal<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, pool_used, na, act, ycap, yincl, ws.qs.as<QState>(),
-                                                  ws.ypool.as<int32_t>(), ws.yvals.as<double>(), ws.ytmp.as<double>());
+    k_yfinal<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, pool_used, ws.yvals.as<double>(), ws.ytmp.as<double>());
     LAUNCHED(c.g);
     pool_used += Y;
     return ER_OK;
@@ -1336,14 +1333,16 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             const int64_t NC = c.hp[0];
             ENSURE(ws.parts, sizeof(TilePart) * NC, false);
             if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk], st));
-            if (g->d_arcs)
-                k_walks<true><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(
-                    NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_arcs, g->d_cols,
-                    ws.ypool.as<int32_t>(), ws.yvals.as<double>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>());
+#define WALK_ARGS                                                                                                \
+    NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack,          \
+        ws.ypool.as<int32_t>(), ws.yvals.as<double>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>()
+            if (g->d_parcs)
+                k_walks<2><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(WALK_ARGS);
+            else if (g->d_arcs)
+                k_walks<1><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(WALK_ARGS);
             else
-                k_walks<false><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(
-                    NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_arcs, g->d_cols,
-                    ws.ypool.as<int32_t>(), ws.yvals.as<double>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>());
+                k_walks<0><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(WALK_ARGS);
+#undef WALK_ARGS
             LAUNCHED(g);
             if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk + 1], st));
             k_amc_reduce<<<blocks_for(na * 32, 256), 256, 0, st>>>(
@@ -1412,6 +1411,25 @@ __global__ void k_build_arcs(int64_t nnz, const int32_t *__restrict__ cols, cons
     const int32_t u = cols[e];
     const uint2 r = rec[u];
     arcs[e] = make_uint4((uint32_t)u, r.x, r.y, 0u);
+}
+
+__global__ void k_build_parcs(int64_t nnz, const int32_t *__restrict__ cols, const uint2 *__restrict__ rec,
+                              PackSpec pk, unsigned long long *__restrict__ parcs)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    const int32_t u = cols[e];
+    const uint2 r = rec[u];
+    parcs[e] = pk.pack((uint32_t)u, r.x, r.y);
+}
+
+cudaError_t build_parcs(er_graph *g)
+{
+    k_build_parcs<<<blocks_for(g->nnz, 256), 256>>>(g->nnz, g->d_cols, g->d_rec, g->pack, g->d_parcs);
+    g->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    return e;
 }
 
 cudaError_t build_arcs(er_graph *g)

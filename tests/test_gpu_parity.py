@@ -243,3 +243,28 @@ def test_unsorted_rows_parity(geer, tiny):
         r, st, ro, so = run_both(geer, h, g, pairs, eps)
         compare(g, pairs, r, st, ro, so, sorted_adj=False)
     geer.er_graph_destroy(h)
+
+
+@pytest.mark.parametrize("graph", ["tiny", "rmat20"])
+def test_walk_layouts_byte_identical(geer, tiny, rmat20, graph):
+    # node records + columns, 16-byte arc records and packed 8-byte arc records are three
+    # encodings of the same CSR: every output bit must agree
+    import os
+    if graph == "tiny":
+        g, pairs = tiny
+        pairs = pairs
+    else:
+        g, pairs, _, _ = rmat20
+        pairs = pairs[::20]
+    outs = {}
+    for lay in ("cols", "arcs", "packed"):
+        os.environ["GEER_WALK_LAYOUT"] = lay
+        try:
+            h = geer.er_graph_create(g.n, g.offsets, g.cols)
+        finally:
+            del os.environ["GEER_WALK_LAYOUT"]
+        geer.er_graph_set_lambda(h, g.lam)
+        r, st = geer.er_query_batch_ex(h, pairs, 0.1, stats=True)
+        outs[lay] = (r.tobytes(), st.tobytes())
+        geer.er_graph_destroy(h)
+    assert outs["cols"] == outs["arcs"] == outs["packed"]
