@@ -201,6 +201,15 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
     }
     cudaError_t e = cudaGetDevice(&g->device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->amc_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+        // keep stream-ordered allocations (per-batch y-tables, AMC group buffers) cached
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     g->n = n;
     g->nnz = offsets[n];
     g->rows_sorted = sorted;
@@ -274,7 +283,9 @@ void er_graph_destroy(er_graph *g)
         if (g->d_arcs) cudaFree(g->d_arcs);
         if (g->d_parcs) cudaFree(g->d_parcs);
         if (g->d_steps) cudaFree(g->d_steps);
+        if (g->amc_stream) cudaStreamSynchronize(g->amc_stream);
         if (g->stream) cudaStreamDestroy(g->stream);
+        if (g->amc_stream) cudaStreamDestroy(g->amc_stream);
         cudaSetDevice(cur);
     }
     delete g;

@@ -87,7 +87,7 @@ struct DevBuf {
 
 struct Workspace {
     DevBuf qs, pairs, out, stats;
-    DevBuf act, act2, cont, idx;                    // active lists / flags / scan outputs
+    DevBuf act, act2, cont, idx, cont2, idx2;       // active lists / flags / scan outputs
     DevBuf fr_id, fr_val, fr_seg, fr_off;           // current frontier
     DevBuf nf_id, nf_val, nf_seg, nf_off;           // next frontier
     DevBuf ent_off;                                 // emission offsets per frontier entry
@@ -122,6 +122,7 @@ struct er_graph {
     bool lambda_set = false;
     int nbits = 1;
     cudaStream_t stream = nullptr;
+    cudaStream_t amc_stream = nullptr;  // AMC groups overlap the SMM head
     std::mutex mu;
     int64_t launches = 0;
     bool profiling = false;

@@ -522,7 +522,8 @@ __global__ void k_nchunks(int32_t na, const int32_t *__restrict__ amc, const QSt
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
-    nch[i] = ((qs[amc[i]].st.eta0 << b) + 31) / 32;
+    const QState &Q = qs[amc[i]];
+    nch[i] = Q.phase == PH_AMC ? ((Q.st.eta0 << b) + 31) / 32 : 0;
 }
 
 __global__ void k_lf_key(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs,
@@ -694,7 +695,7 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
 // Each warp writes the canonical partial {sum Z, sum Z^2, checksum} of its chunk.
 template <int ARC>
 __global__ void __launch_bounds__(WALK_THREADS, 4)
-k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
+k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
         const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
         const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs, PackSpec pk,
         const int32_t *__restrict__ ykeys, const double *__restrict__ yvals, int b, uint32_t key0, uint32_t key1,
@@ -704,70 +705,75 @@ k_walks(int64_t nchunks, int32_t na, const int64_t *__restrict__ cincl, const in
     __shared__ int32_t s_qi[WALK_WARPS];
     __shared__ int32_t s_soff[WALK_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t chunk = (int64_t)blockIdx.x * WALK_WARPS + warp;
-    const bool wvalid = chunk < nchunks;
-    const int32_t i = wvalid ? find_chunk_query(cincl, na, chunk) : -1;
-    if (lane == 0) s_qi[warp] = i;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        // prefix-fit staging plan over the distinct queries of this CTA (consecutive warps)
-        int32_t used = 0;
-        for (int w = 0; w < WALK_WARPS; w++) {
-            const int32_t qi = s_qi[w];
-            if (qi < 0) { s_soff[w] = -1; continue; }
-            if (w > 0 && s_qi[w - 1] == qi) { s_soff[w] = s_soff[w - 1]; continue; }
-            const int32_t cap = 1 << qs[amc[qi]].ylog2;
-            if (used + cap <= WALK_SMEM_SLOTS) { s_soff[w] = used; used += cap; }
-            else s_soff[w] = -1;
+    const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
+    // persistent: CTA-tiles of WALK_WARPS consecutive chunks, round-robin over the grid
+    for (int64_t tile = blockIdx.x; tile * WALK_WARPS < nchunks; tile += gridDim.x) {
+        const int64_t chunk = tile * WALK_WARPS + warp;
+        const bool wvalid = chunk < nchunks;
+        const int32_t i = wvalid ? find_chunk_query(cincl, na, chunk) : -1;
+        if (lane == 0) s_qi[warp] = i;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // prefix-fit staging plan over the distinct queries of this tile (consecutive warps)
+            int32_t used = 0;
+            for (int w = 0; w < WALK_WARPS; w++) {
+                const int32_t qi = s_qi[w];
+                if (qi < 0) { s_soff[w] = -1; continue; }
+                if (w > 0 && s_qi[w - 1] == qi) { s_soff[w] = s_soff[w - 1]; continue; }
+                const int32_t cap = 1 << qs[amc[qi]].ylog2;
+                if (used + cap <= WALK_SMEM_SLOTS) { s_soff[w] = used; used += cap; }
+                else s_soff[w] = -1;
+            }
         }
-    }
-    __syncthreads();
-    for (int w = 0; w < WALK_WARPS; w++) {
-        if (s_soff[w] < 0 || (w > 0 && s_qi[w - 1] == s_qi[w])) continue;
-        const QState &Q = qs[amc[s_qi[w]]];
-        const int32_t cap = 1 << Q.ylog2;
-        const int4 *src = reinterpret_cast<const int4 *>(ykeys + Q.yoff);
-        int4 *dst = reinterpret_cast<int4 *>(sm_keys + s_soff[w]);
-        for (int32_t e = threadIdx.x; e < cap / 4; e += WALK_THREADS) dst[e] = __ldg(src + e);
-    }
-    __syncthreads();
-    if (!wvalid) return;
-
-    const int32_t qi = amc[i];
-    const QState &Q = qs[qi];
-    const int64_t c0 = i == 0 ? 0 : cincl[i - 1];
-    const uint64_t k = (uint64_t)(chunk - c0) * 32u + (uint64_t)lane;
-    const int64_t eta = Q.st.eta0 << b;
-    const bool active = k < (uint64_t)eta;
-    const uint32_t q = (uint32_t)(qbase + qi);
-    const int lgb = Q.ylog2 - YB_LOG;
-    const double *vals = yvals + Q.yoff;
-    double aS = 0.0, aT = 0.0;
-    int32_t eS = 0, eT = 0;
-    if (active) {
-        if (s_soff[warp] >= 0)
-            walk_pair<true, ARC>(rec, arcs, cols, parcs, pk, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k,
-                            key0, key1, aS, aT, eS, eT);
-        else
-            walk_pair<false, ARC>(rec, arcs, cols, parcs, pk, ykeys + Q.yoff, vals, lgb, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, k, key0,
-                             key1, aS, aT, eS, eT);
-    }
-    const double z = active ? aS - aT : 0.0;
-    double s1 = z, s2 = z * z;
-    uint64_t ck = active ? walk_hash(q, (uint32_t)b, 0u, k, eS) + walk_hash(q, (uint32_t)b, 1u, k, eT) : 0ull;
+        __syncthreads();
+        for (int w = 0; w < WALK_WARPS; w++) {
+            if (s_soff[w] < 0 || (w > 0 && s_qi[w - 1] == s_qi[w])) continue;
+            const QState &Q = qs[amc[s_qi[w]]];
+            const int32_t cap = 1 << Q.ylog2;
+            const int4 *src = reinterpret_cast<const int4 *>(ykeys + Q.yoff);
+            int4 *dst = reinterpret_cast<int4 *>(sm_keys + s_soff[w]);
+            for (int32_t e = threadIdx.x; e < cap / 4; e += WALK_THREADS) dst[e] = __ldg(src + e);
+        }
+        __syncthreads();
+        if (wvalid) {
+            const int32_t qi = amc[i];
+            const QState &Q = qs[qi];
+            const int64_t c0 = i == 0 ? 0 : cincl[i - 1];
+            const uint64_t k = (uint64_t)(chunk - c0) * 32u + (uint64_t)lane;
+            const int64_t eta = Q.st.eta0 << b;
+            const bool active = k < (uint64_t)eta;
+            const uint32_t q = (uint32_t)(qbase + qi);
+            const int lgb = Q.ylog2 - YB_LOG;
+            const double *vals = yvals + Q.yoff;
+            double aS = 0.0, aT = 0.0;
+            int32_t eS = 0, eT = 0;
+            if (active) {
+                if (s_soff[warp] >= 0)
+                    walk_pair<true, ARC>(rec, arcs, cols, parcs, pk, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t,
+                                         Q.st.ell_f, q, (uint32_t)b, k, key0, key1, aS, aT, eS, eT);
+                else
+                    walk_pair<false, ARC>(rec, arcs, cols, parcs, pk, ykeys + Q.yoff, vals, lgb, Q.s, Q.t,
+                                          Q.st.ell_f, q, (uint32_t)b, k, key0, key1, aS, aT, eS, eT);
+            }
+            const double z = active ? aS - aT : 0.0;
+            double s1 = z, s2 = z * z;
+            uint64_t ck = active ? walk_hash(q, (uint32_t)b, 0u, k, eS) + walk_hash(q, (uint32_t)b, 1u, k, eT) : 0ull;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-        ck += __shfl_xor_sync(0xffffffffu, ck, o);
-    }
-    if (lane == 0) {
-        TilePart tp;
-        tp.s1 = s1;
-        tp.s2 = s2;
-        tp.ck = ck;
-        tp.pad = 0;
-        parts[chunk] = tp;
+            for (int o = 16; o > 0; o >>= 1) {
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+                ck += __shfl_xor_sync(0xffffffffu, ck, o);
+            }
+            if (lane == 0) {
+                TilePart tp;
+                tp.s1 = s1;
+                tp.s2 = s2;
+                tp.ck = ck;
+                tp.pad = 0;
+                parts[chunk] = tp;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -780,6 +786,7 @@ __global__ void k_amc_reduce(int32_t na, const int32_t *__restrict__ amc, const 
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= na) return;
     const int64_t t0 = i == 0 ? 0 : tile_incl[i - 1], t1 = tile_incl[i];
+    if (t1 == t0) return;   // stopped in an earlier batch
     double s1 = 0.0, s2 = 0.0;
     uint64_t ck = 0;
     for (int64_t t = t0 + lane; t < t1; t += 32) {
@@ -812,7 +819,27 @@ __global__ void k_amc_reduce(int32_t na, const int32_t *__restrict__ amc, const 
     if (fabs(f - P.eps / 2.0) <= 1e-12 * P.eps) Q.st.tie_flags |= 4u;
     const bool stop = f <= P.eps / 2.0 || b == P.tau - 1;
     if (stop) Q.phase = PH_DONE;
-    cont[i] = stop ? 0 : 1;
+    if (cont) cont[i] = stop ? 0 : 1;
+}
+
+// Queries of an active list that leave the SMM head for AMC now (cont == 0, phase AMC).
+__global__ void k_flag_leave(int32_t na, const int32_t *__restrict__ act, const QState *__restrict__ qs,
+                             const int32_t *__restrict__ cont, int32_t *__restrict__ flag)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    flag[i] = ((cont == nullptr || !cont[i]) && qs[act[i]].phase == PH_AMC) ? 1 : 0;
+}
+
+// Sum of eta0 over a list (sizes the per-batch partial buffers of an AMC group).
+__global__ void k_sum_eta0(int32_t na, const int32_t *__restrict__ list, const QState *__restrict__ qs,
+                           unsigned long long *__restrict__ out)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long v = i < na ? (unsigned long long)qs[list[i]].st.eta0 : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
 }
 
 // K8: r' = r_f + r_b (Alg. 3 L11); s = t -> 0.
@@ -899,7 +926,7 @@ void Workspace::release()
 {
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2, &head,
-                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals, &ytmp};
+                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals, &ytmp, &cont2, &idx2};
     for (DevBuf *b : all) b->release();
     if (host_pinned) cudaFreeHost(host_pinned);
     host_pinned = nullptr;
@@ -979,14 +1006,17 @@ int select_list(Ctx &c, const int32_t *ids, const int32_t *flag, int32_t n, int3
     return ER_OK;
 }
 
-// Build y-tables for the queries of `act` with ycap > 0 from frontier (segoff,id,val,seg; nF entries,
-// device count dF).  `cont` may be null (all queries of the list leave the head).
+// Build y-tables for the queries of `act` with ycap > 0 from frontier (segoff,id,val,seg; Fmax
+// entries, device count dF or null).  `cont` may be null (all queries of the list leave the
+// head).  The tables live in a fresh stream-ordered allocation (keys + values) returned through
+// *keys / *vals (freed at the end of the batch); QState.yoff is relative to it.
 int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, const int64_t *segoff,
                   const int32_t *id, const double *val, const int32_t *seg, int64_t Fmax, const int64_t *dF,
-                  int64_t &pool_used, const BatchParams &P)
+                  int32_t **keys_out, double **vals_out)
 {
-    (void)P;
     Workspace &ws = c.ws;
+    *keys_out = nullptr;
+    *vals_out = nullptr;
     ENSURE(ws.ycap, sizeof(int64_t) * (na + 1), false);
     ENSURE(ws.yoff, sizeof(int64_t) * (na + 1), false);
     int64_t *ycap = ws.ycap.as<int64_t>(), *yincl = ws.yoff.as<int64_t>();
@@ -998,22 +1028,111 @@ int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, c
     if (rc) return rc;
     const int64_t Y = c.hp[0];
     if (Y == 0) return ER_OK;
-    ENSURE(ws.ypool, sizeof(int32_t) * (size_t)(pool_used + Y), true);
-    ENSURE(ws.yvals, sizeof(double) * (size_t)(pool_used + Y), true);
-    ENSURE(ws.ytmp, sizeof(double) * (size_t)Y, false);
+    int32_t *keys = nullptr;
+    double *vals = nullptr, *ytmp = nullptr;
+    CK(cudaMallocAsync((void **)&keys, sizeof(int32_t) * Y, c.st));
+    CK(cudaMallocAsync((void **)&vals, sizeof(double) * Y, c.st));
+    CK(cudaMallocAsync((void **)&ytmp, sizeof(double) * Y, c.st));
+    k_yfill<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, keys, vals, ytmp);
+    LAUNCHED(c.g);
+    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, ycap, yincl, 0, ws.qs.as<QState>());
+    LAUNCHED(c.g);
     (void)segoff;
-    k_yfill<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, ws.ypool.as<int32_t>() + pool_used,
-                                                  ws.yvals.as<double>() + pool_used, ws.ytmp.as<double>());
+    k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, act, ycap, ws.qs.as<QState>(), keys,
+                                                      vals, ytmp, 0);
     LAUNCHED(c.g);
-    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, ycap, yincl, pool_used, ws.qs.as<QState>());
+    k_yfinal<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, 0, vals, ytmp);
     LAUNCHED(c.g);
-    k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, act, ycap, ws.qs.as<QState>(),
-                                                      ws.ypool.as<int32_t>(), ws.yvals.as<double>(),
-                                                      ws.ytmp.as<double>(), pool_used);
-    LAUNCHED(c.g);
-    k_yfinal<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, pool_used, ws.yvals.as<double>(), ws.ytmp.as<double>());
-    LAUNCHED(c.g);
-    pool_used += Y;
+    CK(cudaFreeAsync(ytmp, c.st));
+    *keys_out = keys;
+    *vals_out = vals;
+    return ER_OK;
+}
+
+// One AMC group: the queries that left the SMM head in the same wave, with their y-tables.
+// Its whole AMC (tau batches) is enqueued on the AMC stream without host synchronisation.
+struct AmcGroup {
+    int32_t na = 0;
+    int32_t *list = nullptr;     // query ids (device), sorted by descending ell_f
+    int32_t *ykeys = nullptr;    // this group's y-table chunk
+    double *yvals = nullptr;
+    unsigned long long eta0_sum = 0;
+};
+
+struct BatchRes {
+    std::vector<void *> bufs;    // stream-ordered allocations freed at the end of the batch
+    std::vector<cudaEvent_t> walk_ev;  // profiling: start/end pairs of walk launches
+};
+
+int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs, const BatchParams &P, bool prof,
+                     BatchRes &R)
+{
+    const int32_t na = G.na;
+    if (na == 0) return ER_OK;
+    // per-group buffers (stream ordered on the AMC stream)
+    int64_t maxch = (int64_t)((G.eta0_sum << (P.tau - 1)) / 32) + na + 1;
+    uint32_t *kk = nullptr;
+    int32_t *list2 = nullptr;
+    int64_t *nch = nullptr, *cincl = nullptr;
+    TilePart *parts = nullptr;
+    void *tmp = nullptr;
+    size_t tb1 = 0, tb2 = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, (uint32_t *)nullptr, (uint32_t *)nullptr, (int32_t *)nullptr,
+                                       (int32_t *)nullptr, na, 0, 32, sb));
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb2, (int64_t *)nullptr, (int64_t *)nullptr, na, sb));
+    const size_t tbytes = std::max(tb1, tb2) + 256;
+    CK(cudaMallocAsync((void **)&kk, sizeof(uint32_t) * 2 * na, sb));
+    CK(cudaMallocAsync((void **)&list2, sizeof(int32_t) * na, sb));
+    CK(cudaMallocAsync((void **)&nch, sizeof(int64_t) * na, sb));
+    CK(cudaMallocAsync((void **)&cincl, sizeof(int64_t) * na, sb));
+    CK(cudaMallocAsync((void **)&parts, sizeof(TilePart) * maxch, sb));
+    CK(cudaMallocAsync(&tmp, tbytes, sb));
+    for (void *p : {(void *)kk, (void *)list2, (void *)nch, (void *)cincl, (void *)parts, tmp}) R.bufs.push_back(p);
+    const int32_t *list = G.list;
+    if (na > 1) {
+        // order by descending ell_f (stable): warps then see one trip count
+        k_lf_key<<<blocks_for(na, 256), 256, 0, sb>>>(na, G.list, qs, kk);
+        LAUNCHED(g);
+        size_t b1 = tbytes;
+        CK(cub::DeviceRadixSort::SortPairs(tmp, b1, kk, kk + na, G.list, list2, na, 0, 32, sb));
+        g->launches += 2;
+        list = list2;
+    }
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
+    const uint32_t key0 = (uint32_t)P.seed, key1 = (uint32_t)(P.seed >> 32);
+    for (int b = 0; b < P.tau; b++) {
+        k_nchunks<<<blocks_for(na, 256), 256, 0, sb>>>(na, list, qs, b, nch);
+        LAUNCHED(g);
+        size_t b2 = tbytes;
+        CK(cub::DeviceScan::InclusiveSum(tmp, b2, nch, cincl, na, sb));
+        g->launches += 2;
+        const int64_t bound = (int64_t)((G.eta0_sum << b) / 32) + na;   // chunks of batch b, at most
+        const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(4 * nsm, (bound + WALK_WARPS - 1) / WALK_WARPS));
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (prof) {
+            CK(cudaEventCreate(&e0));
+            CK(cudaEventCreate(&e1));
+            CK(cudaEventRecord(e0, sb));
+        }
+#define WALK_ARGS                                                                                                   \
+    na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, G.ykeys, G.yvals, b, key0, key1, P.qbase, \
+        parts
+        if (g->d_parcs) k_walks<2><<<grid, WALK_THREADS, 0, sb>>>(WALK_ARGS);
+        else if (g->d_arcs) k_walks<1><<<grid, WALK_THREADS, 0, sb>>>(WALK_ARGS);
+        else k_walks<0><<<grid, WALK_THREADS, 0, sb>>>(WALK_ARGS);
+#undef WALK_ARGS
+        LAUNCHED(g);
+        if (prof) {
+            CK(cudaEventRecord(e1, sb));
+            R.walk_ev.push_back(e0);
+            R.walk_ev.push_back(e1);
+        }
+        k_amc_reduce<<<blocks_for((int64_t)na * 32, 256), 256, 0, sb>>>(
+            na, list, cincl, parts, b, P, qs, nullptr, prof ? reinterpret_cast<unsigned long long *>(g->d_steps) : nullptr);
+        LAUNCHED(g);
+    }
+    CK(cudaGetLastError());
     return ER_OK;
 }
 
@@ -1128,18 +1247,62 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
     ENSURE(ws.idx, sizeof(int32_t) * (k + 1), false);
     ENSURE(ws.act, sizeof(int32_t) * (k + 1), false);
     ENSURE(ws.act2, sizeof(int32_t) * (k + 1), false);
-    int64_t pool_used = 0;
     int64_t smm_pairs = 0;
     int rc;
 
-    // ---- profiling events: [0] SMM start, [1] SMM end, [2+2j] walk j start, [3+2j] walk j end
+    // AMC stream: each group's walks run concurrently with the SMM waves of the queries still in
+    // the head ("Overlap").
+    cudaStream_t sb = g->amc_stream;
+    cudaEvent_t ev_start = nullptr, ev_smm_end = nullptr, ev_end = nullptr, ev_amc_done = nullptr;
     const bool prof = g->profiling;
-    cudaEvent_t ev[2 + 2 * 8 + 1] = {};
-    int nwalk = 0;
+    BatchRes R;
+    CK(cudaEventCreateWithFlags(&ev_amc_done, cudaEventDisableTiming));
     if (prof) {
-        for (auto &e : ev) CK(cudaEventCreate(&e));
-        CK(cudaEventRecord(ev[0], st));
+        CK(cudaEventCreate(&ev_start));
+        CK(cudaEventCreate(&ev_smm_end));
+        CK(cudaEventCreate(&ev_end));
+        CK(cudaEventRecord(ev_start, st));
     }
+    // the AMC stream starts after everything enqueued so far on the main stream (inputs, setup)
+    auto fork_group = [&](int32_t na, const int32_t *act, const int32_t *cont, int32_t *tkeys, double *tvals) -> int {
+        // list of the queries of act leaving now for AMC, copied into a group-owned buffer
+        int32_t *flag = ws.cont2.as<int32_t>();
+        k_flag_leave<<<blocks_for(na, 256), 256, 0, st>>>(na, act, qs, cont, flag);
+        LAUNCHED(g);
+        int64_t ng = 0;
+        int rr = select_list(c, act, flag, na, ws.act2.as<int32_t>(), ws.idx2.as<int32_t>(), &ng);
+        if (rr) return rr;
+        if (ng == 0) {
+            if (tkeys) R.bufs.push_back(tkeys);
+            if (tvals) R.bufs.push_back(tvals);
+            return ER_OK;
+        }
+        AmcGroup G;
+        G.na = (int32_t)ng;
+        CK(cudaMallocAsync((void **)&G.list, sizeof(int32_t) * ng, st));
+        CK(cudaMemcpyAsync(G.list, ws.act2.p, sizeof(int32_t) * ng, cudaMemcpyDeviceToDevice, st));
+        unsigned long long *d_sum = reinterpret_cast<unsigned long long *>(ws.scalars.as<int64_t>() + 4);
+        CK(cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), st));
+        k_sum_eta0<<<blocks_for(ng, 256), 256, 0, st>>>((int32_t)ng, G.list, qs, d_sum);
+        LAUNCHED(g);
+        rr = read_scalars(c, {reinterpret_cast<const int64_t *>(d_sum)});
+        if (rr) return rr;
+        G.eta0_sum = (unsigned long long)c.hp[0];
+        G.ykeys = tkeys;
+        G.yvals = tvals;
+        R.bufs.push_back(G.list);
+        if (tkeys) R.bufs.push_back(tkeys);
+        if (tvals) R.bufs.push_back(tvals);
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventRecord(e, st));
+        CK(cudaStreamWaitEvent(sb, e, 0));
+        cudaEventDestroy(e);
+        return launch_amc_group(g, sb, G, qs, P, prof, R);
+    };
+    ENSURE(ws.scalars, sizeof(int64_t) * 8, false);
+    ENSURE(ws.cont2, sizeof(int32_t) * (k + 1), false);
+    ENSURE(ws.idx2, sizeof(int32_t) * (k + 1), false);
 
     // ---- SMM head
     {
@@ -1151,7 +1314,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         int64_t na = 0;
         rc = select_list(c, ids, ws.cont.as<int32_t>(), K, ws.act.as<int32_t>(), ws.idx.as<int32_t>(), &na);
         if (rc) return rc;
-        // AMC-only queries (force_ell_b == 0) need tables built from e_s, e_t.
+        // AMC-only queries (force_ell_b == 0): tables from e_s, e_t, one group.
         if (P.force_ell_b == 0) {
             k_flag_phase<<<blocks_for(k, 256), 256, 0, st>>>(k, qs, PH_AMC, ws.cont.as<int32_t>(), ids);
             LAUNCHED(g);
@@ -1168,9 +1331,13 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                                                                        ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(),
                                                                        ws.fr_seg.as<int32_t>(), ws.fr_off.as<int64_t>());
                 LAUNCHED(g);
+                int32_t *tk = nullptr;
+                double *tv = nullptr;
                 rc = build_ytables(c, (int32_t)n0, ws.act.as<int32_t>(), nullptr, ws.fr_off.as<int64_t>(),
                                    ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(), ws.fr_seg.as<int32_t>(), F0, nullptr,
-                                   pool_used, P);
+                                   &tk, &tv);
+                if (rc) return rc;
+                rc = fork_group((int32_t)n0, ws.act.as<int32_t>(), nullptr, tk, tv);
                 if (rc) return rc;
             }
             na = 0;
@@ -1253,11 +1420,17 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             k_decide<<<blocks_for(na, 128), 128, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), ws.segstat.as<SegStat>(),
                                                           P, qs, cont);
             LAUNCHED(g);
-            // y-tables for queries leaving the head now
-            rc = build_ytables(c, (int32_t)na, ws.act.as<int32_t>(), cont, ws.nf_off.as<int64_t>(),
-                               ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), E, dU,
-                               pool_used, P);
-            if (rc) return rc;
+            // y-tables for queries leaving the head now, then their AMC on the AMC stream
+            {
+                int32_t *tk = nullptr;
+                double *tv = nullptr;
+                rc = build_ytables(c, (int32_t)na, ws.act.as<int32_t>(), cont, ws.nf_off.as<int64_t>(),
+                                   ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), E, dU, &tk,
+                                   &tv);
+                if (rc) return rc;
+                rc = fork_group((int32_t)na, ws.act.as<int32_t>(), cont, tk, tv);
+                if (rc) return rc;
+            }
             // compaction of continuing queries
             int32_t *newidx = ws.idx.as<int32_t>();
             rc = scan_incl(c, cont, newidx, na);
@@ -1296,68 +1469,10 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         }
     }
 
-    if (prof) CK(cudaEventRecord(ev[1], st));
-
-    // ---- AMC tail
-    {
-        int32_t *ids = ws.ids.as<int32_t>();
-        k_flag_phase<<<blocks_for(k, 256), 256, 0, st>>>(k, qs, PH_AMC, ws.cont.as<int32_t>(), ids);
-        LAUNCHED(g);
-        int64_t na = 0;
-        rc = select_list(c, ids, ws.cont.as<int32_t>(), K, ws.act.as<int32_t>(), ws.idx.as<int32_t>(), &na);
-        if (rc) return rc;
-        const uint32_t key0 = (uint32_t)P.seed, key1 = (uint32_t)(P.seed >> 32);
-        if (na > 1) {
-            // order the AMC queries by descending ell_f (stable): warps then see one trip count
-            ENSURE(ws.lfkey, sizeof(uint32_t) * 2 * na, false);
-            uint32_t *kk = ws.lfkey.as<uint32_t>();
-            k_lf_key<<<blocks_for(na, 256), 256, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), qs, kk);
-            LAUNCHED(g);
-            rc = cub_call(c, [&](void *tmp, size_t &bytes) {
-                return cub::DeviceRadixSort::SortPairs(tmp, bytes, kk, kk + na, ws.act.as<int32_t>(),
-                                                       ws.act2.as<int32_t>(), (int)na, 0, 32, st);
-            });
-            if (rc) return rc;
-            std::swap(ws.act, ws.act2);
-        }
-        for (int b = 0; b < P.tau && na > 0; b++) {
-            ENSURE(ws.tiles, sizeof(int64_t) * 2 * (na + 1), false);
-            int64_t *nch = ws.tiles.as<int64_t>();
-            int64_t *cincl = nch + (na + 1);
-            k_nchunks<<<blocks_for(na, 256), 256, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), qs, b, nch);
-            LAUNCHED(g);
-            rc = scan_incl(c, nch, cincl, na);
-            if (rc) return rc;
-            rc = read_scalars(c, {cincl + (na - 1)});
-            if (rc) return rc;
-            const int64_t NC = c.hp[0];
-            ENSURE(ws.parts, sizeof(TilePart) * NC, false);
-            if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk], st));
-#define WALK_ARGS                                                                                                \
-    NC, (int32_t)na, cincl, ws.act.as<int32_t>(), qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack,          \
-        ws.ypool.as<int32_t>(), ws.yvals.as<double>(), b, key0, key1, P.qbase, ws.parts.as<TilePart>()
-            if (g->d_parcs)
-                k_walks<2><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(WALK_ARGS);
-            else if (g->d_arcs)
-                k_walks<1><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(WALK_ARGS);
-            else
-                k_walks<0><<<blocks_for(NC, WALK_WARPS), WALK_THREADS, 0, st>>>(WALK_ARGS);
-#undef WALK_ARGS
-            LAUNCHED(g);
-            if (prof) CK(cudaEventRecord(ev[2 + 2 * nwalk + 1], st));
-            k_amc_reduce<<<blocks_for(na * 32, 256), 256, 0, st>>>(
-                (int32_t)na, ws.act.as<int32_t>(), cincl, ws.parts.as<TilePart>(), b, P, qs, ws.cont.as<int32_t>(),
-                prof ? reinterpret_cast<unsigned long long *>(g->d_steps) : nullptr);
-            nwalk++;
-            LAUNCHED(g);
-            int64_t na2 = 0;
-            rc = select_list(c, ws.act.as<int32_t>(), ws.cont.as<int32_t>(), (int32_t)na, ws.act2.as<int32_t>(),
-                             ws.idx.as<int32_t>(), &na2);
-            if (rc) return rc;
-            std::swap(ws.act, ws.act2);
-            na = na2;
-        }
-    }
+    if (prof) CK(cudaEventRecord(ev_smm_end, st));
+    // join: results need every group's AMC
+    CK(cudaEventRecord(ev_amc_done, sb));
+    CK(cudaStreamWaitEvent(st, ev_amc_done, 0));
 
     // ---- results
     double *d_out = out_r;
@@ -1377,28 +1492,29 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         CK(cudaMemcpyAsync(out_r, d_out, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
         if (stats) CK(cudaMemcpyAsync(stats, d_stats, sizeof(er_query_stats) * k, cudaMemcpyDeviceToHost, st));
     }
-    if (prof) CK(cudaEventRecord(ev[18], st));
+    if (prof) CK(cudaEventRecord(ev_end, st));
+    for (void *p : R.bufs) CK(cudaFreeAsync(p, st));
     if (o.synchronous || !o.out_on_device || prof) CK(cudaStreamSynchronize(st));
+    cudaEventDestroy(ev_amc_done);
     if (prof) {
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-        g->prof.smm_ms += ms;
-        for (int j = 0; j < nwalk; j++) {
-            CK(cudaEventElapsedTime(&ms, ev[2 + 2 * j], ev[3 + 2 * j]));
-            g->prof.walk_ms += ms;
+        float ms = 0.f, smm = 0.f, all = 0.f;
+        CK(cudaEventElapsedTime(&smm, ev_start, ev_smm_end));
+        CK(cudaEventElapsedTime(&all, ev_start, ev_end));
+        double walk = 0.0;
+        for (size_t j = 0; j + 1 < R.walk_ev.size(); j += 2) {
+            CK(cudaEventElapsedTime(&ms, R.walk_ev[j], R.walk_ev[j + 1]));
+            walk += ms;
         }
-        float amc_all = 0.f;
-        CK(cudaEventElapsedTime(&amc_all, ev[1], ev[18]));
-        double walk_this = 0.0;
-        for (int j = 0; j < nwalk; j++) {
-            CK(cudaEventElapsedTime(&ms, ev[2 + 2 * j], ev[3 + 2 * j]));
-            walk_this += ms;
-        }
-        g->prof.amc_other_ms += amc_all - walk_this;
-        g->prof.walk_launches += nwalk;
+        g->prof.smm_ms += smm;
+        g->prof.walk_ms += walk;
+        g->prof.amc_other_ms += all - smm;   // AMC time not hidden under the SMM head
+        g->prof.walk_launches += (int64_t)(R.walk_ev.size() / 2);
         g->prof.smm_pairs += smm_pairs;
         g->prof.batches += 1;
-        for (auto &e : ev) cudaEventDestroy(e);
+        for (cudaEvent_t e : R.walk_ev) cudaEventDestroy(e);
+        cudaEventDestroy(ev_start);
+        cudaEventDestroy(ev_smm_end);
+        cudaEventDestroy(ev_end);
     }
     return ER_OK;
 }
