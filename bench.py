@@ -182,23 +182,30 @@ def config_dict(g, args):
 
 
 def spmm_measure(G, h, g, torch, q=SPMM_Q, reps=10):
-    """K9 (er_spmm) on a dense n x q fp64 block: algorithmic bytes / event time."""
+    """K9 (er_spmm) on a dense n x q fp64 block: algorithmic bytes / event time, L2 flushed
+    (256 MiB write) before every timed call, events on the launching stream."""
     X = torch.rand((g.n, q), dtype=torch.float64, device="cuda")
     Y = torch.empty_like(X)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
     st = torch.cuda.Stream()
     for _ in range(3):
         G.er_spmm(h, X, Y, stream=st)
     st.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
+    times = []
     for _ in range(reps):
+        with torch.cuda.stream(st):
+            flush.fill_(3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
         G.er_spmm(h, X, Y, stream=st)
-    e1.record(st)
-    st.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+        e1.record(st)
+        st.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = statistics.median(times)
     # algorithmic bytes: offsets (8 B/row) + cols (4 B/arc) + X gathers (8q B/arc) + Y writes (8q B/row)
     byts = 8 * (g.n + 1) + 4 * g.nnz + 8 * q * g.nnz + 8 * q * g.n
-    return {"q": q, "ms": ms, "achieved_gbs": byts / ms / 1e6, "algorithmic_bytes": byts}
+    return {"q": q, "ms": ms, "achieved_gbs": byts / ms / 1e6, "algorithmic_bytes": byts,
+            "l2": "flushed before each call", "x_block_mb": g.n * q * 8 / 2**20}
 
 
 def main():
@@ -211,6 +218,7 @@ def main():
     ap.add_argument("--queries", type=int, default=10_000)
     ap.add_argument("--ref-sample", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-spmm", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -337,16 +345,23 @@ def main():
                                    "walks": prof["walk_ms"] / args.steps,
                                    "amc_reduce_etc": prof["amc_other_ms"] / args.steps,
                                    "smm_pairs_per_step": prof["smm_pairs"] / args.steps,
-                                   "walk_steps_per_step": prof["walk_steps"] / args.steps},
+                                   "walk_steps_per_step": prof["walk_steps"] / args.steps,
+                                   "ytable_slots_per_step": prof["ytable_slots"] / args.steps,
+                                   "walk_ctas_per_sm": prof["walk_ctas_per_sm"]},
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(pairs.nbytes),
                     "d2h_bytes_per_step": int(nq * 8)},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
         try:
+            if args.no_spmm:
+                raise RuntimeError("skipped (--no-spmm)")
             sp = spmm_measure(G, h, g, torch)
             sp.update({"peak": hbm, "frac": sp["achieved_gbs"] / hbm})
             line["spmm"] = sp
+            sp64 = spmm_measure(G, h, g, torch, q=64)
+            sp64.update({"peak": hbm, "frac": sp64["achieved_gbs"] / hbm})
+            line["spmm_q64"] = sp64
         except Exception as ex:  # noqa: BLE001
             line["spmm"] = {"error": str(ex)}
         if world == 1 and not args.no_cpu_baseline:

@@ -142,6 +142,7 @@ void er_opts_default(er_opts *o);
  *  rb_terms[i]                        series increment of SMM iteration i+1 (i < 8)
  *  walk_checksum                      sum over walks of fmix-hash(q,b,side,k,endpoint) mod 2^64
  *  tie_flags                          bit0: ell, bit1: eta0, bit2: Bernstein decision within 1e-12
+ *  ytable_log2                        log2 of the y-table capacity (implementation diagnostic)
  */
 typedef struct er_query_stats {
     int32_t ell, ell_b, ell_f, batches_run;
@@ -150,7 +151,7 @@ typedef struct er_query_stats {
     double rb_terms[8];
     uint64_t walk_checksum;
     uint32_t tie_flags;
-    uint32_t pad;
+    uint32_t ytable_log2;     /* log2 of the query's y-table slots (0: no AMC); diagnostics only */
 } er_query_stats;
 
 /*
@@ -186,6 +187,8 @@ typedef struct er_profile {
     int64_t walk_steps;      /* walk steps executed (both sides, all batches) */
     int64_t smm_pairs;       /* (u, x) pairs emitted by the SMM push over all waves */
     int64_t batches;         /* query batches profiled */
+    int64_t ytable_slots;    /* y-table slots allocated (Alg. 1 L7 tables of all AMC queries) */
+    int64_t walk_ctas_per_sm; /* resident K6 CTAs per SM (occupancy API) at the last walk launch */
 } er_profile;
 int er_graph_profile(er_graph *g, int enable);
 int er_graph_profile_read(er_graph *g, er_profile *out);

@@ -33,7 +33,7 @@ STATS_DTYPE = np.dtype([
     ("vol_last", "<i8"), ("h_last", "<i8"),
     ("psi", "<f8"), ("r_b", "<f8"), ("r_f", "<f8"), ("f_last", "<f8"), ("sigma2_last", "<f8"),
     ("rb_terms", "<f8", (8,)),
-    ("walk_checksum", "<u8"), ("tie_flags", "<u4"), ("pad", "<u4"),
+    ("walk_checksum", "<u8"), ("tie_flags", "<u4"), ("ytable_log2", "<u4"),
 ])
 
 EXPORTED = ["er_graph_create", "er_graph_create_ex", "er_graph_destroy", "er_query_batch", "er_last_error",
@@ -53,7 +53,8 @@ class er_opts(ctypes.Structure):
 class er_profile(ctypes.Structure):
     _fields_ = [("smm_ms", ctypes.c_double), ("walk_ms", ctypes.c_double), ("amc_other_ms", ctypes.c_double),
                 ("walk_launches", ctypes.c_int64), ("walk_steps", ctypes.c_int64),
-                ("smm_pairs", ctypes.c_int64), ("batches", ctypes.c_int64)]
+                ("smm_pairs", ctypes.c_int64), ("batches", ctypes.c_int64),
+                ("ytable_slots", ctypes.c_int64), ("walk_ctas_per_sm", ctypes.c_int64)]
 
 
 class GeerError(RuntimeError):
@@ -216,17 +217,27 @@ def er_query_batch_ex(g, pairs, eps: float, p_fail: float = 0.01, *, out=None, s
     o.ell_variant = ell_variant
     o.synchronous = int(synchronous)
     if stream is not None:
-        o.cuda_stream = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+        o.cuda_stream = _stream_handle(stream)
     _raise(lib.er_query_batch_ex(g, pp, kk, float(eps), float(p_fail), ctypes.byref(o), op, sp))
     return out, stats
+
+
+def _stream_handle(stream):
+    """cudaStream_t for the C ABI: torch streams, raw handles; torch's legacy default stream
+    (handle 0) is passed as cudaStreamLegacy (0x1), because NULL means the handle's own stream."""
+    if stream is None:
+        return None
+    h = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    return ctypes.c_void_p(h if h else 1)
 
 
 def er_spmm(g, X, Y, normalize: bool = True, stream=None) -> None:
     """Y = P X (or A X) for row-major n x q device tensors (float64)."""
     q = 1 if X.dim() == 1 else int(X.shape[1])
-    s = None
-    if stream is not None:
-        s = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    if stream is None:   # order with torch's work on the tensors (their producers and readers)
+        import torch
+        stream = torch.cuda.current_stream(X.device)
+    s = _stream_handle(stream)
     _raise(lib.er_spmm(g, ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(Y.data_ptr()), q, int(normalize), s))
 
 

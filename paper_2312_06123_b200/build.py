@@ -12,7 +12,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgeer.so"
-SOURCES = ["pipeline.cu", "abi.cu", "lambda.cu"]
+SOURCES = ["pipeline.cu", "abi.cu", "lambda.cu", "spmm.cu"]
 HEADERS = ["geer_internal.h", "geer_device.cuh"]
 INCLUDE = PKG.parent / "include" / "geer.h"
 

@@ -248,6 +248,12 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
             if (!strcmp(env, "cols")) layout = 0;
             if (!strcmp(env, "packed") && packable) layout = 2;
         }
+        if (const char *env = getenv("GEER_WALK_MINB")) g->walk_minb = std::min(4, std::max(2, atoi(env)));
+        if (const char *env = getenv("GEER_AMC_OVERLAP")) g->amc_overlap = atoi(env) != 0;
+        if (const char *env = getenv("GEER_WALK_HINTS")) g->walk_hints = atoi(env) & 3;
+        if (const char *env = getenv("GEER_WALK_KERNEL")) g->walk_kernel = atoi(env) == 4 ? 4 : 3;
+        if (const char *env = getenv("GEER_WALK_NP")) g->walk_np = atoi(env) == 1 ? 1 : 2;
+        if (const char *env = getenv("GEER_WALK_SMEM_KB")) g->walk_smem_words = 256 * std::min(48, std::max(8, atoi(env)));
         g->pack.bo = bo;
         g->pack.bd = bd;
         if (layout == 1 && e == cudaSuccess) {
@@ -283,6 +289,10 @@ void er_graph_destroy(er_graph *g)
         if (g->d_arcs) cudaFree(g->d_arcs);
         if (g->d_parcs) cudaFree(g->d_parcs);
         if (g->d_steps) cudaFree(g->d_steps);
+        if (g->d_rowperm) cudaFree(g->d_rowperm);
+        if (g->d_hseg) cudaFree(g->d_hseg);
+        if (g->d_seg_e0) cudaFree(g->d_seg_e0);
+        if (g->d_seg_row) cudaFree(g->d_seg_row);
         if (g->amc_stream) cudaStreamSynchronize(g->amc_stream);
         if (g->stream) cudaStreamDestroy(g->stream);
         if (g->amc_stream) cudaStreamDestroy(g->amc_stream);
@@ -414,6 +424,7 @@ int er_graph_profile_read(er_graph *g, er_profile *out)
     if (!g || !out) { set_error(ER_EINVAL, "NULL argument"); return ER_EINVAL; }
     std::lock_guard<std::mutex> lk(g->mu);
     *out = g->prof;
+    out->walk_ctas_per_sm = g->walk_occ;
     if (g->d_steps) {
         int64_t steps = 0;
         cudaError_t e = cudaMemcpy(&steps, g->d_steps, sizeof(int64_t), cudaMemcpyDeviceToHost);

@@ -58,6 +58,13 @@ __device__ __forceinline__ uint32_t ybucket(int32_t v, int lgb)
     return lgb == 0 ? 0u : ((uint32_t)v * 0x9E3779B1u) >> (32 - lgb);
 }
 
+// Membership filter of a large y-table (a one-hash Bloom filter over supp(y)): bit of node v in a
+// filter of 2^flg bits (top bits of an odd multiplier independent of ybucket's).
+__device__ __forceinline__ uint32_t fbit(int32_t v, int flg)
+{
+    return ((uint32_t)v * 0x85EBCA6Bu) >> (32 - flg);
+}
+
 // Eq. 10.
 __device__ __forceinline__ double psi_eq10(int64_t lf, double m1s, double m2s, double m1t, double m2t,
                                            double ds, double dt)

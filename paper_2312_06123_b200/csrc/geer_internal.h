@@ -13,6 +13,9 @@
 
 namespace geer {
 
+// K9: rows of degree > SPMM_SEG are summed in segments of SPMM_SEG neighbours (spmm.cu).
+constexpr int SPMM_SEG = 512;
+
 // Query phases.
 enum : int32_t { PH_DONE = 0, PH_SMM = 1, PH_AMC = 2 };
 
@@ -24,6 +27,12 @@ struct QState {
     int32_t phase;         // PH_*
     int32_t ylog2;         // log2 of the y-table capacity in slots (>= 3)
     int64_t yoff;          // offset (in slots) of this query's y-table in the pools
+    int32_t flog2;         // log2 of the membership-filter bits (0: no filter; small tables)
+    int32_t pad2;
+    int64_t foff;          // offset (in 32-bit words) of this query's filter in the filter pool
+    const int32_t *ykeys;  // absolute pointers of this query's table / values / filter (walk kernel)
+    const double *yvals;
+    const uint32_t *yfilt;
     double z;              // last batch mean Z (= r_f)
 };
 
@@ -98,6 +107,7 @@ struct Workspace {
     DevBuf tiles, parts;                            // AMC tiles
     DevBuf cub_tmp;                                 // CUB temp storage
     DevBuf scalars;                                 // small device scalars
+    DevBuf spmm_part;                               // K9 heavy-row segment sums
     DevBuf ids, seglen, segbeg, lfkey;              // 0..k-1 ids; compaction lengths; sort segments; AMC order
     void *host_pinned = nullptr;                    // small pinned host scalars
     size_t host_pinned_cap = 0;
@@ -121,6 +131,13 @@ struct er_graph {
     double lambda = 0.0;
     bool lambda_set = false;
     int nbits = 1;
+    int walk_minb = 3;   // K6 resident CTAs per SM (launch bounds variant; GEER_WALK_MINB 2..4)
+    bool amc_overlap = true;   // AMC per SMM wave on the AMC stream (GEER_AMC_OVERLAP=0: one AMC after the head)
+    int walk_hints = 0;  // K6 L2 cache hints: bit0 y-tables evict-first, bit1 arcs evict-last (GEER_WALK_HINTS)
+    int walk_occ = 0;    // K6 resident CTAs per SM at the last launch (occupancy API)
+    int walk_kernel = 3; // K6 version: 3 = pipelined-probe kernel (default), 4 = multi-chain kernel (GEER_WALK_KERNEL)
+    int walk_np = 2;     // K6 walk pairs per thread (GEER_WALK_NP 1..2)
+    int walk_smem_words = 12288;  // K6 staging area per CTA in 32-bit words (GEER_WALK_SMEM_KB)
     cudaStream_t stream = nullptr;
     cudaStream_t amc_stream = nullptr;  // AMC groups overlap the SMM head
     std::mutex mu;
@@ -128,6 +145,12 @@ struct er_graph {
     bool profiling = false;
     er_profile prof{};
     int64_t *d_steps = nullptr;  // device walk-step counter (profiling)
+    int32_t *d_rowperm = nullptr;  // K9: rows by descending degree (built at the first er_spmm)
+    int64_t n_heavy = 0;           // K9: rows with degree > SPMM_SEG (the prefix of d_rowperm)
+    int64_t n_seg = 0;             // K9: segments of the heavy rows
+    int64_t *d_hseg = nullptr;     // K9: first segment of each heavy row (n_heavy + 1)
+    int64_t *d_seg_e0 = nullptr;   // K9: first arc of each segment
+    int32_t *d_seg_row = nullptr;  // K9: row of each segment
     geer::Workspace ws;
 };
 

@@ -383,60 +383,86 @@ __global__ void k_decide(int32_t na, const int32_t *__restrict__ act, const SegS
 
 // y-table capacity (slots) for queries that leave the SMM head for AMC in this wave:
 // next power of two >= 2 |supp(s*)| + 2 |supp(t*)| (load <= 1/2), at least one 8-slot bucket.
+// Tables too large to stage in the walk kernel's shared memory also get a membership filter of
+// min(2^18, 4 cap) bits (fwords[i] 32-bit words), staged instead (K6).
+constexpr int WALK_SMEM_WORDS = 12288;      // 48 KB of staged y-table keys / filters per CTA
+constexpr int WALK_KEY_SLOTS = 8192;        // largest table staged as keys (pow2 <= WALK_SMEM_WORDS)
+constexpr int FILTER_MAX_LOG2 = 18;         // 32 KB filter
 __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState *__restrict__ qs,
                        const int32_t *__restrict__ cont, const int64_t *__restrict__ segoff,
-                       int64_t *__restrict__ ycap)
+                       int64_t *__restrict__ ycap, int64_t *__restrict__ fwords)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
-    int64_t cap = 0;
+    int64_t cap = 0, fw = 0;
     if ((cont == nullptr || !cont[i]) && qs[act[i]].phase == PH_AMC) {
         const int64_t len = segoff[2 * i + 2] - segoff[2 * i];
         cap = YB;
         while (cap < 2 * len) cap <<= 1;
+        if (cap > WALK_KEY_SLOTS) fw = std::min<int64_t>((int64_t)1 << FILTER_MAX_LOG2, 4 * cap) / 32;
     }
     ycap[i] = cap;
+    fwords[i] = fw;
 }
 
 __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__ ycap,
-                          const int64_t *__restrict__ yincl, int64_t base, QState *__restrict__ qs)
+                          const int64_t *__restrict__ yincl, const int64_t *__restrict__ fwords,
+                          const int64_t *__restrict__ fincl, const int32_t *kbase, const double *vbase,
+                          const uint32_t *fbase, QState *__restrict__ qs)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na || ycap[i] == 0) return;
     QState &Q = qs[act[i]];
     const int64_t cap = ycap[i];
-    Q.yoff = base + yincl[i] - cap;
+    Q.yoff = yincl[i] - cap;
     int lg = 0;
     while ((1ll << lg) < cap) lg++;
     Q.ylog2 = lg;
+    const int64_t fw = fwords[i];
+    Q.foff = fincl[i] - fw;
+    int fl = 0;
+    while (fw > 0 && (32ll << fl) < 32 * fw) fl++;
+    Q.flog2 = fw > 0 ? fl + 5 : 0;
+    Q.ykeys = kbase + Q.yoff;
+    Q.yvals = vbase + Q.yoff;
+    Q.yfilt = fw > 0 ? fbase + Q.foff : nullptr;
 }
 
-__global__ void k_yfill(int64_t Y, int32_t *__restrict__ keys, double *__restrict__ ys, double *__restrict__ yt)
+__global__ void k_yfill(int64_t Y, int32_t *__restrict__ keys, double *__restrict__ ys, int64_t FW,
+                        uint32_t *__restrict__ filt)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < FW) filt[j] = 0u;
     if (j >= Y) return;
     keys[j] = -1;
     ys[j] = 0.0;
-    yt[j] = 0.0;
 }
 
-// K5a: insert every support node of a leaving query into its y-table (find-or-insert; the node
-// may come from both sides).  Side 0 stores s*(v)/d(s) at the slot, side 1 stores t*(v)/d(t) in a
-// scratch array.  Bucketed open addressing: 8 int32 keys per 32-byte bucket, buckets probed
-// linearly, slots in order inside a bucket, claimed by CAS.
+// K5: insert every support node of side `side` of a leaving query into its y-table
+// (find-or-insert: a node may be on both sides).  Launched for side 0, then side 1: side 0
+// stores s*(v)/d(s) at the slot, side 1 subtracts t*(v)/d(t), so every slot ends with
+// y(v) = s*(v)/d(s) - t*(v)/d(t) (Alg. 1 L7 with s = s*, t = t*; a side the node is not on
+// contributes 0.0).  A node occurs once per side, so each pass has one writer per slot.
+// Bucketed open addressing: 8 int32 keys per 32-byte bucket, buckets probed linearly, slots in
+// order inside a bucket, claimed by CAS.
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                           const int32_t *__restrict__ id, const double *__restrict__ val,
                           const int32_t *__restrict__ act, const int64_t *__restrict__ ycap,
                           const QState *__restrict__ qs, int32_t *__restrict__ ykeys, double *__restrict__ ys,
-                          double *__restrict__ yt, int64_t tbase)
+                          uint32_t *__restrict__ filt, int side)
 {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
     const int32_t g = seg[e];
+    if ((g & 1) != side) return;
     const int32_t i = g >> 1;
     if (ycap[i] == 0) return;
     const QState &Q = qs[act[i]];
     const int32_t v = id[e];
+    if (Q.flog2 > 0) {
+        const uint32_t fb = fbit(v, Q.flog2);
+        atomicOr(filt + Q.foff + (fb >> 5), 1u << (fb & 31));
+    }
     int32_t *keys = ykeys + Q.yoff;
     const int lgb = Q.ylog2 - YB_LOG;
     const uint32_t bmask = (1u << lgb) - 1u;
@@ -452,22 +478,13 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
             int32_t k = kk[j];
             if (k == -1) k = atomicCAS(&keys[slot], -1, v);
             if (k == -1 || k == v) {
-                if (g & 1) yt[Q.yoff - tbase + slot] = val[e] / (double)Q.dt;
+                if (side) ys[Q.yoff + slot] = ys[Q.yoff + slot] - val[e] / (double)Q.dt;
                 else ys[Q.yoff + slot] = val[e] / (double)Q.ds;
                 return;
             }
         }
         bk = (bk + 1) & bmask;
     }
-}
-
-// K5b: y(v) = s*(v)/d(s) - t*(v)/d(t) at every slot of the new tables (Alg. 1 L7 with s = s*,
-// t = t*); a side the node is not on contributes 0.0 (its term stayed 0; empty slots stay 0).
-__global__ void k_yfinal(int64_t Y, int64_t tbase, double *__restrict__ ys, const double *__restrict__ yt)
-{
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= Y) return;
-    ys[tbase + j] = ys[tbase + j] - yt[j];
 }
 
 // Continuing segments: new lengths (for the compaction scan).
@@ -518,12 +535,12 @@ __global__ void k_compact_lists(int32_t na, const int32_t *__restrict__ cont, co
 // Walk pairs of batch b per AMC query, and the AMC sort key (descending ell_f) used to order
 // the flattened walk space so warps mostly see one trip count.
 __global__ void k_nchunks(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs, int b,
-                          int64_t *__restrict__ nch)
+                          int32_t per_chunk, int64_t *__restrict__ nch)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
     const QState &Q = qs[amc[i]];
-    nch[i] = Q.phase == PH_AMC ? ((Q.st.eta0 << b) + 31) / 32 : 0;
+    nch[i] = Q.phase == PH_AMC ? ((Q.st.eta0 << b) + per_chunk - 1) / per_chunk : 0;
 }
 
 __global__ void k_lf_key(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs,
@@ -536,7 +553,7 @@ __global__ void k_lf_key(int32_t na, const int32_t *__restrict__ amc, const QSta
 
 constexpr int WALK_WARPS = 8;
 constexpr int WALK_THREADS = 32 * WALK_WARPS;
-constexpr int WALK_SMEM_SLOTS = 8192;      // 32 KB of staged y-table keys per CTA
+constexpr size_t WALK_SMEM_BYTES = sizeof(int32_t) * WALK_SMEM_WORDS;
 
 __device__ __forceinline__ int32_t find_chunk_query(const int64_t *__restrict__ cincl, int32_t n, int64_t c)
 {
@@ -565,8 +582,353 @@ __device__ __forceinline__ int bucket_match(const int4 a, const int4 b, int32_t 
     return m;
 }
 
+// L2 cache policies: the y-tables stream past (evict first), the walk graph stays (evict last).
+__device__ __forceinline__ uint64_t pol_evict_first()
+{
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last()
+{
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ldg_f64(const double *p, uint64_t pol)
+{
+    if (pol == 0) return __ldg(p);   // no cache hint (hints disabled)
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ unsigned long long ldg_u64(const unsigned long long *p, uint64_t pol)
+{
+    if (pol == 0) return __ldg(p);
+    unsigned long long r;
+    asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint32_t ldg_u32(const int32_t *p, uint64_t pol)
+{
+    if (pol == 0) return (uint32_t)__ldg(p);
+    uint32_t r;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint4 ldg_u128(const uint4 *p, uint64_t pol)
+{
+    if (pol == 0) return __ldg(p);
+    uint4 r;
+    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+    return r;
+}
+
+// y-table probe modes of a warp (chosen per tile by the staging plan):
+//   YM_GLOBAL  keys probed in global memory (one 32-byte sector per bucket)
+//   YM_SMEM    the whole key table staged in shared memory
+//   YM_FILTER  the table's membership filter staged in shared memory; global probe only when the
+//              node's filter bit is set (a clear bit proves y(v) = 0: v is not in supp(y))
+enum { YM_GLOBAL = 0, YM_SMEM = 1, YM_FILTER = 2 };
+
+struct YView {
+    const int32_t *keys;        // global keys of the table
+    const int32_t *skeys;       // staged keys (YM_SMEM)
+    const uint32_t *sfilt;      // staged filter (YM_FILTER)
+    const double *vals;         // global values
+    int lgb, flg;
+    uint64_t pol;               // evict-first policy for table loads
+};
+
+template <int MODE>
+__device__ __forceinline__ void load_bucket(const YView &Y, int32_t v, uint32_t bk, int4 &a, int4 &b)
+{
+    if (MODE == YM_SMEM) {
+        const int32_t *p = Y.skeys + (size_t)bk * YB;
+        a = reinterpret_cast<const int4 *>(p)[0];
+        b = reinterpret_cast<const int4 *>(p)[1];
+        return;
+    }
+    if (MODE == YM_FILTER) {
+        const uint32_t fb = fbit(v, Y.flg);
+        if (!((Y.sfilt[fb >> 5] >> (fb & 31)) & 1u)) {
+            a = make_int4(-1, -1, -1, -1);   // not in the support: an empty bucket -> y = 0
+            b = a;
+            return;
+        }
+    }
+    // one 32-byte sector in one instruction (LDG.E.ENL2.256 on sm_100a)
+    const int32_t *p = Y.keys + (size_t)bk * YB;
+    if (Y.pol == 0) {
+        asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+            : "l"(p));
+        return;
+    }
+    asm("ld.global.nc.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+        : "l"(p), "l"(Y.pol));
+}
+
+// Slow path: v not in its first bucket and the bucket is full -> probe the following buckets
+// (in shared memory for YM_SMEM, else in global memory).
+template <int MODE>
+__device__ __forceinline__ double probe_rest(const YView &Y, uint32_t bk, int32_t v)
+{
+    const uint32_t bmask = (1u << Y.lgb) - 1u;
+    while (true) {
+        bk = (bk + 1) & bmask;
+        int4 a, b;
+        load_bucket<MODE == YM_SMEM ? YM_SMEM : YM_GLOBAL>(Y, v, bk, a, b);
+        bool empty;
+        const int m = bucket_match(a, b, v, &empty);
+        if (m >= 0) return ldg_f64(Y.vals + (size_t)bk * YB + m, Y.pol);
+        if (empty) return 0.0;
+    }
+}
+
+template <int ARC>
+__device__ __forceinline__ uint4 next_arc(const uint2 R, uint64_t r64, const uint4 *__restrict__ arcs,
+                                          const int32_t *__restrict__ cols,
+                                          const unsigned long long *__restrict__ parcs, PackSpec pk, uint64_t pl)
+{
+    const uint64_t e = (uint64_t)R.x + __umul64hi(r64, (uint64_t)R.y);   // idx = floor(r64 d / 2^64) (R10)
+    if (ARC == 2) return pk.unpack(ldg_u64(parcs + e, pl));
+    if (ARC == 1) return ldg_u128(arcs + e, pl);
+    uint4 A;
+    A.x = ldg_u32(cols + e, pl);
+    return A;
+}
+
+// y(v) lookup of one node: slot index of v in its query's table, or -1 when v is not in
+// supp(y) (then y(v) = 0, Alg. 1 L7 outside U_s and U_t).  Bucketed open addressing: 8 keys
+// per bucket, buckets probed linearly.
+__device__ __forceinline__ int64_t ylookup_smem(const int32_t *skeys, int lgb, int32_t v)
+{
+    const uint32_t bmask = (1u << lgb) - 1u;
+    uint32_t bk = ybucket(v, lgb);
+    while (true) {
+        int4 a, b;
+        load_bucket<YM_SMEM>(YView{nullptr, skeys, nullptr, nullptr, lgb, 0, 0}, v, bk, a, b);
+        bool empty;
+        const int m = bucket_match(a, b, v, &empty);
+        if (m >= 0) return (int64_t)bk * YB + m;
+        if (empty) return -1;
+        bk = (bk + 1) & bmask;
+    }
+}
+__device__ __forceinline__ int64_t ylookup_global(const int32_t *keys, int lgb, int32_t v, uint64_t pol)
+{
+    const uint32_t bmask = (1u << lgb) - 1u;
+    uint32_t bk = ybucket(v, lgb);
+    while (true) {
+        int4 a, b;
+        load_bucket<YM_GLOBAL>(YView{keys, nullptr, nullptr, nullptr, lgb, 0, pol}, v, bk, a, b);
+        bool empty;
+        const int m = bucket_match(a, b, v, &empty);
+        if (m >= 0) return (int64_t)bk * YB + m;
+        if (empty) return -1;
+        bk = (bk + 1) & bmask;
+    }
+}
+
+// NP walk pairs per thread = 2 NP independent chains (S_k from s, T_k from t for each pair),
+// advanced in lock step so 2 NP arc loads are in flight per thread.  Per step and chain:
+// Philox draw (R10; the even step's words are cached from the odd step's call), one arc
+// load (the chain's only dependent memory access), then y(v) by a shared-memory probe (keys
+// or membership filter staged per tile; a global probe only when the filter cannot exclude v)
+// whose value load is consumed one step later.  y values are added in step order (R9, R13).
+template <int ARC, int NP>
+__device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
+                                            const int32_t *__restrict__ cols,
+                                            const unsigned long long *__restrict__ parcs, PackSpec pk, int mode,
+                                            const int32_t *sbase, const int32_t *__restrict__ gkeys,
+                                            const double *__restrict__ gvals, int lgb, int flg, uint64_t pol,
+                                            int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b,
+                                            const uint64_t *kk, uint32_t key0, uint32_t key1, double *acc,
+                                            int32_t *endv, int hints)
+{
+    constexpr int C = 2 * NP;
+    uint2 R[C];
+    int32_t v[C];
+    double pv[C];
+    uint32_t cz[C], cw[C];
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+        v[c] = (c & 1) ? t : s;
+        R[c] = __ldg(rec + v[c]);
+        acc[c] = 0.0;
+        pv[c] = 0.0;
+        cz[c] = 0u;
+        cw[c] = 0u;
+    }
+    const uint64_t pl = (hints & 2) ? pol_evict_last() : 0;
+    for (int32_t j = 1; j <= lf; j++) {
+        uint4 A[C];
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            uint64_t r64;
+            if (j & 1) {
+                const uint64_t k = kk[c >> 1];
+                const U4 r = philox4x32_10(U4{(uint32_t)((j - 1) >> 1), (uint32_t)k, q,
+                                              (b << 29) | ((uint32_t)(c & 1) << 28) | (uint32_t)(k >> 32)},
+                                           key0, key1);
+                r64 = ((uint64_t)r.y << 32) | r.x;
+                cz[c] = r.z;
+                cw[c] = r.w;
+            } else {
+                r64 = ((uint64_t)cw[c] << 32) | cz[c];
+            }
+            A[c] = next_arc<ARC>(R[c], r64, arcs, cols, parcs, pk, pl);
+        }
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            acc[c] += pv[c];   // y of the previous step, in step order
+            pv[c] = 0.0;
+            v[c] = (int32_t)A[c].x;
+            if (ARC) R[c] = make_uint2(A[c].y, A[c].z);
+            else R[c] = __ldg(rec + v[c]);
+            int64_t slot;
+            if (mode == YM_SMEM) {
+                slot = ylookup_smem(sbase, lgb, v[c]);
+            } else {
+                slot = -1;
+                bool maybe = true;
+                if (mode == YM_FILTER) {
+                    const uint32_t fb = fbit(v[c], flg);
+                    maybe = (reinterpret_cast<const uint32_t *>(sbase)[fb >> 5] >> (fb & 31)) & 1u;
+                }
+                if (maybe) slot = ylookup_global(gkeys, lgb, v[c], pol);
+            }
+            if (slot >= 0) pv[c] = ldg_f64(gvals + slot, pol);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+        acc[c] += pv[c];
+        endv[c] = v[c];
+    }
+}
+
+// K6: warp = one chunk of 32 NP walk pairs of one query (chunks of all AMC queries are laid
+// out query after query, queries ordered by descending ell_f; lane l, pair p runs walk
+// k = 32 NP chunk' + 32 p + l).  Per CTA-tile of WALK_WARPS chunks, a staging plan puts each
+// distinct query's key table (if it fits) or else its membership filter into shared memory; a
+// query for which neither fits probes global memory.  Each warp writes the canonical partial
+// {sum Z, sum Z^2, checksum} of its chunk.
+template <int ARC, int NP, int MINB>
+__global__ void __launch_bounds__(WALK_THREADS, MINB)
+k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
+        const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
+        const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
+        uint32_t key0, uint32_t key1, int64_t qbase, int32_t smem_words, int hints, TilePart *__restrict__ parts)
+{
+    extern __shared__ __align__(32) int32_t sm_words[];
+    __shared__ int32_t s_qi[WALK_WARPS];
+    __shared__ int32_t s_soff[WALK_WARPS];
+    __shared__ int32_t s_mode[WALK_WARPS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
+    const uint64_t pol = (hints & 1) ? pol_evict_first() : 0;
+    // persistent: CTA-tiles of WALK_WARPS consecutive chunks, round-robin over the grid
+    for (int64_t tile = blockIdx.x; tile * WALK_WARPS < nchunks; tile += gridDim.x) {
+        const int64_t chunk = tile * WALK_WARPS + warp;
+        const bool wvalid = chunk < nchunks;
+        const int32_t i = wvalid ? find_chunk_query(cincl, na, chunk) : -1;
+        if (lane == 0) s_qi[warp] = i;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // prefix-fit staging plan over the distinct queries of this tile (consecutive warps)
+            int32_t used = 0;
+            for (int w = 0; w < WALK_WARPS; w++) {
+                const int32_t qi = s_qi[w];
+                s_mode[w] = YM_GLOBAL;
+                s_soff[w] = 0;
+                if (qi < 0) continue;
+                if (w > 0 && s_qi[w - 1] == qi) { s_soff[w] = s_soff[w - 1]; s_mode[w] = s_mode[w - 1]; continue; }
+                const QState &Q = qs[amc[qi]];
+                const int32_t cap = 1 << Q.ylog2;
+                const int32_t fwords = Q.flog2 > 0 ? (1 << (Q.flog2 - 5)) : 0;
+                if (cap <= WALK_KEY_SLOTS && used + cap <= smem_words) {
+                    s_soff[w] = used; s_mode[w] = YM_SMEM; used += cap;
+                } else if (fwords > 0 && used + fwords <= smem_words) {
+                    s_soff[w] = used; s_mode[w] = YM_FILTER; used += fwords;
+                }
+            }
+        }
+        __syncthreads();
+        for (int w = 0; w < WALK_WARPS; w++) {
+            if (s_mode[w] == YM_GLOBAL || (w > 0 && s_qi[w - 1] == s_qi[w])) continue;
+            const QState &Q = qs[amc[s_qi[w]]];
+            const int4 *src;
+            int32_t words;
+            if (s_mode[w] == YM_SMEM) {
+                src = reinterpret_cast<const int4 *>(Q.ykeys);
+                words = 1 << Q.ylog2;
+            } else {
+                src = reinterpret_cast<const int4 *>(Q.yfilt);
+                words = 1 << (Q.flog2 - 5);
+            }
+            int4 *dst = reinterpret_cast<int4 *>(sm_words + s_soff[w]);
+            for (int32_t e = threadIdx.x; e < words / 4; e += WALK_THREADS) dst[e] = __ldg(src + e);
+        }
+        __syncthreads();
+        if (wvalid) {
+            const int32_t qi = amc[i];
+            const QState &Q = qs[qi];
+            const int64_t c0 = i == 0 ? 0 : cincl[i - 1];
+            const int64_t eta = Q.st.eta0 << b;
+            const uint32_t q = (uint32_t)(qbase + qi);
+            uint64_t kk[NP];
+            bool any = false;
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                kk[p] = (uint64_t)(chunk - c0) * (32u * NP) + 32u * p + (uint64_t)lane;
+                any |= kk[p] < (uint64_t)eta;
+            }
+            double acc[2 * NP];
+            int32_t endv[2 * NP];
+            double s1 = 0.0, s2 = 0.0;
+            uint64_t ck = 0ull;
+            if (any) {
+                walk_chains<ARC, NP>(rec, arcs, cols, parcs, pk, s_mode[warp], sm_words + s_soff[warp], Q.ykeys,
+                                     Q.yvals, Q.ylog2 - YB_LOG, Q.flog2, pol, Q.s, Q.t, Q.st.ell_f, q,
+                                     (uint32_t)b, kk, key0, key1, acc, endv, hints);
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    if (kk[p] < (uint64_t)eta) {
+                        const double z = acc[2 * p] - acc[2 * p + 1];   // Z_k (Alg. 1 L8)
+                        s1 += z;
+                        s2 += z * z;
+                        ck += walk_hash(q, (uint32_t)b, 0u, kk[p], endv[2 * p]) +
+                              walk_hash(q, (uint32_t)b, 1u, kk[p], endv[2 * p + 1]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+                ck += __shfl_xor_sync(0xffffffffu, ck, o);
+            }
+            if (lane == 0) {
+                TilePart tp;
+                tp.s1 = s1;
+                tp.s2 = s2;
+                tp.ck = ck;
+                tp.pad = 0;
+                parts[chunk] = tp;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---- K6 v3 (the previous walk kernel, kept for A/B measurement: GEER_WALK_KERNEL=3)
+constexpr int WALK3_SMEM_SLOTS = 8192;
 template <bool SMEM>
-__device__ __forceinline__ void load_bucket(const int32_t *keys, uint32_t bk, int4 &a, int4 &b)
+__device__ __forceinline__ void load_bucket3(const int32_t *keys, uint32_t bk, int4 &a, int4 &b)
 {
     const int32_t *p = keys + (size_t)bk * YB;
     if (SMEM) {
@@ -582,13 +944,13 @@ __device__ __forceinline__ void load_bucket(const int32_t *keys, uint32_t bk, in
 
 // Slow path: v not in its first bucket and the bucket is full -> probe the following buckets.
 template <bool SMEM>
-__device__ __forceinline__ double probe_rest(const int32_t *keys, const double *__restrict__ vals, uint32_t bk,
+__device__ __forceinline__ double probe_rest3(const int32_t *keys, const double *__restrict__ vals, uint32_t bk,
                                           uint32_t bmask, int32_t v)
 {
     while (true) {
         bk = (bk + 1) & bmask;
         int4 a, b;
-        load_bucket<SMEM>(keys, bk, a, b);
+        load_bucket3<SMEM>(keys, bk, a, b);
         bool empty;
         const int m = bucket_match(a, b, v, &empty);
         if (m >= 0) return __ldg(vals + (size_t)bk * YB + m);
@@ -602,7 +964,7 @@ __device__ __forceinline__ double probe_rest(const int32_t *keys, const double *
 // serial.  Arc records {u, off(u), d(u), -} make the chain one 16-byte load per step.
 // y values are added in step order (R9, R13).
 template <bool SMEM, int ARC>
-__device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
+__device__ __forceinline__ void walk_pair3(const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
                                           const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs,
                                           PackSpec pk,
                                           const int32_t *keys, const double *__restrict__ vals, int lgb,
@@ -654,9 +1016,9 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
             pvS = 0.0;
             pvT = 0.0;
             if (mS >= 0) pvS = __ldg(vals + (size_t)bS * YB + mS);
-            else if (!eS) aS += probe_rest<SMEM>(keys, vals, bS, bmask, vS);
+            else if (!eS) aS += probe_rest3<SMEM>(keys, vals, bS, bmask, vS);
             if (mT >= 0) pvT = __ldg(vals + (size_t)bT * YB + mT);
-            else if (!eT) aT += probe_rest<SMEM>(keys, vals, bT, bmask, vT);
+            else if (!eT) aT += probe_rest3<SMEM>(keys, vals, bT, bmask, vT);
         }
         vS = (int32_t)AS.x;
         vT = (int32_t)AT.x;
@@ -667,8 +1029,8 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
             RS = __ldg(rec + vS);
             RT = __ldg(rec + vT);
         }
-        load_bucket<SMEM>(keys, ybucket(vS, lgb), kS0, kS1);
-        load_bucket<SMEM>(keys, ybucket(vT, lgb), kT0, kT1);
+        load_bucket3<SMEM>(keys, ybucket(vS, lgb), kS0, kS1);
+        load_bucket3<SMEM>(keys, ybucket(vT, lgb), kT0, kT1);
     }
     // resolve the last step
     aS += pvS;
@@ -679,9 +1041,9 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
         const int mS = bucket_match(kS0, kS1, vS, &eS);
         const int mT = bucket_match(kT0, kT1, vT, &eT);
         if (mS >= 0) aS += __ldg(vals + (size_t)bS * YB + mS);
-        else if (!eS) aS += probe_rest<SMEM>(keys, vals, bS, bmask, vS);
+        else if (!eS) aS += probe_rest3<SMEM>(keys, vals, bS, bmask, vS);
         if (mT >= 0) aT += __ldg(vals + (size_t)bT * YB + mT);
-        else if (!eT) aT += probe_rest<SMEM>(keys, vals, bT, bmask, vT);
+        else if (!eT) aT += probe_rest3<SMEM>(keys, vals, bT, bmask, vT);
     }
     accS = aS;
     accT = aT;
@@ -695,13 +1057,12 @@ __device__ __forceinline__ void walk_pair(const uint2 *__restrict__ rec, const u
 // Each warp writes the canonical partial {sum Z, sum Z^2, checksum} of its chunk.
 template <int ARC>
 __global__ void __launch_bounds__(WALK_THREADS, 4)
-k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
+k_walks3(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
         const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
         const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs, PackSpec pk,
-        const int32_t *__restrict__ ykeys, const double *__restrict__ yvals, int b, uint32_t key0, uint32_t key1,
-        int64_t qbase, TilePart *__restrict__ parts)
+        int b, uint32_t key0, uint32_t key1, int64_t qbase, TilePart *__restrict__ parts)
 {
-    __shared__ __align__(32) int32_t sm_keys[WALK_SMEM_SLOTS];
+    __shared__ __align__(32) int32_t sm_keys[WALK3_SMEM_SLOTS];
     __shared__ int32_t s_qi[WALK_WARPS];
     __shared__ int32_t s_soff[WALK_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -721,7 +1082,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
                 if (qi < 0) { s_soff[w] = -1; continue; }
                 if (w > 0 && s_qi[w - 1] == qi) { s_soff[w] = s_soff[w - 1]; continue; }
                 const int32_t cap = 1 << qs[amc[qi]].ylog2;
-                if (used + cap <= WALK_SMEM_SLOTS) { s_soff[w] = used; used += cap; }
+                if (used + cap <= WALK3_SMEM_SLOTS) { s_soff[w] = used; used += cap; }
                 else s_soff[w] = -1;
             }
         }
@@ -730,7 +1091,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             if (s_soff[w] < 0 || (w > 0 && s_qi[w - 1] == s_qi[w])) continue;
             const QState &Q = qs[amc[s_qi[w]]];
             const int32_t cap = 1 << Q.ylog2;
-            const int4 *src = reinterpret_cast<const int4 *>(ykeys + Q.yoff);
+            const int4 *src = reinterpret_cast<const int4 *>(Q.ykeys);
             int4 *dst = reinterpret_cast<int4 *>(sm_keys + s_soff[w]);
             for (int32_t e = threadIdx.x; e < cap / 4; e += WALK_THREADS) dst[e] = __ldg(src + e);
         }
@@ -744,15 +1105,15 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             const bool active = k < (uint64_t)eta;
             const uint32_t q = (uint32_t)(qbase + qi);
             const int lgb = Q.ylog2 - YB_LOG;
-            const double *vals = yvals + Q.yoff;
+            const double *vals = Q.yvals;
             double aS = 0.0, aT = 0.0;
             int32_t eS = 0, eT = 0;
             if (active) {
                 if (s_soff[warp] >= 0)
-                    walk_pair<true, ARC>(rec, arcs, cols, parcs, pk, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t,
+                    walk_pair3<true, ARC>(rec, arcs, cols, parcs, pk, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t,
                                          Q.st.ell_f, q, (uint32_t)b, k, key0, key1, aS, aT, eS, eT);
                 else
-                    walk_pair<false, ARC>(rec, arcs, cols, parcs, pk, ykeys + Q.yoff, vals, lgb, Q.s, Q.t,
+                    walk_pair3<false, ARC>(rec, arcs, cols, parcs, pk, Q.ykeys, vals, lgb, Q.s, Q.t,
                                           Q.st.ell_f, q, (uint32_t)b, k, key0, key1, aS, aT, eS, eT);
             }
             const double z = active ? aS - aT : 0.0;
@@ -850,6 +1211,7 @@ __global__ void k_finalize(int64_t k, const QState *__restrict__ qs, double *__r
     if (i >= k) return;
     const QState &Q = qs[i];
     er_query_stats st = Q.st;
+    st.ytable_log2 = (uint32_t)Q.ylog2;
     double r;
     if (Q.s == Q.t) {
         memset(&st, 0, sizeof(st));
@@ -867,22 +1229,6 @@ __global__ void k_select(int32_t n, const int32_t *__restrict__ in, const int32_
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n && flag[i]) out[incl[i] - 1] = in[i];
-}
-
-// ============================================================================ K9: dense SpMM
-// Y[v, c] = (sum_{w in N(v)} X[w, c]) [/ d(v)], sequential over the row in CSR order.
-// One thread per (row, column); consecutive threads = consecutive columns of one row.
-__global__ void k_spmm_simple(int64_t n, int32_t q, const int64_t *__restrict__ off, const int32_t *__restrict__ cols,
-                              const double *__restrict__ X, double *__restrict__ Y, int normalize)
-{
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= n * q) return;
-    const int64_t v = tid / q;
-    const int32_t c = (int32_t)(tid - v * q);
-    const int64_t e0 = off[v], e1 = off[v + 1];
-    double sum = 0.0;
-    for (int64_t e = e0; e < e1; e++) sum += X[(int64_t)__ldg(cols + e) * q + c];
-    Y[tid] = normalize ? sum / (double)(e1 - e0) : sum;
 }
 
 // ============================================================================ host side
@@ -926,7 +1272,7 @@ void Workspace::release()
 {
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2, &head,
-                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals, &ytmp, &cont2, &idx2};
+                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals, &ytmp, &cont2, &idx2, &spmm_part};
     for (DevBuf *b : all) b->release();
     if (host_pinned) cudaFreeHost(host_pinned);
     host_pinned = nullptr;
@@ -1012,40 +1358,46 @@ int select_list(Ctx &c, const int32_t *ids, const int32_t *flag, int32_t n, int3
 // *keys / *vals (freed at the end of the batch); QState.yoff is relative to it.
 int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, const int64_t *segoff,
                   const int32_t *id, const double *val, const int32_t *seg, int64_t Fmax, const int64_t *dF,
-                  int32_t **keys_out, double **vals_out)
+                  int32_t **keys_out, double **vals_out, uint32_t **filt_out)
 {
     Workspace &ws = c.ws;
     *keys_out = nullptr;
     *vals_out = nullptr;
-    ENSURE(ws.ycap, sizeof(int64_t) * (na + 1), false);
-    ENSURE(ws.yoff, sizeof(int64_t) * (na + 1), false);
+    *filt_out = nullptr;
+    ENSURE(ws.ycap, sizeof(int64_t) * 2 * (na + 1), false);
+    ENSURE(ws.yoff, sizeof(int64_t) * 2 * (na + 1), false);
     int64_t *ycap = ws.ycap.as<int64_t>(), *yincl = ws.yoff.as<int64_t>();
-    k_ycap<<<blocks_for(na, 256), 256, 0, c.st>>>(na, act, ws.qs.as<QState>(), cont, segoff, ycap);
+    int64_t *fw = ycap + (na + 1), *fincl = yincl + (na + 1);
+    k_ycap<<<blocks_for(na, 256), 256, 0, c.st>>>(na, act, ws.qs.as<QState>(), cont, segoff, ycap, fw);
     LAUNCHED(c.g);
     int rc = scan_incl(c, ycap, yincl, na);
     if (rc) return rc;
-    rc = read_scalars(c, {yincl + (na - 1)});
+    rc = scan_incl(c, fw, fincl, na);
     if (rc) return rc;
-    const int64_t Y = c.hp[0];
+    rc = read_scalars(c, {yincl + (na - 1), fincl + (na - 1)});
+    if (rc) return rc;
+    const int64_t Y = c.hp[0], FW = c.hp[1];
     if (Y == 0) return ER_OK;
+    if (c.g->profiling) c.g->prof.ytable_slots += Y;
     int32_t *keys = nullptr;
-    double *vals = nullptr, *ytmp = nullptr;
+    double *vals = nullptr;
+    uint32_t *filt = nullptr;
     CK(cudaMallocAsync((void **)&keys, sizeof(int32_t) * Y, c.st));
     CK(cudaMallocAsync((void **)&vals, sizeof(double) * Y, c.st));
-    CK(cudaMallocAsync((void **)&ytmp, sizeof(double) * Y, c.st));
-    k_yfill<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, keys, vals, ytmp);
+    if (FW > 0) CK(cudaMallocAsync((void **)&filt, sizeof(uint32_t) * FW, c.st));
+    k_yfill<<<blocks_for(std::max(Y, FW), 256), 256, 0, c.st>>>(Y, keys, vals, FW, filt);
     LAUNCHED(c.g);
-    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, ycap, yincl, 0, ws.qs.as<QState>());
+    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, ycap, yincl, fw, fincl, keys, vals, filt,
+                                                      ws.qs.as<QState>());
     LAUNCHED(c.g);
-    (void)segoff;
-    k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, act, ycap, ws.qs.as<QState>(), keys,
-                                                      vals, ytmp, 0);
-    LAUNCHED(c.g);
-    k_yfinal<<<blocks_for(Y, 256), 256, 0, c.st>>>(Y, 0, vals, ytmp);
-    LAUNCHED(c.g);
-    CK(cudaFreeAsync(ytmp, c.st));
+    for (int side = 0; side < 2; side++) {
+        k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, act, ycap, ws.qs.as<QState>(),
+                                                          keys, vals, filt, side);
+        LAUNCHED(c.g);
+    }
     *keys_out = keys;
     *vals_out = vals;
+    *filt_out = filt;
     return ER_OK;
 }
 
@@ -1056,6 +1408,7 @@ struct AmcGroup {
     int32_t *list = nullptr;     // query ids (device), sorted by descending ell_f
     int32_t *ykeys = nullptr;    // this group's y-table chunk
     double *yvals = nullptr;
+    uint32_t *filt = nullptr;    // this group's membership filters
     unsigned long long eta0_sum = 0;
 };
 
@@ -1070,7 +1423,8 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
     const int32_t na = G.na;
     if (na == 0) return ER_OK;
     // per-group buffers (stream ordered on the AMC stream)
-    int64_t maxch = (int64_t)((G.eta0_sum << (P.tau - 1)) / 32) + na + 1;
+    const int per_chunk = 32 * g->walk_np;
+    int64_t maxch = (int64_t)((G.eta0_sum << (P.tau - 1)) / per_chunk) + na + 1;
     uint32_t *kk = nullptr;
     int32_t *list2 = nullptr;
     int64_t *nch = nullptr, *cincl = nullptr;
@@ -1102,25 +1456,61 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
     const uint32_t key0 = (uint32_t)P.seed, key1 = (uint32_t)(P.seed >> 32);
     for (int b = 0; b < P.tau; b++) {
-        k_nchunks<<<blocks_for(na, 256), 256, 0, sb>>>(na, list, qs, b, nch);
+        k_nchunks<<<blocks_for(na, 256), 256, 0, sb>>>(na, list, qs, b, per_chunk, nch);
         LAUNCHED(g);
         size_t b2 = tbytes;
         CK(cub::DeviceScan::InclusiveSum(tmp, b2, nch, cincl, na, sb));
         g->launches += 2;
-        const int64_t bound = (int64_t)((G.eta0_sum << b) / 32) + na;   // chunks of batch b, at most
-        const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(4 * nsm, (bound + WALK_WARPS - 1) / WALK_WARPS));
+        const int64_t bound = (int64_t)((G.eta0_sum << b) / per_chunk) + na;   // chunks of batch b, at most
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (prof) {
             CK(cudaEventCreate(&e0));
             CK(cudaEventCreate(&e1));
             CK(cudaEventRecord(e0, sb));
         }
-#define WALK_ARGS                                                                                                   \
-    na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, G.ykeys, G.yvals, b, key0, key1, P.qbase, \
-        parts
-        if (g->d_parcs) k_walks<2><<<grid, WALK_THREADS, 0, sb>>>(WALK_ARGS);
-        else if (g->d_arcs) k_walks<1><<<grid, WALK_THREADS, 0, sb>>>(WALK_ARGS);
-        else k_walks<0><<<grid, WALK_THREADS, 0, sb>>>(WALK_ARGS);
+#define WALK_ARGS                                                                                           \
+    na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, P.qbase, smem_words, \
+        g->walk_hints, parts
+#define WALK_LAUNCH(ARC, NP, MINB)                                                                          \
+    do {                                                                                                    \
+        CK(cudaFuncSetAttribute(k_walks<ARC, NP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                (int)smem_bytes));                                                          \
+        int occ = 0;                                                                                        \
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walks<ARC, NP, MINB>, WALK_THREADS,        \
+                                                         smem_bytes));                                      \
+        /* persistent grid: exactly the resident CTAs (a second wave would serialise) */                    \
+        const unsigned grid = (unsigned)std::max<int64_t>(                                                  \
+            1, std::min<int64_t>((int64_t)std::max(occ, 1) * nsm, (bound + WALK_WARPS - 1) / WALK_WARPS));  \
+        g->walk_occ = occ;                                                                                  \
+        k_walks<ARC, NP, MINB><<<grid, WALK_THREADS, smem_bytes, sb>>>(WALK_ARGS);                          \
+    } while (0)
+#define WALK_ARC(NP, MINB)                                   \
+    do {                                                     \
+        if (g->d_parcs) WALK_LAUNCH(2, NP, MINB);            \
+        else if (g->d_arcs) WALK_LAUNCH(1, NP, MINB);        \
+        else WALK_LAUNCH(0, NP, MINB);                       \
+    } while (0)
+        if (g->walk_kernel == 3) {
+            const unsigned grid3 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(4 * nsm, (bound + WALK_WARPS - 1) / WALK_WARPS));
+            if (g->d_parcs) k_walks3<2><<<grid3, WALK_THREADS, 0, sb>>>(na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, P.qbase, parts);
+            else if (g->d_arcs) k_walks3<1><<<grid3, WALK_THREADS, 0, sb>>>(na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, P.qbase, parts);
+            else k_walks3<0><<<grid3, WALK_THREADS, 0, sb>>>(na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, P.qbase, parts);
+            g->walk_occ = 4;
+        } else {
+        const int32_t smem_words = g->walk_smem_words;
+        const size_t smem_bytes = sizeof(int32_t) * (size_t)smem_words;
+        if (g->walk_np == 1) {
+            if (g->walk_minb == 2) WALK_ARC(1, 2);
+            else if (g->walk_minb == 3) WALK_ARC(1, 3);
+            else WALK_ARC(1, 4);
+        } else {
+            if (g->walk_minb == 2) WALK_ARC(2, 2);
+            else if (g->walk_minb == 3) WALK_ARC(2, 3);
+            else WALK_ARC(2, 4);
+        }
+        }
+#undef WALK_ARC
+#undef WALK_LAUNCH
 #undef WALK_ARGS
         LAUNCHED(g);
         if (prof) {
@@ -1264,41 +1654,48 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         CK(cudaEventRecord(ev_start, st));
     }
     // the AMC stream starts after everything enqueued so far on the main stream (inputs, setup)
-    auto fork_group = [&](int32_t na, const int32_t *act, const int32_t *cont, int32_t *tkeys, double *tvals) -> int {
-        // list of the queries of act leaving now for AMC, copied into a group-owned buffer
-        int32_t *flag = ws.cont2.as<int32_t>();
-        k_flag_leave<<<blocks_for(na, 256), 256, 0, st>>>(na, act, qs, cont, flag);
-        LAUNCHED(g);
-        int64_t ng = 0;
-        int rr = select_list(c, act, flag, na, ws.act2.as<int32_t>(), ws.idx2.as<int32_t>(), &ng);
-        if (rr) return rr;
-        if (ng == 0) {
-            if (tkeys) R.bufs.push_back(tkeys);
-            if (tvals) R.bufs.push_back(tvals);
-            return ER_OK;
-        }
+    // Launch the AMC of a list of queries (all in phase PH_AMC with their y-tables built) on the
+    // AMC stream, after everything enqueued so far on the main stream.
+    auto launch_list = [&](int32_t ng, const int32_t *list_src) -> int {
         AmcGroup G;
-        G.na = (int32_t)ng;
+        G.na = ng;
         CK(cudaMallocAsync((void **)&G.list, sizeof(int32_t) * ng, st));
-        CK(cudaMemcpyAsync(G.list, ws.act2.p, sizeof(int32_t) * ng, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(G.list, list_src, sizeof(int32_t) * ng, cudaMemcpyDeviceToDevice, st));
         unsigned long long *d_sum = reinterpret_cast<unsigned long long *>(ws.scalars.as<int64_t>() + 4);
         CK(cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), st));
-        k_sum_eta0<<<blocks_for(ng, 256), 256, 0, st>>>((int32_t)ng, G.list, qs, d_sum);
+        k_sum_eta0<<<blocks_for(ng, 256), 256, 0, st>>>(ng, G.list, qs, d_sum);
         LAUNCHED(g);
-        rr = read_scalars(c, {reinterpret_cast<const int64_t *>(d_sum)});
+        int rr = read_scalars(c, {reinterpret_cast<const int64_t *>(d_sum)});
         if (rr) return rr;
         G.eta0_sum = (unsigned long long)c.hp[0];
-        G.ykeys = tkeys;
-        G.yvals = tvals;
         R.bufs.push_back(G.list);
-        if (tkeys) R.bufs.push_back(tkeys);
-        if (tvals) R.bufs.push_back(tvals);
         cudaEvent_t e;
         CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaEventRecord(e, st));
         CK(cudaStreamWaitEvent(sb, e, 0));
         cudaEventDestroy(e);
         return launch_amc_group(g, sb, G, qs, P, prof, R);
+    };
+    // Queries of an SMM wave that leave the head now: with overlap, their AMC starts at once on
+    // the AMC stream (concurrent with the remaining waves); otherwise all AMC queries run
+    // together after the head (fewer, fuller walk launches).  The tables' buffers live until
+    // the end of the batch either way.
+    const bool overlap = g->amc_overlap;
+    auto fork_group = [&](int32_t na, const int32_t *act, const int32_t *cont, int32_t *tkeys, double *tvals,
+                          uint32_t *tfilt) -> int {
+        if (tkeys) R.bufs.push_back(tkeys);
+        if (tvals) R.bufs.push_back(tvals);
+        if (tfilt) R.bufs.push_back(tfilt);
+        if (!overlap) return ER_OK;
+        // list of the queries of act leaving now for AMC
+        int32_t *flag = ws.cont2.as<int32_t>();
+        k_flag_leave<<<blocks_for(na, 256), 256, 0, st>>>(na, act, qs, cont, flag);
+        LAUNCHED(g);
+        int64_t ng = 0;
+        int rr = select_list(c, act, flag, na, ws.act2.as<int32_t>(), ws.idx2.as<int32_t>(), &ng);
+        if (rr) return rr;
+        if (ng == 0) return ER_OK;
+        return launch_list((int32_t)ng, ws.act2.as<int32_t>());
     };
     ENSURE(ws.scalars, sizeof(int64_t) * 8, false);
     ENSURE(ws.cont2, sizeof(int32_t) * (k + 1), false);
@@ -1333,11 +1730,12 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                 LAUNCHED(g);
                 int32_t *tk = nullptr;
                 double *tv = nullptr;
+                uint32_t *tf = nullptr;
                 rc = build_ytables(c, (int32_t)n0, ws.act.as<int32_t>(), nullptr, ws.fr_off.as<int64_t>(),
                                    ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(), ws.fr_seg.as<int32_t>(), F0, nullptr,
-                                   &tk, &tv);
+                                   &tk, &tv, &tf);
                 if (rc) return rc;
-                rc = fork_group((int32_t)n0, ws.act.as<int32_t>(), nullptr, tk, tv);
+                rc = fork_group((int32_t)n0, ws.act.as<int32_t>(), nullptr, tk, tv, tf);
                 if (rc) return rc;
             }
             na = 0;
@@ -1424,11 +1822,12 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             {
                 int32_t *tk = nullptr;
                 double *tv = nullptr;
+                uint32_t *tf = nullptr;
                 rc = build_ytables(c, (int32_t)na, ws.act.as<int32_t>(), cont, ws.nf_off.as<int64_t>(),
                                    ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), E, dU, &tk,
-                                   &tv);
+                                   &tv, &tf);
                 if (rc) return rc;
-                rc = fork_group((int32_t)na, ws.act.as<int32_t>(), cont, tk, tv);
+                rc = fork_group((int32_t)na, ws.act.as<int32_t>(), cont, tk, tv, tf);
                 if (rc) return rc;
             }
             // compaction of continuing queries
@@ -1469,7 +1868,23 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         }
     }
 
-    if (prof) CK(cudaEventRecord(ev_smm_end, st));
+    if (!overlap) {
+        // every query now in phase AMC: one AMC run over all of them
+        ENSURE(ws.ids, sizeof(int32_t) * (k + 1), false);
+        k_flag_phase<<<blocks_for(k, 256), 256, 0, st>>>(k, qs, PH_AMC, ws.cont.as<int32_t>(), ws.ids.as<int32_t>());
+        LAUNCHED(g);
+        int64_t n_amc = 0;
+        rc = select_list(c, ws.ids.as<int32_t>(), ws.cont.as<int32_t>(), K, ws.act.as<int32_t>(),
+                         ws.idx.as<int32_t>(), &n_amc);
+        if (rc) return rc;
+        if (prof) CK(cudaEventRecord(ev_smm_end, st));
+        if (n_amc > 0) {
+            rc = launch_list((int32_t)n_amc, ws.act.as<int32_t>());
+            if (rc) return rc;
+        }
+    } else if (prof) {
+        CK(cudaEventRecord(ev_smm_end, st));
+    }
     // join: results need every group's AMC
     CK(cudaEventRecord(ev_amc_done, sb));
     CK(cudaStreamWaitEvent(st, ev_amc_done, 0));
@@ -1555,15 +1970,6 @@ cudaError_t build_arcs(er_graph *g)
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     return e;
-}
-
-int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st)
-{
-    const int64_t total = g->n * (int64_t)q;
-    k_spmm_simple<<<blocks_for(total, 256), 256, 0, st>>>(g->n, q, g->d_off, g->d_cols, X, Y, normalize);
-    LAUNCHED(g);
-    CK(cudaGetLastError());
-    return ER_OK;
 }
 
 }  // namespace geer

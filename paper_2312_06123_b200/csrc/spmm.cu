@@ -1,0 +1,275 @@
+// spmm.cu -- K9: dense-block SpMM  Y = M X  for a row-major n x q fp64 block, M = D^-1 A or A.
+//
+// This is the dense form of Alg. 2 L4 "s* <- P s*" applied to q columns at once (the
+// SMM / SMM-to-ell ground-truth engine) and of Fig. 3's #path recursion with
+// A in place of P.  Per (row v, column c):
+//
+//     Y[v, c] = ( sum_{w in N(v)} X[w, c] ) / d(v)        (the /d(v) only when normalize)
+//
+// Summation order (R13, "K9"): rows of degree <= SPMM_SEG are summed SEQUENTIALLY in
+// the row's CSR order, so they are bit-identical to the oracle's dense pull
+// (oracle_propagate_dense); a longer row is cut into consecutive segments of SPMM_SEG
+// neighbours, each summed sequentially, and the segment sums are then added sequentially in
+// segment order (a fixed order: run-to-run bit-reproducible, within a few ulps of the plain
+// sequential sum).
+//
+// Layout and load balance ("K9"):
+//  * once per graph, the work items are built: one per heavy-row segment, then one per light
+//    row (degree <= SPMM_SEG) in degree-descending order, so the long items start first and a
+//    warp's sub-warps see similar lengths;
+//  * one sub-warp of LPR lanes per item; lane l owns the 16-byte column vectors l, l+LPR, ...
+//    of the row (128-bit loads of X rows, coalesced across the sub-warp); the neighbour loop is
+//    unrolled by 8 so 8 independent gathers are in flight per lane, then added in CSR order;
+//  * heavy-row segment sums go to a scratch block and a second kernel adds them per row.
+// No tensor cores: the contraction has one nonzero per (row, neighbour) and fp64 accumulation.
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "geer_internal.h"
+
+namespace geer {
+
+namespace {
+
+constexpr int SPMM_THREADS = 256;
+constexpr int SPMM_UNROLL = 8;
+
+inline unsigned blocks_for(int64_t n, int per) { return (unsigned)((n + per - 1) / per); }
+
+template <int VEC> struct VecT;
+template <> struct VecT<1> { using T = double; };
+template <> struct VecT<2> { using T = double2; };
+
+__device__ __forceinline__ void vadd(double &a, const double b) { a += b; }
+__device__ __forceinline__ void vadd(double2 &a, const double2 b) { a.x += b.x; a.y += b.y; }
+__device__ __forceinline__ void vzero(double &a) { a = 0.0; }
+__device__ __forceinline__ void vzero(double2 &a) { a.x = 0.0; a.y = 0.0; }
+__device__ __forceinline__ void vdiv(double &a, double d) { a = a / d; }
+__device__ __forceinline__ void vdiv(double2 &a, double d) { a.x = a.x / d; a.y = a.y / d; }
+
+// Items [0, nseg) are heavy-row segments (segment p covers cols[seg_e0[p], min(seg_e0[p] +
+// SPMM_SEG, off[row + 1])) of row seg_row[p] and writes the segment sum to part[p]); items
+// [nseg, nitems) are the light rows rows[item - nseg] (full row, written to Y).
+template <int LPR, int VEC>
+__global__ void __launch_bounds__(SPMM_THREADS)
+k_spmm_rows(int64_t nseg, int64_t nitems, const int64_t *__restrict__ seg_e0, const int32_t *__restrict__ seg_row,
+            const int32_t *__restrict__ rows, const int64_t *__restrict__ off, const int32_t *__restrict__ cols,
+            const double *__restrict__ X, double *__restrict__ Y, double *__restrict__ part, int32_t q, int normalize)
+{
+    using V = typename VecT<VEC>::T;
+    const int64_t it = ((int64_t)blockIdx.x * SPMM_THREADS + threadIdx.x) / LPR;
+    const int l = threadIdx.x % LPR;
+    if (it >= nitems) return;
+    int64_t e0, e1;
+    V *out;
+    bool norm;
+    double dv;
+    const int32_t nvec = q / VEC;
+    if (it < nseg) {
+        const int32_t v = seg_row[it];
+        e0 = seg_e0[it];
+        e1 = min(e0 + (int64_t)SPMM_SEG, off[v + 1]);
+        out = reinterpret_cast<V *>(part) + it * nvec;
+        norm = false;
+        dv = 1.0;
+    } else {
+        const int32_t v = rows[it - nseg];
+        e0 = off[v];
+        e1 = off[v + 1];
+        out = reinterpret_cast<V *>(Y) + (int64_t)v * nvec;
+        norm = normalize != 0;
+        dv = (double)(e1 - e0);
+    }
+    const V *__restrict__ Xv = reinterpret_cast<const V *>(X);
+    for (int32_t cv = l; cv < nvec; cv += LPR) {
+        V acc;
+        vzero(acc);
+        int64_t e = e0;
+        for (; e + SPMM_UNROLL <= e1; e += SPMM_UNROLL) {
+            int32_t w[SPMM_UNROLL];
+#pragma unroll
+            for (int j = 0; j < SPMM_UNROLL; j++) w[j] = __ldg(cols + e + j);
+            V x[SPMM_UNROLL];
+#pragma unroll
+            for (int j = 0; j < SPMM_UNROLL; j++) x[j] = __ldg(Xv + (int64_t)w[j] * nvec + cv);
+#pragma unroll
+            for (int j = 0; j < SPMM_UNROLL; j++) vadd(acc, x[j]);   // CSR order (R13)
+        }
+        if (e < e1) {
+            const int rem = (int)(e1 - e);
+            int32_t w[SPMM_UNROLL];
+#pragma unroll
+            for (int j = 0; j < SPMM_UNROLL; j++) w[j] = j < rem ? __ldg(cols + e + j) : 0;
+            V x[SPMM_UNROLL];
+#pragma unroll
+            for (int j = 0; j < SPMM_UNROLL; j++)
+                if (j < rem) x[j] = __ldg(Xv + (int64_t)w[j] * nvec + cv);
+#pragma unroll
+            for (int j = 0; j < SPMM_UNROLL; j++)
+                if (j < rem) vadd(acc, x[j]);
+        }
+        if (norm) vdiv(acc, dv);
+        out[cv] = acc;
+    }
+}
+
+// Heavy rows: Y[v, c] = (segment sums of v, added in segment order) [/ d(v)].  One thread per
+// (heavy row, column).
+__global__ void k_spmm_heavy_sum(int64_t nheavy, const int32_t *__restrict__ rows, const int64_t *__restrict__ hseg,
+                                 const int64_t *__restrict__ off, const double *__restrict__ part,
+                                 double *__restrict__ Y, int32_t q, int normalize)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nheavy * q) return;
+    const int64_t h = t / q;
+    const int32_t c = (int32_t)(t - h * q);
+    const int32_t v = rows[h];
+    double acc = 0.0;
+    for (int64_t p = hseg[h]; p < hseg[h + 1]; p++) acc += part[p * q + c];
+    Y[(int64_t)v * q + c] = normalize ? acc / (double)(off[v + 1] - off[v]) : acc;
+}
+
+__global__ void k_deg_key(int64_t n, const int64_t *__restrict__ off, uint32_t *__restrict__ key,
+                          int32_t *__restrict__ ids)
+{
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int64_t d = off[v + 1] - off[v];
+    key[v] = ~(uint32_t)std::min<int64_t>(d, 0xffffffffll);   // descending degree
+    ids[v] = (int32_t)v;
+}
+
+// Segment table of the heavy rows (the first nheavy rows of the permutation): hseg[h] = first
+// segment of heavy row h (exclusive prefix of ceil(d / SPMM_SEG)).
+__global__ void k_fill_segs(int64_t nheavy, const int32_t *__restrict__ rows, const int64_t *__restrict__ hseg,
+                            const int64_t *__restrict__ off, int64_t *__restrict__ seg_e0, int32_t *__restrict__ seg_row)
+{
+    const int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= nheavy) return;
+    const int32_t v = rows[h];
+    for (int64_t p = hseg[h]; p < hseg[h + 1]; p++) {
+        seg_e0[p] = off[v] + (p - hseg[h]) * SPMM_SEG;
+        seg_row[p] = v;
+    }
+}
+
+#define CK(call)                                            \
+    do {                                                    \
+        cudaError_t _e = (call);                            \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+// Degree-descending row permutation (stable: equal degrees keep ascending ids), the heavy
+// prefix (degree > SPMM_SEG) and its segment table.
+int build_spmm_plan(er_graph *g, cudaStream_t st)
+{
+    const int64_t n = g->n;
+    uint32_t *k1 = nullptr, *k2 = nullptr;
+    int32_t *ids = nullptr;
+    void *tmp = nullptr;
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k2, ids, g->d_rowperm, (int)n, 0, 32, st));
+    CK(cudaMalloc(&g->d_rowperm, sizeof(int32_t) * n));
+    CK(cudaMallocAsync((void **)&k1, sizeof(uint32_t) * n, st));
+    CK(cudaMallocAsync((void **)&k2, sizeof(uint32_t) * n, st));
+    CK(cudaMallocAsync((void **)&ids, sizeof(int32_t) * n, st));
+    CK(cudaMallocAsync(&tmp, tb + 16, st));
+    k_deg_key<<<blocks_for(n, 256), 256, 0, st>>>(n, g->d_off, k1, ids);
+    g->launches++;
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k2, ids, g->d_rowperm, (int)n, 0, 32, st));
+    g->launches += 2;
+    CK(cudaFreeAsync(k1, st));
+    CK(cudaFreeAsync(k2, st));
+    CK(cudaFreeAsync(ids, st));
+    CK(cudaFreeAsync(tmp, st));
+    CK(cudaStreamSynchronize(st));
+    // heavy prefix: rows are degree-descending, binary search for the first degree <= SPMM_SEG
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        int32_t v = 0;
+        int64_t o[2];
+        CK(cudaMemcpy(&v, g->d_rowperm + mid, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(o, g->d_off + v, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        if (o[1] - o[0] <= SPMM_SEG) hi = mid;
+        else lo = mid + 1;
+    }
+    const int64_t nh = lo;
+    g->n_heavy = nh;
+    g->n_seg = 0;
+    if (nh > 0) {
+        std::vector<int32_t> hrows(nh);
+        CK(cudaMemcpy(hrows.data(), g->d_rowperm, sizeof(int32_t) * nh, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> hseg(nh + 1, 0);
+        for (int64_t h = 0; h < nh; h++) {
+            int64_t o[2];
+            CK(cudaMemcpy(o, g->d_off + hrows[h], 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+            hseg[h + 1] = hseg[h] + (o[1] - o[0] + SPMM_SEG - 1) / SPMM_SEG;
+        }
+        const int64_t ns = hseg[nh];
+        g->n_seg = ns;
+        CK(cudaMalloc(&g->d_hseg, sizeof(int64_t) * (nh + 1)));
+        CK(cudaMalloc(&g->d_seg_e0, sizeof(int64_t) * ns));
+        CK(cudaMalloc(&g->d_seg_row, sizeof(int32_t) * ns));
+        CK(cudaMemcpy(g->d_hseg, hseg.data(), sizeof(int64_t) * (nh + 1), cudaMemcpyHostToDevice));
+        k_fill_segs<<<blocks_for(nh, 128), 128, 0, st>>>(nh, g->d_rowperm, g->d_hseg, g->d_off, g->d_seg_e0,
+                                                         g->d_seg_row);
+        g->launches++;
+        CK(cudaStreamSynchronize(st));
+    }
+    return ER_OK;
+}
+
+template <int VEC>
+void launch_rows(er_graph *g, const double *X, double *Y, double *part, int32_t q, int normalize, cudaStream_t st)
+{
+    const int nvec = q / VEC;
+    int lpr = 1;
+    while (lpr < nvec && lpr < 32) lpr <<= 1;
+    const int64_t nitems = g->n_seg + (g->n - g->n_heavy);
+    const unsigned grid = blocks_for(nitems * lpr, SPMM_THREADS);
+#define L(LPR)                                                                                               \
+    k_spmm_rows<LPR, VEC><<<grid, SPMM_THREADS, 0, st>>>(g->n_seg, nitems, g->d_seg_e0, g->d_seg_row,          \
+                                                         g->d_rowperm + g->n_heavy, g->d_off, g->d_cols, X, Y, \
+                                                         part, q, normalize)
+    switch (lpr) {
+        case 1: L(1); break;
+        case 2: L(2); break;
+        case 4: L(4); break;
+        case 8: L(8); break;
+        case 16: L(16); break;
+        default: L(32); break;
+    }
+#undef L
+    g->launches++;
+}
+
+}  // namespace
+
+int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st)
+{
+    if (!g->d_rowperm) {
+        const int rc = build_spmm_plan(g, g->stream);
+        if (rc) return rc;
+    }
+    const bool vec2 = (q % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) % 16 == 0);
+    double *part = nullptr;
+    if (g->n_seg > 0) {
+        CK(g->ws.spmm_part.ensure(sizeof(double) * (size_t)g->n_seg * q, false, st));
+        part = g->ws.spmm_part.as<double>();
+    }
+    if (vec2) launch_rows<2>(g, X, Y, part, q, normalize, st);
+    else launch_rows<1>(g, X, Y, part, q, normalize, st);
+    if (g->n_heavy > 0) {
+        k_spmm_heavy_sum<<<blocks_for(g->n_heavy * q, 256), 256, 0, st>>>(g->n_heavy, g->d_rowperm, g->d_hseg,
+                                                                          g->d_off, part, Y, q, normalize);
+        g->launches++;
+    }
+    CK(cudaGetLastError());
+    return ER_OK;
+}
+
+}  // namespace geer

@@ -1,0 +1,13 @@
+set -x
+python __graft_entry__.py build > gpurun_out/build.log 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
+run() { tag=$1; shift; env "$@" timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-spmm > gpurun_out/bench_$tag.log 2>&1; }
+run v3 GEER_WALK_KERNEL=3
+run v3_overlap GEER_WALK_KERNEL=3 GEER_AMC_OVERLAP=1
+run np1_m4_s24 GEER_WALK_NP=1 GEER_WALK_MINB=4 GEER_WALK_SMEM_KB=24
+run np1_m4_s32 GEER_WALK_NP=1 GEER_WALK_MINB=4 GEER_WALK_SMEM_KB=32
+run np1_m3_s32 GEER_WALK_NP=1 GEER_WALK_MINB=3 GEER_WALK_SMEM_KB=32
+run np2_m3_s32 GEER_WALK_NP=2 GEER_WALK_MINB=3 GEER_WALK_SMEM_KB=32
+run np2_m4_s24 GEER_WALK_NP=2 GEER_WALK_MINB=4 GEER_WALK_SMEM_KB=24
+run np1_m4_s16 GEER_WALK_NP=1 GEER_WALK_MINB=4 GEER_WALK_SMEM_KB=16
+tail -3 gpurun_out/gpu_tests.log

@@ -268,3 +268,101 @@ def test_walk_layouts_byte_identical(geer, tiny, rmat20, graph):
         outs[lay] = (r.tobytes(), st.tobytes())
         geer.er_graph_destroy(h)
     assert outs["cols"] == outs["arcs"] == outs["packed"]
+
+
+def _hub_graph(n=3000, seed=5):
+    """Hubs of degree n-1 and 1500 (K9 rows cut into SPMM_SEG = 512 segments) over a sparse
+    random graph, plus rows of degree exactly 512 and 513 (the segment boundary)."""
+    rng = np.random.default_rng(seed)
+    E = [(0, i) for i in range(1, n)] + [(1, int(j)) for j in rng.choice(np.arange(2, n), min(1500, n - 2), replace=False)]
+    if n >= 1200:
+        E += [(2, int(j)) for j in range(3, 3 + 510)] + [(3, int(j)) for j in range(600, 600 + 510)]
+    iu = rng.integers(4, n, 4 * n)
+    ju = rng.integers(4, n, 4 * n)
+    E += [(int(a), int(b)) for a, b in zip(iu, ju) if a != b]
+    return W.from_edges(n, E, "hubs")
+
+
+def _seg_sum_pull(g, x, normalize, seg=512):
+    """K9's documented order (R13): sequential inside segments of 512 neighbours,
+    segment sums added in order; equals the plain sequential pull on rows of degree <= 512."""
+    y = np.zeros(g.n)
+    for v in range(g.n):
+        nb = g.neighbors(v)
+        acc = 0.0
+        for s0 in range(0, len(nb), seg):
+            part = 0.0
+            for w in nb[s0:s0 + seg]:
+                part += x[w]
+            acc += part
+        y[v] = acc / len(nb) if normalize else acc
+    return y
+
+
+@pytest.mark.parametrize("q", [1, 2, 3, 7, 16, 33, 64, 130, 256])
+def test_spmm_k9_every_column(geer, q):
+    """K9 (light rows and segmented heavy rows, both vector widths): rows of degree <= 512 are
+    bit-identical to the oracle's sequential dense pull (R13); longer rows equal the documented
+    segmented order bit for bit and the oracle within 1e-13 relative; for A and P = D^-1 A."""
+    import torch
+    g = _hub_graph()
+    d = g.degrees()
+    assert d.max() == g.n - 1 and (d > 512).sum() >= 2 and {512, 513} <= set(d.tolist())
+    light = d <= 512
+    h = geer.er_graph_create(g.n, g.offsets, g.cols, flags=geer.ER_CREATE_SPMM_ONLY)
+    try:
+        X = np.random.default_rng(q).random((g.n, q))
+        Xd = torch.from_numpy(X).cuda()
+        for normalize in (True, False):
+            Y = torch.full((g.n, q), np.nan, dtype=torch.float64, device="cuda")
+            geer.er_spmm(h, Xd, Y, normalize=normalize)
+            Yh = Y.cpu().numpy()
+            for c in range(q) if q <= 16 else (0, q // 2, q - 1):
+                want = oracle.propagate_dense(g, X[:, c], normalize=normalize)
+                assert np.array_equal(Yh[light, c], want[light]), (q, c, normalize)
+                assert np.allclose(Yh[~light, c], want[~light], rtol=1e-13, atol=0), (q, c, normalize)
+                assert np.array_equal(Yh[~light, c], _seg_sum_pull(g, X[:, c], normalize)[~light])
+    finally:
+        geer.er_graph_destroy(h)
+
+
+def test_spmm_k9_unaligned_block(geer):
+    """A block whose base is only 8-byte aligned takes the scalar path; same bits."""
+    import torch
+    g = _hub_graph(800, 7)
+    h = geer.er_graph_create(g.n, g.offsets, g.cols, flags=geer.ER_CREATE_SPMM_ONLY)
+    try:
+        q = 4
+        X = np.random.default_rng(1).random((g.n, q))
+        buf = torch.zeros(g.n * q + 1, dtype=torch.float64, device="cuda")
+        Xd = buf[1:].view(g.n, q)
+        Xd.copy_(torch.from_numpy(X))
+        ybuf = torch.zeros(g.n * q + 1, dtype=torch.float64, device="cuda")
+        Y = ybuf[1:].view(g.n, q)
+        geer.er_spmm(h, Xd, Y)
+        light = g.degrees() <= 512
+        for c in range(q):
+            want = oracle.propagate_dense(g, X[:, c])
+            got = Y.cpu().numpy()[:, c]
+            assert np.array_equal(got[light], want[light])
+            assert np.allclose(got[~light], want[~light], rtol=1e-13, atol=0)
+    finally:
+        geer.er_graph_destroy(h)
+
+
+def test_spmm_k9_rmat20_sampled_columns(geer, rmat20):
+    """At BASELINE config 1's full size, in bench.py's launch configuration (q = 16): two
+    columns checked against the oracle's pull over all n rows (bit-exact on rows of degree
+    <= 512, 1e-13 relative on the segmented hub rows)."""
+    import torch
+    g, _, _, h = rmat20
+    q = 16
+    X = np.random.default_rng(3).random((g.n, q))
+    Y = torch.empty((g.n, q), dtype=torch.float64, device="cuda")
+    geer.er_spmm(h, torch.from_numpy(X).cuda(), Y)
+    Yh = Y.cpu().numpy()
+    light = g.degrees() <= 512
+    for c in (0, 11):
+        want = oracle.propagate_dense(g, X[:, c])
+        assert np.array_equal(Yh[light, c], want[light])
+        assert np.allclose(Yh[~light, c], want[~light], rtol=1e-13, atol=0)
