@@ -170,15 +170,25 @@ def reference_arm(args):
     return 0
 
 
+WORKLOAD_NAMES = {
+    "rmat20": "R-MAT s20 ef5 (.57,.19,.19,.05) LCC",
+    "lj_full": "LiveJournal-shaped R-MAT s23 ef4.5 (.57,.19,.19,.05) LCC (GPU generator)",
+    "orkut_full": "Orkut-shaped R-MAT s22 ef28 (.45,.22,.22,.11) LCC (GPU generator)",
+    "lj": "LiveJournal-shaped R-MAT s23 ef4.5 (.57,.19,.19,.05) LCC",
+    "orkut": "Orkut-density R-MAT s18 ef40 (.45,.22,.22,.11) LCC",
+}
+
+
 def config_dict(g, args):
-    return {"workload": f"R-MAT s20 ef5 (.57,.19,.19,.05) LCC, {args.queries} queries/GPU "
+    return {"workload": f"{WORKLOAD_NAMES.get(args.config, args.config)}, {args.queries} queries/GPU "
                         f"(50% random pairs, 50% edges), eps={args.eps}, delta=0.01, tau=5",
             "n": int(g.n), "m": int(g.m), "max_degree": int(g.degrees().max()),
             "lambda": float(g.lam) if g.lam is not None else None,
             "queries_per_gpu": args.queries, "eps": args.eps, "delta": 0.01, "tau": 5,
             "parallelism": f"queries sharded over {args.gpus} GPU(s), CSR replicated",
             "l2": "flushed between steps (256 MiB device write outside the timed events)",
-            "seeds": {"graph": 20231211, "queries": 20231212, "walks": "0x2312061232DEC0DE"}}
+            "seeds": {"graph": getattr(args, "graph_seed", 20231211), "queries": "graph seed + 1 + rank",
+                      "walks": "0x2312061232DEC0DE"}}
 
 
 def spmm_measure(G, h, g, torch, q=SPMM_Q, reps=10):
@@ -219,6 +229,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spmm", action="store_true")
+    ap.add_argument("--config", default=CONFIG, help="workload (BASELINE configs[1] = rmat20 is the graded line)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -246,10 +257,12 @@ def main():
     import workloads as W
     from paper_2312_06123_b200.dist import gather_results
 
-    g, _, _ = W.load_config(CONFIG, with_lambda=False)
+    g, _, _ = W.load_config(args.config, with_lambda=False)
     nq = args.queries
     # rank r answers its own 10k-query set (weak scaling); rank 0's set is the N=1 set
-    pairs = np.ascontiguousarray(W.query_pairs(g, nq, seed=20231212 + rank))
+    gseed = W.CONFIGS[args.config][1]["seed"]
+    args.graph_seed = gseed
+    pairs = np.ascontiguousarray(W.query_pairs(g, nq, seed=gseed + 1 + rank))
     lo = rank * nq
     h = G.er_graph_create(g.n, g.offsets, g.cols)
     g.lam = G.er_graph_estimate_lambda(h)
@@ -347,6 +360,7 @@ def main():
                                    "smm_pairs_per_step": prof["smm_pairs"] / args.steps,
                                    "walk_steps_per_step": prof["walk_steps"] / args.steps,
                                    "ytable_slots_per_step": prof["ytable_slots"] / args.steps,
+                                   "yrank_records_per_step": prof["yrank_records"] / args.steps,
                                    "walk_ctas_per_sm": prof["walk_ctas_per_sm"]},
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(pairs.nbytes),
                     "d2h_bytes_per_step": int(nq * 8)},

@@ -124,6 +124,12 @@ typedef struct er_opts {
     int32_t ell_variant;       /* 0: Eq. 6 refined ell (default); 1: Eq. 5 Peng et al.'s ell */
     int32_t synchronous;       /* 1 (default): return after the results are final; 0: asynchronous on
                                   cuda_stream when both pointers are on the device */
+    int32_t pad0;
+    const int64_t *query_ids;  /* NULL (default): query i has global index query_index_base + i;
+                                  else query_ids[i] (k entries, host or device like pairs), each in
+                                  [0, 2^32).  The global index keys the query's RNG streams (R10),
+                                  so a query's result does not depend on which rank or batch runs
+                                  it (cost-model sharding, paper_2312_06123_b200/dist.py) */
 } er_opts;
 
 #define ER_DEFAULT_SEED 0x2312061232DEC0DEULL
@@ -187,7 +193,8 @@ typedef struct er_profile {
     int64_t walk_steps;      /* walk steps executed (both sides, all batches) */
     int64_t smm_pairs;       /* (u, x) pairs emitted by the SMM push over all waves */
     int64_t batches;         /* query batches profiled */
-    int64_t ytable_slots;    /* y-table slots allocated (Alg. 1 L7 tables of all AMC queries) */
+    int64_t ytable_slots;    /* hash y-table slots allocated (Alg. 1 L7 tables of the AMC queries) */
+    int64_t yrank_records;   /* rank-bitmap y-table records allocated (16 B per 64 node ids) */
     int64_t walk_ctas_per_sm; /* resident K6 CTAs per SM (occupancy API) at the last walk launch */
 } er_profile;
 int er_graph_profile(er_graph *g, int enable);

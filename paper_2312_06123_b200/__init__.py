@@ -47,14 +47,16 @@ class er_opts(ctypes.Structure):
     _fields_ = [("tau", ctypes.c_int32), ("force_ell_b", ctypes.c_int32), ("seed", ctypes.c_uint64),
                 ("query_index_base", ctypes.c_int64), ("cuda_stream", ctypes.c_void_p),
                 ("pairs_on_device", ctypes.c_int32), ("out_on_device", ctypes.c_int32),
-                ("ell_variant", ctypes.c_int32), ("synchronous", ctypes.c_int32)]
+                ("ell_variant", ctypes.c_int32), ("synchronous", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("query_ids", ctypes.c_void_p)]
 
 
 class er_profile(ctypes.Structure):
     _fields_ = [("smm_ms", ctypes.c_double), ("walk_ms", ctypes.c_double), ("amc_other_ms", ctypes.c_double),
                 ("walk_launches", ctypes.c_int64), ("walk_steps", ctypes.c_int64),
                 ("smm_pairs", ctypes.c_int64), ("batches", ctypes.c_int64),
-                ("ytable_slots", ctypes.c_int64), ("walk_ctas_per_sm", ctypes.c_int64)]
+                ("ytable_slots", ctypes.c_int64), ("yrank_records", ctypes.c_int64),
+                ("walk_ctas_per_sm", ctypes.c_int64)]
 
 
 class GeerError(RuntimeError):
@@ -184,7 +186,7 @@ def er_query_batch(g, pairs, eps: float, p_fail: float = 0.01):
 def er_query_batch_ex(g, pairs, eps: float, p_fail: float = 0.01, *, out=None, stats=None,
                       tau: int = 5, seed: int = ER_DEFAULT_SEED, query_index_base: int = 0,
                       force_ell_b: int = -1, ell_variant: int = 0, stream=None, synchronous: bool = True,
-                      k: int | None = None):
+                      k: int | None = None, query_ids=None):
     """Extended query.  ``pairs``/``out``/``stats`` are numpy arrays (host) or torch CUDA
     tensors (device); ``out``/``stats`` are allocated on the host when None.
     ``stats=True`` allocates a host STATS_DTYPE array.  Returns (out, stats)."""
@@ -216,6 +218,18 @@ def er_query_batch_ex(g, pairs, eps: float, p_fail: float = 0.01, *, out=None, s
     o.out_on_device = int(odev)
     o.ell_variant = ell_variant
     o.synchronous = int(synchronous)
+    if query_ids is not None:
+        if hasattr(query_ids, "data_ptr"):
+            if bool(query_ids.is_cuda) != bool(pdev):
+                raise ValueError("query_ids must live where pairs live (host or device)")
+            o.query_ids = ctypes.c_void_p(query_ids.data_ptr())
+        else:
+            if pdev:
+                raise ValueError("query_ids must live where pairs live (host or device)")
+            query_ids = np.ascontiguousarray(query_ids, dtype=np.int64)
+            if query_ids.shape[0] != kk:
+                raise ValueError("query_ids needs one entry per query")
+            o.query_ids = query_ids.ctypes.data_as(ctypes.c_void_p)
     if stream is not None:
         o.cuda_stream = _stream_handle(stream)
     _raise(lib.er_query_batch_ex(g, pp, kk, float(eps), float(p_fail), ctypes.byref(o), op, sp))

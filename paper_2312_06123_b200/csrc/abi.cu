@@ -176,6 +176,7 @@ void er_opts_default(er_opts *o)
     o->out_on_device = 0;
     o->ell_variant = 0;
     o->synchronous = 1;
+    o->query_ids = nullptr;
 }
 
 er_graph *er_graph_create(int64_t n, const int64_t *offsets, const int32_t *cols)
@@ -202,6 +203,11 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
     cudaError_t e = cudaGetDevice(&g->device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->amc_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        e = cudaStreamCreateWithPriority(&g->head_stream, cudaStreamNonBlocking, hi);
+    }
     if (e == cudaSuccess) {
         // keep stream-ordered allocations (per-batch y-tables, AMC group buffers) cached
         cudaMemPool_t pool;
@@ -248,10 +254,12 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
             if (!strcmp(env, "cols")) layout = 0;
             if (!strcmp(env, "packed") && packable) layout = 2;
         }
-        if (const char *env = getenv("GEER_WALK_MINB")) g->walk_minb = std::min(4, std::max(2, atoi(env)));
+        if (const char *env = getenv("GEER_WALK_MINB")) g->walk_minb = atoi(env) == 3 ? 3 : 4;
         if (const char *env = getenv("GEER_AMC_OVERLAP")) g->amc_overlap = atoi(env) != 0;
-        if (const char *env = getenv("GEER_WALK_HINTS")) g->walk_hints = atoi(env) & 3;
-        if (const char *env = getenv("GEER_WALK_KERNEL")) g->walk_kernel = atoi(env) == 4 ? 4 : 3;
+        if (const char *env = getenv("GEER_WALK_PERSIST")) g->walk_persist = atoi(env) != 0;
+        if (const char *env = getenv("GEER_YTABLE")) g->ytable_force = !strcmp(env, "hash") ? 1 : !strcmp(env, "rank") ? 2 : 0;
+        if (const char *env = getenv("GEER_Y_EVICT_FIRST")) g->y_evict_first = atoi(env) != 0;
+        if (const char *env = getenv("GEER_L2_PERSIST")) g->l2_persist = atoi(env) != 0;
         if (const char *env = getenv("GEER_WALK_NP")) g->walk_np = atoi(env) == 1 ? 1 : 2;
         if (const char *env = getenv("GEER_WALK_SMEM_KB")) g->walk_smem_words = 256 * std::min(48, std::max(8, atoi(env)));
         g->pack.bo = bo;
@@ -264,6 +272,28 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
             e = cudaMalloc(&g->d_parcs, sizeof(unsigned long long) * std::max<int64_t>(g->nnz, 1));
             if (e == cudaSuccess) e = geer::build_parcs(g);
         }
+    }
+    if (e == cudaSuccess && g->l2_persist) {
+        // keep the walk graph in L2: a persisting access-policy window on the AMC stream (the
+        // y-tables stream past it).  Sets the device's persisting-L2 limit (a process-wide
+        // setting), so it is opt-in (GEER_L2_PERSIST=1).
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, g->device) == cudaSuccess && prop.persistingL2CacheMaxSize > 0) {
+            void *base = g->d_parcs ? (void *)g->d_parcs : g->d_arcs ? (void *)g->d_arcs : (void *)g->d_cols;
+            const size_t want = g->d_parcs ? 8 * (size_t)g->nnz : g->d_arcs ? 16 * (size_t)g->nnz : 4 * (size_t)g->nnz;
+            const size_t lim = std::min(want, (size_t)prop.persistingL2CacheMaxSize);
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+            cudaStreamAttrValue a{};
+            a.accessPolicyWindow.base_ptr = base;
+            a.accessPolicyWindow.num_bytes = std::min(want, (size_t)prop.accessPolicyMaxWindowSize);
+            a.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)lim / (double)a.accessPolicyWindow.num_bytes);
+            a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cudaStreamSetAttribute(g->amc_stream, cudaStreamAttributeAccessPolicyWindow, &a);
+            g->l2_window = a.accessPolicyWindow.num_bytes;
+            g->l2_persist_bytes = lim;
+        }
+        cudaGetLastError();
     }
     if (e != cudaSuccess) {
         cuda_fail(e, "er_graph_create");
@@ -296,6 +326,12 @@ void er_graph_destroy(er_graph *g)
         if (g->amc_stream) cudaStreamSynchronize(g->amc_stream);
         if (g->stream) cudaStreamDestroy(g->stream);
         if (g->amc_stream) cudaStreamDestroy(g->amc_stream);
+        if (g->head_stream) {
+            cudaStreamSynchronize(g->head_stream);
+            cudaStreamDestroy(g->head_stream);
+        }
+        if (g->ev_in) cudaEventDestroy(g->ev_in);
+        if (g->ev_out) cudaEventDestroy(g->ev_out);
         cudaSetDevice(cur);
     }
     delete g;
@@ -346,6 +382,14 @@ int er_query_batch_ex(er_graph *g, const int32_t *pairs, int64_t k, double eps, 
     if (opt.query_index_base < 0 || opt.query_index_base + k > ((int64_t)1 << 32)) {
         set_error(ER_EINVAL, "query indices must fit in 32 bits");
         return ER_EINVAL;
+    }
+    if (opt.query_ids && !opt.pairs_on_device) {
+        for (int64_t i = 0; i < k; i++) {
+            if (opt.query_ids[i] < 0 || opt.query_ids[i] >= ((int64_t)1 << 32)) {
+                set_error(ER_EINVAL, "query_ids[" + std::to_string(i) + "] outside [0, 2^32)");
+                return ER_EINVAL;
+            }
+        }
     }
     std::lock_guard<std::mutex> lk(g->mu);
     if (g->query_block != ER_OK) { set_error(g->query_block, "graph created ER_CREATE_SPMM_ONLY: not connected or bipartite"); return g->query_block; }

@@ -23,16 +23,16 @@ enum : int32_t { PH_DONE = 0, PH_SMM = 1, PH_AMC = 2 };
 struct QState {
     er_query_stats st;     // public diagnostics, copied out at the end
     int32_t s, t;          // query endpoints
+    uint32_t gq;           // global query index (RNG key, R10): query_index_base + i or query_ids[i]
+    int32_t pad3;
     int32_t ds, dt;        // degrees d(s), d(t)
     int32_t phase;         // PH_*
     int32_t ylog2;         // log2 of the y-table capacity in slots (>= 3)
-    int64_t yoff;          // offset (in slots) of this query's y-table in the pools
-    int32_t flog2;         // log2 of the membership-filter bits (0: no filter; small tables)
+    int32_t ymode;         // y-table layout: 0 hash (ykeys, ylog2), 1 rank bitmap (yrec)
     int32_t pad2;
-    int64_t foff;          // offset (in 32-bit words) of this query's filter in the filter pool
-    const int32_t *ykeys;  // absolute pointers of this query's table / values / filter (walk kernel)
-    const double *yvals;
-    const uint32_t *yfilt;
+    const int32_t *ykeys;  // hash keys (YT_HASH)
+    const uint4 *yrec;     // rank records {bits lo, bits hi, rank, 0} per 64 node ids (YT_RANK)
+    const double *yvals;   // values (by slot, or by rank)
     double z;              // last batch mean Z (= r_f)
 };
 
@@ -108,6 +108,8 @@ struct Workspace {
     DevBuf cub_tmp;                                 // CUB temp storage
     DevBuf scalars;                                 // small device scalars
     DevBuf spmm_part;                               // K9 heavy-row segment sums
+    DevBuf qids;                                    // device copy of er_opts.query_ids
+    std::vector<DevBuf> ychunk;                     // y-tables of each SMM wave (grow-only, kept)
     DevBuf ids, seglen, segbeg, lfkey;              // 0..k-1 ids; compaction lengths; sort segments; AMC order
     void *host_pinned = nullptr;                    // small pinned host scalars
     size_t host_pinned_cap = 0;
@@ -131,15 +133,20 @@ struct er_graph {
     double lambda = 0.0;
     bool lambda_set = false;
     int nbits = 1;
-    int walk_minb = 3;   // K6 resident CTAs per SM (launch bounds variant; GEER_WALK_MINB 2..4)
-    bool amc_overlap = true;   // AMC per SMM wave on the AMC stream (GEER_AMC_OVERLAP=0: one AMC after the head)
-    int walk_hints = 0;  // K6 L2 cache hints: bit0 y-tables evict-first, bit1 arcs evict-last (GEER_WALK_HINTS)
+    int walk_minb = 4;   // K6 resident CTAs per SM (launch bounds variant; GEER_WALK_MINB 3..4)
+    bool amc_overlap = false;  // AMC per SMM wave on the AMC stream (GEER_AMC_OVERLAP=1) or one AMC after the head
     int walk_occ = 0;    // K6 resident CTAs per SM at the last launch (occupancy API)
-    int walk_kernel = 3; // K6 version: 3 = pipelined-probe kernel (default), 4 = multi-chain kernel (GEER_WALK_KERNEL)
-    int walk_np = 2;     // K6 walk pairs per thread (GEER_WALK_NP 1..2)
-    int walk_smem_words = 12288;  // K6 staging area per CTA in 32-bit words (GEER_WALK_SMEM_KB)
+    bool walk_persist = true;   // K6 persistent grid + atomic tile counter (GEER_WALK_PERSIST=1) or one tile per CTA
+    int ytable_force = 0;  // y-table layout: 0 by footprint, 1 hash only, 2 rank bitmap only (GEER_YTABLE)
+    int y_evict_first = 0; // K6: L2 evict-first policy on y-table loads (GEER_Y_EVICT_FIRST)
+    bool l2_persist = false; // K6: persisting-L2 access window over the walk graph (GEER_L2_PERSIST)
+    size_t l2_window = 0, l2_persist_bytes = 0;
+    int walk_np = 1;     // K6 walk pairs per thread (GEER_WALK_NP 1..2)
+    int walk_smem_words = 6144;   // K6 staging area per CTA in 32-bit words (GEER_WALK_SMEM_KB)
     cudaStream_t stream = nullptr;
     cudaStream_t amc_stream = nullptr;  // AMC groups overlap the SMM head
+    cudaStream_t head_stream = nullptr; // high-priority stream of the SMM head (forked from the caller's)
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;  // fork / join with the caller's stream
     std::mutex mu;
     int64_t launches = 0;
     bool profiling = false;

@@ -8,10 +8,11 @@
 //     K3 k_run_reduce     ordered sequential sum per (segment, u), / d(u)
 //     K4 (fused in K3) + k_seg_max2  vol, top-2, x(s), x(t) per segment  Eq. 10, Eq. 15
 //        k_decide         r_b += term; psi -> eta* -> eta0 -> h; switch   Alg. 3 L7, L9
-//     K5 k_yinsert        y = s*/d_s - t*/d_t into a per-query hash table Alg. 1 L7
+//     K5 k_yinsert        y = s*/d_s - t*/d_t into a per-query table      Alg. 1 L7
+//        (+ k_yrank)      (hash, or rank bitmap for large supports)
 //        compaction       frontier + active list of continuing queries
-//   AMC waves b = 0..tau-1:
-//     K6 k_walks          thread = walk pair, flattened over queries; Philox (q,b,side,k,step)  Alg. 1 L5-L9
+//   AMC batches b = 0..tau-1 (after the head, or per SMM wave on a second stream):
+//     K6 k_walks          thread = walk pair(s), flattened over queries; Philox (q,b,side,k,step)  Alg. 1 L5-L9
 //     K7 k_amc_reduce     Z, sigma^2, Bernstein f, stop or double         Alg. 1 L11-L14
 //   K8 k_finalize         r' = r_f + r_b                                  Alg. 3 L11
 //
@@ -41,8 +42,8 @@ static inline unsigned blocks_for(int64_t n, int per) { return (unsigned)((n + p
 // ============================================================================ kernels
 
 // K1: per-query setup.
-__global__ void k_setup(int64_t k, const int32_t *__restrict__ pairs, const int64_t *__restrict__ off,
-                        BatchParams P, QState *__restrict__ qs)
+__global__ void k_setup(int64_t k, const int32_t *__restrict__ pairs, const int64_t *__restrict__ ids,
+                        const int64_t *__restrict__ off, BatchParams P, QState *__restrict__ qs)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= k) return;
@@ -51,6 +52,7 @@ __global__ void k_setup(int64_t k, const int32_t *__restrict__ pairs, const int6
     const int32_t s = pairs[2 * i], t = pairs[2 * i + 1];
     Q.s = s;
     Q.t = t;
+    Q.gq = (uint32_t)(ids ? ids[i] : P.qbase + i);
     Q.ds = (int32_t)(off[s + 1] - off[s]);
     Q.dt = (int32_t)(off[t + 1] - off[t]);
     Q.phase = PH_DONE;
@@ -381,90 +383,94 @@ __global__ void k_decide(int32_t na, const int32_t *__restrict__ act, const SegS
     }
 }
 
-// y-table capacity (slots) for queries that leave the SMM head for AMC in this wave:
-// next power of two >= 2 |supp(s*)| + 2 |supp(t*)| (load <= 1/2), at least one 8-slot bucket.
-// Tables too large to stage in the walk kernel's shared memory also get a membership filter of
-// min(2^18, 4 cap) bits (fwords[i] 32-bit words), staged instead (K6).
-constexpr int WALK_SMEM_WORDS = 12288;      // 48 KB of staged y-table keys / filters per CTA
-constexpr int WALK_KEY_SLOTS = 8192;        // largest table staged as keys (pow2 <= WALK_SMEM_WORDS)
-constexpr int FILTER_MAX_LOG2 = 18;         // 32 KB filter
+// y-tables (K5): y(v) = s*(v)/d(s) - t*(v)/d(t) on U = supp(s*) u supp(t*) for each query that
+// leaves the SMM head for AMC in this wave (Alg. 1 L7 with s = s*, t = t*).  Two layouts,
+// chosen per query by footprint:
+//  * hash (YT_HASH): open addressing, 8 int32 keys per 32-byte bucket, buckets probed linearly;
+//    capacity = next power of two >= 2 (|supp s*| + |supp t*|) (load <= 1/2), >= one bucket;
+//    values fp64 by slot.  Small tables are staged whole in the walk kernel's shared memory.
+//  * rank bitmap (YT_RANK): one 16-byte record {uint64 bits; uint32 rank; pad} per 64 node ids
+//    (bit v of U, rank = |U| below the record), values fp64 by rank: y(v) is at
+//    vals[rank + popc(bits below v)].  Exact membership in one 16-byte load, no probing; used
+//    when 16 ceil(n/64) B is below the hash's 12 B/slot footprint (large supports).
+constexpr int YT_HASH = 0;
+constexpr int YT_RANK = 1;
+constexpr int WALK_SMEM_WORDS = 6144;       // 24 KB of staged y-table keys per CTA
+constexpr int WALK_KEY_SLOTS = 4096;        // largest hash table staged in shared memory
+
+// Per leaving query i: hslots[i] hash slots, vslots[i] value slots, rrecs[i] rank records.
 __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState *__restrict__ qs,
-                       const int32_t *__restrict__ cont, const int64_t *__restrict__ segoff,
-                       int64_t *__restrict__ ycap, int64_t *__restrict__ fwords)
+                       const int32_t *__restrict__ cont, const int64_t *__restrict__ segoff, int64_t nrec,
+                       int force, int64_t *__restrict__ hslots, int64_t *__restrict__ vslots,
+                       int64_t *__restrict__ rrecs)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
-    int64_t cap = 0, fw = 0;
+    int64_t h = 0, v = 0, r = 0;
     if ((cont == nullptr || !cont[i]) && qs[act[i]].phase == PH_AMC) {
-        const int64_t len = segoff[2 * i + 2] - segoff[2 * i];
-        cap = YB;
+        const int64_t len = segoff[2 * i + 2] - segoff[2 * i];   // |supp s*| + |supp t*| >= |U|
+        int64_t cap = YB;
         while (cap < 2 * len) cap <<= 1;
-        if (cap > WALK_KEY_SLOTS) fw = std::min<int64_t>((int64_t)1 << FILTER_MAX_LOG2, 4 * cap) / 32;
+        const bool rank = force == 2 || (force == 0 && cap > WALK_KEY_SLOTS && 16 * nrec < 12 * cap);
+        if (rank) {
+            r = nrec;
+            v = len;
+        } else {
+            h = cap;
+            v = cap;
+        }
     }
-    ycap[i] = cap;
-    fwords[i] = fw;
+    hslots[i] = h;
+    vslots[i] = v;
+    rrecs[i] = r;
 }
 
-__global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__ ycap,
-                          const int64_t *__restrict__ yincl, const int64_t *__restrict__ fwords,
-                          const int64_t *__restrict__ fincl, const int32_t *kbase, const double *vbase,
-                          const uint32_t *fbase, QState *__restrict__ qs)
+__global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__ hslots,
+                          const int64_t *__restrict__ hincl, const int64_t *__restrict__ vslots,
+                          const int64_t *__restrict__ vincl, const int64_t *__restrict__ rrecs,
+                          const int64_t *__restrict__ rincl, const int32_t *kbase, const double *vbase,
+                          const uint4 *rbase, QState *__restrict__ qs)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= na || ycap[i] == 0) return;
+    if (i >= na || vslots[i] == 0) return;
     QState &Q = qs[act[i]];
-    const int64_t cap = ycap[i];
-    Q.yoff = yincl[i] - cap;
-    int lg = 0;
-    while ((1ll << lg) < cap) lg++;
-    Q.ylog2 = lg;
-    const int64_t fw = fwords[i];
-    Q.foff = fincl[i] - fw;
-    int fl = 0;
-    while (fw > 0 && (32ll << fl) < 32 * fw) fl++;
-    Q.flog2 = fw > 0 ? fl + 5 : 0;
-    Q.ykeys = kbase + Q.yoff;
-    Q.yvals = vbase + Q.yoff;
-    Q.yfilt = fw > 0 ? fbase + Q.foff : nullptr;
+    Q.yvals = vbase + (vincl[i] - vslots[i]);
+    if (rrecs[i] > 0) {
+        Q.ymode = YT_RANK;
+        Q.yrec = rbase + (rincl[i] - rrecs[i]);
+        Q.ykeys = nullptr;
+        Q.ylog2 = 0;
+    } else {
+        const int64_t cap = hslots[i];
+        Q.ymode = YT_HASH;
+        Q.ykeys = kbase + (hincl[i] - cap);
+        Q.yrec = nullptr;
+        int lg = 0;
+        while ((1ll << lg) < cap) lg++;
+        Q.ylog2 = lg;
+    }
 }
 
-__global__ void k_yfill(int64_t Y, int32_t *__restrict__ keys, double *__restrict__ ys, int64_t FW,
-                        uint32_t *__restrict__ filt)
+__global__ void k_yfill(int64_t H, int32_t *__restrict__ keys, int64_t V, double *__restrict__ vals, int64_t R,
+                        uint4 *__restrict__ recs)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < FW) filt[j] = 0u;
-    if (j >= Y) return;
-    keys[j] = -1;
-    ys[j] = 0.0;
+    if (j < H) keys[j] = -1;
+    if (j < V) vals[j] = 0.0;
+    if (j < R) recs[j] = make_uint4(0u, 0u, 0u, 0u);
 }
 
-// K5: insert every support node of side `side` of a leaving query into its y-table
-// (find-or-insert: a node may be on both sides).  Launched for side 0, then side 1: side 0
-// stores s*(v)/d(s) at the slot, side 1 subtracts t*(v)/d(t), so every slot ends with
-// y(v) = s*(v)/d(s) - t*(v)/d(t) (Alg. 1 L7 with s = s*, t = t*; a side the node is not on
-// contributes 0.0).  A node occurs once per side, so each pass has one writer per slot.
-// Bucketed open addressing: 8 int32 keys per 32-byte bucket, buckets probed linearly, slots in
-// order inside a bucket, claimed by CAS.
-__global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
-                          const int32_t *__restrict__ id, const double *__restrict__ val,
-                          const int32_t *__restrict__ act, const int64_t *__restrict__ ycap,
-                          const QState *__restrict__ qs, int32_t *__restrict__ ykeys, double *__restrict__ ys,
-                          uint32_t *__restrict__ filt, int side)
+__device__ __forceinline__ int64_t rank_index(const uint4 r, int32_t v)
 {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
-    const int32_t g = seg[e];
-    if ((g & 1) != side) return;
-    const int32_t i = g >> 1;
-    if (ycap[i] == 0) return;
-    const QState &Q = qs[act[i]];
-    const int32_t v = id[e];
-    if (Q.flog2 > 0) {
-        const uint32_t fb = fbit(v, Q.flog2);
-        atomicOr(filt + Q.foff + (fb >> 5), 1u << (fb & 31));
-    }
-    int32_t *keys = ykeys + Q.yoff;
-    const int lgb = Q.ylog2 - YB_LOG;
+    const unsigned long long bits = ((unsigned long long)r.y << 32) | r.x;
+    const int b = v & 63;
+    if (!((bits >> b) & 1ull)) return -1;
+    return (int64_t)r.z + __popcll(bits & ((1ull << b) - 1ull));
+}
+
+// Hash find-or-insert of v; returns its slot.
+__device__ __forceinline__ int64_t hash_insert(int32_t *keys, int lgb, int32_t v)
+{
     const uint32_t bmask = (1u << lgb) - 1u;
     uint32_t bk = ybucket(v, lgb);
     while (true) {
@@ -477,13 +483,78 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
             const uint32_t slot = bk * YB + j;
             int32_t k = kk[j];
             if (k == -1) k = atomicCAS(&keys[slot], -1, v);
-            if (k == -1 || k == v) {
-                if (side) ys[Q.yoff + slot] = ys[Q.yoff + slot] - val[e] / (double)Q.dt;
-                else ys[Q.yoff + slot] = val[e] / (double)Q.ds;
-                return;
-            }
+            if (k == -1 || k == v) return slot;
         }
         bk = (bk + 1) & bmask;
+    }
+}
+
+// K5 passes over the support entries (frontier entry e: node id[e], value val[e], segment
+// seg[e] = 2 i + side) of the leaving queries:
+//   pass 0: hash: side 0 find-or-insert, vals[slot] = s*(v)/d(s);  rank: set bit v (both sides)
+//   (k_yrank between passes 0 and 1)
+//   pass 1: hash: side 1 find-or-insert, vals[slot] -= t*(v)/d(t); rank: side 0 vals[idx] = s*(v)/d(s)
+//   pass 2: rank: side 1 vals[idx] -= t*(v)/d(t)
+// so every entry ends with y(v) = s*(v)/d(s) - t*(v)/d(t), a side the node is not on
+// contributing 0.0 (values start at 0.0).  A node occurs once per side: one writer per value
+// in every pass.
+__global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
+                          const int32_t *__restrict__ id, const double *__restrict__ val,
+                          const int32_t *__restrict__ act, const int64_t *__restrict__ vslots,
+                          const QState *__restrict__ qs, int pass)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
+    const int32_t g = seg[e];
+    const int32_t i = g >> 1;
+    if (vslots[i] == 0) return;
+    const int side = g & 1;
+    const QState &Q = qs[act[i]];
+    const int32_t v = id[e];
+    double *vals = const_cast<double *>(Q.yvals);
+    if (Q.ymode == YT_HASH) {
+        if (pass != side) return;
+        const int64_t slot = hash_insert(const_cast<int32_t *>(Q.ykeys), Q.ylog2 - YB_LOG, v);
+        if (side) vals[slot] = vals[slot] - val[e] / (double)Q.dt;
+        else vals[slot] = val[e] / (double)Q.ds;
+        return;
+    }
+    uint4 *recs = const_cast<uint4 *>(Q.yrec);
+    if (pass == 0) {
+        atomicOr(reinterpret_cast<unsigned long long *>(recs + (v >> 6)), 1ull << (v & 63));
+        return;
+    }
+    if (pass != side + 1) return;
+    const int64_t idx = rank_index(recs[v >> 6], v);
+    if (side) vals[idx] = vals[idx] - val[e] / (double)Q.dt;
+    else vals[idx] = val[e] / (double)Q.ds;
+}
+
+// Ranks of the rank-bitmap tables: rank(record w) = popcount of all records before w.  One CTA
+// per leaving query (non-rank queries exit).
+constexpr int YRANK_THREADS = 256;
+__global__ void __launch_bounds__(YRANK_THREADS)
+k_yrank(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__ rrecs, QState *__restrict__ qs)
+{
+    const int32_t i = blockIdx.x;
+    if (i >= na || rrecs[i] == 0) return;
+    uint4 *recs = const_cast<uint4 *>(qs[act[i]].yrec);
+    const int64_t R = rrecs[i];
+    typedef cub::BlockScan<uint32_t, YRANK_THREADS> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    uint32_t carry = 0;
+    for (int64_t base = 0; base < R; base += YRANK_THREADS) {
+        const int64_t w = base + threadIdx.x;
+        uint4 r = w < R ? recs[w] : make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t c = (uint32_t)(__popc(r.x) + __popc(r.y));
+        uint32_t excl, tot;
+        Scan(tmp).ExclusiveSum(c, excl, tot);
+        if (w < R) {
+            r.z = carry + excl;
+            recs[w] = r;
+        }
+        carry += tot;
+        __syncthreads();
     }
 }
 
@@ -553,7 +624,6 @@ __global__ void k_lf_key(int32_t na, const int32_t *__restrict__ amc, const QSta
 
 constexpr int WALK_WARPS = 8;
 constexpr int WALK_THREADS = 32 * WALK_WARPS;
-constexpr size_t WALK_SMEM_BYTES = sizeof(int32_t) * WALK_SMEM_WORDS;
 
 __device__ __forceinline__ int32_t find_chunk_query(const int64_t *__restrict__ cincl, int32_t n, int64_t c)
 {
@@ -582,135 +652,40 @@ __device__ __forceinline__ int bucket_match(const int4 a, const int4 b, int32_t 
     return m;
 }
 
-// L2 cache policies: the y-tables stream past (evict first), the walk graph stays (evict last).
+// y-structure loads with an optional L2 evict-first policy (pol != 0): the tables stream past,
+// the walk graph's arc records should stay in L2.
 __device__ __forceinline__ uint64_t pol_evict_first()
 {
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ uint64_t pol_evict_last()
+__device__ __forceinline__ double ld_y(const double *p, uint64_t pol)
 {
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ double ldg_f64(const double *p, uint64_t pol)
-{
-    if (pol == 0) return __ldg(p);   // no cache hint (hints disabled)
+    if (!pol) return __ldg(p);
     double r;
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
     return r;
 }
-__device__ __forceinline__ unsigned long long ldg_u64(const unsigned long long *p, uint64_t pol)
+__device__ __forceinline__ uint4 ld_y(const uint4 *p, uint64_t pol)
 {
-    if (pol == 0) return __ldg(p);
-    unsigned long long r;
-    asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ uint32_t ldg_u32(const int32_t *p, uint64_t pol)
-{
-    if (pol == 0) return (uint32_t)__ldg(p);
-    uint32_t r;
-    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ uint4 ldg_u128(const uint4 *p, uint64_t pol)
-{
-    if (pol == 0) return __ldg(p);
+    if (!pol) return __ldg(p);
     uint4 r;
     asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
         : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
     return r;
 }
 
-// y-table probe modes of a warp (chosen per tile by the staging plan):
-//   YM_GLOBAL  keys probed in global memory (one 32-byte sector per bucket)
-//   YM_SMEM    the whole key table staged in shared memory
-//   YM_FILTER  the table's membership filter staged in shared memory; global probe only when the
-//              node's filter bit is set (a clear bit proves y(v) = 0: v is not in supp(y))
-enum { YM_GLOBAL = 0, YM_SMEM = 1, YM_FILTER = 2 };
-
-struct YView {
-    const int32_t *keys;        // global keys of the table
-    const int32_t *skeys;       // staged keys (YM_SMEM)
-    const uint32_t *sfilt;      // staged filter (YM_FILTER)
-    const double *vals;         // global values
-    int lgb, flg;
-    uint64_t pol;               // evict-first policy for table loads
-};
-
-template <int MODE>
-__device__ __forceinline__ void load_bucket(const YView &Y, int32_t v, uint32_t bk, int4 &a, int4 &b)
-{
-    if (MODE == YM_SMEM) {
-        const int32_t *p = Y.skeys + (size_t)bk * YB;
-        a = reinterpret_cast<const int4 *>(p)[0];
-        b = reinterpret_cast<const int4 *>(p)[1];
-        return;
-    }
-    if (MODE == YM_FILTER) {
-        const uint32_t fb = fbit(v, Y.flg);
-        if (!((Y.sfilt[fb >> 5] >> (fb & 31)) & 1u)) {
-            a = make_int4(-1, -1, -1, -1);   // not in the support: an empty bucket -> y = 0
-            b = a;
-            return;
-        }
-    }
-    // one 32-byte sector in one instruction (LDG.E.ENL2.256 on sm_100a)
-    const int32_t *p = Y.keys + (size_t)bk * YB;
-    if (Y.pol == 0) {
-        asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-            : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-            : "l"(p));
-        return;
-    }
-    asm("ld.global.nc.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
-        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-        : "l"(p), "l"(Y.pol));
-}
-
-// Slow path: v not in its first bucket and the bucket is full -> probe the following buckets
-// (in shared memory for YM_SMEM, else in global memory).
-template <int MODE>
-__device__ __forceinline__ double probe_rest(const YView &Y, uint32_t bk, int32_t v)
-{
-    const uint32_t bmask = (1u << Y.lgb) - 1u;
-    while (true) {
-        bk = (bk + 1) & bmask;
-        int4 a, b;
-        load_bucket<MODE == YM_SMEM ? YM_SMEM : YM_GLOBAL>(Y, v, bk, a, b);
-        bool empty;
-        const int m = bucket_match(a, b, v, &empty);
-        if (m >= 0) return ldg_f64(Y.vals + (size_t)bk * YB + m, Y.pol);
-        if (empty) return 0.0;
-    }
-}
-
-template <int ARC>
-__device__ __forceinline__ uint4 next_arc(const uint2 R, uint64_t r64, const uint4 *__restrict__ arcs,
-                                          const int32_t *__restrict__ cols,
-                                          const unsigned long long *__restrict__ parcs, PackSpec pk, uint64_t pl)
-{
-    const uint64_t e = (uint64_t)R.x + __umul64hi(r64, (uint64_t)R.y);   // idx = floor(r64 d / 2^64) (R10)
-    if (ARC == 2) return pk.unpack(ldg_u64(parcs + e, pl));
-    if (ARC == 1) return ldg_u128(arcs + e, pl);
-    uint4 A;
-    A.x = ldg_u32(cols + e, pl);
-    return A;
-}
-
-// y(v) lookup of one node: slot index of v in its query's table, or -1 when v is not in
-// supp(y) (then y(v) = 0, Alg. 1 L7 outside U_s and U_t).  Bucketed open addressing: 8 keys
-// per bucket, buckets probed linearly.
+// Hash lookups: slot of v, or -1 when v is not in supp(y) (then y(v) = 0, Alg. 1 L7 outside
+// U_s and U_t).  Staged keys in shared memory, or the table in global memory (one 32-byte
+// sector per bucket, LDG.E.ENL2.256).
 __device__ __forceinline__ int64_t ylookup_smem(const int32_t *skeys, int lgb, int32_t v)
 {
     const uint32_t bmask = (1u << lgb) - 1u;
     uint32_t bk = ybucket(v, lgb);
     while (true) {
-        int4 a, b;
-        load_bucket<YM_SMEM>(YView{nullptr, skeys, nullptr, nullptr, lgb, 0, 0}, v, bk, a, b);
+        const int4 a = reinterpret_cast<const int4 *>(skeys + (size_t)bk * YB)[0];
+        const int4 b = reinterpret_cast<const int4 *>(skeys + (size_t)bk * YB)[1];
         bool empty;
         const int m = bucket_match(a, b, v, &empty);
         if (m >= 0) return (int64_t)bk * YB + m;
@@ -724,7 +699,14 @@ __device__ __forceinline__ int64_t ylookup_global(const int32_t *keys, int lgb, 
     uint32_t bk = ybucket(v, lgb);
     while (true) {
         int4 a, b;
-        load_bucket<YM_GLOBAL>(YView{keys, nullptr, nullptr, nullptr, lgb, 0, pol}, v, bk, a, b);
+        if (pol)
+            asm("ld.global.nc.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                : "l"(keys + (size_t)bk * YB), "l"(pol));
+        else
+            asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                : "l"(keys + (size_t)bk * YB));
         bool empty;
         const int m = bucket_match(a, b, v, &empty);
         if (m >= 0) return (int64_t)bk * YB + m;
@@ -733,27 +715,47 @@ __device__ __forceinline__ int64_t ylookup_global(const int32_t *keys, int lgb, 
     }
 }
 
+template <int ARC>
+__device__ __forceinline__ uint4 next_arc(const uint2 R, uint64_t r64, const uint4 *__restrict__ arcs,
+                                          const int32_t *__restrict__ cols,
+                                          const unsigned long long *__restrict__ parcs, PackSpec pk)
+{
+    const uint64_t e = (uint64_t)R.x + __umul64hi(r64, (uint64_t)R.y);   // idx = floor(r64 d / 2^64) (R10)
+    if (ARC == 2) return pk.unpack(__ldg(parcs + e));
+    if (ARC == 1) return __ldg(arcs + e);
+    uint4 A;
+    A.x = (uint32_t)__ldg(cols + e);
+    return A;
+}
+
+// y-lookup modes of a warp (its query's table layout and the tile's staging plan).
+enum { YM_GLOBAL = 0, YM_SMEM = 1, YM_RANK = 2 };
+
 // NP walk pairs per thread = 2 NP independent chains (S_k from s, T_k from t for each pair),
 // advanced in lock step so 2 NP arc loads are in flight per thread.  Per step and chain:
-// Philox draw (R10; the even step's words are cached from the odd step's call), one arc
-// load (the chain's only dependent memory access), then y(v) by a shared-memory probe (keys
-// or membership filter staged per tile; a global probe only when the filter cannot exclude v)
-// whose value load is consumed one step later.  y values are added in step order (R9, R13).
+// Philox draw (R10; the even step's words are cached from the odd step's call), one arc load
+// (the chain's only dependent memory access), then y(v):
+//   YM_SMEM    hash keys staged in shared memory: probe now, value load consumed next step;
+//   YM_GLOBAL  hash keys in global memory: probe now (32-byte bucket loads), value next step;
+//   YM_RANK    rank-bitmap record load issued now and resolved next step (overlapping the next
+//              arc load), value load consumed the step after.
+// y values are added in step order (R9, R13).
 template <int ARC, int NP>
 __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
                                             const int32_t *__restrict__ cols,
                                             const unsigned long long *__restrict__ parcs, PackSpec pk, int mode,
-                                            const int32_t *sbase, const int32_t *__restrict__ gkeys,
-                                            const double *__restrict__ gvals, int lgb, int flg, uint64_t pol,
-                                            int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b,
+                                            const int32_t *skeys, const int32_t *__restrict__ gkeys,
+                                            const uint4 *__restrict__ yrec, const double *__restrict__ gvals,
+                                            int lgb, int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b,
                                             const uint64_t *kk, uint32_t key0, uint32_t key1, double *acc,
-                                            int32_t *endv, int hints)
+                                            int32_t *endv, uint64_t pol)
 {
     constexpr int C = 2 * NP;
     uint2 R[C];
     int32_t v[C];
     double pv[C];
     uint32_t cz[C], cw[C];
+    uint4 prec[C];       // YM_RANK: record of the previous step's node, resolved this step
 #pragma unroll
     for (int c = 0; c < C; c++) {
         v[c] = (c & 1) ? t : s;
@@ -762,8 +764,8 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
         pv[c] = 0.0;
         cz[c] = 0u;
         cw[c] = 0u;
+        prec[c] = make_uint4(0u, 0u, 0u, 0u);   // no bits: the start node is not summed (R9)
     }
-    const uint64_t pl = (hints & 2) ? pol_evict_last() : 0;
     for (int32_t j = 1; j <= lf; j++) {
         uint4 A[C];
 #pragma unroll
@@ -780,59 +782,69 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
             } else {
                 r64 = ((uint64_t)cw[c] << 32) | cz[c];
             }
-            A[c] = next_arc<ARC>(R[c], r64, arcs, cols, parcs, pk, pl);
+            A[c] = next_arc<ARC>(R[c], r64, arcs, cols, parcs, pk);
         }
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            acc[c] += pv[c];   // y of the previous step, in step order
+            acc[c] += pv[c];   // y of an earlier step, in step order
             pv[c] = 0.0;
+            if (mode == YM_RANK) {
+                const int64_t idx = rank_index(prec[c], v[c]);   // v[c] = previous step's node
+                if (idx >= 0) pv[c] = ld_y(gvals + idx, pol);
+            }
             v[c] = (int32_t)A[c].x;
             if (ARC) R[c] = make_uint2(A[c].y, A[c].z);
             else R[c] = __ldg(rec + v[c]);
-            int64_t slot;
-            if (mode == YM_SMEM) {
-                slot = ylookup_smem(sbase, lgb, v[c]);
+            if (mode == YM_RANK) {
+                prec[c] = ld_y(yrec + (v[c] >> 6), pol);
             } else {
-                slot = -1;
-                bool maybe = true;
-                if (mode == YM_FILTER) {
-                    const uint32_t fb = fbit(v[c], flg);
-                    maybe = (reinterpret_cast<const uint32_t *>(sbase)[fb >> 5] >> (fb & 31)) & 1u;
-                }
-                if (maybe) slot = ylookup_global(gkeys, lgb, v[c], pol);
+                const int64_t slot =
+                    mode == YM_SMEM ? ylookup_smem(skeys, lgb, v[c]) : ylookup_global(gkeys, lgb, v[c], pol);
+                if (slot >= 0) pv[c] = ld_y(gvals + slot, pol);
             }
-            if (slot >= 0) pv[c] = ldg_f64(gvals + slot, pol);
         }
     }
 #pragma unroll
     for (int c = 0; c < C; c++) {
         acc[c] += pv[c];
+        if (mode == YM_RANK && lf > 0) {
+            const int64_t idx = rank_index(prec[c], v[c]);
+            if (idx >= 0) acc[c] += ld_y(gvals + idx, pol);
+        }
         endv[c] = v[c];
     }
 }
 
 // K6: warp = one chunk of 32 NP walk pairs of one query (chunks of all AMC queries are laid
 // out query after query, queries ordered by descending ell_f; lane l, pair p runs walk
-// k = 32 NP chunk' + 32 p + l).  Per CTA-tile of WALK_WARPS chunks, a staging plan puts each
-// distinct query's key table (if it fits) or else its membership filter into shared memory; a
-// query for which neither fits probes global memory.  Each warp writes the canonical partial
-// {sum Z, sum Z^2, checksum} of its chunk.
+// k = 32 NP chunk' + 32 p + l).  Per CTA-tile of WALK_WARPS chunks, a staging plan puts the
+// hash keys of each distinct small-table query of the tile into shared memory.  Each warp
+// writes the canonical partial {sum Z, sum Z^2, checksum} of its chunk.
 template <int ARC, int NP, int MINB>
 __global__ void __launch_bounds__(WALK_THREADS, MINB)
 k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
         const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
         const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
-        uint32_t key0, uint32_t key1, int64_t qbase, int32_t smem_words, int hints, TilePart *__restrict__ parts)
+        uint32_t key0, uint32_t key1, int32_t smem_words, int y_evict_first,
+        unsigned long long *__restrict__ tile_ctr, TilePart *__restrict__ parts)
 {
     extern __shared__ __align__(32) int32_t sm_words[];
     __shared__ int32_t s_qi[WALK_WARPS];
     __shared__ int32_t s_soff[WALK_WARPS];
     __shared__ int32_t s_mode[WALK_WARPS];
+    __shared__ int64_t s_tile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
-    const uint64_t pol = (hints & 1) ? pol_evict_first() : 0;
-    // persistent: CTA-tiles of WALK_WARPS consecutive chunks, round-robin over the grid
-    for (int64_t tile = blockIdx.x; tile * WALK_WARPS < nchunks; tile += gridDim.x) {
+    const uint64_t pol = y_evict_first ? pol_evict_first() : 0;
+    // persistent: CTA-tiles of WALK_WARPS consecutive chunks handed out by an atomic counter
+    // (dynamic balance: the first tiles, of the longest walks, are the longest); with
+    // tile_ctr == nullptr one tile per CTA, tile = blockIdx.x
+    for (int it = 0;; it++) {
+        if (threadIdx.x == 0)
+            s_tile = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1ull) : (it == 0 ? (int64_t)blockIdx.x : nchunks);
+        __syncthreads();
+        const int64_t tile = s_tile;
+        if (tile * WALK_WARPS >= nchunks) break;
         const int64_t chunk = tile * WALK_WARPS + warp;
         const bool wvalid = chunk < nchunks;
         const int32_t i = wvalid ? find_chunk_query(cincl, na, chunk) : -1;
@@ -843,34 +855,26 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             int32_t used = 0;
             for (int w = 0; w < WALK_WARPS; w++) {
                 const int32_t qi = s_qi[w];
-                s_mode[w] = YM_GLOBAL;
                 s_soff[w] = 0;
-                if (qi < 0) continue;
+                if (qi < 0) { s_mode[w] = YM_GLOBAL; continue; }
                 if (w > 0 && s_qi[w - 1] == qi) { s_soff[w] = s_soff[w - 1]; s_mode[w] = s_mode[w - 1]; continue; }
                 const QState &Q = qs[amc[qi]];
+                if (Q.ymode == YT_RANK) { s_mode[w] = YM_RANK; continue; }
                 const int32_t cap = 1 << Q.ylog2;
-                const int32_t fwords = Q.flog2 > 0 ? (1 << (Q.flog2 - 5)) : 0;
                 if (cap <= WALK_KEY_SLOTS && used + cap <= smem_words) {
                     s_soff[w] = used; s_mode[w] = YM_SMEM; used += cap;
-                } else if (fwords > 0 && used + fwords <= smem_words) {
-                    s_soff[w] = used; s_mode[w] = YM_FILTER; used += fwords;
+                } else {
+                    s_mode[w] = YM_GLOBAL;
                 }
             }
         }
         __syncthreads();
         for (int w = 0; w < WALK_WARPS; w++) {
-            if (s_mode[w] == YM_GLOBAL || (w > 0 && s_qi[w - 1] == s_qi[w])) continue;
+            if (s_mode[w] != YM_SMEM || (w > 0 && s_qi[w - 1] == s_qi[w])) continue;
             const QState &Q = qs[amc[s_qi[w]]];
-            const int4 *src;
-            int32_t words;
-            if (s_mode[w] == YM_SMEM) {
-                src = reinterpret_cast<const int4 *>(Q.ykeys);
-                words = 1 << Q.ylog2;
-            } else {
-                src = reinterpret_cast<const int4 *>(Q.yfilt);
-                words = 1 << (Q.flog2 - 5);
-            }
+            const int4 *src = reinterpret_cast<const int4 *>(Q.ykeys);
             int4 *dst = reinterpret_cast<int4 *>(sm_words + s_soff[w]);
+            const int32_t words = 1 << Q.ylog2;
             for (int32_t e = threadIdx.x; e < words / 4; e += WALK_THREADS) dst[e] = __ldg(src + e);
         }
         __syncthreads();
@@ -879,7 +883,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             const QState &Q = qs[qi];
             const int64_t c0 = i == 0 ? 0 : cincl[i - 1];
             const int64_t eta = Q.st.eta0 << b;
-            const uint32_t q = (uint32_t)(qbase + qi);
+            const uint32_t q = Q.gq;
             uint64_t kk[NP];
             bool any = false;
 #pragma unroll
@@ -893,8 +897,8 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             uint64_t ck = 0ull;
             if (any) {
                 walk_chains<ARC, NP>(rec, arcs, cols, parcs, pk, s_mode[warp], sm_words + s_soff[warp], Q.ykeys,
-                                     Q.yvals, Q.ylog2 - YB_LOG, Q.flog2, pol, Q.s, Q.t, Q.st.ell_f, q,
-                                     (uint32_t)b, kk, key0, key1, acc, endv, hints);
+                                     Q.yrec, Q.yvals, Q.ylog2 - YB_LOG, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, kk,
+                                     key0, key1, acc, endv, pol);
 #pragma unroll
                 for (int p = 0; p < NP; p++) {
                     if (kk[p] < (uint64_t)eta) {
@@ -906,219 +910,6 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
                     }
                 }
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-                ck += __shfl_xor_sync(0xffffffffu, ck, o);
-            }
-            if (lane == 0) {
-                TilePart tp;
-                tp.s1 = s1;
-                tp.s2 = s2;
-                tp.ck = ck;
-                tp.pad = 0;
-                parts[chunk] = tp;
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// ---- K6 v3 (the previous walk kernel, kept for A/B measurement: GEER_WALK_KERNEL=3)
-constexpr int WALK3_SMEM_SLOTS = 8192;
-template <bool SMEM>
-__device__ __forceinline__ void load_bucket3(const int32_t *keys, uint32_t bk, int4 &a, int4 &b)
-{
-    const int32_t *p = keys + (size_t)bk * YB;
-    if (SMEM) {
-        a = reinterpret_cast<const int4 *>(p)[0];
-        b = reinterpret_cast<const int4 *>(p)[1];
-    } else {
-        // one 32-byte sector in one instruction (LDG.E.ENL2.256 on sm_100a)
-        asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-                     : "l"(p));
-    }
-}
-
-// Slow path: v not in its first bucket and the bucket is full -> probe the following buckets.
-template <bool SMEM>
-__device__ __forceinline__ double probe_rest3(const int32_t *keys, const double *__restrict__ vals, uint32_t bk,
-                                          uint32_t bmask, int32_t v)
-{
-    while (true) {
-        bk = (bk + 1) & bmask;
-        int4 a, b;
-        load_bucket3<SMEM>(keys, bk, a, b);
-        bool empty;
-        const int m = bucket_match(a, b, v, &empty);
-        if (m >= 0) return __ldg(vals + (size_t)bk * YB + m);
-        if (empty) return 0.0;
-    }
-}
-
-// One walk pair (S_k from s, T_k from t), both chains advanced in one loop.  Software
-// pipelined: step j issues the load of step j's arc before it resolves the y probe of step
-// j-1's node, and a hit's value load is consumed one step later, so only the arc chain is
-// serial.  Arc records {u, off(u), d(u), -} make the chain one 16-byte load per step.
-// y values are added in step order (R9, R13).
-template <bool SMEM, int ARC>
-__device__ __forceinline__ void walk_pair3(const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
-                                          const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs,
-                                          PackSpec pk,
-                                          const int32_t *keys, const double *__restrict__ vals, int lgb,
-                                          int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b, uint64_t k,
-                                          uint32_t key0, uint32_t key1, double &accS, double &accT,
-                                          int32_t &endS, int32_t &endT)
-{
-    const uint32_t bmask = (1u << lgb) - 1u;
-    const uint32_t c3S = (b << 29) | (0u << 28) | (uint32_t)(k >> 32);
-    const uint32_t c3T = (b << 29) | (1u << 28) | (uint32_t)(k >> 32);
-    uint2 RS = __ldg(rec + s), RT = __ldg(rec + t);   // {offset, degree} of the current nodes
-    int32_t vS = s, vT = t;
-    double aS = 0.0, aT = 0.0;
-    double pvS = 0.0, pvT = 0.0;        // pending hit values (added one step later)
-    int4 kS0, kS1, kT0, kT1;            // bucket keys of the current nodes
-    U4 rS = {0, 0, 0, 0}, rT = {0, 0, 0, 0};
-    for (int32_t j = 1; j <= lf; j++) {
-        uint64_t r64S, r64T;
-        if (j & 1) {
-            const uint32_t cc = (uint32_t)((j - 1) >> 1);
-            rS = philox4x32_10(U4{cc, (uint32_t)k, q, c3S}, key0, key1);
-            rT = philox4x32_10(U4{cc, (uint32_t)k, q, c3T}, key0, key1);
-            r64S = ((uint64_t)rS.y << 32) | rS.x;
-            r64T = ((uint64_t)rT.y << 32) | rT.x;
-        } else {
-            r64S = ((uint64_t)rS.w << 32) | rS.z;
-            r64T = ((uint64_t)rT.w << 32) | rT.z;
-        }
-        uint4 AS, AT;
-        if (ARC == 1) {
-            AS = __ldg(arcs + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
-            AT = __ldg(arcs + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
-        } else if (ARC == 2) {
-            const unsigned long long PS = __ldg(parcs + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
-            const unsigned long long PT = __ldg(parcs + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
-            AS = pk.unpack(PS);
-            AT = pk.unpack(PT);
-        } else {
-            AS.x = (uint32_t)__ldg(cols + ((uint64_t)RS.x + __umul64hi(r64S, (uint64_t)RS.y)));
-            AT.x = (uint32_t)__ldg(cols + ((uint64_t)RT.x + __umul64hi(r64T, (uint64_t)RT.y)));
-        }
-        if (j > 1) {
-            aS += pvS;
-            aT += pvT;
-            bool eS, eT;
-            const uint32_t bS = ybucket(vS, lgb), bT = ybucket(vT, lgb);
-            const int mS = bucket_match(kS0, kS1, vS, &eS);
-            const int mT = bucket_match(kT0, kT1, vT, &eT);
-            pvS = 0.0;
-            pvT = 0.0;
-            if (mS >= 0) pvS = __ldg(vals + (size_t)bS * YB + mS);
-            else if (!eS) aS += probe_rest3<SMEM>(keys, vals, bS, bmask, vS);
-            if (mT >= 0) pvT = __ldg(vals + (size_t)bT * YB + mT);
-            else if (!eT) aT += probe_rest3<SMEM>(keys, vals, bT, bmask, vT);
-        }
-        vS = (int32_t)AS.x;
-        vT = (int32_t)AT.x;
-        if (ARC) {
-            RS = make_uint2(AS.y, AS.z);
-            RT = make_uint2(AT.y, AT.z);
-        } else {
-            RS = __ldg(rec + vS);
-            RT = __ldg(rec + vT);
-        }
-        load_bucket3<SMEM>(keys, ybucket(vS, lgb), kS0, kS1);
-        load_bucket3<SMEM>(keys, ybucket(vT, lgb), kT0, kT1);
-    }
-    // resolve the last step
-    aS += pvS;
-    aT += pvT;
-    if (lf > 0) {
-        bool eS, eT;
-        const uint32_t bS = ybucket(vS, lgb), bT = ybucket(vT, lgb);
-        const int mS = bucket_match(kS0, kS1, vS, &eS);
-        const int mT = bucket_match(kT0, kT1, vT, &eT);
-        if (mS >= 0) aS += __ldg(vals + (size_t)bS * YB + mS);
-        else if (!eS) aS += probe_rest3<SMEM>(keys, vals, bS, bmask, vS);
-        if (mT >= 0) aT += __ldg(vals + (size_t)bT * YB + mT);
-        else if (!eT) aT += probe_rest3<SMEM>(keys, vals, bT, bmask, vT);
-    }
-    accS = aS;
-    accT = aT;
-    endS = vS;
-    endT = vT;
-}
-
-// K6: warp = one chunk of 32 walk pairs of one query (chunks of all AMC queries are laid out
-// query after query, queries ordered by descending ell_f).  The CTA stages the y-table keys of
-// its (<= 8) queries in shared memory when they fit; otherwise the warp probes global memory.
-// Each warp writes the canonical partial {sum Z, sum Z^2, checksum} of its chunk.
-template <int ARC>
-__global__ void __launch_bounds__(WALK_THREADS, 4)
-k_walks3(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
-        const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
-        const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs, PackSpec pk,
-        int b, uint32_t key0, uint32_t key1, int64_t qbase, TilePart *__restrict__ parts)
-{
-    __shared__ __align__(32) int32_t sm_keys[WALK3_SMEM_SLOTS];
-    __shared__ int32_t s_qi[WALK_WARPS];
-    __shared__ int32_t s_soff[WALK_WARPS];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
-    // persistent: CTA-tiles of WALK_WARPS consecutive chunks, round-robin over the grid
-    for (int64_t tile = blockIdx.x; tile * WALK_WARPS < nchunks; tile += gridDim.x) {
-        const int64_t chunk = tile * WALK_WARPS + warp;
-        const bool wvalid = chunk < nchunks;
-        const int32_t i = wvalid ? find_chunk_query(cincl, na, chunk) : -1;
-        if (lane == 0) s_qi[warp] = i;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            // prefix-fit staging plan over the distinct queries of this tile (consecutive warps)
-            int32_t used = 0;
-            for (int w = 0; w < WALK_WARPS; w++) {
-                const int32_t qi = s_qi[w];
-                if (qi < 0) { s_soff[w] = -1; continue; }
-                if (w > 0 && s_qi[w - 1] == qi) { s_soff[w] = s_soff[w - 1]; continue; }
-                const int32_t cap = 1 << qs[amc[qi]].ylog2;
-                if (used + cap <= WALK3_SMEM_SLOTS) { s_soff[w] = used; used += cap; }
-                else s_soff[w] = -1;
-            }
-        }
-        __syncthreads();
-        for (int w = 0; w < WALK_WARPS; w++) {
-            if (s_soff[w] < 0 || (w > 0 && s_qi[w - 1] == s_qi[w])) continue;
-            const QState &Q = qs[amc[s_qi[w]]];
-            const int32_t cap = 1 << Q.ylog2;
-            const int4 *src = reinterpret_cast<const int4 *>(Q.ykeys);
-            int4 *dst = reinterpret_cast<int4 *>(sm_keys + s_soff[w]);
-            for (int32_t e = threadIdx.x; e < cap / 4; e += WALK_THREADS) dst[e] = __ldg(src + e);
-        }
-        __syncthreads();
-        if (wvalid) {
-            const int32_t qi = amc[i];
-            const QState &Q = qs[qi];
-            const int64_t c0 = i == 0 ? 0 : cincl[i - 1];
-            const uint64_t k = (uint64_t)(chunk - c0) * 32u + (uint64_t)lane;
-            const int64_t eta = Q.st.eta0 << b;
-            const bool active = k < (uint64_t)eta;
-            const uint32_t q = (uint32_t)(qbase + qi);
-            const int lgb = Q.ylog2 - YB_LOG;
-            const double *vals = Q.yvals;
-            double aS = 0.0, aT = 0.0;
-            int32_t eS = 0, eT = 0;
-            if (active) {
-                if (s_soff[warp] >= 0)
-                    walk_pair3<true, ARC>(rec, arcs, cols, parcs, pk, sm_keys + s_soff[warp], vals, lgb, Q.s, Q.t,
-                                         Q.st.ell_f, q, (uint32_t)b, k, key0, key1, aS, aT, eS, eT);
-                else
-                    walk_pair3<false, ARC>(rec, arcs, cols, parcs, pk, Q.ykeys, vals, lgb, Q.s, Q.t,
-                                          Q.st.ell_f, q, (uint32_t)b, k, key0, key1, aS, aT, eS, eT);
-            }
-            const double z = active ? aS - aT : 0.0;
-            double s1 = z, s2 = z * z;
-            uint64_t ck = active ? walk_hash(q, (uint32_t)b, 0u, k, eS) + walk_hash(q, (uint32_t)b, 1u, k, eT) : 0ull;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 s1 += __shfl_xor_sync(0xffffffffu, s1, o);
@@ -1272,8 +1063,10 @@ void Workspace::release()
 {
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2, &head,
-                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals, &ytmp, &cont2, &idx2, &spmm_part};
+                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals, &ytmp, &cont2, &idx2, &spmm_part, &qids};
     for (DevBuf *b : all) b->release();
+    for (DevBuf &b : ychunk) b.release();
+    ychunk.clear();
     if (host_pinned) cudaFreeHost(host_pinned);
     host_pinned = nullptr;
     host_pinned_cap = 0;
@@ -1352,52 +1145,59 @@ int select_list(Ctx &c, const int32_t *ids, const int32_t *flag, int32_t n, int3
     return ER_OK;
 }
 
-// Build y-tables for the queries of `act` with ycap > 0 from frontier (segoff,id,val,seg; Fmax
-// entries, device count dF or null).  `cont` may be null (all queries of the list leave the
-// head).  The tables live in a fresh stream-ordered allocation (keys + values) returned through
-// *keys / *vals (freed at the end of the batch); QState.yoff is relative to it.
+// Build the y-tables (K5) of the queries of `act` that leave the head now, from the frontier
+// (segoff, id, val, seg; Fmax entries, device count dF or null).  `cont` may be null (all
+// queries of the list leave).  The tables of SMM wave `wave` live in a grow-only workspace
+// buffer kept across batches: {vals fp64[V] | rank records uint4[R] | hash keys int32[H]};
+// QState holds absolute pointers into it.
 int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, const int64_t *segoff,
                   const int32_t *id, const double *val, const int32_t *seg, int64_t Fmax, const int64_t *dF,
-                  int32_t **keys_out, double **vals_out, uint32_t **filt_out)
+                  int wave)
 {
     Workspace &ws = c.ws;
-    *keys_out = nullptr;
-    *vals_out = nullptr;
-    *filt_out = nullptr;
-    ENSURE(ws.ycap, sizeof(int64_t) * 2 * (na + 1), false);
-    ENSURE(ws.yoff, sizeof(int64_t) * 2 * (na + 1), false);
-    int64_t *ycap = ws.ycap.as<int64_t>(), *yincl = ws.yoff.as<int64_t>();
-    int64_t *fw = ycap + (na + 1), *fincl = yincl + (na + 1);
-    k_ycap<<<blocks_for(na, 256), 256, 0, c.st>>>(na, act, ws.qs.as<QState>(), cont, segoff, ycap, fw);
+    ENSURE(ws.ycap, sizeof(int64_t) * 3 * (na + 1), false);
+    ENSURE(ws.yoff, sizeof(int64_t) * 3 * (na + 1), false);
+    int64_t *hs = ws.ycap.as<int64_t>(), *vs = hs + (na + 1), *rs = vs + (na + 1);
+    int64_t *hi = ws.yoff.as<int64_t>(), *vi = hi + (na + 1), *ri = vi + (na + 1);
+    const int64_t nrec = (c.g->n + 63) / 64;
+    k_ycap<<<blocks_for(na, 256), 256, 0, c.st>>>(na, act, ws.qs.as<QState>(), cont, segoff, nrec, c.g->ytable_force,
+                                                  hs, vs, rs);
     LAUNCHED(c.g);
-    int rc = scan_incl(c, ycap, yincl, na);
+    int rc = scan_incl(c, hs, hi, na);
+    if (!rc) rc = scan_incl(c, vs, vi, na);
+    if (!rc) rc = scan_incl(c, rs, ri, na);
+    if (!rc) rc = read_scalars(c, {hi + (na - 1), vi + (na - 1), ri + (na - 1)});
     if (rc) return rc;
-    rc = scan_incl(c, fw, fincl, na);
-    if (rc) return rc;
-    rc = read_scalars(c, {yincl + (na - 1), fincl + (na - 1)});
-    if (rc) return rc;
-    const int64_t Y = c.hp[0], FW = c.hp[1];
-    if (Y == 0) return ER_OK;
-    if (c.g->profiling) c.g->prof.ytable_slots += Y;
-    int32_t *keys = nullptr;
-    double *vals = nullptr;
-    uint32_t *filt = nullptr;
-    CK(cudaMallocAsync((void **)&keys, sizeof(int32_t) * Y, c.st));
-    CK(cudaMallocAsync((void **)&vals, sizeof(double) * Y, c.st));
-    if (FW > 0) CK(cudaMallocAsync((void **)&filt, sizeof(uint32_t) * FW, c.st));
-    k_yfill<<<blocks_for(std::max(Y, FW), 256), 256, 0, c.st>>>(Y, keys, vals, FW, filt);
+    const int64_t H = c.hp[0], V = c.hp[1], R = c.hp[2];
+    if (V == 0) return ER_OK;
+    if (c.g->profiling) {
+        c.g->prof.ytable_slots += H;
+        c.g->prof.yrank_records += R;
+    }
+    if ((int)ws.ychunk.size() <= wave) ws.ychunk.resize(wave + 1);
+    DevBuf &yb = ws.ychunk[wave];
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };   // 256-byte aligned regions
+    const size_t o_rec = up(sizeof(double) * V), o_key = o_rec + up(sizeof(uint4) * R);
+    const size_t ybytes = o_key + up(sizeof(int32_t) * H);
+    if (ybytes > yb.cap) CK(cudaDeviceSynchronize());   // the old buffer may still serve an earlier AMC
+    ENSURE(yb, ybytes, false);
+    double *vals = yb.as<double>();
+    uint4 *recs = reinterpret_cast<uint4 *>(yb.as<char>() + o_rec);
+    int32_t *keys = reinterpret_cast<int32_t *>(yb.as<char>() + o_key);   // buckets need 32-byte alignment
+    k_yfill<<<blocks_for(std::max(std::max(H, V), R), 256), 256, 0, c.st>>>(H, keys, V, vals, R, recs);
     LAUNCHED(c.g);
-    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, ycap, yincl, fw, fincl, keys, vals, filt,
+    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, hs, hi, vs, vi, rs, ri, keys, vals, recs,
                                                       ws.qs.as<QState>());
     LAUNCHED(c.g);
-    for (int side = 0; side < 2; side++) {
-        k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, act, ycap, ws.qs.as<QState>(),
-                                                          keys, vals, filt, side);
+    for (int pass = 0; pass < 3; pass++) {
+        if (pass == 1 && R > 0) {
+            k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, act, rs, ws.qs.as<QState>());
+            LAUNCHED(c.g);
+        }
+        if (pass == 2 && R == 0) break;
+        k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, act, vs, ws.qs.as<QState>(), pass);
         LAUNCHED(c.g);
     }
-    *keys_out = keys;
-    *vals_out = vals;
-    *filt_out = filt;
     return ER_OK;
 }
 
@@ -1406,9 +1206,6 @@ int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, c
 struct AmcGroup {
     int32_t na = 0;
     int32_t *list = nullptr;     // query ids (device), sorted by descending ell_f
-    int32_t *ykeys = nullptr;    // this group's y-table chunk
-    double *yvals = nullptr;
-    uint32_t *filt = nullptr;    // this group's membership filters
     unsigned long long eta0_sum = 0;
 };
 
@@ -1423,7 +1220,7 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
     const int32_t na = G.na;
     if (na == 0) return ER_OK;
     // per-group buffers (stream ordered on the AMC stream)
-    const int per_chunk = 32 * g->walk_np;
+    const int per_chunk = 32 * g->walk_np;   // walk pairs per warp-chunk
     int64_t maxch = (int64_t)((G.eta0_sum << (P.tau - 1)) / per_chunk) + na + 1;
     uint32_t *kk = nullptr;
     int32_t *list2 = nullptr;
@@ -1440,6 +1237,10 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
     CK(cudaMallocAsync((void **)&nch, sizeof(int64_t) * na, sb));
     CK(cudaMallocAsync((void **)&cincl, sizeof(int64_t) * na, sb));
     CK(cudaMallocAsync((void **)&parts, sizeof(TilePart) * maxch, sb));
+    unsigned long long *tctr = nullptr;   // K6 tile counters, one per batch
+    CK(cudaMallocAsync((void **)&tctr, sizeof(unsigned long long) * P.tau, sb));
+    CK(cudaMemsetAsync(tctr, 0, sizeof(unsigned long long) * P.tau, sb));
+    R.bufs.push_back(tctr);
     CK(cudaMallocAsync(&tmp, tbytes, sb));
     for (void *p : {(void *)kk, (void *)list2, (void *)nch, (void *)cincl, (void *)parts, tmp}) R.bufs.push_back(p);
     const int32_t *list = G.list;
@@ -1468,9 +1269,10 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
             CK(cudaEventCreate(&e1));
             CK(cudaEventRecord(e0, sb));
         }
-#define WALK_ARGS                                                                                           \
-    na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, P.qbase, smem_words, \
-        g->walk_hints, parts
+#define WALK_ARGS                                                                                         \
+    na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, smem_words,      \
+        g->y_evict_first,                                                                                     \
+        persist ? tctr + b : nullptr, parts
 #define WALK_LAUNCH(ARC, NP, MINB)                                                                          \
     do {                                                                                                    \
         CK(cudaFuncSetAttribute(k_walks<ARC, NP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
@@ -1479,8 +1281,9 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walks<ARC, NP, MINB>, WALK_THREADS,        \
                                                          smem_bytes));                                      \
         /* persistent grid: exactly the resident CTAs (a second wave would serialise) */                    \
+        const int64_t tiles = (bound + WALK_WARPS - 1) / WALK_WARPS;                                         \
         const unsigned grid = (unsigned)std::max<int64_t>(                                                  \
-            1, std::min<int64_t>((int64_t)std::max(occ, 1) * nsm, (bound + WALK_WARPS - 1) / WALK_WARPS));  \
+            1, persist ? std::min<int64_t>((int64_t)std::max(occ, 1) * nsm, tiles) : tiles);                \
         g->walk_occ = occ;                                                                                  \
         k_walks<ARC, NP, MINB><<<grid, WALK_THREADS, smem_bytes, sb>>>(WALK_ARGS);                          \
     } while (0)
@@ -1490,24 +1293,17 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
         else if (g->d_arcs) WALK_LAUNCH(1, NP, MINB);        \
         else WALK_LAUNCH(0, NP, MINB);                       \
     } while (0)
-        if (g->walk_kernel == 3) {
-            const unsigned grid3 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(4 * nsm, (bound + WALK_WARPS - 1) / WALK_WARPS));
-            if (g->d_parcs) k_walks3<2><<<grid3, WALK_THREADS, 0, sb>>>(na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, P.qbase, parts);
-            else if (g->d_arcs) k_walks3<1><<<grid3, WALK_THREADS, 0, sb>>>(na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, P.qbase, parts);
-            else k_walks3<0><<<grid3, WALK_THREADS, 0, sb>>>(na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, P.qbase, parts);
-            g->walk_occ = 4;
-        } else {
         const int32_t smem_words = g->walk_smem_words;
+        // persistent CTAs would hold every SM until the last tile: with the SMM head running
+        // concurrently (overlap) the hardware scheduler interleaves one-tile CTAs instead
+        const bool persist = g->walk_persist && !g->amc_overlap;
         const size_t smem_bytes = sizeof(int32_t) * (size_t)smem_words;
         if (g->walk_np == 1) {
-            if (g->walk_minb == 2) WALK_ARC(1, 2);
-            else if (g->walk_minb == 3) WALK_ARC(1, 3);
+            if (g->walk_minb == 3) WALK_ARC(1, 3);
             else WALK_ARC(1, 4);
         } else {
-            if (g->walk_minb == 2) WALK_ARC(2, 2);
-            else if (g->walk_minb == 3) WALK_ARC(2, 3);
+            if (g->walk_minb == 3) WALK_ARC(2, 3);
             else WALK_ARC(2, 4);
-        }
         }
 #undef WALK_ARC
 #undef WALK_LAUNCH
@@ -1593,7 +1389,17 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                     double *out_r, er_query_stats *stats)
 {
     Workspace &ws = g->ws;
-    cudaStream_t st = o.cuda_stream ? (cudaStream_t)o.cuda_stream : g->stream;
+    // The batch runs on the handle's high-priority head stream (so SMM-head kernels are scheduled
+    // ahead of AMC walk CTAs when both are queued), forked from and joined back into the
+    // caller's stream.
+    const cudaStream_t user = o.cuda_stream ? (cudaStream_t)o.cuda_stream : g->stream;
+    const cudaStream_t st = g->head_stream;
+    if (!g->ev_in) {
+        CK(cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g->ev_out, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(g->ev_in, user));
+    CK(cudaStreamWaitEvent(st, g->ev_in, 0));
     if (!ws.host_pinned) {
         CK(cudaMallocHost(&ws.host_pinned, 4096));
         ws.host_pinned_cap = 4096;
@@ -1627,9 +1433,15 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         CK(cudaMemcpyAsync(ws.pairs.p, pairs, sizeof(int32_t) * 2 * k, cudaMemcpyHostToDevice, st));
         d_pairs = ws.pairs.as<int32_t>();
     }
+    const int64_t *d_ids = o.query_ids;
+    if (d_ids && !o.pairs_on_device) {
+        ENSURE(ws.qids, sizeof(int64_t) * k, false);
+        CK(cudaMemcpyAsync(ws.qids.p, o.query_ids, sizeof(int64_t) * k, cudaMemcpyHostToDevice, st));
+        d_ids = ws.qids.as<int64_t>();
+    }
     ENSURE(ws.qs, sizeof(QState) * k, false);
     QState *qs = ws.qs.as<QState>();
-    k_setup<<<blocks_for(k, 128), 128, 0, st>>>(k, d_pairs, g->d_off, P, qs);
+    k_setup<<<blocks_for(k, 128), 128, 0, st>>>(k, d_pairs, d_ids, g->d_off, P, qs);
     LAUNCHED(g);
 
     const int32_t K = (int32_t)k;
@@ -1681,11 +1493,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
     // together after the head (fewer, fuller walk launches).  The tables' buffers live until
     // the end of the batch either way.
     const bool overlap = g->amc_overlap;
-    auto fork_group = [&](int32_t na, const int32_t *act, const int32_t *cont, int32_t *tkeys, double *tvals,
-                          uint32_t *tfilt) -> int {
-        if (tkeys) R.bufs.push_back(tkeys);
-        if (tvals) R.bufs.push_back(tvals);
-        if (tfilt) R.bufs.push_back(tfilt);
+    auto fork_group = [&](int32_t na, const int32_t *act, const int32_t *cont) -> int {
         if (!overlap) return ER_OK;
         // list of the queries of act leaving now for AMC
         int32_t *flag = ws.cont2.as<int32_t>();
@@ -1728,14 +1536,11 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                                                                        ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(),
                                                                        ws.fr_seg.as<int32_t>(), ws.fr_off.as<int64_t>());
                 LAUNCHED(g);
-                int32_t *tk = nullptr;
-                double *tv = nullptr;
-                uint32_t *tf = nullptr;
                 rc = build_ytables(c, (int32_t)n0, ws.act.as<int32_t>(), nullptr, ws.fr_off.as<int64_t>(),
                                    ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(), ws.fr_seg.as<int32_t>(), F0, nullptr,
-                                   &tk, &tv, &tf);
+                                   0);
                 if (rc) return rc;
-                rc = fork_group((int32_t)n0, ws.act.as<int32_t>(), nullptr, tk, tv, tf);
+                rc = fork_group((int32_t)n0, ws.act.as<int32_t>(), nullptr);
                 if (rc) return rc;
             }
             na = 0;
@@ -1753,6 +1558,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             LAUNCHED(g);
         }
         bool first_wave = true;
+        int wave_no = 0;
         while (na > 0) {
             const int32_t nseg = (int32_t)(2 * na);
             // emission offsets
@@ -1820,14 +1626,11 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             LAUNCHED(g);
             // y-tables for queries leaving the head now, then their AMC on the AMC stream
             {
-                int32_t *tk = nullptr;
-                double *tv = nullptr;
-                uint32_t *tf = nullptr;
                 rc = build_ytables(c, (int32_t)na, ws.act.as<int32_t>(), cont, ws.nf_off.as<int64_t>(),
-                                   ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), E, dU, &tk,
-                                   &tv, &tf);
+                                   ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), E, dU,
+                                   1 + wave_no);
                 if (rc) return rc;
-                rc = fork_group((int32_t)na, ws.act.as<int32_t>(), cont, tk, tv, tf);
+                rc = fork_group((int32_t)na, ws.act.as<int32_t>(), cont);
                 if (rc) return rc;
             }
             // compaction of continuing queries
@@ -1865,6 +1668,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             na = na2;
             F = F2;
             first_wave = false;
+            wave_no++;
         }
     }
 
@@ -1909,6 +1713,8 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
     }
     if (prof) CK(cudaEventRecord(ev_end, st));
     for (void *p : R.bufs) CK(cudaFreeAsync(p, st));
+    CK(cudaEventRecord(g->ev_out, st));
+    CK(cudaStreamWaitEvent(user, g->ev_out, 0));   // the caller's stream sees the results
     if (o.synchronous || !o.out_on_device || prof) CK(cudaStreamSynchronize(st));
     cudaEventDestroy(ev_amc_done);
     if (prof) {

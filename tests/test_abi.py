@@ -58,7 +58,7 @@ int main(void) {
   O(er_query_stats, walk_checksum); O(er_query_stats, tie_flags);
   printf("opts %zu\n", sizeof(er_opts));
   O(er_opts, seed); O(er_opts, query_index_base); O(er_opts, cuda_stream);
-  O(er_opts, pairs_on_device); O(er_opts, synchronous);
+  O(er_opts, pairs_on_device); O(er_opts, synchronous); O(er_opts, query_ids);
   return 0;
 }''')
     exe = tmp_path / "layout"
@@ -71,13 +71,14 @@ int main(void) {
         assert vals[f] == d.fields[f][1], f
     o = G.er_opts
     assert vals["opts"] == ctypes.sizeof(o)
-    for f in ("seed", "query_index_base", "cuda_stream", "pairs_on_device", "synchronous"):
+    for f in ("seed", "query_index_base", "cuda_stream", "pairs_on_device", "synchronous", "query_ids"):
         assert vals[f] == getattr(o, f).offset, f
 
 
 def test_defaults(G):
     o = G.er_opts_default()
     assert o.tau == 5 and o.force_ell_b == -1 and o.seed == G.ER_DEFAULT_SEED and o.synchronous == 1
+    assert not o.query_ids
     text = HEADER.read_text()
     assert "0x%XULL" % G.ER_DEFAULT_SEED in text
 

@@ -366,3 +366,65 @@ def test_spmm_k9_rmat20_sampled_columns(geer, rmat20):
         want = oracle.propagate_dense(g, X[:, c])
         assert np.array_equal(Yh[light, c], want[light])
         assert np.allclose(Yh[~light, c], want[~light], rtol=1e-13, atol=0)
+
+
+def test_query_ids_partition_reproduces_batch(geer, rmat20):
+    """Cost-model partition (dist.partition) with global query ids: every query's result is
+    byte-identical to the unsharded batch (RNG keyed by the global index, R10), for host and
+    device id arrays; and an id outside [0, 2^32) is rejected."""
+    import torch
+    from paper_2312_06123_b200.dist import partition, predicted_cost
+    g, pairs, _, h = rmat20
+    sub = pairs[:2000]
+    full, _ = geer.er_query_batch_ex(h, sub, 0.2)
+    parts = partition(predicted_cost(sub, g.degrees(), g.lam, 0.2), 3)
+    got = np.empty_like(full)
+    for r, idx in enumerate(parts):
+        if r == 0:
+            got[idx] = geer.er_query_batch_ex(h, sub[idx], 0.2, query_ids=idx)[0]
+        else:   # device pairs + device ids
+            out = torch.zeros(len(idx), dtype=torch.float64, device="cuda")
+            geer.er_query_batch_ex(h, torch.from_numpy(np.ascontiguousarray(sub[idx])).cuda(), 0.2, out=out,
+                                   query_ids=torch.from_numpy(idx.astype(np.int64)).cuda())
+            got[idx] = out.cpu().numpy()
+    assert got.tobytes() == full.tobytes()
+    with pytest.raises(geer.GeerError):
+        geer.er_query_batch_ex(h, sub[:2], 0.2, query_ids=np.array([0, 1 << 32]))
+
+
+@pytest.mark.parametrize("graph", ["tiny", "rmat20"])
+def test_ytable_layouts_and_kernel_variants_byte_identical(graph, tiny, rmat20):
+    """The y-table layout (hash / rank bitmap) and the walk-kernel schedule
+    (persistent or not, overlap with the head) change no output bit: they are layouts and
+    schedules of the same arithmetic.  Two walk pairs per thread regroup the per-chunk partial
+    sums (64 walks per warp instead of 32): walk endpoints stay bit-identical, estimates agree
+    to ulps.  Each combination runs in a fresh process (the knobs are read at
+    er_graph_create)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, '.'); import workloads as W;"
+            "import paper_2312_06123_b200 as G;"
+            f"g, pairs, _ = W.load_config('{graph}');"
+            "h = G.er_graph_create(g.n, g.offsets, g.cols); G.er_graph_set_lambda(h, float(sys.argv[1]));"
+            "r, st = G.er_query_batch_ex(h, pairs[:3000], 0.1, stats=True);"
+            "sys.stdout.buffer.write(r.tobytes() + st['walk_checksum'].tobytes())")
+    g = (tiny if graph == "tiny" else rmat20)[0]
+    outs = {}
+    for env in ({"GEER_YTABLE": "hash"}, {"GEER_YTABLE": "rank"}, {},
+                {"GEER_WALK_NP": "2"}, {"GEER_WALK_NP": "2", "GEER_WALK_MINB": "3"}, {"GEER_WALK_PERSIST": "0"},
+                {"GEER_AMC_OVERLAP": "1"}):
+        e = dict(os.environ, **env)
+        outs[str(env)] = subprocess.run([sys.executable, "-c", code, repr(g.lam)], env=e, check=True,
+                                        capture_output=True, cwd=str(W.Path(__file__).resolve().parents[1])).stdout
+    ref = outs["{}"]
+    assert len(ref) > 0
+    n = len(ref) // 16
+    r0, c0 = np.frombuffer(ref[:8 * n], np.float64), np.frombuffer(ref[8 * n:], np.uint64)
+    for k, v in outs.items():
+        if "GEER_WALK_NP" in k:
+            r1, c1 = np.frombuffer(v[:8 * n], np.float64), np.frombuffer(v[8 * n:], np.uint64)
+            assert np.array_equal(c1, c0), k
+            assert np.abs(r1 - r0).max() <= 1e-12, k
+        else:
+            assert v == ref, k

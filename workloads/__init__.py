@@ -12,6 +12,10 @@ Recipes (DESIGN.md "Inputs"):
                    quadrant probabilities (a,b,c,d), symmetrise, drop self-loops,
                    dedupe, keep the largest connected component, random relabel,
                    CSR with every adjacency list sorted ascending.
+* ``rmat_torch``   the same recipe in torch on the GPU (configs 3-5 at full size, where numpy
+                   takes minutes): counter-seeded torch.Generator draws, torch.unique for
+                   dedupe, min-label propagation for the largest component.  A different
+                   random stream from ``rmat`` (numpy), so a different (equally valid) graph.
 * ``query_pairs``  the paper's protocol: half uniform random node pairs,
                    half uniform random edges, each edge oriented by a fair coin.
 * ``lambda_of``    lambda = max(|lambda_2|, |lambda_n|) of P (Eq. 6) by
@@ -231,6 +235,72 @@ def rmat(scale: int, edge_factor: float, a=0.57, b=0.19, c=0.19, d=0.05, seed: i
                                         "abcd": [a, b, c, d], "seed": seed})
 
 
+def rmat_torch(scale: int, edge_factor: float, a=0.57, b=0.19, c=0.19, d=0.05, seed: int = 20231212,
+               device: str | None = None, name: str | None = None) -> Graph:
+    """R-MAT on the GPU (torch), same recipe as ``rmat``: symmetrise, drop self-loops, dedupe,
+    keep the largest connected component, random relabel, sorted CSR.  Returns a host Graph."""
+    import torch
+    assert abs(a + b + c + d - 1.0) < 1e-9
+    dev = torch.device(device or ("cuda" if torch.cuda.is_available() else "cpu"))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    N = 1 << scale
+    ne = int(edge_factor * N)
+    ab, abc = a + b, a + b + c
+    keys = []
+    chunk = 1 << 26
+    for lo in range(0, ne, chunk):
+        m = min(chunk, ne - lo)
+        u = torch.zeros(m, dtype=torch.int64, device=dev)
+        v = torch.zeros(m, dtype=torch.int64, device=dev)
+        for _ in range(scale):
+            r = torch.rand(m, generator=gen, device=dev, dtype=torch.float64)
+            ub = (r >= ab).to(torch.int64)
+            vb = (((r >= a) & (r < ab)) | (r >= abc)).to(torch.int64)
+            u = (u << 1) | ub
+            v = (v << 1) | vb
+        keep = u != v
+        u, v = u[keep], v[keep]
+        keys.append(torch.unique(torch.cat([u * N + v, v * N + u])))
+        del u, v, keep
+    key = torch.unique(torch.cat(keys))
+    del keys
+    u = key // N
+    v = key % N
+    del key
+    # largest connected component: min-label propagation over the (symmetric) arcs
+    lab = torch.arange(N, device=dev, dtype=torch.int64)
+    while True:
+        nl = lab.clone()
+        nl.scatter_reduce_(0, u, lab[v], reduce="amin")
+        nl = nl[nl]                      # pointer jumping
+        if torch.equal(nl, lab):
+            break
+        lab = nl
+    present = torch.zeros(N, dtype=torch.bool, device=dev)
+    present[u] = True
+    cnt = torch.bincount(lab[present], minlength=N)
+    big = int(torch.argmax(cnt))
+    keepn = torch.nonzero(present & (lab == big)).squeeze(1)
+    n = int(keepn.numel())
+    relabel = torch.full((N,), -1, dtype=torch.int64, device=dev)
+    relabel[keepn] = torch.randperm(n, generator=gen, device=dev)
+    mk = relabel[u] >= 0
+    u2, v2 = relabel[u[mk]], relabel[v[mk]]
+    del u, v, mk, lab, relabel
+    key, _ = torch.sort(u2 * n + v2)
+    del u2, v2
+    uu = key // n
+    cols = (key % n).to(torch.int32)
+    counts = torch.bincount(uu, minlength=n)
+    off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    off[1:] = torch.cumsum(counts, 0)
+    nm = name or f"rmat_torch_s{scale}_ef{edge_factor:g}_{a:g}_{b:g}_{c:g}_{d:g}_seed{seed}"
+    return Graph(n, off.cpu().numpy(), cols.cpu().numpy(), nm,
+                 meta={"scale": scale, "edge_factor": edge_factor, "abcd": [a, b, c, d], "seed": seed,
+                       "generator": "torch"})
+
+
 # ------------------------------------------------------------ queries
 def query_pairs(g: Graph, nq: int, seed: int) -> np.ndarray:
     """P:616 protocol: first half uniform random node pairs, second half uniform
@@ -276,6 +346,10 @@ CONFIGS = {
     "lj": ("rmat", dict(scale=23, edge_factor=4.5, seed=20231212), 100_000, [0.1]),
     "orkut": ("rmat", dict(scale=18, edge_factor=40, a=0.45, b=0.22, c=0.22, d=0.11, seed=20231213),
               100_000, [0.2, 0.1]),
+    # full-size stand-ins generated on the GPU (rmat_torch)
+    "lj_full": ("rmat_torch", dict(scale=23, edge_factor=4.5, seed=20231212), 100_000, [0.1]),
+    "orkut_full": ("rmat_torch", dict(scale=22, edge_factor=28, a=0.45, b=0.22, c=0.22, d=0.11, seed=20231213),
+                   100_000, [0.2, 0.1]),
 }
 
 
@@ -297,7 +371,7 @@ def load_config(name: str, with_lambda: bool = False) -> tuple[Graph, np.ndarray
                   float(z["lam"]) if float(z["lam"]) > 0 else None)
         pairs = z["pairs"]
     else:
-        g = tiny_er(**params) if kind == "tiny_er" else rmat(**params)
+        g = {"tiny_er": tiny_er, "rmat": rmat, "rmat_torch": rmat_torch}[kind](**params)
         pairs = query_pairs(g, nq, seed=params["seed"] + 1)
         g.lam = None
     if with_lambda and g.lam is None:
