@@ -994,6 +994,23 @@ __global__ void k_sum_eta0(int32_t na, const int32_t *__restrict__ list, const Q
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
 }
 
+// All queries in phase PH_AMC: flags for the AMC list and the sum of their eta0 (sizes the
+// per-batch partial buffers), in one pass.
+__global__ void k_amc_flags(int64_t k, const QState *__restrict__ qs, int32_t *__restrict__ flags,
+                            int32_t *__restrict__ ids, unsigned long long *__restrict__ eta0_sum)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool amc = i < k && qs[i].phase == PH_AMC;
+    if (i < k) {
+        flags[i] = amc ? 1 : 0;
+        ids[i] = (int32_t)i;
+    }
+    unsigned long long v = amc ? (unsigned long long)qs[i].st.eta0 : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(eta0_sum, v);
+}
+
 // K8: r' = r_f + r_b (Alg. 3 L11); s = t -> 0.
 __global__ void k_finalize(int64_t k, const QState *__restrict__ qs, double *__restrict__ out,
                            er_query_stats *__restrict__ stats)
@@ -1150,9 +1167,10 @@ int select_list(Ctx &c, const int32_t *ids, const int32_t *flag, int32_t n, int3
 // queries of the list leave).  The tables of SMM wave `wave` live in a grow-only workspace
 // buffer kept across batches: {vals fp64[V] | rank records uint4[R] | hash keys int32[H]};
 // QState holds absolute pointers into it.
-int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, const int64_t *segoff,
-                  const int32_t *id, const double *val, const int32_t *seg, int64_t Fmax, const int64_t *dF,
-                  int wave)
+// Phase 1 (no host sync): per-query sizes and their inclusive scans; the three totals are at
+// *tot_h, *tot_v, *tot_r (device) for the caller to read with its other scalars.
+int ytable_plan(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, const int64_t *segoff,
+                const int64_t **tot_h, const int64_t **tot_v, const int64_t **tot_r)
 {
     Workspace &ws = c.ws;
     ENSURE(ws.ycap, sizeof(int64_t) * 3 * (na + 1), false);
@@ -1166,9 +1184,19 @@ int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, c
     int rc = scan_incl(c, hs, hi, na);
     if (!rc) rc = scan_incl(c, vs, vi, na);
     if (!rc) rc = scan_incl(c, rs, ri, na);
-    if (!rc) rc = read_scalars(c, {hi + (na - 1), vi + (na - 1), ri + (na - 1)});
-    if (rc) return rc;
-    const int64_t H = c.hp[0], V = c.hp[1], R = c.hp[2];
+    *tot_h = hi + (na - 1);
+    *tot_v = vi + (na - 1);
+    *tot_r = ri + (na - 1);
+    return rc;
+}
+
+// Phase 2: allocate and fill the tables planned by ytable_plan (totals H, V, R read by the caller).
+int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int32_t *id, const double *val, const int32_t *seg,
+                 int64_t Fmax, const int64_t *dF, int wave, int64_t H, int64_t V, int64_t R)
+{
+    Workspace &ws = c.ws;
+    int64_t *hs = ws.ycap.as<int64_t>(), *vs = hs + (na + 1), *rs = vs + (na + 1);
+    int64_t *hi = ws.yoff.as<int64_t>(), *vi = hi + (na + 1), *ri = vi + (na + 1);
     if (V == 0) return ER_OK;
     if (c.g->profiling) {
         c.g->prof.ytable_slots += H;
@@ -1199,6 +1227,18 @@ int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, c
         LAUNCHED(c.g);
     }
     return ER_OK;
+}
+
+int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, const int64_t *segoff,
+                  const int32_t *id, const double *val, const int32_t *seg, int64_t Fmax, const int64_t *dF,
+                  int wave)
+{
+    const int64_t *th, *tv, *tr;
+    int rc = ytable_plan(c, na, act, cont, segoff, &th, &tv, &tr);
+    if (!rc) rc = read_scalars(c, {th, tv, tr});
+    if (rc) return rc;
+    const int64_t H = c.hp[0], V = c.hp[1], R = c.hp[2];
+    return ytable_build(c, na, act, id, val, seg, Fmax, dF, wave, H, V, R);
 }
 
 // One AMC group: the queries that left the SMM head in the same wave, with their y-tables.
@@ -1350,11 +1390,16 @@ int smm_group(Ctx &c, int64_t E, int64_t F, int32_t nseg, const int64_t *ent_off
     // chunk boundaries in emission order (segbeg on the host: nseg+1 int32)
     const int32_t nchunks = (int32_t)((nseg + spc - 1) / spc);
     std::vector<int32_t> hb(nchunks + 1);
-    for (int32_t ch = 0; ch <= nchunks; ch++) {
-        const int64_t gs = std::min<int64_t>((int64_t)ch * spc, nseg);
-        CK(cudaMemcpyAsync(&hb[ch], segbeg + gs, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    if (nchunks == 1) {
+        hb[0] = 0;                 // one chunk: all E pairs (no host read)
+        hb[1] = (int32_t)E;
+    } else {
+        for (int32_t ch = 0; ch <= nchunks; ch++) {
+            const int64_t gs = std::min<int64_t>((int64_t)ch * spc, nseg);
+            CK(cudaMemcpyAsync(&hb[ch], segbeg + gs, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        }
+        CK(cudaStreamSynchronize(st));
     }
-    CK(cudaStreamSynchronize(st));
     for (int32_t ch = 0; ch < nchunks; ch++) {
         const int64_t lo = hb[ch], n = (int64_t)hb[ch + 1] - hb[ch];
         if (n <= 0) continue;
@@ -1468,18 +1513,21 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
     // the AMC stream starts after everything enqueued so far on the main stream (inputs, setup)
     // Launch the AMC of a list of queries (all in phase PH_AMC with their y-tables built) on the
     // AMC stream, after everything enqueued so far on the main stream.
-    auto launch_list = [&](int32_t ng, const int32_t *list_src) -> int {
+    auto launch_list = [&](int32_t ng, const int32_t *list_src, int64_t known_eta0_sum = -1) -> int {
         AmcGroup G;
         G.na = ng;
         CK(cudaMallocAsync((void **)&G.list, sizeof(int32_t) * ng, st));
         CK(cudaMemcpyAsync(G.list, list_src, sizeof(int32_t) * ng, cudaMemcpyDeviceToDevice, st));
-        unsigned long long *d_sum = reinterpret_cast<unsigned long long *>(ws.scalars.as<int64_t>() + 4);
-        CK(cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), st));
-        k_sum_eta0<<<blocks_for(ng, 256), 256, 0, st>>>(ng, G.list, qs, d_sum);
-        LAUNCHED(g);
-        int rr = read_scalars(c, {reinterpret_cast<const int64_t *>(d_sum)});
-        if (rr) return rr;
-        G.eta0_sum = (unsigned long long)c.hp[0];
+        if (known_eta0_sum < 0) {
+            unsigned long long *d_sum = reinterpret_cast<unsigned long long *>(ws.scalars.as<int64_t>() + 4);
+            CK(cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), st));
+            k_sum_eta0<<<blocks_for(ng, 256), 256, 0, st>>>(ng, G.list, qs, d_sum);
+            LAUNCHED(g);
+            int rr = read_scalars(c, {reinterpret_cast<const int64_t *>(d_sum)});
+            if (rr) return rr;
+            known_eta0_sum = c.hp[0];
+        }
+        G.eta0_sum = (unsigned long long)known_eta0_sum;
         R.bufs.push_back(G.list);
         cudaEvent_t e;
         CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1624,16 +1672,11 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             k_decide<<<blocks_for(na, 128), 128, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), ws.segstat.as<SegStat>(),
                                                           P, qs, cont);
             LAUNCHED(g);
-            // y-tables for queries leaving the head now, then their AMC on the AMC stream
-            {
-                rc = build_ytables(c, (int32_t)na, ws.act.as<int32_t>(), cont, ws.nf_off.as<int64_t>(),
-                                   ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), E, dU,
-                                   1 + wave_no);
-                if (rc) return rc;
-                rc = fork_group((int32_t)na, ws.act.as<int32_t>(), cont);
-                if (rc) return rc;
-            }
-            // compaction of continuing queries
+            // y-table plan of the queries leaving the head now + compaction scans of the others,
+            // then ONE host read for all sizes
+            const int64_t *th, *tv, *tr;
+            rc = ytable_plan(c, (int32_t)na, ws.act.as<int32_t>(), cont, ws.nf_off.as<int64_t>(), &th, &tv, &tr);
+            if (rc) return rc;
             int32_t *newidx = ws.idx.as<int32_t>();
             rc = scan_incl(c, cont, newidx, na);
             if (rc) return rc;
@@ -1646,9 +1689,19 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             if (rc) return rc;
             CK(cudaMemcpyAsync(c.hp + 0, newidx + (na - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(c.hp + 1, segnew + (nseg - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(c.hp + 2, th, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(c.hp + 3, tv, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(c.hp + 4, tr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             const int64_t na2 = (int64_t)(*reinterpret_cast<int32_t *>(c.hp + 0));
             const int64_t F2 = c.hp[1];
+            const int64_t YH = c.hp[2], YV = c.hp[3], YR = c.hp[4];
+            // y-tables, then (overlap) their AMC on the AMC stream
+            rc = ytable_build(c, (int32_t)na, ws.act.as<int32_t>(), ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
+                              ws.nf_seg.as<int32_t>(), E, dU, 1 + wave_no, YH, YV, YR);
+            if (rc) return rc;
+            rc = fork_group((int32_t)na, ws.act.as<int32_t>(), cont);
+            if (rc) return rc;
             if (na2 > 0) {
                 ENSURE(ws.fr_id, sizeof(int32_t) * F2, false);
                 ENSURE(ws.fr_val, sizeof(double) * F2, false);
@@ -1675,15 +1728,23 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
     if (!overlap) {
         // every query now in phase AMC: one AMC run over all of them
         ENSURE(ws.ids, sizeof(int32_t) * (k + 1), false);
-        k_flag_phase<<<blocks_for(k, 256), 256, 0, st>>>(k, qs, PH_AMC, ws.cont.as<int32_t>(), ws.ids.as<int32_t>());
+        unsigned long long *d_sum = reinterpret_cast<unsigned long long *>(ws.scalars.as<int64_t>() + 5);
+        CK(cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), st));
+        k_amc_flags<<<blocks_for(k, 256), 256, 0, st>>>(k, qs, ws.cont.as<int32_t>(), ws.ids.as<int32_t>(), d_sum);
         LAUNCHED(g);
-        int64_t n_amc = 0;
-        rc = select_list(c, ws.ids.as<int32_t>(), ws.cont.as<int32_t>(), K, ws.act.as<int32_t>(),
-                         ws.idx.as<int32_t>(), &n_amc);
+        rc = scan_incl(c, ws.cont.as<int32_t>(), ws.idx.as<int32_t>(), K);
         if (rc) return rc;
+        k_select<<<blocks_for(K, 256), 256, 0, st>>>(K, ws.ids.as<int32_t>(), ws.cont.as<int32_t>(),
+                                                      ws.idx.as<int32_t>(), ws.act.as<int32_t>());
+        LAUNCHED(g);
+        CK(cudaMemcpyAsync(c.hp + 0, ws.idx.as<int32_t>() + (K - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(c.hp + 1, d_sum, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const int64_t n_amc = (int64_t)(*reinterpret_cast<int32_t *>(c.hp + 0));
+        const int64_t amc_eta0 = c.hp[1];
         if (prof) CK(cudaEventRecord(ev_smm_end, st));
         if (n_amc > 0) {
-            rc = launch_list((int32_t)n_amc, ws.act.as<int32_t>());
+            rc = launch_list((int32_t)n_amc, ws.act.as<int32_t>(), amc_eta0);
             if (rc) return rc;
         }
     } else if (prof) {
