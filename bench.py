@@ -378,6 +378,21 @@ def main():
             line["spmm_q64"] = sp64
         except Exception as ex:  # noqa: BLE001
             line["spmm"] = {"error": str(ex)}
+        try:
+            # the paper's accuracy protocol: 100 random pairs + 100 edges against the
+            # deterministic series run to a 1e-8 tail (er_smm_series, K9 passes)
+            half = nq // 2
+            sub = np.concatenate([pairs[:100], pairs[half:half + 100]])
+            t0 = time.perf_counter()
+            truth, ells = G.er_smm_series(h, sub, tol=1e-8)
+            t_truth = time.perf_counter() - t0
+            est = G.er_query_batch_ex(h, sub, args.eps, 0.01, query_index_base=lo)[0]
+            err = np.abs(est - truth)
+            line["accuracy"] = {"queries": int(len(sub)), "eps": args.eps, "max_abs_err": float(err.max()),
+                                "mean_abs_err": float(err.mean()), "frac_within_eps": float(np.mean(err <= args.eps)),
+                                "truth": "er_smm_series tol 1e-8 (Thm 3.1 tail), L mean %.0f, %.2f s" % (ells.mean(), t_truth)}
+        except Exception as ex:  # noqa: BLE001
+            line["accuracy"] = {"error": str(ex)}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_leg(g, g.lam, pairs, args.eps)
         print(json.dumps(line), flush=True)

@@ -180,6 +180,21 @@ int er_query_batch_ex(er_graph *g, const int32_t *pairs, int64_t k, double eps, 
 int er_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, void *stream);
 
 /*
+ * er_smm_series -- the deterministic series truncated by a tolerance (SMM-to-ell, the paper's
+ * SMM baseline and its ground-truth generator, Alg. 2, Thm 3.1):
+ *     r_L(s,t) = sum_{i=0..L} ( y_i(s) - y_i(t) ),  y_0 = e_s/d_s - e_t/d_t,  y_{i+1} = P y_i
+ * (the single signed vector form of Alg. 2's s*, t* pair: y_i = P^i e_s / d_s - P^i e_t / d_t).
+ * L per query = Eq. 6's ell with eps = tol (the smallest L whose Thm 3.1 tail bound
+ * (2/d_s + 2/d_t) lambda^(L+1) / (1 - lambda) is <= tol), capped at max_iters.  Each step is one
+ * K9 pass over a block of up to 64 query columns.  s = t gives 0.
+ *   pairs   HOST int32[2k];  out_r HOST double[k];  ells HOST int32[k] (L used; may be NULL)
+ *   tol > 0, 0 <= max_iters <= 100000; lambda must be set (er_graph_set_lambda / estimate).
+ * Synchronous.  Errors: ER_EINVAL (arguments / node ids), ER_ESPECTRAL (lambda unset).
+ */
+int er_smm_series(er_graph *g, const int32_t *pairs, int64_t k, double tol, int32_t max_iters, double *out_r,
+                  int32_t *ells);
+
+/*
  * Profiling (used by bench.py for the live roofline).  When enabled, every query batch
  * records CUDA events on its stream around each AMC walk launch (K6) and around the SMM
  * head, and counts walk steps on the device; er_graph_profile_read returns the sums since

@@ -182,6 +182,24 @@ def smm(g, s, t, ell_b):
     return float(rb), terms[:ell_b], xs, xt
 
 
+def series_signed(g, s, t, L) -> float:
+    """Eq. 4's r_L(s,t) in the single signed-vector form (SURVEY 8(c) reading 1):
+    y_0 = e_s/d_s - e_t/d_t, y_{i+1} = P y_i, r_L = sum_{i=0..L} (y_i(s) - y_i(t)),
+    each P step the oracle's sequential dense pull."""
+    d = np.diff(np.asarray(g.offsets))
+    if s == t:
+        return 0.0
+    y = np.zeros(g.n)
+    y[s] = 1.0 / d[s]
+    y[t] = -1.0 / d[t]
+    total = 0.0
+    for i in range(L + 1):
+        total += y[s] - y[t]
+        if i < L:
+            y = propagate_dense(g, y)
+    return float(total)
+
+
 def walk(g, start, lf, seed=DEFAULT_SEED, q=0, b=0, side=0, k=0, y=None):
     off, cols = _csr(g)
     trace = np.zeros(max(lf, 1), dtype=np.int32)

@@ -40,7 +40,7 @@ EXPORTED = ["er_graph_create", "er_graph_create_ex", "er_graph_destroy", "er_que
             "er_last_error_message", "er_graph_lambda", "er_graph_set_lambda",
             "er_graph_estimate_lambda", "er_graph_num_nodes", "er_graph_num_arcs",
             "er_graph_kernel_launches", "er_opts_default", "er_query_batch_ex", "er_spmm",
-            "er_graph_profile", "er_graph_profile_read"]
+            "er_graph_profile", "er_graph_profile_read", "er_smm_series"]
 
 
 class er_opts(ctypes.Structure):
@@ -93,6 +93,8 @@ def _load():
     L.er_opts_default.restype = None
     L.er_spmm.argtypes = [vp, vp, vp, i32, i32, vp]
     L.er_spmm.restype = ctypes.c_int
+    L.er_smm_series.argtypes = [vp, vp, i64, dbl, i32, vp, vp]
+    L.er_smm_series.restype = ctypes.c_int
     L.er_graph_profile.argtypes = [vp, ctypes.c_int]
     L.er_graph_profile_read.argtypes = [vp, ctypes.POINTER(er_profile)]
     return L
@@ -253,6 +255,18 @@ def er_spmm(g, X, Y, normalize: bool = True, stream=None) -> None:
         stream = torch.cuda.current_stream(X.device)
     s = _stream_handle(stream)
     _raise(lib.er_spmm(g, ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(Y.data_ptr()), q, int(normalize), s))
+
+
+def er_smm_series(g, pairs, tol: float = 1e-10, max_iters: int = 100000):
+    """Deterministic series r_L(s,t) truncated at Thm 3.1's tail bound <= tol (SMM-to-ell /
+    ground truth, include/geer.h).  Host arrays in/out.  Returns (r, L)."""
+    p = np.ascontiguousarray(np.asarray(pairs, dtype=np.int32).reshape(-1, 2))
+    k = p.shape[0]
+    out = np.zeros(k, dtype=np.float64)
+    ells = np.zeros(k, dtype=np.int32)
+    _raise(lib.er_smm_series(g, p.ctypes.data_as(ctypes.c_void_p), k, float(tol), int(max_iters),
+                             out.ctypes.data_as(ctypes.c_void_p), ells.ctypes.data_as(ctypes.c_void_p)))
+    return out, ells
 
 
 def er_graph_profile(g, enable: bool = True) -> None:

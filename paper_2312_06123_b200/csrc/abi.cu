@@ -260,6 +260,7 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_YTABLE")) g->ytable_force = !strcmp(env, "hash") ? 1 : !strcmp(env, "rank") ? 2 : 0;
         if (const char *env = getenv("GEER_Y_EVICT_FIRST")) g->y_evict_first = atoi(env) != 0;
         if (const char *env = getenv("GEER_L2_PERSIST")) g->l2_persist = atoi(env) != 0;
+        if (const char *env = getenv("GEER_OVERLAP_FRAC")) g->overlap_frac = std::min(1.0, std::max(0.1, atof(env)));
         if (const char *env = getenv("GEER_WALK_NP")) g->walk_np = atoi(env) == 1 ? 1 : 2;
         if (const char *env = getenv("GEER_WALK_SMEM_KB")) g->walk_smem_words = 256 * std::min(48, std::max(8, atoi(env)));
         g->pack.bo = bo;
@@ -423,6 +424,32 @@ int er_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normaliz
     if (q < 1 || q > 256) { set_error(ER_EINVAL, "q must be in [1,256]"); return ER_EINVAL; }
     std::lock_guard<std::mutex> lk(g->mu);
     return run_spmm(g, X, Y, q, normalize, stream ? (cudaStream_t)stream : g->stream);
+}
+
+int er_smm_series(er_graph *g, const int32_t *pairs, int64_t k, double tol, int32_t max_iters, double *out_r,
+                  int32_t *ells)
+{
+    clear_error();
+    if (!g) { set_error(ER_EINVAL, "NULL graph"); return ER_EINVAL; }
+    if (k < 0 || (k > 0 && (!pairs || !out_r))) { set_error(ER_EINVAL, "bad k / NULL pointers"); return ER_EINVAL; }
+    if (!(tol > 0.0) || !std::isfinite(tol)) { set_error(ER_EINVAL, "tol must be > 0"); return ER_EINVAL; }
+    if (max_iters < 0 || max_iters > 100000) { set_error(ER_EINVAL, "max_iters must be in [0, 100000]"); return ER_EINVAL; }
+    for (int64_t i = 0; i < 2 * k; i++) {
+        if (pairs[i] < 0 || pairs[i] >= g->n) {
+            set_error(ER_EINVAL, "node id out of range at pairs[" + std::to_string(i) + "]");
+            return ER_EINVAL;
+        }
+    }
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->query_block != ER_OK) { set_error(g->query_block, "graph is not connected or bipartite"); return g->query_block; }
+    if (!g->lambda_set) { set_error(ER_ESPECTRAL, "lambda not set"); return ER_ESPECTRAL; }
+    if (k == 0) return ER_OK;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != g->device) cudaSetDevice(g->device);
+    const int rc = run_smm_series(g, pairs, k, tol, max_iters, out_r, ells);
+    if (cur != g->device) cudaSetDevice(cur);
+    return rc;
 }
 
 int er_graph_estimate_lambda(er_graph *g, int iters, double *lambda_out)

@@ -134,6 +134,7 @@ struct er_graph {
     bool lambda_set = false;
     int nbits = 1;
     int walk_minb = 4;   // K6 resident CTAs per SM (launch bounds variant; GEER_WALK_MINB 3..4)
+    double overlap_frac = 0.75;  // overlap mode: fraction of K6 resident-CTA slots (GEER_OVERLAP_FRAC)
     bool amc_overlap = false;  // AMC per SMM wave on the AMC stream (GEER_AMC_OVERLAP=1) or one AMC after the head
     int walk_occ = 0;    // K6 resident CTAs per SM at the last launch (occupancy API)
     bool walk_persist = true;   // K6 persistent grid + atomic tile counter (GEER_WALK_PERSIST=1) or one tile per CTA
@@ -170,6 +171,8 @@ int cuda_fail(cudaError_t e, const char *what);
 int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, double p_fail,
                     const er_opts &o, double *out_r, er_query_stats *stats);
 int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st);
+int run_smm_series(er_graph *g, const int32_t *pairs, int64_t k, double tol, int32_t max_iters, double *out_r,
+                   int32_t *ells);
 int run_estimate_lambda(er_graph *g, int iters, double *lambda_out);
 cudaError_t build_arcs(er_graph *g);
 cudaError_t build_parcs(er_graph *g);

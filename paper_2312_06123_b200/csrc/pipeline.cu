@@ -1323,7 +1323,8 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
         /* persistent grid: exactly the resident CTAs (a second wave would serialise) */                    \
         const int64_t tiles = (bound + WALK_WARPS - 1) / WALK_WARPS;                                         \
         const unsigned grid = (unsigned)std::max<int64_t>(                                                  \
-            1, persist ? std::min<int64_t>((int64_t)std::max(occ, 1) * nsm, tiles) : tiles);                \
+            1, persist ? std::min<int64_t>((int64_t)std::max(1.0, slot_frac * std::max(occ, 1) * nsm), tiles)  \
+                       : tiles);                                                                            \
         g->walk_occ = occ;                                                                                  \
         k_walks<ARC, NP, MINB><<<grid, WALK_THREADS, smem_bytes, sb>>>(WALK_ARGS);                          \
     } while (0)
@@ -1334,9 +1335,10 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
         else WALK_LAUNCH(0, NP, MINB);                       \
     } while (0)
         const int32_t smem_words = g->walk_smem_words;
-        // persistent CTAs would hold every SM until the last tile: with the SMM head running
-        // concurrently (overlap) the hardware scheduler interleaves one-tile CTAs instead
-        const bool persist = g->walk_persist && !g->amc_overlap;
+        // with the SMM head running concurrently (overlap), the persistent walk grid takes only a
+        // fraction of the resident-CTA slots so head kernels always find room on every SM
+        const bool persist = g->walk_persist;
+        const double slot_frac = g->amc_overlap ? g->overlap_frac : 1.0;
         const size_t smem_bytes = sizeof(int32_t) * (size_t)smem_words;
         if (g->walk_np == 1) {
             if (g->walk_minb == 3) WALK_ARC(1, 3);

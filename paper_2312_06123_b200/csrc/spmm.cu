@@ -26,6 +26,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "geer_internal.h"
@@ -270,6 +271,103 @@ int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normali
     }
     CK(cudaGetLastError());
     return ER_OK;
+}
+
+}  // namespace geer
+
+// ============================================================================ SMM-to-ell series
+namespace geer {
+namespace {
+
+// X[:, c] = e_s/d_s - e_t/d_t for the block's queries (X zeroed before).
+__global__ void k_series_init(int32_t q, const int32_t *__restrict__ pairs, const int64_t *__restrict__ off,
+                              double *__restrict__ X)
+{
+    const int32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= q) return;
+    const int32_t s = pairs[2 * c], t = pairs[2 * c + 1];
+    if (s == t) return;
+    X[(int64_t)s * q + c] = 1.0 / (double)(off[s + 1] - off[s]);
+    X[(int64_t)t * q + c] = -1.0 / (double)(off[t + 1] - off[t]);
+}
+
+// acc[c] += y_i(s) - y_i(t) while i <= L_c (series term i of Thm 3.1's r_L).
+__global__ void k_series_acc(int32_t q, int32_t i, const int32_t *__restrict__ pairs, const int32_t *__restrict__ ell,
+                             const double *__restrict__ X, double *__restrict__ acc)
+{
+    const int32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= q || i > ell[c]) return;
+    const int32_t s = pairs[2 * c], t = pairs[2 * c + 1];
+    if (s == t) return;
+    acc[c] += X[(int64_t)s * q + c] - X[(int64_t)t * q + c];
+}
+
+}  // namespace
+
+int run_smm_series(er_graph *g, const int32_t *pairs, int64_t k, double tol, int32_t max_iters, double *out_r,
+                   int32_t *ells)
+{
+    const int64_t n = g->n;
+    const int32_t QB = 64;
+    cudaStream_t st = g->stream;
+    // L per query on the host: Eq. 6 with eps = tol; natural log (R2), clamp at 0 (R3)
+    std::vector<int32_t> L(k);
+    std::vector<int64_t> off_s(2), off_t(2);
+    const double lam = g->lambda;
+    for (int64_t i = 0; i < k; i++) {
+        const int32_t s = pairs[2 * i], t = pairs[2 * i + 1];
+        if (s == t) { L[i] = -1; continue; }
+        CK(cudaMemcpy(off_s.data(), g->d_off + s, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(off_t.data(), g->d_off + t, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        const double ds = (double)(off_s[1] - off_s[0]), dt = (double)(off_t[1] - off_t[0]);
+        const double x = std::log((2.0 / ds + 2.0 / dt) / (tol * (1.0 - lam))) / std::log(1.0 / lam) - 1.0;
+        double c = std::ceil(x);
+        if (c < 0.0) c = 0.0;
+        L[i] = (int32_t)std::min<double>(c, (double)max_iters);
+    }
+    double *X = nullptr, *Y = nullptr, *acc = nullptr;
+    int32_t *dp = nullptr, *dl = nullptr;
+    CK(cudaMalloc(&X, sizeof(double) * n * QB));
+    CK(cudaMalloc(&Y, sizeof(double) * n * QB));
+    CK(cudaMalloc(&acc, sizeof(double) * QB));
+    CK(cudaMalloc(&dp, sizeof(int32_t) * 2 * QB));
+    CK(cudaMalloc(&dl, sizeof(int32_t) * QB));
+    int rc = ER_OK;
+    for (int64_t b0 = 0; b0 < k && rc == ER_OK; b0 += QB) {
+        const int32_t q = (int32_t)std::min<int64_t>(QB, k - b0);
+        int32_t Lmax = -1;
+        for (int32_t c = 0; c < q; c++) Lmax = std::max(Lmax, L[b0 + c]);
+        cudaMemcpyAsync(dp, pairs + 2 * b0, sizeof(int32_t) * 2 * q, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(dl, L.data() + b0, sizeof(int32_t) * q, cudaMemcpyHostToDevice, st);
+        cudaMemsetAsync(X, 0, sizeof(double) * n * q, st);
+        cudaMemsetAsync(acc, 0, sizeof(double) * q, st);
+        k_series_init<<<1, QB, 0, st>>>(q, dp, g->d_off, X);
+        g->launches++;
+        double *cur = X, *nxt = Y;
+        for (int32_t i = 0; i <= Lmax; i++) {
+            k_series_acc<<<1, QB, 0, st>>>(q, i, dp, dl, cur, acc);
+            g->launches++;
+            if (i == Lmax) break;
+            rc = run_spmm(g, cur, nxt, q, 1, st);   // y_{i+1} = P y_i (K9)
+            if (rc) break;
+            std::swap(cur, nxt);
+        }
+        if (rc == ER_OK) {
+            cudaError_t e = cudaMemcpyAsync(out_r + b0, acc, sizeof(double) * q, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) rc = cuda_fail(e, "er_smm_series");
+        }
+    }
+    for (int64_t i = 0; i < k; i++) {
+        if (L[i] < 0) out_r[i] = 0.0;
+        if (ells) ells[i] = std::max(L[i], 0);
+    }
+    cudaFree(X);
+    cudaFree(Y);
+    cudaFree(acc);
+    cudaFree(dp);
+    cudaFree(dl);
+    return rc;
 }
 
 }  // namespace geer

@@ -428,3 +428,35 @@ def test_ytable_layouts_and_kernel_variants_byte_identical(graph, tiny, rmat20):
             assert np.abs(r1 - r0).max() <= 1e-12, k
         else:
             assert v == ref, k
+
+
+def test_smm_series_tiny_is_exact_er(geer, tiny, tiny_h):
+    """er_smm_series (K9 passes over the signed vector, SMM-to-ell) at tol = 1e-11 equals the
+    exact ER (dense pseudo-inverse, Def. 2.1) within the Thm 3.1 tail; L is Eq. 6's ell at
+    eps = tol; s = t gives 0."""
+    g, pairs = tiny
+    r, L = geer.er_smm_series(tiny_h, pairs, tol=1e-11)
+    ex = exact.er_pinv(g, pairs)
+    assert np.abs(r - ex).max() <= 2e-11
+    d = g.degrees()
+    want_L = [oracle.refined_ell(int(d[s]), int(d[t]), 1e-11, g.lam) for s, t in pairs]
+    assert np.array_equal(L, want_L)
+    r2, _ = geer.er_smm_series(tiny_h, [[5, 5], [0, 1]], tol=1e-11)
+    assert r2[0] == 0.0 and abs(r2[1] - exact.er_pinv(g, np.array([[0, 1]]))[0]) <= 2e-11
+
+
+def test_smm_series_rmat20_vs_oracle_and_geer_accuracy(geer, rmat20):
+    """At BASELINE config 1's size: (1) er_smm_series equals the oracle's signed-vector series
+    (same L) within 1e-10 relative on sampled queries; (2) the paper's accuracy protocol:
+    GEER's eps = 0.1 estimates are within eps of the converged series (tol 1e-8) on 100 random
+    pairs + 100 edges (each holds with probability >= 1 - delta, delta = 0.01)."""
+    g, pairs, _, h = rmat20
+    sub = np.concatenate([pairs[:100], pairs[5000:5100]])
+    truth, L = geer.er_smm_series(h, sub, tol=1e-8)
+    for j in (0, 7, 100, 150):
+        s, t = (int(x) for x in sub[j])
+        ref = oracle.series_signed(g, s, t, int(L[j]))
+        assert abs(truth[j] - ref) <= 1e-10 * max(1.0, abs(ref)), j
+    est, _ = geer.er_query_batch_ex(h, sub, 0.1)
+    err = np.abs(est - truth)
+    assert np.mean(err <= 0.1) >= 0.99 and err.max() <= 0.2, err.max()

@@ -144,3 +144,21 @@ def test_spectral_identity_eq17():
         Pi = np.linalg.matrix_power(P, i)
         recon = (F * w ** i) @ F.T * pi[None, :]
         assert np.allclose(Pi, recon, atol=1e-8)
+
+
+def test_series_signed_matches_matrix_powers_and_converges():
+    """oracle.series_signed (sparse pull, signed vector) equals Eq. 4 by dense matrix powers
+    (exact.r_ell) and converges to the exact ER (Thm 3.1) on small non-bipartite graphs."""
+    import oracle
+    import workloads as W
+    for g, pairs in ((W.random_small(2, 40, 0.12), [(0, 5), (3, 17), (9, 9)]), (W.lollipop(6), [(0, 8), (1, 4)]),
+                     (W.petersen(), [(0, 7)])):
+        for s, t in pairs:
+            for L in (0, 1, 4, 9):
+                assert abs(oracle.series_signed(g, s, t, L) - exact.r_ell(g, s, t, L)) <= 1e-12
+            if s != t:
+                # Thm 3.1: with L = Eq. 6's ell at eps = 1e-10 the tail is <= 1e-10
+                lam = exact.lambda_dense(g)
+                L = oracle.refined_ell(int(g.degrees()[s]), int(g.degrees()[t]), 1e-10, lam)
+                r = exact.er_pinv(g, np.array([[s, t]]))[0]
+                assert abs(oracle.series_signed(g, s, t, L) - r) <= 1e-10 + 1e-12 * r
