@@ -146,42 +146,53 @@ __global__ void k_emit(int64_t E, int64_t F, const int64_t *__restrict__ ent_off
                        const int64_t *__restrict__ off, const int32_t *__restrict__ cols, KeyT *__restrict__ keys,
                        double *__restrict__ vals)
 {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= E) return;
-    int64_t lo = 0, hi = F;  // ent_off[lo] <= p < ent_off[hi]
+    // thread = EMIT_PER consecutive output positions: one binary search, then a linear advance
+    constexpr int EMIT_PER = 4;
+    const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * EMIT_PER;
+    if (p0 >= E) return;
+    int64_t lo = 0, hi = F;  // ent_off[lo] <= p0 < ent_off[hi]
     while (hi - lo > 1) {
         const int64_t mid = (lo + hi) >> 1;
-        if (ent_off[mid] <= p) lo = mid;
+        if (ent_off[mid] <= p0) lo = mid;
         else hi = mid;
     }
-    const int32_t v = id[lo];
-    const uint32_t u = (uint32_t)cols[off[v] + (p - ent_off[lo])];
-    keys[p] = ((KeyT)(seg[lo] % spc) << nbits) | (KeyT)u;
-    vals[p] = val[lo];
+    int64_t e = lo, next = ent_off[e + 1];
+    int32_t v = id[e];
+    KeyT sk = (KeyT)(seg[e] % spc) << nbits;
+    const int64_t p1 = p0 + EMIT_PER < E ? p0 + EMIT_PER : E;
+    for (int64_t p = p0; p < p1; p++) {
+        while (p >= next) {   // every frontier node has degree >= 1 (connected graph)
+            e++;
+            next = ent_off[e + 1];
+            v = id[e];
+            sk = (KeyT)(seg[e] % spc) << nbits;
+        }
+        keys[p] = sk | (KeyT)(uint32_t)cols[off[v] + (p - ent_off[e])];
+        vals[p] = val[e];
+    }
 }
 
-// Run heads of the (per-segment) sorted keys: a key change or a segment start.
+// Run head flag of sorted position p: a key change.  The keys carry the (chunk-local) segment id
+// above the node bits and consecutive segments differ in it, so a segment start is always a
+// key change.
 template <class KeyT>
-__global__ void k_heads(int64_t E, const KeyT *__restrict__ keys, int32_t *__restrict__ head)
-{
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= E) return;
-    head[p] = (p == 0 || keys[p] != keys[p - 1]) ? 1 : 0;
-}
+struct HeadFlag {
+    const KeyT *keys;
+    __host__ __device__ __forceinline__ int32_t operator()(const int32_t &p) const
+    {
+        return (p == 0 || keys[p] != keys[p - 1]) ? 1 : 0;
+    }
+};
 
-__global__ void k_mark_segbeg(int32_t nseg, const int32_t *__restrict__ segbeg, int32_t *__restrict__ head)
-{
-    const int32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g < nseg && segbeg[g] < segbeg[g + 1]) head[segbeg[g]] = 1;
-}
-
-// runidx = inclusive scan of heads; runstart[r] = first position of run r; runstart[U] = E.
-__global__ void k_runstart(int64_t E, const int32_t *__restrict__ head, const int64_t *__restrict__ runincl,
+// runincl = inclusive scan of the head flags; runstart[r] = first position of run r;
+// runstart[U] = E; *dU = U.
+template <class KeyT>
+__global__ void k_runstart(int64_t E, const KeyT *__restrict__ keys, const int32_t *__restrict__ runincl,
                            int64_t *__restrict__ runstart, int64_t *__restrict__ dU)
 {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= E) return;
-    if (head[p]) runstart[runincl[p] - 1] = p;
+    if (p == 0 || keys[p] != keys[p - 1]) runstart[runincl[p] - 1] = p;
     if (p == E - 1) {
         runstart[runincl[p]] = E;
         *dU = runincl[p];
@@ -214,7 +225,7 @@ __device__ __forceinline__ bool warp_seg_head(int32_t g)
 // max1 (max of non-negative doubles as uint64 bit patterns), x(s), x(t) (single writers).
 template <class KeyT>
 __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const int64_t *__restrict__ runstart,
-                             const KeyT *__restrict__ keys, int nbits, const double *__restrict__ vals,
+                             const KeyT *__restrict__ keys, int nbits, int one_chunk, const double *__restrict__ vals,
                              const int32_t *__restrict__ segbeg, int32_t nseg, const int64_t *__restrict__ off,
                              const int32_t *__restrict__ act, const QState *__restrict__ qs,
                              int32_t *__restrict__ nid, double *__restrict__ nval, int32_t *__restrict__ nseg_out,
@@ -226,16 +237,21 @@ __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const
     unsigned long long deg = 0, bits = 0;
     if (live) {
         const int64_t p0 = runstart[r], p1 = runstart[r + 1];
-        const int32_t u = (int32_t)(keys[p0] & (((KeyT)1 << nbits) - 1));
-        int32_t lo = 0, hi = nseg;  // segbeg[lo] <= p0 < segbeg[hi]
-        while (hi - lo > 1) {
-            const int32_t mid = (lo + hi) >> 1;
-            if (segbeg[mid] <= p0) lo = mid;
-            else hi = mid;
+        const KeyT k0 = keys[p0];
+        const int32_t u = (int32_t)(k0 & (((KeyT)1 << nbits) - 1));
+        if (one_chunk) {
+            g = (int32_t)(k0 >> nbits);   // all segments in one sort chunk: the key holds g
+        } else {
+            int32_t lo = 0, hi = nseg;  // segbeg[lo] <= p0 < segbeg[hi]
+            while (hi - lo > 1) {
+                const int32_t mid = (lo + hi) >> 1;
+                if (segbeg[mid] <= p0) lo = mid;
+                else hi = mid;
+            }
+            g = lo;
         }
-        g = lo;
         double sum = 0.0;
-        for (int64_t p = p0; p < p1; p++) sum += vals[p];
+        for (int64_t p = p0; p < p1; p++) sum += vals[p];   // ascending source order (R13)
         const int64_t d = off[u + 1] - off[u];
         const double x = sum / (double)d;
         nid[r] = u;
@@ -451,12 +467,10 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int
     }
 }
 
-__global__ void k_yfill(int64_t H, int32_t *__restrict__ keys, int64_t V, double *__restrict__ vals, int64_t R,
-                        uint4 *__restrict__ recs)
+__global__ void k_yfill(int64_t H, int32_t *__restrict__ keys, int64_t R, uint4 *__restrict__ recs)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j < H) keys[j] = -1;
-    if (j < V) vals[j] = 0.0;
     if (j < R) recs[j] = make_uint4(0u, 0u, 0u, 0u);
 }
 
@@ -489,19 +503,32 @@ __device__ __forceinline__ int64_t hash_insert(int32_t *keys, int lgb, int32_t v
     }
 }
 
-// K5 passes over the support entries (frontier entry e: node id[e], value val[e], segment
-// seg[e] = 2 i + side) of the leaving queries:
-//   pass 0: hash: side 0 find-or-insert, vals[slot] = s*(v)/d(s);  rank: set bit v (both sides)
-//   (k_yrank between passes 0 and 1)
-//   pass 1: hash: side 1 find-or-insert, vals[slot] -= t*(v)/d(t); rank: side 0 vals[idx] = s*(v)/d(s)
-//   pass 2: rank: side 1 vals[idx] -= t*(v)/d(t)
-// so every entry ends with y(v) = s*(v)/d(s) - t*(v)/d(t), a side the node is not on
-// contributing 0.0 (values start at 0.0).  A node occurs once per side: one writer per value
-// in every pass.
+// Position of node v in the sorted id range [lo, hi), or -1.
+__device__ __forceinline__ int64_t find_sorted(const int32_t *__restrict__ id, int64_t lo, int64_t hi, int32_t v)
+{
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const int32_t x = id[mid];
+        if (x == v) return mid;
+        if (x < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return -1;
+}
+
+// K5 over the support entries (frontier entry e: node id[e], value val[e], segment seg[e] =
+// 2 i + side; each segment sorted by node id) of the leaving queries.  Every node v of
+// U = supp(s*) u supp(t*) has one OWNER entry (its side-0 entry, else its side-1 entry), which
+// finds v's entry on the other side by binary search and writes
+//     y(v) = s*(v)/d(s) - t*(v)/d(t)          (a side v is not on contributes 0.0 / d = 0.0)
+// exactly once (Alg. 1 L7 with s = s*, t = t*).
+//   pass 0: hash: owners insert v (CAS on the key slot) and write y;  rank: every entry sets bit v
+//   (k_yrank between the passes)
+//   pass 1: rank: owners write y at rank + popc(bits below v)
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                           const int32_t *__restrict__ id, const double *__restrict__ val,
-                          const int32_t *__restrict__ act, const int64_t *__restrict__ vslots,
-                          const QState *__restrict__ qs, int pass)
+                          const int64_t *__restrict__ segoff, const int32_t *__restrict__ act,
+                          const int64_t *__restrict__ vslots, const QState *__restrict__ qs, int pass)
 {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
@@ -511,23 +538,20 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
     const int side = g & 1;
     const QState &Q = qs[act[i]];
     const int32_t v = id[e];
+    if (Q.ymode == YT_RANK && pass == 0) {
+        atomicOr(reinterpret_cast<unsigned long long *>(const_cast<uint4 *>(Q.yrec) + (v >> 6)), 1ull << (v & 63));
+        return;
+    }
+    if ((Q.ymode == YT_HASH) != (pass == 0)) return;
+    // owner test and the other side's value
+    const int64_t other = find_sorted(id, segoff[g ^ 1], segoff[(g ^ 1) + 1], v);
+    if (side == 1 && other >= 0) return;   // the side-0 entry owns v
+    const double xs = side == 0 ? val[e] : 0.0;
+    const double xt = side == 1 ? val[e] : (other >= 0 ? val[other] : 0.0);
+    const double y = xs / (double)Q.ds - xt / (double)Q.dt;
     double *vals = const_cast<double *>(Q.yvals);
-    if (Q.ymode == YT_HASH) {
-        if (pass != side) return;
-        const int64_t slot = hash_insert(const_cast<int32_t *>(Q.ykeys), Q.ylog2 - YB_LOG, v);
-        if (side) vals[slot] = vals[slot] - val[e] / (double)Q.dt;
-        else vals[slot] = val[e] / (double)Q.ds;
-        return;
-    }
-    uint4 *recs = const_cast<uint4 *>(Q.yrec);
-    if (pass == 0) {
-        atomicOr(reinterpret_cast<unsigned long long *>(recs + (v >> 6)), 1ull << (v & 63));
-        return;
-    }
-    if (pass != side + 1) return;
-    const int64_t idx = rank_index(recs[v >> 6], v);
-    if (side) vals[idx] = vals[idx] - val[e] / (double)Q.dt;
-    else vals[idx] = val[e] / (double)Q.ds;
+    if (Q.ymode == YT_HASH) vals[hash_insert(const_cast<int32_t *>(Q.ykeys), Q.ylog2 - YB_LOG, v)] = y;
+    else vals[rank_index(Q.yrec[v >> 6], v)] = y;
 }
 
 // Ranks of the rank-bitmap tables: rank(record w) = popcount of all records before w.  One CTA
@@ -1191,8 +1215,8 @@ int ytable_plan(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, con
 }
 
 // Phase 2: allocate and fill the tables planned by ytable_plan (totals H, V, R read by the caller).
-int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int32_t *id, const double *val, const int32_t *seg,
-                 int64_t Fmax, const int64_t *dF, int wave, int64_t H, int64_t V, int64_t R)
+int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, const int32_t *id, const double *val,
+                 const int32_t *seg, int64_t Fmax, const int64_t *dF, int wave, int64_t H, int64_t V, int64_t R)
 {
     Workspace &ws = c.ws;
     int64_t *hs = ws.ycap.as<int64_t>(), *vs = hs + (na + 1), *rs = vs + (na + 1);
@@ -1212,18 +1236,19 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int32_t *id, cons
     double *vals = yb.as<double>();
     uint4 *recs = reinterpret_cast<uint4 *>(yb.as<char>() + o_rec);
     int32_t *keys = reinterpret_cast<int32_t *>(yb.as<char>() + o_key);   // buckets need 32-byte alignment
-    k_yfill<<<blocks_for(std::max(std::max(H, V), R), 256), 256, 0, c.st>>>(H, keys, V, vals, R, recs);
+    k_yfill<<<blocks_for(std::max(H, R), 256), 256, 0, c.st>>>(H, keys, R, recs);
     LAUNCHED(c.g);
     k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, hs, hi, vs, vi, rs, ri, keys, vals, recs,
                                                       ws.qs.as<QState>());
     LAUNCHED(c.g);
-    for (int pass = 0; pass < 3; pass++) {
-        if (pass == 1 && R > 0) {
+    for (int pass = 0; pass < 2; pass++) {
+        if (pass == 1) {
+            if (R == 0) break;
             k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, act, rs, ws.qs.as<QState>());
             LAUNCHED(c.g);
         }
-        if (pass == 2 && R == 0) break;
-        k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, act, vs, ws.qs.as<QState>(), pass);
+        k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, segoff, act, vs, ws.qs.as<QState>(),
+                                                          pass);
         LAUNCHED(c.g);
     }
     return ER_OK;
@@ -1238,7 +1263,7 @@ int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, c
     if (!rc) rc = read_scalars(c, {th, tv, tr});
     if (rc) return rc;
     const int64_t H = c.hp[0], V = c.hp[1], R = c.hp[2];
-    return ytable_build(c, na, act, id, val, seg, Fmax, dF, wave, H, V, R);
+    return ytable_build(c, na, act, segoff, id, val, seg, Fmax, dF, wave, H, V, R);
 }
 
 // One AMC group: the queries that left the SMM head in the same wave, with their y-tables.
@@ -1370,7 +1395,7 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
 // significant key bits; the result is in ws.keys2 / ws.vals2.
 template <class KeyT>
 int smm_group(Ctx &c, int64_t E, int64_t F, int32_t nseg, const int64_t *ent_off, const int32_t *segbeg, int nbits,
-              int64_t *dU)
+              int64_t *dU, int *one_chunk)
 {
     Workspace &ws = c.ws;
     er_graph *g = c.g;
@@ -1386,11 +1411,13 @@ int smm_group(Ctx &c, int64_t E, int64_t F, int32_t nseg, const int64_t *ent_off
     ENSURE(ws.vals2, sizeof(double) * E, false);
     KeyT *k1 = ws.keys.as<KeyT>(), *k2 = ws.keys2.as<KeyT>();
     double *v1 = ws.vals.as<double>(), *v2 = ws.vals2.as<double>();
-    k_emit<KeyT><<<blocks_for(E, 256), 256, 0, st>>>(E, F, ent_off, ws.fr_id.as<int32_t>(), ws.fr_val.as<double>(),
-                                                     ws.fr_seg.as<int32_t>(), spc, nbits, g->d_off, g->d_cols, k1, v1);
+    k_emit<KeyT><<<blocks_for((E + 3) / 4, 256), 256, 0, st>>>(E, F, ent_off, ws.fr_id.as<int32_t>(),
+                                                                 ws.fr_val.as<double>(), ws.fr_seg.as<int32_t>(), spc,
+                                                                 nbits, g->d_off, g->d_cols, k1, v1);
     LAUNCHED(g);
     // chunk boundaries in emission order (segbeg on the host: nseg+1 int32)
     const int32_t nchunks = (int32_t)((nseg + spc - 1) / spc);
+    *one_chunk = nchunks == 1 ? 1 : 0;
     std::vector<int32_t> hb(nchunks + 1);
     if (nchunks == 1) {
         hb[0] = 0;                 // one chunk: all E pairs (no host read)
@@ -1414,18 +1441,16 @@ int smm_group(Ctx &c, int64_t E, int64_t F, int32_t nseg, const int64_t *ent_off
         });
         if (rc) return rc;
     }
-    ENSURE(ws.runidx, sizeof(int64_t) * E, false);
+    ENSURE(ws.runidx, sizeof(int32_t) * E, false);
     ENSURE(ws.runstart, sizeof(int64_t) * (E + 1), false);
-    k_heads<KeyT><<<blocks_for(E, 256), 256, 0, st>>>(E, k2, ws.head.as<int32_t>());
-    LAUNCHED(g);
-    k_mark_segbeg<<<blocks_for(nseg, 256), 256, 0, st>>>(nseg, segbeg, ws.head.as<int32_t>());
-    LAUNCHED(g);
+    // run ids: scan of head flags computed on the fly from the sorted keys (no flag array)
+    cub::TransformInputIterator<int32_t, HeadFlag<KeyT>, cub::CountingInputIterator<int32_t>> heads(
+        cub::CountingInputIterator<int32_t>(0), HeadFlag<KeyT>{k2});
     int rc = cub_call(c, [&](void *tmp, size_t &bytes) {
-        return cub::DeviceScan::InclusiveSum(tmp, bytes, ws.head.as<int32_t>(), ws.runidx.as<int64_t>(), E, st);
+        return cub::DeviceScan::InclusiveSum(tmp, bytes, heads, ws.runidx.as<int32_t>(), (int)E, st);
     });
     if (rc) return rc;
-    k_runstart<<<blocks_for(E, 256), 256, 0, st>>>(E, ws.head.as<int32_t>(), ws.runidx.as<int64_t>(),
-                                                   ws.runstart.as<int64_t>(), dU);
+    k_runstart<KeyT><<<blocks_for(E, 256), 256, 0, st>>>(E, k2, ws.runidx.as<int32_t>(), ws.runstart.as<int64_t>(), dU);
     LAUNCHED(g);
     return ER_OK;
 }
@@ -1631,14 +1656,15 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             int64_t *dU = ws.scalars.as<int64_t>();
             const bool fast_first = first_wave && g->rows_sorted;
             int32_t *segbeg = nullptr;
+            int one_chunk = 0;
             if (!fast_first) {
                 ENSURE(ws.segbeg, sizeof(int32_t) * (nseg + 1), false);
                 segbeg = ws.segbeg.as<int32_t>();
                 k_segbeg<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, ws.fr_off.as<int64_t>(), ent_off, segbeg);
                 LAUNCHED(g);
                 ENSURE(ws.head, sizeof(int32_t) * E, false);
-                if (P.nbits <= 24) rc = smm_group<uint32_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU);
-                else rc = smm_group<uint64_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU);
+                if (P.nbits <= 24) rc = smm_group<uint32_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU, &one_chunk);
+                else rc = smm_group<uint64_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU, &one_chunk);
                 if (rc) return rc;
             }
             ENSURE(ws.nf_id, sizeof(int32_t) * E, false);
@@ -1655,12 +1681,12 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             } else
             if (P.nbits <= 24)
                 k_run_reduce<uint32_t><<<blocks_for(E, 256), 256, 0, st>>>(
-                    E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint32_t>(), P.nbits, ws.vals2.as<double>(), segbeg,
+                    E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint32_t>(), P.nbits, one_chunk, ws.vals2.as<double>(), segbeg,
                     nseg, g->d_off, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                     ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>());
             else
                 k_run_reduce<uint64_t><<<blocks_for(E, 256), 256, 0, st>>>(
-                    E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint64_t>(), P.nbits, ws.vals2.as<double>(), segbeg,
+                    E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint64_t>(), P.nbits, one_chunk, ws.vals2.as<double>(), segbeg,
                     nseg, g->d_off, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                     ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>());
             LAUNCHED(g);
@@ -1699,8 +1725,8 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             const int64_t F2 = c.hp[1];
             const int64_t YH = c.hp[2], YV = c.hp[3], YR = c.hp[4];
             // y-tables, then (overlap) their AMC on the AMC stream
-            rc = ytable_build(c, (int32_t)na, ws.act.as<int32_t>(), ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
-                              ws.nf_seg.as<int32_t>(), E, dU, 1 + wave_no, YH, YV, YR);
+            rc = ytable_build(c, (int32_t)na, ws.act.as<int32_t>(), ws.nf_off.as<int64_t>(), ws.nf_id.as<int32_t>(),
+                              ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), E, dU, 1 + wave_no, YH, YV, YR);
             if (rc) return rc;
             rc = fork_group((int32_t)na, ws.act.as<int32_t>(), cont);
             if (rc) return rc;
