@@ -130,6 +130,12 @@ typedef struct er_opts {
                                   [0, 2^32).  The global index keys the query's RNG streams (R10),
                                   so a query's result does not depend on which rank or batch runs
                                   it (cost-model sharding, paper_2312_06123_b200/dist.py) */
+    double switch_ratio;       /* variant: leave the SMM head iff vol > switch_ratio * h;
+                                  1.0 (default) is Eq. 15; any value keeps the eps guarantee */
+    int32_t reuse_samples;     /* variant: 1 = batch b keeps the previous batches'
+                                  samples and draws only the new ones (one sample stream per query, batch
+                                  key 0); 0 (default) = fresh samples per batch (R8) */
+    int32_t pad1;
 } er_opts;
 
 #define ER_DEFAULT_SEED 0x2312061232DEC0DEULL

@@ -41,7 +41,7 @@ STATS_DTYPE = np.dtype([
 class _Opts(ctypes.Structure):
     _fields_ = [("tau", ctypes.c_int), ("seed", ctypes.c_uint64),
                 ("query_index_base", ctypes.c_int64), ("force_ell_b", ctypes.c_int),
-                ("ell_variant", ctypes.c_int)]
+                ("ell_variant", ctypes.c_int), ("switch_ratio", ctypes.c_double), ("reuse_samples", ctypes.c_int)]
 
 
 DEFAULT_SEED = 0x2312061232DEC0DE  # same documented default as the library (R10)
@@ -221,14 +221,15 @@ def amc_samples(g, s, t, xs, xt, lf, count, seed=DEFAULT_SEED, q=0, b=0) -> np.n
 
 # ---------------------------------------------------------------- GEER batch
 def geer_batch(g, lam, pairs, eps, delta=0.01, tau=5, seed=DEFAULT_SEED, query_index_base=0,
-               force_ell_b=-1, ell_variant=0, nthreads=0, with_stats=True):
+               force_ell_b=-1, ell_variant=0, nthreads=0, with_stats=True, switch_ratio=1.0, reuse_samples=0):
     """Alg. 3 (GEER) per query; returns (r, stats) with stats a STATS_DTYPE array."""
     off, cols = _csr(g)
     pairs = np.ascontiguousarray(np.asarray(pairs, dtype=np.int32).reshape(-1, 2))
     k = pairs.shape[0]
     out = np.zeros(k, dtype=np.float64)
     st = np.zeros(k, dtype=STATS_DTYPE) if with_stats else None
-    o = _Opts(tau, seed & 0xFFFFFFFFFFFFFFFF, query_index_base, force_ell_b, ell_variant)
+    o = _Opts(tau, seed & 0xFFFFFFFFFFFFFFFF, query_index_base, force_ell_b, ell_variant, float(switch_ratio),
+              int(reuse_samples))
     rc = lib().oracle_geer_batch(g.n, _p(off), _p(cols), lam, _p(pairs), k, eps, delta,
                                  ctypes.byref(o), nthreads, _p(out), None if st is None else _p(st))
     if rc != 0:

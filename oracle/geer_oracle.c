@@ -243,6 +243,8 @@ typedef struct {
     int64_t query_index_base;
     int force_ell_b;   /* -1: Eq.15 decides ell_b; >=0: run exactly min(force, ell) SMM iterations */
     int ell_variant;   /* 0: Eq.6 (refined), 1: Eq.5 (Peng) */
+    double switch_ratio;  /* SURVEY 8(f)#4 variant: stop the SMM head iff vol > switch_ratio * h (1.0 = Eq.15) */
+    int reuse_samples;    /* SURVEY 8(f)#4 variant: batch b keeps batch b-1's eta samples and adds eta new ones */
 } oracle_opts_t;
 
 /*
@@ -391,7 +393,8 @@ static double geer_one(int64_t n, const int64_t *off, const int32_t *cols, doubl
         int64_t h = oracle_h(eta0, tau);
         st->vol_last = vol;
         st->h_last = h;
-        if (o->force_ell_b < 0 && vol > h) break;
+        if (o->force_ell_b < 0 && (o->switch_ratio == 1.0 ? vol > h : (double)vol > o->switch_ratio * (double)h))
+            break;
     }
     st->ell_b = (int32_t)ell_b;
     st->r_b = r_b;
@@ -410,25 +413,36 @@ static double geer_one(int64_t n, const int64_t *off, const int32_t *cols, doubl
         const double dprime = delta / (double)tau;   /* f(., ., psi, delta/tau), Alg.1 L13 */
         int64_t eta = eta0;
         uint64_t ck = 0;
+        double S1 = 0.0, S2 = 0.0;
+        int64_t k_new = 0;                            /* reuse variant: walks drawn so far */
         for (int b = 0; b < tau; b++) {
-            double S1 = 0.0, S2 = 0.0;                /* Alg.1 L4: Z <- 0, sigma^2 <- 0 (fresh batch, R8) */
-            for (int64_t k = 0; k < eta; k++) {
+            int64_t k_lo = 0;
+            uint32_t bkey = (uint32_t)b;
+            if (o->reuse_samples) {
+                k_lo = k_new;                         /* keep samples 0..k_new-1, draw k_new..eta-1 */
+                bkey = 0;                             /* a sample's stream does not depend on the batch */
+            } else {
+                S1 = 0.0;                             /* Alg.1 L4: Z <- 0, sigma^2 <- 0 (fresh batch, R8) */
+                S2 = 0.0;
+            }
+            for (int64_t k = k_lo; k < eta; k++) {
                 double aS, aT;
-                int32_t eS = walk(off, cols, y, s, lf, o->seed, q, (uint32_t)b, 0, (uint64_t)k, &aS, NULL);
-                int32_t eT = walk(off, cols, y, t, lf, o->seed, q, (uint32_t)b, 1, (uint64_t)k, &aT, NULL);
+                int32_t eS = walk(off, cols, y, s, lf, o->seed, q, bkey, 0, (uint64_t)k, &aS, NULL);
+                int32_t eT = walk(off, cols, y, t, lf, o->seed, q, bkey, 1, (uint64_t)k, &aT, NULL);
                 double Zk = aS - aT;                  /* Alg.1 L7 */
                 S1 += Zk;                             /* L8 */
                 S2 += Zk * Zk;                        /* L9 */
-                ck += oracle_walk_hash(q, (uint32_t)b, 0, (uint64_t)k, eS);
-                ck += oracle_walk_hash(q, (uint32_t)b, 1, (uint64_t)k, eT);
+                ck += oracle_walk_hash(q, bkey, 0, (uint64_t)k, eS);
+                ck += oracle_walk_hash(q, bkey, 1, (uint64_t)k, eT);
             }
             double Z = S1 / (double)eta;              /* L11 */
             double var = S2 / (double)eta - Z * Z;    /* L12 (one-pass form, R7) */
             if (var < 0.0) var = 0.0;
             double f = oracle_bernstein_f((double)eta, var, psi, dprime);
             st->batches_run = b + 1;
-            st->walks_total += eta;
-            st->steps_total += 2 * eta * lf;
+            st->walks_total += eta - k_lo;
+            st->steps_total += 2 * (eta - k_lo) * lf;
+            k_new = eta;
             st->f_last = f;
             st->sigma2_last = var;
             r_f = Z;

@@ -48,7 +48,8 @@ class er_opts(ctypes.Structure):
                 ("query_index_base", ctypes.c_int64), ("cuda_stream", ctypes.c_void_p),
                 ("pairs_on_device", ctypes.c_int32), ("out_on_device", ctypes.c_int32),
                 ("ell_variant", ctypes.c_int32), ("synchronous", ctypes.c_int32), ("pad0", ctypes.c_int32),
-                ("query_ids", ctypes.c_void_p)]
+                ("query_ids", ctypes.c_void_p), ("switch_ratio", ctypes.c_double), ("reuse_samples", ctypes.c_int32),
+                ("pad1", ctypes.c_int32)]
 
 
 class er_profile(ctypes.Structure):
@@ -188,7 +189,7 @@ def er_query_batch(g, pairs, eps: float, p_fail: float = 0.01):
 def er_query_batch_ex(g, pairs, eps: float, p_fail: float = 0.01, *, out=None, stats=None,
                       tau: int = 5, seed: int = ER_DEFAULT_SEED, query_index_base: int = 0,
                       force_ell_b: int = -1, ell_variant: int = 0, stream=None, synchronous: bool = True,
-                      k: int | None = None, query_ids=None):
+                      k: int | None = None, query_ids=None, switch_ratio: float = 1.0, reuse_samples: bool = False):
     """Extended query.  ``pairs``/``out``/``stats`` are numpy arrays (host) or torch CUDA
     tensors (device); ``out``/``stats`` are allocated on the host when None.
     ``stats=True`` allocates a host STATS_DTYPE array.  Returns (out, stats)."""
@@ -220,6 +221,8 @@ def er_query_batch_ex(g, pairs, eps: float, p_fail: float = 0.01, *, out=None, s
     o.out_on_device = int(odev)
     o.ell_variant = ell_variant
     o.synchronous = int(synchronous)
+    o.switch_ratio = float(switch_ratio)
+    o.reuse_samples = int(bool(reuse_samples))
     if query_ids is not None:
         if hasattr(query_ids, "data_ptr"):
             if bool(query_ids.is_cuda) != bool(pdev):

@@ -177,6 +177,8 @@ void er_opts_default(er_opts *o)
     o->ell_variant = 0;
     o->synchronous = 1;
     o->query_ids = nullptr;
+    o->switch_ratio = 1.0;
+    o->reuse_samples = 0;
 }
 
 er_graph *er_graph_create(int64_t n, const int64_t *offsets, const int32_t *cols)
@@ -380,6 +382,8 @@ int er_query_batch_ex(er_graph *g, const int32_t *pairs, int64_t k, double eps, 
     if (opt.tau < 1 || opt.tau > 8) { set_error(ER_EINVAL, "tau must be in [1,8]"); return ER_EINVAL; }
     if (opt.ell_variant != 0 && opt.ell_variant != 1) { set_error(ER_EINVAL, "ell_variant must be 0 or 1"); return ER_EINVAL; }
     if (opt.force_ell_b < -1) { set_error(ER_EINVAL, "force_ell_b must be >= -1"); return ER_EINVAL; }
+    if (!(opt.switch_ratio >= 0.0) || !std::isfinite(opt.switch_ratio)) { set_error(ER_EINVAL, "switch_ratio must be >= 0"); return ER_EINVAL; }
+    if (opt.reuse_samples != 0 && opt.reuse_samples != 1) { set_error(ER_EINVAL, "reuse_samples must be 0 or 1"); return ER_EINVAL; }
     if (opt.query_index_base < 0 || opt.query_index_base + k > ((int64_t)1 << 32)) {
         set_error(ER_EINVAL, "query indices must fit in 32 bits");
         return ER_EINVAL;

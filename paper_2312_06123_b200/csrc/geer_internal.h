@@ -34,6 +34,7 @@ struct QState {
     const uint4 *yrec;     // rank records {bits lo, bits hi, rank, 0} per 64 node ids (YT_RANK)
     const double *yvals;   // values (by slot, or by rank)
     double z;              // last batch mean Z (= r_f)
+    double s1acc, s2acc;   // running sums of Z_k, Z_k^2 (reuse variant)
 };
 
 
@@ -79,6 +80,8 @@ struct BatchParams {
     int32_t tau;
     int32_t force_ell_b;
     int32_t ell_variant;
+    int32_t reuse;          // variant: keep samples across batches
+    double switch_ratio;    // variant: Eq. 15 threshold multiplier
     int32_t nbits;          // bits of a node id (sort keys)
     uint64_t seed;
     int64_t qbase;          // global index of query 0

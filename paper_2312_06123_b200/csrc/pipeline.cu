@@ -384,7 +384,8 @@ __global__ void k_decide(int32_t na, const int32_t *__restrict__ act, const SegS
     Q.st.vol_last = vol;
     Q.st.h_last = h;
     const int64_t maxit = P.force_ell_b >= 0 ? (P.force_ell_b < ell ? P.force_ell_b : ell) : ell;
-    const bool go = ell_b < maxit && !(P.force_ell_b < 0 && vol > h);
+    const bool over = P.switch_ratio == 1.0 ? vol > h : (double)vol > P.switch_ratio * (double)h;   // Eq. 15
+    const bool go = ell_b < maxit && !(P.force_ell_b < 0 && over);
     cont[i] = go ? 1 : 0;
     if (!go) {
         const int64_t lf = ell - ell_b;
@@ -629,13 +630,18 @@ __global__ void k_compact_lists(int32_t na, const int32_t *__restrict__ cont, co
 
 // Walk pairs of batch b per AMC query, and the AMC sort key (descending ell_f) used to order
 // the flattened walk space so warps mostly see one trip count.
+// First walk index and number of walks drawn in batch b: all eta_b = eta0 2^b fresh (R8), or, with
+// sample reuse, only the eta_b - eta_{b-1} new ones k in [eta_{b-1}, eta_b).
+__device__ __forceinline__ int64_t walks_lo(int64_t eta0, int b, int reuse) { return reuse && b > 0 ? eta0 << (b - 1) : 0; }
+
 __global__ void k_nchunks(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs, int b,
-                          int32_t per_chunk, int64_t *__restrict__ nch)
+                          int reuse, int32_t per_chunk, int64_t *__restrict__ nch)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
     const QState &Q = qs[amc[i]];
-    nch[i] = Q.phase == PH_AMC ? ((Q.st.eta0 << b) + per_chunk - 1) / per_chunk : 0;
+    const int64_t cnt = (Q.st.eta0 << b) - walks_lo(Q.st.eta0, b, reuse);
+    nch[i] = Q.phase == PH_AMC ? (cnt + per_chunk - 1) / per_chunk : 0;
 }
 
 __global__ void k_lf_key(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs,
@@ -849,7 +855,7 @@ __global__ void __launch_bounds__(WALK_THREADS, MINB)
 k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
         const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
         const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
-        uint32_t key0, uint32_t key1, int32_t smem_words, int y_evict_first,
+        uint32_t key0, uint32_t key1, int32_t smem_words, int y_evict_first, int reuse,
         unsigned long long *__restrict__ tile_ctr, TilePart *__restrict__ parts)
 {
     extern __shared__ __align__(32) int32_t sm_words[];
@@ -907,12 +913,14 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             const QState &Q = qs[qi];
             const int64_t c0 = i == 0 ? 0 : cincl[i - 1];
             const int64_t eta = Q.st.eta0 << b;
+            const uint64_t klo = (uint64_t)walks_lo(Q.st.eta0, b, reuse);
+            const uint32_t bkey = reuse ? 0u : (uint32_t)b;   // reuse: one sample stream per query
             const uint32_t q = Q.gq;
             uint64_t kk[NP];
             bool any = false;
 #pragma unroll
             for (int p = 0; p < NP; p++) {
-                kk[p] = (uint64_t)(chunk - c0) * (32u * NP) + 32u * p + (uint64_t)lane;
+                kk[p] = klo + (uint64_t)(chunk - c0) * (32u * NP) + 32u * p + (uint64_t)lane;
                 any |= kk[p] < (uint64_t)eta;
             }
             double acc[2 * NP];
@@ -921,7 +929,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             uint64_t ck = 0ull;
             if (any) {
                 walk_chains<ARC, NP>(rec, arcs, cols, parcs, pk, s_mode[warp], sm_words + s_soff[warp], Q.ykeys,
-                                     Q.yrec, Q.yvals, Q.ylog2 - YB_LOG, Q.s, Q.t, Q.st.ell_f, q, (uint32_t)b, kk,
+                                     Q.yrec, Q.yvals, Q.ylog2 - YB_LOG, Q.s, Q.t, Q.st.ell_f, q, bkey, kk,
                                      key0, key1, acc, endv, pol);
 #pragma unroll
                 for (int p = 0; p < NP; p++) {
@@ -929,8 +937,8 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
                         const double z = acc[2 * p] - acc[2 * p + 1];   // Z_k (Alg. 1 L8)
                         s1 += z;
                         s2 += z * z;
-                        ck += walk_hash(q, (uint32_t)b, 0u, kk[p], endv[2 * p]) +
-                              walk_hash(q, (uint32_t)b, 1u, kk[p], endv[2 * p + 1]);
+                        ck += walk_hash(q, bkey, 0u, kk[p], endv[2 * p]) +
+                              walk_hash(q, bkey, 1u, kk[p], endv[2 * p + 1]);
                     }
                 }
             }
@@ -979,15 +987,22 @@ __global__ void k_amc_reduce(int32_t na, const int32_t *__restrict__ amc, const 
     if (lane != 0) return;
     QState &Q = qs[amc[i]];
     const int64_t eta = Q.st.eta0 << b;
+    const int64_t drawn = eta - walks_lo(Q.st.eta0, b, P.reuse);
+    if (P.reuse) {   // running sums over all samples so far
+        Q.s1acc = (b == 0 ? 0.0 : Q.s1acc) + s1;
+        Q.s2acc = (b == 0 ? 0.0 : Q.s2acc) + s2;
+        s1 = Q.s1acc;
+        s2 = Q.s2acc;
+    }
     const double etaf = (double)eta;
     const double Z = s1 / etaf;
     double var = s2 / etaf - Z * Z;
     if (var < 0.0) var = 0.0;
     const double f = sqrt(2.0 * var * P.L_bern / etaf) + 3.0 * Q.st.psi * P.L_bern / etaf;
     Q.st.batches_run = b + 1;
-    Q.st.walks_total += eta;
-    Q.st.steps_total += 2 * eta * (int64_t)Q.st.ell_f;
-    if (steps_counter) atomicAdd(steps_counter, (unsigned long long)(2 * eta * (int64_t)Q.st.ell_f));
+    Q.st.walks_total += drawn;
+    Q.st.steps_total += 2 * drawn * (int64_t)Q.st.ell_f;
+    if (steps_counter) atomicAdd(steps_counter, (unsigned long long)(2 * drawn * (int64_t)Q.st.ell_f));
     Q.st.walk_checksum += ck;
     Q.st.f_last = f;
     Q.st.sigma2_last = var;
@@ -1322,7 +1337,7 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
     const uint32_t key0 = (uint32_t)P.seed, key1 = (uint32_t)(P.seed >> 32);
     for (int b = 0; b < P.tau; b++) {
-        k_nchunks<<<blocks_for(na, 256), 256, 0, sb>>>(na, list, qs, b, per_chunk, nch);
+        k_nchunks<<<blocks_for(na, 256), 256, 0, sb>>>(na, list, qs, b, P.reuse, per_chunk, nch);
         LAUNCHED(g);
         size_t b2 = tbytes;
         CK(cub::DeviceScan::InclusiveSum(tmp, b2, nch, cincl, na, sb));
@@ -1336,7 +1351,7 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
         }
 #define WALK_ARGS                                                                                         \
     na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, smem_words,      \
-        g->y_evict_first,                                                                                     \
+        g->y_evict_first, P.reuse,                                                                            \
         persist ? tctr + b : nullptr, parts
 #define WALK_LAUNCH(ARC, NP, MINB)                                                                          \
     do {                                                                                                    \
@@ -1493,6 +1508,8 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
     P.tau = o.tau;
     P.force_ell_b = o.force_ell_b;
     P.ell_variant = o.ell_variant;
+    P.reuse = o.reuse_samples;
+    P.switch_ratio = o.switch_ratio;
     P.nbits = g->nbits;
     P.seed = o.seed;
     P.qbase = o.query_index_base;

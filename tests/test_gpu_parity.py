@@ -44,7 +44,8 @@ def compare(g, pairs, r_gpu, st_gpu, r_or, st_or, sorted_adj=True):
 
 def run_both(G, h, g, pairs, eps, **kw):
     r, st = G.er_query_batch_ex(h, pairs, eps, 0.01, stats=True, **kw)
-    okw = {k: v for k, v in kw.items() if k in ("tau", "seed", "query_index_base", "force_ell_b", "ell_variant")}
+    okw = {k: v for k, v in kw.items() if k in ("tau", "seed", "query_index_base", "force_ell_b", "ell_variant",
+                                                "switch_ratio", "reuse_samples")}
     ro, so = oracle.geer_batch(g, g.lam, pairs, eps, delta=0.01, **okw)
     return r, st, ro, so
 
@@ -69,7 +70,9 @@ def test_tiny_parity_and_exact(geer, tiny, tiny_h, eps):
 
 
 @pytest.mark.parametrize("kw", [dict(tau=1), dict(tau=8), dict(force_ell_b=0), dict(force_ell_b=3),
-                                dict(ell_variant=1), dict(seed=12345, query_index_base=777)])
+                                dict(ell_variant=1), dict(seed=12345, query_index_base=777),
+                                dict(switch_ratio=0.25), dict(switch_ratio=4.0), dict(reuse_samples=1),
+                                dict(reuse_samples=1, force_ell_b=0, tau=7)])
 def test_tiny_parity_options(geer, tiny, tiny_h, kw):
     g, pairs = tiny
     r, st, ro, so = run_both(geer, tiny_h, g, pairs, 0.2, **kw)
@@ -202,6 +205,15 @@ def test_rmat20_lambda_vs_arpack(rmat20):
     g, _, _, _ = rmat20
     ref = W.lambda_of(g)
     assert ref - 1e-9 <= g.lam <= ref + 2e-5
+
+
+@pytest.mark.parametrize("kw", [dict(switch_ratio=0.3), dict(reuse_samples=1)])
+def test_rmat20_parity_variants(geer, rmat20, kw):
+    """SURVEY 8(f)#4 variant knobs at config-1 size (first 2000 queries): GPU = oracle."""
+    g, pairs, _, h = rmat20
+    sub = np.concatenate([pairs[:1000], pairs[5000:6000]])
+    r, st, ro, so = run_both(geer, h, g, sub, 0.1, **kw)
+    compare(g, sub, r, st, ro, so)
 
 
 @pytest.mark.parametrize("eps", [0.5, 0.2, 0.1])

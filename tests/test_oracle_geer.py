@@ -310,3 +310,43 @@ def test_walk_checksum_is_sum_of_endpoint_hashes():
             e1 = oracle.walk(g, 7, lf, q=5, b=b, side=1, k=k)[0]
             ck = (ck + oracle.walk_hash(5, b, 0, k, e0) + oracle.walk_hash(5, b, 1, k, e1)) % 2 ** 64
     assert ck == int(row["walk_checksum"])
+
+
+def test_variant_switch_ratio_extremes(tiny):
+    """SURVEY 8(f)#4 GPU-cost switch knob: ratio -> infinity never leaves the SMM head (ell_b = ell,
+    r' = r_ell by dense matrix powers, Eq. 4); ratio 0 leaves after the first iteration; 1.0 is
+    Eq. 15 (the default)."""
+    g, pairs = tiny
+    sub = pairs[:12]
+    r_inf, st_inf = oracle.geer_batch(g, g.lam, sub, 0.1, switch_ratio=1e18)
+    assert np.array_equal(st_inf["ell_b"], st_inf["ell"]) and (st_inf["batches_run"] == 0).all()
+    for (s, t), r, L in zip(sub, r_inf, st_inf["ell"]):
+        assert abs(r - exact.r_ell(g, int(s), int(t), int(L))) <= 1e-12
+    _, st0 = oracle.geer_batch(g, g.lam, sub, 0.1, switch_ratio=0.0)
+    assert ((st0["ell_b"] == 1) | (st0["ell"] == 0)).all()
+    r1, st1 = oracle.geer_batch(g, g.lam, sub, 0.1, switch_ratio=1.0)
+    rd, sd = oracle.geer_batch(g, g.lam, sub, 0.1)
+    assert r1.tobytes() == rd.tobytes()
+
+
+def test_variant_reuse_samples_is_running_mean(tiny):
+    """SURVEY 8(f)#4 sample-reuse knob: the final estimate is r_b + the mean of Z_0..Z_{eta-1} of
+    ONE sample stream (batch key 0), eta = the last batch size; walks are never redrawn."""
+    g, pairs = tiny
+    sub = pairs[:30]
+    r, st = oracle.geer_batch(g, g.lam, sub, 0.1, reuse_samples=1)
+    checked = 0
+    for i, ((s, t), ri) in enumerate(zip(sub, r)):
+        lf = int(st["ell_f"][i])
+        if lf <= 0:
+            continue
+        eta_last = int(st["eta0"][i]) << (int(st["batches_run"][i]) - 1)
+        assert int(st["walks_total"][i]) == eta_last
+        rb, _, xs, xt = oracle.smm(g, int(s), int(t), int(st["ell_b"][i]))
+        z = oracle.amc_samples(g, int(s), int(t), xs, xt, lf, eta_last, q=i, b=0)
+        acc = 0.0
+        for zk in z:
+            acc += zk
+        assert ri == rb + acc / eta_last
+        checked += 1
+    assert checked > 10
