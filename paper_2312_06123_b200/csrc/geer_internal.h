@@ -31,7 +31,8 @@ struct QState {
     int32_t ymode;         // y-table layout: 0 hash (ykeys, ylog2), 1 rank bitmap (yrec)
     int32_t pad2;
     const int32_t *ykeys;  // hash keys (YT_HASH)
-    const uint4 *yrec;     // rank records {bits lo, bits hi, rank, 0} per 64 node ids (YT_RANK)
+    const uint4 *yrec;     // rank records {U bits lo, U bits hi, rank U, rank t*-side} per 64 node ids (YT_RANK)
+    const uint4 *yaux;     // build-time {s*-side bits, t*-side bits} per 64 node ids (YT_RANK)
     const double *yvals;   // values (by slot, or by rank)
     double z;              // last batch mean Z (= r_f)
     double s1acc, s2acc;   // running sums of Z_k, Z_k^2 (reuse variant)

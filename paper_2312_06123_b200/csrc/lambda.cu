@@ -52,6 +52,12 @@ __global__ void k_lz_matvec(int64_t n, const int64_t *__restrict__ off, const in
     w[v] = isd[v] * s;
 }
 
+__global__ void k_lz_mul(int64_t n, const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ c)
+{
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) c[v] = a[v] * b[v];
+}
+
 __global__ void k_lz_dot(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
                          double *__restrict__ part)
 {
@@ -138,10 +144,11 @@ int run_estimate_lambda(er_graph *g, int iters, double *lambda_out)
     cudaStream_t st = g->stream;
     const int m = (int)std::min<int64_t>(iters, std::min<int64_t>(n - 1, 400));
     double *buf = nullptr, *part = nullptr, *scal = nullptr;
-    CKL(cudaMalloc(&buf, sizeof(double) * 5 * n));
+    CKL(cudaMalloc(&buf, sizeof(double) * 7 * n));
     CKL(cudaMalloc(&part, sizeof(double) * DOT_BLOCKS));
     CKL(cudaMalloc(&scal, sizeof(double) * 4));
-    double *isd = buf, *u1 = buf + n, *qp = buf + 2 * n, *q = buf + 3 * n, *w = buf + 4 * n;
+    double *isd = buf, *u1 = buf + n, *qp = buf + 2 * n, *q = buf + 3 * n, *w = buf + 4 * n, *ty = buf + 5 * n,
+           *tz = buf + 6 * n;
     const unsigned B = (unsigned)((n + 255) / 256);
     int rc = ER_OK;
     auto dot = [&](const double *a, const double *b, double *out) -> int {
@@ -166,7 +173,11 @@ int run_estimate_lambda(er_graph *g, int iters, double *lambda_out)
         g->launches++;
         double bprev = 0.0;
         for (int j = 0; j < m; j++) {
-            k_lz_matvec<<<B, 256, 0, st>>>(n, g->d_off, g->d_cols, isd, q, w);
+            // w = N q = D^-1/2 A D^-1/2 q, the A product on K9 (load-balanced over hub rows)
+            k_lz_mul<<<B, 256, 0, st>>>(n, isd, q, ty);
+            g->launches++;
+            if ((rc = run_spmm(g, ty, tz, 1, 0, st))) break;
+            k_lz_mul<<<B, 256, 0, st>>>(n, isd, tz, w);
             g->launches++;
             double a = 0.0;
             if ((rc = dot(q, w, &a))) break;

@@ -226,7 +226,7 @@ __device__ __forceinline__ bool warp_seg_head(int32_t g)
 template <class KeyT>
 __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const int64_t *__restrict__ runstart,
                              const KeyT *__restrict__ keys, int nbits, int one_chunk, const double *__restrict__ vals,
-                             const int32_t *__restrict__ segbeg, int32_t nseg, const int64_t *__restrict__ off,
+                             const int32_t *__restrict__ segbeg, int32_t nseg, const uint2 *__restrict__ rec,
                              const int32_t *__restrict__ act, const QState *__restrict__ qs,
                              int32_t *__restrict__ nid, double *__restrict__ nval, int32_t *__restrict__ nseg_out,
                              SegStat *__restrict__ ss)
@@ -252,7 +252,7 @@ __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const
         }
         double sum = 0.0;
         for (int64_t p = p0; p < p1; p++) sum += vals[p];   // ascending source order (R13)
-        const int64_t d = off[u + 1] - off[u];
+        const int64_t d = (int64_t)__ldg(rec + u).y;   // node record {offset, degree}
         const double x = sum / (double)d;
         nid[r] = u;
         nval[r] = x;
@@ -276,7 +276,7 @@ __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const
 // order, so no push/sort is needed.  Same statistics as k_run_reduce.
 __global__ void k_first_wave(int64_t E, int32_t nseg, const int64_t *__restrict__ ent_off,
                              const int32_t *__restrict__ fr_id, const int64_t *__restrict__ off,
-                             const int32_t *__restrict__ cols, const int32_t *__restrict__ act,
+                             const uint2 *__restrict__ rec, const int32_t *__restrict__ cols, const int32_t *__restrict__ act,
                              const QState *__restrict__ qs, int32_t *__restrict__ nid, double *__restrict__ nval,
                              int32_t *__restrict__ nseg_out, SegStat *__restrict__ ss, int64_t *__restrict__ dU)
 {
@@ -294,7 +294,7 @@ __global__ void k_first_wave(int64_t E, int32_t nseg, const int64_t *__restrict_
         g = lo;
         const int32_t v = fr_id[g];
         const int32_t u = cols[off[v] + (p - ent_off[g])];
-        const int64_t d = off[u + 1] - off[u];
+        const int64_t d = (int64_t)__ldg(rec + u).y;   // node record {offset, degree}
         const double sum = 0.0 + 1.0;
         const double x = sum / (double)d;
         nid[p] = u;
@@ -446,7 +446,7 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int
                           const int64_t *__restrict__ hincl, const int64_t *__restrict__ vslots,
                           const int64_t *__restrict__ vincl, const int64_t *__restrict__ rrecs,
                           const int64_t *__restrict__ rincl, const int32_t *kbase, const double *vbase,
-                          const uint4 *rbase, QState *__restrict__ qs)
+                          const uint4 *rbase, const uint4 *abase, QState *__restrict__ qs)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na || vslots[i] == 0) return;
@@ -455,6 +455,7 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int
     if (rrecs[i] > 0) {
         Q.ymode = YT_RANK;
         Q.yrec = rbase + (rincl[i] - rrecs[i]);
+        Q.yaux = abase + (rincl[i] - rrecs[i]);
         Q.ykeys = nullptr;
         Q.ylog2 = 0;
     } else {
@@ -468,11 +469,11 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int
     }
 }
 
-__global__ void k_yfill(int64_t H, int32_t *__restrict__ keys, int64_t R, uint4 *__restrict__ recs)
+__global__ void k_yfill(int64_t H, int32_t *__restrict__ keys, int64_t R, uint4 *__restrict__ aux)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j < H) keys[j] = -1;
-    if (j < R) recs[j] = make_uint4(0u, 0u, 0u, 0u);
+    if (j < R) aux[j] = make_uint4(0u, 0u, 0u, 0u);   // the records themselves are written by k_yrank
 }
 
 __device__ __forceinline__ int64_t rank_index(const uint4 r, int32_t v)
@@ -520,12 +521,14 @@ __device__ __forceinline__ int64_t find_sorted(const int32_t *__restrict__ id, i
 // K5 over the support entries (frontier entry e: node id[e], value val[e], segment seg[e] =
 // 2 i + side; each segment sorted by node id) of the leaving queries.  Every node v of
 // U = supp(s*) u supp(t*) has one OWNER entry (its side-0 entry, else its side-1 entry), which
-// finds v's entry on the other side by binary search and writes
+// finds v's entry on the other side and writes
 //     y(v) = s*(v)/d(s) - t*(v)/d(t)          (a side v is not on contributes 0.0 / d = 0.0)
 // exactly once (Alg. 1 L7 with s = s*, t = t*).
-//   pass 0: hash: owners insert v (CAS on the key slot) and write y;  rank: every entry sets bit v
-//   (k_yrank between the passes)
-//   pass 1: rank: owners write y at rank + popc(bits below v)
+//   pass 0: hash: owners find the other side by binary search, insert v (CAS on the key slot)
+//           and write y;  rank: every entry sets its side's bit of v
+//   (k_yrank between the passes: union bits, rank of U and rank of the t* side per record)
+//   pass 1: rank: owners find v's t* entry by rank (segment start + rank T + popc) and write y
+//           at rank U + popc(U bits below v)
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                           const int32_t *__restrict__ id, const double *__restrict__ val,
                           const int64_t *__restrict__ segoff, const int32_t *__restrict__ act,
@@ -539,11 +542,30 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
     const int side = g & 1;
     const QState &Q = qs[act[i]];
     const int32_t v = id[e];
-    if (Q.ymode == YT_RANK && pass == 0) {
-        atomicOr(reinterpret_cast<unsigned long long *>(const_cast<uint4 *>(Q.yrec) + (v >> 6)), 1ull << (v & 63));
+    if (Q.ymode == YT_RANK) {
+        // membership bits per side in the build-time aux records {S bits, T bits}; k_yrank turns
+        // them into the walk records {U bits, rank U, rank T}; no searches
+        uint4 *aux = const_cast<uint4 *>(Q.yaux);
+        const uint64_t bit = 1ull << (v & 63);
+        if (pass == 0) {
+            atomicOr(reinterpret_cast<unsigned long long *>(aux + (v >> 6)) + side, bit);
+            return;
+        }
+        const uint4 a = aux[v >> 6];
+        const uint64_t sbits = ((uint64_t)a.y << 32) | a.x, tbits = ((uint64_t)a.w << 32) | a.z;
+        if (side == 1 && (sbits & bit)) return;   // the side-0 entry owns v
+        const uint4 r = Q.yrec[v >> 6];
+        const uint64_t below = bit - 1ull;
+        double xt = 0.0;
+        if (side == 1) xt = val[e];
+        else if (tbits & bit) xt = val[segoff[g ^ 1] + r.w + __popcll(tbits & below)];   // v's t* entry
+        const double xs = side == 0 ? val[e] : 0.0;
+        const double y = xs / (double)Q.ds - xt / (double)Q.dt;
+        const uint64_t ubits = ((uint64_t)r.y << 32) | r.x;
+        const_cast<double *>(Q.yvals)[r.z + __popcll(ubits & below)] = y;
         return;
     }
-    if ((Q.ymode == YT_HASH) != (pass == 0)) return;
+    if (pass != 0) return;
     // owner test and the other side's value
     const int64_t other = find_sorted(id, segoff[g ^ 1], segoff[(g ^ 1) + 1], v);
     if (side == 1 && other >= 0) return;   // the side-0 entry owns v
@@ -564,19 +586,22 @@ k_yrank(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__
     const int32_t i = blockIdx.x;
     if (i >= na || rrecs[i] == 0) return;
     uint4 *recs = const_cast<uint4 *>(qs[act[i]].yrec);
+    const uint4 *aux = qs[act[i]].yaux;
     const int64_t R = rrecs[i];
-    typedef cub::BlockScan<uint32_t, YRANK_THREADS> Scan;
+    typedef cub::BlockScan<unsigned long long, YRANK_THREADS> Scan;
     __shared__ typename Scan::TempStorage tmp;
-    uint32_t carry = 0;
+    unsigned long long carry = 0;   // (rank U << 32) | rank T
     for (int64_t base = 0; base < R; base += YRANK_THREADS) {
         const int64_t w = base + threadIdx.x;
-        uint4 r = w < R ? recs[w] : make_uint4(0u, 0u, 0u, 0u);
-        const uint32_t c = (uint32_t)(__popc(r.x) + __popc(r.y));
-        uint32_t excl, tot;
+        const uint4 a = w < R ? aux[w] : make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t ux = a.x | a.z, uy = a.y | a.w;
+        const unsigned long long c = ((unsigned long long)(__popc(ux) + __popc(uy)) << 32) |
+                                     (unsigned long long)(__popc(a.z) + __popc(a.w));
+        unsigned long long excl, tot;
         Scan(tmp).ExclusiveSum(c, excl, tot);
         if (w < R) {
-            r.z = carry + excl;
-            recs[w] = r;
+            const unsigned long long rk = carry + excl;
+            recs[w] = make_uint4(ux, uy, (uint32_t)(rk >> 32), (uint32_t)rk);
         }
         carry += tot;
         __syncthreads();
@@ -1244,16 +1269,18 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
     if ((int)ws.ychunk.size() <= wave) ws.ychunk.resize(wave + 1);
     DevBuf &yb = ws.ychunk[wave];
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };   // 256-byte aligned regions
-    const size_t o_rec = up(sizeof(double) * V), o_key = o_rec + up(sizeof(uint4) * R);
+    const size_t o_rec = up(sizeof(double) * V), o_aux = o_rec + up(sizeof(uint4) * R);
+    const size_t o_key = o_aux + up(sizeof(uint4) * R);
     const size_t ybytes = o_key + up(sizeof(int32_t) * H);
     if (ybytes > yb.cap) CK(cudaDeviceSynchronize());   // the old buffer may still serve an earlier AMC
     ENSURE(yb, ybytes, false);
     double *vals = yb.as<double>();
     uint4 *recs = reinterpret_cast<uint4 *>(yb.as<char>() + o_rec);
+    uint4 *aux = reinterpret_cast<uint4 *>(yb.as<char>() + o_aux);      // build-time {S bits, T bits}
     int32_t *keys = reinterpret_cast<int32_t *>(yb.as<char>() + o_key);   // buckets need 32-byte alignment
-    k_yfill<<<blocks_for(std::max(H, R), 256), 256, 0, c.st>>>(H, keys, R, recs);
+    k_yfill<<<blocks_for(std::max(H, R), 256), 256, 0, c.st>>>(H, keys, R, aux);
     LAUNCHED(c.g);
-    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, hs, hi, vs, vi, rs, ri, keys, vals, recs,
+    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, hs, hi, vs, vi, rs, ri, keys, vals, recs, aux,
                                                       ws.qs.as<QState>());
     LAUNCHED(c.g);
     for (int pass = 0; pass < 2; pass++) {
@@ -1692,19 +1719,19 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             CK(cudaMemsetAsync(ws.segstat.p, 0, sizeof(SegStat) * nseg, st));
             if (fast_first) {
                 k_first_wave<<<blocks_for(E, 256), 256, 0, st>>>(E, nseg, ent_off, ws.fr_id.as<int32_t>(), g->d_off,
-                                                                 g->d_cols, ws.act.as<int32_t>(), qs,
+                                                                 g->d_rec, g->d_cols, ws.act.as<int32_t>(), qs,
                                                                  ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                                                                  ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>(), dU);
             } else
             if (P.nbits <= 24)
                 k_run_reduce<uint32_t><<<blocks_for(E, 256), 256, 0, st>>>(
                     E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint32_t>(), P.nbits, one_chunk, ws.vals2.as<double>(), segbeg,
-                    nseg, g->d_off, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
+                    nseg, g->d_rec, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                     ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>());
             else
                 k_run_reduce<uint64_t><<<blocks_for(E, 256), 256, 0, st>>>(
                     E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint64_t>(), P.nbits, one_chunk, ws.vals2.as<double>(), segbeg,
-                    nseg, g->d_off, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
+                    nseg, g->d_rec, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                     ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>());
             LAUNCHED(g);
             k_seg_max2<<<blocks_for(E, 256), 256, 0, st>>>(E, dU, ws.nf_seg.as<int32_t>(), ws.nf_val.as<double>(),

@@ -474,24 +474,27 @@ def test_smm_series_rmat20_vs_oracle_and_geer_accuracy(geer, rmat20):
     assert np.mean(err <= 0.1) >= 0.99 and err.max() <= 0.2, err.max()
 
 
-@pytest.mark.parametrize("config,eps", [("lj_full", 0.1), ("orkut_full", 0.1)])
-def test_full_size_configs_parity_sampled(geer, config, eps):
-    """BASELINE configs 2 and 3 at full size (GPU R-MAT generator: LiveJournal-shaped n ~ 3.2M,
-    m ~ 37M; Orkut-shaped n ~ 4M, m ~ 117M), in the bench's launch configuration: sampled
-    queries -- the first 100 random pairs and the first 100 edges of the 100k-query set, each
-    block with its global query index base -- against the oracle (decisions, walk checksums
-    exact; |r' - r'_oracle| <= 1e-9), plus the converged series (er_smm_series) within eps."""
+@pytest.mark.parametrize("config,eps,nq", [("lj_full", 0.1, 100), ("orkut_full", 0.1, 100), ("friendster", 0.1, 40)])
+def test_full_size_configs_parity_sampled(geer, config, eps, nq):
+    """BASELINE configs 2-4 at full size (GPU R-MAT generator: LiveJournal-shaped n ~ 3.2M,
+    m ~ 37M; Orkut-shaped n ~ 4M, m ~ 117M; Friendster-shaped n ~ 60M, m ~ 1.8B), in the
+    bench's launch configuration: sampled queries -- the first nq random pairs and the first
+    nq edges of the query set, each block with its global query index base -- against the
+    oracle (decisions, walk checksums exact; |r' - r'_oracle| <= 1e-9), plus the converged
+    series (er_smm_series) within eps on a few of them."""
     g, pairs, _ = W.load_config(config)
     h = geer.er_graph_create(g.n, g.offsets, g.cols)
     try:
         g.lam = geer.er_graph_estimate_lambda(h)
         half = len(pairs) // 2
         for base in (0, half):
-            sub = pairs[base:base + 100]
+            sub = pairs[base:base + nq]
             r, st = geer.er_query_batch_ex(h, sub, eps, 0.01, stats=True, query_index_base=base)
-            ro, so = oracle.geer_batch(g, g.lam, sub, eps, delta=0.01, query_index_base=base)
+            ro, so = oracle.geer_batch(g, g.lam, sub, eps, delta=0.01, query_index_base=base,
+                                       nthreads=8 if g.n > 10_000_000 else 0)
             compare(g, sub, r, st, ro, so)
-            truth, _ = geer.er_smm_series(h, sub[:20], tol=1e-7)
-            assert np.abs(r[:20] - truth).max() <= eps
+            ns = 20 if g.nnz < (1 << 30) else 4
+            truth, _ = geer.er_smm_series(h, sub[:ns], tol=1e-7)
+            assert np.abs(r[:ns] - truth).max() <= eps
     finally:
         geer.er_graph_destroy(h)

@@ -43,3 +43,15 @@ def test_query_pairs_protocol():
     assert all((int(s), int(t)) in adj for s, t in edges)             # second half: edges
     assert 0.35 < np.mean(edges[:, 0] < edges[:, 1]) < 0.65           # fair-coin orientation
     assert np.array_equal(p, W.query_pairs(g, 1001, seed=5))
+
+
+def test_rmat_torch_bucketed_dedupe_is_identical():
+    """The bucketed torch.unique path (used for billion-arc graphs) builds the same graph."""
+    g1 = W.rmat_torch(12, 6, seed=9, device="cpu")
+    old = W._UNIQUE_BUCKET
+    try:
+        W._UNIQUE_BUCKET = 5000
+        g2 = W.rmat_torch(12, 6, seed=9, device="cpu")
+    finally:
+        W._UNIQUE_BUCKET = old
+    assert np.array_equal(g1.offsets, g2.offsets) and np.array_equal(g1.cols, g2.cols)

@@ -235,6 +235,9 @@ def rmat(scale: int, edge_factor: float, a=0.57, b=0.19, c=0.19, d=0.05, seed: i
                                         "abcd": [a, b, c, d], "seed": seed})
 
 
+_UNIQUE_BUCKET = 1 << 29   # elements per torch.unique call in rmat_torch (memory / 32-bit sort limits)
+
+
 def rmat_torch(scale: int, edge_factor: float, a=0.57, b=0.19, c=0.19, d=0.05, seed: int = 20231212,
                device: str | None = None, name: str | None = None) -> Graph:
     """R-MAT on the GPU (torch), same recipe as ``rmat``: symmetrise, drop self-loops, dedupe,
@@ -247,6 +250,7 @@ def rmat_torch(scale: int, edge_factor: float, a=0.57, b=0.19, c=0.19, d=0.05, s
     N = 1 << scale
     ne = int(edge_factor * N)
     ab, abc = a + b, a + b + c
+    # undirected edge set: canonical keys min * N + max per chunk, deduped
     keys = []
     chunk = 1 << 26
     for lo in range(0, ne, chunk):
@@ -259,44 +263,81 @@ def rmat_torch(scale: int, edge_factor: float, a=0.57, b=0.19, c=0.19, d=0.05, s
             vb = (((r >= a) & (r < ab)) | (r >= abc)).to(torch.int64)
             u = (u << 1) | ub
             v = (v << 1) | vb
+            del r, ub, vb
         keep = u != v
-        u, v = u[keep], v[keep]
-        keys.append(torch.unique(torch.cat([u * N + v, v * N + u])))
-        del u, v, keep
-    key = torch.unique(torch.cat(keys))
+        lo_, hi_ = torch.minimum(u[keep], v[keep]), torch.maximum(u[keep], v[keep])
+        keys.append(torch.unique(lo_ * N + hi_))
+        del u, v, keep, lo_, hi_
+    # dedupe across chunks bucketwise by key range (keeps every sort below 2^31 elements and
+    # the peak memory low); buckets concatenate in ascending key order
+    nb = max(1, -(-sum(k.numel() for k in keys) // _UNIQUE_BUCKET))
+    ea_l, eb_l = [], []
+    for j in range(nb):
+        lo_k, hi_k = (j * N) // nb * N, ((j + 1) * N) // nb * N
+        kj = torch.unique(torch.cat([k[(k >= lo_k) & (k < hi_k)] for k in keys]))
+        ea_l.append((kj // N).to(torch.int32))   # undirected edges (ea < eb)
+        eb_l.append((kj % N).to(torch.int32))
+        del kj
     del keys
-    u = key // N
-    v = key % N
-    del key
-    # largest connected component: min-label propagation over the (symmetric) arcs
+    ea, eb = torch.cat(ea_l), torch.cat(eb_l)
+    del ea_l, eb_l
+    # largest connected component: min-label propagation + pointer jumping over both arc
+    # directions (index tensors widened to int64 one slice at a time)
     lab = torch.arange(N, device=dev, dtype=torch.int64)
+    E = ea.numel()
+    sl = 1 << 27
     while True:
         nl = lab.clone()
-        nl.scatter_reduce_(0, u, lab[v], reduce="amin")
+        for s0 in range(0, E, sl):
+            xa, xb = ea[s0:s0 + sl].long(), eb[s0:s0 + sl].long()
+            nl.scatter_reduce_(0, xa, lab[xb], reduce="amin")
+            nl.scatter_reduce_(0, xb, lab[xa], reduce="amin")
+            del xa, xb
         nl = nl[nl]                      # pointer jumping
         if torch.equal(nl, lab):
             break
         lab = nl
+    del nl
     present = torch.zeros(N, dtype=torch.bool, device=dev)
-    present[u] = True
+    for s0 in range(0, E, sl):
+        present[ea[s0:s0 + sl].long()] = True
+        present[eb[s0:s0 + sl].long()] = True
     cnt = torch.bincount(lab[present], minlength=N)
     big = int(torch.argmax(cnt))
     keepn = torch.nonzero(present & (lab == big)).squeeze(1)
     n = int(keepn.numel())
     relabel = torch.full((N,), -1, dtype=torch.int64, device=dev)
     relabel[keepn] = torch.randperm(n, generator=gen, device=dev)
-    mk = relabel[u] >= 0
-    u2, v2 = relabel[u[mk]], relabel[v[mk]]
-    del u, v, mk, lab, relabel
-    key, _ = torch.sort(u2 * n + v2)
-    del u2, v2
-    uu = key // n
-    cols = (key % n).to(torch.int32)
-    counts = torch.bincount(uu, minlength=n)
+    del cnt, keepn, present
+    # both endpoints of an edge are in the same component: keep the edges of the LCC
+    mk = lab[ea.long()] == big
+    ra = relabel[ea[mk].long()].to(torch.int32)
+    rb = relabel[eb[mk].long()].to(torch.int32)
+    del ea, eb, mk, lab, relabel
+    # symmetric CSR with sorted rows: sorted arc keys row * n + col, built bucketwise by row range
+    nb = max(1, -(-2 * ra.numel() // _UNIQUE_BUCKET))
+    cols_l = []
+    counts = torch.zeros(n, dtype=torch.int64, device=dev)
+    for j in range(nb):
+        r0, r1 = (j * n) // nb, ((j + 1) * n) // nb
+        m1 = (ra >= r0) & (ra < r1)
+        m2 = (rb >= r0) & (rb < r1)
+        kj = torch.unique(torch.cat([ra[m1].long() * n + rb[m1].long(), rb[m2].long() * n + ra[m2].long()]))
+        del m1, m2
+        counts += torch.bincount(kj // n, minlength=n)
+        cols_l.append((kj % n).to(torch.int32))
+        del kj
+    del ra, rb
+    cols = torch.cat(cols_l)
+    del cols_l
     off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
     off[1:] = torch.cumsum(counts, 0)
     nm = name or f"rmat_torch_s{scale}_ef{edge_factor:g}_{a:g}_{b:g}_{c:g}_{d:g}_seed{seed}"
-    return Graph(n, off.cpu().numpy(), cols.cpu().numpy(), nm,
+    off_h, cols_h = off.cpu().numpy(), cols.cpu().numpy()
+    del off, cols, counts
+    if dev.type == "cuda":
+        torch.cuda.empty_cache()   # hand the generator's memory back before the graph is uploaded
+    return Graph(n, off_h, cols_h, nm,
                  meta={"scale": scale, "edge_factor": edge_factor, "abcd": [a, b, c, d], "seed": seed,
                        "generator": "torch"})
 
@@ -350,6 +391,8 @@ CONFIGS = {
     "lj_full": ("rmat_torch", dict(scale=23, edge_factor=4.5, seed=20231212), 100_000, [0.1]),
     "orkut_full": ("rmat_torch", dict(scale=22, edge_factor=28, a=0.45, b=0.22, c=0.22, d=0.11, seed=20231213),
                    100_000, [0.2, 0.1]),
+    # BASELINE config 4 (Friendster-shaped, n ~ 65M, m ~ 1.8B, int64 offsets): 1M queries, 125k per GPU
+    "friendster": ("rmat_torch", dict(scale=27, edge_factor=13.5, seed=20231214), 1_000_000, [0.1]),
 }
 
 
@@ -376,7 +419,8 @@ def load_config(name: str, with_lambda: bool = False) -> tuple[Graph, np.ndarray
         g.lam = None
     if with_lambda and g.lam is None:
         g.lam = lambda_of(g)
-    if not f.exists() or (with_lambda and g.lam is not None):
+    big = g.nnz > (1 << 30)   # multi-GB graphs are regenerated (seconds on the GPU), not cached
+    if not big and (not f.exists() or (with_lambda and g.lam is not None)):
         tmp = f.with_suffix(".tmp%d.npz" % os.getpid())
         np.savez(tmp, n=g.n, offsets=g.offsets, cols=g.cols, name=g.name,
                  lam=g.lam if g.lam is not None else -1.0, pairs=pairs)
