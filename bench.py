@@ -140,7 +140,7 @@ def reference_arm(args):
     import oracle
     import workloads as W
     oracle.build()
-    g, pairs_all, _ = W.load_config(CONFIG, with_lambda=True)
+    g, pairs_all, _ = W.load_config(args.config, with_lambda=True)
     pairs = pairs_all[: args.queries]
     half = len(pairs) // 2
     ns = args.ref_sample // 2
