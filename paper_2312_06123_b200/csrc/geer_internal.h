@@ -105,16 +105,15 @@ struct Workspace {
     DevBuf nf_id, nf_val, nf_seg, nf_off;           // next frontier
     DevBuf ent_off;                                 // emission offsets per frontier entry
     DevBuf keys, vals, keys2, vals2;                // emitted (key, value) pairs + sort buffers
-    DevBuf head, runidx, runstart;                  // run-length reduction
+    DevBuf runidx, runstart;                        // run-length reduction
     DevBuf segstat;                                 // SegStat per segment
-    DevBuf ycap, yoff, ypool, yvals, ytmp;          // y-tables: int32 keys (8 per bucket) | fp64 values | t* scratch
-    DevBuf tiles, parts;                            // AMC tiles
+    DevBuf ycap, yoff;                              // y-table sizes and their scans (per leaving query)
     DevBuf cub_tmp;                                 // CUB temp storage
     DevBuf scalars;                                 // small device scalars
     DevBuf spmm_part;                               // K9 heavy-row segment sums
     DevBuf qids;                                    // device copy of er_opts.query_ids
     std::vector<DevBuf> ychunk;                     // y-tables of each SMM wave (grow-only, kept)
-    DevBuf ids, seglen, segbeg, lfkey;              // 0..k-1 ids; compaction lengths; sort segments; AMC order
+    DevBuf ids, seglen, segbeg;                     // 0..k-1 ids; compaction lengths; sort segments
     void *host_pinned = nullptr;                    // small pinned host scalars
     size_t host_pinned_cap = 0;
     void release();

@@ -1143,8 +1143,9 @@ void DevBuf::release()
 void Workspace::release()
 {
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
-                     &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2, &head,
-                     &runidx, &runstart, &segstat, &ycap, &yoff, &ypool, &tiles, &parts, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &lfkey, &yvals, &ytmp, &cont2, &idx2, &spmm_part, &qids};
+                     &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2,
+                     &runidx, &runstart, &segstat, &ycap, &yoff, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &cont2,
+                     &idx2, &spmm_part, &qids};
     for (DevBuf *b : all) b->release();
     for (DevBuf &b : ychunk) b.release();
     ychunk.clear();
@@ -1706,7 +1707,6 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                 segbeg = ws.segbeg.as<int32_t>();
                 k_segbeg<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, ws.fr_off.as<int64_t>(), ent_off, segbeg);
                 LAUNCHED(g);
-                ENSURE(ws.head, sizeof(int32_t) * E, false);
                 if (P.nbits <= 24) rc = smm_group<uint32_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU, &one_chunk);
                 else rc = smm_group<uint64_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU, &one_chunk);
                 if (rc) return rc;
