@@ -428,7 +428,9 @@ __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState
         const int64_t len = segoff[2 * i + 2] - segoff[2 * i];   // |supp s*| + |supp t*| >= |U|
         int64_t cap = YB;
         while (cap < 2 * len) cap <<= 1;
-        const bool rank = force == 2 || (force == 0 && cap > WALK_KEY_SLOTS && 16 * nrec < 12 * cap);
+        // rank when the table cannot be staged and the records take at most twice the hash footprint:
+        // rank lookups are pipelined off the walk chain, global hash probes are not
+        const bool rank = force == 2 || (force == 0 && cap > WALK_KEY_SLOTS && 16 * nrec < 24 * cap);
         if (rank) {
             r = nrec;
             v = len;
