@@ -84,7 +84,8 @@ void er_graph_destroy(er_graph *g);
  *   eps     additive error eps > 0 (Eq. 2)
  *   p_fail  failure probability delta in (0,1) per query (Thm 3.4); tau = 5 batches
  *   out_r   HOST double[k], caller-allocated; out_r[i] = r'(s_i, t_i)
- * Synchronous.  Uses the library's default seed, query_index_base = 0.
+ * Synchronous.  Uses the library's default seed, query_index_base = 0.  Batches larger than
+ * 2^18 queries run as consecutive sub-batches of the same results (bounded device memory).
  * Any out-of-range id fails the whole call with ER_EINVAL before any work.
  * Estimates are returned unclamped (they may be slightly negative).
  */

@@ -263,6 +263,7 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_Y_EVICT_FIRST")) g->y_evict_first = atoi(env) != 0;
         if (const char *env = getenv("GEER_L2_PERSIST")) g->l2_persist = atoi(env) != 0;
         if (const char *env = getenv("GEER_OVERLAP_FRAC")) g->overlap_frac = std::min(1.0, std::max(0.1, atof(env)));
+        if (const char *env = getenv("GEER_MAX_SUB_BATCH")) g->max_sub_batch = std::max<int64_t>(1, atoll(env));
         if (const char *env = getenv("GEER_WALK_NP")) g->walk_np = atoi(env) == 1 ? 1 : 2;
         if (const char *env = getenv("GEER_WALK_SMEM_KB")) g->walk_smem_words = 256 * std::min(48, std::max(8, atoi(env)));
         g->pack.bo = bo;
@@ -411,7 +412,18 @@ int er_query_batch_ex(er_graph *g, const int32_t *pairs, int64_t k, double eps, 
     int cur = 0;
     cudaGetDevice(&cur);
     if (cur != g->device) cudaSetDevice(g->device);
-    const int rc = run_query_batch(g, pairs, k, eps, p_fail, opt, out_r, stats);
+    // Very large batches run as consecutive sub-batches (bounded workspaces and per-wave pair
+    // counts); every query keeps its global index, so the results are those of one batch.
+    int rc = ER_OK;
+    const int64_t sub = g->max_sub_batch;
+    for (int64_t lo = 0; lo < k && rc == ER_OK; lo += sub) {
+        const int64_t kk = std::min(sub, k - lo);
+        er_opts o2 = opt;
+        if (opt.query_ids) o2.query_ids = opt.query_ids + lo;
+        else o2.query_index_base = opt.query_index_base + lo;
+        if (lo + kk < k) o2.synchronous = 1;   // only the last sub-batch may return early
+        rc = run_query_batch(g, pairs + 2 * lo, kk, eps, p_fail, o2, out_r + lo, stats ? stats + lo : nullptr);
+    }
     if (cur != g->device) cudaSetDevice(cur);
     return rc;
 }

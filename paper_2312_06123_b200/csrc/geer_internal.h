@@ -145,6 +145,7 @@ struct er_graph {
     int y_evict_first = 0; // K6: L2 evict-first policy on y-table loads (GEER_Y_EVICT_FIRST)
     bool l2_persist = false; // K6: persisting-L2 access window over the walk graph (GEER_L2_PERSIST)
     size_t l2_window = 0, l2_persist_bytes = 0;
+    int64_t max_sub_batch = 1 << 18;  // queries per internal sub-batch (GEER_MAX_SUB_BATCH)
     int walk_np = 1;     // K6 walk pairs per thread (GEER_WALK_NP 1..2)
     int walk_smem_words = 6144;   // K6 staging area per CTA in 32-bit words (GEER_WALK_SMEM_KB)
     cudaStream_t stream = nullptr;

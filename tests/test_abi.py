@@ -114,3 +114,16 @@ def test_null_handle_errors(G):
     assert G.lib.er_graph_set_lambda(None, 0.5) == G.ER_EINVAL
     assert G.lib.er_graph_kernel_launches(None) == -1
     G.lib.er_graph_destroy(None)  # NULL-safe
+    r = np.zeros(1)
+    assert G.lib.er_smm_series(None, p.ctypes.data_as(ctypes.c_void_p), 1, 1e-8, 10,
+                               r.ctypes.data_as(ctypes.c_void_p), None) == G.ER_EINVAL
+    assert G.lib.er_spmm(None, None, None, 4, 1, None) == G.ER_EINVAL
+    assert G.lib.er_graph_estimate_lambda(None, 0, None) == G.ER_EINVAL
+    assert G.er_last_error() == G.ER_EINVAL and "NULL" in G.er_last_error_message()
+
+
+def test_opts_validation_without_device(G):
+    """Option checks happen before any device work (a NULL graph is reported first; the
+    option ranges are covered on the GPU by the parity tests)."""
+    o = G.er_opts_default()
+    assert o.switch_ratio == 1.0 and o.reuse_samples == 0 and not o.query_ids

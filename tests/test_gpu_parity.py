@@ -498,3 +498,25 @@ def test_full_size_configs_parity_sampled(geer, config, eps, nq):
             assert np.abs(r[:ns] - truth).max() <= eps
     finally:
         geer.er_graph_destroy(h)
+
+
+def test_sub_batches_are_byte_identical(geer, rmat20):
+    """A batch split into internal sub-batches (GEER_MAX_SUB_BATCH) returns the bytes of the
+    single batch: every query keeps its global index (fresh process: the knob is read at
+    er_graph_create)."""
+    import os
+    import subprocess
+    import sys
+    g = rmat20[0]
+    code = ("import sys, numpy as np; sys.path.insert(0, '.'); import workloads as W;"
+            "import paper_2312_06123_b200 as G;"
+            "g, pairs, _ = W.load_config('rmat20');"
+            "h = G.er_graph_create(g.n, g.offsets, g.cols); G.er_graph_set_lambda(h, float(sys.argv[1]));"
+            "r, st = G.er_query_batch_ex(h, pairs[:3000], 0.1, stats=True, query_index_base=123);"
+            "sys.stdout.buffer.write(r.tobytes() + st.tobytes())")
+    outs = []
+    for env in ({}, {"GEER_MAX_SUB_BATCH": "700"}):
+        outs.append(subprocess.run([sys.executable, "-c", code, repr(g.lam)], env=dict(os.environ, **env),
+                                   check=True, capture_output=True,
+                                   cwd=str(W.Path(__file__).resolve().parents[1])).stdout)
+    assert len(outs[0]) > 0 and outs[0] == outs[1]
