@@ -187,6 +187,7 @@ def config_dict(g, args):
             "queries_per_gpu": args.queries, "eps": args.eps, "delta": 0.01, "tau": 5,
             "parallelism": f"queries sharded over {args.gpus} GPU(s), CSR replicated",
             "l2": "flushed between steps (256 MiB device write outside the timed events)",
+            "switch_ratio": args.switch_ratio,
             "seeds": {"graph": getattr(args, "graph_seed", 20231211), "queries": "graph seed + 1 + rank",
                       "walks": "0x2312061232DEC0DE"}}
 
@@ -229,6 +230,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spmm", action="store_true")
+    ap.add_argument("--switch-ratio", type=float, default=1.0,
+                    help="variant knob (DESIGN R22): leave the SMM head iff vol > ratio * h; 1.0 = Eq. 15")
     ap.add_argument("--config", default=CONFIG, help="workload (BASELINE configs[1] = rmat20 is the graded line)")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -273,7 +276,8 @@ def main():
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
 
     def step():
-        G.er_query_batch_ex(h, pairs_d, args.eps, 0.01, out=out_d, stream=st, query_index_base=lo)
+        G.er_query_batch_ex(h, pairs_d, args.eps, 0.01, out=out_d, stream=st, query_index_base=lo,
+                            switch_ratio=args.switch_ratio)
         if dist:
             with torch.cuda.stream(st):
                 gather_results(out_d, nq * world)
@@ -326,7 +330,7 @@ def main():
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
-        r = G.er_query_batch_ex(h, host_pairs, args.eps, 0.01, query_index_base=lo)[0]
+        r = G.er_query_batch_ex(h, host_pairs, args.eps, 0.01, query_index_base=lo, switch_ratio=args.switch_ratio)[0]
         if dist:
             gather_results(torch.from_numpy(r).cuda(), nq * world).cpu()
         e2e_times.append(time.perf_counter() - t0)
@@ -387,7 +391,7 @@ def main():
             t0 = time.perf_counter()
             truth, ells = G.er_smm_series(h, sub, tol=1e-8)
             t_truth = time.perf_counter() - t0
-            est = G.er_query_batch_ex(h, sub, args.eps, 0.01, query_index_base=lo)[0]
+            est = G.er_query_batch_ex(h, sub, args.eps, 0.01, query_index_base=lo, switch_ratio=args.switch_ratio)[0]
             err = np.abs(est - truth)
             line["accuracy"] = {"queries": int(len(sub)), "eps": args.eps, "max_abs_err": float(err.max()),
                                 "mean_abs_err": float(err.mean()), "frac_within_eps": float(np.mean(err <= args.eps)),
