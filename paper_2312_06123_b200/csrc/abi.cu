@@ -74,13 +74,15 @@ static int validate(int64_t n, const int64_t *off, const int32_t *cols, bool *ro
         const int64_t e0 = off[v], e1 = off[v + 1];
         md = std::max(md, (int32_t)(e1 - e0));
         int cls = -1;
+        bool row_inc = true;   // strictly increasing: no duplicates possible
         for (int64_t e = e0; e < e1; e++) {
             const int32_t u = cols[e];
             if (u < 0 || u >= n) { cls = 0; break; }
             if (u == v) { cls = 1; break; }
-            if (e > e0 && cols[e - 1] >= u) sorted = false;
+            if (e > e0 && cols[e - 1] >= u) row_inc = false;
         }
-        if (cls < 0) {
+        if (!row_inc) sorted = false;
+        if (cls < 0 && !row_inc) {
             // duplicates: sorted copy of the row
             std::vector<int32_t> row(cols + e0, cols + e1);
             std::sort(row.begin(), row.end());
@@ -122,27 +124,44 @@ static int validate(int64_t n, const int64_t *off, const int32_t *cols, bool *ro
         }
     }
     if (asym >= 0) { set_error(ER_EASYM, "adjacency not symmetric at node " + std::to_string(asym)); return ER_EASYM; }
-    // connectivity + 2-colouring (BFS from node 0)
-    std::vector<int8_t> colr(n, -1);
-    std::vector<int32_t> queue;
-    queue.reserve(n);
-    colr[0] = 0;
-    queue.push_back(0);
-    bool bip = true;
-    for (size_t h = 0; h < queue.size(); h++) {
-        const int32_t v = queue[h];
-        for (int64_t e = off[v]; e < off[v + 1]; e++) {
-            const int32_t u = cols[e];
-            if (colr[u] < 0) {
-                colr[u] = 1 - colr[v];
-                queue.push_back(u);
-            } else if (colr[u] == colr[v]) {
-                bip = false;
+    // connectivity + 2-colouring: level-synchronous parallel BFS from node 0, then every arc
+    // must join levels of different parity (an arc inside one parity class closes an odd cycle)
+    std::vector<int32_t> level(n, -1);
+    level[0] = 0;
+    std::vector<int32_t> frontier{0}, next;
+    int64_t visited = 1;
+    for (int32_t L = 0; !frontier.empty(); L++) {
+        next.clear();
+#pragma omp parallel
+        {
+            std::vector<int32_t> local;
+#pragma omp for schedule(dynamic, 256) nowait
+            for (int64_t i = 0; i < (int64_t)frontier.size(); i++) {
+                const int32_t v = frontier[i];
+                for (int64_t e = off[v]; e < off[v + 1]; e++) {
+                    const int32_t u = cols[e];
+                    int32_t expect = -1;
+                    if (__atomic_load_n(&level[u], __ATOMIC_RELAXED) == -1 &&
+                        __atomic_compare_exchange_n(&level[u], &expect, L + 1, false, __ATOMIC_RELAXED,
+                                                    __ATOMIC_RELAXED))
+                        local.push_back(u);
+                }
             }
+#pragma omp critical
+            next.insert(next.end(), local.begin(), local.end());
         }
+        visited += (int64_t)next.size();
+        frontier.swap(next);
+    }
+    bool bip = true;
+    if (visited == n) {
+#pragma omp parallel for schedule(dynamic, 4096) reduction(&& : bip)
+        for (int64_t v = 0; v < n; v++)
+            for (int64_t e = off[v]; e < off[v + 1]; e++)
+                if (((level[v] ^ level[cols[e]]) & 1) == 0) { bip = false; break; }
     }
     *spectral_code = ER_OK;
-    if ((int64_t)queue.size() != n) *spectral_code = ER_EDISCONNECTED;
+    if (visited != n) *spectral_code = ER_EDISCONNECTED;
     else if (bip) *spectral_code = ER_EBIPARTITE;
     if (*spectral_code != ER_OK && !spmm_only) {
         if (*spectral_code == ER_EDISCONNECTED) set_error(ER_EDISCONNECTED, "graph is not connected");
