@@ -12,8 +12,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgeer.so"
-SOURCES = ["pipeline.cu", "abi.cu", "lambda.cu", "spmm.cu"]
-HEADERS = ["geer_internal.h", "geer_device.cuh"]
+SOURCES = ["pipeline.cu", "ytable.cu", "walks.cu", "abi.cu", "lambda.cu", "spmm.cu"]
+HEADERS = ["geer_internal.h", "geer_device.cuh", "stages.h"]
 INCLUDE = PKG.parent / "include" / "geer.h"
 
 NVCC_FLAGS = [
@@ -44,17 +44,39 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile every source to an object in parallel (one nvcc per file), then link."""
     if not force and not needs_build():
         return LIB
-    tmp = LIB.with_suffix(".so.tmp%d" % os.getpid())
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-o", str(tmp), *[str(CSRC / s) for s in SOURCES], "-lgomp"]
+    from concurrent.futures import ThreadPoolExecutor
+    obj_dir = PKG / "_obj"
+    obj_dir.mkdir(exist_ok=True)
+    tag = "%d" % os.getpid()
+
+    def compile_one(src: str):
+        obj = obj_dir / (Path(src).stem + "." + tag + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", str(obj), str(CSRC / src)]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    log = []
+    for obj, r in results:
+        log.append(r.stdout + r.stderr)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building libgeer.so (%s)" % obj.name)
+    tmp = LIB.with_suffix(".so.tmp" + tag)
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+           "-o", str(tmp), *[str(o) for o, _ in results], "-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
+    for o, _ in results:
+        o.unlink(missing_ok=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libgeer.so")
-    (PKG / "build_ptxas.log").write_text(r.stderr)
+        raise RuntimeError("nvcc failed linking libgeer.so")
+    (PKG / "build_ptxas.log").write_text("".join(log))
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write("".join(log))
     os.replace(tmp, LIB)
     return LIB
 

@@ -1,4 +1,5 @@
-// pipeline.cu -- the GEER query pipeline on one B200 (sm_100a).
+// pipeline.cu -- the GEER query pipeline on one B200 (sm_100a): K1-K4, K8 and the batch driver;
+// K5 lives in ytable.cu, K6/K7 in walks.cu.
 //
 // Per batch of k queries:
 //   K1 k_setup            ell (Eq. 6), r_b^0, phase per query            Alg. 3 L1-L4
@@ -18,26 +19,13 @@
 //
 // Everything is deterministic: no floating-point atomics, fixed reduction orders.
 
-#include <cub/cub.cuh>
-
-#include <algorithm>
 #include <cmath>
 #include <cstring>
 
 #include "geer_device.cuh"
-#include "geer_internal.h"
+#include "stages.h"
 
 namespace geer {
-
-#define CK(call)                                            \
-    do {                                                    \
-        cudaError_t _e = (call);                            \
-        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
-    } while (0)
-
-#define LAUNCHED(g) ((g)->launches++)
-
-static inline unsigned blocks_for(int64_t n, int per) { return (unsigned)((n + per - 1) / per); }
 
 // ============================================================================ kernels
 
@@ -400,216 +388,6 @@ __global__ void k_decide(int32_t na, const int32_t *__restrict__ act, const SegS
     }
 }
 
-// y-tables (K5): y(v) = s*(v)/d(s) - t*(v)/d(t) on U = supp(s*) u supp(t*) for each query that
-// leaves the SMM head for AMC in this wave (Alg. 1 L7 with s = s*, t = t*).  Two layouts,
-// chosen per query by footprint:
-//  * hash (YT_HASH): open addressing, 8 int32 keys per 32-byte bucket, buckets probed linearly;
-//    capacity = next power of two >= 2 (|supp s*| + |supp t*|) (load <= 1/2), >= one bucket;
-//    values fp64 by slot.  Small tables are staged whole in the walk kernel's shared memory.
-//  * rank bitmap (YT_RANK): one 16-byte record {uint64 bits; uint32 rank; pad} per 64 node ids
-//    (bit v of U, rank = |U| below the record), values fp64 by rank: y(v) is at
-//    vals[rank + popc(bits below v)].  Exact membership in one 16-byte load, no probing; used
-//    when 16 ceil(n/64) B is below the hash's 12 B/slot footprint (large supports).
-constexpr int YT_HASH = 0;
-constexpr int YT_RANK = 1;
-constexpr int WALK_SMEM_WORDS = 6144;       // 24 KB of staged y-table keys per CTA
-constexpr int WALK_KEY_SLOTS = 4096;        // largest hash table staged in shared memory
-
-// Per leaving query i: hslots[i] hash slots, vslots[i] value slots, rrecs[i] rank records.
-__global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState *__restrict__ qs,
-                       const int32_t *__restrict__ cont, const int64_t *__restrict__ segoff, int64_t nrec,
-                       int force, int64_t *__restrict__ hslots, int64_t *__restrict__ vslots,
-                       int64_t *__restrict__ rrecs)
-{
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= na) return;
-    int64_t h = 0, v = 0, r = 0;
-    if ((cont == nullptr || !cont[i]) && qs[act[i]].phase == PH_AMC) {
-        const int64_t len = segoff[2 * i + 2] - segoff[2 * i];   // |supp s*| + |supp t*| >= |U|
-        int64_t cap = YB;
-        while (cap < 2 * len) cap <<= 1;
-        // rank when the table cannot be staged and the records take at most twice the hash footprint:
-        // rank lookups are pipelined off the walk chain, global hash probes are not
-        const bool rank = force == 2 || (force == 0 && cap > WALK_KEY_SLOTS && 16 * nrec < 24 * cap);
-        if (rank) {
-            r = nrec;
-            v = len;
-        } else {
-            h = cap;
-            v = cap;
-        }
-    }
-    hslots[i] = h;
-    vslots[i] = v;
-    rrecs[i] = r;
-}
-
-__global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__ hslots,
-                          const int64_t *__restrict__ hincl, const int64_t *__restrict__ vslots,
-                          const int64_t *__restrict__ vincl, const int64_t *__restrict__ rrecs,
-                          const int64_t *__restrict__ rincl, const int32_t *kbase, const double *vbase,
-                          const uint4 *rbase, const uint4 *abase, QState *__restrict__ qs)
-{
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= na || vslots[i] == 0) return;
-    QState &Q = qs[act[i]];
-    Q.yvals = vbase + (vincl[i] - vslots[i]);
-    if (rrecs[i] > 0) {
-        Q.ymode = YT_RANK;
-        Q.yrec = rbase + (rincl[i] - rrecs[i]);
-        Q.yaux = abase + (rincl[i] - rrecs[i]);
-        Q.ykeys = nullptr;
-        Q.ylog2 = 0;
-    } else {
-        const int64_t cap = hslots[i];
-        Q.ymode = YT_HASH;
-        Q.ykeys = kbase + (hincl[i] - cap);
-        Q.yrec = nullptr;
-        int lg = 0;
-        while ((1ll << lg) < cap) lg++;
-        Q.ylog2 = lg;
-    }
-}
-
-__global__ void k_yfill(int64_t H, int32_t *__restrict__ keys, int64_t R, uint4 *__restrict__ aux)
-{
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < H) keys[j] = -1;
-    if (j < R) aux[j] = make_uint4(0u, 0u, 0u, 0u);   // the records themselves are written by k_yrank
-}
-
-__device__ __forceinline__ int64_t rank_index(const uint4 r, int32_t v)
-{
-    const unsigned long long bits = ((unsigned long long)r.y << 32) | r.x;
-    const int b = v & 63;
-    if (!((bits >> b) & 1ull)) return -1;
-    return (int64_t)r.z + __popcll(bits & ((1ull << b) - 1ull));
-}
-
-// Hash find-or-insert of v; returns its slot.
-__device__ __forceinline__ int64_t hash_insert(int32_t *keys, int lgb, int32_t v)
-{
-    const uint32_t bmask = (1u << lgb) - 1u;
-    uint32_t bk = ybucket(v, lgb);
-    while (true) {
-        const int4 *bp = reinterpret_cast<const int4 *>(keys + bk * YB);
-        int4 A, B;
-        asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(A.x), "=r"(A.y), "=r"(A.z), "=r"(A.w) : "l"(bp));
-        asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(B.x), "=r"(B.y), "=r"(B.z), "=r"(B.w) : "l"(bp + 1));
-        const int32_t kk[YB] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
-        for (int j = 0; j < YB; j++) {
-            const uint32_t slot = bk * YB + j;
-            int32_t k = kk[j];
-            if (k == -1) k = atomicCAS(&keys[slot], -1, v);
-            if (k == -1 || k == v) return slot;
-        }
-        bk = (bk + 1) & bmask;
-    }
-}
-
-// Position of node v in the sorted id range [lo, hi), or -1.
-__device__ __forceinline__ int64_t find_sorted(const int32_t *__restrict__ id, int64_t lo, int64_t hi, int32_t v)
-{
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        const int32_t x = id[mid];
-        if (x == v) return mid;
-        if (x < v) lo = mid + 1;
-        else hi = mid;
-    }
-    return -1;
-}
-
-// K5 over the support entries (frontier entry e: node id[e], value val[e], segment seg[e] =
-// 2 i + side; each segment sorted by node id) of the leaving queries.  Every node v of
-// U = supp(s*) u supp(t*) has one OWNER entry (its side-0 entry, else its side-1 entry), which
-// finds v's entry on the other side and writes
-//     y(v) = s*(v)/d(s) - t*(v)/d(t)          (a side v is not on contributes 0.0 / d = 0.0)
-// exactly once (Alg. 1 L7 with s = s*, t = t*).
-//   pass 0: hash: owners find the other side by binary search, insert v (CAS on the key slot)
-//           and write y;  rank: every entry sets its side's bit of v
-//   (k_yrank between the passes: union bits, rank of U and rank of the t* side per record)
-//   pass 1: rank: owners find v's t* entry by rank (segment start + rank T + popc) and write y
-//           at rank U + popc(U bits below v)
-__global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
-                          const int32_t *__restrict__ id, const double *__restrict__ val,
-                          const int64_t *__restrict__ segoff, const int32_t *__restrict__ act,
-                          const int64_t *__restrict__ vslots, const QState *__restrict__ qs, int pass)
-{
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
-    const int32_t g = seg[e];
-    const int32_t i = g >> 1;
-    if (vslots[i] == 0) return;
-    const int side = g & 1;
-    const QState &Q = qs[act[i]];
-    const int32_t v = id[e];
-    if (Q.ymode == YT_RANK) {
-        // membership bits per side in the build-time aux records {S bits, T bits}; k_yrank turns
-        // them into the walk records {U bits, rank U, rank T}; no searches
-        uint4 *aux = const_cast<uint4 *>(Q.yaux);
-        const uint64_t bit = 1ull << (v & 63);
-        if (pass == 0) {
-            atomicOr(reinterpret_cast<unsigned long long *>(aux + (v >> 6)) + side, bit);
-            return;
-        }
-        const uint4 a = aux[v >> 6];
-        const uint64_t sbits = ((uint64_t)a.y << 32) | a.x, tbits = ((uint64_t)a.w << 32) | a.z;
-        if (side == 1 && (sbits & bit)) return;   // the side-0 entry owns v
-        const uint4 r = Q.yrec[v >> 6];
-        const uint64_t below = bit - 1ull;
-        double xt = 0.0;
-        if (side == 1) xt = val[e];
-        else if (tbits & bit) xt = val[segoff[g ^ 1] + r.w + __popcll(tbits & below)];   // v's t* entry
-        const double xs = side == 0 ? val[e] : 0.0;
-        const double y = xs / (double)Q.ds - xt / (double)Q.dt;
-        const uint64_t ubits = ((uint64_t)r.y << 32) | r.x;
-        const_cast<double *>(Q.yvals)[r.z + __popcll(ubits & below)] = y;
-        return;
-    }
-    if (pass != 0) return;
-    // owner test and the other side's value
-    const int64_t other = find_sorted(id, segoff[g ^ 1], segoff[(g ^ 1) + 1], v);
-    if (side == 1 && other >= 0) return;   // the side-0 entry owns v
-    const double xs = side == 0 ? val[e] : 0.0;
-    const double xt = side == 1 ? val[e] : (other >= 0 ? val[other] : 0.0);
-    const double y = xs / (double)Q.ds - xt / (double)Q.dt;
-    double *vals = const_cast<double *>(Q.yvals);
-    if (Q.ymode == YT_HASH) vals[hash_insert(const_cast<int32_t *>(Q.ykeys), Q.ylog2 - YB_LOG, v)] = y;
-    else vals[rank_index(Q.yrec[v >> 6], v)] = y;
-}
-
-// Ranks of the rank-bitmap tables: rank(record w) = popcount of all records before w.  One CTA
-// per leaving query (non-rank queries exit).
-constexpr int YRANK_THREADS = 256;
-__global__ void __launch_bounds__(YRANK_THREADS)
-k_yrank(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__ rrecs, QState *__restrict__ qs)
-{
-    const int32_t i = blockIdx.x;
-    if (i >= na || rrecs[i] == 0) return;
-    uint4 *recs = const_cast<uint4 *>(qs[act[i]].yrec);
-    const uint4 *aux = qs[act[i]].yaux;
-    const int64_t R = rrecs[i];
-    typedef cub::BlockScan<unsigned long long, YRANK_THREADS> Scan;
-    __shared__ typename Scan::TempStorage tmp;
-    unsigned long long carry = 0;   // (rank U << 32) | rank T
-    for (int64_t base = 0; base < R; base += YRANK_THREADS) {
-        const int64_t w = base + threadIdx.x;
-        const uint4 a = w < R ? aux[w] : make_uint4(0u, 0u, 0u, 0u);
-        const uint32_t ux = a.x | a.z, uy = a.y | a.w;
-        const unsigned long long c = ((unsigned long long)(__popc(ux) + __popc(uy)) << 32) |
-                                     (unsigned long long)(__popc(a.z) + __popc(a.w));
-        unsigned long long excl, tot;
-        Scan(tmp).ExclusiveSum(c, excl, tot);
-        if (w < R) {
-            const unsigned long long rk = carry + excl;
-            recs[w] = make_uint4(ux, uy, (uint32_t)(rk >> 32), (uint32_t)rk);
-        }
-        carry += tot;
-        __syncthreads();
-    }
-}
-
 // Continuing segments: new lengths (for the compaction scan).
 __global__ void k_seglen(int32_t nseg, const int32_t *__restrict__ cont, const int64_t *__restrict__ segoff,
                          int64_t *__restrict__ len)
@@ -653,392 +431,6 @@ __global__ void k_compact_lists(int32_t na, const int32_t *__restrict__ cont, co
     if (i == na - 1) segoff2[2 * newidx_incl[i]] = segnew_incl[2 * na - 1];
 }
 
-// ---------------------------------------------------------------------------- AMC
-
-// Walk pairs of batch b per AMC query, and the AMC sort key (descending ell_f) used to order
-// the flattened walk space so warps mostly see one trip count.
-// First walk index and number of walks drawn in batch b: all eta_b = eta0 2^b fresh (R8), or, with
-// sample reuse, only the eta_b - eta_{b-1} new ones k in [eta_{b-1}, eta_b).
-__device__ __forceinline__ int64_t walks_lo(int64_t eta0, int b, int reuse) { return reuse && b > 0 ? eta0 << (b - 1) : 0; }
-
-__global__ void k_nchunks(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs, int b,
-                          int reuse, int32_t per_chunk, int64_t *__restrict__ nch)
-{
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= na) return;
-    const QState &Q = qs[amc[i]];
-    const int64_t cnt = (Q.st.eta0 << b) - walks_lo(Q.st.eta0, b, reuse);
-    nch[i] = Q.phase == PH_AMC ? (cnt + per_chunk - 1) / per_chunk : 0;
-}
-
-__global__ void k_lf_key(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs,
-                         uint32_t *__restrict__ key)
-{
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= na) return;
-    key[i] = ~(uint32_t)qs[amc[i]].st.ell_f;
-}
-
-constexpr int WALK_WARPS = 8;
-constexpr int WALK_THREADS = 32 * WALK_WARPS;
-
-__device__ __forceinline__ int32_t find_chunk_query(const int64_t *__restrict__ cincl, int32_t n, int64_t c)
-{
-    int32_t lo = 0, hi = n - 1;  // smallest i with cincl[i] > c
-    while (lo < hi) {
-        const int32_t mid = (lo + hi) >> 1;
-        if (cincl[mid] > c) hi = mid;
-        else lo = mid + 1;
-    }
-    return lo;
-}
-
-// 8 keys of a bucket: index of v, or -1; *empty = the bucket has a free slot.
-__device__ __forceinline__ int bucket_match(const int4 a, const int4 b, int32_t v, bool *empty)
-{
-    int m = -1;
-    m = (b.w == v) ? 7 : m;
-    m = (b.z == v) ? 6 : m;
-    m = (b.y == v) ? 5 : m;
-    m = (b.x == v) ? 4 : m;
-    m = (a.w == v) ? 3 : m;
-    m = (a.z == v) ? 2 : m;
-    m = (a.y == v) ? 1 : m;
-    m = (a.x == v) ? 0 : m;
-    *empty = (a.x < 0) | (a.y < 0) | (a.z < 0) | (a.w < 0) | (b.x < 0) | (b.y < 0) | (b.z < 0) | (b.w < 0);
-    return m;
-}
-
-// y-structure loads with an optional L2 evict-first policy (pol != 0): the tables stream past,
-// the walk graph's arc records should stay in L2.
-__device__ __forceinline__ uint64_t pol_evict_first()
-{
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ double ld_y(const double *p, uint64_t pol)
-{
-    if (!pol) return __ldg(p);
-    double r;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ uint4 ld_y(const uint4 *p, uint64_t pol)
-{
-    if (!pol) return __ldg(p);
-    uint4 r;
-    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
-    return r;
-}
-
-// Hash lookups: slot of v, or -1 when v is not in supp(y) (then y(v) = 0, Alg. 1 L7 outside
-// U_s and U_t).  Staged keys in shared memory, or the table in global memory (one 32-byte
-// sector per bucket, LDG.E.ENL2.256).
-__device__ __forceinline__ int64_t ylookup_smem(const int32_t *skeys, int lgb, int32_t v)
-{
-    const uint32_t bmask = (1u << lgb) - 1u;
-    uint32_t bk = ybucket(v, lgb);
-    while (true) {
-        const int4 a = reinterpret_cast<const int4 *>(skeys + (size_t)bk * YB)[0];
-        const int4 b = reinterpret_cast<const int4 *>(skeys + (size_t)bk * YB)[1];
-        bool empty;
-        const int m = bucket_match(a, b, v, &empty);
-        if (m >= 0) return (int64_t)bk * YB + m;
-        if (empty) return -1;
-        bk = (bk + 1) & bmask;
-    }
-}
-__device__ __forceinline__ int64_t ylookup_global(const int32_t *keys, int lgb, int32_t v, uint64_t pol)
-{
-    const uint32_t bmask = (1u << lgb) - 1u;
-    uint32_t bk = ybucket(v, lgb);
-    while (true) {
-        int4 a, b;
-        if (pol)
-            asm("ld.global.nc.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
-                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-                : "l"(keys + (size_t)bk * YB), "l"(pol));
-        else
-            asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-                : "l"(keys + (size_t)bk * YB));
-        bool empty;
-        const int m = bucket_match(a, b, v, &empty);
-        if (m >= 0) return (int64_t)bk * YB + m;
-        if (empty) return -1;
-        bk = (bk + 1) & bmask;
-    }
-}
-
-template <int ARC>
-__device__ __forceinline__ uint4 next_arc(const uint2 R, uint64_t r64, const uint4 *__restrict__ arcs,
-                                          const int32_t *__restrict__ cols,
-                                          const unsigned long long *__restrict__ parcs, PackSpec pk)
-{
-    const uint64_t e = (uint64_t)R.x + __umul64hi(r64, (uint64_t)R.y);   // idx = floor(r64 d / 2^64) (R10)
-    if (ARC == 2) return pk.unpack(__ldg(parcs + e));
-    if (ARC == 1) return __ldg(arcs + e);
-    uint4 A;
-    A.x = (uint32_t)__ldg(cols + e);
-    return A;
-}
-
-// y-lookup modes of a warp (its query's table layout and the tile's staging plan).
-enum { YM_GLOBAL = 0, YM_SMEM = 1, YM_RANK = 2 };
-
-// NP walk pairs per thread = 2 NP independent chains (S_k from s, T_k from t for each pair),
-// advanced in lock step so 2 NP arc loads are in flight per thread.  Per step and chain:
-// Philox draw (R10; the even step's words are cached from the odd step's call), one arc load
-// (the chain's only dependent memory access), then y(v):
-//   YM_SMEM    hash keys staged in shared memory: probe now, value load consumed next step;
-//   YM_GLOBAL  hash keys in global memory: probe now (32-byte bucket loads), value next step;
-//   YM_RANK    rank-bitmap record load issued now and resolved next step (overlapping the next
-//              arc load), value load consumed the step after.
-// y values are added in step order (R9, R13).
-template <int ARC, int NP>
-__device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
-                                            const int32_t *__restrict__ cols,
-                                            const unsigned long long *__restrict__ parcs, PackSpec pk, int mode,
-                                            const int32_t *skeys, const int32_t *__restrict__ gkeys,
-                                            const uint4 *__restrict__ yrec, const double *__restrict__ gvals,
-                                            int lgb, int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b,
-                                            const uint64_t *kk, uint32_t key0, uint32_t key1, double *acc,
-                                            int32_t *endv, uint64_t pol)
-{
-    constexpr int C = 2 * NP;
-    uint2 R[C];
-    int32_t v[C];
-    double pv[C];
-    uint32_t cz[C], cw[C];
-    uint4 prec[C];       // YM_RANK: record of the previous step's node, resolved this step
-#pragma unroll
-    for (int c = 0; c < C; c++) {
-        v[c] = (c & 1) ? t : s;
-        R[c] = __ldg(rec + v[c]);
-        acc[c] = 0.0;
-        pv[c] = 0.0;
-        cz[c] = 0u;
-        cw[c] = 0u;
-        prec[c] = make_uint4(0u, 0u, 0u, 0u);   // no bits: the start node is not summed (R9)
-    }
-    for (int32_t j = 1; j <= lf; j++) {
-        uint4 A[C];
-#pragma unroll
-        for (int c = 0; c < C; c++) {
-            uint64_t r64;
-            if (j & 1) {
-                const uint64_t k = kk[c >> 1];
-                const U4 r = philox4x32_10(U4{(uint32_t)((j - 1) >> 1), (uint32_t)k, q,
-                                              (b << 29) | ((uint32_t)(c & 1) << 28) | (uint32_t)(k >> 32)},
-                                           key0, key1);
-                r64 = ((uint64_t)r.y << 32) | r.x;
-                cz[c] = r.z;
-                cw[c] = r.w;
-            } else {
-                r64 = ((uint64_t)cw[c] << 32) | cz[c];
-            }
-            A[c] = next_arc<ARC>(R[c], r64, arcs, cols, parcs, pk);
-        }
-#pragma unroll
-        for (int c = 0; c < C; c++) {
-            acc[c] += pv[c];   // y of an earlier step, in step order
-            pv[c] = 0.0;
-            if (mode == YM_RANK) {
-                const int64_t idx = rank_index(prec[c], v[c]);   // v[c] = previous step's node
-                if (idx >= 0) pv[c] = ld_y(gvals + idx, pol);
-            }
-            v[c] = (int32_t)A[c].x;
-            if (ARC) R[c] = make_uint2(A[c].y, A[c].z);
-            else R[c] = __ldg(rec + v[c]);
-            if (mode == YM_RANK) {
-                prec[c] = ld_y(yrec + (v[c] >> 6), pol);
-            } else {
-                const int64_t slot =
-                    mode == YM_SMEM ? ylookup_smem(skeys, lgb, v[c]) : ylookup_global(gkeys, lgb, v[c], pol);
-                if (slot >= 0) pv[c] = ld_y(gvals + slot, pol);
-            }
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < C; c++) {
-        acc[c] += pv[c];
-        if (mode == YM_RANK && lf > 0) {
-            const int64_t idx = rank_index(prec[c], v[c]);
-            if (idx >= 0) acc[c] += ld_y(gvals + idx, pol);
-        }
-        endv[c] = v[c];
-    }
-}
-
-// K6: warp = one chunk of 32 NP walk pairs of one query (chunks of all AMC queries are laid
-// out query after query, queries ordered by descending ell_f; lane l, pair p runs walk
-// k = 32 NP chunk' + 32 p + l).  Per CTA-tile of WALK_WARPS chunks, a staging plan puts the
-// hash keys of each distinct small-table query of the tile into shared memory.  Each warp
-// writes the canonical partial {sum Z, sum Z^2, checksum} of its chunk.
-template <int ARC, int NP, int MINB>
-__global__ void __launch_bounds__(WALK_THREADS, MINB)
-k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
-        const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
-        const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
-        uint32_t key0, uint32_t key1, int32_t smem_words, int y_evict_first, int reuse,
-        unsigned long long *__restrict__ tile_ctr, TilePart *__restrict__ parts)
-{
-    extern __shared__ __align__(32) int32_t sm_words[];
-    __shared__ int32_t s_qi[WALK_WARPS];
-    __shared__ int32_t s_soff[WALK_WARPS];
-    __shared__ int32_t s_mode[WALK_WARPS];
-    __shared__ int64_t s_tile;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
-    const uint64_t pol = y_evict_first ? pol_evict_first() : 0;
-    // persistent: CTA-tiles of WALK_WARPS consecutive chunks handed out by an atomic counter
-    // (dynamic balance: the first tiles, of the longest walks, are the longest); with
-    // tile_ctr == nullptr one tile per CTA, tile = blockIdx.x
-    for (int it = 0;; it++) {
-        if (threadIdx.x == 0)
-            s_tile = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1ull) : (it == 0 ? (int64_t)blockIdx.x : nchunks);
-        __syncthreads();
-        const int64_t tile = s_tile;
-        if (tile * WALK_WARPS >= nchunks) break;
-        const int64_t chunk = tile * WALK_WARPS + warp;
-        const bool wvalid = chunk < nchunks;
-        const int32_t i = wvalid ? find_chunk_query(cincl, na, chunk) : -1;
-        if (lane == 0) s_qi[warp] = i;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            // prefix-fit staging plan over the distinct queries of this tile (consecutive warps)
-            int32_t used = 0;
-            for (int w = 0; w < WALK_WARPS; w++) {
-                const int32_t qi = s_qi[w];
-                s_soff[w] = 0;
-                if (qi < 0) { s_mode[w] = YM_GLOBAL; continue; }
-                if (w > 0 && s_qi[w - 1] == qi) { s_soff[w] = s_soff[w - 1]; s_mode[w] = s_mode[w - 1]; continue; }
-                const QState &Q = qs[amc[qi]];
-                if (Q.ymode == YT_RANK) { s_mode[w] = YM_RANK; continue; }
-                const int32_t cap = 1 << Q.ylog2;
-                if (cap <= WALK_KEY_SLOTS && used + cap <= smem_words) {
-                    s_soff[w] = used; s_mode[w] = YM_SMEM; used += cap;
-                } else {
-                    s_mode[w] = YM_GLOBAL;
-                }
-            }
-        }
-        __syncthreads();
-        for (int w = 0; w < WALK_WARPS; w++) {
-            if (s_mode[w] != YM_SMEM || (w > 0 && s_qi[w - 1] == s_qi[w])) continue;
-            const QState &Q = qs[amc[s_qi[w]]];
-            const int4 *src = reinterpret_cast<const int4 *>(Q.ykeys);
-            int4 *dst = reinterpret_cast<int4 *>(sm_words + s_soff[w]);
-            const int32_t words = 1 << Q.ylog2;
-            for (int32_t e = threadIdx.x; e < words / 4; e += WALK_THREADS) dst[e] = __ldg(src + e);
-        }
-        __syncthreads();
-        if (wvalid) {
-            const int32_t qi = amc[i];
-            const QState &Q = qs[qi];
-            const int64_t c0 = i == 0 ? 0 : cincl[i - 1];
-            const int64_t eta = Q.st.eta0 << b;
-            const uint64_t klo = (uint64_t)walks_lo(Q.st.eta0, b, reuse);
-            const uint32_t bkey = reuse ? 0u : (uint32_t)b;   // reuse: one sample stream per query
-            const uint32_t q = Q.gq;
-            uint64_t kk[NP];
-            bool any = false;
-#pragma unroll
-            for (int p = 0; p < NP; p++) {
-                kk[p] = klo + (uint64_t)(chunk - c0) * (32u * NP) + 32u * p + (uint64_t)lane;
-                any |= kk[p] < (uint64_t)eta;
-            }
-            double acc[2 * NP];
-            int32_t endv[2 * NP];
-            double s1 = 0.0, s2 = 0.0;
-            uint64_t ck = 0ull;
-            if (any) {
-                walk_chains<ARC, NP>(rec, arcs, cols, parcs, pk, s_mode[warp], sm_words + s_soff[warp], Q.ykeys,
-                                     Q.yrec, Q.yvals, Q.ylog2 - YB_LOG, Q.s, Q.t, Q.st.ell_f, q, bkey, kk,
-                                     key0, key1, acc, endv, pol);
-#pragma unroll
-                for (int p = 0; p < NP; p++) {
-                    if (kk[p] < (uint64_t)eta) {
-                        const double z = acc[2 * p] - acc[2 * p + 1];   // Z_k (Alg. 1 L8)
-                        s1 += z;
-                        s2 += z * z;
-                        ck += walk_hash(q, bkey, 0u, kk[p], endv[2 * p]) +
-                              walk_hash(q, bkey, 1u, kk[p], endv[2 * p + 1]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-                ck += __shfl_xor_sync(0xffffffffu, ck, o);
-            }
-            if (lane == 0) {
-                TilePart tp;
-                tp.s1 = s1;
-                tp.s2 = s2;
-                tp.ck = ck;
-                tp.pad = 0;
-                parts[chunk] = tp;
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// K7: one warp per active query: sum its tiles, Alg. 1 L11-L14.
-__global__ void k_amc_reduce(int32_t na, const int32_t *__restrict__ amc, const int64_t *__restrict__ tile_incl,  // partial slots
-                             const TilePart *__restrict__ parts, int b, BatchParams P, QState *__restrict__ qs,
-                             int32_t *__restrict__ cont, unsigned long long *__restrict__ steps_counter)
-{
-    const int lane = threadIdx.x & 31;
-    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (i >= na) return;
-    const int64_t t0 = i == 0 ? 0 : tile_incl[i - 1], t1 = tile_incl[i];
-    if (t1 == t0) return;   // stopped in an earlier batch
-    double s1 = 0.0, s2 = 0.0;
-    uint64_t ck = 0;
-    for (int64_t t = t0 + lane; t < t1; t += 32) {
-        s1 += parts[t].s1;
-        s2 += parts[t].s2;
-        ck += parts[t].ck;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-        ck += __shfl_xor_sync(0xffffffffu, ck, o);
-    }
-    if (lane != 0) return;
-    QState &Q = qs[amc[i]];
-    const int64_t eta = Q.st.eta0 << b;
-    const int64_t drawn = eta - walks_lo(Q.st.eta0, b, P.reuse);
-    if (P.reuse) {   // running sums over all samples so far
-        Q.s1acc = (b == 0 ? 0.0 : Q.s1acc) + s1;
-        Q.s2acc = (b == 0 ? 0.0 : Q.s2acc) + s2;
-        s1 = Q.s1acc;
-        s2 = Q.s2acc;
-    }
-    const double etaf = (double)eta;
-    const double Z = s1 / etaf;
-    double var = s2 / etaf - Z * Z;
-    if (var < 0.0) var = 0.0;
-    const double f = sqrt(2.0 * var * P.L_bern / etaf) + 3.0 * Q.st.psi * P.L_bern / etaf;
-    Q.st.batches_run = b + 1;
-    Q.st.walks_total += drawn;
-    Q.st.steps_total += 2 * drawn * (int64_t)Q.st.ell_f;
-    if (steps_counter) atomicAdd(steps_counter, (unsigned long long)(2 * drawn * (int64_t)Q.st.ell_f));
-    Q.st.walk_checksum += ck;
-    Q.st.f_last = f;
-    Q.st.sigma2_last = var;
-    Q.z = Z;
-    if (fabs(f - P.eps / 2.0) <= 1e-12 * P.eps) Q.st.tie_flags |= 4u;
-    const bool stop = f <= P.eps / 2.0 || b == P.tau - 1;
-    if (stop) Q.phase = PH_DONE;
-    if (cont) cont[i] = stop ? 0 : 1;
-}
 
 // Queries of an active list that leave the SMM head for AMC now (cont == 0, phase AMC).
 __global__ void k_flag_leave(int32_t na, const int32_t *__restrict__ act, const QState *__restrict__ qs,
@@ -1158,58 +550,6 @@ void Workspace::release()
 
 namespace {
 
-struct Ctx {
-    er_graph *g;
-    cudaStream_t st;
-    Workspace &ws;
-    int64_t *hp;  // pinned host scalars
-};
-
-#define ENSURE(buf, bytes, keep) CK((buf).ensure((bytes), (keep), c.st))
-
-template <class F>
-int cub_call(Ctx &c, F &&f)
-{
-    size_t bytes = 0;
-    CK(f((void *)nullptr, bytes));
-    ENSURE(c.ws.cub_tmp, bytes + 16, false);
-    size_t b2 = c.ws.cub_tmp.cap;
-    CK(f(c.ws.cub_tmp.p, b2));
-    c.g->launches += 2;
-    return ER_OK;
-}
-
-// out[0] = 0, out[1..n] = inclusive prefix sums of in[0..n).
-template <class T>
-int scan_offsets(Ctx &c, const T *in, T *out, int64_t n)
-{
-    CK(cudaMemsetAsync(out, 0, sizeof(T), c.st));
-    if (n == 0) return ER_OK;
-    return cub_call(c, [&](void *tmp, size_t &bytes) {
-        return cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, c.st);
-    });
-}
-
-template <class T>
-int scan_incl(Ctx &c, const T *in, T *out, int64_t n)
-{
-    if (n == 0) return ER_OK;
-    return cub_call(c, [&](void *tmp, size_t &bytes) {
-        return cub::DeviceScan::InclusiveSum(tmp, bytes, in, out, n, c.st);
-    });
-}
-
-int read_scalars(Ctx &c, std::initializer_list<const int64_t *> src)
-{
-    int j = 0;
-    for (const int64_t *p : src) {
-        CK(cudaMemcpyAsync(c.hp + j, p, sizeof(int64_t), cudaMemcpyDeviceToHost, c.st));
-        j++;
-    }
-    CK(cudaStreamSynchronize(c.st));
-    return ER_OK;
-}
-
 // Select ids[i] for which flag[i] != 0, in order.  Returns the count through *cnt.
 int select_list(Ctx &c, const int32_t *ids, const int32_t *flag, int32_t n, int32_t *out, int32_t *incl_tmp,
                 int64_t *cnt)
@@ -1229,210 +569,6 @@ int select_list(Ctx &c, const int32_t *ids, const int32_t *flag, int32_t n, int3
     return ER_OK;
 }
 
-// Build the y-tables (K5) of the queries of `act` that leave the head now, from the frontier
-// (segoff, id, val, seg; Fmax entries, device count dF or null).  `cont` may be null (all
-// queries of the list leave).  The tables of SMM wave `wave` live in a grow-only workspace
-// buffer kept across batches: {vals fp64[V] | rank records uint4[R] | hash keys int32[H]};
-// QState holds absolute pointers into it.
-// Phase 1 (no host sync): per-query sizes and their inclusive scans; the three totals are at
-// *tot_h, *tot_v, *tot_r (device) for the caller to read with its other scalars.
-int ytable_plan(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, const int64_t *segoff,
-                const int64_t **tot_h, const int64_t **tot_v, const int64_t **tot_r)
-{
-    Workspace &ws = c.ws;
-    ENSURE(ws.ycap, sizeof(int64_t) * 3 * (na + 1), false);
-    ENSURE(ws.yoff, sizeof(int64_t) * 3 * (na + 1), false);
-    int64_t *hs = ws.ycap.as<int64_t>(), *vs = hs + (na + 1), *rs = vs + (na + 1);
-    int64_t *hi = ws.yoff.as<int64_t>(), *vi = hi + (na + 1), *ri = vi + (na + 1);
-    const int64_t nrec = (c.g->n + 63) / 64;
-    k_ycap<<<blocks_for(na, 256), 256, 0, c.st>>>(na, act, ws.qs.as<QState>(), cont, segoff, nrec, c.g->ytable_force,
-                                                  hs, vs, rs);
-    LAUNCHED(c.g);
-    int rc = scan_incl(c, hs, hi, na);
-    if (!rc) rc = scan_incl(c, vs, vi, na);
-    if (!rc) rc = scan_incl(c, rs, ri, na);
-    *tot_h = hi + (na - 1);
-    *tot_v = vi + (na - 1);
-    *tot_r = ri + (na - 1);
-    return rc;
-}
-
-// Phase 2: allocate and fill the tables planned by ytable_plan (totals H, V, R read by the caller).
-int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, const int32_t *id, const double *val,
-                 const int32_t *seg, int64_t Fmax, const int64_t *dF, int wave, int64_t H, int64_t V, int64_t R)
-{
-    Workspace &ws = c.ws;
-    int64_t *hs = ws.ycap.as<int64_t>(), *vs = hs + (na + 1), *rs = vs + (na + 1);
-    int64_t *hi = ws.yoff.as<int64_t>(), *vi = hi + (na + 1), *ri = vi + (na + 1);
-    if (V == 0) return ER_OK;
-    if (c.g->profiling) {
-        c.g->prof.ytable_slots += H;
-        c.g->prof.yrank_records += R;
-    }
-    if ((int)ws.ychunk.size() <= wave) ws.ychunk.resize(wave + 1);
-    DevBuf &yb = ws.ychunk[wave];
-    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };   // 256-byte aligned regions
-    const size_t o_rec = up(sizeof(double) * V), o_aux = o_rec + up(sizeof(uint4) * R);
-    const size_t o_key = o_aux + up(sizeof(uint4) * R);
-    const size_t ybytes = o_key + up(sizeof(int32_t) * H);
-    if (ybytes > yb.cap) CK(cudaDeviceSynchronize());   // the old buffer may still serve an earlier AMC
-    ENSURE(yb, ybytes, false);
-    double *vals = yb.as<double>();
-    uint4 *recs = reinterpret_cast<uint4 *>(yb.as<char>() + o_rec);
-    uint4 *aux = reinterpret_cast<uint4 *>(yb.as<char>() + o_aux);      // build-time {S bits, T bits}
-    int32_t *keys = reinterpret_cast<int32_t *>(yb.as<char>() + o_key);   // buckets need 32-byte alignment
-    k_yfill<<<blocks_for(std::max(H, R), 256), 256, 0, c.st>>>(H, keys, R, aux);
-    LAUNCHED(c.g);
-    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, hs, hi, vs, vi, rs, ri, keys, vals, recs, aux,
-                                                      ws.qs.as<QState>());
-    LAUNCHED(c.g);
-    for (int pass = 0; pass < 2; pass++) {
-        if (pass == 1) {
-            if (R == 0) break;
-            k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, act, rs, ws.qs.as<QState>());
-            LAUNCHED(c.g);
-        }
-        k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, segoff, act, vs, ws.qs.as<QState>(),
-                                                          pass);
-        LAUNCHED(c.g);
-    }
-    return ER_OK;
-}
-
-int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, const int64_t *segoff,
-                  const int32_t *id, const double *val, const int32_t *seg, int64_t Fmax, const int64_t *dF,
-                  int wave)
-{
-    const int64_t *th, *tv, *tr;
-    int rc = ytable_plan(c, na, act, cont, segoff, &th, &tv, &tr);
-    if (!rc) rc = read_scalars(c, {th, tv, tr});
-    if (rc) return rc;
-    const int64_t H = c.hp[0], V = c.hp[1], R = c.hp[2];
-    return ytable_build(c, na, act, segoff, id, val, seg, Fmax, dF, wave, H, V, R);
-}
-
-// One AMC group: the queries that left the SMM head in the same wave, with their y-tables.
-// Its whole AMC (tau batches) is enqueued on the AMC stream without host synchronisation.
-struct AmcGroup {
-    int32_t na = 0;
-    int32_t *list = nullptr;     // query ids (device), sorted by descending ell_f
-    unsigned long long eta0_sum = 0;
-};
-
-struct BatchRes {
-    std::vector<void *> bufs;    // stream-ordered allocations freed at the end of the batch
-    std::vector<cudaEvent_t> walk_ev;  // profiling: start/end pairs of walk launches
-};
-
-int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs, const BatchParams &P, bool prof,
-                     BatchRes &R)
-{
-    const int32_t na = G.na;
-    if (na == 0) return ER_OK;
-    // per-group buffers (stream ordered on the AMC stream)
-    const int per_chunk = 32 * g->walk_np;   // walk pairs per warp-chunk
-    int64_t maxch = (int64_t)((G.eta0_sum << (P.tau - 1)) / per_chunk) + na + 1;
-    uint32_t *kk = nullptr;
-    int32_t *list2 = nullptr;
-    int64_t *nch = nullptr, *cincl = nullptr;
-    TilePart *parts = nullptr;
-    void *tmp = nullptr;
-    size_t tb1 = 0, tb2 = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, (uint32_t *)nullptr, (uint32_t *)nullptr, (int32_t *)nullptr,
-                                       (int32_t *)nullptr, na, 0, 32, sb));
-    CK(cub::DeviceScan::InclusiveSum(nullptr, tb2, (int64_t *)nullptr, (int64_t *)nullptr, na, sb));
-    const size_t tbytes = std::max(tb1, tb2) + 256;
-    CK(cudaMallocAsync((void **)&kk, sizeof(uint32_t) * 2 * na, sb));
-    CK(cudaMallocAsync((void **)&list2, sizeof(int32_t) * na, sb));
-    CK(cudaMallocAsync((void **)&nch, sizeof(int64_t) * na, sb));
-    CK(cudaMallocAsync((void **)&cincl, sizeof(int64_t) * na, sb));
-    CK(cudaMallocAsync((void **)&parts, sizeof(TilePart) * maxch, sb));
-    unsigned long long *tctr = nullptr;   // K6 tile counters, one per batch
-    CK(cudaMallocAsync((void **)&tctr, sizeof(unsigned long long) * P.tau, sb));
-    CK(cudaMemsetAsync(tctr, 0, sizeof(unsigned long long) * P.tau, sb));
-    R.bufs.push_back(tctr);
-    CK(cudaMallocAsync(&tmp, tbytes, sb));
-    for (void *p : {(void *)kk, (void *)list2, (void *)nch, (void *)cincl, (void *)parts, tmp}) R.bufs.push_back(p);
-    const int32_t *list = G.list;
-    if (na > 1) {
-        // order by descending ell_f (stable): warps then see one trip count
-        k_lf_key<<<blocks_for(na, 256), 256, 0, sb>>>(na, G.list, qs, kk);
-        LAUNCHED(g);
-        size_t b1 = tbytes;
-        CK(cub::DeviceRadixSort::SortPairs(tmp, b1, kk, kk + na, G.list, list2, na, 0, 32, sb));
-        g->launches += 2;
-        list = list2;
-    }
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
-    const uint32_t key0 = (uint32_t)P.seed, key1 = (uint32_t)(P.seed >> 32);
-    for (int b = 0; b < P.tau; b++) {
-        k_nchunks<<<blocks_for(na, 256), 256, 0, sb>>>(na, list, qs, b, P.reuse, per_chunk, nch);
-        LAUNCHED(g);
-        size_t b2 = tbytes;
-        CK(cub::DeviceScan::InclusiveSum(tmp, b2, nch, cincl, na, sb));
-        g->launches += 2;
-        const int64_t bound = (int64_t)((G.eta0_sum << b) / per_chunk) + na;   // chunks of batch b, at most
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (prof) {
-            CK(cudaEventCreate(&e0));
-            CK(cudaEventCreate(&e1));
-            CK(cudaEventRecord(e0, sb));
-        }
-#define WALK_ARGS                                                                                         \
-    na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, smem_words,      \
-        g->y_evict_first, P.reuse,                                                                            \
-        persist ? tctr + b : nullptr, parts
-#define WALK_LAUNCH(ARC, NP, MINB)                                                                          \
-    do {                                                                                                    \
-        CK(cudaFuncSetAttribute(k_walks<ARC, NP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                                (int)smem_bytes));                                                          \
-        int occ = 0;                                                                                        \
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walks<ARC, NP, MINB>, WALK_THREADS,        \
-                                                         smem_bytes));                                      \
-        /* persistent grid: exactly the resident CTAs (a second wave would serialise) */                    \
-        const int64_t tiles = (bound + WALK_WARPS - 1) / WALK_WARPS;                                         \
-        const unsigned grid = (unsigned)std::max<int64_t>(                                                  \
-            1, persist ? std::min<int64_t>((int64_t)std::max(1.0, slot_frac * std::max(occ, 1) * nsm), tiles)  \
-                       : tiles);                                                                            \
-        g->walk_occ = occ;                                                                                  \
-        k_walks<ARC, NP, MINB><<<grid, WALK_THREADS, smem_bytes, sb>>>(WALK_ARGS);                          \
-    } while (0)
-#define WALK_ARC(NP, MINB)                                   \
-    do {                                                     \
-        if (g->d_parcs) WALK_LAUNCH(2, NP, MINB);            \
-        else if (g->d_arcs) WALK_LAUNCH(1, NP, MINB);        \
-        else WALK_LAUNCH(0, NP, MINB);                       \
-    } while (0)
-        const int32_t smem_words = g->walk_smem_words;
-        // with the SMM head running concurrently (overlap), the persistent walk grid takes only a
-        // fraction of the resident-CTA slots so head kernels always find room on every SM
-        const bool persist = g->walk_persist;
-        const double slot_frac = g->amc_overlap ? g->overlap_frac : 1.0;
-        const size_t smem_bytes = sizeof(int32_t) * (size_t)smem_words;
-        if (g->walk_np == 1) {
-            if (g->walk_minb == 3) WALK_ARC(1, 3);
-            else WALK_ARC(1, 4);
-        } else {
-            if (g->walk_minb == 3) WALK_ARC(2, 3);
-            else WALK_ARC(2, 4);
-        }
-#undef WALK_ARC
-#undef WALK_LAUNCH
-#undef WALK_ARGS
-        LAUNCHED(g);
-        if (prof) {
-            CK(cudaEventRecord(e1, sb));
-            R.walk_ev.push_back(e0);
-            R.walk_ev.push_back(e1);
-        }
-        k_amc_reduce<<<blocks_for((int64_t)na * 32, 256), 256, 0, sb>>>(
-            na, list, cincl, parts, b, P, qs, nullptr, prof ? reinterpret_cast<unsigned long long *>(g->d_steps) : nullptr);
-        LAUNCHED(g);
-    }
-    CK(cudaGetLastError());
-    return ER_OK;
-}
 
 // Emit + group one SMM wave: pairs (key, x(v)) sorted by (segment, u), stable (ascending v
 // kept inside each (segment, u) run), then run heads / starts.  Segments are sorted in chunks

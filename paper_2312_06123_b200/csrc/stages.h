@@ -1,0 +1,131 @@
+// stages.h -- host-side helpers and stage entry points shared by the query-pipeline translation
+// units: pipeline.cu (K1-K4, K8 and run_query_batch), ytable.cu (K5), walks.cu (K6, K7).
+#pragma once
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <initializer_list>
+#include <vector>
+
+#include "geer_device.cuh"
+#include "geer_internal.h"
+
+namespace geer {
+
+#define CK(call)                                            \
+    do {                                                    \
+        cudaError_t _e = (call);                            \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+#define LAUNCHED(g) ((g)->launches++)
+
+static inline unsigned blocks_for(int64_t n, int per) { return (unsigned)((n + per - 1) / per); }
+
+// y-table layouts (ytable.cu) and the walk kernel's staging limits (walks.cu).
+constexpr int YT_HASH = 0;
+constexpr int YT_RANK = 1;
+constexpr int WALK_SMEM_WORDS = 6144;       // 24 KB of staged y-table keys per CTA
+constexpr int WALK_KEY_SLOTS = 4096;        // largest hash table staged in shared memory
+
+// Rank-bitmap lookup: record r = {U bits lo, U bits hi, rank U, rank T} of the 64 node ids
+// around v; position of y(v) in the value array, or -1 when v is not in U.
+__device__ __forceinline__ int64_t rank_index(const uint4 r, int32_t v)
+{
+    const unsigned long long bits = ((unsigned long long)r.y << 32) | r.x;
+    const int b = v & 63;
+    if (!((bits >> b) & 1ull)) return -1;
+    return (int64_t)r.z + __popcll(bits & ((1ull << b) - 1ull));
+}
+
+// Walk pairs of AMC batch b: the first walk index drawn in batch b -- all eta_b = eta0 2^b fresh
+// (R8), or, with sample reuse (R23), only the eta_b - eta_{b-1} new ones k in [eta_{b-1}, eta_b).
+__device__ __forceinline__ int64_t walks_lo(int64_t eta0, int b, int reuse) { return reuse && b > 0 ? eta0 << (b - 1) : 0; }
+
+struct Ctx {
+    er_graph *g;
+    cudaStream_t st;
+    Workspace &ws;
+    int64_t *hp;  // pinned host scalars
+};
+
+#define ENSURE(buf, bytes, keep) CK((buf).ensure((bytes), (keep), c.st))
+
+template <class F>
+int cub_call(Ctx &c, F &&f)
+{
+    size_t bytes = 0;
+    CK(f((void *)nullptr, bytes));
+    ENSURE(c.ws.cub_tmp, bytes + 16, false);
+    size_t b2 = c.ws.cub_tmp.cap;
+    CK(f(c.ws.cub_tmp.p, b2));
+    c.g->launches += 2;
+    return ER_OK;
+}
+
+// out[0] = 0, out[1..n] = inclusive prefix sums of in[0..n).
+template <class T>
+int scan_offsets(Ctx &c, const T *in, T *out, int64_t n)
+{
+    CK(cudaMemsetAsync(out, 0, sizeof(T), c.st));
+    if (n == 0) return ER_OK;
+    return cub_call(c, [&](void *tmp, size_t &bytes) {
+        return cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, c.st);
+    });
+}
+
+template <class T>
+int scan_incl(Ctx &c, const T *in, T *out, int64_t n)
+{
+    if (n == 0) return ER_OK;
+    return cub_call(c, [&](void *tmp, size_t &bytes) {
+        return cub::DeviceScan::InclusiveSum(tmp, bytes, in, out, n, c.st);
+    });
+}
+
+inline int read_scalars(Ctx &c, std::initializer_list<const int64_t *> src)
+{
+    int j = 0;
+    for (const int64_t *p : src) {
+        CK(cudaMemcpyAsync(c.hp + j, p, sizeof(int64_t), cudaMemcpyDeviceToHost, c.st));
+        j++;
+    }
+    CK(cudaStreamSynchronize(c.st));
+    return ER_OK;
+}
+
+// K5 (ytable.cu).  Build the y-tables of the queries of `act` that leave the head now, from the
+// frontier (segoff, id, val, seg; Fmax entries, device count dF or null).  `cont` may be null (all
+// queries of the list leave).  The tables of SMM wave `wave` live in a grow-only workspace
+// buffer kept across batches: {vals fp64[V] | rank records uint4[R] | aux uint4[R] | hash keys
+// int32[H]}; QState holds absolute pointers into it.
+// Phase 1 (no host sync): per-query sizes and their inclusive scans; the three totals are at
+// *tot_h, *tot_v, *tot_r (device) for the caller to read with its other scalars.
+int ytable_plan(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, const int64_t *segoff,
+                const int64_t **tot_h, const int64_t **tot_v, const int64_t **tot_r);
+// Phase 2: allocate and fill the tables planned by ytable_plan (totals H, V, R read by the caller).
+int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, const int32_t *id, const double *val,
+                 const int32_t *seg, int64_t Fmax, const int64_t *dF, int wave, int64_t H, int64_t V, int64_t R);
+// Both phases with one host read in between.
+int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, const int64_t *segoff,
+                  const int32_t *id, const double *val, const int32_t *seg, int64_t Fmax, const int64_t *dF,
+                  int wave);
+
+// K6 + K7 (walks.cu).  One AMC group: the queries that left the SMM head in the same wave, with
+// their y-tables.  Its whole AMC (tau batches) is enqueued on stream sb without host sync.
+struct AmcGroup {
+    int32_t na = 0;
+    int32_t *list = nullptr;     // query ids (device)
+    unsigned long long eta0_sum = 0;
+};
+
+struct BatchRes {
+    std::vector<void *> bufs;          // stream-ordered allocations freed at the end of the batch
+    std::vector<cudaEvent_t> walk_ev;  // profiling: start/end pairs of walk launches
+};
+
+int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs, const BatchParams &P, bool prof,
+                     BatchRes &R);
+
+}  // namespace geer
