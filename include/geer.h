@@ -136,8 +136,17 @@ typedef struct er_opts {
     int32_t reuse_samples;     /* variant: 1 = batch b keeps the previous batches'
                                   samples and draws only the new ones (one sample stream per query, batch
                                   key 0); 0 (default) = fresh samples per batch (R8) */
-    int32_t pad1;
+    int32_t smm_mode;          /* how SMM iterations after the first are applied (Alg. 3 L6):
+                                  0 (default) per wave by a cost model: sparse frontier push (K2/K3) or
+                                  the dense block pull (K9, exact sequential sums) when the wave's pushes
+                                  would cost more than a full pass over the CSR for its columns;
+                                  1 = frontier push only; 2 = dense pull whenever the wave has at most
+                                  ER_DENSE_MAX_QUERIES active queries.  All modes give bit-identical
+                                  results (R13, R25); only speed differs */
 } er_opts;
+
+/* Dense-mode limit: a wave runs dense only with <= this many active queries (2 columns each). */
+#define ER_DENSE_MAX_QUERIES 128
 
 #define ER_DEFAULT_SEED 0x2312061232DEC0DEULL
 
@@ -187,6 +196,16 @@ int er_query_batch_ex(er_graph *g, const int32_t *pairs, int64_t k, double eps, 
 int er_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, void *stream);
 
 /*
+ * er_spmm_ex -- er_spmm with flags: ER_SPMM_NORMALIZE (M = D^-1 A, else A) and ER_SPMM_EXACT
+ * (every row, heavy rows included, summed sequentially in CSR order: bit-identical to the plain
+ * dense pull; without it rows of degree > 512 are summed in 512-neighbour segments, DESIGN.md
+ * R13).  Same arguments and errors as er_spmm.
+ */
+#define ER_SPMM_NORMALIZE 1
+#define ER_SPMM_EXACT 2
+int er_spmm_ex(er_graph *g, const double *X, double *Y, int32_t q, int32_t flags, void *stream);
+
+/*
  * er_smm_series -- the deterministic series truncated by a tolerance (SMM-to-ell, the paper's
  * SMM baseline and its ground-truth generator, Alg. 2, Thm 3.1):
  *     r_L(s,t) = sum_{i=0..L} ( y_i(s) - y_i(t) ),  y_0 = e_s/d_s - e_t/d_t,  y_{i+1} = P y_i
@@ -218,6 +237,9 @@ typedef struct er_profile {
     int64_t ytable_slots;    /* hash y-table slots allocated (Alg. 1 L7 tables of the AMC queries) */
     int64_t yrank_records;   /* rank-bitmap y-table records allocated (16 B per 64 node ids) */
     int64_t walk_ctas_per_sm; /* resident K6 CTAs per SM (occupancy API) at the last walk launch */
+    int64_t smm_waves;       /* SMM waves after the first (frontier + dense) */
+    int64_t smm_dense_waves; /* of which applied by the dense pull (K9) */
+    int64_t smm_dense_cols;  /* block columns (2 per active query) summed over the dense waves */
 } er_profile;
 int er_graph_profile(er_graph *g, int enable);
 int er_graph_profile_read(er_graph *g, er_profile *out);

@@ -40,7 +40,7 @@ EXPORTED = ["er_graph_create", "er_graph_create_ex", "er_graph_destroy", "er_que
             "er_last_error_message", "er_graph_lambda", "er_graph_set_lambda",
             "er_graph_estimate_lambda", "er_graph_num_nodes", "er_graph_num_arcs",
             "er_graph_kernel_launches", "er_opts_default", "er_query_batch_ex", "er_spmm",
-            "er_graph_profile", "er_graph_profile_read", "er_smm_series"]
+            "er_graph_profile", "er_graph_profile_read", "er_smm_series", "er_spmm_ex"]
 
 
 class er_opts(ctypes.Structure):
@@ -49,7 +49,7 @@ class er_opts(ctypes.Structure):
                 ("pairs_on_device", ctypes.c_int32), ("out_on_device", ctypes.c_int32),
                 ("ell_variant", ctypes.c_int32), ("synchronous", ctypes.c_int32), ("pad0", ctypes.c_int32),
                 ("query_ids", ctypes.c_void_p), ("switch_ratio", ctypes.c_double), ("reuse_samples", ctypes.c_int32),
-                ("pad1", ctypes.c_int32)]
+                ("smm_mode", ctypes.c_int32)]
 
 
 class er_profile(ctypes.Structure):
@@ -57,7 +57,8 @@ class er_profile(ctypes.Structure):
                 ("walk_launches", ctypes.c_int64), ("walk_steps", ctypes.c_int64),
                 ("smm_pairs", ctypes.c_int64), ("batches", ctypes.c_int64),
                 ("ytable_slots", ctypes.c_int64), ("yrank_records", ctypes.c_int64),
-                ("walk_ctas_per_sm", ctypes.c_int64)]
+                ("walk_ctas_per_sm", ctypes.c_int64), ("smm_waves", ctypes.c_int64),
+                ("smm_dense_waves", ctypes.c_int64), ("smm_dense_cols", ctypes.c_int64)]
 
 
 class GeerError(RuntimeError):
@@ -94,6 +95,8 @@ def _load():
     L.er_opts_default.restype = None
     L.er_spmm.argtypes = [vp, vp, vp, i32, i32, vp]
     L.er_spmm.restype = ctypes.c_int
+    L.er_spmm_ex.argtypes = [vp, vp, vp, i32, i32, vp]
+    L.er_spmm_ex.restype = ctypes.c_int
     L.er_smm_series.argtypes = [vp, vp, i64, dbl, i32, vp, vp]
     L.er_smm_series.restype = ctypes.c_int
     L.er_graph_profile.argtypes = [vp, ctypes.c_int]
@@ -189,7 +192,8 @@ def er_query_batch(g, pairs, eps: float, p_fail: float = 0.01):
 def er_query_batch_ex(g, pairs, eps: float, p_fail: float = 0.01, *, out=None, stats=None,
                       tau: int = 5, seed: int = ER_DEFAULT_SEED, query_index_base: int = 0,
                       force_ell_b: int = -1, ell_variant: int = 0, stream=None, synchronous: bool = True,
-                      k: int | None = None, query_ids=None, switch_ratio: float = 1.0, reuse_samples: bool = False):
+                      k: int | None = None, query_ids=None, switch_ratio: float = 1.0, reuse_samples: bool = False,
+                      smm_mode: int = 0):
     """Extended query.  ``pairs``/``out``/``stats`` are numpy arrays (host) or torch CUDA
     tensors (device); ``out``/``stats`` are allocated on the host when None.
     ``stats=True`` allocates a host STATS_DTYPE array.  Returns (out, stats)."""
@@ -223,6 +227,7 @@ def er_query_batch_ex(g, pairs, eps: float, p_fail: float = 0.01, *, out=None, s
     o.synchronous = int(synchronous)
     o.switch_ratio = float(switch_ratio)
     o.reuse_samples = int(bool(reuse_samples))
+    o.smm_mode = int(smm_mode)
     if query_ids is not None:
         if hasattr(query_ids, "data_ptr"):
             if bool(query_ids.is_cuda) != bool(pdev):
@@ -250,14 +255,24 @@ def _stream_handle(stream):
     return ctypes.c_void_p(h if h else 1)
 
 
-def er_spmm(g, X, Y, normalize: bool = True, stream=None) -> None:
-    """Y = P X (or A X) for row-major n x q device tensors (float64)."""
+ER_SPMM_NORMALIZE = 1
+ER_SPMM_EXACT = 2
+SMM_AUTO, SMM_FRONTIER, SMM_DENSE = 0, 1, 2   # er_opts.smm_mode
+
+
+def er_spmm(g, X, Y, normalize: bool = True, stream=None, exact: bool = False) -> None:
+    """Y = P X (or A X) for row-major n x q device tensors (float64).  ``exact``: every row
+    summed sequentially in CSR order (er_spmm_ex with ER_SPMM_EXACT)."""
     q = 1 if X.dim() == 1 else int(X.shape[1])
     if stream is None:   # order with torch's work on the tensors (their producers and readers)
         import torch
         stream = torch.cuda.current_stream(X.device)
     s = _stream_handle(stream)
-    _raise(lib.er_spmm(g, ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(Y.data_ptr()), q, int(normalize), s))
+    if exact:
+        flags = (ER_SPMM_NORMALIZE if normalize else 0) | ER_SPMM_EXACT
+        _raise(lib.er_spmm_ex(g, ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(Y.data_ptr()), q, flags, s))
+    else:
+        _raise(lib.er_spmm(g, ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(Y.data_ptr()), q, int(normalize), s))
 
 
 def er_smm_series(g, pairs, tol: float = 1e-10, max_iters: int = 100000):

@@ -198,6 +198,7 @@ void er_opts_default(er_opts *o)
     o->query_ids = nullptr;
     o->switch_ratio = 1.0;
     o->reuse_samples = 0;
+    o->smm_mode = 0;
 }
 
 er_graph *er_graph_create(int64_t n, const int64_t *offsets, const int32_t *cols)
@@ -284,6 +285,7 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_OVERLAP_FRAC")) g->overlap_frac = std::min(1.0, std::max(0.1, atof(env)));
         if (const char *env = getenv("GEER_MAX_SUB_BATCH")) g->max_sub_batch = std::max<int64_t>(1, atoll(env));
         if (const char *env = getenv("GEER_WALK_NP")) g->walk_np = atoi(env) == 1 ? 1 : 2;
+        if (const char *env = getenv("GEER_HUB_CB")) { const int v = atoi(env); g->hub_cb = (v == 8 || v == 16) ? v : 32; }
         if (const char *env = getenv("GEER_WALK_SMEM_KB")) g->walk_smem_words = 256 * std::min(48, std::max(8, atoi(env)));
         g->pack.bo = bo;
         g->pack.bd = bd;
@@ -355,6 +357,12 @@ void er_graph_destroy(er_graph *g)
         }
         if (g->ev_in) cudaEventDestroy(g->ev_in);
         if (g->ev_out) cudaEventDestroy(g->ev_out);
+        if (g->spmm_stream) {
+            cudaStreamSynchronize(g->spmm_stream);
+            cudaStreamDestroy(g->spmm_stream);
+            cudaEventDestroy(g->spmm_fork);
+            cudaEventDestroy(g->spmm_join);
+        }
         cudaSetDevice(cur);
     }
     delete g;
@@ -404,6 +412,7 @@ int er_query_batch_ex(er_graph *g, const int32_t *pairs, int64_t k, double eps, 
     if (opt.force_ell_b < -1) { set_error(ER_EINVAL, "force_ell_b must be >= -1"); return ER_EINVAL; }
     if (!(opt.switch_ratio >= 0.0) || !std::isfinite(opt.switch_ratio)) { set_error(ER_EINVAL, "switch_ratio must be >= 0"); return ER_EINVAL; }
     if (opt.reuse_samples != 0 && opt.reuse_samples != 1) { set_error(ER_EINVAL, "reuse_samples must be 0 or 1"); return ER_EINVAL; }
+    if (opt.smm_mode < 0 || opt.smm_mode > 2) { set_error(ER_EINVAL, "smm_mode must be 0, 1 or 2"); return ER_EINVAL; }
     if (opt.query_index_base < 0 || opt.query_index_base + k > ((int64_t)1 << 32)) {
         set_error(ER_EINVAL, "query indices must fit in 32 bits");
         return ER_EINVAL;
@@ -452,13 +461,20 @@ int er_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, dou
     return er_query_batch_ex(g, pairs, k, eps, p_fail, nullptr, out_r, nullptr);
 }
 
-int er_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, void *stream)
+int er_spmm_ex(er_graph *g, const double *X, double *Y, int32_t q, int32_t flags, void *stream)
 {
     clear_error();
     if (!g || !X || !Y || X == Y) { set_error(ER_EINVAL, "bad arguments"); return ER_EINVAL; }
     if (q < 1 || q > 256) { set_error(ER_EINVAL, "q must be in [1,256]"); return ER_EINVAL; }
+    if (flags & ~(ER_SPMM_NORMALIZE | ER_SPMM_EXACT)) { set_error(ER_EINVAL, "unknown flags"); return ER_EINVAL; }
     std::lock_guard<std::mutex> lk(g->mu);
-    return run_spmm(g, X, Y, q, normalize, stream ? (cudaStream_t)stream : g->stream);
+    return run_spmm(g, X, Y, q, (flags & ER_SPMM_NORMALIZE) ? 1 : 0, stream ? (cudaStream_t)stream : g->stream,
+                    (flags & ER_SPMM_EXACT) != 0);
+}
+
+int er_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, void *stream)
+{
+    return er_spmm_ex(g, X, Y, q, normalize ? ER_SPMM_NORMALIZE : 0, stream);
 }
 
 int er_smm_series(er_graph *g, const int32_t *pairs, int64_t k, double tol, int32_t max_iters, double *out_r,

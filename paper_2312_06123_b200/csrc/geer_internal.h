@@ -111,6 +111,7 @@ struct Workspace {
     DevBuf cub_tmp;                                 // CUB temp storage
     DevBuf scalars;                                 // small device scalars
     DevBuf spmm_part;                               // K9 heavy-row segment sums
+    DevBuf dense_x, dense_y, dense_cnt;             // SMM dense mode: n x q blocks, per-tile counts
     DevBuf qids;                                    // device copy of er_opts.query_ids
     std::vector<DevBuf> ychunk;                     // y-tables of each SMM wave (grow-only, kept)
     DevBuf ids, seglen, segbeg;                     // 0..k-1 ids; compaction lengths; sort segments
@@ -163,6 +164,9 @@ struct er_graph {
     int64_t *d_hseg = nullptr;     // K9: first segment of each heavy row (n_heavy + 1)
     int64_t *d_seg_e0 = nullptr;   // K9: first arc of each segment
     int32_t *d_seg_row = nullptr;  // K9: row of each segment
+    int hub_cb = 32;                     // K9 exact: columns per heavy-row CTA (GEER_HUB_CB 8/16/32)
+    cudaStream_t spmm_stream = nullptr;  // K9 exact: heavy rows concurrent with the light rows
+    cudaEvent_t spmm_fork = nullptr, spmm_join = nullptr;
     geer::Workspace ws;
 };
 
@@ -174,7 +178,9 @@ int cuda_fail(cudaError_t e, const char *what);
 // Pipeline entry (pipeline.cu).
 int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, double p_fail,
                     const er_opts &o, double *out_r, er_query_stats *stats);
-int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st);
+// K9: Y = M X (spmm.cu).  exact = every row summed sequentially in CSR order (heavy rows too).
+int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st,
+             bool exact = false);
 int run_smm_series(er_graph *g, const int32_t *pairs, int64_t k, double tol, int32_t max_iters, double *out_r,
                    int32_t *ells);
 int run_estimate_lambda(er_graph *g, int iters, double *lambda_out);

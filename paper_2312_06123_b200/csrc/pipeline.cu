@@ -539,7 +539,7 @@ void Workspace::release()
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2,
                      &runidx, &runstart, &segstat, &ycap, &yoff, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &cont2,
-                     &idx2, &spmm_part, &qids};
+                     &idx2, &spmm_part, &qids, &dense_x, &dense_y, &dense_cnt};
     for (DevBuf *b : all) b->release();
     for (DevBuf &b : ychunk) b.release();
     ychunk.clear();
@@ -838,9 +838,22 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             ENSURE(ws.scalars, sizeof(int64_t) * 8, false);
             int64_t *dU = ws.scalars.as<int64_t>();
             const bool fast_first = first_wave && g->rows_sorted;
+            // push (K2/K3) or dense pull (K9) for this wave (er_opts.smm_mode, R25)
+            bool dense = false;
+            if (!fast_first && o.smm_mode != 1 && na <= ER_DENSE_MAX_QUERIES &&
+                2.0 * 8.0 * (double)g->n * (double)(2 * na) <= DENSE_MAX_BYTES)
+                dense = o.smm_mode == 2 || dense_wave_pays(g, (int32_t)na, E);
+            if (prof && !fast_first) {
+                g->prof.smm_waves++;
+                if (dense) {
+                    g->prof.smm_dense_waves++;
+                    g->prof.smm_dense_cols += 2 * na;
+                }
+            }
+            if (dense) smm_pairs -= E;   // no push pairs
             int32_t *segbeg = nullptr;
             int one_chunk = 0;
-            if (!fast_first) {
+            if (!fast_first && !dense) {
                 ENSURE(ws.segbeg, sizeof(int32_t) * (nseg + 1), false);
                 segbeg = ws.segbeg.as<int32_t>();
                 k_segbeg<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, ws.fr_off.as<int64_t>(), ent_off, segbeg);
@@ -855,13 +868,15 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             ENSURE(ws.nf_off, sizeof(int64_t) * (nseg + 1), false);
             ENSURE(ws.segstat, sizeof(SegStat) * nseg, false);
             CK(cudaMemsetAsync(ws.segstat.p, 0, sizeof(SegStat) * nseg, st));
-            if (fast_first) {
+            if (dense) {
+                rc = smm_dense_wave(c, (int32_t)na, F, ws.act.as<int32_t>(), dU);
+                if (rc) return rc;
+            } else if (fast_first) {
                 k_first_wave<<<blocks_for(E, 256), 256, 0, st>>>(E, nseg, ent_off, ws.fr_id.as<int32_t>(), g->d_off,
                                                                  g->d_rec, g->d_cols, ws.act.as<int32_t>(), qs,
                                                                  ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                                                                  ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>(), dU);
-            } else
-            if (P.nbits <= 24)
+            } else if (P.nbits <= 24)
                 k_run_reduce<uint32_t><<<blocks_for(E, 256), 256, 0, st>>>(
                     E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint32_t>(), P.nbits, one_chunk, ws.vals2.as<double>(), segbeg,
                     nseg, g->d_rec, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
@@ -871,7 +886,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                     E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint64_t>(), P.nbits, one_chunk, ws.vals2.as<double>(), segbeg,
                     nseg, g->d_rec, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                     ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>());
-            LAUNCHED(g);
+            if (!dense) LAUNCHED(g);
             k_seg_max2<<<blocks_for(E, 256), 256, 0, st>>>(E, dU, ws.nf_seg.as<int32_t>(), ws.nf_val.as<double>(),
                                                            ws.segstat.as<SegStat>());
             LAUNCHED(g);

@@ -11,7 +11,9 @@
 // (oracle_propagate_dense); a longer row is cut into consecutive segments of SPMM_SEG
 // neighbours, each summed sequentially, and the segment sums are then added sequentially in
 // segment order (a fixed order: run-to-run bit-reproducible, within a few ulps of the plain
-// sequential sum).
+// sequential sum).  The EXACT variant (the SMM head's dense mode, and er_spmm_ex) sums every
+// row sequentially in CSR order: a heavy row gets a CTA that gathers chunks of its neighbours'
+// X rows into shared memory in parallel and one thread per column adds them in order.
 //
 // Layout and load balance ("K9"):
 //  * once per graph, the work items are built: one per heavy-row segment, then one per light
@@ -133,6 +135,129 @@ __global__ void k_spmm_heavy_sum(int64_t nheavy, const int32_t *__restrict__ row
     Y[(int64_t)v * q + c] = normalize ? acc / (double)(off[v + 1] - off[v]) : acc;
 }
 
+// EXACT heavy rows.  CTA (heavy row v, block of HUB_CB columns): v's neighbours are streamed in
+// chunks of HUB_ROWS rows through a HUB_STAGES-deep ring of shared-memory stages filled by
+// cp.async (LDGSTS, 16-byte copies of the X row segments when VEC = 2); thread c < w adds column
+// c's values sequentially in CSR order (R13) while the next stages are in flight, so Y is the
+// plain sequential sum and the copies overlap the dependent add chain.  Column blocks of one row
+// run on different SMs (the chain of a column cannot be split without changing the order).
+constexpr int HUB_STAGE = 4096;     // doubles per stage (32 KB)
+constexpr int HUB_STAGES = 3;       // ring depth (96 KB)
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *dst, const void *src)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    if (BYTES == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Stage layout: HUB_ROWS rows of HUB_CB doubles (columns cb .. cb + w - 1 used).  Thread t
+// copies vector k = t % LPR of rows j = t / LPR + i RPI (all index math compile-time); the rows'
+// neighbour ids are loaded one chunk ahead into registers, so issuing a chunk never waits on a
+// cols load.
+template <int VEC, int HUB_CB>
+struct HubChunk {
+    static constexpr int HUB_ROWS = HUB_STAGE / HUB_CB;  // rows per chunk
+    static constexpr int LPR = HUB_CB / VEC;            // threads per row
+    static constexpr int RPI = SPMM_THREADS / LPR;      // rows per pass
+    static constexpr int PER = HUB_ROWS / RPI;          // passes (copies per thread) per chunk
+    int32_t u[PER];
+    __device__ __forceinline__ void load(const int32_t *__restrict__ cols, int64_t r0, int32_t m)
+    {
+#pragma unroll
+        for (int p = 0; p < PER; p++) {
+            const int32_t j = (int32_t)threadIdx.x / LPR + p * RPI;
+            u[p] = j < m ? __ldg(cols + r0 + j) : 0;
+        }
+    }
+    __device__ __forceinline__ void issue(double *dst, const double *__restrict__ X, int32_t q, int32_t cb, int32_t m,
+                                          int32_t wv)
+    {
+        const int32_t k = (int32_t)threadIdx.x % LPR;
+        if (k >= wv) return;
+#pragma unroll
+        for (int p = 0; p < PER; p++) {
+            const int32_t j = (int32_t)threadIdx.x / LPR + p * RPI;
+            if (j < m) cp_async<8 * VEC>(dst + j * HUB_CB + k * VEC, X + (int64_t)u[p] * q + cb + k * VEC);
+        }
+    }
+};
+
+template <int VEC, int HUB_CB>
+__global__ void __launch_bounds__(SPMM_THREADS)
+k_spmm_hub_exact(const int32_t *__restrict__ rows, const int64_t *__restrict__ off, const int32_t *__restrict__ cols,
+                 const double *__restrict__ X, double *__restrict__ Y, int32_t q, int normalize)
+{
+    constexpr int HUB_ROWS = HubChunk<VEC, HUB_CB>::HUB_ROWS;
+    extern __shared__ __align__(16) double hub_sm[];
+    const int32_t v = rows[blockIdx.x];
+    const int32_t cb = blockIdx.y * HUB_CB;
+    const int32_t w = min(HUB_CB, q - cb);
+    const int32_t wv = w / VEC;
+    const int64_t e0 = off[v], e1 = off[v + 1];
+    const int64_t nch = (e1 - e0 + HUB_ROWS - 1) / HUB_ROWS;
+    auto rows_of = [&](int64_t c) { return c < nch ? (int32_t)min((int64_t)HUB_ROWS, e1 - (e0 + c * HUB_ROWS)) : 0; };
+    HubChunk<VEC, HUB_CB> hc;
+    // prologue: chunks 0 .. HUB_STAGES-2 in flight, ids of chunk HUB_STAGES-1 in registers
+#pragma unroll 1
+    for (int c = 0; c < HUB_STAGES - 1; c++) {
+        hc.load(cols, e0 + (int64_t)c * HUB_ROWS, rows_of(c));
+        hc.issue(hub_sm + c * HUB_STAGE, X, q, cb, rows_of(c), wv);
+        cp_async_commit();
+    }
+    hc.load(cols, e0 + (int64_t)(HUB_STAGES - 1) * HUB_ROWS, rows_of(HUB_STAGES - 1));
+    double acc = 0.0;
+    for (int64_t c = 0; c < nch; c++) {
+        const int64_t cn = c + HUB_STAGES - 1;   // chunk whose copies start now
+        hc.issue(hub_sm + (cn % HUB_STAGES) * HUB_STAGE, X, q, cb, rows_of(cn), wv);
+        cp_async_commit();   // one group per chunk (possibly empty): uniform group counting
+        hc.load(cols, e0 + (cn + 1) * HUB_ROWS, rows_of(cn + 1));
+        cp_async_wait<HUB_STAGES - 1>();   // this thread's copies of chunk c have landed
+        __syncthreads();                   // ... and everyone's
+        if ((int32_t)threadIdx.x < w) {
+            const double *col = hub_sm + (c % HUB_STAGES) * HUB_STAGE + threadIdx.x;
+            const int32_t m = rows_of(c);
+            // software-pipelined: the next 8 values are loaded while the current 8 are added,
+            // so the loop runs at the latency of the dependent DADD chain
+            int32_t j = 0;
+            if (m >= 8) {
+                double t[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) t[i] = col[i * HUB_CB];
+                for (j = 8; j + 8 <= m; j += 8) {
+                    double u[8];
+#pragma unroll
+                    for (int i = 0; i < 8; i++) u[i] = col[(j + i) * HUB_CB];
+#pragma unroll
+                    for (int i = 0; i < 8; i++) acc += t[i];   // CSR order
+#pragma unroll
+                    for (int i = 0; i < 8; i++) t[i] = u[i];
+                }
+#pragma unroll
+                for (int i = 0; i < 8; i++) acc += t[i];
+            }
+            for (; j < m; j++) acc += col[j * HUB_CB];
+        }
+        __syncthreads();                   // stage c is refilled by the next iteration's issue
+    }
+    cp_async_wait<0>();
+    if ((int32_t)threadIdx.x < w) Y[(int64_t)v * q + cb + threadIdx.x] = normalize ? acc / (double)(e1 - e0) : acc;
+}
+
+// Heavy row h: number of SPMM_SEG segments.
+__global__ void k_hseg_count(int64_t nheavy, const int32_t *__restrict__ rows, const int64_t *__restrict__ off,
+                             int64_t *__restrict__ cnt)
+{
+    const int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= nheavy) return;
+    const int32_t v = rows[h];
+    cnt[h] = (off[v + 1] - off[v] + SPMM_SEG - 1) / SPMM_SEG;
+}
+
 __global__ void k_deg_key(int64_t n, const int64_t *__restrict__ off, uint32_t *__restrict__ key,
                           int32_t *__restrict__ ids)
 {
@@ -202,20 +327,26 @@ int build_spmm_plan(er_graph *g, cudaStream_t st)
     g->n_heavy = nh;
     g->n_seg = 0;
     if (nh > 0) {
-        std::vector<int32_t> hrows(nh);
-        CK(cudaMemcpy(hrows.data(), g->d_rowperm, sizeof(int32_t) * nh, cudaMemcpyDeviceToHost));
-        std::vector<int64_t> hseg(nh + 1, 0);
-        for (int64_t h = 0; h < nh; h++) {
-            int64_t o[2];
-            CK(cudaMemcpy(o, g->d_off + hrows[h], 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
-            hseg[h + 1] = hseg[h] + (o[1] - o[0] + SPMM_SEG - 1) / SPMM_SEG;
-        }
-        const int64_t ns = hseg[nh];
-        g->n_seg = ns;
+        // hseg = exclusive prefix of the heavy rows' segment counts (on the device)
+        int64_t *cnt = nullptr;
         CK(cudaMalloc(&g->d_hseg, sizeof(int64_t) * (nh + 1)));
+        CK(cudaMallocAsync((void **)&cnt, sizeof(int64_t) * nh, st));
+        k_hseg_count<<<blocks_for(nh, 256), 256, 0, st>>>(nh, g->d_rowperm, g->d_off, cnt);
+        g->launches++;
+        size_t sb = 0;
+        CK(cub::DeviceScan::InclusiveSum(nullptr, sb, cnt, g->d_hseg + 1, (int)nh, st));
+        CK(cudaMallocAsync(&tmp, sb + 16, st));
+        CK(cudaMemsetAsync(g->d_hseg, 0, sizeof(int64_t), st));
+        CK(cub::DeviceScan::InclusiveSum(tmp, sb, cnt, g->d_hseg + 1, (int)nh, st));
+        g->launches += 2;
+        CK(cudaFreeAsync(tmp, st));
+        CK(cudaFreeAsync(cnt, st));
+        int64_t ns = 0;
+        CK(cudaMemcpyAsync(&ns, g->d_hseg + nh, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        g->n_seg = ns;
         CK(cudaMalloc(&g->d_seg_e0, sizeof(int64_t) * ns));
         CK(cudaMalloc(&g->d_seg_row, sizeof(int32_t) * ns));
-        CK(cudaMemcpy(g->d_hseg, hseg.data(), sizeof(int64_t) * (nh + 1), cudaMemcpyHostToDevice));
         k_fill_segs<<<blocks_for(nh, 128), 128, 0, st>>>(nh, g->d_rowperm, g->d_hseg, g->d_off, g->d_seg_e0,
                                                          g->d_seg_row);
         g->launches++;
@@ -224,16 +355,20 @@ int build_spmm_plan(er_graph *g, cudaStream_t st)
     return ER_OK;
 }
 
+// Light rows (and, unless exact, the heavy-row segments) through k_spmm_rows.
 template <int VEC>
-void launch_rows(er_graph *g, const double *X, double *Y, double *part, int32_t q, int normalize, cudaStream_t st)
+void launch_rows(er_graph *g, const double *X, double *Y, double *part, int32_t q, int normalize, bool exact,
+                 cudaStream_t st)
 {
     const int nvec = q / VEC;
     int lpr = 1;
     while (lpr < nvec && lpr < 32) lpr <<= 1;
-    const int64_t nitems = g->n_seg + (g->n - g->n_heavy);
+    const int64_t nseg = exact ? 0 : g->n_seg;
+    const int64_t nitems = nseg + (g->n - g->n_heavy);
+    if (nitems == 0) return;
     const unsigned grid = blocks_for(nitems * lpr, SPMM_THREADS);
 #define L(LPR)                                                                                               \
-    k_spmm_rows<LPR, VEC><<<grid, SPMM_THREADS, 0, st>>>(g->n_seg, nitems, g->d_seg_e0, g->d_seg_row,          \
+    k_spmm_rows<LPR, VEC><<<grid, SPMM_THREADS, 0, st>>>(nseg, nitems, g->d_seg_e0, g->d_seg_row,              \
                                                          g->d_rowperm + g->n_heavy, g->d_off, g->d_cols, X, Y, \
                                                          part, q, normalize)
     switch (lpr) {
@@ -250,7 +385,7 @@ void launch_rows(er_graph *g, const double *X, double *Y, double *part, int32_t 
 
 }  // namespace
 
-int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st)
+int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st, bool exact)
 {
     if (!g->d_rowperm) {
         const int rc = build_spmm_plan(g, g->stream);
@@ -258,17 +393,49 @@ int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normali
     }
     const bool vec2 = (q % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) % 16 == 0);
     double *part = nullptr;
-    if (g->n_seg > 0) {
+    if (!exact && g->n_seg > 0) {
         CK(g->ws.spmm_part.ensure(sizeof(double) * (size_t)g->n_seg * q, false, st));
         part = g->ws.spmm_part.as<double>();
     }
-    if (vec2) launch_rows<2>(g, X, Y, part, q, normalize, st);
-    else launch_rows<1>(g, X, Y, part, q, normalize, st);
-    if (g->n_heavy > 0) {
+    if (exact && g->n_heavy > 0) {
+        // heavy rows on a forked stream, concurrent with the light rows (their longest chains
+        // would otherwise be the kernel's tail)
+        if (!g->spmm_stream) {
+            CK(cudaStreamCreateWithFlags(&g->spmm_stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&g->spmm_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&g->spmm_join, cudaEventDisableTiming));
+        }
+        CK(cudaEventRecord(g->spmm_fork, st));
+        CK(cudaStreamWaitEvent(g->spmm_stream, g->spmm_fork, 0));
+        const size_t smem = sizeof(double) * HUB_STAGE * HUB_STAGES;
+#define HUB(VEC, CB)                                                                                          \
+    do {                                                                                                      \
+        const dim3 grid((unsigned)g->n_heavy, (unsigned)((q + CB - 1) / CB));                                 \
+        CK(cudaFuncSetAttribute(k_spmm_hub_exact<VEC, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        k_spmm_hub_exact<VEC, CB><<<grid, SPMM_THREADS, smem, g->spmm_stream>>>(g->d_rowperm, g->d_off, g->d_cols, \
+                                                                               X, Y, q, normalize);        \
+    } while (0)
+        if (vec2) {
+            if (g->hub_cb == 32) HUB(2, 32);
+            else if (g->hub_cb == 16) HUB(2, 16);
+            else HUB(2, 8);
+        } else {
+            if (g->hub_cb == 32) HUB(1, 32);
+            else if (g->hub_cb == 16) HUB(1, 16);
+            else HUB(1, 8);
+        }
+#undef HUB
+        g->launches++;
+        CK(cudaEventRecord(g->spmm_join, g->spmm_stream));
+    }
+    if (vec2) launch_rows<2>(g, X, Y, part, q, normalize, exact, st);
+    else launch_rows<1>(g, X, Y, part, q, normalize, exact, st);
+    if (!exact && g->n_heavy > 0) {
         k_spmm_heavy_sum<<<blocks_for(g->n_heavy * q, 256), 256, 0, st>>>(g->n_heavy, g->d_rowperm, g->d_hseg,
                                                                           g->d_off, part, Y, q, normalize);
         g->launches++;
     }
+    if (exact && g->n_heavy > 0) CK(cudaStreamWaitEvent(st, g->spmm_join, 0));
     CK(cudaGetLastError());
     return ER_OK;
 }

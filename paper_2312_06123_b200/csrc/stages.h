@@ -112,6 +112,15 @@ int build_ytables(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, c
                   const int32_t *id, const double *val, const int32_t *seg, int64_t Fmax, const int64_t *dF,
                   int wave);
 
+// SMM dense mode (dense.cu): whether a wave of na queries emitting E push pairs runs dense, and
+// the wave itself: frontier (ws.fr_*) -> next frontier (ws.nf_*, sized >= E by the caller) with
+// the K4a statistics in ws.segstat (zeroed by the caller) and the entry count at *dU (device).
+constexpr double DENSE_PUSH_NS_PER_PAIR = 0.1;   // measured push cost per emitted pair
+constexpr double DENSE_BYTES_PER_NS = 2500.0;    // effective bandwidth of a dense wave (conservative)
+constexpr double DENSE_MAX_BYTES = 16.0 * (1ull << 30);   // X + Y blocks
+bool dense_wave_pays(const er_graph *g, int32_t na, int64_t E);
+int smm_dense_wave(Ctx &c, int32_t na, int64_t F, const int32_t *act, int64_t *dU);
+
 // K6 + K7 (walks.cu).  One AMC group: the queries that left the SMM head in the same wave, with
 // their y-tables.  Its whole AMC (tau batches) is enqueued on stream sb without host sync.
 struct AmcGroup {

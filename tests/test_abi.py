@@ -59,6 +59,9 @@ int main(void) {
   printf("opts %zu\n", sizeof(er_opts));
   O(er_opts, seed); O(er_opts, query_index_base); O(er_opts, cuda_stream);
   O(er_opts, pairs_on_device); O(er_opts, synchronous); O(er_opts, query_ids);
+  O(er_opts, switch_ratio); O(er_opts, reuse_samples); O(er_opts, smm_mode);
+  printf("profile %zu\n", sizeof(er_profile));
+  O(er_profile, walk_ctas_per_sm); O(er_profile, smm_dense_waves);
   return 0;
 }''')
     exe = tmp_path / "layout"
@@ -71,8 +74,12 @@ int main(void) {
         assert vals[f] == d.fields[f][1], f
     o = G.er_opts
     assert vals["opts"] == ctypes.sizeof(o)
-    for f in ("seed", "query_index_base", "cuda_stream", "pairs_on_device", "synchronous", "query_ids"):
+    for f in ("seed", "query_index_base", "cuda_stream", "pairs_on_device", "synchronous", "query_ids",
+              "switch_ratio", "reuse_samples", "smm_mode"):
         assert vals[f] == getattr(o, f).offset, f
+    assert vals["profile"] == ctypes.sizeof(G.er_profile)
+    for f in ("walk_ctas_per_sm", "smm_dense_waves"):
+        assert vals[f] == getattr(G.er_profile, f).offset, f
 
 
 def test_defaults(G):
@@ -118,6 +125,7 @@ def test_null_handle_errors(G):
     assert G.lib.er_smm_series(None, p.ctypes.data_as(ctypes.c_void_p), 1, 1e-8, 10,
                                r.ctypes.data_as(ctypes.c_void_p), None) == G.ER_EINVAL
     assert G.lib.er_spmm(None, None, None, 4, 1, None) == G.ER_EINVAL
+    assert G.lib.er_spmm_ex(None, None, None, 4, G.ER_SPMM_EXACT, None) == G.ER_EINVAL
     assert G.lib.er_graph_estimate_lambda(None, 0, None) == G.ER_EINVAL
     assert G.er_last_error() == G.ER_EINVAL and "NULL" in G.er_last_error_message()
 
@@ -126,4 +134,4 @@ def test_opts_validation_without_device(G):
     """Option checks happen before any device work (a NULL graph is reported first; the
     option ranges are covered on the GPU by the parity tests)."""
     o = G.er_opts_default()
-    assert o.switch_ratio == 1.0 and o.reuse_samples == 0 and not o.query_ids
+    assert o.switch_ratio == 1.0 and o.reuse_samples == 0 and not o.query_ids and o.smm_mode == G.SMM_AUTO
