@@ -188,6 +188,7 @@ def config_dict(g, args):
             "parallelism": f"queries sharded over {args.gpus} GPU(s), CSR replicated",
             "l2": "flushed between steps (256 MiB device write outside the timed events)",
             "switch_ratio": args.switch_ratio,
+            "smm_mode": {0: "auto (cost model)", 1: "frontier push", 2: "dense pull"}[args.smm_mode],
             "seeds": {"graph": getattr(args, "graph_seed", 20231211), "queries": "graph seed + 1 + rank",
                       "walks": "0x2312061232DEC0DE"}}
 
@@ -232,6 +233,8 @@ def main():
     ap.add_argument("--no-spmm", action="store_true")
     ap.add_argument("--switch-ratio", type=float, default=1.0,
                     help="variant knob (DESIGN R22): leave the SMM head iff vol > ratio * h; 1.0 = Eq. 15")
+    ap.add_argument("--smm-mode", type=int, default=0, choices=[0, 1, 2],
+                    help="SMM head: 0 per-wave cost model (default), 1 push only, 2 dense pull (R25)")
     ap.add_argument("--config", default=CONFIG, help="workload (BASELINE configs[1] = rmat20 is the graded line)")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -277,7 +280,7 @@ def main():
 
     def step():
         G.er_query_batch_ex(h, pairs_d, args.eps, 0.01, out=out_d, stream=st, query_index_base=lo,
-                            switch_ratio=args.switch_ratio)
+                            switch_ratio=args.switch_ratio, smm_mode=args.smm_mode)
         if dist:
             with torch.cuda.stream(st):
                 gather_results(out_d, nq * world)
@@ -330,7 +333,8 @@ def main():
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
-        r = G.er_query_batch_ex(h, host_pairs, args.eps, 0.01, query_index_base=lo, switch_ratio=args.switch_ratio)[0]
+        r = G.er_query_batch_ex(h, host_pairs, args.eps, 0.01, query_index_base=lo,
+                                switch_ratio=args.switch_ratio, smm_mode=args.smm_mode)[0]
         if dist:
             gather_results(torch.from_numpy(r).cuda(), nq * world).cpu()
         e2e_times.append(time.perf_counter() - t0)
@@ -365,7 +369,9 @@ def main():
                                    "walk_steps_per_step": prof["walk_steps"] / args.steps,
                                    "ytable_slots_per_step": prof["ytable_slots"] / args.steps,
                                    "yrank_records_per_step": prof["yrank_records"] / args.steps,
-                                   "walk_ctas_per_sm": prof["walk_ctas_per_sm"]},
+                                   "walk_ctas_per_sm": prof["walk_ctas_per_sm"],
+                                   "smm_waves_per_step": prof["smm_waves"] / args.steps,
+                                   "smm_dense_waves_per_step": prof["smm_dense_waves"] / args.steps},
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(pairs.nbytes),
                     "d2h_bytes_per_step": int(nq * 8)},
             "gpu_launches": int(launches),
@@ -391,7 +397,8 @@ def main():
             t0 = time.perf_counter()
             truth, ells = G.er_smm_series(h, sub, tol=1e-8)
             t_truth = time.perf_counter() - t0
-            est = G.er_query_batch_ex(h, sub, args.eps, 0.01, query_index_base=lo, switch_ratio=args.switch_ratio)[0]
+            est = G.er_query_batch_ex(h, sub, args.eps, 0.01, query_index_base=lo,
+                                      switch_ratio=args.switch_ratio, smm_mode=args.smm_mode)[0]
             err = np.abs(est - truth)
             line["accuracy"] = {"queries": int(len(sub)), "eps": args.eps, "max_abs_err": float(err.max()),
                                 "mean_abs_err": float(err.mean()), "frac_within_eps": float(np.mean(err <= args.eps)),
