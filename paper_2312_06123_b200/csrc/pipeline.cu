@@ -917,13 +917,15 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             CK(cudaMemcpyAsync(c.hp + 2, th, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(c.hp + 3, tv, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(c.hp + 4, tr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(c.hp + 5, dU, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             const int64_t na2 = (int64_t)(*reinterpret_cast<int32_t *>(c.hp + 0));
             const int64_t F2 = c.hp[1];
             const int64_t YH = c.hp[2], YV = c.hp[3], YR = c.hp[4];
+            const int64_t U = c.hp[5];   // next-frontier entries (<= E): the grid of the passes below
             // y-tables, then (overlap) their AMC on the AMC stream
             rc = ytable_build(c, (int32_t)na, ws.act.as<int32_t>(), ws.nf_off.as<int64_t>(), ws.nf_id.as<int32_t>(),
-                              ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), E, dU, 1 + wave_no, YH, YV, YR);
+                              ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), U, dU, 1 + wave_no, YH, YV, YR);
             if (rc) return rc;
             rc = fork_group((int32_t)na, ws.act.as<int32_t>(), cont);
             if (rc) return rc;
@@ -932,8 +934,8 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                 ENSURE(ws.fr_val, sizeof(double) * F2, false);
                 ENSURE(ws.fr_seg, sizeof(int32_t) * F2, false);
                 ENSURE(ws.fr_off, sizeof(int64_t) * (2 * na2 + 1), false);
-                k_compact_entries<<<blocks_for(E, 256), 256, 0, st>>>(
-                    E, dU, ws.nf_seg.as<int32_t>(), ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
+                k_compact_entries<<<blocks_for(U, 256), 256, 0, st>>>(
+                    U, dU, ws.nf_seg.as<int32_t>(), ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                     ws.nf_off.as<int64_t>(), cont, newidx, segnew, seglen, ws.fr_id.as<int32_t>(),
                     ws.fr_val.as<double>(), ws.fr_seg.as<int32_t>());
                 LAUNCHED(g);
