@@ -141,8 +141,10 @@ typedef struct er_opts {
                                   the dense block pull (K9, exact sequential sums) when the wave's pushes
                                   would cost more than a full pass over the CSR for its columns;
                                   1 = frontier push only; 2 = dense pull whenever the wave has at most
-                                  ER_DENSE_MAX_QUERIES active queries.  All modes give bit-identical
-                                  results (R13, R25); only speed differs */
+                                  ER_DENSE_MAX_QUERIES active queries.  On graphs with sorted adjacency
+                                  lists all modes give bit-identical results; otherwise the push sums
+                                  in ascending source order and the pull in CSR order (within 1e-10
+                                  relative, R13, R25); only speed differs */
 } er_opts;
 
 /* Dense-mode limit: a wave runs dense only with <= this many active queries (2 columns each). */

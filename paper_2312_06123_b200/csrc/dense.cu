@@ -7,9 +7,10 @@
 //   extract   the nonzeros of each column g in ascending row order -> the next frontier segment
 //             g, exactly the layout K3 produces, with the K4a statistics (vol, max1, x(s), x(t))
 //
-// Bit-identical to the push: x >= 0, so the pull's extra terms are exact zeros (0.0 + a = a,
-// a + 0.0 = a), its nonzero terms arrive in ascending source order like K3's runs, and the
-// support is the set of nonzero sums (R13).
+// Bit-identical to the push on sorted adjacency lists: x >= 0, so the pull's extra terms are
+// exact zeros (0.0 + a = a, a + 0.0 = a), its nonzero terms arrive in CSR = ascending source
+// order like K3's runs, and the support is the set of nonzero sums (R13).  On unsorted lists the
+// pull keeps CSR order (the oracle's), the push ascending source order.
 
 #include <algorithm>
 

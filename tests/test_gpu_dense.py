@@ -124,6 +124,29 @@ def test_rmat20_cost_model_picks_dense_for_dense_supports(geer, rmat20):
     assert r0.tobytes() == r1.tobytes() and s0.tobytes() == s1.tobytes()
 
 
+def test_unsorted_rows_dense_mode_matches_oracle_order(geer, tiny):
+    """Adjacency rows in random order: the push sums in ascending source order (within 1e-10 of
+    the oracle, R13) but the dense pull sums in CSR order -- the oracle's order -- so with
+    smm_mode = dense r_b and psi are bit-identical to the oracle even here."""
+    g0, pairs = tiny
+    rng = np.random.default_rng(9)
+    cols = g0.cols.copy()
+    for v in range(g0.n):
+        a, b = g0.offsets[v], g0.offsets[v + 1]
+        cols[a:b] = rng.permutation(cols[a:b])
+    g = W.Graph(g0.n, g0.offsets.copy(), cols, "tiny_shuffled", g0.lam)
+    h = geer.er_graph_create(g.n, g.offsets, g.cols)
+    try:
+        geer.er_graph_set_lambda(h, g.lam)
+        for kw in ({}, dict(force_ell_b=4)):
+            r, st, ro, so = run_both(geer, h, g, pairs, 0.1, smm_mode=geer.SMM_DENSE, **kw)
+            compare(g, pairs, r, st, ro, so, sorted_adj=True)
+            r1, st1, _, _ = run_both(geer, h, g, pairs, 0.1, smm_mode=geer.SMM_FRONTIER, **kw)
+            compare(g, pairs, r1, st1, ro, so, sorted_adj=False)
+    finally:
+        geer.er_graph_destroy(h)
+
+
 def test_dense_mode_limits(geer, tiny):
     """More than ER_DENSE_MAX_QUERIES active queries: the wave falls back to the push (same
     bits); an invalid smm_mode is rejected."""
