@@ -100,15 +100,35 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def ncu_traffic_per_step():
-    """dram bytes per walk step of K6 from the committed ncu --set full summary, if any."""
+def ncu_walk_summary():
+    """K6's committed ncu --set full summary (captured on BASELINE config 1), if any."""
     for p in sorted((ROOT / "profiles").glob("ncu_k_walks_*.json"), reverse=True):
         try:
-            d = json.loads(p.read_text())
-            return float(d["dram_bytes_per_walk_step"]), p.name
+            return json.loads(p.read_text()), p.name
         except Exception:
             continue
     return None, None
+
+
+def random_access_ceiling(mb):
+    """Measured dependent random 8-byte load rate (G loads/s) for a working set of `mb` MB
+    (profiles/l2_ubench_r01.txt, scripts/l2_ubench.cu), linearly interpolated."""
+    pts = []
+    for p in sorted((ROOT / "profiles").glob("l2_ubench_*.txt"), reverse=True):
+        for line in p.read_text().splitlines():
+            f = line.split()
+            if len(f) >= 3 and f[1] == "MB" and not line.startswith("#"):
+                pts.append((float(f[0]), float(f[2])))
+        break
+    if not pts:
+        return None
+    pts.sort()
+    if mb <= pts[0][0]:
+        return pts[0][1]
+    for (x0, y0), (x1, y1) in zip(pts, pts[1:]):
+        if mb <= x1:
+            return y0 + (y1 - y0) * (mb - x0) / (x1 - x0)
+    return pts[-1][1]
 
 
 def cpu_baseline_leg(g, lam, pairs, eps, target_s=10.0):
@@ -348,8 +368,21 @@ def main():
         walk_launch_ms = prof["walk_ms"] / max(prof["walk_launches"], 1)
         bytes_per_launch = WALK_BYTES_PER_STEP * prof["walk_steps"] / max(prof["walk_launches"], 1)
         achieved = bytes_per_launch / (walk_launch_ms / 1e3) / 1e9 if walk_launch_ms > 0 else 0.0
-        tps, tsrc = ncu_traffic_per_step()
+        ncu, tsrc = ncu_walk_summary() if args.config == CONFIG else (None, None)
+        tps = float(ncu["dram_bytes_per_walk_step"]) if ncu else None
         traffic = tps * prof["walk_steps"] / max(prof["walk_launches"], 1) if tps else None
+        # K6 is bound by dependent random loads into L2, not by HBM bandwidth: its L1->L2 load
+        # requests per second against the measured random-load ceiling for its arc working set
+        steps_s = prof["walk_steps"] / max(prof["walk_ms"] / 1e3, 1e-12)
+        arc_mb = 8.0 * float(g.offsets[-1]) / 2**20   # packed 8-byte arc records (config 1, as profiled)
+        ceil = random_access_ceiling(arc_mb)
+        rand = None
+        if ncu and ceil:
+            req = steps_s * float(ncu["l1_to_l2_sectors_per_walk_step"]) / 1e9
+            rand = {"achieved_g_requests_s": req, "ceiling_g_loads_s": ceil, "frac": req / ceil,
+                    "arc_working_set_mb": arc_mb, "walk_steps_per_s": steps_s,
+                    "l1_to_l2_sectors_per_step": float(ncu["l1_to_l2_sectors_per_walk_step"]),
+                    "source": f"{tsrc} + profiles/l2_ubench_r01.txt"}
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
@@ -357,7 +390,7 @@ def main():
             "config": config_dict(g, args),
             "roofline": {"bound": "hbm", "kernel": "k_walks (K6, AMC walks)", "achieved": achieved,
                          "peak": hbm, "peak_kind": how, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": traffic, "traffic_source": tsrc,
+                         "traffic": traffic, "traffic_source": tsrc, "random_access": rand,
                          "algorithmic_bytes_per_step": WALK_BYTES_PER_STEP,
                          "walk_steps_per_launch": prof["walk_steps"] / max(prof["walk_launches"], 1),
                          "avg_launch_ms": walk_launch_ms,
