@@ -108,6 +108,7 @@ struct Workspace {
     DevBuf runidx, runstart;                        // run-length reduction
     DevBuf segstat;                                 // SegStat per segment
     DevBuf ycap, yoff;                              // y-table sizes and their scans (per leaving query)
+    DevBuf ydesc;                                   // K5 build-time table descriptors (per leaving query)
     DevBuf cub_tmp;                                 // CUB temp storage
     DevBuf scalars;                                 // small device scalars
     DevBuf spmm_part;                               // K9 heavy-row segment sums

@@ -539,7 +539,7 @@ void Workspace::release()
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2,
                      &runidx, &runstart, &segstat, &ycap, &yoff, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &cont2,
-                     &idx2, &spmm_part, &qids, &dense_x, &dense_y, &dense_cnt};
+                     &idx2, &spmm_part, &qids, &dense_x, &dense_y, &dense_cnt, &ydesc};
     for (DevBuf *b : all) b->release();
     for (DevBuf &b : ychunk) b.release();
     ychunk.clear();

@@ -49,31 +49,60 @@ __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState
     rrecs[i] = r;
 }
 
+// Build-time descriptor of leaving query i's table (a compact copy of its QState y fields,
+// indexed by i: K5 reaches it in one load from the entry's segment).
+struct YDesc {
+    int32_t *keys;     // YT_HASH: 2^(lgb + YB_LOG) int32 keys
+    uint4 *rec;        // YT_RANK: walk records {U bits, rank U, rank T}
+    uint4 *aux;        // YT_RANK: build-time records {S bits, T bits}
+    double *vals;      // y values (by slot or by rank)
+    int32_t mode;      // -1: the query does not leave now; YT_HASH / YT_RANK
+    int32_t lgb;       // YT_HASH: log2 of the bucket count
+    int32_t ds, dt;    // d(s), d(t)
+};
+
 __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__ hslots,
                           const int64_t *__restrict__ hincl, const int64_t *__restrict__ vslots,
                           const int64_t *__restrict__ vincl, const int64_t *__restrict__ rrecs,
-                          const int64_t *__restrict__ rincl, const int32_t *kbase, const double *vbase,
-                          const uint4 *rbase, const uint4 *abase, QState *__restrict__ qs)
+                          const int64_t *__restrict__ rincl, int32_t *kbase, double *vbase, uint4 *rbase,
+                          uint4 *abase, QState *__restrict__ qs, YDesc *__restrict__ yd)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= na || vslots[i] == 0) return;
-    QState &Q = qs[act[i]];
-    Q.yvals = vbase + (vincl[i] - vslots[i]);
-    if (rrecs[i] > 0) {
-        Q.ymode = YT_RANK;
-        Q.yrec = rbase + (rincl[i] - rrecs[i]);
-        Q.yaux = abase + (rincl[i] - rrecs[i]);
-        Q.ykeys = nullptr;
-        Q.ylog2 = 0;
-    } else {
-        const int64_t cap = hslots[i];
-        Q.ymode = YT_HASH;
-        Q.ykeys = kbase + (hincl[i] - cap);
-        Q.yrec = nullptr;
-        int lg = 0;
-        while ((1ll << lg) < cap) lg++;
-        Q.ylog2 = lg;
+    if (i >= na) return;
+    YDesc D;
+    D.mode = -1;
+    D.keys = nullptr;
+    D.rec = D.aux = nullptr;
+    D.vals = nullptr;
+    D.lgb = 0;
+    D.ds = D.dt = 1;
+    if (vslots[i] != 0) {
+        QState &Q = qs[act[i]];
+        D.ds = Q.ds;
+        D.dt = Q.dt;
+        D.vals = vbase + (vincl[i] - vslots[i]);
+        Q.yvals = D.vals;
+        if (rrecs[i] > 0) {
+            D.mode = Q.ymode = YT_RANK;
+            D.rec = rbase + (rincl[i] - rrecs[i]);
+            D.aux = abase + (rincl[i] - rrecs[i]);
+            Q.yrec = D.rec;
+            Q.yaux = D.aux;
+            Q.ykeys = nullptr;
+            Q.ylog2 = 0;
+        } else {
+            const int64_t cap = hslots[i];
+            D.mode = Q.ymode = YT_HASH;
+            D.keys = kbase + (hincl[i] - cap);
+            Q.ykeys = D.keys;
+            Q.yrec = nullptr;
+            int lg = 0;
+            while ((1ll << lg) < cap) lg++;
+            Q.ylog2 = lg;
+            D.lgb = lg - YB_LOG;
+        }
     }
+    yd[i] = D;
 }
 
 __global__ void k_yfill(int64_t H, int32_t *__restrict__ keys, int64_t R, uint4 *__restrict__ aux)
@@ -83,8 +112,19 @@ __global__ void k_yfill(int64_t H, int32_t *__restrict__ keys, int64_t R, uint4 
     if (j < R) aux[j] = make_uint4(0u, 0u, 0u, 0u);   // the records themselves are written by k_yrank
 }
 
-// Hash find-or-insert of v; returns its slot.
-__device__ __forceinline__ int64_t hash_insert(int32_t *keys, int lgb, int32_t v)
+__device__ __forceinline__ int32_t cas_global(int32_t *p, int32_t cmp, int32_t val)
+{
+    int32_t old;
+    asm volatile("atom.global.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "l"(p), "r"(cmp), "r"(val) : "memory");
+    return old;
+}
+__device__ __forceinline__ void or_global(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("red.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Hash find-or-insert of v; returns its slot, *found = v was already present.
+__device__ __forceinline__ int64_t hash_insert(int32_t *keys, int lgb, int32_t v, bool *found)
 {
     const uint32_t bmask = (1u << lgb) - 1u;
     uint32_t bk = ybucket(v, lgb);
@@ -97,95 +137,80 @@ __device__ __forceinline__ int64_t hash_insert(int32_t *keys, int lgb, int32_t v
         for (int j = 0; j < YB; j++) {
             const uint32_t slot = bk * YB + j;
             int32_t k = kk[j];
-            if (k == -1) k = atomicCAS(&keys[slot], -1, v);
-            if (k == -1 || k == v) return slot;
+            if (k == -1) k = cas_global(keys + slot, -1, v);
+            if (k == -1 || k == v) {
+                *found = k == v;
+                return slot;
+            }
         }
         bk = (bk + 1) & bmask;
     }
 }
 
-// Position of node v in the sorted id range [lo, hi), or -1.
-__device__ __forceinline__ int64_t find_sorted(const int32_t *__restrict__ id, int64_t lo, int64_t hi, int32_t v)
-{
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        const int32_t x = id[mid];
-        if (x == v) return mid;
-        if (x < v) lo = mid + 1;
-        else hi = mid;
-    }
-    return -1;
-}
-
 // K5 over the support entries (frontier entry e: node id[e], value val[e], segment seg[e] =
 // 2 i + side; each segment sorted by node id) of the leaving queries.  Every node v of
-// U = supp(s*) u supp(t*) has one OWNER entry (its side-0 entry, else its side-1 entry), which
-// finds v's entry on the other side and writes
+// U = supp(s*) u supp(t*) gets
 //     y(v) = s*(v)/d(s) - t*(v)/d(t)          (a side v is not on contributes 0.0 / d = 0.0)
-// exactly once (Alg. 1 L7 with s = s*, t = t*).
-//   pass 0: hash: owners find the other side by binary search, insert v (CAS on the key slot)
-//           and write y;  rank: every entry sets its side's bit of v
-//   (k_yrank between the passes: union bits, rank of U and rank of the t* side per record)
-//   pass 1: rank: owners find v's t* entry by rank (segment start + rank T + popc) and write y
-//           at rank U + popc(U bits below v)
+// written exactly once in its final form (Alg. 1 L7 with s = s*, t = t*), no searches:
+//   hash  pass 0: t* entries insert v with -(t*(v)/d(t)) (= 0.0/d(s) - t*(v)/d(t) exactly);
+//         pass 1: s* entries find-or-insert v: y = s*(v)/d(s) + stored (= a - b exactly, IEEE
+//                 a - b is a + (-b)) if v was inserted by its t* entry, else s*(v)/d(s) - 0.0
+//   rank  pass 0: every entry sets its side's bit of v in the build-time aux records;
+//         (k_yrank between the passes: union bits, rank of U and rank of the t* side per record)
+//         pass 1: v's owner (its s* entry, else its t* entry) finds v's t* entry by rank (segment
+//                 start + rank T + popc) and writes y at rank U + popc(U bits below v)
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                           const int32_t *__restrict__ id, const double *__restrict__ val,
-                          const int64_t *__restrict__ segoff, const int32_t *__restrict__ act,
-                          const int64_t *__restrict__ vslots, const QState *__restrict__ qs, int pass)
+                          const int64_t *__restrict__ segoff, const YDesc *__restrict__ yd, int pass)
 {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
     const int32_t g = seg[e];
-    const int32_t i = g >> 1;
-    if (vslots[i] == 0) return;
+    const YDesc D = yd[g >> 1];
+    if (D.mode < 0) return;
     const int side = g & 1;
-    const QState &Q = qs[act[i]];
     const int32_t v = id[e];
-    if (Q.ymode == YT_RANK) {
-        // membership bits per side in the build-time aux records {S bits, T bits}; k_yrank turns
-        // them into the walk records {U bits, rank U, rank T}; no searches
-        uint4 *aux = const_cast<uint4 *>(Q.yaux);
+    if (D.mode == YT_RANK) {
         const uint64_t bit = 1ull << (v & 63);
         if (pass == 0) {
-            atomicOr(reinterpret_cast<unsigned long long *>(aux + (v >> 6)) + side, bit);
+            or_global(reinterpret_cast<unsigned long long *>(D.aux + (v >> 6)) + side, bit);
             return;
         }
-        const uint4 a = aux[v >> 6];
+        const uint4 a = D.aux[v >> 6];
         const uint64_t sbits = ((uint64_t)a.y << 32) | a.x, tbits = ((uint64_t)a.w << 32) | a.z;
         if (side == 1 && (sbits & bit)) return;   // the side-0 entry owns v
-        const uint4 r = Q.yrec[v >> 6];
+        const uint4 r = D.rec[v >> 6];
         const uint64_t below = bit - 1ull;
         double xt = 0.0;
         if (side == 1) xt = val[e];
         else if (tbits & bit) xt = val[segoff[g ^ 1] + r.w + __popcll(tbits & below)];   // v's t* entry
         const double xs = side == 0 ? val[e] : 0.0;
-        const double y = xs / (double)Q.ds - xt / (double)Q.dt;
+        const double y = xs / (double)D.ds - xt / (double)D.dt;
         const uint64_t ubits = ((uint64_t)r.y << 32) | r.x;
-        const_cast<double *>(Q.yvals)[r.z + __popcll(ubits & below)] = y;
+        D.vals[r.z + __popcll(ubits & below)] = y;
         return;
     }
-    if (pass != 0) return;
-    // owner test and the other side's value
-    const int64_t other = find_sorted(id, segoff[g ^ 1], segoff[(g ^ 1) + 1], v);
-    if (side == 1 && other >= 0) return;   // the side-0 entry owns v
-    const double xs = side == 0 ? val[e] : 0.0;
-    const double xt = side == 1 ? val[e] : (other >= 0 ? val[other] : 0.0);
-    const double y = xs / (double)Q.ds - xt / (double)Q.dt;
-    double *vals = const_cast<double *>(Q.yvals);
-    if (Q.ymode == YT_HASH) vals[hash_insert(const_cast<int32_t *>(Q.ykeys), Q.ylog2 - YB_LOG, v)] = y;
-    else vals[rank_index(Q.yrec[v >> 6], v)] = y;
+    if (side != (pass == 0 ? 1 : 0)) return;
+    bool found;
+    const int64_t slot = hash_insert(D.keys, D.lgb, v, &found);
+    if (side == 1) {
+        D.vals[slot] = -(val[e] / (double)D.dt);
+    } else {
+        const double a = val[e] / (double)D.ds;
+        D.vals[slot] = found ? a + D.vals[slot] : a - 0.0;
+    }
 }
 
 // Ranks of the rank-bitmap tables: rank(record w) = popcount of all records before w.  One CTA
 // per leaving query (non-rank queries exit).
 constexpr int YRANK_THREADS = 256;
 __global__ void __launch_bounds__(YRANK_THREADS)
-k_yrank(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__ rrecs, QState *__restrict__ qs)
+k_yrank(int32_t na, const int64_t *__restrict__ rrecs, const YDesc *__restrict__ yd)
 {
     const int32_t i = blockIdx.x;
     if (i >= na || rrecs[i] == 0) return;
-    uint4 *recs = const_cast<uint4 *>(qs[act[i]].yrec);
-    const uint4 *aux = qs[act[i]].yaux;
+    uint4 *recs = yd[i].rec;
+    const uint4 *aux = yd[i].aux;
     const int64_t R = rrecs[i];
     typedef cub::BlockScan<unsigned long long, YRANK_THREADS> Scan;
     __shared__ typename Scan::TempStorage tmp;
@@ -257,17 +282,17 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
     int32_t *keys = reinterpret_cast<int32_t *>(yb.as<char>() + o_key);   // buckets need 32-byte alignment
     k_yfill<<<blocks_for(std::max(H, R), 256), 256, 0, c.st>>>(H, keys, R, aux);
     LAUNCHED(c.g);
+    ENSURE(ws.ydesc, sizeof(YDesc) * (na + 1), false);
+    YDesc *yd = ws.ydesc.as<YDesc>();
     k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, hs, hi, vs, vi, rs, ri, keys, vals, recs, aux,
-                                                      ws.qs.as<QState>());
+                                                      ws.qs.as<QState>(), yd);
     LAUNCHED(c.g);
     for (int pass = 0; pass < 2; pass++) {
-        if (pass == 1) {
-            if (R == 0) break;
-            k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, act, rs, ws.qs.as<QState>());
+        if (pass == 1 && R > 0) {
+            k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, rs, yd);
             LAUNCHED(c.g);
         }
-        k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, segoff, act, vs, ws.qs.as<QState>(),
-                                                          pass);
+        k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, segoff, yd, pass);
         LAUNCHED(c.g);
     }
     return ER_OK;
