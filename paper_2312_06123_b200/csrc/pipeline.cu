@@ -187,26 +187,50 @@ __global__ void k_runstart(int64_t E, const KeyT *__restrict__ keys, const int32
     }
 }
 
-// Segmented warp reduction over lanes sorted by g: the first lane of each run of equal g
-// ends up holding op over that run's lanes (order-independent ops only: +, max).
-template <class T, class Op>
-__device__ __forceinline__ T warp_seg_reduce(T v, int32_t g, Op op)
-{
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const T ov = __shfl_down_sync(0xffffffffu, v, o);
-        const int32_t og = __shfl_down_sync(0xffffffffu, g, o);
-        if (lane + o < 32 && og == g) v = op(v, ov);
-    }
-    return v;
-}
-
+// First lane of each run of equal g (lanes sorted by g).
 __device__ __forceinline__ bool warp_seg_head(int32_t g)
 {
     const int32_t pg = __shfl_up_sync(0xffffffffu, g, 1);
     return (threadIdx.x & 31) == 0 || pg != g;
 }
+
+// Two segmented reductions at once (a with opA, b with opB; integer + / max only, so the result
+// does not depend on the grouping) over lanes sorted by g.  Returns true on the lane holding a
+// run's totals (its first lane).  Fast path when the whole warp is one run (the common case:
+// segments hold hundreds to millions of entries).
+template <class OpA, class OpB>
+__device__ __forceinline__ bool warp_seg_reduce2(unsigned long long &a, unsigned long long &b, int32_t g, OpA opA,
+                                                 OpB opB)
+{
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    if (__all_sync(full, g == __shfl_sync(full, g, 0))) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a = opA(a, __shfl_xor_sync(full, a, o));
+            b = opB(b, __shfl_xor_sync(full, b, o));
+        }
+        return lane == 0;
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long oa = __shfl_down_sync(full, a, o);
+        const unsigned long long ob = __shfl_down_sync(full, b, o);
+        const int32_t og = __shfl_down_sync(full, g, o);
+        if (lane + o < 32 && og == g) {
+            a = opA(a, oa);
+            b = opB(b, ob);
+        }
+    }
+    return warp_seg_head(g);
+}
+
+struct OpAdd {
+    __device__ unsigned long long operator()(unsigned long long x, unsigned long long y) const { return x + y; }
+};
+struct OpMax {
+    __device__ unsigned long long operator()(unsigned long long x, unsigned long long y) const { return x > y ? x : y; }
+};
 
 // K3 + K4a: x'(u) = (sum of the run, sequential in ascending source order) / d(u) (R1, R13),
 // fused with the segment statistics that are order-independent: vol = sum d(u) (int64 add),
@@ -251,11 +275,9 @@ __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const
         if (u == Q.s) ss[g].at_s = x;
         if (u == Q.t) ss[g].at_t = x;
     }
-    const unsigned long long vsum = warp_seg_reduce(deg, g, [](unsigned long long a, unsigned long long b) { return a + b; });
-    const unsigned long long vmax = warp_seg_reduce(bits, g, [](unsigned long long a, unsigned long long b) { return a > b ? a : b; });
-    if (live && warp_seg_head(g)) {
-        atomicAdd(reinterpret_cast<unsigned long long *>(&ss[g].vol), vsum);
-        atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max1), vmax);
+    if (warp_seg_reduce2(deg, bits, g, OpAdd(), OpMax()) && live) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(&ss[g].vol), deg);
+        atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max1), bits);
     }
 }
 
@@ -295,11 +317,9 @@ __global__ void k_first_wave(int64_t E, int32_t nseg, const int64_t *__restrict_
         if (u == Q.t) ss[g].at_t = x;
         if (p == 0) *dU = E;
     }
-    const unsigned long long vsum = warp_seg_reduce(deg, g, [](unsigned long long a, unsigned long long b) { return a + b; });
-    const unsigned long long vmax = warp_seg_reduce(bits, g, [](unsigned long long a, unsigned long long b) { return a > b ? a : b; });
-    if (live && warp_seg_head(g)) {
-        atomicAdd(reinterpret_cast<unsigned long long *>(&ss[g].vol), vsum);
-        atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max1), vmax);
+    if (warp_seg_reduce2(deg, bits, g, OpAdd(), OpMax()) && live) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(&ss[g].vol), deg);
+        atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max1), bits);
     }
 }
 
@@ -318,11 +338,9 @@ __global__ void k_seg_max2(int64_t Fmax, const int64_t *__restrict__ dF, const i
         if (b < m1) below = b;
         else eq = 1;
     }
-    const unsigned long long vb = warp_seg_reduce(below, g, [](unsigned long long a, unsigned long long b) { return a > b ? a : b; });
-    const unsigned long long ve = warp_seg_reduce(eq, g, [](unsigned long long a, unsigned long long b) { return a + b; });
-    if (live && warp_seg_head(g)) {
-        if (vb) atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max2), vb);
-        if (ve) atomicAdd(&ss[g].n_max1, ve);
+    if (warp_seg_reduce2(below, eq, g, OpMax(), OpAdd()) && live) {
+        if (below) atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max2), below);
+        if (eq) atomicAdd(&ss[g].n_max1, eq);
     }
 }
 
