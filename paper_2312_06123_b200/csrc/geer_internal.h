@@ -125,6 +125,7 @@ struct Workspace {
 
 struct er_graph {
     int device = 0;
+    int num_sms = 148;            // multiprocessors of the device (set at creation)
     int64_t n = 0, nnz = 0;
     int64_t *d_off = nullptr;
     int32_t *d_cols = nullptr;

@@ -243,8 +243,12 @@ __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const
                              int32_t *__restrict__ nid, double *__restrict__ nval, int32_t *__restrict__ nseg_out,
                              SegStat *__restrict__ ss)
 {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = r < Emax && r < *dU;
+    // grid-stride over the U <= Emax runs (the grid is sized for the resident CTAs, U is known
+    // on the device only); the loop bound is block-uniform, so warps stay converged
+    const int64_t U = min(Emax, *dU);
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < U; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = base + threadIdx.x;
+    const bool live = r < U;
     int32_t g = 0x7fffffff;
     unsigned long long deg = 0, bits = 0;
     if (live) {
@@ -278,6 +282,7 @@ __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const
     if (warp_seg_reduce2(deg, bits, g, OpAdd(), OpMax()) && live) {
         atomicAdd(reinterpret_cast<unsigned long long *>(&ss[g].vol), deg);
         atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max1), bits);
+    }
     }
 }
 
@@ -327,20 +332,23 @@ __global__ void k_first_wave(int64_t E, int32_t nseg, const int64_t *__restrict_
 __global__ void k_seg_max2(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                            const double *__restrict__ val, SegStat *__restrict__ ss)
 {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = e < Fmax && e < *dF;
-    int32_t g = 0x7fffffff;
-    unsigned long long below = 0, eq = 0;
-    if (live) {
-        g = seg[e];
-        const unsigned long long b = (unsigned long long)__double_as_longlong(val[e]);
-        const unsigned long long m1 = *reinterpret_cast<const unsigned long long *>(&ss[g].max1);
-        if (b < m1) below = b;
-        else eq = 1;
-    }
-    if (warp_seg_reduce2(below, eq, g, OpMax(), OpAdd()) && live) {
-        if (below) atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max2), below);
-        if (eq) atomicAdd(&ss[g].n_max1, eq);
+    const int64_t F = min(Fmax, *dF);   // grid-stride, block-uniform bound (as k_run_reduce)
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < F; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = base + threadIdx.x;
+        const bool live = e < F;
+        int32_t g = 0x7fffffff;
+        unsigned long long below = 0, eq = 0;
+        if (live) {
+            g = seg[e];
+            const unsigned long long b = (unsigned long long)__double_as_longlong(val[e]);
+            const unsigned long long m1 = *reinterpret_cast<const unsigned long long *>(&ss[g].max1);
+            if (b < m1) below = b;
+            else eq = 1;
+        }
+        if (warp_seg_reduce2(below, eq, g, OpMax(), OpAdd()) && live) {
+            if (below) atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max2), below);
+            if (eq) atomicAdd(&ss[g].n_max1, eq);
+        }
     }
 }
 
@@ -895,17 +903,17 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                                                                  ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                                                                  ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>(), dU);
             } else if (P.nbits <= 24)
-                k_run_reduce<uint32_t><<<blocks_for(E, 256), 256, 0, st>>>(
+                k_run_reduce<uint32_t><<<resident_grid(g, E, 256), 256, 0, st>>>(
                     E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint32_t>(), P.nbits, one_chunk, ws.vals2.as<double>(), segbeg,
                     nseg, g->d_rec, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                     ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>());
             else
-                k_run_reduce<uint64_t><<<blocks_for(E, 256), 256, 0, st>>>(
+                k_run_reduce<uint64_t><<<resident_grid(g, E, 256), 256, 0, st>>>(
                     E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint64_t>(), P.nbits, one_chunk, ws.vals2.as<double>(), segbeg,
                     nseg, g->d_rec, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                     ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>());
             if (!dense) LAUNCHED(g);
-            k_seg_max2<<<blocks_for(E, 256), 256, 0, st>>>(E, dU, ws.nf_seg.as<int32_t>(), ws.nf_val.as<double>(),
+            k_seg_max2<<<resident_grid(g, E, 256), 256, 0, st>>>(E, dU, ws.nf_seg.as<int32_t>(), ws.nf_val.as<double>(),
                                                            ws.segstat.as<SegStat>());
             LAUNCHED(g);
             k_seg_off<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, dU, ws.nf_seg.as<int32_t>(),

@@ -23,6 +23,14 @@ namespace geer {
 
 static inline unsigned blocks_for(int64_t n, int per) { return (unsigned)((n + per - 1) / per); }
 
+// Grid of a grid-stride kernel over at most n items: one wave of resident CTAs (2048 threads
+// per SM), fewer when n is small.
+static inline unsigned resident_grid(const er_graph *g, int64_t n, int threads)
+{
+    const int64_t full = (int64_t)g->num_sms * (2048 / threads);
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(full, (n + threads - 1) / threads));
+}
+
 // y-table layouts (ytable.cu) and the walk kernel's staging limits (walks.cu).
 constexpr int YT_HASH = 0;
 constexpr int YT_RANK = 1;

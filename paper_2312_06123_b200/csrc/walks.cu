@@ -427,8 +427,7 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
         g->launches += 2;
         list = list2;
     }
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
+    const int nsm = g->num_sms;
     const uint32_t key0 = (uint32_t)P.seed, key1 = (uint32_t)(P.seed >> 32);
     for (int b = 0; b < P.tau; b++) {
         k_nchunks<<<blocks_for(na, 256), 256, 0, sb>>>(na, list, qs, b, P.reuse, per_chunk, nch);
