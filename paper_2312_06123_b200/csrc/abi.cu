@@ -277,7 +277,7 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
             if (!strcmp(env, "cols")) layout = 0;
             if (!strcmp(env, "packed") && packable) layout = 2;
         }
-        if (const char *env = getenv("GEER_WALK_MINB")) g->walk_minb = atoi(env) == 3 ? 3 : 4;
+        if (const char *env = getenv("GEER_WALK_MINB")) { const int v = atoi(env); g->walk_minb = (v >= 3 && v <= 6) ? v : 4; }
         if (const char *env = getenv("GEER_AMC_OVERLAP")) g->amc_overlap = atoi(env) != 0;
         if (const char *env = getenv("GEER_WALK_PERSIST")) g->walk_persist = atoi(env) != 0;
         if (const char *env = getenv("GEER_YTABLE")) g->ytable_force = !strcmp(env, "hash") ? 1 : !strcmp(env, "rank") ? 2 : 0;
@@ -287,7 +287,10 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_MAX_SUB_BATCH")) g->max_sub_batch = std::max<int64_t>(1, atoll(env));
         if (const char *env = getenv("GEER_WALK_NP")) g->walk_np = atoi(env) == 1 ? 1 : 2;
         if (const char *env = getenv("GEER_HUB_CB")) { const int v = atoi(env); g->hub_cb = (v == 8 || v == 16) ? v : 32; }
-        if (const char *env = getenv("GEER_WALK_SMEM_KB")) g->walk_smem_words = 256 * std::min(48, std::max(8, atoi(env)));
+        if (const char *env = getenv("GEER_WALK_SMEM_KB")) g->walk_smem_words = 256 * std::min(48, std::max(0, atoi(env)));
+        if (const char *env = getenv("GEER_RANK_MIN_CAP")) g->rank_min_cap = std::max<int64_t>(0, atoll(env));
+        if (const char *env = getenv("GEER_RANK_RATIO")) g->rank_ratio = std::max<int64_t>(0, atoll(env));
+        if (const char *env = getenv("GEER_WALK_CARVEOUT")) g->walk_carveout = std::min(100, std::max(-1, atoi(env)));
         g->pack.bo = bo;
         g->pack.bd = bd;
         if (layout == 1 && e == cudaSuccess) {

@@ -144,13 +144,17 @@ struct er_graph {
     bool amc_overlap = false;  // AMC per SMM wave on the AMC stream (GEER_AMC_OVERLAP=1) or one AMC after the head
     int walk_occ = 0;    // K6 resident CTAs per SM at the last launch (occupancy API)
     bool walk_persist = true;   // K6 persistent grid + atomic tile counter (GEER_WALK_PERSIST=1) or one tile per CTA
+    int64_t rank_min_cap = 4096;  // K5: rank bitmap only for tables above this many hash slots (GEER_RANK_MIN_CAP)
+    int64_t rank_ratio = 24;      // ... and when 16 B x records < rank_ratio x slots (GEER_RANK_RATIO)
     int ytable_force = 0;  // y-table layout: 0 by footprint, 1 hash only, 2 rank bitmap only (GEER_YTABLE)
     int y_evict_first = 0; // K6: L2 evict-first policy on y-table loads (GEER_Y_EVICT_FIRST)
     bool l2_persist = false; // K6: persisting-L2 access window over the walk graph (GEER_L2_PERSIST)
     size_t l2_window = 0, l2_persist_bytes = 0;
     int64_t max_sub_batch = 1 << 18;  // queries per internal sub-batch (GEER_MAX_SUB_BATCH)
     int walk_np = 1;     // K6 walk pairs per thread (GEER_WALK_NP 1..2)
-    int walk_smem_words = 6144;   // K6 staging area per CTA in 32-bit words (GEER_WALK_SMEM_KB)
+    int walk_smem_words = 0;      // K6 staging area per CTA in 32-bit words (GEER_WALK_SMEM_KB; default none:
+                                  // shared memory taken from L1 costs more walk throughput than staging saves)
+    int walk_carveout = -1;       // K6 preferred shared-memory carveout in % (-1: driver default; GEER_WALK_CARVEOUT)
     cudaStream_t stream = nullptr;
     cudaStream_t amc_stream = nullptr;  // AMC groups overlap the SMM head
     cudaStream_t head_stream = nullptr; // high-priority stream of the SMM head (forked from the caller's)

@@ -34,7 +34,6 @@ static inline unsigned resident_grid(const er_graph *g, int64_t n, int threads)
 // y-table layouts (ytable.cu) and the walk kernel's staging limits (walks.cu).
 constexpr int YT_HASH = 0;
 constexpr int YT_RANK = 1;
-constexpr int WALK_SMEM_WORDS = 6144;       // 24 KB of staged y-table keys per CTA
 constexpr int WALK_KEY_SLOTS = 4096;        // largest hash table staged in shared memory
 
 // Rank-bitmap lookup: record r = {U bits lo, U bits hi, rank U, rank T} of the 64 node ids

@@ -450,6 +450,9 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
     do {                                                                                                    \
         CK(cudaFuncSetAttribute(k_walks<ARC, NP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                 (int)smem_bytes));                                                          \
+        if (g->walk_carveout >= 0)                                                                          \
+            CK(cudaFuncSetAttribute(k_walks<ARC, NP, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,   \
+                                    g->walk_carveout));                                                     \
         int occ = 0;                                                                                        \
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walks<ARC, NP, MINB>, WALK_THREADS,        \
                                                          smem_bytes));                                      \
@@ -475,6 +478,8 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
         const size_t smem_bytes = sizeof(int32_t) * (size_t)smem_words;
         if (g->walk_np == 1) {
             if (g->walk_minb == 3) WALK_ARC(1, 3);
+            else if (g->walk_minb == 5) WALK_ARC(1, 5);
+            else if (g->walk_minb == 6) WALK_ARC(1, 6);
             else WALK_ARC(1, 4);
         } else {
             if (g->walk_minb == 3) WALK_ARC(2, 3);

@@ -154,6 +154,19 @@ int main(int argc, char **argv)
         RUN("packed_philox", 1, (k_packed<1, true>), nw, lf, d_pa, d_rec, (int)n, bo, bd, d_out);
         RUN("packed_philox", 2, (k_packed<2, true>), nw, lf, d_pa, d_rec, (int)n, bo, bd, d_out);
         RUN("packed_philox", 4, (k_packed<4, true>), nw, lf, d_pa, d_rec, (int)n, bo, bd, d_out);
+        // the same chains at 4 resident CTAs of 256 threads per SM (K6's occupancy): 50 KB of
+        // dynamic shared memory per CTA caps residency
+#define RUN4(NAME, C, KERNEL, ...)                                                                      \
+        {                                                                                               \
+            const int64_t thr = (nw + C - 1) / C;                                                       \
+            cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, 50 * 1024);       \
+            float ms = timeit([&] { KERNEL<<<(unsigned)((thr + 255) / 256), 256, 50 * 1024>>>(__VA_ARGS__); }); \
+            printf("%-16s walks=%8lld C=%d  %7.3f ms  %7.1f Gsteps/s  (4 CTAs/SM)\n", NAME, (long long)nw, C, ms, \
+                   (double)nw * lf / ms / 1e6);                                                         \
+        }
+        RUN4("packed_philox", 2, (k_packed<2, true>), nw, lf, d_pa, d_rec, (int)n, bo, bd, d_out);
+        RUN4("packed_philox", 4, (k_packed<4, true>), nw, lf, d_pa, d_rec, (int)n, bo, bd, d_out);
+        RUN4("packed_philox", 8, (k_packed<8, true>), nw, lf, d_pa, d_rec, (int)n, bo, bd, d_out);
         RUN("cols_hash", 1, (k_cols<1>), nw, lf, d_cols, d_rec, (int)n, d_out);
         RUN("cols_hash", 2, (k_cols<2>), nw, lf, d_cols, d_rec, (int)n, d_out);
         RUN("cols_hash", 4, (k_cols<4>), nw, lf, d_cols, d_rec, (int)n, d_out);
