@@ -49,20 +49,14 @@ __device__ __forceinline__ uint64_t walk_hash(uint32_t q, uint32_t b, uint32_t s
     return fmix64(h ^ (uint64_t)(uint32_t)end);
 }
 
-// y-tables: buckets of YB = 8 int32 keys (one 32-byte sector); bucket of node v in a table of
-// 2^lgb buckets (multiplicative hash, top bits).
-constexpr int YB = 8;
-constexpr int YB_LOG = 3;
+// y-tables: buckets of YB = 4 int32 keys (one 16-byte load, the size of a rank record, so the
+// walk kernel pipelines both the same way); bucket of node v in a table of 2^lgb buckets
+// (multiplicative hash, top bits).
+constexpr int YB = 4;
+constexpr int YB_LOG = 2;
 __device__ __forceinline__ uint32_t ybucket(int32_t v, int lgb)
 {
     return lgb == 0 ? 0u : ((uint32_t)v * 0x9E3779B1u) >> (32 - lgb);
-}
-
-// Membership filter of a large y-table (a one-hash Bloom filter over supp(y)): bit of node v in a
-// filter of 2^flg bits (top bits of an odd multiplier independent of ybucket's).
-__device__ __forceinline__ uint32_t fbit(int32_t v, int flg)
-{
-    return ((uint32_t)v * 0x85EBCA6Bu) >> (32 - flg);
 }
 
 // Eq. 10.

@@ -40,19 +40,15 @@ __device__ __forceinline__ int32_t find_chunk_query(const int64_t *__restrict__ 
     return lo;
 }
 
-// 8 keys of a bucket: index of v, or -1; *empty = the bucket has a free slot.
-__device__ __forceinline__ int bucket_match(const int4 a, const int4 b, int32_t v, bool *empty)
+// The 4 keys of a bucket: index of v, or -1; *empty = the bucket has a free slot.
+__device__ __forceinline__ int bucket_match(const int4 a, int32_t v, bool *empty)
 {
     int m = -1;
-    m = (b.w == v) ? 7 : m;
-    m = (b.z == v) ? 6 : m;
-    m = (b.y == v) ? 5 : m;
-    m = (b.x == v) ? 4 : m;
     m = (a.w == v) ? 3 : m;
     m = (a.z == v) ? 2 : m;
     m = (a.y == v) ? 1 : m;
     m = (a.x == v) ? 0 : m;
-    *empty = (a.x < 0) | (a.y < 0) | (a.z < 0) | (a.w < 0) | (b.x < 0) | (b.y < 0) | (b.z < 0) | (b.w < 0);
+    *empty = (a.x < 0) | (a.y < 0) | (a.z < 0) | (a.w < 0);
     return m;
 }
 
@@ -81,42 +77,53 @@ __device__ __forceinline__ uint4 ld_y(const uint4 *p, uint64_t pol)
 }
 
 // Hash lookups: slot of v, or -1 when v is not in supp(y) (then y(v) = 0, Alg. 1 L7 outside
-// U_s and U_t).  Staged keys in shared memory, or the table in global memory (one 32-byte
-// sector per bucket, LDG.E.ENL2.256).
+// U_s and U_t).  Staged keys in shared memory, or the table in global memory (one 16-byte
+// bucket per probe).  ylookup_global_from continues a global probe at bucket bk.
+__device__ __forceinline__ int4 ld_bucket(const int32_t *keys, uint32_t bk, uint64_t pol)
+{
+    const int4 *p = reinterpret_cast<const int4 *>(keys + (size_t)bk * YB);
+    if (!pol) return __ldg(p);
+    int4 a;
+    asm("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(p), "l"(pol));
+    return a;
+}
 __device__ __forceinline__ int64_t ylookup_smem(const int32_t *skeys, int lgb, int32_t v)
 {
     const uint32_t bmask = (1u << lgb) - 1u;
     uint32_t bk = ybucket(v, lgb);
     while (true) {
         const int4 a = reinterpret_cast<const int4 *>(skeys + (size_t)bk * YB)[0];
-        const int4 b = reinterpret_cast<const int4 *>(skeys + (size_t)bk * YB)[1];
         bool empty;
-        const int m = bucket_match(a, b, v, &empty);
+        const int m = bucket_match(a, v, &empty);
         if (m >= 0) return (int64_t)bk * YB + m;
         if (empty) return -1;
         bk = (bk + 1) & bmask;
     }
 }
-__device__ __forceinline__ int64_t ylookup_global(const int32_t *keys, int lgb, int32_t v, uint64_t pol)
+__device__ __forceinline__ int64_t ylookup_global_from(const int32_t *keys, int lgb, int32_t v, uint32_t bk,
+                                                       uint64_t pol)
 {
     const uint32_t bmask = (1u << lgb) - 1u;
-    uint32_t bk = ybucket(v, lgb);
     while (true) {
-        int4 a, b;
-        if (pol)
-            asm("ld.global.nc.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
-                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-                : "l"(keys + (size_t)bk * YB), "l"(pol));
-        else
-            asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-                : "l"(keys + (size_t)bk * YB));
+        const int4 a = ld_bucket(keys, bk, pol);
         bool empty;
-        const int m = bucket_match(a, b, v, &empty);
+        const int m = bucket_match(a, v, &empty);
         if (m >= 0) return (int64_t)bk * YB + m;
         if (empty) return -1;
         bk = (bk + 1) & bmask;
     }
+}
+// Resolve a global probe whose first bucket `a` (of node v) was loaded one step earlier.
+__device__ __forceinline__ int64_t ylookup_resolve(const int4 a, const int32_t *keys, int lgb, int32_t v,
+                                                   uint64_t pol)
+{
+    bool empty;
+    const int m = bucket_match(a, v, &empty);
+    const uint32_t bk = ybucket(v, lgb);
+    if (m >= 0) return (int64_t)bk * YB + m;
+    if (empty) return -1;
+    return ylookup_global_from(keys, lgb, v, (bk + 1) & ((1u << lgb) - 1u), pol);   // full bucket: rare
 }
 
 template <int ARC>
@@ -140,9 +147,13 @@ enum { YM_GLOBAL = 0, YM_SMEM = 1, YM_RANK = 2 };
 // Philox draw (R10; the even step's words are cached from the odd step's call), one arc load
 // (the chain's only dependent memory access), then y(v):
 //   YM_SMEM    hash keys staged in shared memory: probe now, value load consumed next step;
-//   YM_GLOBAL  hash keys in global memory: probe now (32-byte bucket loads), value next step;
-//   YM_RANK    rank-bitmap record load issued now and resolved next step (overlapping the next
-//              arc load), value load consumed the step after.
+//   YM_GLOBAL  hash keys in global memory: first bucket (16 B) load issued now and resolved next
+//              step (a full bucket continues synchronously, rare at load <= 1/2), value load
+//              consumed the step after;
+//   YM_RANK    rank-bitmap record (16 B) load issued now and resolved next step, value load
+//              consumed the step after.
+// The pipelined loads (bucket or record) overlap the next arc load, so only the arc load is
+// on the chain.
 // y values are added in step order (R9, R13).
 template <int ARC, int NP>
 __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
@@ -159,7 +170,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
     int32_t v[C];
     double pv[C];
     uint32_t cz[C], cw[C];
-    uint4 prec[C];       // YM_RANK: record of the previous step's node, resolved this step
+    uint4 prec[C];       // YM_RANK record / YM_GLOBAL first bucket of the previous step's node
 #pragma unroll
     for (int c = 0; c < C; c++) {
         v[c] = (c & 1) ? t : s;
@@ -168,7 +179,8 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
         pv[c] = 0.0;
         cz[c] = 0u;
         cw[c] = 0u;
-        prec[c] = make_uint4(0u, 0u, 0u, 0u);   // no bits: the start node is not summed (R9)
+        // the start node is not summed (R9): no rank bits / an empty bucket
+        prec[c] = mode == YM_GLOBAL ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0u, 0u, 0u, 0u);
     }
     for (int32_t j = 1; j <= lf; j++) {
         uint4 A[C];
@@ -192,8 +204,10 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
         for (int c = 0; c < C; c++) {
             acc[c] += pv[c];   // y of an earlier step, in step order
             pv[c] = 0.0;
-            if (mode == YM_RANK) {
-                const int64_t idx = rank_index(prec[c], v[c]);   // v[c] = previous step's node
+            if (mode != YM_SMEM) {   // resolve the previous step's node (v[c])
+                const int64_t idx = mode == YM_RANK ? rank_index(prec[c], v[c])
+                                                    : ylookup_resolve(*reinterpret_cast<const int4 *>(&prec[c]),
+                                                                      gkeys, lgb, v[c], pol);
                 if (idx >= 0) pv[c] = ld_y(gvals + idx, pol);
             }
             v[c] = (int32_t)A[c].x;
@@ -201,9 +215,11 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
             else R[c] = __ldg(rec + v[c]);
             if (mode == YM_RANK) {
                 prec[c] = ld_y(yrec + (v[c] >> 6), pol);
+            } else if (mode == YM_GLOBAL) {
+                const int4 bk = ld_bucket(gkeys, ybucket(v[c], lgb), pol);
+                prec[c] = make_uint4((uint32_t)bk.x, (uint32_t)bk.y, (uint32_t)bk.z, (uint32_t)bk.w);
             } else {
-                const int64_t slot =
-                    mode == YM_SMEM ? ylookup_smem(skeys, lgb, v[c]) : ylookup_global(gkeys, lgb, v[c], pol);
+                const int64_t slot = ylookup_smem(skeys, lgb, v[c]);
                 if (slot >= 0) pv[c] = ld_y(gvals + slot, pol);
             }
         }
@@ -211,8 +227,10 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
 #pragma unroll
     for (int c = 0; c < C; c++) {
         acc[c] += pv[c];
-        if (mode == YM_RANK && lf > 0) {
-            const int64_t idx = rank_index(prec[c], v[c]);
+        if (mode != YM_SMEM && lf > 0) {
+            const int64_t idx = mode == YM_RANK ? rank_index(prec[c], v[c])
+                                                : ylookup_resolve(*reinterpret_cast<const int4 *>(&prec[c]), gkeys,
+                                                                  lgb, v[c], pol);
             if (idx >= 0) acc[c] += ld_y(gvals + idx, pol);
         }
         endv[c] = v[c];

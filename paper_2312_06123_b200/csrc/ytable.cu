@@ -11,10 +11,10 @@ namespace geer {
 // y-tables (K5): y(v) = s*(v)/d(s) - t*(v)/d(t) on U = supp(s*) u supp(t*) for each query that
 // leaves the SMM head for AMC in this wave (Alg. 1 L7 with s = s*, t = t*).  Two layouts,
 // chosen per query by footprint:
-//  * hash (YT_HASH): open addressing, 8 int32 keys per 32-byte bucket, buckets probed linearly;
+//  * hash (YT_HASH): open addressing, 4 int32 keys per 16-byte bucket, buckets probed linearly;
 //    capacity = next power of two >= 2 (|supp s*| + |supp t*|) (load <= 1/2), >= one bucket;
-//    values fp64 by slot.  Tables of <= WALK_KEY_SLOTS keys are staged whole in the walk
-//    kernel's shared memory.
+//    values fp64 by slot.  (Tables of <= WALK_KEY_SLOTS keys can be staged whole in the walk
+//    kernel's shared memory, GEER_WALK_SMEM_KB; off by default.)
 //  * rank bitmap (YT_RANK): one 16-byte record {U bits (64); rank U; rank T} per 64 node ids
 //    (bit v of U; ranks = |U| and |supp t*| below the record), values fp64 by rank: y(v) is at
 //    vals[rank U + popc(U bits below v)].  Exact membership in one 16-byte load, no probing;
@@ -131,10 +131,9 @@ __device__ __forceinline__ int64_t hash_insert(int32_t *keys, int lgb, int32_t v
     uint32_t bk = ybucket(v, lgb);
     while (true) {
         const int4 *bp = reinterpret_cast<const int4 *>(keys + bk * YB);
-        int4 A, B;
+        int4 A;
         asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(A.x), "=r"(A.y), "=r"(A.z), "=r"(A.w) : "l"(bp));
-        asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(B.x), "=r"(B.y), "=r"(B.z), "=r"(B.w) : "l"(bp + 1));
-        const int32_t kk[YB] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+        const int32_t kk[YB] = {A.x, A.y, A.z, A.w};
         for (int j = 0; j < YB; j++) {
             const uint32_t slot = bk * YB + j;
             int32_t k = kk[j];
