@@ -290,6 +290,7 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_WALK_SMEM_KB")) g->walk_smem_words = 256 * std::min(48, std::max(0, atoi(env)));
         if (const char *env = getenv("GEER_RANK_MIN_CAP")) g->rank_min_cap = std::max<int64_t>(0, atoll(env));
         if (const char *env = getenv("GEER_RANK_RATIO")) g->rank_ratio = std::max<int64_t>(0, atoll(env));
+        if (const char *env = getenv("GEER_RANK_MAX_KB")) g->rank_max_bytes = 1024 * std::max<int64_t>(0, atoll(env));
         if (const char *env = getenv("GEER_WALK_CARVEOUT")) g->walk_carveout = std::min(100, std::max(-1, atoi(env)));
         g->pack.bo = bo;
         g->pack.bd = bd;

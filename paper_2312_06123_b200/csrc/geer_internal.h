@@ -146,6 +146,8 @@ struct er_graph {
     bool walk_persist = true;   // K6 persistent grid + atomic tile counter (GEER_WALK_PERSIST=1) or one tile per CTA
     int64_t rank_min_cap = 4096;  // K5: rank bitmap only for tables above this many hash slots (GEER_RANK_MIN_CAP)
     int64_t rank_ratio = 24;      // ... and when 16 B x records < rank_ratio x slots (GEER_RANK_RATIO)
+    int64_t rank_max_bytes = 960 << 10;  // ... and when the records take at most this, i.e. graphs up to
+                                         // ~3.9M nodes (GEER_RANK_MAX_KB; measured on configs 1-4)
     int ytable_force = 0;  // y-table layout: 0 by footprint, 1 hash only, 2 rank bitmap only (GEER_YTABLE)
     int y_evict_first = 0; // K6: L2 evict-first policy on y-table loads (GEER_Y_EVICT_FIRST)
     bool l2_persist = false; // K6: persisting-L2 access window over the walk graph (GEER_L2_PERSIST)

@@ -23,7 +23,7 @@ namespace geer {
 // Per leaving query i: hslots[i] hash slots, vslots[i] value slots, rrecs[i] rank records.
 __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState *__restrict__ qs,
                        const int32_t *__restrict__ cont, const int64_t *__restrict__ segoff, int64_t nrec,
-                       int force, int64_t min_cap, int64_t ratio, int64_t *__restrict__ hslots,
+                       int force, int64_t min_cap, int64_t ratio, int64_t max_bytes, int64_t *__restrict__ hslots,
                        int64_t *__restrict__ vslots,
                        int64_t *__restrict__ rrecs)
 {
@@ -36,7 +36,10 @@ __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState
         while (cap < 2 * len) cap <<= 1;
         // rank when the table cannot be staged and the records take at most twice the hash footprint:
         // rank lookups are pipelined off the walk chain, global hash probes are not
-        const bool rank = force == 2 || (force == 0 && cap > min_cap && 16 * nrec < ratio * cap);
+        // rank when the table cannot be small, its records are cheaper than twice the hash layout,
+        // and they are small enough to stay mostly in L2 (large graphs: hash)
+        const bool rank = force == 2 || (force == 0 && cap > min_cap && 16 * nrec < ratio * cap &&
+                                         16 * nrec <= max_bytes);
         if (rank) {
             r = nrec;
             v = len;
@@ -245,7 +248,7 @@ int ytable_plan(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, con
     int64_t *hi = ws.yoff.as<int64_t>(), *vi = hi + (na + 1), *ri = vi + (na + 1);
     const int64_t nrec = (c.g->n + 63) / 64;
     k_ycap<<<blocks_for(na, 256), 256, 0, c.st>>>(na, act, ws.qs.as<QState>(), cont, segoff, nrec, c.g->ytable_force,
-                                                  c.g->rank_min_cap, c.g->rank_ratio, hs, vs, rs);
+                                                  c.g->rank_min_cap, c.g->rank_ratio, c.g->rank_max_bytes, hs, vs, rs);
     LAUNCHED(c.g);
     int rc = scan_incl(c, hs, hi, na);
     if (!rc) rc = scan_incl(c, vs, vi, na);
