@@ -406,9 +406,9 @@ def test_query_ids_partition_reproduces_batch(geer, rmat20):
 
 @pytest.mark.parametrize("graph", ["tiny", "rmat20"])
 def test_ytable_layouts_and_kernel_variants_byte_identical(graph, tiny, rmat20):
-    """The y-table layout (hash / rank bitmap) and the walk-kernel schedule
-    (persistent or not, overlap with the head) change no output bit: they are layouts and
-    schedules of the same arithmetic.  Two walk pairs per thread regroup the per-chunk partial
+    """The y-table layout (hash / rank bitmap), shared-memory staging of small hash
+    tables and the walk-kernel schedule (persistent or not, overlap with the head) change no
+    output bit: they are layouts and schedules of the same arithmetic.  Two walk pairs per thread regroup the per-chunk partial
     sums (64 walks per warp instead of 32): walk endpoints stay bit-identical, estimates agree
     to ulps.  Each combination runs in a fresh process (the knobs are read at
     er_graph_create)."""
@@ -423,7 +423,8 @@ def test_ytable_layouts_and_kernel_variants_byte_identical(graph, tiny, rmat20):
             "sys.stdout.buffer.write(r.tobytes() + st['walk_checksum'].tobytes())")
     g = (tiny if graph == "tiny" else rmat20)[0]
     outs = {}
-    for env in ({"GEER_YTABLE": "hash"}, {"GEER_YTABLE": "rank"}, {},
+    for env in ({"GEER_YTABLE": "hash"}, {"GEER_YTABLE": "rank"}, {}, {"GEER_RANK_MAX_KB": "0"},
+                {"GEER_WALK_SMEM_KB": "8"}, {"GEER_WALK_SMEM_KB": "24", "GEER_YTABLE": "hash"},
                 {"GEER_WALK_NP": "2"}, {"GEER_WALK_NP": "2", "GEER_WALK_MINB": "3"}, {"GEER_WALK_PERSIST": "0"},
                 {"GEER_AMC_OVERLAP": "1"}):
         e = dict(os.environ, **env)
