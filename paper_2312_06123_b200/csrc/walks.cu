@@ -237,11 +237,73 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
     }
 }
 
-// K6: warp = one chunk of 32 NP walk pairs of one query (chunks of all AMC queries are laid
-// out query after query, queries ordered by descending ell_f; lane l, pair p runs walk
-// k = 32 NP chunk' + 32 p + l).  Per CTA-tile of WALK_WARPS chunks, a staging plan puts the
-// hash keys of each distinct small-table query of the tile into shared memory.  Each warp
-// writes the canonical partial {sum Z, sum Z^2, checksum} of its chunk.
+// One chunk of K6: 32 NP walk pairs of AMC query list entry i (lane l, pair p runs walk
+// k = 32 NP chunk' + 32 p + l, chunk' = chunk - the query's first chunk); writes the canonical
+// partial {sum Z, sum Z^2, checksum} of the chunk.
+template <int ARC, int NP>
+__device__ __forceinline__ void walk_chunk(int64_t chunk, int32_t i, int mode, const int32_t *skeys,
+                                           const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
+                                           const QState *__restrict__ qs, const uint2 *__restrict__ rec,
+                                           const uint4 *__restrict__ arcs, const int32_t *__restrict__ cols,
+                                           const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
+                                           uint32_t key0, uint32_t key1, int reuse, uint64_t pol,
+                                           TilePart *__restrict__ parts)
+{
+    const int lane = threadIdx.x & 31;
+    const QState &Q = qs[amc[i]];
+    const int64_t c0 = i == 0 ? 0 : cincl[i - 1];
+    const int64_t eta = Q.st.eta0 << b;
+    const uint64_t klo = (uint64_t)walks_lo(Q.st.eta0, b, reuse);
+    const uint32_t bkey = reuse ? 0u : (uint32_t)b;   // reuse: one sample stream per query
+    const uint32_t q = Q.gq;
+    uint64_t kk[NP];
+    bool any = false;
+#pragma unroll
+    for (int p = 0; p < NP; p++) {
+        kk[p] = klo + (uint64_t)(chunk - c0) * (32u * NP) + 32u * p + (uint64_t)lane;
+        any |= kk[p] < (uint64_t)eta;
+    }
+    double acc[2 * NP];
+    int32_t endv[2 * NP];
+    double s1 = 0.0, s2 = 0.0;
+    uint64_t ck = 0ull;
+    if (any) {
+        walk_chains<ARC, NP>(rec, arcs, cols, parcs, pk, mode, skeys, Q.ykeys, Q.yrec, Q.yvals, Q.ylog2 - YB_LOG,
+                             Q.s, Q.t, Q.st.ell_f, q, bkey, kk, key0, key1, acc, endv, pol);
+#pragma unroll
+        for (int p = 0; p < NP; p++) {
+            if (kk[p] < (uint64_t)eta) {
+                const double z = acc[2 * p] - acc[2 * p + 1];   // Z_k (Alg. 1 L8)
+                s1 += z;
+                s2 += z * z;
+                ck += walk_hash(q, bkey, 0u, kk[p], endv[2 * p]) + walk_hash(q, bkey, 1u, kk[p], endv[2 * p + 1]);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        ck += __shfl_xor_sync(0xffffffffu, ck, o);
+    }
+    if (lane == 0) {
+        TilePart tp;
+        tp.s1 = s1;
+        tp.s2 = s2;
+        tp.ck = ck;
+        tp.pad = 0;
+        parts[chunk] = tp;
+    }
+}
+
+// K6: warp = one chunk of 32 NP walk pairs of one query at a time (chunks of all AMC queries
+// are laid out query after query, queries ordered by descending ell_f).  Persistent: chunks are
+// handed out by an atomic counter (dynamic balance: the first chunks, of the longest walks, are
+// the longest); with tile_ctr == nullptr one chunk per warp.  Default (smem_words == 0): every
+// warp takes its own chunks, no barriers.  With a staging area (GEER_WALK_SMEM_KB > 0): CTA-tiles
+// of WALK_WARPS consecutive chunks, and a per-tile plan stages the hash keys of each distinct
+// small-table query of the tile in shared memory (slower on B200: shared memory is taken from
+// the L1 that holds the loads in flight).
 template <int ARC, int NP, int MINB>
 __global__ void __launch_bounds__(WALK_THREADS, MINB)
 k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
@@ -258,9 +320,21 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
     const uint64_t pol = y_evict_first ? pol_evict_first() : 0;
-    // persistent: CTA-tiles of WALK_WARPS consecutive chunks handed out by an atomic counter
-    // (dynamic balance: the first tiles, of the longest walks, are the longest); with
-    // tile_ctr == nullptr one tile per CTA, tile = blockIdx.x
+    if (smem_words == 0) {
+        for (int it = 0;; it++) {
+            int64_t chunk = 0;
+            if (lane == 0)
+                chunk = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1ull)
+                                 : (it == 0 ? (int64_t)blockIdx.x * WALK_WARPS + warp : nchunks);
+            chunk = __shfl_sync(0xffffffffu, chunk, 0);
+            if (chunk >= nchunks) break;
+            const int32_t i = find_chunk_query(cincl, na, chunk);
+            const int mode = qs[amc[i]].ymode == YT_RANK ? YM_RANK : YM_GLOBAL;
+            walk_chunk<ARC, NP>(chunk, i, mode, nullptr, cincl, amc, qs, rec, arcs, cols, parcs, pk, b, key0, key1,
+                                reuse, pol, parts);
+        }
+        return;
+    }
     for (int it = 0;; it++) {
         if (threadIdx.x == 0)
             s_tile = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1ull) : (it == 0 ? (int64_t)blockIdx.x : nchunks);
@@ -300,55 +374,9 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             for (int32_t e = threadIdx.x; e < words / 4; e += WALK_THREADS) dst[e] = __ldg(src + e);
         }
         __syncthreads();
-        if (wvalid) {
-            const int32_t qi = amc[i];
-            const QState &Q = qs[qi];
-            const int64_t c0 = i == 0 ? 0 : cincl[i - 1];
-            const int64_t eta = Q.st.eta0 << b;
-            const uint64_t klo = (uint64_t)walks_lo(Q.st.eta0, b, reuse);
-            const uint32_t bkey = reuse ? 0u : (uint32_t)b;   // reuse: one sample stream per query
-            const uint32_t q = Q.gq;
-            uint64_t kk[NP];
-            bool any = false;
-#pragma unroll
-            for (int p = 0; p < NP; p++) {
-                kk[p] = klo + (uint64_t)(chunk - c0) * (32u * NP) + 32u * p + (uint64_t)lane;
-                any |= kk[p] < (uint64_t)eta;
-            }
-            double acc[2 * NP];
-            int32_t endv[2 * NP];
-            double s1 = 0.0, s2 = 0.0;
-            uint64_t ck = 0ull;
-            if (any) {
-                walk_chains<ARC, NP>(rec, arcs, cols, parcs, pk, s_mode[warp], sm_words + s_soff[warp], Q.ykeys,
-                                     Q.yrec, Q.yvals, Q.ylog2 - YB_LOG, Q.s, Q.t, Q.st.ell_f, q, bkey, kk,
-                                     key0, key1, acc, endv, pol);
-#pragma unroll
-                for (int p = 0; p < NP; p++) {
-                    if (kk[p] < (uint64_t)eta) {
-                        const double z = acc[2 * p] - acc[2 * p + 1];   // Z_k (Alg. 1 L8)
-                        s1 += z;
-                        s2 += z * z;
-                        ck += walk_hash(q, bkey, 0u, kk[p], endv[2 * p]) +
-                              walk_hash(q, bkey, 1u, kk[p], endv[2 * p + 1]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-                ck += __shfl_xor_sync(0xffffffffu, ck, o);
-            }
-            if (lane == 0) {
-                TilePart tp;
-                tp.s1 = s1;
-                tp.s2 = s2;
-                tp.ck = ck;
-                tp.pad = 0;
-                parts[chunk] = tp;
-            }
-        }
+        if (wvalid)
+            walk_chunk<ARC, NP>(chunk, i, s_mode[warp], sm_words + s_soff[warp], cincl, amc, qs, rec, arcs, cols,
+                                parcs, pk, b, key0, key1, reuse, pol, parts);
         __syncthreads();
     }
 }
