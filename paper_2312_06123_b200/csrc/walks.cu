@@ -321,6 +321,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
     const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
     const uint64_t pol = y_evict_first ? pol_evict_first() : 0;
     if (smem_words == 0) {
+        int32_t i = 0;   // a warp's chunks only increase: its query index only moves forward
         for (int it = 0;; it++) {
             int64_t chunk = 0;
             if (lane == 0)
@@ -328,7 +329,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
                                  : (it == 0 ? (int64_t)blockIdx.x * WALK_WARPS + warp : nchunks);
             chunk = __shfl_sync(0xffffffffu, chunk, 0);
             if (chunk >= nchunks) break;
-            const int32_t i = find_chunk_query(cincl, na, chunk);
+            if (cincl[i] <= chunk) i += 1 + find_chunk_query(cincl + i + 1, na - i - 1, chunk);
             const int mode = qs[amc[i]].ymode == YT_RANK ? YM_RANK : YM_GLOBAL;
             walk_chunk<ARC, NP>(chunk, i, mode, nullptr, cincl, amc, qs, rec, arcs, cols, parcs, pk, b, key0, key1,
                                 reuse, pol, parts);
