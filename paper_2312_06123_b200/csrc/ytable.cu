@@ -205,8 +205,9 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
 }
 
 // Ranks of the rank-bitmap tables: rank(record w) = popcount of all records before w.  One CTA
-// per leaving query (non-rank queries exit).
+// per leaving query (non-rank queries exit); YRANK_ITEMS consecutive records per thread per pass.
 constexpr int YRANK_THREADS = 256;
+constexpr int YRANK_ITEMS = 4;
 __global__ void __launch_bounds__(YRANK_THREADS)
 k_yrank(int32_t na, const int64_t *__restrict__ rrecs, const YDesc *__restrict__ yd)
 {
@@ -218,17 +219,24 @@ k_yrank(int32_t na, const int64_t *__restrict__ rrecs, const YDesc *__restrict__
     typedef cub::BlockScan<unsigned long long, YRANK_THREADS> Scan;
     __shared__ typename Scan::TempStorage tmp;
     unsigned long long carry = 0;   // (rank U << 32) | rank T
-    for (int64_t base = 0; base < R; base += YRANK_THREADS) {
-        const int64_t w = base + threadIdx.x;
-        const uint4 a = w < R ? aux[w] : make_uint4(0u, 0u, 0u, 0u);
-        const uint32_t ux = a.x | a.z, uy = a.y | a.w;
-        const unsigned long long c = ((unsigned long long)(__popc(ux) + __popc(uy)) << 32) |
-                                     (unsigned long long)(__popc(a.z) + __popc(a.w));
-        unsigned long long excl, tot;
+    for (int64_t base = 0; base < R; base += YRANK_THREADS * YRANK_ITEMS) {
+        const int64_t w0 = base + (int64_t)threadIdx.x * YRANK_ITEMS;
+        uint4 a[YRANK_ITEMS];
+        unsigned long long c[YRANK_ITEMS];
+#pragma unroll
+        for (int j = 0; j < YRANK_ITEMS; j++) {
+            a[j] = w0 + j < R ? aux[w0 + j] : make_uint4(0u, 0u, 0u, 0u);
+            c[j] = ((unsigned long long)(__popc(a[j].x | a[j].z) + __popc(a[j].y | a[j].w)) << 32) |
+                   (unsigned long long)(__popc(a[j].z) + __popc(a[j].w));
+        }
+        unsigned long long excl[YRANK_ITEMS], tot;
         Scan(tmp).ExclusiveSum(c, excl, tot);
-        if (w < R) {
-            const unsigned long long rk = carry + excl;
-            recs[w] = make_uint4(ux, uy, (uint32_t)(rk >> 32), (uint32_t)rk);
+#pragma unroll
+        for (int j = 0; j < YRANK_ITEMS; j++) {
+            if (w0 + j < R) {
+                const unsigned long long rk = carry + excl[j];
+                recs[w0 + j] = make_uint4(a[j].x | a[j].z, a[j].y | a[j].w, (uint32_t)(rk >> 32), (uint32_t)rk);
+            }
         }
         carry += tot;
         __syncthreads();
