@@ -110,27 +110,6 @@ def ncu_walk_summary():
     return None, None
 
 
-def random_access_ceiling(mb):
-    """Measured dependent random 8-byte load rate (G loads/s) for a working set of `mb` MB
-    (profiles/l2_ubench_r01.txt, scripts/l2_ubench.cu), linearly interpolated."""
-    pts = []
-    for p in sorted((ROOT / "profiles").glob("l2_ubench_*.txt"), reverse=True):
-        for line in p.read_text().splitlines():
-            f = line.split()
-            if len(f) >= 3 and f[1] == "MB" and not line.startswith("#"):
-                pts.append((float(f[0]), float(f[2])))
-        break
-    if not pts:
-        return None
-    pts.sort()
-    if mb <= pts[0][0]:
-        return pts[0][1]
-    for (x0, y0), (x1, y1) in zip(pts, pts[1:]):
-        if mb <= x1:
-            return y0 + (y1 - y0) * (mb - x0) / (x1 - x0)
-    return pts[-1][1]
-
-
 def cpu_baseline_leg(g, lam, pairs, eps, target_s=10.0):
     """The oracle as it stands, on the host cores, over a bounded sample of the workload."""
     import oracle
@@ -371,18 +350,20 @@ def main():
         ncu, tsrc = ncu_walk_summary() if args.config == CONFIG else (None, None)
         tps = float(ncu["dram_bytes_per_walk_step"]) if ncu else None
         traffic = tps * prof["walk_steps"] / max(prof["walk_launches"], 1) if tps else None
-        # K6 is bound by dependent random loads into L2, not by HBM bandwidth: its L1->L2 load
-        # requests per second against the measured random-load ceiling for its arc working set
+        # K6 is bound by random accesses served by L2, not by HBM bandwidth: its L2 side from the
+        # committed ncu capture of the same kernel on this config (sectors per step, and the
+        # L2 throughput ncu reports against its own peak)
         steps_s = prof["walk_steps"] / max(prof["walk_ms"] / 1e3, 1e-12)
-        arc_mb = 8.0 * float(g.offsets[-1]) / 2**20   # packed 8-byte arc records (config 1, as profiled)
-        ceil = random_access_ceiling(arc_mb)
         rand = None
-        if ncu and ceil:
-            req = steps_s * float(ncu["l1_to_l2_sectors_per_walk_step"]) / 1e9
-            rand = {"achieved_g_requests_s": req, "ceiling_g_loads_s": ceil, "frac": req / ceil,
-                    "arc_working_set_mb": arc_mb, "walk_steps_per_s": steps_s,
+        if ncu:
+            m = ncu.get("metrics", {})
+            l2pct = m.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", "").split()
+            rand = {"walk_steps_per_s": steps_s,
                     "l1_to_l2_sectors_per_step": float(ncu["l1_to_l2_sectors_per_walk_step"]),
-                    "source": f"{tsrc} + profiles/l2_ubench_r01.txt"}
+                    "l2_sectors_per_step": float(ncu["l2_sectors_per_walk_step"]),
+                    "l2_throughput_pct_of_peak": float(l2pct[0]) if l2pct else None,
+                    "l2_hit_pct": float(m.get("lts__t_sector_hit_rate.pct", "nan").split()[0]),
+                    "source": tsrc}
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
@@ -390,7 +371,7 @@ def main():
             "config": config_dict(g, args),
             "roofline": {"bound": "hbm", "kernel": "k_walks (K6, AMC walks)", "achieved": achieved,
                          "peak": hbm, "peak_kind": how, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": traffic, "traffic_source": tsrc, "random_access": rand,
+                         "traffic": traffic, "traffic_source": tsrc, "l2_side": rand,
                          "algorithmic_bytes_per_step": WALK_BYTES_PER_STEP,
                          "walk_steps_per_launch": prof["walk_steps"] / max(prof["walk_launches"], 1),
                          "avg_launch_ms": walk_launch_ms,
