@@ -362,6 +362,12 @@ void er_graph_destroy(er_graph *g)
         }
         if (g->ev_in) cudaEventDestroy(g->ev_in);
         if (g->ev_out) cudaEventDestroy(g->ev_out);
+        if (g->ybuild_stream) {
+            cudaStreamSynchronize(g->ybuild_stream);
+            cudaStreamDestroy(g->ybuild_stream);
+            cudaEventDestroy(g->ev_yfork);
+            cudaEventDestroy(g->ev_ydone);
+        }
         if (g->spmm_stream) {
             cudaStreamSynchronize(g->spmm_stream);
             cudaStreamDestroy(g->spmm_stream);

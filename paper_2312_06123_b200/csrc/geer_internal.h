@@ -161,6 +161,8 @@ struct er_graph {
     cudaStream_t amc_stream = nullptr;  // AMC groups overlap the SMM head
     cudaStream_t head_stream = nullptr; // high-priority stream of the SMM head (forked from the caller's)
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;  // fork / join with the caller's stream
+    cudaStream_t ybuild_stream = nullptr;  // K5 y-table builds concurrent with the next SMM wave
+    cudaEvent_t ev_yfork = nullptr, ev_ydone = nullptr;
     std::mutex mu;
     int64_t launches = 0;
     bool profiling = false;

@@ -676,6 +676,9 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
     if (!g->ev_in) {
         CK(cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g->ev_out, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g->ev_yfork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g->ev_ydone, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&g->ybuild_stream, cudaStreamNonBlocking));
     }
     CK(cudaEventRecord(g->ev_in, user));
     CK(cudaStreamWaitEvent(st, g->ev_in, 0));
@@ -843,6 +846,8 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         }
         bool first_wave = true;
         int wave_no = 0;
+        const cudaStream_t ystream = overlap ? nullptr : g->ybuild_stream;
+        bool y_pending = false;
         while (na > 0) {
             const int32_t nseg = (int32_t)(2 * na);
             // emission offsets
@@ -887,6 +892,10 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                 if (P.nbits <= 24) rc = smm_group<uint32_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU, &one_chunk);
                 else rc = smm_group<uint64_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU, &one_chunk);
                 if (rc) return rc;
+            }
+            if (y_pending) {   // the previous wave's y-table build reads the arrays rewritten below
+                CK(cudaStreamWaitEvent(st, g->ev_ydone, 0));
+                y_pending = false;
             }
             ENSURE(ws.nf_id, sizeof(int32_t) * E, false);
             ENSURE(ws.nf_val, sizeof(double) * E, false);
@@ -949,10 +958,26 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             const int64_t F2 = c.hp[1];
             const int64_t YH = c.hp[2], YV = c.hp[3], YR = c.hp[4];
             const int64_t U = c.hp[5];   // next-frontier entries (<= E): the grid of the passes below
-            // y-tables, then (overlap) their AMC on the AMC stream
-            rc = ytable_build(c, (int32_t)na, ws.act.as<int32_t>(), ws.nf_off.as<int64_t>(), ws.nf_id.as<int32_t>(),
-                              ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), U, dU, 1 + wave_no, YH, YV, YR);
-            if (rc) return rc;
+            // y-tables, then (overlap) their AMC on the AMC stream.  Without overlap the tables are
+            // built on a side stream concurrently with this wave's compaction and the next wave's
+            // emission and sort (both latency-bound); the next wave waits for them before it
+            // rewrites the next-frontier arrays the build reads ("K5").
+            if (ystream) {
+                CK(cudaEventRecord(g->ev_yfork, st));
+                CK(cudaStreamWaitEvent(ystream, g->ev_yfork, 0));
+                Ctx cy{g, ystream, ws, c.hp};
+                rc = ytable_build(cy, (int32_t)na, ws.act.as<int32_t>(), ws.nf_off.as<int64_t>(),
+                                  ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), U, nullptr,
+                                  1 + wave_no, YH, YV, YR);
+                if (rc) return rc;
+                CK(cudaEventRecord(g->ev_ydone, ystream));
+                y_pending = true;
+            } else {
+                rc = ytable_build(c, (int32_t)na, ws.act.as<int32_t>(), ws.nf_off.as<int64_t>(),
+                                  ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(), ws.nf_seg.as<int32_t>(), U, dU,
+                                  1 + wave_no, YH, YV, YR);
+                if (rc) return rc;
+            }
             rc = fork_group((int32_t)na, ws.act.as<int32_t>(), cont);
             if (rc) return rc;
             if (na2 > 0) {
@@ -979,6 +1004,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
     }
 
     if (!overlap) {
+        CK(cudaStreamWaitEvent(st, g->ev_ydone, 0));   // the last wave's y-tables (no-op if none)
         // every query now in phase AMC: one AMC run over all of them
         ENSURE(ws.ids, sizeof(int32_t) * (k + 1), false);
         unsigned long long *d_sum = reinterpret_cast<unsigned long long *>(ws.scalars.as<int64_t>() + 5);
