@@ -277,6 +277,10 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
             if (!strcmp(env, "cols")) layout = 0;
             if (!strcmp(env, "packed") && packable) layout = 2;
         }
+        // K6 scheduling: per-warp chunks when the walk graph is L2-resident (packed), CTA-tiles of
+        // 8 chunks when it is DRAM-resident (measured: 4.40 vs 4.56 ms on config 1, 544 vs 529 ms
+        // on config 2)
+        g->walk_tiles = layout != 2;
         if (const char *env = getenv("GEER_WALK_MINB")) { const int v = atoi(env); g->walk_minb = (v >= 3 && v <= 6) ? v : 4; }
         if (const char *env = getenv("GEER_AMC_OVERLAP")) g->amc_overlap = atoi(env) != 0;
         if (const char *env = getenv("GEER_WALK_PERSIST")) g->walk_persist = atoi(env) != 0;
@@ -291,6 +295,7 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_RANK_MIN_CAP")) g->rank_min_cap = std::max<int64_t>(0, atoll(env));
         if (const char *env = getenv("GEER_RANK_RATIO")) g->rank_ratio = std::max<int64_t>(0, atoll(env));
         if (const char *env = getenv("GEER_RANK_MAX_KB")) g->rank_max_bytes = 1024 * std::max<int64_t>(0, atoll(env));
+        if (const char *env = getenv("GEER_WALK_TILES")) g->walk_tiles = atoi(env) != 0;
         if (const char *env = getenv("GEER_WALK_CARVEOUT")) g->walk_carveout = std::min(100, std::max(-1, atoi(env)));
         g->pack.bo = bo;
         g->pack.bd = bd;

@@ -156,6 +156,7 @@ struct er_graph {
     int walk_np = 1;     // K6 walk pairs per thread (GEER_WALK_NP 1..2)
     int walk_smem_words = 0;      // K6 staging area per CTA in 32-bit words (GEER_WALK_SMEM_KB; default none:
                                   // shared memory taken from L1 costs more walk throughput than staging saves)
+    bool walk_tiles = false;      // K6: CTA-tiles of 8 chunks even without staging (GEER_WALK_TILES=1)
     int walk_carveout = -1;       // K6 preferred shared-memory carveout in % (-1: driver default; GEER_WALK_CARVEOUT)
     cudaStream_t stream = nullptr;
     cudaStream_t amc_stream = nullptr;  // AMC groups overlap the SMM head

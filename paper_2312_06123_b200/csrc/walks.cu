@@ -517,12 +517,13 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
         else if (g->d_arcs) WALK_LAUNCH(1, NP, MINB);        \
         else WALK_LAUNCH(0, NP, MINB);                       \
     } while (0)
-        const int32_t smem_words = g->walk_smem_words;
+        // smem_words: staging capacity (tile path); 0 = per-warp chunks; -1 = tile path, no staging
+        const int32_t smem_words = g->walk_smem_words > 0 ? g->walk_smem_words : (g->walk_tiles ? -1 : 0);
         // with the SMM head running concurrently (overlap), the persistent walk grid takes only a
         // fraction of the resident-CTA slots so head kernels always find room on every SM
         const bool persist = g->walk_persist;
         const double slot_frac = g->amc_overlap ? g->overlap_frac : 1.0;
-        const size_t smem_bytes = sizeof(int32_t) * (size_t)smem_words;
+        const size_t smem_bytes = sizeof(int32_t) * (size_t)std::max(smem_words, 0);
         if (g->walk_np == 1) {
             if (g->walk_minb == 3) WALK_ARC(1, 3);
             else if (g->walk_minb == 5) WALK_ARC(1, 5);
