@@ -290,7 +290,7 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
     double *vals = yb.as<double>();
     uint4 *recs = reinterpret_cast<uint4 *>(yb.as<char>() + o_rec);
     uint4 *aux = reinterpret_cast<uint4 *>(yb.as<char>() + o_aux);      // build-time {S bits, T bits}
-    int32_t *keys = reinterpret_cast<int32_t *>(yb.as<char>() + o_key);   // buckets need 32-byte alignment
+    int32_t *keys = reinterpret_cast<int32_t *>(yb.as<char>() + o_key);   // 16-byte buckets: aligned region
     k_yfill<<<blocks_for(std::max(H, R), 256), 256, 0, c.st>>>(H, keys, R, aux);
     LAUNCHED(c.g);
     ENSURE(ws.ydesc, sizeof(YDesc) * (na + 1), false);
