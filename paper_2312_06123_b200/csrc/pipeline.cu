@@ -289,11 +289,15 @@ __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const
 // K2/K3 for the first SMM iteration when every adjacency row is sorted: from s* = e_s the
 // iterate is s*(u) = (0.0 + 1.0)/d(u) on N(s) (one contribution per u), already in ascending u
 // order, so no push/sort is needed.  Same statistics as k_run_reduce.
+// u and d(u) come from the walk graph's arc records when it has them (one sequential read per
+// entry along the row of s) instead of cols + a random node-record load.
 __global__ void k_first_wave(int64_t E, int32_t nseg, const int64_t *__restrict__ ent_off,
                              const int32_t *__restrict__ fr_id, const int64_t *__restrict__ off,
-                             const uint2 *__restrict__ rec, const int32_t *__restrict__ cols, const int32_t *__restrict__ act,
-                             const QState *__restrict__ qs, int32_t *__restrict__ nid, double *__restrict__ nval,
-                             int32_t *__restrict__ nseg_out, SegStat *__restrict__ ss, int64_t *__restrict__ dU)
+                             const uint2 *__restrict__ rec, const int32_t *__restrict__ cols,
+                             const uint4 *__restrict__ arcs, const unsigned long long *__restrict__ parcs, PackSpec pk,
+                             const int32_t *__restrict__ act, const QState *__restrict__ qs, int32_t *__restrict__ nid,
+                             double *__restrict__ nval, int32_t *__restrict__ nseg_out, SegStat *__restrict__ ss,
+                             int64_t *__restrict__ dU)
 {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = p < E;
@@ -308,8 +312,21 @@ __global__ void k_first_wave(int64_t E, int32_t nseg, const int64_t *__restrict_
         }
         g = lo;
         const int32_t v = fr_id[g];
-        const int32_t u = cols[off[v] + (p - ent_off[g])];
-        const int64_t d = (int64_t)__ldg(rec + u).y;   // node record {offset, degree}
+        const int64_t a = off[v] + (p - ent_off[g]);
+        int32_t u;
+        int64_t d;
+        if (parcs) {
+            const uint4 r = pk.unpack(__ldg(parcs + a));
+            u = (int32_t)r.x;
+            d = (int64_t)r.z;
+        } else if (arcs) {
+            const uint4 r = __ldg(arcs + a);
+            u = (int32_t)r.x;
+            d = (int64_t)r.z;
+        } else {
+            u = cols[a];
+            d = (int64_t)__ldg(rec + u).y;   // node record {offset, degree}
+        }
         const double sum = 0.0 + 1.0;
         const double x = sum / (double)d;
         nid[p] = u;
@@ -908,7 +925,8 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                 if (rc) return rc;
             } else if (fast_first) {
                 k_first_wave<<<blocks_for(E, 256), 256, 0, st>>>(E, nseg, ent_off, ws.fr_id.as<int32_t>(), g->d_off,
-                                                                 g->d_rec, g->d_cols, ws.act.as<int32_t>(), qs,
+                                                                 g->d_rec, g->d_cols, g->d_arcs, g->d_parcs, g->pack,
+                                                                 ws.act.as<int32_t>(), qs,
                                                                  ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                                                                  ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>(), dU);
             } else if (P.nbits <= 24)
