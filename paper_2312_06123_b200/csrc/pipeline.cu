@@ -789,6 +789,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaEventRecord(e, st));
         CK(cudaStreamWaitEvent(sb, e, 0));
+        CK(cudaStreamWaitEvent(sb, g->ev_ydone, 0));   // the last SMM wave's y-tables (side stream)
         cudaEventDestroy(e);
         return launch_amc_group(g, sb, G, qs, P, prof, R);
     };
@@ -1022,8 +1023,8 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
     }
 
     if (!overlap) {
-        CK(cudaStreamWaitEvent(st, g->ev_ydone, 0));   // the last wave's y-tables (no-op if none)
-        // every query now in phase AMC: one AMC run over all of them
+        // every query now in phase AMC: one AMC run over all of them (the AMC stream waits for
+        // the last wave's y-tables, so this list building overlaps their build)
         ENSURE(ws.ids, sizeof(int32_t) * (k + 1), false);
         unsigned long long *d_sum = reinterpret_cast<unsigned long long *>(ws.scalars.as<int64_t>() + 5);
         CK(cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), st));
@@ -1050,6 +1051,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
     // join: results need every group's AMC
     CK(cudaEventRecord(ev_amc_done, sb));
     CK(cudaStreamWaitEvent(st, ev_amc_done, 0));
+    CK(cudaStreamWaitEvent(st, g->ev_ydone, 0));   // y-tables built even when no query reached AMC
 
     // ---- results
     double *d_out = out_r;
