@@ -425,6 +425,7 @@ def test_ytable_layouts_and_kernel_variants_byte_identical(graph, tiny, rmat20):
     outs = {}
     for env in ({"GEER_YTABLE": "hash"}, {"GEER_YTABLE": "rank"}, {}, {"GEER_RANK_MAX_KB": "0"},
                 {"GEER_WALK_SMEM_KB": "8"}, {"GEER_WALK_SMEM_KB": "24", "GEER_YTABLE": "hash"},
+                {"GEER_WALK_TILES": "1"}, {"GEER_WALK_LAYOUT": "arcs"}, {"GEER_WALK_LAYOUT": "cols"},
                 {"GEER_WALK_NP": "2"}, {"GEER_WALK_NP": "2", "GEER_WALK_MINB": "3"}, {"GEER_WALK_PERSIST": "0"},
                 {"GEER_AMC_OVERLAP": "1"}):
         e = dict(os.environ, **env)
