@@ -383,9 +383,12 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
 }
 
 // K7: one warp per AMC query: sum its chunk partials (chunk order, R13), then Alg. 1 L11-L14.
+// Also writes the chunk count of batch b+1 into nch (0 once a query stops; a query that had no
+// chunks in batch b already has 0 there), so only batch 0 needs k_nchunks.
 __global__ void k_amc_reduce(int32_t na, const int32_t *__restrict__ amc, const int64_t *__restrict__ tile_incl,
                              const TilePart *__restrict__ parts, int b, BatchParams P, QState *__restrict__ qs,
-                             unsigned long long *__restrict__ steps_counter)
+                             unsigned long long *__restrict__ steps_counter, int64_t *__restrict__ nch,
+                             int32_t per_chunk)
 {
     const int lane = threadIdx.x & 31;
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -394,6 +397,7 @@ __global__ void k_amc_reduce(int32_t na, const int32_t *__restrict__ amc, const 
     if (t1 == t0) return;   // stopped in an earlier batch
     double s1 = 0.0, s2 = 0.0;
     uint64_t ck = 0;
+#pragma unroll 4
     for (int64_t t = t0 + lane; t < t1; t += 32) {
         s1 += parts[t].s1;
         s2 += parts[t].s2;
@@ -431,6 +435,8 @@ __global__ void k_amc_reduce(int32_t na, const int32_t *__restrict__ amc, const 
     if (fabs(f - P.eps / 2.0) <= 1e-12 * P.eps) Q.st.tie_flags |= 4u;
     const bool stop = f <= P.eps / 2.0 || b == P.tau - 1;
     if (stop) Q.phase = PH_DONE;
+    const int64_t next = (Q.st.eta0 << (b + 1)) - walks_lo(Q.st.eta0, b + 1, P.reuse);
+    nch[i] = stop ? 0 : (next + per_chunk - 1) / per_chunk;
 }
 
 // ---------------------------------------------------------------------------- host side
@@ -477,8 +483,10 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
     const int nsm = g->num_sms;
     const uint32_t key0 = (uint32_t)P.seed, key1 = (uint32_t)(P.seed >> 32);
     for (int b = 0; b < P.tau; b++) {
-        k_nchunks<<<blocks_for(na, 256), 256, 0, sb>>>(na, list, qs, b, P.reuse, per_chunk, nch);
-        LAUNCHED(g);
+        if (b == 0) {   // later batches: written by the previous batch's k_amc_reduce
+            k_nchunks<<<blocks_for(na, 256), 256, 0, sb>>>(na, list, qs, b, P.reuse, per_chunk, nch);
+            LAUNCHED(g);
+        }
         size_t b2 = tbytes;
         CK(cub::DeviceScan::InclusiveSum(tmp, b2, nch, cincl, na, sb));
         g->launches += 2;
@@ -543,7 +551,8 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
             R.walk_ev.push_back(e1);
         }
         k_amc_reduce<<<blocks_for((int64_t)na * 32, 256), 256, 0, sb>>>(
-            na, list, cincl, parts, b, P, qs, prof ? reinterpret_cast<unsigned long long *>(g->d_steps) : nullptr);
+            na, list, cincl, parts, b, P, qs, prof ? reinterpret_cast<unsigned long long *>(g->d_steps) : nullptr,
+            nch, per_chunk);
         LAUNCHED(g);
     }
     CK(cudaGetLastError());
