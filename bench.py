@@ -385,7 +385,8 @@ def main():
                                    "yrank_records_per_step": prof["yrank_records"] / args.steps,
                                    "walk_ctas_per_sm": prof["walk_ctas_per_sm"],
                                    "smm_waves_per_step": prof["smm_waves"] / args.steps,
-                                   "smm_dense_waves_per_step": prof["smm_dense_waves"] / args.steps},
+                                   "smm_dense_waves_per_step": prof["smm_dense_waves"] / args.steps,
+                                   "amc_span": prof["amc_span_ms"] / args.steps},
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(pairs.nbytes),
                     "d2h_bytes_per_step": int(nq * 8)},
             "gpu_launches": int(launches),

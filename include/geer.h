@@ -242,6 +242,8 @@ typedef struct er_profile {
     int64_t smm_waves;       /* SMM waves after the first (frontier + dense) */
     int64_t smm_dense_waves; /* of which applied by the dense pull (K9) */
     int64_t smm_dense_cols;  /* block columns (2 per active query) summed over the dense waves */
+    double amc_span_ms;      /* first K6 launch start to last K6 launch end, per batch, summed (the
+                                part above walk_ms is the AMC loop's K7 / scan / launch gaps) */
 } er_profile;
 int er_graph_profile(er_graph *g, int enable);
 int er_graph_profile_read(er_graph *g, er_profile *out);

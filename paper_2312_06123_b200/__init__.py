@@ -58,7 +58,8 @@ class er_profile(ctypes.Structure):
                 ("smm_pairs", ctypes.c_int64), ("batches", ctypes.c_int64),
                 ("ytable_slots", ctypes.c_int64), ("yrank_records", ctypes.c_int64),
                 ("walk_ctas_per_sm", ctypes.c_int64), ("smm_waves", ctypes.c_int64),
-                ("smm_dense_waves", ctypes.c_int64), ("smm_dense_cols", ctypes.c_int64)]
+                ("smm_dense_waves", ctypes.c_int64), ("smm_dense_cols", ctypes.c_int64),
+                ("amc_span_ms", ctypes.c_double)]
 
 
 class GeerError(RuntimeError):

@@ -1086,6 +1086,10 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             CK(cudaEventElapsedTime(&ms, R.walk_ev[j], R.walk_ev[j + 1]));
             walk += ms;
         }
+        if (R.walk_ev.size() >= 2) {
+            CK(cudaEventElapsedTime(&ms, R.walk_ev.front(), R.walk_ev.back()));
+            g->prof.amc_span_ms += ms;
+        }
         g->prof.smm_ms += smm;
         g->prof.walk_ms += walk;
         g->prof.amc_other_ms += all - smm;   // AMC time not hidden under the SMM head
