@@ -105,7 +105,7 @@ struct Workspace {
     DevBuf nf_id, nf_val, nf_seg, nf_off;           // next frontier
     DevBuf ent_off;                                 // emission offsets per frontier entry
     DevBuf keys, vals, keys2, vals2;                // emitted (key, value) pairs + sort buffers
-    DevBuf runidx, runstart;                        // run-length reduction
+    DevBuf runstart;                                // run-length reduction: first pair of each run
     DevBuf segstat;                                 // SegStat per segment
     DevBuf ycap, yoff;                              // y-table sizes and their scans (per leaving query)
     DevBuf ydesc;                                   // K5 build-time table descriptors (per leaving query)

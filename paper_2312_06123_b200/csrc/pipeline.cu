@@ -163,29 +163,12 @@ __global__ void k_emit(int64_t E, int64_t F, const int64_t *__restrict__ ent_off
 // Run head flag of sorted position p: a key change.  The keys carry the (chunk-local) segment id
 // above the node bits and consecutive segments differ in it, so a segment start is always a
 // key change.
+// Run heads of the sorted keys: position p starts a run of equal (segment, u).
 template <class KeyT>
-struct HeadFlag {
+struct IsRunHead {
     const KeyT *keys;
-    __host__ __device__ __forceinline__ int32_t operator()(const int32_t &p) const
-    {
-        return (p == 0 || keys[p] != keys[p - 1]) ? 1 : 0;
-    }
+    __device__ __forceinline__ bool operator()(int64_t p) const { return p == 0 || keys[p] != keys[p - 1]; }
 };
-
-// runincl = inclusive scan of the head flags; runstart[r] = first position of run r;
-// runstart[U] = E; *dU = U.
-template <class KeyT>
-__global__ void k_runstart(int64_t E, const KeyT *__restrict__ keys, const int32_t *__restrict__ runincl,
-                           int64_t *__restrict__ runstart, int64_t *__restrict__ dU)
-{
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= E) return;
-    if (p == 0 || keys[p] != keys[p - 1]) runstart[runincl[p] - 1] = p;
-    if (p == E - 1) {
-        runstart[runincl[p]] = E;
-        *dU = runincl[p];
-    }
-}
 
 // First lane of each run of equal g (lanes sorted by g).
 __device__ __forceinline__ bool warp_seg_head(int32_t g)
@@ -252,7 +235,7 @@ __global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const
     int32_t g = 0x7fffffff;
     unsigned long long deg = 0, bits = 0;
     if (live) {
-        const int64_t p0 = runstart[r], p1 = runstart[r + 1];
+        const int64_t p0 = runstart[r], p1 = r + 1 < U ? runstart[r + 1] : Emax;   // the last run ends at E
         const KeyT k0 = keys[p0];
         const int32_t u = (int32_t)(k0 & (((KeyT)1 << nbits) - 1));
         if (one_chunk) {
@@ -581,7 +564,7 @@ void Workspace::release()
 {
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2,
-                     &runidx, &runstart, &segstat, &ycap, &yoff, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &cont2,
+                     &runstart, &segstat, &ycap, &yoff, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &cont2,
                      &idx2, &spmm_part, &qids, &dense_x, &dense_y, &dense_cnt, &ydesc};
     for (DevBuf *b : all) b->release();
     for (DevBuf &b : ychunk) b.release();
@@ -665,17 +648,13 @@ int smm_group(Ctx &c, int64_t E, int64_t F, int32_t nseg, const int64_t *ent_off
         });
         if (rc) return rc;
     }
-    ENSURE(ws.runidx, sizeof(int32_t) * E, false);
     ENSURE(ws.runstart, sizeof(int64_t) * (E + 1), false);
-    // run ids: scan of head flags computed on the fly from the sorted keys (no flag array)
-    cub::TransformInputIterator<int32_t, HeadFlag<KeyT>, cub::CountingInputIterator<int32_t>> heads(
-        cub::CountingInputIterator<int32_t>(0), HeadFlag<KeyT>{k2});
+    // run starts: the positions of the run heads, selected in one pass (count -> *dU)
     int rc = cub_call(c, [&](void *tmp, size_t &bytes) {
-        return cub::DeviceScan::InclusiveSum(tmp, bytes, heads, ws.runidx.as<int32_t>(), (int)E, st);
+        return cub::DeviceSelect::If(tmp, bytes, cub::CountingInputIterator<int64_t>(0), ws.runstart.as<int64_t>(), dU,
+                                     E, IsRunHead<KeyT>{k2}, st);
     });
     if (rc) return rc;
-    k_runstart<KeyT><<<blocks_for(E, 256), 256, 0, st>>>(E, k2, ws.runidx.as<int32_t>(), ws.runstart.as<int64_t>(), dU);
-    LAUNCHED(g);
     return ER_OK;
 }
 
