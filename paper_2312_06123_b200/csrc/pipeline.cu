@@ -134,28 +134,36 @@ __global__ void k_emit(int64_t E, int64_t F, const int64_t *__restrict__ ent_off
                        const int64_t *__restrict__ off, const int32_t *__restrict__ cols, KeyT *__restrict__ keys,
                        double *__restrict__ vals)
 {
-    // thread = EMIT_PER consecutive output positions: one binary search, then a linear advance
+    // warp = 32 * EMIT_PER consecutive output positions, lane l writing base + l + 32 i (coalesced
+    // key / value stores and cols loads): lane 0 binary-searches the entry of the warp's first
+    // position, then every lane steps forward from it (a warp's span crosses few entries)
     constexpr int EMIT_PER = 4;
-    const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * EMIT_PER;
-    if (p0 >= E) return;
-    int64_t lo = 0, hi = F;  // ent_off[lo] <= p0 < ent_off[hi]
-    while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (ent_off[mid] <= p0) lo = mid;
-        else hi = mid;
+    const int lane = threadIdx.x & 31;
+    const int64_t base = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * EMIT_PER;
+    if (base >= E) return;   // whole warp
+    int64_t e0 = 0;
+    if (lane == 0) {
+        int64_t lo = 0, hi = F;  // ent_off[lo] <= base < ent_off[hi]
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (ent_off[mid] <= base) lo = mid;
+            else hi = mid;
+        }
+        e0 = lo;
     }
-    int64_t e = lo, next = ent_off[e + 1];
-    int32_t v = id[e];
-    KeyT sk = (KeyT)(seg[e] % spc) << nbits;
-    const int64_t p1 = p0 + EMIT_PER < E ? p0 + EMIT_PER : E;
-    for (int64_t p = p0; p < p1; p++) {
+    int64_t e = __shfl_sync(0xffffffffu, e0, 0);
+    int64_t start = ent_off[e], next = ent_off[e + 1];
+#pragma unroll
+    for (int i = 0; i < EMIT_PER; i++) {
+        const int64_t p = base + 32 * i + lane;
+        if (p >= E) break;
         while (p >= next) {   // every frontier node has degree >= 1 (connected graph)
             e++;
+            start = next;
             next = ent_off[e + 1];
-            v = id[e];
-            sk = (KeyT)(seg[e] % spc) << nbits;
         }
-        keys[p] = sk | (KeyT)(uint32_t)cols[off[v] + (p - ent_off[e])];
+        const int32_t v = id[e];
+        keys[p] = ((KeyT)(seg[e] % spc) << nbits) | (KeyT)(uint32_t)cols[off[v] + (p - start)];
         vals[p] = val[e];
     }
 }
@@ -618,7 +626,7 @@ int smm_group(Ctx &c, int64_t E, int64_t F, int32_t nseg, const int64_t *ent_off
     ENSURE(ws.vals2, sizeof(double) * E, false);
     KeyT *k1 = ws.keys.as<KeyT>(), *k2 = ws.keys2.as<KeyT>();
     double *v1 = ws.vals.as<double>(), *v2 = ws.vals2.as<double>();
-    k_emit<KeyT><<<blocks_for((E + 3) / 4, 256), 256, 0, st>>>(E, F, ent_off, ws.fr_id.as<int32_t>(),
+    k_emit<KeyT><<<blocks_for((E + 3) / 4 + 31, 256), 256, 0, st>>>(E, F, ent_off, ws.fr_id.as<int32_t>(),
                                                                  ws.fr_val.as<double>(), ws.fr_seg.as<int32_t>(), spc,
                                                                  nbits, g->d_off, g->d_cols, k1, v1);
     LAUNCHED(g);
