@@ -20,12 +20,20 @@ namespace geer {
 //    vals[rank U + popc(U bits below v)].  Exact membership in one 16-byte load, no probing;
 //    used for tables too large to stage whose records take less than twice the hash layout's
 //    12 B/slot (keys + values).
-// Per leaving query i: hslots[i] hash slots, vslots[i] value slots, rrecs[i] rank records.
+// Per leaving query i: h hash slots, v value slots, r rank records (0 for queries that stay).
+struct YSizes {
+    int64_t h, v, r;
+};
+struct YSizesPlus {
+    __device__ __forceinline__ YSizes operator()(const YSizes &a, const YSizes &b) const
+    {
+        return YSizes{a.h + b.h, a.v + b.v, a.r + b.r};
+    }
+};
+
 __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState *__restrict__ qs,
                        const int32_t *__restrict__ cont, const int64_t *__restrict__ segoff, int64_t nrec,
-                       int force, int64_t min_cap, int64_t ratio, int64_t max_bytes, int64_t *__restrict__ hslots,
-                       int64_t *__restrict__ vslots,
-                       int64_t *__restrict__ rrecs)
+                       int force, int64_t min_cap, int64_t ratio, int64_t max_bytes, YSizes *__restrict__ sz)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
@@ -34,8 +42,6 @@ __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState
         const int64_t len = segoff[2 * i + 2] - segoff[2 * i];   // |supp s*| + |supp t*| >= |U|
         int64_t cap = YB;
         while (cap < 2 * len) cap <<= 1;
-        // rank when the table cannot be staged and the records take at most twice the hash footprint:
-        // rank lookups are pipelined off the walk chain, global hash probes are not
         // rank when the table cannot be small, its records are cheaper than twice the hash layout,
         // and they are small enough to stay mostly in L2 (large graphs: hash)
         const bool rank = force == 2 || (force == 0 && cap > min_cap && 16 * nrec < ratio * cap &&
@@ -48,9 +54,7 @@ __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState
             v = cap;
         }
     }
-    hslots[i] = h;
-    vslots[i] = v;
-    rrecs[i] = r;
+    sz[i] = YSizes{h, v, r};
 }
 
 // Build-time descriptor of leaving query i's table (a compact copy of its QState y fields,
@@ -65,14 +69,13 @@ struct YDesc {
     int32_t ds, dt;    // d(s), d(t)
 };
 
-__global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int64_t *__restrict__ hslots,
-                          const int64_t *__restrict__ hincl, const int64_t *__restrict__ vslots,
-                          const int64_t *__restrict__ vincl, const int64_t *__restrict__ rrecs,
-                          const int64_t *__restrict__ rincl, int32_t *kbase, double *vbase, uint4 *rbase,
+__global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const YSizes *__restrict__ sz,
+                          const YSizes *__restrict__ incl, int32_t *kbase, double *vbase, uint4 *rbase,
                           uint4 *abase, QState *__restrict__ qs, YDesc *__restrict__ yd)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
+    const YSizes n = sz[i], c = incl[i];
     YDesc D;
     D.mode = -1;
     D.keys = nullptr;
@@ -80,24 +83,24 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const int
     D.vals = nullptr;
     D.lgb = 0;
     D.ds = D.dt = 1;
-    if (vslots[i] != 0) {
+    if (n.v != 0) {
         QState &Q = qs[act[i]];
         D.ds = Q.ds;
         D.dt = Q.dt;
-        D.vals = vbase + (vincl[i] - vslots[i]);
+        D.vals = vbase + (c.v - n.v);
         Q.yvals = D.vals;
-        if (rrecs[i] > 0) {
+        if (n.r > 0) {
             D.mode = Q.ymode = YT_RANK;
-            D.rec = rbase + (rincl[i] - rrecs[i]);
-            D.aux = abase + (rincl[i] - rrecs[i]);
+            D.rec = rbase + (c.r - n.r);
+            D.aux = abase + (c.r - n.r);
             Q.yrec = D.rec;
             Q.yaux = D.aux;
             Q.ykeys = nullptr;
             Q.ylog2 = 0;
         } else {
-            const int64_t cap = hslots[i];
+            const int64_t cap = n.h;
             D.mode = Q.ymode = YT_HASH;
-            D.keys = kbase + (hincl[i] - cap);
+            D.keys = kbase + (c.h - cap);
             Q.ykeys = D.keys;
             Q.yrec = nullptr;
             int lg = 0;
@@ -209,13 +212,13 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
 constexpr int YRANK_THREADS = 256;
 constexpr int YRANK_ITEMS = 4;
 __global__ void __launch_bounds__(YRANK_THREADS)
-k_yrank(int32_t na, const int64_t *__restrict__ rrecs, const YDesc *__restrict__ yd)
+k_yrank(int32_t na, const YSizes *__restrict__ sz, const YDesc *__restrict__ yd)
 {
     const int32_t i = blockIdx.x;
-    if (i >= na || rrecs[i] == 0) return;
+    if (i >= na || sz[i].r == 0) return;
     uint4 *recs = yd[i].rec;
     const uint4 *aux = yd[i].aux;
-    const int64_t R = rrecs[i];
+    const int64_t R = sz[i].r;
     typedef cub::BlockScan<unsigned long long, YRANK_THREADS> Scan;
     __shared__ typename Scan::TempStorage tmp;
     unsigned long long carry = 0;   // (rank U << 32) | rank T
@@ -250,20 +253,19 @@ int ytable_plan(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, con
                 const int64_t **tot_h, const int64_t **tot_v, const int64_t **tot_r)
 {
     Workspace &ws = c.ws;
-    ENSURE(ws.ycap, sizeof(int64_t) * 3 * (na + 1), false);
-    ENSURE(ws.yoff, sizeof(int64_t) * 3 * (na + 1), false);
-    int64_t *hs = ws.ycap.as<int64_t>(), *vs = hs + (na + 1), *rs = vs + (na + 1);
-    int64_t *hi = ws.yoff.as<int64_t>(), *vi = hi + (na + 1), *ri = vi + (na + 1);
+    ENSURE(ws.ycap, sizeof(YSizes) * (na + 1), false);
+    ENSURE(ws.yoff, sizeof(YSizes) * (na + 1), false);
+    YSizes *sz = ws.ycap.as<YSizes>(), *incl = ws.yoff.as<YSizes>();
     const int64_t nrec = (c.g->n + 63) / 64;
     k_ycap<<<blocks_for(na, 256), 256, 0, c.st>>>(na, act, ws.qs.as<QState>(), cont, segoff, nrec, c.g->ytable_force,
-                                                  c.g->rank_min_cap, c.g->rank_ratio, c.g->rank_max_bytes, hs, vs, rs);
+                                                  c.g->rank_min_cap, c.g->rank_ratio, c.g->rank_max_bytes, sz);
     LAUNCHED(c.g);
-    int rc = scan_incl(c, hs, hi, na);
-    if (!rc) rc = scan_incl(c, vs, vi, na);
-    if (!rc) rc = scan_incl(c, rs, ri, na);
-    *tot_h = hi + (na - 1);
-    *tot_v = vi + (na - 1);
-    *tot_r = ri + (na - 1);
+    int rc = cub_call(c, [&](void *tmp, size_t &bytes) {   // the three size scans in one pass
+        return cub::DeviceScan::InclusiveScan(tmp, bytes, sz, incl, YSizesPlus(), (int)na, c.st);
+    });
+    *tot_h = &incl[na - 1].h;
+    *tot_v = &incl[na - 1].v;
+    *tot_r = &incl[na - 1].r;
     return rc;
 }
 
@@ -272,8 +274,7 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
                  const int32_t *seg, int64_t Fmax, const int64_t *dF, int wave, int64_t H, int64_t V, int64_t R)
 {
     Workspace &ws = c.ws;
-    int64_t *hs = ws.ycap.as<int64_t>(), *vs = hs + (na + 1), *rs = vs + (na + 1);
-    int64_t *hi = ws.yoff.as<int64_t>(), *vi = hi + (na + 1), *ri = vi + (na + 1);
+    const YSizes *sz = ws.ycap.as<YSizes>(), *incl = ws.yoff.as<YSizes>();
     if (V == 0) return ER_OK;
     if (c.g->profiling) {
         c.g->prof.ytable_slots += H;
@@ -295,12 +296,12 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
     LAUNCHED(c.g);
     ENSURE(ws.ydesc, sizeof(YDesc) * (na + 1), false);
     YDesc *yd = ws.ydesc.as<YDesc>();
-    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, hs, hi, vs, vi, rs, ri, keys, vals, recs, aux,
+    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, sz, incl, keys, vals, recs, aux,
                                                       ws.qs.as<QState>(), yd);
     LAUNCHED(c.g);
     for (int pass = 0; pass < 2; pass++) {
         if (pass == 1 && R > 0) {
-            k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, rs, yd);
+            k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, sz, yd);
             LAUNCHED(c.g);
         }
         k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, segoff, yd, pass);
