@@ -1019,8 +1019,9 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         LAUNCHED(g);
         rc = scan_incl(c, ws.cont.as<int32_t>(), ws.idx.as<int32_t>(), K);
         if (rc) return rc;
+        // the list goes to act2: the last wave's y-table build (side stream) may still read act
         k_select<<<blocks_for(K, 256), 256, 0, st>>>(K, ws.ids.as<int32_t>(), ws.cont.as<int32_t>(),
-                                                      ws.idx.as<int32_t>(), ws.act.as<int32_t>());
+                                                      ws.idx.as<int32_t>(), ws.act2.as<int32_t>());
         LAUNCHED(g);
         CK(cudaMemcpyAsync(c.hp + 0, ws.idx.as<int32_t>() + (K - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(c.hp + 1, d_sum, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -1029,7 +1030,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         const int64_t amc_eta0 = c.hp[1];
         if (prof) CK(cudaEventRecord(ev_smm_end, st));
         if (n_amc > 0) {
-            rc = launch_list((int32_t)n_amc, ws.act.as<int32_t>(), amc_eta0);
+            rc = launch_list((int32_t)n_amc, ws.act2.as<int32_t>(), amc_eta0);
             if (rc) return rc;
         }
     } else if (prof) {
