@@ -483,7 +483,8 @@ def test_full_size_configs_parity_sampled(geer, config, eps, nq):
     bench's launch configuration: sampled queries -- the first nq random pairs and the first
     nq edges of the query set, each block with its global query index base -- against the
     oracle (decisions, walk checksums exact; |r' - r'_oracle| <= 1e-9), plus the converged
-    series (er_smm_series) within eps on a few of them."""
+    series (er_smm_series) within eps on a few of them; then the bench's whole per-GPU batch,
+    whose first nq results must be the sampled ones bit for bit."""
     g, pairs, _ = W.load_config(config)
     h = geer.er_graph_create(g.n, g.offsets, g.cols)
     try:
@@ -498,6 +499,15 @@ def test_full_size_configs_parity_sampled(geer, config, eps, nq):
             ns = 20 if g.nnz < (1 << 30) else 4
             truth, _ = geer.er_smm_series(h, sub[:ns], tol=1e-7)
             assert np.abs(r[:ns] - truth).max() <= eps
+            if base == 0:
+                r0 = r
+        # the bench's own batch (one GPU's query set, all streams and overlaps as timed): its first
+        # nq results are the sampled ones bit for bit (global query indices key every walk)
+        nbench = {"lj_full": 100_000, "orkut_full": 100_000, "friendster": 125_000}[config]
+        big = np.ascontiguousarray(pairs[:nbench])
+        rb, _ = geer.er_query_batch_ex(h, big, eps, 0.01)
+        assert np.isfinite(rb).all()
+        assert rb[:nq].tobytes() == r0.tobytes()
     finally:
         geer.er_graph_destroy(h)
 
