@@ -359,6 +359,8 @@ def main():
             m = ncu.get("metrics", {})
             l2pct = m.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", "").split()
             rand = {"walk_steps_per_s": steps_s,
+                    # north_star's walk evidence: the sustained random 32-byte sector rate
+                    "random_sectors_per_s": steps_s * float(ncu["l1_to_l2_sectors_per_walk_step"]),
                     "l1_to_l2_sectors_per_step": float(ncu["l1_to_l2_sectors_per_walk_step"]),
                     "l2_sectors_per_step": float(ncu["l2_sectors_per_walk_step"]),
                     "l2_throughput_pct_of_peak": float(l2pct[0]) if l2pct else None,
