@@ -740,8 +740,9 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
     int64_t smm_pairs = 0;
     int rc;
 
-    // AMC stream: each group's walks run concurrently with the SMM waves of the queries still in
-    // the head ("Overlap").
+    // AMC stream: the walks of all AMC queries after the head (default), or, with
+    // GEER_AMC_OVERLAP=1, each wave's leavers concurrently with the remaining SMM waves
+    // (measured slower).
     cudaStream_t sb = g->amc_stream;
     cudaEvent_t ev_start = nullptr, ev_smm_end = nullptr, ev_end = nullptr, ev_amc_done = nullptr;
     const bool prof = g->profiling;
@@ -753,9 +754,8 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         CK(cudaEventCreate(&ev_end));
         CK(cudaEventRecord(ev_start, st));
     }
-    // the AMC stream starts after everything enqueued so far on the main stream (inputs, setup)
-    // Launch the AMC of a list of queries (all in phase PH_AMC with their y-tables built) on the
-    // AMC stream, after everything enqueued so far on the main stream.
+    // Launch the AMC of a list of queries (all in phase PH_AMC) on the AMC stream, after
+    // everything enqueued so far on the head stream and after the y-table builds.
     auto launch_list = [&](int32_t ng, const int32_t *list_src, int64_t known_eta0_sum = -1) -> int {
         AmcGroup G;
         G.na = ng;
