@@ -163,7 +163,7 @@ __global__ void k_emit(int64_t E, int64_t F, const int64_t *__restrict__ ent_off
             next = ent_off[e + 1];
         }
         const int32_t v = id[e];
-        keys[p] = ((KeyT)(seg[e] % spc) << nbits) | (KeyT)(uint32_t)cols[off[v] + (p - start)];
+        keys[p] = ((KeyT)(seg[e] & (spc - 1)) << nbits) | (KeyT)(uint32_t)cols[off[v] + (p - start)];   // spc = 2^k
         vals[p] = val[e];
     }
 }
