@@ -155,44 +155,26 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Stage layout: HUB_ROWS rows of HUB_CB doubles (columns cb .. cb + w - 1 used).  Thread t
-// copies vector k = t % LPR of rows j = t / LPR + i RPI (all index math compile-time); the rows'
-// neighbour ids are loaded one chunk ahead into registers, so issuing a chunk never waits on a
-// cols load.
-template <int VEC, int HUB_CB>
-struct HubChunk {
-    static constexpr int HUB_ROWS = HUB_STAGE / HUB_CB;  // rows per chunk
-    static constexpr int LPR = HUB_CB / VEC;            // threads per row
-    static constexpr int RPI = SPMM_THREADS / LPR;      // rows per pass
-    static constexpr int PER = HUB_ROWS / RPI;          // passes (copies per thread) per chunk
-    int32_t u[PER];
-    __device__ __forceinline__ void load(const int32_t *__restrict__ cols, int64_t r0, int32_t m)
-    {
-#pragma unroll
-        for (int p = 0; p < PER; p++) {
-            const int32_t j = (int32_t)threadIdx.x / LPR + p * RPI;
-            u[p] = j < m ? __ldg(cols + r0 + j) : 0;
-        }
-    }
-    __device__ __forceinline__ void issue(double *dst, const double *__restrict__ X, int32_t q, int32_t cb, int32_t m,
-                                          int32_t wv)
-    {
-        const int32_t k = (int32_t)threadIdx.x % LPR;
-        if (k >= wv) return;
-#pragma unroll
-        for (int p = 0; p < PER; p++) {
-            const int32_t j = (int32_t)threadIdx.x / LPR + p * RPI;
-            if (j < m) cp_async<8 * VEC>(dst + j * HUB_CB + k * VEC, X + (int64_t)u[p] * q + cb + k * VEC);
-        }
-    }
-};
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// Warp-specialised: warp 0 consumes (lane c < w adds column c's values in CSR order), warps 1..7
+// produce (cp.async copies of the X row segments of the chunk's neighbours into the stage ring,
+// neighbour ids prefetched one chunk ahead).  Per stage s two named barriers: FULL (1 + s; the
+// producers arrive once their copies of the chunk have landed, the consumer waits) and EMPTY
+// (1 + HUB_STAGES + s; the consumer arrives when it is done with the stage, the producers wait
+// before refilling it), so the consumer's dependent-add chain never waits on a CTA-wide barrier.
+// Stage layout: HUB_ROWS rows of HUB_CB doubles (columns cb .. cb + w - 1 used).
 template <int VEC, int HUB_CB>
 __global__ void __launch_bounds__(SPMM_THREADS)
 k_spmm_hub_exact(const int32_t *__restrict__ rows, const int64_t *__restrict__ off, const int32_t *__restrict__ cols,
                  const double *__restrict__ X, double *__restrict__ Y, int32_t q, int normalize)
 {
-    constexpr int HUB_ROWS = HubChunk<VEC, HUB_CB>::HUB_ROWS;
+    constexpr int HUB_ROWS = HUB_STAGE / HUB_CB;   // rows per chunk
+    constexpr int NPT = SPMM_THREADS - 32;          // producer threads
+    constexpr int LPR = HUB_CB / VEC;               // producer threads per row
+    constexpr int RPI = NPT / LPR;                  // rows per producer pass
+    constexpr int PER = (HUB_ROWS + RPI - 1) / RPI; // passes per chunk
     extern __shared__ __align__(16) double hub_sm[];
     const int32_t v = rows[blockIdx.x];
     const int32_t cb = blockIdx.y * HUB_CB;
@@ -201,51 +183,78 @@ k_spmm_hub_exact(const int32_t *__restrict__ rows, const int64_t *__restrict__ o
     const int64_t e0 = off[v], e1 = off[v + 1];
     const int64_t nch = (e1 - e0 + HUB_ROWS - 1) / HUB_ROWS;
     auto rows_of = [&](int64_t c) { return c < nch ? (int32_t)min((int64_t)HUB_ROWS, e1 - (e0 + c * HUB_ROWS)) : 0; };
-    HubChunk<VEC, HUB_CB> hc;
-    // prologue: chunks 0 .. HUB_STAGES-2 in flight, ids of chunk HUB_STAGES-1 in registers
-#pragma unroll 1
-    for (int c = 0; c < HUB_STAGES - 1; c++) {
-        hc.load(cols, e0 + (int64_t)c * HUB_ROWS, rows_of(c));
-        hc.issue(hub_sm + c * HUB_STAGE, X, q, cb, rows_of(c), wv);
-        cp_async_commit();
-    }
-    hc.load(cols, e0 + (int64_t)(HUB_STAGES - 1) * HUB_ROWS, rows_of(HUB_STAGES - 1));
-    double acc = 0.0;
-    for (int64_t c = 0; c < nch; c++) {
-        const int64_t cn = c + HUB_STAGES - 1;   // chunk whose copies start now
-        hc.issue(hub_sm + (cn % HUB_STAGES) * HUB_STAGE, X, q, cb, rows_of(cn), wv);
-        cp_async_commit();   // one group per chunk (possibly empty): uniform group counting
-        hc.load(cols, e0 + (cn + 1) * HUB_ROWS, rows_of(cn + 1));
-        cp_async_wait<HUB_STAGES - 1>();   // this thread's copies of chunk c have landed
-        __syncthreads();                   // ... and everyone's
-        if ((int32_t)threadIdx.x < w) {
-            const double *col = hub_sm + (c % HUB_STAGES) * HUB_STAGE + threadIdx.x;
-            const int32_t m = rows_of(c);
-            // software-pipelined: the next 8 values are loaded while the current 8 are added,
-            // so the loop runs at the latency of the dependent DADD chain
-            int32_t j = 0;
-            if (m >= 8) {
-                double t[8];
+    if (threadIdx.x < 32) {
+        // consumer
+        const int lane = threadIdx.x;
+        double acc = 0.0;
+        for (int64_t c = 0; c < nch; c++) {
+            const int st = (int)(c % HUB_STAGES);
+            named_sync(1 + st, SPMM_THREADS);   // chunk c has landed
+            if (lane < w) {
+                const double *col = hub_sm + st * HUB_STAGE + lane;
+                const int32_t m = rows_of(c);
+                // software-pipelined: the next 8 values are loaded while the current 8 are added,
+                // so the loop runs at the latency of the dependent DADD chain
+                int32_t j = 0;
+                if (m >= 8) {
+                    double t[8];
 #pragma unroll
-                for (int i = 0; i < 8; i++) t[i] = col[i * HUB_CB];
-                for (j = 8; j + 8 <= m; j += 8) {
-                    double u[8];
+                    for (int i = 0; i < 8; i++) t[i] = col[i * HUB_CB];
+                    for (j = 8; j + 8 <= m; j += 8) {
+                        double u[8];
 #pragma unroll
-                    for (int i = 0; i < 8; i++) u[i] = col[(j + i) * HUB_CB];
+                        for (int i = 0; i < 8; i++) u[i] = col[(j + i) * HUB_CB];
 #pragma unroll
-                    for (int i = 0; i < 8; i++) acc += t[i];   // CSR order
+                        for (int i = 0; i < 8; i++) acc += t[i];   // CSR order
 #pragma unroll
-                    for (int i = 0; i < 8; i++) t[i] = u[i];
+                        for (int i = 0; i < 8; i++) t[i] = u[i];
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; i++) acc += t[i];
                 }
-#pragma unroll
-                for (int i = 0; i < 8; i++) acc += t[i];
+                for (; j < m; j++) acc += col[j * HUB_CB];
             }
-            for (; j < m; j++) acc += col[j * HUB_CB];
+            if (c + HUB_STAGES < nch) named_arrive(1 + HUB_STAGES + st, SPMM_THREADS);   // stage free
         }
-        __syncthreads();                   // stage c is refilled by the next iteration's issue
+        if (lane < w) Y[(int64_t)v * q + cb + lane] = normalize ? acc / (double)(e1 - e0) : acc;
+        return;
+    }
+    // producers
+    const int pt = threadIdx.x - 32;
+    const int kv = pt % LPR, jr = pt / LPR;   // vector within the row, first row
+    const bool active = jr < RPI && kv < wv;
+    int32_t u[PER];
+    auto load = [&](int64_t c) {
+        const int32_t m = rows_of(c);
+        const int64_t r0 = e0 + c * HUB_ROWS;
+#pragma unroll
+        for (int p = 0; p < PER; p++) {
+            const int32_t j = jr + p * RPI;
+            u[p] = (active && j < m) ? __ldg(cols + r0 + j) : 0;
+        }
+    };
+    load(0);
+    for (int64_t c = 0; c < nch; c++) {
+        const int st = (int)(c % HUB_STAGES);
+        if (c >= HUB_STAGES) named_sync(1 + HUB_STAGES + st, SPMM_THREADS);   // the consumer freed it
+        if (active) {
+            double *dst = hub_sm + st * HUB_STAGE;
+            const int32_t m = rows_of(c);
+#pragma unroll
+            for (int p = 0; p < PER; p++) {
+                const int32_t j = jr + p * RPI;
+                if (j < m) cp_async<8 * VEC>(dst + j * HUB_CB + kv * VEC, X + (int64_t)u[p] * q + cb + kv * VEC);
+            }
+        }
+        cp_async_commit();
+        if (c + 1 < nch) load(c + 1);   // the next chunk's ids, in flight during the copies
+        if (c >= 1) {
+            cp_async_wait<1>();   // chunk c-1's copies (this thread's) have landed
+            named_arrive(1 + (int)((c - 1) % HUB_STAGES), SPMM_THREADS);
+        }
     }
     cp_async_wait<0>();
-    if ((int32_t)threadIdx.x < w) Y[(int64_t)v * q + cb + threadIdx.x] = normalize ? acc / (double)(e1 - e0) : acc;
+    if (nch > 0) named_arrive(1 + (int)((nch - 1) % HUB_STAGES), SPMM_THREADS);
 }
 
 // Heavy row h: number of SPMM_SEG segments.
