@@ -59,7 +59,7 @@ def tiny_h(geer, tiny):
     geer.er_graph_destroy(h)
 
 
-@pytest.mark.parametrize("eps", [0.5, 0.1, 0.05])
+@pytest.mark.parametrize("eps", [0.5, 0.1, 0.05, 0.02, 0.01])
 def test_tiny_parity_and_exact(geer, tiny, tiny_h, eps):
     g, pairs = tiny
     r, st, ro, so = run_both(geer, tiny_h, g, pairs, eps)
