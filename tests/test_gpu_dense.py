@@ -41,6 +41,20 @@ def test_spmm_k9_exact_every_row(geer, q):
         geer.er_graph_destroy(h)
 
 
+def test_spmm_ex_rejects_unknown_flags(geer):
+    import ctypes
+    import torch
+    g = _hub_graph(800, 3)
+    h = geer.er_graph_create(g.n, g.offsets, g.cols, flags=geer.ER_CREATE_SPMM_ONLY)
+    try:
+        X = torch.zeros((g.n, 2), dtype=torch.float64, device="cuda")
+        Y = torch.zeros_like(X)
+        rc = geer.lib.er_spmm_ex(h, ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(Y.data_ptr()), 2, 4, None)
+        assert rc == geer.ER_EINVAL and "flags" in geer.er_last_error_message()
+    finally:
+        geer.er_graph_destroy(h)
+
+
 def _modes(geer, h, pairs, eps, **kw):
     """(r, stats, dense waves) for smm_mode = frontier, dense, auto."""
     out = {}
