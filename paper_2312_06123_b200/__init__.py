@@ -2,8 +2,10 @@
 
 Thin ctypes binding over ``libgeer.so`` (include/geer.h).  Argument marshalling
 only: every step of a query runs in the library's CUDA kernels.  There is no
-CPU fallback -- importing this package raises if the shared library is missing
-or fails to load.
+CPU fallback -- the first call into the library raises if the shared library is
+missing or fails to load.  The library is loaded lazily (on the first ABI call or
+the first access of ``lib``), so host-only modules of the package (``dist``) import
+without it.
 
 Names follow the C ABI: ``er_graph_create``, ``er_query_batch``,
 ``er_graph_destroy`` (+ ``er_query_batch_ex``, ``er_graph_set_lambda``, ...).
@@ -70,7 +72,7 @@ class GeerError(RuntimeError):
 
 def _load():
     if not LIB_PATH.exists():
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2312_06123_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python __graft_entry__.py build` "
                           "(there is no CPU fallback)")
     L = ctypes.CDLL(str(LIB_PATH))
     vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
@@ -105,12 +107,26 @@ def _load():
     return L
 
 
-lib = _load()
+_lib = None
+
+
+def _get():
+    """The loaded libgeer.so (loaded on first use; raises ImportError if it is missing)."""
+    global _lib
+    if _lib is None:
+        _lib = _load()
+    return _lib
+
+
+def __getattr__(name):   # PEP 562: ``paper_2312_06123_b200.lib`` loads the library lazily
+    if name == "lib":
+        return _get()
+    raise AttributeError(name)
 
 
 def _raise(rc: int):
     if rc != ER_OK:
-        raise GeerError(rc, lib.er_last_error_message().decode())
+        raise GeerError(rc, _get().er_last_error_message().decode())
 
 
 def _ptr(a):
@@ -121,11 +137,11 @@ def _ptr(a):
 
 
 def er_last_error() -> int:
-    return int(lib.er_last_error())
+    return int(_get().er_last_error())
 
 
 def er_last_error_message() -> str:
-    return lib.er_last_error_message().decode()
+    return _get().er_last_error_message().decode()
 
 
 ER_CREATE_SPMM_ONLY = 1
@@ -135,7 +151,7 @@ def er_graph_create(n: int, offsets, cols, flags: int = 0) -> int:
     """Copy a host CSR (int64 offsets[n+1], int32 cols) to the current CUDA device."""
     off = np.ascontiguousarray(offsets, dtype=np.int64)
     col = np.ascontiguousarray(cols, dtype=np.int32)
-    h = lib.er_graph_create_ex(int(n), off.ctypes.data_as(ctypes.c_void_p), col.ctypes.data_as(ctypes.c_void_p),
+    h = _get().er_graph_create_ex(int(n), off.ctypes.data_as(ctypes.c_void_p), col.ctypes.data_as(ctypes.c_void_p),
                                int(flags))
     if not h:
         _raise(er_last_error() or ER_ECUDA)
@@ -143,40 +159,40 @@ def er_graph_create(n: int, offsets, cols, flags: int = 0) -> int:
 
 
 def er_graph_destroy(g) -> None:
-    lib.er_graph_destroy(g)
+    _get().er_graph_destroy(g)
 
 
 def er_graph_set_lambda(g, lam: float) -> None:
-    _raise(lib.er_graph_set_lambda(g, float(lam)))
+    _raise(_get().er_graph_set_lambda(g, float(lam)))
 
 
 def er_graph_lambda(g) -> float:
     out = ctypes.c_double(0.0)
-    _raise(lib.er_graph_lambda(g, ctypes.byref(out)))
+    _raise(_get().er_graph_lambda(g, ctypes.byref(out)))
     return out.value
 
 
 def er_graph_estimate_lambda(g, iters: int = 0) -> float:
     out = ctypes.c_double(0.0)
-    _raise(lib.er_graph_estimate_lambda(g, int(iters), ctypes.byref(out)))
+    _raise(_get().er_graph_estimate_lambda(g, int(iters), ctypes.byref(out)))
     return out.value
 
 
 def er_graph_kernel_launches(g) -> int:
-    return int(lib.er_graph_kernel_launches(g))
+    return int(_get().er_graph_kernel_launches(g))
 
 
 def er_graph_num_nodes(g) -> int:
-    return int(lib.er_graph_num_nodes(g))
+    return int(_get().er_graph_num_nodes(g))
 
 
 def er_graph_num_arcs(g) -> int:
-    return int(lib.er_graph_num_arcs(g))
+    return int(_get().er_graph_num_arcs(g))
 
 
 def er_opts_default() -> er_opts:
     o = er_opts()
-    lib.er_opts_default(ctypes.byref(o))
+    _get().er_opts_default(ctypes.byref(o))
     return o
 
 
@@ -185,7 +201,7 @@ def er_query_batch(g, pairs, eps: float, p_fail: float = 0.01):
     p = np.ascontiguousarray(np.asarray(pairs, dtype=np.int32).reshape(-1, 2))
     k = p.shape[0]
     out = np.zeros(k, dtype=np.float64)
-    _raise(lib.er_query_batch(g, p.ctypes.data_as(ctypes.c_void_p), k, float(eps), float(p_fail),
+    _raise(_get().er_query_batch(g, p.ctypes.data_as(ctypes.c_void_p), k, float(eps), float(p_fail),
                               out.ctypes.data_as(ctypes.c_void_p)))
     return out
 
@@ -243,7 +259,7 @@ def er_query_batch_ex(g, pairs, eps: float, p_fail: float = 0.01, *, out=None, s
             o.query_ids = query_ids.ctypes.data_as(ctypes.c_void_p)
     if stream is not None:
         o.cuda_stream = _stream_handle(stream)
-    _raise(lib.er_query_batch_ex(g, pp, kk, float(eps), float(p_fail), ctypes.byref(o), op, sp))
+    _raise(_get().er_query_batch_ex(g, pp, kk, float(eps), float(p_fail), ctypes.byref(o), op, sp))
     return out, stats
 
 
@@ -271,9 +287,9 @@ def er_spmm(g, X, Y, normalize: bool = True, stream=None, exact: bool = False) -
     s = _stream_handle(stream)
     if exact:
         flags = (ER_SPMM_NORMALIZE if normalize else 0) | ER_SPMM_EXACT
-        _raise(lib.er_spmm_ex(g, ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(Y.data_ptr()), q, flags, s))
+        _raise(_get().er_spmm_ex(g, ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(Y.data_ptr()), q, flags, s))
     else:
-        _raise(lib.er_spmm(g, ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(Y.data_ptr()), q, int(normalize), s))
+        _raise(_get().er_spmm(g, ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(Y.data_ptr()), q, int(normalize), s))
 
 
 def er_smm_series(g, pairs, tol: float = 1e-10, max_iters: int = 100000):
@@ -283,18 +299,18 @@ def er_smm_series(g, pairs, tol: float = 1e-10, max_iters: int = 100000):
     k = p.shape[0]
     out = np.zeros(k, dtype=np.float64)
     ells = np.zeros(k, dtype=np.int32)
-    _raise(lib.er_smm_series(g, p.ctypes.data_as(ctypes.c_void_p), k, float(tol), int(max_iters),
+    _raise(_get().er_smm_series(g, p.ctypes.data_as(ctypes.c_void_p), k, float(tol), int(max_iters),
                              out.ctypes.data_as(ctypes.c_void_p), ells.ctypes.data_as(ctypes.c_void_p)))
     return out, ells
 
 
 def er_graph_profile(g, enable: bool = True) -> None:
-    _raise(lib.er_graph_profile(g, int(enable)))
+    _raise(_get().er_graph_profile(g, int(enable)))
 
 
 def er_graph_profile_read(g) -> dict:
     p = er_profile()
-    _raise(lib.er_graph_profile_read(g, ctypes.byref(p)))
+    _raise(_get().er_graph_profile_read(g, ctypes.byref(p)))
     return {f: getattr(p, f) for f, _ in er_profile._fields_}
 
 

@@ -875,10 +875,14 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             int64_t *dU = ws.scalars.as<int64_t>();
             const bool fast_first = first_wave && g->rows_sorted;
             // push (K2/K3) or dense pull (K9) for this wave (er_opts.smm_mode, R25)
+            // On unsorted adjacency lists the push (ascending source order) and the pull (CSR order)
+            // round differently, so the automatic choice, which depends on the other queries of the
+            // wave, would make a query's bits depend on batch composition: only an explicit
+            // smm_mode = 2 runs dense there.
             bool dense = false;
             if (!fast_first && o.smm_mode != 1 && na <= ER_DENSE_MAX_QUERIES &&
                 2.0 * 8.0 * (double)g->n * (double)(2 * na) <= DENSE_MAX_BYTES)
-                dense = o.smm_mode == 2 || dense_wave_pays(g, (int32_t)na, E);
+                dense = o.smm_mode == 2 || (g->rows_sorted && dense_wave_pays(g, (int32_t)na, E));
             if (prof && !fast_first) {
                 g->prof.smm_waves++;
                 if (dense) {

@@ -37,10 +37,10 @@ def geer():
 
 @pytest.fixture(scope="session")
 def rmat20(geer):
-    """BASELINE config 1 (R-MAT s20 ef5, 10k queries) with lambda from the device Lanczos
-    estimate, pinned for both the library and the oracle (R12)."""
+    """BASELINE config 1 (R-MAT s20 ef5, 10k queries) with ARPACK's lambda (the paper's
+    preprocessing), pinned for both the library and the oracle (R12)."""
     import workloads as W
-    g, pairs, eps = W.load_config("rmat20", with_lambda=False)
+    g, pairs, eps = W.load_config("rmat20", with_lambda=True)
     h = geer.er_graph_create(g.n, g.offsets, g.cols)
-    g.lam = geer.er_graph_estimate_lambda(h)
+    geer.er_graph_set_lambda(h, g.lam)
     return g, pairs, eps, h

@@ -12,6 +12,7 @@ import pytest
 
 import oracle
 import workloads as W
+from oracle import exact
 
 from test_gpu_parity import _hub_graph, compare, run_both
 
@@ -97,9 +98,10 @@ def test_hub_graph_dense_mode_parity(geer):
     """Queries at and around the hubs (rows cut into K9 segments by the non-exact order): the
     dense mode stays bit-identical to the push and to the oracle."""
     g = _hub_graph()
+    g.lam = exact.lambda_dense(g)   # the dense eigensolver's lambda on both sides (R12)
     h = geer.er_graph_create(g.n, g.offsets, g.cols)
     try:
-        g.lam = geer.er_graph_estimate_lambda(h)
+        geer.er_graph_set_lambda(h, g.lam)
         rng = np.random.default_rng(11)
         pairs = np.stack([np.r_[0, 1, 2, 3, rng.integers(0, g.n, 60)],
                           np.r_[1, 5, 3, 700, rng.integers(0, g.n, 60)]], axis=1).astype(np.int32)
@@ -157,6 +159,32 @@ def test_unsorted_rows_dense_mode_matches_oracle_order(geer, tiny):
             compare(g, pairs, r, st, ro, so, sorted_adj=True)
             r1, st1, _, _ = run_both(geer, h, g, pairs, 0.1, smm_mode=geer.SMM_FRONTIER, **kw)
             compare(g, pairs, r1, st1, ro, so, sorted_adj=False)
+    finally:
+        geer.er_graph_destroy(h)
+
+
+def test_unsorted_rows_bits_do_not_depend_on_batch(geer, tiny):
+    """Shuffled adjacency rows: with the default smm_mode (cost model), a query's bits must not
+    depend on the other queries of its batch (dist.py's sharding claim).  The automatic dense
+    switch is off on unsorted rows (the pull would sum in CSR order, the push in ascending source
+    order), so each query run alone -- where the cost model would otherwise pick the pull --
+    gives the bits it gets inside the whole batch."""
+    g0, pairs = tiny
+    rng = np.random.default_rng(19)
+    cols = g0.cols.copy()
+    for v in range(g0.n):
+        a, b = g0.offsets[v], g0.offsets[v + 1]
+        cols[a:b] = rng.permutation(cols[a:b])
+    g = W.Graph(g0.n, g0.offsets.copy(), cols, "tiny_shuffled", g0.lam)
+    h = geer.er_graph_create(g.n, g.offsets, g.cols)
+    try:
+        geer.er_graph_set_lambda(h, g.lam)
+        for kw in (dict(force_ell_b=4), dict(force_ell_b=6)):
+            rall, sall = geer.er_query_batch_ex(h, pairs, 0.05, 0.01, stats=True, **kw)
+            for i in range(0, len(pairs), 9):
+                r1, s1 = geer.er_query_batch_ex(h, pairs[i:i + 1], 0.05, 0.01, stats=True,
+                                                query_ids=np.array([i], dtype=np.int64), **kw)
+                assert r1.tobytes() == rall[i:i + 1].tobytes() and s1.tobytes() == sall[i:i + 1].tobytes(), i
     finally:
         geer.er_graph_destroy(h)
 
