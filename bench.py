@@ -1,19 +1,23 @@
 """bench.py -- GEER epsilon-approximate PER queries/s on B200 (BASELINE.json metric).
 
-Workload (BASELINE configs[1]): R-MAT scale 20, edge factor 5, (a,b,c,d) = (.57,.19,.19,.05),
-symmetrised, deduped, self-loops dropped, largest connected component, random relabel;
-10,000 queries per GPU (half uniform random pairs, half uniform random edges);
-eps = 0.1, delta = 0.01, tau = 5.  lambda from the library's device Lanczos
-estimate (preprocessing, untimed like the paper's ARPACK step).
+Graded workload (BASELINE configs[2], the configuration the metric "(1/2/4/8 B200)" is quoted
+on): LiveJournal-shaped R-MAT (s23, edge factor 4.5, (a,b,c,d) = (.57,.19,.19,.05), symmetrised,
+deduped, self-loops dropped, largest connected component, random relabel; generated on the GPU,
+n = 3.2M, 2m = 74M arcs), 100,000 queries per GPU (half uniform random pairs, half uniform random
+edges), eps = 0.1, delta = 0.01, tau = 5.  lambda is preprocessing (untimed, like
+the paper's ARPACK step): workloads.lambda_for (a fully re-orthogonalised Lanczos in
+torch), pinned on the library AND on the reference arm, so both arms run the same config.
 
-A step = one er_query_batch_ex over the rank's queries (inputs resident in HBM, results
-left in HBM), followed by the NCCL all-gather of results when N > 1.  W untimed warm-up
-steps, then K steps, each bracketed by CUDA events on the library's launch stream, with
-L2 flushed between steps (a 256 MiB write, outside the events).  value = queries of all
-ranks / max-over-ranks of the summed step time.
+A step = one er_query_batch_ex over the rank's queries (inputs resident in HBM, results left in
+HBM), followed by the all-gather of results when N > 1.  W untimed warm-up steps, then K steps,
+each bracketed by CUDA events on the library's launch stream, with L2 flushed between steps (a
+256 MiB write, outside the events; the inputs are larger than L2 anyway).  value = queries of all
+ranks / max-over-ranks of the summed step time.  e2e = the same through the C ABI with pinned HOST
+buffers (H2D pairs + D2H results inside the timed region).
 
-Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
         torchrun --nproc-per-node N bench.py --gpus N ...
+        python bench.py --plumbing-check   (no GPU: the N > 1 step plumbing with a host stand-in)
 """
 from __future__ import annotations
 
@@ -33,17 +37,45 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "eps-approx PER queries/sec (1/2/4/8 B200); SpMM HBM GB/s vs peak"
-CONFIG = "rmat20"
-WALK_BYTES_PER_STEP = 24   # off[v], off[v+1] (16 B) + cols[idx] (4 B) + y-key probe (4 B)
-SPMM_Q = 16                # columns of the K9 dense-block measurement
+CONFIG = "lj_full"          # BASELINE configs[2]
+# queries per GPU of each workload (weak scaling: every rank answers its own set)
+QUERIES_PER_GPU = {"tiny": 100, "rmat20": 10_000, "lj_full": 100_000, "orkut_full": 100_000,
+                   "friendster": 125_000, "lj": 100_000, "orkut": 100_000}
+ALG_BYTES_PER_STEP = 96     # a walk step touches at most 3 random 32-byte sectors
+SPMM_Q = 16                 # columns of the K9 dense-block measurement
 
 
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def sector_ceilings():
+    """App. A.6 random-sector ceilings measured by scripts/sector_ubench.cu (profiles/): the
+    independent random 32-byte sector rate with an L2-resident buffer (48-64 MB) and a
+    DRAM-resident one (16 GB), in G sectors/s."""
+    for p in sorted((ROOT / "profiles").glob("sector_ubench_r*.jsonl"), reverse=True):
+        rows = [json.loads(x) for x in p.read_text().splitlines() if x.strip().startswith("{")]
+        ind = {r["buffer_mb"]: r["g_sectors_per_s"] for r in rows if r.get("mode") == "independent"}
+        if not ind:
+            continue
+        l2 = max(v for k, v in ind.items() if 48 <= k <= 64) if any(48 <= k <= 64 for k in ind) else None
+        dram = ind.get(16384.0) or ind.get(16384)
+        return {"l2_g_sectors_per_s": l2, "dram_g_sectors_per_s": dram, "source": f"profiles/{p.name}"}
+    return None
+
+
+def ncu_summary(kind: str, config: str):
+    """The committed ncu --set full summary of a kernel (K6 walks / K9 spmm) on this config."""
+    for p in sorted((ROOT / "profiles").glob(f"ncu_{kind}_{config}_r*.json"), reverse=True):
+        try:
+            return json.loads(p.read_text()), f"profiles/{p.name}"
+        except Exception:
+            continue
+    return None, None
 
 
 class ClockSampler:
@@ -100,37 +132,52 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def ncu_walk_summary():
-    """K6's committed ncu --set full summary (captured on BASELINE config 1), if any."""
-    for p in sorted((ROOT / "profiles").glob("ncu_k_walks_*.json"), reverse=True):
-        try:
-            return json.loads(p.read_text()), p.name
-        except Exception:
-            continue
-    return None, None
+WORKLOAD_NAMES = {
+    "tiny": "tiny G(1000, 8/999) + spanning path + triangle",
+    "rmat20": "R-MAT s20 ef5 (.57,.19,.19,.05) LCC",
+    "lj_full": "LiveJournal-shaped R-MAT s23 ef4.5 (.57,.19,.19,.05) LCC (GPU generator)",
+    "orkut_full": "Orkut-shaped R-MAT s22 ef28 (.45,.22,.22,.11) LCC (GPU generator)",
+    "friendster": "Friendster-shaped R-MAT s27 ef13.5 (.57,.19,.19,.05) LCC (GPU generator), one GPU's shard",
+    "lj": "LiveJournal-shaped R-MAT s23 ef4.5 (.57,.19,.19,.05) LCC",
+    "orkut": "Orkut-density R-MAT s18 ef40 (.45,.22,.22,.11) LCC",
+}
 
 
-def cpu_baseline_leg(g, lam, pairs, eps, target_s=10.0):
-    """The oracle as it stands, on the host cores, over a bounded sample of the workload."""
-    import oracle
-    oracle.build()
-    k = len(pairs)
-    half = k // 2
-    n = 250
-    while True:
-        idx = np.concatenate([np.arange(0, min(n, half)), np.arange(half, half + min(n, k - half))])
-        sub = pairs[idx]
-        t0 = time.perf_counter()
-        oracle.geer_batch(g, lam, sub, eps, delta=0.01, with_stats=False)
-        dt = time.perf_counter() - t0
-        if dt >= target_s or n >= half:
-            break
-        n = min(half, int(n * max(2.0, target_s / max(dt, 1e-3) * 1.1)))
-    return {"value": len(sub) / dt, "unit": "queries/s", "cores": oracle.max_threads(), "kind": "oracle",
-            "sample": f"{len(sub)} of the {k} queries (first {len(sub)//2} random pairs + first "
-                      f"{len(sub) - len(sub)//2} edges), eps={eps}, delta=0.01, tau=5, {dt:.1f} s"}
+def config_dict(g, args, world):
+    import workloads as W
+    gseed = W.CONFIGS[args.config][1]["seed"]
+    return {"workload": f"{WORKLOAD_NAMES.get(args.config, args.config)}, {args.queries} queries/GPU "
+                        f"(50% random pairs, 50% edges), eps={args.eps}, delta=0.01, tau=5",
+            "baseline_config_index": {"tiny": 0, "rmat20": 1, "lj_full": 2, "orkut_full": 3,
+                                      "friendster": 4}.get(args.config),
+            "n": int(g.n), "m": int(g.m), "max_degree": int(g.degrees().max()),
+            "lambda": float(g.lam) if g.lam is not None else None,
+            "lambda_source": "workloads.lambda_for (ARPACK <= 2^24 arcs, else torch Lanczos with full "
+                             "re-orthogonalisation), pinned on both arms",
+            "queries_per_gpu": args.queries, "eps": args.eps, "delta": 0.01, "tau": 5,
+            "parallelism": f"queries sharded over {world} GPU(s) ({args.scaling} scaling), CSR replicated",
+            "l2": "flushed between steps (256 MiB device write outside the timed events); the graph and "
+                  "walk state exceed L2",
+            "switch_ratio": args.switch_ratio,
+            "smm_mode": {0: "auto (cost model)", 1: "frontier push", 2: "dense pull"}[args.smm_mode],
+            "seeds": {"graph": gseed, "queries": "graph seed + 1 + rank", "walks": "0x2312061232DEC0DE"}}
 
 
+def load_workload(args):
+    import workloads as W
+    g, _, _ = W.load_config(args.config, with_lambda=False)
+    return g
+
+
+def rank_pairs(g, args, rank):
+    """Weak scaling: rank r answers its own nq-query set (rank 0's set is the N=1 set), global
+    query indices [r nq, (r+1) nq) (they key the RNG streams)."""
+    import workloads as W
+    gseed = W.CONFIGS[args.config][1]["seed"]
+    return np.ascontiguousarray(W.query_pairs(g, args.queries, seed=gseed + 1 + rank)), rank * args.queries
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
 def reference_arm(args):
     """--impl reference: the oracle (CPU, host cores) on the same workload, metric and unit."""
     rank = int(os.environ.get("RANK", "0"))
@@ -139,57 +186,74 @@ def reference_arm(args):
     import oracle
     import workloads as W
     oracle.build()
-    g, pairs_all, _ = W.load_config(args.config, with_lambda=True)
-    pairs = pairs_all[: args.queries]
+    g = load_workload(args)
+    g.lam = W.lambda_for(g)
+    pairs, _ = rank_pairs(g, args, 0)
     half = len(pairs) // 2
-    ns = args.ref_sample // 2
-    sub = np.concatenate([pairs[:ns], pairs[half:half + ns]])
+    ns = max(1, args.ref_sample // 2)
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oracle.geer_batch(g, g.lam, sub, args.eps, delta=0.01, with_stats=False,
-                          query_index_base=0)
+        oracle.geer_batch(g, g.lam, pairs[:ns], args.eps, delta=0.01, with_stats=False, query_index_base=0)
+        oracle.geer_batch(g, g.lam, pairs[half:half + ns], args.eps, delta=0.01, with_stats=False,
+                          query_index_base=half)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
     tot = sum(times)
-    value = len(sub) * len(times) / tot
+    value = 2 * ns * len(times) / tot
     cores = oracle.max_threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(g, args),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(g, args, args.gpus),
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{len(sub)} of the {len(pairs)} queries per step "
-                                   f"({ns} random pairs + {ns} edges)"},
+                         "sample": f"{2 * ns} of the {len(pairs)} queries per step "
+                                   f"(first {ns} random pairs + first {ns} edges, same global indices)"},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-WORKLOAD_NAMES = {
-    "rmat20": "R-MAT s20 ef5 (.57,.19,.19,.05) LCC",
-    "lj_full": "LiveJournal-shaped R-MAT s23 ef4.5 (.57,.19,.19,.05) LCC (GPU generator)",
-    "orkut_full": "Orkut-shaped R-MAT s22 ef28 (.45,.22,.22,.11) LCC (GPU generator)",
-    "lj": "LiveJournal-shaped R-MAT s23 ef4.5 (.57,.19,.19,.05) LCC",
-    "orkut": "Orkut-density R-MAT s18 ef40 (.45,.22,.22,.11) LCC",
-}
-
-
-def config_dict(g, args):
-    return {"workload": f"{WORKLOAD_NAMES.get(args.config, args.config)}, {args.queries} queries/GPU "
-                        f"(50% random pairs, 50% edges), eps={args.eps}, delta=0.01, tau=5",
-            "n": int(g.n), "m": int(g.m), "max_degree": int(g.degrees().max()),
-            "lambda": float(g.lam) if g.lam is not None else None,
-            "queries_per_gpu": args.queries, "eps": args.eps, "delta": 0.01, "tau": 5,
-            "parallelism": f"queries sharded over {args.gpus} GPU(s), CSR replicated",
-            "l2": "flushed between steps (256 MiB device write outside the timed events)",
-            "switch_ratio": args.switch_ratio,
-            "smm_mode": {0: "auto (cost model)", 1: "frontier push", 2: "dense pull"}[args.smm_mode],
-            "seeds": {"graph": getattr(args, "graph_seed", 20231211), "queries": "graph seed + 1 + rank",
-                      "walks": "0x2312061232DEC0DE"}}
+# ------------------------------------------------------------------ cpu baseline + parity summary
+def cpu_baseline_leg(G, h, g, pairs, lo, args, target_s=15.0):
+    """The oracle as it stands, on the host cores, over a bounded sample of the workload (first n
+    random pairs + first n edges, their global indices), timed; the same run's per-query stats are
+    compared with the library's on the same queries (the sampled parity summary)."""
+    import oracle
+    oracle.build()
+    k = len(pairs)
+    half = k // 2
+    n = 50
+    while True:
+        blocks = [(0, min(n, half)), (half, min(n, k - half))]
+        t0 = time.perf_counter()
+        outs = [oracle.geer_batch(g, g.lam, pairs[b:b + m], args.eps, delta=0.01, query_index_base=lo + b)
+                for b, m in blocks]
+        dt = time.perf_counter() - t0
+        if dt >= target_s or n >= half:
+            break
+        n = min(half, int(n * max(2.0, target_s / max(dt, 1e-3) * 1.1)))
+    m_tot = sum(m for _, m in blocks)
+    # parity summary: the library on the same queries (same global indices)
+    max_err, ties, ck_eq, dec_eq = 0.0, 0, 0, 0
+    dec = ["ell", "ell_b", "batches_run", "eta0", "walks_total", "steps_total"]
+    for (b, m), (ro, so) in zip(blocks, outs):
+        r, st = G.er_query_batch_ex(h, pairs[b:b + m], args.eps, 0.01, stats=True, query_index_base=lo + b,
+                                    switch_ratio=args.switch_ratio, smm_mode=args.smm_mode)
+        max_err = max(max_err, float(np.abs(r - ro).max()))
+        ties += int(((st["tie_flags"] | so["tie_flags"]) != 0).sum())
+        ck_eq += int((st["walk_checksum"] == so["walk_checksum"]).sum())
+        dec_eq += int(np.all([st[f] == so[f] for f in dec], axis=0).sum())
+    base = {"value": m_tot / dt, "unit": "queries/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"{m_tot} of the {k} queries (first {blocks[0][1]} random pairs + first {blocks[1][1]} "
+                      f"edges, their global indices), eps={args.eps}, delta=0.01, tau=5, {dt:.1f} s"}
+    parity = {"queries": m_tot, "max_abs_diff_r": max_err, "ties": ties, "walk_checksums_equal": ck_eq,
+              "decisions_equal": dec_eq, "tolerance_r": 1e-9,
+              "note": "library vs oracle on the cpu_baseline sample, same lambda / seed / global indices"}
+    return base, parity
 
 
 def spmm_measure(G, h, g, torch, q=SPMM_Q, reps=10):
@@ -215,39 +279,170 @@ def spmm_measure(G, h, g, torch, q=SPMM_Q, reps=10):
     ms = statistics.median(times)
     # algorithmic bytes: offsets (8 B/row) + cols (4 B/arc) + X gathers (8q B/arc) + Y writes (8q B/row)
     byts = 8 * (g.n + 1) + 4 * g.nnz + 8 * q * g.nnz + 8 * q * g.n
+    del X, Y, flush
     return {"q": q, "ms": ms, "achieved_gbs": byts / ms / 1e6, "algorithmic_bytes": byts,
             "l2": "flushed before each call", "x_block_mb": g.n * q * 8 / 2**20}
 
 
+def walk_roofline(prof, args, hbm, hbm_how, max_ms, walk_graph_bytes):
+    """K6's roofline: measured random sectors/s (ncu sectors per walk step x the live walk-step
+    rate) against the matching App. A.6 ceiling -- L2 when the walk graph fits the ~64 MB of L2
+    that random accesses can use, else DRAM -- plus SURVEY 8(d)'s algorithmic bytes against HBM."""
+    launches = max(prof["walk_launches"], 1)
+    walk_launch_ms = prof["walk_ms"] / launches
+    steps_per_launch = prof["walk_steps"] / launches
+    steps_s = prof["walk_steps"] / max(prof["walk_ms"] / 1e3, 1e-12)
+    alg = {"bound": "hbm", "bytes_per_step": ALG_BYTES_PER_STEP,
+           "achieved_gbs": ALG_BYTES_PER_STEP * steps_s / 1e9, "peak_gbs": hbm, "peak_kind": hbm_how,
+           "frac": ALG_BYTES_PER_STEP * steps_s / 1e9 / hbm,
+           "note": "SURVEY 8(d): <= 3 random 32-byte sectors per step (node record, column, y probe)"}
+    ncu, nsrc = ncu_summary("k_walks", args.config)
+    ceil = sector_ceilings()
+    l2_resident = walk_graph_bytes <= 64 * 2**20
+    out = {"kernel": "k_walks (K6, AMC walks)", "walk_steps_per_s": steps_s, "avg_launch_ms": walk_launch_ms,
+           "walk_steps_per_launch": steps_per_launch, "walk_share_of_step": prof["walk_ms"] / max(max_ms, 1e-9),
+           "walk_graph_mb": walk_graph_bytes / 2**20, "hbm_algorithmic": alg}
+    if ncu and ceil:
+        if l2_resident and ceil["l2_g_sectors_per_s"]:
+            spp = float(ncu["l2_sectors_per_walk_step"])
+            peak_gs = ceil["l2_g_sectors_per_s"]
+            bound = "random_sector_l2"
+        else:
+            spp = float(ncu["dram_bytes_per_walk_step"]) / 32.0
+            peak_gs = ceil["dram_g_sectors_per_s"]
+            bound = "random_sector_dram"
+        ach = spp * steps_s * 32 / 1e9
+        out.update({"bound": bound, "achieved": ach, "peak": peak_gs * 32, "unit": "GB/s",
+                    "frac": ach / (peak_gs * 32), "sectors_per_step": spp,
+                    "achieved_g_sectors_per_s": spp * steps_s / 1e9, "peak_g_sectors_per_s": peak_gs,
+                    "peak_source": ceil["source"] + " (independent random 32-byte sector reads, "
+                                   + ("48-64 MB buffer)" if bound == "random_sector_l2" else "16 GB buffer)"),
+                    "traffic": float(ncu["dram_bytes_per_walk_step"]) * steps_per_launch,
+                    "traffic_source": nsrc,
+                    "ncu": {k: ncu.get(k) for k in ("dram_bytes_per_walk_step", "l2_sectors_per_walk_step",
+                                                     "l1_to_l2_sectors_per_walk_step")}})
+    else:
+        out.update({"bound": "hbm", "achieved": alg["achieved_gbs"], "peak": hbm, "unit": "GB/s",
+                    "frac": alg["frac"], "traffic": None,
+                    "note": "no committed ncu summary / sector ceiling for this config: algorithmic bytes vs HBM"})
+    return out
+
+
+# ------------------------------------------------------------------ the N > 1 plumbing
+class DistCtx:
+    """Process group of the run: NCCL on GPUs, gloo on request (collectives then move through
+    host tensors), nothing at N = 1."""
+
+    def __init__(self, backend: str, device):
+        import torch
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.backend = backend
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=device)
+            else:
+                dist.init_process_group("gloo")
+            self.dist = dist
+        self.torch = torch
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def gather(self, out_local, k_total):
+        """The one collective: all-gather of the fp64 results in global order (dist.gather_results)."""
+        if not self.dist:
+            return out_local
+        from paper_2312_06123_b200.dist import gather_results
+        if self.backend == "gloo" and out_local.is_cuda:
+            return gather_results(out_local.cpu(), k_total).to(out_local.device)
+        return gather_results(out_local, k_total)
+
+    def max(self, x: float) -> float:
+        if not self.dist:
+            return x
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.dist:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+def plumbing_check(args):
+    """No GPU: the N > 1 step plumbing of the GPU arm (process group, the all-gather inside every
+    timed step, the e2e gather, the max over ranks, rank-0 printing) with gloo and a host stand-in
+    for the library call (out[i] = 0.5 * global index + 1).  Prints a JSON line flagged
+    "plumbing_check" -- never a measurement."""
+    import torch
+    ctx = DistCtx("gloo", None)
+    nq = args.queries
+    lo = ctx.rank * nq
+    out = torch.zeros(nq, dtype=torch.float64)
+
+    def step():
+        out.copy_(torch.arange(lo, lo + nq, dtype=torch.float64) * 0.5 + 1.0)
+        return ctx.gather(out, nq * ctx.world)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        full = step()
+    dt = ctx.max(time.perf_counter() - t0)
+    want = torch.arange(0, nq * ctx.world, dtype=torch.float64) * 0.5 + 1.0
+    ok = bool(torch.equal(full, want))
+    if ctx.rank == 0:
+        print(json.dumps({"plumbing_check": True, "n_ranks": ctx.world, "gathered_ok": ok,
+                          "value": nq * ctx.world * args.steps / dt, "unit": "stand-in queries/s"}), flush=True)
+    ctx.close()
+    return 0 if ok else 1
+
+
+# ------------------------------------------------------------------ main (our arm)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=CONFIG, help="workload (BASELINE configs[2] = lj_full is the graded line)")
     ap.add_argument("--eps", type=float, default=0.1)
-    ap.add_argument("--queries", type=int, default=10_000)
-    ap.add_argument("--ref-sample", type=int, default=1000)
+    ap.add_argument("--queries", type=int, default=None, help="queries per GPU (default: the config's)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank its own query set; strong: one global set partitioned by the cost model")
+    ap.add_argument("--ref-sample", type=int, default=400, help="reference arm: queries per step (half random, half edges)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spmm", action="store_true")
+    ap.add_argument("--no-accuracy", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--plumbing-check", action="store_true", help="no GPU: N > 1 plumbing with a host stand-in")
     ap.add_argument("--switch-ratio", type=float, default=1.0,
                     help="variant knob (DESIGN R22): leave the SMM head iff vol > ratio * h; 1.0 = Eq. 15")
     ap.add_argument("--smm-mode", type=int, default=0, choices=[0, 1, 2],
                     help="SMM head: 0 per-wave cost model (default), 1 push only, 2 dense pull (R25)")
-    ap.add_argument("--config", default=CONFIG, help="workload (BASELINE configs[1] = rmat20 is the graded line)")
     args = ap.parse_args()
+    if args.queries is None:
+        args.queries = QUERIES_PER_GPU.get(args.config, 10_000)
+    if args.plumbing_check:
+        return plumbing_check(args)
     if args.impl == "reference":
         return reference_arm(args)
 
     import torch
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
+    import workloads as W
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev_index = local % max(torch.cuda.device_count(), 1)   # gloo runs may put several ranks on one GPU
+    torch.cuda.set_device(dev_index)
+    ctx = DistCtx(args.dist_backend, torch.device("cuda", dev_index))
+    world, rank = ctx.world, ctx.rank
     assert world == args.gpus or world == 1, "--gpus must match the launched world size"
 
     import importlib.util
@@ -256,33 +451,52 @@ def main():
     spec.loader.exec_module(bm)
     if rank == 0:
         bm.build()
-    if dist:
-        dist.barrier()
+    ctx.barrier()
     import paper_2312_06123_b200 as G
-    import workloads as W
-    from paper_2312_06123_b200.dist import gather_results
+    from paper_2312_06123_b200.dist import partition, predicted_cost, gather_partitioned
 
-    g, _, _ = W.load_config(args.config, with_lambda=False)
+    t_setup = time.perf_counter()
+    g = load_workload(args)
+    g.lam = W.lambda_for(g)
+    torch.cuda.empty_cache()
     nq = args.queries
-    # rank r answers its own 10k-query set (weak scaling); rank 0's set is the N=1 set
-    gseed = W.CONFIGS[args.config][1]["seed"]
-    args.graph_seed = gseed
-    pairs = np.ascontiguousarray(W.query_pairs(g, nq, seed=gseed + 1 + rank))
-    lo = rank * nq
+    if args.scaling == "weak":
+        pairs, lo = rank_pairs(g, args, rank)
+        qids = None
+        k_total = nq * world
+    else:
+        # strong: one fixed global list (the config's query count, e.g. configs[4]'s 1M), split by the
+        # deterministic cost-model partition every rank computes identically (dist.partition)
+        gseed = W.CONFIGS[args.config][1]["seed"]
+        k_total = W.CONFIGS[args.config][2]
+        allp = np.ascontiguousarray(W.query_pairs(g, k_total, seed=gseed + 1))
+        parts = partition(predicted_cost(allp, g.degrees(), g.lam, args.eps), world)
+        idx = parts[rank]
+        pairs = np.ascontiguousarray(allp[idx])
+        qids = torch.from_numpy(idx.astype(np.int64)).cuda()
+        lo = 0
+        nq = len(idx)
     h = G.er_graph_create(g.n, g.offsets, g.cols)
-    g.lam = G.er_graph_estimate_lambda(h)
+    G.er_graph_set_lambda(h, g.lam)
+    setup_s = time.perf_counter() - t_setup
 
     st = torch.cuda.Stream()
     pairs_d = torch.from_numpy(pairs).cuda()
     out_d = torch.zeros(nq, dtype=torch.float64, device="cuda")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
+    qkw = dict(switch_ratio=args.switch_ratio, smm_mode=args.smm_mode)
 
     def step():
-        G.er_query_batch_ex(h, pairs_d, args.eps, 0.01, out=out_d, stream=st, query_index_base=lo,
-                            switch_ratio=args.switch_ratio, smm_mode=args.smm_mode)
-        if dist:
+        if qids is None:
+            G.er_query_batch_ex(h, pairs_d, args.eps, 0.01, out=out_d, stream=st, query_index_base=lo, **qkw)
+        else:
+            G.er_query_batch_ex(h, pairs_d, args.eps, 0.01, out=out_d, stream=st, query_ids=qids, **qkw)
+        if ctx.dist:
             with torch.cuda.stream(st):
-                gather_results(out_d, nq * world)
+                if qids is None:
+                    ctx.gather(out_d, k_total)
+                else:
+                    gather_partitioned(out_d if args.dist_backend == "nccl" else out_d.cpu(), parts)
 
     for _ in range(args.warmup):
         step()
@@ -290,14 +504,13 @@ def main():
 
     uuid = None
     try:
-        uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(dev_index).uuid)
     except Exception:
         pass
     clocks = ClockSampler(uuid)
     G.er_graph_profile(h, True)
     l0 = G.er_graph_kernel_launches(h)
-    if dist:
-        dist.barrier()
+    ctx.barrier()
     torch.cuda.synchronize()
     total_ms = 0.0
     for _ in range(args.steps):
@@ -309,127 +522,138 @@ def main():
         e1.record(st)
         st.synchronize()
         total_ms += e0.elapsed_time(e1)
-    if dist:
-        dist.barrier()
+    ctx.barrier()
     torch.cuda.synchronize()
     launches = G.er_graph_kernel_launches(h) - l0
     prof = G.er_graph_profile_read(h)
     G.er_graph_profile(h, False)
     clk = clocks.stop()
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
-    value = nq * world * args.steps / (max_ms / 1000.0)
+    max_ms = ctx.max(total_ms)
+    value = k_total * args.steps / (max_ms / 1000.0)
 
     # ---- e2e: the plain C-ABI call with HOST buffers (H2D pairs + D2H results inside), pinned
     host_pairs = torch.from_numpy(np.ascontiguousarray(pairs)).pin_memory()
     host_out = torch.empty(nq, dtype=torch.float64).pin_memory()
+    host_ids = None if qids is None else qids.cpu().numpy()
     e2e_times = []
     for _ in range(args.steps):
         with torch.cuda.stream(st):
             flush.fill_(2)
         st.synchronize()
-        if dist:
-            dist.barrier()
+        ctx.barrier()
         t0 = time.perf_counter()
-        r = G.er_query_batch_ex(h, host_pairs, args.eps, 0.01, out=host_out, query_index_base=lo,
-                                switch_ratio=args.switch_ratio, smm_mode=args.smm_mode)[0]
-        if dist:
-            gather_results(r.cuda(), nq * world).cpu()
+        if host_ids is None:
+            r = G.er_query_batch_ex(h, host_pairs, args.eps, 0.01, out=host_out, query_index_base=lo, **qkw)[0]
+        else:
+            r = G.er_query_batch_ex(h, host_pairs, args.eps, 0.01, out=host_out, query_ids=host_ids, **qkw)[0]
+        if ctx.dist:
+            if qids is None:
+                ctx.gather(torch.as_tensor(r).cuda(), k_total).cpu()
+            else:
+                gather_partitioned(torch.as_tensor(r).cuda() if args.dist_backend == "nccl" else torch.as_tensor(r),
+                                   parts).cpu()
         e2e_times.append(time.perf_counter() - t0)
-    te = torch.tensor([sum(e2e_times)], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = nq * world * args.steps / float(te.item())
+    e2e_value = k_total * args.steps / ctx.max(sum(e2e_times))
 
+    # ---- random pairs and edges separately (P:616 splits them; same global indices as the batch)
+    split = None
+    if args.scaling == "weak":
+        half = nq // 2
+        split = {}
+        for name, (a, b) in {"random_pairs": (0, half), "edges": (half, nq)}.items():
+            ms = 0.0
+            for _ in range(2):
+                with torch.cuda.stream(st):
+                    flush.fill_(4)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                G.er_query_batch_ex(h, pairs_d[a:b], args.eps, 0.01, out=out_d[a:b], stream=st,
+                                    query_index_base=lo + a, **qkw)
+                e1.record(st)
+                st.synchronize()
+                ms += e0.elapsed_time(e1)
+            ms = ctx.max(ms)
+            split[name] = {"queries_per_gpu": b - a, "value": (b - a) * world * 2 / (ms / 1000.0),
+                           "unit": "queries/s", "ms_per_call": ms / 2}
+
+    line = None
     if rank == 0:
         hbm, how = peaks()
-        walk_launch_ms = prof["walk_ms"] / max(prof["walk_launches"], 1)
-        bytes_per_launch = WALK_BYTES_PER_STEP * prof["walk_steps"] / max(prof["walk_launches"], 1)
-        achieved = bytes_per_launch / (walk_launch_ms / 1e3) / 1e9 if walk_launch_ms > 0 else 0.0
-        ncu, tsrc = ncu_walk_summary() if args.config == CONFIG else (None, None)
-        tps = float(ncu["dram_bytes_per_walk_step"]) if ncu else None
-        traffic = tps * prof["walk_steps"] / max(prof["walk_launches"], 1) if tps else None
-        # K6 is bound by random accesses served by L2, not by HBM bandwidth: its L2 side from the
-        # committed ncu capture of the same kernel on this config (sectors per step, and the
-        # L2 throughput ncu reports against its own peak)
-        steps_s = prof["walk_steps"] / max(prof["walk_ms"] / 1e3, 1e-12)
-        rand = None
-        if ncu:
-            m = ncu.get("metrics", {})
-            l2pct = m.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", "").split()
-            rand = {"walk_steps_per_s": steps_s,
-                    # north_star's walk evidence: the sustained random 32-byte sector rate
-                    "random_sectors_per_s": steps_s * float(ncu["l1_to_l2_sectors_per_walk_step"]),
-                    "l1_to_l2_sectors_per_step": float(ncu["l1_to_l2_sectors_per_walk_step"]),
-                    "l2_sectors_per_step": float(ncu["l2_sectors_per_walk_step"]),
-                    "l2_throughput_pct_of_peak": float(l2pct[0]) if l2pct else None,
-                    "l2_hit_pct": float(m.get("lts__t_sector_hit_rate.pct", "nan").split()[0]),
-                    "source": tsrc}
+        walk_graph_bytes = prof["walk_graph_bytes"]
+        roof = walk_roofline(prof, args, hbm, how, max_ms, walk_graph_bytes)
+        smm_alg = 12.0 * prof["smm_pairs"]   # 4 B column + 8 B value per edge visit
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(g, args),
-            "roofline": {"bound": "hbm", "kernel": "k_walks (K6, AMC walks)", "achieved": achieved,
-                         "peak": hbm, "peak_kind": how, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": traffic, "traffic_source": tsrc, "l2_side": rand,
-                         "algorithmic_bytes_per_step": WALK_BYTES_PER_STEP,
-                         "walk_steps_per_launch": prof["walk_steps"] / max(prof["walk_launches"], 1),
-                         "avg_launch_ms": walk_launch_ms,
-                         "walk_share_of_step": prof["walk_ms"] / max(max_ms, 1e-9)},
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(g, args, world),
+            "roofline": roof,
             "phases_ms_per_step": {"smm_head": prof["smm_ms"] / args.steps,
                                    "walks": prof["walk_ms"] / args.steps,
-                                   "amc_reduce_etc": prof["amc_other_ms"] / args.steps,
+                                   "amc_after_head": prof["amc_other_ms"] / args.steps,
+                                   "amc_span": prof["amc_span_ms"] / args.steps,
                                    "smm_pairs_per_step": prof["smm_pairs"] / args.steps,
                                    "walk_steps_per_step": prof["walk_steps"] / args.steps,
                                    "ytable_slots_per_step": prof["ytable_slots"] / args.steps,
                                    "yrank_records_per_step": prof["yrank_records"] / args.steps,
                                    "walk_ctas_per_sm": prof["walk_ctas_per_sm"],
                                    "smm_waves_per_step": prof["smm_waves"] / args.steps,
-                                   "smm_dense_waves_per_step": prof["smm_dense_waves"] / args.steps,
-                                   "amc_span": prof["amc_span_ms"] / args.steps},
+                                   "smm_dense_waves_per_step": prof["smm_dense_waves"] / args.steps},
+            "smm_head_spmm": {"algorithmic_bytes_per_step": smm_alg / args.steps,
+                              "algorithmic_gbs": smm_alg / max(prof["smm_ms"] / 1e3, 1e-12) / 1e9,
+                              "note": "SURVEY 8(d): 12 B per push pair (column + value), over the SMM head's "
+                                      "event time (push, grouping, stats, y-tables)"},
+            "queries_split": split,
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(pairs.nbytes),
                     "d2h_bytes_per_step": int(nq * 8)},
             "gpu_launches": int(launches),
             "clocks": clk,
+            "setup_s": setup_s,
         }
+    if rank == 0 and not args.no_spmm:
         try:
-            if args.no_spmm:
-                raise RuntimeError("skipped (--no-spmm)")
-            sp = spmm_measure(G, h, g, torch)
-            sp.update({"peak": hbm, "frac": sp["achieved_gbs"] / hbm})
+            hbm, _ = peaks()
+            sp = {}
+            for q in (SPMM_Q, 64):
+                r_ = spmm_measure(G, h, g, torch, q=q)
+                r_.update({"peak": hbm, "frac": r_["achieved_gbs"] / hbm})
+                nc, ns_ = ncu_summary(f"k_spmm_q{q}", args.config)
+                if nc:
+                    r_["ncu_dram_gbs"] = nc.get("dram_gbs")
+                    r_["ncu_dram_frac"] = nc.get("dram_gbs", 0) / hbm
+                    r_["ncu_source"] = ns_
+                sp[f"q{q}"] = r_
             line["spmm"] = sp
-            sp64 = spmm_measure(G, h, g, torch, q=64)
-            sp64.update({"peak": hbm, "frac": sp64["achieved_gbs"] / hbm})
-            line["spmm_q64"] = sp64
+            torch.cuda.empty_cache()
         except Exception as ex:  # noqa: BLE001
             line["spmm"] = {"error": str(ex)}
+    if rank == 0 and not args.no_accuracy:
         try:
             # the paper's accuracy protocol: 100 random pairs + 100 edges against the
             # deterministic series run to a 1e-8 tail (er_smm_series, K9 passes)
             half = nq // 2
-            na_ = 100 if g.nnz < (1 << 30) else 20   # billion-arc graphs: 20 + 20 (each series pass reads all arcs)
+            na_ = 100 if g.nnz < (1 << 30) else 20
             sub = np.concatenate([pairs[:na_], pairs[half:half + na_]])
             t0 = time.perf_counter()
             truth, ells = G.er_smm_series(h, sub, tol=1e-8)
             t_truth = time.perf_counter() - t0
-            est = G.er_query_batch_ex(h, sub, args.eps, 0.01, query_index_base=lo,
-                                      switch_ratio=args.switch_ratio, smm_mode=args.smm_mode)[0]
+            est = np.concatenate([
+                G.er_query_batch_ex(h, pairs[:na_], args.eps, 0.01, query_index_base=lo, **qkw)[0],
+                G.er_query_batch_ex(h, pairs[half:half + na_], args.eps, 0.01, query_index_base=lo + half, **qkw)[0]])
             err = np.abs(est - truth)
             line["accuracy"] = {"queries": int(len(sub)), "eps": args.eps, "max_abs_err": float(err.max()),
                                 "mean_abs_err": float(err.mean()), "frac_within_eps": float(np.mean(err <= args.eps)),
                                 "truth": "er_smm_series tol 1e-8 (Thm 3.1 tail), L mean %.0f, %.2f s" % (ells.mean(), t_truth)}
         except Exception as ex:  # noqa: BLE001
             line["accuracy"] = {"error": str(ex)}
-        if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline_leg(g, g.lam, pairs, args.eps)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.scaling == "weak":
+        base, parity = cpu_baseline_leg(G, h, g, pairs, lo, args)
+        line["cpu_baseline"] = base
+        line["parity_summary"] = parity
+    if rank == 0:
         print(json.dumps(line), flush=True)
     G.er_graph_destroy(h)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+    ctx.close()
     return 0
 
 

@@ -244,6 +244,9 @@ typedef struct er_profile {
     int64_t smm_dense_cols;  /* block columns (2 per active query) summed over the dense waves */
     double amc_span_ms;      /* first K6 launch start to last K6 launch end, per batch, summed (the
                                 part above walk_ms is the AMC loop's K7 / scan / launch gaps) */
+    int64_t walk_graph_bytes; /* bytes of the walk graph K6 reads (layout below), for the roofline */
+    int32_t walk_layout;     /* 0: cols + node records, 1: 16-byte arc records, 2: packed 8-byte arc records */
+    int32_t pad_;
 } er_profile;
 int er_graph_profile(er_graph *g, int enable);
 int er_graph_profile_read(er_graph *g, er_profile *out);

@@ -61,7 +61,8 @@ class er_profile(ctypes.Structure):
                 ("ytable_slots", ctypes.c_int64), ("yrank_records", ctypes.c_int64),
                 ("walk_ctas_per_sm", ctypes.c_int64), ("smm_waves", ctypes.c_int64),
                 ("smm_dense_waves", ctypes.c_int64), ("smm_dense_cols", ctypes.c_int64),
-                ("amc_span_ms", ctypes.c_double)]
+                ("amc_span_ms", ctypes.c_double), ("walk_graph_bytes", ctypes.c_int64),
+                ("walk_layout", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 class GeerError(RuntimeError):

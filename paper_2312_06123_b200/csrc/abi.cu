@@ -563,6 +563,8 @@ int er_graph_profile_read(er_graph *g, er_profile *out)
     std::lock_guard<std::mutex> lk(g->mu);
     *out = g->prof;
     out->walk_ctas_per_sm = g->walk_occ;
+    out->walk_layout = g->d_parcs ? 2 : g->d_arcs ? 1 : 0;
+    out->walk_graph_bytes = g->d_parcs ? 8 * g->nnz : g->d_arcs ? 16 * g->nnz : 4 * g->nnz + 8 * g->n;
     if (g->d_steps) {
         int64_t steps = 0;
         cudaError_t e = cudaMemcpy(&steps, g->d_steps, sizeof(int64_t), cudaMemcpyDeviceToHost);

@@ -61,7 +61,8 @@ int main(void) {
   O(er_opts, pairs_on_device); O(er_opts, synchronous); O(er_opts, query_ids);
   O(er_opts, switch_ratio); O(er_opts, reuse_samples); O(er_opts, smm_mode);
   printf("profile %zu\n", sizeof(er_profile));
-  O(er_profile, walk_ctas_per_sm); O(er_profile, smm_dense_waves);
+  O(er_profile, walk_ctas_per_sm); O(er_profile, smm_dense_waves); O(er_profile, walk_graph_bytes);
+  O(er_profile, walk_layout);
   return 0;
 }''')
     exe = tmp_path / "layout"
@@ -78,7 +79,7 @@ int main(void) {
               "switch_ratio", "reuse_samples", "smm_mode"):
         assert vals[f] == getattr(o, f).offset, f
     assert vals["profile"] == ctypes.sizeof(G.er_profile)
-    for f in ("walk_ctas_per_sm", "smm_dense_waves"):
+    for f in ("walk_ctas_per_sm", "smm_dense_waves", "walk_graph_bytes", "walk_layout"):
         assert vals[f] == getattr(G.er_profile, f).offset, f
 
 

@@ -38,3 +38,23 @@ def test_reference_arm_other_ranks_are_silent():
     p = _run({"RANK": "1", "WORLD_SIZE": "2"}, "--config", "tiny", "--steps", "1", "--warmup", "0")
     assert p.returncode == 0, p.stderr[-2000:]
     assert not [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_plumbing_check_two_ranks_gloo():
+    """bench.py's N > 1 step plumbing (process group, the all-gather inside each timed step, the
+    max over ranks, rank-0 printing) under torchrun with 2 ranks on gloo, a host stand-in for the
+    library call.  The gathered results must equal every rank's stand-in values in global order."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
+                        "--plumbing-check", "--gpus", "2", "--queries", "1001", "--steps", "3", "--warmup", "1"],
+                       capture_output=True, text=True, cwd=str(ROOT), timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["plumbing_check"] is True and d["n_ranks"] == 2 and d["gathered_ok"] is True

@@ -431,6 +431,9 @@ def lambda_torch(g: Graph, m: int = 240, device: str | None = None, mem_gb: floa
             k = j + 1
             break
         V[j + 1] = w / b
+    del N, V, w, u1, d, isd, crow
+    if dev.type == "cuda":
+        torch.cuda.empty_cache()
     T = np.diag(alpha[:k]) + np.diag(beta[: k - 1], 1) + np.diag(beta[: k - 1], -1)
     theta, Y = np.linalg.eigh(T)
     i_max = int(np.argmax(np.abs(theta)))
