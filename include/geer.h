@@ -101,9 +101,13 @@ const char *er_last_error_message(void); /* human-readable message, never NULL *
 int er_graph_lambda(const er_graph *g, double *lambda_out);      /* ER_ESPECTRAL if unset */
 int er_graph_set_lambda(er_graph *g, double lambda);             /* lambda in (0, 1-1e-12] */
 /*
- * er_graph_estimate_lambda -- estimate lambda on the device (Lanczos on
- * N = D^-1/2 A D^-1/2 with sqrt(d) deflated) and pin it.
- *   iters      Krylov steps (0 = default 120)
+ * er_graph_estimate_lambda -- estimate lambda on the device and pin it (the paper's ARPACK
+ * preprocessing): Lanczos on N = D^-1/2 A D^-1/2 with sqrt(d) projected out and
+ * full re-orthogonalisation against the stored Krylov basis (at most 16 GB of it), stopped when
+ * both extreme Ritz pairs have converged (residual estimate < 1e-11) or after `iters` steps; the
+ * result is max over both ends of |theta| + ||N x - theta x|| with the explicit residual of the
+ * extreme Ritz vector x -- an upper estimate of max(|lambda_2|, |lambda_n|) (R12).
+ *   iters      Krylov steps at most (0 = default 500; <= 2000, further capped at 511 and by memory)
  *   lambda_out the estimate (may be NULL)
  */
 int er_graph_estimate_lambda(er_graph *g, int iters, double *lambda_out);

@@ -12,8 +12,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgeer.so"
-SOURCES = ["pipeline.cu", "ytable.cu", "walks.cu", "dense.cu", "abi.cu", "lambda.cu", "spmm.cu"]
-HEADERS = ["geer_internal.h", "geer_device.cuh", "stages.h"]
+SOURCES = ["pipeline.cu", "smm_push.cu", "ytable.cu", "walks.cu", "dense.cu", "abi.cu", "lambda.cu", "spmm.cu"]
+HEADERS = ["geer_internal.h", "geer_device.cuh", "stages.h", "scan.cuh"]
 INCLUDE = PKG.parent / "include" / "geer.h"
 
 NVCC_FLAGS = [

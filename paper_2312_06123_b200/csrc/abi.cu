@@ -271,7 +271,13 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         const double pack_foot = 8.0 * (double)g->nnz;
         int layout = 0;  // 0 cols, 1 arcs16, 2 packed
         if (packable && pack_foot <= 0.75 * (double)l2) layout = 2;
-        else if (cols_foot > 0.5 * (double)l2) layout = 1;
+        (void)cols_foot;
+        // DRAM-resident graphs keep cols + node records: a random DRAM access moves a 128-byte line
+        // whatever the record size (profiles/sector_ubench_r02.jsonl, ncu: 127 B per 8-byte load),
+        // so the smaller 4-byte column array wins by its higher L2 hit rate (LJ-shaped config:
+        // 495 vs 517 ms of walks per step, profiles/exp_layout_lj_r02.jsonl); its arc loads are
+        // evict-first in L2 so they do not push out the y-tables and node records
+        if (layout == 0) g->arc_policy = 1;
         if (const char *env = getenv("GEER_WALK_LAYOUT")) {
             if (!strcmp(env, "arcs")) layout = 1;
             if (!strcmp(env, "cols")) layout = 0;
@@ -286,9 +292,13 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_WALK_PERSIST")) g->walk_persist = atoi(env) != 0;
         if (const char *env = getenv("GEER_YTABLE")) g->ytable_force = !strcmp(env, "hash") ? 1 : !strcmp(env, "rank") ? 2 : 0;
         if (const char *env = getenv("GEER_Y_EVICT_FIRST")) g->y_evict_first = atoi(env) != 0;
+        if (const char *env = getenv("GEER_Y_POLICY")) g->y_evict_first = std::min(2, std::max(0, atoi(env)));
+        if (const char *env = getenv("GEER_ARC_POLICY")) g->arc_policy = std::min(2, std::max(0, atoi(env)));
+        if (const char *env = getenv("GEER_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(env));
         if (const char *env = getenv("GEER_L2_PERSIST")) g->l2_persist = atoi(env) != 0;
         if (const char *env = getenv("GEER_OVERLAP_FRAC")) g->overlap_frac = std::min(1.0, std::max(0.1, atof(env)));
         if (const char *env = getenv("GEER_MAX_SUB_BATCH")) g->max_sub_batch = std::max<int64_t>(1, atoll(env));
+        if (const char *env = getenv("GEER_WAVE_PAIRS_MAX")) g->wave_pairs_max = std::max<int64_t>(1, atoll(env));
         if (const char *env = getenv("GEER_WALK_NP")) g->walk_np = atoi(env) == 1 ? 1 : 2;
         if (const char *env = getenv("GEER_HUB_CB")) { const int v = atoi(env); g->hub_cb = (v == 8 || v == 16) ? v : 32; }
         if (const char *env = getenv("GEER_WALK_SMEM_KB")) g->walk_smem_words = 256 * std::min(48, std::max(0, atoi(env)));
@@ -527,7 +537,7 @@ int er_graph_estimate_lambda(er_graph *g, int iters, double *lambda_out)
     if (iters < 0 || iters > 2000) { set_error(ER_EINVAL, "iters must be in [0,2000]"); return ER_EINVAL; }
     std::lock_guard<std::mutex> lk(g->mu);
     double lam = 0.0;
-    const int rc = run_estimate_lambda(g, iters == 0 ? 120 : iters, &lam);
+    const int rc = run_estimate_lambda(g, iters == 0 ? 500 : iters, &lam);
     if (rc) return rc;
     if (!(lam > 0.0 && lam <= 1.0 - 1e-12)) {
         set_error(ER_ESPECTRAL, "estimated lambda outside (0, 1-1e-12]");

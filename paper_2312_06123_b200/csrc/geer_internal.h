@@ -116,6 +116,9 @@ struct Workspace {
     DevBuf qids;                                    // device copy of er_opts.query_ids
     std::vector<DevBuf> ychunk;                     // y-tables of each SMM wave (grow-only, kept)
     DevBuf ids, seglen, segbeg;                     // 0..k-1 ids; compaction lengths; sort segments
+    DevBuf pk_seg, pk_bkt, pk_keys, pk_alt, pk_out; // SMM push (smm_push.cu): plan, buckets, keys, outputs
+    int64_t pk_nbmax = 0, pk_e = 0, pk_F = 0;       // the current push chunk's bucket bound and pair count,
+                                                    // the wave's frontier entry count
     void *host_pinned = nullptr;                    // small pinned host scalars
     size_t host_pinned_cap = 0;
     void release();
@@ -149,10 +152,12 @@ struct er_graph {
     int64_t rank_max_bytes = 960 << 10;  // ... and when the records take at most this, i.e. graphs up to
                                          // ~3.9M nodes (GEER_RANK_MAX_KB; measured on configs 1-4)
     int ytable_force = 0;  // y-table layout: 0 by footprint, 1 hash only, 2 rank bitmap only (GEER_YTABLE)
-    int y_evict_first = 0; // K6: L2 evict-first policy on y-table loads (GEER_Y_EVICT_FIRST)
+    int y_evict_first = 0; // K6: L2 policy on y-table loads: 0 none, 1 evict-first, 2 evict-last (GEER_Y_POLICY)
+    int arc_policy = 0;    // K6: arc loads 0 plain, 1 L2 evict-first, 2 + no L1 allocation (GEER_ARC_POLICY)
     bool l2_persist = false; // K6: persisting-L2 access window over the walk graph (GEER_L2_PERSIST)
     size_t l2_window = 0, l2_persist_bytes = 0;
     int64_t max_sub_batch = 1 << 18;  // queries per internal sub-batch (GEER_MAX_SUB_BATCH)
+    int64_t wave_pairs_max = (int64_t)1 << 28;  // SMM push: pairs per chunk of a wave (GEER_WAVE_PAIRS_MAX)
     int walk_np = 1;     // K6 walk pairs per thread (GEER_WALK_NP 1..2)
     int walk_smem_words = 0;      // K6 staging area per CTA in 32-bit words (GEER_WALK_SMEM_KB; default none:
                                   // shared memory taken from L1 costs more walk throughput than staging saves)

@@ -4,10 +4,11 @@
 // Per batch of k queries:
 //   K1 k_setup            ell (Eq. 6), r_b^0, phase per query            Alg. 3 L1-L4
 //   SMM waves, each:      s* <- P s*, t* <- P t* for every active query   Alg. 3 L6-L8
-//     K2 k_emit           push (u, x(v)) for v in frontier, u in N(v)
-//        CUB radix sort   stable sort by (segment, u) on packed keys, chunked by segments
-//     K3 k_run_reduce     ordered sequential sum per (segment, u), / d(u)
-//     K4 (fused in K3) + k_seg_max2  vol, top-2, x(s), x(t) per segment  Eq. 10, Eq. 15
+//     wave 1              k_first_wave: closed form x'(u) = 1/d(u) on N(s) (sorted rows)
+//     K2/K3 push          smm_push.cu: bucketed push (u, e) -> per-bucket radix sort in shared
+//                         memory -> ordered sequential sum per (segment, u), / d(u); K4 stats
+//                         (vol, top-2, x(s), x(t)) per bucket, merged per segment
+//     or dense pull       dense.cu + K9 exact, chosen per wave by a cost model (R25)
 //        k_decide         r_b += term; psi -> eta* -> eta0 -> h; switch   Alg. 3 L7, L9
 //     K5 k_yinsert        y = s*/d_s - t*/d_t into a per-query table      Alg. 1 L7
 //        (+ k_yrank)      (hash, or rank bitmap for large supports)
@@ -19,6 +20,7 @@
 //
 // Everything is deterministic: no floating-point atomics, fixed reduction orders.
 
+#include <array>
 #include <cmath>
 #include <cstring>
 
@@ -115,68 +117,15 @@ __global__ void k_ent_deg(int64_t F, const int32_t *__restrict__ id, const int64
     deg[e] = off[v + 1] - off[v];
 }
 
-// Segment begins in the emission order: segbeg[g] = ent_off[segoff[g]] (g = 0..nseg).
-__global__ void k_segbeg(int32_t nseg, const int64_t *__restrict__ segoff, const int64_t *__restrict__ ent_off,
-                         int32_t *__restrict__ segbeg)
-{
-    const int32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g > nseg) return;
-    segbeg[g] = (int32_t)ent_off[segoff[g]];
-}
 
-// K2: push.  Output position p belongs to entry e = max{e : ent_off[e] <= p}; the pair is
-// (key = (seg mod spc) << nbits | u, value = x(v)) with u the (p - ent_off[e])-th neighbour of
-// v.  Pairs are written in frontier order: segment by segment, ascending v inside a segment.
-// Segments are sorted in chunks of spc segments, so the chunk-local segment id fits the key.
-template <class KeyT>
-__global__ void k_emit(int64_t E, int64_t F, const int64_t *__restrict__ ent_off, const int32_t *__restrict__ id,
-                       const double *__restrict__ val, const int32_t *__restrict__ seg, int64_t spc, int nbits,
-                       const int64_t *__restrict__ off, const int32_t *__restrict__ cols, KeyT *__restrict__ keys,
-                       double *__restrict__ vals)
+// Pair offset of the first pair of each active query's segments (wave splitting: chunks of
+// whole queries): pe[i] = ent_off[fr_off[2 i]], i = 0..na.
+__global__ void k_query_pairs(int32_t na, const int64_t *__restrict__ fr_off, const int64_t *__restrict__ ent_off,
+                              int64_t *__restrict__ pe)
 {
-    // warp = 32 * EMIT_PER consecutive output positions, lane l writing base + l + 32 i (coalesced
-    // key / value stores and cols loads): lane 0 binary-searches the entry of the warp's first
-    // position, then every lane steps forward from it (a warp's span crosses few entries)
-    constexpr int EMIT_PER = 4;
-    const int lane = threadIdx.x & 31;
-    const int64_t base = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * EMIT_PER;
-    if (base >= E) return;   // whole warp
-    int64_t e0 = 0;
-    if (lane == 0) {
-        int64_t lo = 0, hi = F;  // ent_off[lo] <= base < ent_off[hi]
-        while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (ent_off[mid] <= base) lo = mid;
-            else hi = mid;
-        }
-        e0 = lo;
-    }
-    int64_t e = __shfl_sync(0xffffffffu, e0, 0);
-    int64_t start = ent_off[e], next = ent_off[e + 1];
-#pragma unroll
-    for (int i = 0; i < EMIT_PER; i++) {
-        const int64_t p = base + 32 * i + lane;
-        if (p >= E) break;
-        while (p >= next) {   // every frontier node has degree >= 1 (connected graph)
-            e++;
-            start = next;
-            next = ent_off[e + 1];
-        }
-        const int32_t v = id[e];
-        keys[p] = ((KeyT)(seg[e] & (spc - 1)) << nbits) | (KeyT)(uint32_t)cols[off[v] + (p - start)];   // spc = 2^k
-        vals[p] = val[e];
-    }
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i <= na) pe[i] = ent_off[fr_off[2 * i]];
 }
-
-// Run head flag of sorted position p: a key change.  The keys carry the (chunk-local) segment id
-// above the node bits and consecutive segments differ in it, so a segment start is always a
-// key change.
-// Run heads of the sorted keys: position p starts a run of equal (segment, u).
-template <class KeyT>
-struct IsRunHead {
-    const KeyT *keys;
-    __device__ __forceinline__ bool operator()(int64_t p) const { return p == 0 || keys[p] != keys[p - 1]; }
-};
 
 // First lane of each run of equal g (lanes sorted by g).
 __device__ __forceinline__ bool warp_seg_head(int32_t g)
@@ -222,60 +171,6 @@ struct OpAdd {
 struct OpMax {
     __device__ unsigned long long operator()(unsigned long long x, unsigned long long y) const { return x > y ? x : y; }
 };
-
-// K3 + K4a: x'(u) = (sum of the run, sequential in ascending source order) / d(u) (R1, R13),
-// fused with the segment statistics that are order-independent: vol = sum d(u) (int64 add),
-// max1 (max of non-negative doubles as uint64 bit patterns), x(s), x(t) (single writers).
-template <class KeyT>
-__global__ void k_run_reduce(int64_t Emax, const int64_t *__restrict__ dU, const int64_t *__restrict__ runstart,
-                             const KeyT *__restrict__ keys, int nbits, int one_chunk, const double *__restrict__ vals,
-                             const int32_t *__restrict__ segbeg, int32_t nseg, const uint2 *__restrict__ rec,
-                             const int32_t *__restrict__ act, const QState *__restrict__ qs,
-                             int32_t *__restrict__ nid, double *__restrict__ nval, int32_t *__restrict__ nseg_out,
-                             SegStat *__restrict__ ss)
-{
-    // grid-stride over the U <= Emax runs (the grid is sized for the resident CTAs, U is known
-    // on the device only); the loop bound is block-uniform, so warps stay converged
-    const int64_t U = min(Emax, *dU);
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < U; base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = base + threadIdx.x;
-    const bool live = r < U;
-    int32_t g = 0x7fffffff;
-    unsigned long long deg = 0, bits = 0;
-    if (live) {
-        const int64_t p0 = runstart[r], p1 = r + 1 < U ? runstart[r + 1] : Emax;   // the last run ends at E
-        const KeyT k0 = keys[p0];
-        const int32_t u = (int32_t)(k0 & (((KeyT)1 << nbits) - 1));
-        if (one_chunk) {
-            g = (int32_t)(k0 >> nbits);   // all segments in one sort chunk: the key holds g
-        } else {
-            int32_t lo = 0, hi = nseg;  // segbeg[lo] <= p0 < segbeg[hi]
-            while (hi - lo > 1) {
-                const int32_t mid = (lo + hi) >> 1;
-                if (segbeg[mid] <= p0) lo = mid;
-                else hi = mid;
-            }
-            g = lo;
-        }
-        double sum = 0.0;
-        for (int64_t p = p0; p < p1; p++) sum += vals[p];   // ascending source order (R13)
-        const int64_t d = (int64_t)__ldg(rec + u).y;   // node record {offset, degree}
-        const double x = sum / (double)d;
-        nid[r] = u;
-        nval[r] = x;
-        nseg_out[r] = g;
-        deg = (unsigned long long)d;
-        bits = (unsigned long long)__double_as_longlong(x);
-        const QState &Q = qs[act[g >> 1]];
-        if (u == Q.s) ss[g].at_s = x;
-        if (u == Q.t) ss[g].at_t = x;
-    }
-    if (warp_seg_reduce2(deg, bits, g, OpAdd(), OpMax()) && live) {
-        atomicAdd(reinterpret_cast<unsigned long long *>(&ss[g].vol), deg);
-        atomicMax(reinterpret_cast<unsigned long long *>(&ss[g].max1), bits);
-    }
-    }
-}
 
 // K2/K3 for the first SMM iteration when every adjacency row is sorted: from s* = e_s the
 // iterate is s*(u) = (0.0 + 1.0)/d(u) on N(s) (one contribution per u), already in ascending u
@@ -573,7 +468,8 @@ void Workspace::release()
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2,
                      &runstart, &segstat, &ycap, &yoff, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &cont2,
-                     &idx2, &spmm_part, &qids, &dense_x, &dense_y, &dense_cnt, &ydesc};
+                     &idx2, &spmm_part, &qids, &dense_x, &dense_y, &dense_cnt, &ydesc, &pk_seg, &pk_bkt, &pk_keys,
+                     &pk_alt, &pk_out};
     for (DevBuf *b : all) b->release();
     for (DevBuf &b : ychunk) b.release();
     ychunk.clear();
@@ -603,68 +499,6 @@ int select_list(Ctx &c, const int32_t *ids, const int32_t *flag, int32_t n, int3
     return ER_OK;
 }
 
-
-// Emit + group one SMM wave: pairs (key, x(v)) sorted by (segment, u), stable (ascending v
-// kept inside each (segment, u) run), then run heads / starts.  Segments are sorted in chunks
-// of spc = 2^(keybits - nbits) segments with one radix sort per chunk over only the
-// significant key bits; the result is in ws.keys2 / ws.vals2.
-template <class KeyT>
-int smm_group(Ctx &c, int64_t E, int64_t F, int32_t nseg, const int64_t *ent_off, const int32_t *segbeg, int nbits,
-              int64_t *dU, int *one_chunk)
-{
-    Workspace &ws = c.ws;
-    er_graph *g = c.g;
-    cudaStream_t st = c.st;
-    const int keybits = (int)(8 * sizeof(KeyT));
-    int gb = 1;
-    while ((1ll << gb) < nseg) gb++;
-    const int cbits = std::min(gb, keybits - nbits);
-    const int64_t spc = (int64_t)1 << cbits;
-    ENSURE(ws.keys, sizeof(KeyT) * E, false);
-    ENSURE(ws.keys2, sizeof(KeyT) * E, false);
-    ENSURE(ws.vals, sizeof(double) * E, false);
-    ENSURE(ws.vals2, sizeof(double) * E, false);
-    KeyT *k1 = ws.keys.as<KeyT>(), *k2 = ws.keys2.as<KeyT>();
-    double *v1 = ws.vals.as<double>(), *v2 = ws.vals2.as<double>();
-    k_emit<KeyT><<<blocks_for((E + 3) / 4 + 31, 256), 256, 0, st>>>(E, F, ent_off, ws.fr_id.as<int32_t>(),
-                                                                 ws.fr_val.as<double>(), ws.fr_seg.as<int32_t>(), spc,
-                                                                 nbits, g->d_off, g->d_cols, k1, v1);
-    LAUNCHED(g);
-    // chunk boundaries in emission order (segbeg on the host: nseg+1 int32)
-    const int32_t nchunks = (int32_t)((nseg + spc - 1) / spc);
-    *one_chunk = nchunks == 1 ? 1 : 0;
-    std::vector<int32_t> hb(nchunks + 1);
-    if (nchunks == 1) {
-        hb[0] = 0;                 // one chunk: all E pairs (no host read)
-        hb[1] = (int32_t)E;
-    } else {
-        for (int32_t ch = 0; ch <= nchunks; ch++) {
-            const int64_t gs = std::min<int64_t>((int64_t)ch * spc, nseg);
-            CK(cudaMemcpyAsync(&hb[ch], segbeg + gs, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        }
-        CK(cudaStreamSynchronize(st));
-    }
-    for (int32_t ch = 0; ch < nchunks; ch++) {
-        const int64_t lo = hb[ch], n = (int64_t)hb[ch + 1] - hb[ch];
-        if (n <= 0) continue;
-        const int64_t segs = std::min<int64_t>(spc, nseg - (int64_t)ch * spc);
-        int cb = 1;
-        while ((1ll << cb) < segs) cb++;
-        const int end_bit = nbits + cb;
-        int rc = cub_call(c, [&](void *tmp, size_t &bytes) {
-            return cub::DeviceRadixSort::SortPairs(tmp, bytes, k1 + lo, k2 + lo, v1 + lo, v2 + lo, (int)n, 0, end_bit, st);
-        });
-        if (rc) return rc;
-    }
-    ENSURE(ws.runstart, sizeof(int64_t) * (E + 1), false);
-    // run starts: the positions of the run heads, selected in one pass (count -> *dU)
-    int rc = cub_call(c, [&](void *tmp, size_t &bytes) {
-        return cub::DeviceSelect::If(tmp, bytes, cub::CountingInputIterator<int64_t>(0), ws.runstart.as<int64_t>(), dU,
-                                     E, IsRunHead<KeyT>{k2}, st);
-    });
-    if (rc) return rc;
-    return ER_OK;
-}
 
 }  // namespace
 
@@ -867,10 +701,6 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
             if (rc) return rc;
             const int64_t E = c.hp[0];
             smm_pairs += E;
-            if (E > (int64_t)INT32_MAX) {
-                set_error(ER_ENOMEM, "SMM wave emits more than 2^31 pairs");
-                return ER_ENOMEM;
-            }
             ENSURE(ws.scalars, sizeof(int64_t) * 8, false);
             int64_t *dU = ws.scalars.as<int64_t>();
             const bool fast_first = first_wave && g->rows_sorted;
@@ -891,15 +721,33 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                 }
             }
             if (dense) smm_pairs -= E;   // no push pairs
-            int32_t *segbeg = nullptr;
-            int one_chunk = 0;
-            if (!fast_first && !dense) {
-                ENSURE(ws.segbeg, sizeof(int32_t) * (nseg + 1), false);
-                segbeg = ws.segbeg.as<int32_t>();
-                k_segbeg<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, ws.fr_off.as<int64_t>(), ent_off, segbeg);
-                LAUNCHED(g);
-                if (P.nbits <= 24) rc = smm_group<uint32_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU, &one_chunk);
-                else rc = smm_group<uint64_t>(c, E, F, nseg, ent_off, segbeg, P.nbits, dU, &one_chunk);
+            const bool push = !fast_first && !dense;
+            // push chunks {first segment, segments, first pair, pairs}: whole queries, at most
+            // wave_pairs_max pairs each unless one query alone has more
+            std::vector<std::array<int64_t, 4>> chunks;
+            if (push) {
+                ws.pk_F = F;
+                if (E <= g->wave_pairs_max) {
+                    chunks.push_back({0, (int64_t)nseg, 0, E});
+                } else {
+                    ENSURE(ws.seglen, sizeof(int64_t) * (na + 1), false);
+                    int64_t *pe = ws.seglen.as<int64_t>();
+                    k_query_pairs<<<blocks_for(na + 1, 256), 256, 0, st>>>((int32_t)na, ws.fr_off.as<int64_t>(),
+                                                                          ent_off, pe);
+                    LAUNCHED(g);
+                    std::vector<int64_t> hpe(na + 1);
+                    CK(cudaMemcpyAsync(hpe.data(), pe, sizeof(int64_t) * (na + 1), cudaMemcpyDeviceToHost, st));
+                    CK(cudaStreamSynchronize(st));
+                    int64_t q0 = 0;
+                    while (q0 < na) {
+                        int64_t q1 = q0 + 1;
+                        while (q1 < na && hpe[q1 + 1] - hpe[q0] <= g->wave_pairs_max) q1++;
+                        chunks.push_back({2 * q0, 2 * (q1 - q0), hpe[q0], hpe[q1] - hpe[q0]});
+                        q0 = q1;
+                    }
+                }
+                // part A of the first chunk: reads the frontier, writes the push workspaces only
+                rc = smm_push_wave_a(c, (int32_t)chunks[0][0], (int32_t)chunks[0][1], chunks[0][2], chunks[0][3], ent_off);
                 if (rc) return rc;
             }
             if (y_pending) {   // the previous wave's y-table build reads the arrays rewritten below
@@ -921,23 +769,26 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
                                                                  ws.act.as<int32_t>(), qs,
                                                                  ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
                                                                  ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>(), dU);
-            } else if (P.nbits <= 24)
-                k_run_reduce<uint32_t><<<resident_grid(g, E, 256), 256, 0, st>>>(
-                    E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint32_t>(), P.nbits, one_chunk, ws.vals2.as<double>(), segbeg,
-                    nseg, g->d_rec, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
-                    ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>());
-            else
-                k_run_reduce<uint64_t><<<resident_grid(g, E, 256), 256, 0, st>>>(
-                    E, dU, ws.runstart.as<int64_t>(), ws.keys2.as<uint64_t>(), P.nbits, one_chunk, ws.vals2.as<double>(), segbeg,
-                    nseg, g->d_rec, ws.act.as<int32_t>(), qs, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),
-                    ws.nf_seg.as<int32_t>(), ws.segstat.as<SegStat>());
-            if (!dense) LAUNCHED(g);
-            k_seg_max2<<<resident_grid(g, E, 256), 256, 0, st>>>(E, dU, ws.nf_seg.as<int32_t>(), ws.nf_val.as<double>(),
-                                                           ws.segstat.as<SegStat>());
-            LAUNCHED(g);
-            k_seg_off<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, dU, ws.nf_seg.as<int32_t>(),
-                                                                 ws.nf_off.as<int64_t>());
-            LAUNCHED(g);
+                LAUNCHED(g);
+            } else {   // part B: statistics and the contiguous next frontier; then the other chunks
+                for (size_t ch = 0; ch < chunks.size(); ch++) {
+                    if (ch > 0) {
+                        rc = smm_push_wave_a(c, (int32_t)chunks[ch][0], (int32_t)chunks[ch][1], chunks[ch][2],
+                                             chunks[ch][3], ent_off);
+                        if (rc) return rc;
+                    }
+                    rc = smm_push_wave_b(c, (int32_t)chunks[ch][0], (int32_t)chunks[ch][1], dU);
+                    if (rc) return rc;
+                }
+            }
+            if (!push) {   // first wave / dense: max2 and the segment offsets of the next frontier
+                k_seg_max2<<<resident_grid(g, E, 256), 256, 0, st>>>(E, dU, ws.nf_seg.as<int32_t>(),
+                                                                     ws.nf_val.as<double>(), ws.segstat.as<SegStat>());
+                LAUNCHED(g);
+                k_seg_off<<<blocks_for(nseg + 1, 256), 256, 0, st>>>(nseg, dU, ws.nf_seg.as<int32_t>(),
+                                                                     ws.nf_off.as<int64_t>());
+                LAUNCHED(g);
+            }
             int32_t *cont = ws.cont.as<int32_t>();
             k_decide<<<blocks_for(na, 128), 128, 0, st>>>((int32_t)na, ws.act.as<int32_t>(), ws.segstat.as<SegStat>(),
                                                           P, qs, cont);

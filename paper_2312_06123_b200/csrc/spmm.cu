@@ -25,7 +25,6 @@
 //  * heavy-row segment sums go to a scratch block and a second kernel adds them per row.
 // No tensor cores: the contraction has one nonzero per (row, neighbour) and fp64 accumulation.
 
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -257,39 +256,8 @@ k_spmm_hub_exact(const int32_t *__restrict__ rows, const int64_t *__restrict__ o
     if (nch > 0) named_arrive(1 + (int)((nch - 1) % HUB_STAGES), SPMM_THREADS);
 }
 
-// Heavy row h: number of SPMM_SEG segments.
-__global__ void k_hseg_count(int64_t nheavy, const int32_t *__restrict__ rows, const int64_t *__restrict__ off,
-                             int64_t *__restrict__ cnt)
-{
-    const int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (h >= nheavy) return;
-    const int32_t v = rows[h];
-    cnt[h] = (off[v + 1] - off[v] + SPMM_SEG - 1) / SPMM_SEG;
-}
 
-__global__ void k_deg_key(int64_t n, const int64_t *__restrict__ off, uint32_t *__restrict__ key,
-                          int32_t *__restrict__ ids)
-{
-    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    const int64_t d = off[v + 1] - off[v];
-    key[v] = ~(uint32_t)std::min<int64_t>(d, 0xffffffffll);   // descending degree
-    ids[v] = (int32_t)v;
-}
 
-// Segment table of the heavy rows (the first nheavy rows of the permutation): hseg[h] = first
-// segment of heavy row h (exclusive prefix of ceil(d / SPMM_SEG)).
-__global__ void k_fill_segs(int64_t nheavy, const int32_t *__restrict__ rows, const int64_t *__restrict__ hseg,
-                            const int64_t *__restrict__ off, int64_t *__restrict__ seg_e0, int32_t *__restrict__ seg_row)
-{
-    const int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (h >= nheavy) return;
-    const int32_t v = rows[h];
-    for (int64_t p = hseg[h]; p < hseg[h + 1]; p++) {
-        seg_e0[p] = off[v] + (p - hseg[h]) * SPMM_SEG;
-        seg_row[p] = v;
-    }
-}
 
 #define CK(call)                                            \
     do {                                                    \
@@ -298,68 +266,50 @@ __global__ void k_fill_segs(int64_t nheavy, const int32_t *__restrict__ rows, co
     } while (0)
 
 // Degree-descending row permutation (stable: equal degrees keep ascending ids), the heavy
-// prefix (degree > SPMM_SEG) and its segment table.
+// prefix (degree > SPMM_SEG) and its segment table: a counting sort by degree on the host over a
+// copy of the offsets (once per graph, at the first K9 call).
 int build_spmm_plan(er_graph *g, cudaStream_t st)
 {
     const int64_t n = g->n;
-    uint32_t *k1 = nullptr, *k2 = nullptr;
-    int32_t *ids = nullptr;
-    void *tmp = nullptr;
-    size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k2, ids, g->d_rowperm, (int)n, 0, 32, st));
-    CK(cudaMalloc(&g->d_rowperm, sizeof(int32_t) * n));
-    CK(cudaMallocAsync((void **)&k1, sizeof(uint32_t) * n, st));
-    CK(cudaMallocAsync((void **)&k2, sizeof(uint32_t) * n, st));
-    CK(cudaMallocAsync((void **)&ids, sizeof(int32_t) * n, st));
-    CK(cudaMallocAsync(&tmp, tb + 16, st));
-    k_deg_key<<<blocks_for(n, 256), 256, 0, st>>>(n, g->d_off, k1, ids);
-    g->launches++;
-    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k2, ids, g->d_rowperm, (int)n, 0, 32, st));
-    g->launches += 2;
-    CK(cudaFreeAsync(k1, st));
-    CK(cudaFreeAsync(k2, st));
-    CK(cudaFreeAsync(ids, st));
-    CK(cudaFreeAsync(tmp, st));
+    std::vector<int64_t> off(n + 1);
     CK(cudaStreamSynchronize(st));
-    // heavy prefix: rows are degree-descending, binary search for the first degree <= SPMM_SEG
-    int64_t lo = 0, hi = n;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        int32_t v = 0;
-        int64_t o[2];
-        CK(cudaMemcpy(&v, g->d_rowperm + mid, sizeof(int32_t), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(o, g->d_off + v, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
-        if (o[1] - o[0] <= SPMM_SEG) hi = mid;
-        else lo = mid + 1;
+    CK(cudaMemcpy(off.data(), g->d_off, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+    int64_t md = 0;
+    for (int64_t v = 0; v < n; v++) md = std::max<int64_t>(md, off[v + 1] - off[v]);
+    std::vector<int64_t> pos(md + 2, 0);   // pos[d] = first slot of degree d (descending order)
+    for (int64_t v = 0; v < n; v++) pos[off[v + 1] - off[v]]++;
+    int64_t run = 0;
+    for (int64_t d = md; d >= 0; d--) {
+        const int64_t c = pos[d];
+        pos[d] = run;
+        run += c;
     }
-    const int64_t nh = lo;
+    std::vector<int32_t> perm(n);
+    for (int64_t v = 0; v < n; v++) perm[pos[off[v + 1] - off[v]]++] = (int32_t)v;
+    int64_t nh = 0;
+    while (nh < n && off[perm[nh] + 1] - off[perm[nh]] > SPMM_SEG) nh++;
+    std::vector<int64_t> hseg(nh + 1, 0), seg_e0;
+    std::vector<int32_t> seg_row;
+    for (int64_t h = 0; h < nh; h++) {
+        const int32_t v = perm[h];
+        const int64_t d = off[v + 1] - off[v], ns = (d + SPMM_SEG - 1) / SPMM_SEG;
+        hseg[h + 1] = hseg[h] + ns;
+        for (int64_t p = 0; p < ns; p++) {
+            seg_e0.push_back(off[v] + p * SPMM_SEG);
+            seg_row.push_back(v);
+        }
+    }
+    CK(cudaMalloc(&g->d_rowperm, sizeof(int32_t) * n));
+    CK(cudaMemcpy(g->d_rowperm, perm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
     g->n_heavy = nh;
-    g->n_seg = 0;
+    g->n_seg = (int64_t)seg_e0.size();
     if (nh > 0) {
-        // hseg = exclusive prefix of the heavy rows' segment counts (on the device)
-        int64_t *cnt = nullptr;
         CK(cudaMalloc(&g->d_hseg, sizeof(int64_t) * (nh + 1)));
-        CK(cudaMallocAsync((void **)&cnt, sizeof(int64_t) * nh, st));
-        k_hseg_count<<<blocks_for(nh, 256), 256, 0, st>>>(nh, g->d_rowperm, g->d_off, cnt);
-        g->launches++;
-        size_t sb = 0;
-        CK(cub::DeviceScan::InclusiveSum(nullptr, sb, cnt, g->d_hseg + 1, (int)nh, st));
-        CK(cudaMallocAsync(&tmp, sb + 16, st));
-        CK(cudaMemsetAsync(g->d_hseg, 0, sizeof(int64_t), st));
-        CK(cub::DeviceScan::InclusiveSum(tmp, sb, cnt, g->d_hseg + 1, (int)nh, st));
-        g->launches += 2;
-        CK(cudaFreeAsync(tmp, st));
-        CK(cudaFreeAsync(cnt, st));
-        int64_t ns = 0;
-        CK(cudaMemcpyAsync(&ns, g->d_hseg + nh, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        g->n_seg = ns;
-        CK(cudaMalloc(&g->d_seg_e0, sizeof(int64_t) * ns));
-        CK(cudaMalloc(&g->d_seg_row, sizeof(int32_t) * ns));
-        k_fill_segs<<<blocks_for(nh, 128), 128, 0, st>>>(nh, g->d_rowperm, g->d_hseg, g->d_off, g->d_seg_e0,
-                                                         g->d_seg_row);
-        g->launches++;
-        CK(cudaStreamSynchronize(st));
+        CK(cudaMalloc(&g->d_seg_e0, sizeof(int64_t) * g->n_seg));
+        CK(cudaMalloc(&g->d_seg_row, sizeof(int32_t) * g->n_seg));
+        CK(cudaMemcpy(g->d_hseg, hseg.data(), sizeof(int64_t) * (nh + 1), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(g->d_seg_e0, seg_e0.data(), sizeof(int64_t) * g->n_seg, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(g->d_seg_row, seg_row.data(), sizeof(int32_t) * g->n_seg, cudaMemcpyHostToDevice));
     }
     return ER_OK;
 }

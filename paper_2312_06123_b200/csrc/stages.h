@@ -2,7 +2,6 @@
 // units: pipeline.cu (K1-K4, K8 and run_query_batch), ytable.cu (K5), walks.cu (K6, K7).
 #pragma once
 
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <initializer_list>
@@ -10,6 +9,7 @@
 
 #include "geer_device.cuh"
 #include "geer_internal.h"
+#include "scan.cuh"
 
 namespace geer {
 
@@ -59,15 +59,15 @@ struct Ctx {
 
 #define ENSURE(buf, bytes, keep) CK((buf).ensure((bytes), (keep), c.st))
 
-template <class F>
-int cub_call(Ctx &c, F &&f)
+// Device-wide scans (scan.cuh) with the workspace's scan temporary (head stream only: the AMC and
+// y-build streams bring their own temporaries).
+template <class T, class Op>
+int scan_op(Ctx &c, const T *in, T *out, int64_t n, T zero, Op op)
 {
-    size_t bytes = 0;
-    CK(f((void *)nullptr, bytes));
-    ENSURE(c.ws.cub_tmp, bytes + 16, false);
-    size_t b2 = c.ws.cub_tmp.cap;
-    CK(f(c.ws.cub_tmp.p, b2));
-    c.g->launches += 2;
+    if (n <= 0) return ER_OK;
+    ENSURE(c.ws.cub_tmp, scan_tmp_bytes<T>(n), false);
+    c.g->launches += scan_launch(c.st, in, out, n, zero, op, c.ws.cub_tmp.p);
+    CK(cudaGetLastError());
     return ER_OK;
 }
 
@@ -76,19 +76,13 @@ template <class T>
 int scan_offsets(Ctx &c, const T *in, T *out, int64_t n)
 {
     CK(cudaMemsetAsync(out, 0, sizeof(T), c.st));
-    if (n == 0) return ER_OK;
-    return cub_call(c, [&](void *tmp, size_t &bytes) {
-        return cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, c.st);
-    });
+    return scan_op(c, in, out + 1, n, (T)0, ScanAdd<T>());
 }
 
 template <class T>
 int scan_incl(Ctx &c, const T *in, T *out, int64_t n)
 {
-    if (n == 0) return ER_OK;
-    return cub_call(c, [&](void *tmp, size_t &bytes) {
-        return cub::DeviceScan::InclusiveSum(tmp, bytes, in, out, n, c.st);
-    });
+    return scan_op(c, in, out, n, (T)0, ScanAdd<T>());
 }
 
 inline int read_scalars(Ctx &c, std::initializer_list<const int64_t *> src)
@@ -127,6 +121,15 @@ constexpr double DENSE_BYTES_PER_NS = 2500.0;    // effective bandwidth of a den
 constexpr double DENSE_MAX_BYTES = 16.0 * (1ull << 30);   // X + Y blocks
 bool dense_wave_pays(const er_graph *g, int32_t na, int64_t E);
 int smm_dense_wave(Ctx &c, int32_t na, int64_t F, const int32_t *act, int64_t *dU);
+
+// SMM push wave (smm_push.cu): part A (plan, count, scatter, reduce; push workspaces only) and
+// part B (merge, gather: ws.segstat, ws.nf_*, ws.nf_off, *dU), see the file's header.
+// A wave's queries are pushed in chunks of whole queries (segments [g0, g0 + ns), pairs
+// [P0, P0 + E)) whose pair count stays within er_graph::wave_pairs_max (GEER_WAVE_PAIRS_MAX), so
+// the workspaces stay bounded; chunks are independent (wave splitting).  ws.pk_F = the
+// frontier's entry count.
+int smm_push_wave_a(Ctx &c, int32_t g0, int32_t ns, int64_t P0, int64_t E, const int64_t *ent_off);
+int smm_push_wave_b(Ctx &c, int32_t g0, int32_t ns, int64_t *dU);
 
 // K6 + K7 (walks.cu).  One AMC group: the queries that left the SMM head in the same wave, with
 // their y-tables.  Its whole AMC (tau batches) is enqueued on stream sb without host sync.

@@ -18,12 +18,71 @@ __global__ void k_nchunks(int32_t na, const int32_t *__restrict__ amc, const QSt
     nch[i] = Q.phase == PH_AMC ? (cnt + per_chunk - 1) / per_chunk : 0;
 }
 
-__global__ void k_lf_key(int32_t na, const int32_t *__restrict__ amc, const QState *__restrict__ qs,
-                         uint32_t *__restrict__ key)
+// Stable order of an AMC list by descending ell_f (bins of ell_f clamped at LF_BINS - 1), by one
+// CTA: histogram, bin offsets, then tiles of LF_NT items placed in list order (a lane's slot = its
+// bin's running offset + the same-bin items of earlier warps and lanes of the tile).
+constexpr int LF_NT = 1024;
+constexpr int LF_BINS = 1024;
+__global__ void __launch_bounds__(LF_NT) k_lf_order(int32_t na, const int32_t *__restrict__ amc,
+                                                    const QState *__restrict__ qs, int32_t *__restrict__ out)
 {
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= na) return;
-    key[i] = ~(uint32_t)qs[amc[i]].st.ell_f;
+    __shared__ unsigned int off[LF_BINS];
+    __shared__ unsigned char wcnt[LF_NT / 32][LF_BINS + 1];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < LF_BINS; i += LF_NT) off[i] = 0u;
+    for (int i = tid; i < (LF_NT / 32) * (LF_BINS + 1); i += LF_NT) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+    auto bin = [&](int32_t i) {   // descending ell_f first
+        const int32_t lf = qs[amc[i]].st.ell_f;
+        return (unsigned)(LF_BINS - 1 - (lf < LF_BINS - 1 ? lf : LF_BINS - 1));
+    };
+    for (int32_t i = tid; i < na; i += LF_NT) atomicAdd(&off[bin(i)], 1u);
+    __syncthreads();
+    if (warp == 0) {   // exclusive scan of the bin counts, LF_BINS / 32 per lane
+        constexpr int PER = LF_BINS / 32;
+        unsigned v[PER], sum = 0;
+#pragma unroll
+        for (int j = 0; j < PER; j++) {
+            v[j] = off[lane * PER + j];
+            sum += v[j];
+        }
+        unsigned incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        unsigned run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < PER; j++) {
+            off[lane * PER + j] = run;
+            run += v[j];
+        }
+    }
+    __syncthreads();
+    for (int32_t t0 = 0; t0 < na; t0 += LF_NT) {
+        const int32_t i = t0 + tid;
+        const bool valid = i < na;
+        const unsigned d = valid ? bin(i) : (unsigned)LF_BINS;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned lt = peers & ((1u << lane) - 1u);
+        if (lt == 0) wcnt[warp][d] = (unsigned char)__popc(peers);
+        __syncthreads();
+        if (valid) {
+            unsigned pos = off[d] + __popc(lt);
+            for (int w = 0; w < warp; w++) pos += wcnt[w][d];
+            out[pos] = amc[i];
+        }
+        __syncthreads();
+        for (int bb = tid; bb < LF_BINS; bb += LF_NT) {
+            unsigned c = 0;
+            for (int w = 0; w < LF_NT / 32; w++) c += wcnt[w][bb];
+            off[bb] += c;
+        }
+        __syncthreads();
+        if (lt == 0) wcnt[warp][d] = 0;
+        __syncthreads();
+    }
 }
 
 constexpr int WALK_WARPS = 8;
@@ -59,6 +118,49 @@ __device__ __forceinline__ uint64_t pol_evict_first()
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last()
+{
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// Walk-graph (arc) loads with an optional L2 policy (apol != 0) and, with na1, no L1 allocation:
+// on DRAM-resident graphs every arc load is a one-off random access, so it should not push the
+// y-tables of the queries being walked out of L2 (GEER_ARC_POLICY).
+template <class T>
+__device__ __forceinline__ T ld_arc(const T *p, uint64_t apol, int na1);
+template <>
+__device__ __forceinline__ uint4 ld_arc<uint4>(const uint4 *p, uint64_t apol, int na1)
+{
+    if (!apol) return __ldg(p);
+    uint4 r;
+    if (na1)
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(apol));
+    else
+        asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(apol));
+    return r;
+}
+template <>
+__device__ __forceinline__ unsigned long long ld_arc<unsigned long long>(const unsigned long long *p, uint64_t apol,
+                                                                         int na1)
+{
+    if (!apol) return __ldg(p);
+    unsigned long long r;
+    if (na1) asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(apol));
+    else asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(apol));
+    return r;
+}
+template <>
+__device__ __forceinline__ int32_t ld_arc<int32_t>(const int32_t *p, uint64_t apol, int na1)
+{
+    if (!apol) return __ldg(p);
+    int32_t r;
+    if (na1) asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(apol));
+    else asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(apol));
+    return r;
 }
 __device__ __forceinline__ double ld_y(const double *p, uint64_t pol)
 {
@@ -129,13 +231,14 @@ __device__ __forceinline__ int64_t ylookup_resolve(const int4 a, const int32_t *
 template <int ARC>
 __device__ __forceinline__ uint4 next_arc(const uint2 R, uint64_t r64, const uint4 *__restrict__ arcs,
                                           const int32_t *__restrict__ cols,
-                                          const unsigned long long *__restrict__ parcs, PackSpec pk)
+                                          const unsigned long long *__restrict__ parcs, PackSpec pk, uint64_t apol,
+                                          int na1)
 {
     const uint64_t e = (uint64_t)R.x + __umul64hi(r64, (uint64_t)R.y);   // idx = floor(r64 d / 2^64) (R10)
-    if (ARC == 2) return pk.unpack(__ldg(parcs + e));
-    if (ARC == 1) return __ldg(arcs + e);
+    if (ARC == 2) return pk.unpack(ld_arc(parcs + e, apol, na1));
+    if (ARC == 1) return ld_arc(arcs + e, apol, na1);
     uint4 A;
-    A.x = (uint32_t)__ldg(cols + e);
+    A.x = (uint32_t)ld_arc(cols + e, apol, na1);
     return A;
 }
 
@@ -163,7 +266,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
                                             const uint4 *__restrict__ yrec, const double *__restrict__ gvals,
                                             int lgb, int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b,
                                             const uint64_t *kk, uint32_t key0, uint32_t key1, double *acc,
-                                            int32_t *endv, uint64_t pol)
+                                            int32_t *endv, uint64_t pol, uint64_t apol, int na1)
 {
     constexpr int C = 2 * NP;
     uint2 R[C];
@@ -198,7 +301,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
             } else {
                 r64 = ((uint64_t)cw[c] << 32) | cz[c];
             }
-            A[c] = next_arc<ARC>(R[c], r64, arcs, cols, parcs, pk);
+            A[c] = next_arc<ARC>(R[c], r64, arcs, cols, parcs, pk, apol, na1);
         }
 #pragma unroll
         for (int c = 0; c < C; c++) {
@@ -246,8 +349,8 @@ __device__ __forceinline__ void walk_chunk(int64_t chunk, int32_t i, int mode, c
                                            const QState *__restrict__ qs, const uint2 *__restrict__ rec,
                                            const uint4 *__restrict__ arcs, const int32_t *__restrict__ cols,
                                            const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
-                                           uint32_t key0, uint32_t key1, int reuse, uint64_t pol,
-                                           TilePart *__restrict__ parts)
+                                           uint32_t key0, uint32_t key1, int reuse, uint64_t pol, uint64_t apol,
+                                           int na1, TilePart *__restrict__ parts)
 {
     const int lane = threadIdx.x & 31;
     const QState &Q = qs[amc[i]];
@@ -269,7 +372,7 @@ __device__ __forceinline__ void walk_chunk(int64_t chunk, int32_t i, int mode, c
     uint64_t ck = 0ull;
     if (any) {
         walk_chains<ARC, NP>(rec, arcs, cols, parcs, pk, mode, skeys, Q.ykeys, Q.yrec, Q.yvals, Q.ylog2 - YB_LOG,
-                             Q.s, Q.t, Q.st.ell_f, q, bkey, kk, key0, key1, acc, endv, pol);
+                             Q.s, Q.t, Q.st.ell_f, q, bkey, kk, key0, key1, acc, endv, pol, apol, na1);
 #pragma unroll
         for (int p = 0; p < NP; p++) {
             if (kk[p] < (uint64_t)eta) {
@@ -309,7 +412,7 @@ __global__ void __launch_bounds__(WALK_THREADS, MINB)
 k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
         const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
         const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
-        uint32_t key0, uint32_t key1, int32_t smem_words, int y_evict_first, int reuse,
+        uint32_t key0, uint32_t key1, int32_t smem_words, int y_policy, int arc_policy, int reuse,
         unsigned long long *__restrict__ tile_ctr, TilePart *__restrict__ parts)
 {
     extern __shared__ __align__(32) int32_t sm_words[];
@@ -319,7 +422,9 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
     __shared__ int64_t s_tile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
-    const uint64_t pol = y_evict_first ? pol_evict_first() : 0;
+    const uint64_t pol = y_policy == 1 ? pol_evict_first() : y_policy == 2 ? pol_evict_last() : 0;
+    const uint64_t apol = arc_policy ? pol_evict_first() : 0;
+    const int na1 = arc_policy == 2;
     if (smem_words == 0) {
         int32_t i = 0;   // a warp's chunks only increase: its query index only moves forward
         for (int it = 0;; it++) {
@@ -332,7 +437,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             if (cincl[i] <= chunk) i += 1 + find_chunk_query(cincl + i + 1, na - i - 1, chunk);
             const int mode = qs[amc[i]].ymode == YT_RANK ? YM_RANK : YM_GLOBAL;
             walk_chunk<ARC, NP>(chunk, i, mode, nullptr, cincl, amc, qs, rec, arcs, cols, parcs, pk, b, key0, key1,
-                                reuse, pol, parts);
+                                reuse, pol, apol, na1, parts);
         }
         return;
     }
@@ -377,7 +482,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
         __syncthreads();
         if (wvalid)
             walk_chunk<ARC, NP>(chunk, i, s_mode[warp], sm_words + s_soff[warp], cincl, amc, qs, rec, arcs, cols,
-                                parcs, pk, b, key0, key1, reuse, pol, parts);
+                                parcs, pk, b, key0, key1, reuse, pol, apol, na1, parts);
         __syncthreads();
     }
 }
@@ -449,17 +554,11 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
     // per-group buffers (stream ordered on the AMC stream)
     const int per_chunk = 32 * g->walk_np;   // walk pairs per warp-chunk
     int64_t maxch = (int64_t)((G.eta0_sum << (P.tau - 1)) / per_chunk) + na + 1;
-    uint32_t *kk = nullptr;
     int32_t *list2 = nullptr;
     int64_t *nch = nullptr, *cincl = nullptr;
     TilePart *parts = nullptr;
     void *tmp = nullptr;
-    size_t tb1 = 0, tb2 = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, (uint32_t *)nullptr, (uint32_t *)nullptr, (int32_t *)nullptr,
-                                       (int32_t *)nullptr, na, 0, 32, sb));
-    CK(cub::DeviceScan::InclusiveSum(nullptr, tb2, (int64_t *)nullptr, (int64_t *)nullptr, na, sb));
-    const size_t tbytes = std::max(tb1, tb2) + 256;
-    CK(cudaMallocAsync((void **)&kk, sizeof(uint32_t) * 2 * na, sb));
+    const size_t tbytes = scan_tmp_bytes<int64_t>(na) + 256;
     CK(cudaMallocAsync((void **)&list2, sizeof(int32_t) * na, sb));
     CK(cudaMallocAsync((void **)&nch, sizeof(int64_t) * na, sb));
     CK(cudaMallocAsync((void **)&cincl, sizeof(int64_t) * na, sb));
@@ -469,15 +568,12 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
     CK(cudaMemsetAsync(tctr, 0, sizeof(unsigned long long) * P.tau, sb));
     R.bufs.push_back(tctr);
     CK(cudaMallocAsync(&tmp, tbytes, sb));
-    for (void *p : {(void *)kk, (void *)list2, (void *)nch, (void *)cincl, (void *)parts, tmp}) R.bufs.push_back(p);
+    for (void *p : {(void *)list2, (void *)nch, (void *)cincl, (void *)parts, tmp}) R.bufs.push_back(p);
     const int32_t *list = G.list;
     if (na > 1) {
-        // order by descending ell_f (stable): warps then see one trip count
-        k_lf_key<<<blocks_for(na, 256), 256, 0, sb>>>(na, G.list, qs, kk);
+        // order by descending ell_f (stable): the longest walks start first
+        k_lf_order<<<1, LF_NT, 0, sb>>>(na, G.list, qs, list2);
         LAUNCHED(g);
-        size_t b1 = tbytes;
-        CK(cub::DeviceRadixSort::SortPairs(tmp, b1, kk, kk + na, G.list, list2, na, 0, 32, sb));
-        g->launches += 2;
         list = list2;
     }
     const int nsm = g->num_sms;
@@ -487,9 +583,7 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
             k_nchunks<<<blocks_for(na, 256), 256, 0, sb>>>(na, list, qs, b, P.reuse, per_chunk, nch);
             LAUNCHED(g);
         }
-        size_t b2 = tbytes;
-        CK(cub::DeviceScan::InclusiveSum(tmp, b2, nch, cincl, na, sb));
-        g->launches += 2;
+        g->launches += scan_launch(sb, nch, cincl, (int64_t)na, (int64_t)0, ScanAdd<int64_t>(), tmp);
         const int64_t bound = (int64_t)((G.eta0_sum << b) / per_chunk) + na;   // chunks of batch b, at most
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (prof) {
@@ -499,7 +593,7 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
         }
 #define WALK_ARGS                                                                                         \
     na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, smem_words,      \
-        g->y_evict_first, P.reuse,                                                                            \
+        g->y_evict_first, g->arc_policy, P.reuse,                                                             \
         persist ? tctr + b : nullptr, parts
 #define WALK_LAUNCH(ARC, NP, MINB)                                                                          \
     do {                                                                                                    \

@@ -219,8 +219,8 @@ k_yrank(int32_t na, const YSizes *__restrict__ sz, const YDesc *__restrict__ yd)
     uint4 *recs = yd[i].rec;
     const uint4 *aux = yd[i].aux;
     const int64_t R = sz[i].r;
-    typedef cub::BlockScan<unsigned long long, YRANK_THREADS> Scan;
-    __shared__ typename Scan::TempStorage tmp;
+    static_assert(YRANK_THREADS == SCAN_NT, "k_yrank uses the CTA scan of scan.cuh");
+    __shared__ unsigned long long sh[SCAN_NT / 32];
     unsigned long long carry = 0;   // (rank U << 32) | rank T
     for (int64_t base = 0; base < R; base += YRANK_THREADS * YRANK_ITEMS) {
         const int64_t w0 = base + (int64_t)threadIdx.x * YRANK_ITEMS;
@@ -232,8 +232,16 @@ k_yrank(int32_t na, const YSizes *__restrict__ sz, const YDesc *__restrict__ yd)
             c[j] = ((unsigned long long)(__popc(a[j].x | a[j].z) + __popc(a[j].y | a[j].w)) << 32) |
                    (unsigned long long)(__popc(a[j].z) + __popc(a[j].w));
         }
-        unsigned long long excl[YRANK_ITEMS], tot;
-        Scan(tmp).ExclusiveSum(c, excl, tot);
+        unsigned long long excl[YRANK_ITEMS], tot, sum = 0;
+#pragma unroll
+        for (int j = 0; j < YRANK_ITEMS; j++) sum += c[j];
+        unsigned long long run;
+        cta_scan(sum, sh, ScanAdd<unsigned long long>(), 0ull, &run, &tot);
+#pragma unroll
+        for (int j = 0; j < YRANK_ITEMS; j++) {
+            excl[j] = run;
+            run += c[j];
+        }
 #pragma unroll
         for (int j = 0; j < YRANK_ITEMS; j++) {
             if (w0 + j < R) {
@@ -260,9 +268,7 @@ int ytable_plan(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, con
     k_ycap<<<blocks_for(na, 256), 256, 0, c.st>>>(na, act, ws.qs.as<QState>(), cont, segoff, nrec, c.g->ytable_force,
                                                   c.g->rank_min_cap, c.g->rank_ratio, c.g->rank_max_bytes, sz);
     LAUNCHED(c.g);
-    int rc = cub_call(c, [&](void *tmp, size_t &bytes) {   // the three size scans in one pass
-        return cub::DeviceScan::InclusiveScan(tmp, bytes, sz, incl, YSizesPlus(), (int)na, c.st);
-    });
+    int rc = scan_op(c, sz, incl, (int64_t)na, YSizes{0, 0, 0}, YSizesPlus());   // the three size scans in one pass
     *tot_h = &incl[na - 1].h;
     *tot_v = &incl[na - 1].v;
     *tot_r = &incl[na - 1].r;

@@ -15,10 +15,11 @@
 // random 64-bit words first.  Output: one JSON object per line.
 //
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o scripts/sector_ubench scripts/sector_ubench.cu
-// Run:   scripts/sector_ubench [max_gb] > profiles/sector_ubench_r02.jsonl
+// Run:   scripts/sector_ubench [max_gb [sizes_mb,... [l2_fetch_bytes]]] > profiles/sector_ubench_r02.jsonl
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -53,6 +54,43 @@ __device__ __forceinline__ uint64_t ldnc(const uint64_t *p)
     uint64_t v;
     asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(v) : "l"(p));
     return v;
+}
+// load flavours (for the sector-granularity experiment): 0 nc, 1 ca, 2 cg, 3 cs, 4 lu, 5 cv,
+// 6 nc + L1::no_allocate, 7 ca + L1::no_allocate
+template <int FL>
+__device__ __forceinline__ uint64_t ldf(const uint64_t *p)
+{
+    uint64_t v;
+    if (FL == 0) asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    if (FL == 1) asm volatile("ld.global.ca.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    if (FL == 2) asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    if (FL == 3) asm volatile("ld.global.cs.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    if (FL == 4) asm volatile("ld.global.lu.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    if (FL == 5) asm volatile("ld.global.cv.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    if (FL == 6) asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    if (FL == 7) asm volatile("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+template <int FL>
+__global__ void __launch_bounds__(256) k_flavour(const uint64_t *__restrict__ buf, uint64_t nsect, int iters,
+                                                 unsigned long long *sink)
+{
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t x = mix(tid + 0x9E3779B97F4A7C15ULL) | 1ull;
+    uint64_t acc = 0;
+    for (int it = 0; it < iters; it++) {
+        uint64_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            x ^= x << 13;
+            x ^= x >> 7;
+            x ^= x << 17;
+            v[u] = ldf<FL>(buf + 4 * __umul64hi(x, nsect));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) acc += v[u];
+    }
+    if (acc == 0x12345678ull) atomicAdd(sink, 1ull);
 }
 
 template <int U>
@@ -130,13 +168,23 @@ int main(int argc, char **argv)
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev));
     const uint64_t max_bytes = (uint64_t)(max_gb * (1ull << 30));
+    if (argc > 3) {   // optional L2 fetch granularity hint in bytes (cudaLimitMaxL2FetchGranularity)
+        CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(argv[3])));
+    }
+    size_t gran = 0;
+    CK(cudaDeviceGetLimit(&gran, cudaLimitMaxL2FetchGranularity));
+    fprintf(stderr, "L2 fetch granularity limit: %zu\n", gran);
     uint64_t *buf = nullptr;
     CK(cudaMalloc(&buf, max_bytes));
     unsigned long long *sink;
     CK(cudaMalloc(&sink, 8));
     k_fill<<<nsm * 8, 256>>>(buf, max_bytes / 8, 20231210);
     CK(cudaDeviceSynchronize());
-    const std::vector<double> sizes_mb = {16, 32, 48, 64, 80, 96, 128, 256, 1024, 4096, 16384, 32768};
+    std::vector<double> sizes_mb = {16, 32, 48, 64, 80, 96, 128, 256, 1024, 4096, 16384, 32768};
+    if (argc > 2) {   // optional comma-separated subset of buffer sizes in MB
+        sizes_mb.clear();
+        for (char *t = strtok(argv[2], ","); t; t = strtok(nullptr, ",")) sizes_mb.push_back(atof(t));
+    }
     const int threads = 256, blocks = nsm * (2048 / threads);   // full occupancy, one wave
     for (double mb : sizes_mb) {
         const uint64_t bytes = (uint64_t)(mb * (1 << 20));
@@ -148,8 +196,25 @@ int main(int argc, char **argv)
             const double ms = time_ms([&] { k_independent<8><<<blocks, threads>>>(buf, nsect, iters, sink); });
             const double loads = (double)blocks * threads * iters * 8;
             printf("{\"mode\": \"independent\", \"buffer_mb\": %.0f, \"loads_in_flight\": %d, \"ms\": %.4f, "
-                   "\"g_sectors_per_s\": %.2f, \"sector_gbs\": %.1f}\n",
-                   mb, blocks * threads * 8, ms, loads / ms / 1e6, 32.0 * loads / ms / 1e6);
+                   "\"g_sectors_per_s\": %.2f, \"sector_gbs\": %.1f, \"l2_fetch_limit\": %zu}\n",
+                   mb, blocks * threads * 8, ms, loads / ms / 1e6, 32.0 * loads / ms / 1e6, gran);
+        }
+        if (getenv("UBENCH_FLAVOURS")) {
+            const int iters = mb >= 1024 ? 64 : 256;
+            const double loads = (double)blocks * threads * iters * 8;
+            double ms[8];
+            ms[0] = time_ms([&] { k_flavour<0><<<blocks, threads>>>(buf, nsect, iters, sink); });
+            ms[1] = time_ms([&] { k_flavour<1><<<blocks, threads>>>(buf, nsect, iters, sink); });
+            ms[2] = time_ms([&] { k_flavour<2><<<blocks, threads>>>(buf, nsect, iters, sink); });
+            ms[3] = time_ms([&] { k_flavour<3><<<blocks, threads>>>(buf, nsect, iters, sink); });
+            ms[4] = time_ms([&] { k_flavour<4><<<blocks, threads>>>(buf, nsect, iters, sink); });
+            ms[5] = time_ms([&] { k_flavour<5><<<blocks, threads>>>(buf, nsect, iters, sink); });
+            ms[6] = time_ms([&] { k_flavour<6><<<blocks, threads>>>(buf, nsect, iters, sink); });
+            ms[7] = time_ms([&] { k_flavour<7><<<blocks, threads>>>(buf, nsect, iters, sink); });
+            const char *nm[8] = {"nc", "ca", "cg", "cs", "lu", "cv", "nc_L1na", "ca_L1na"};
+            for (int f = 0; f < 8; f++)
+                printf("{\"mode\": \"flavour\", \"flavour\": \"%s\", \"buffer_mb\": %.0f, \"ms\": %.4f, "
+                       "\"g_sectors_per_s\": %.2f}\n", nm[f], mb, ms[f], loads / ms[f] / 1e6);
         }
         for (int C : {1, 2, 4, 8}) {
             const int iters = mb >= 1024 ? 128 : 512;
