@@ -284,10 +284,17 @@ def spmm_measure(G, h, g, torch, q=SPMM_Q, reps=10):
             "l2": "flushed before each call", "x_block_mb": g.n * q * 8 / 2**20}
 
 
-def walk_roofline(prof, args, hbm, hbm_how, max_ms, walk_graph_bytes):
-    """K6's roofline: measured random sectors/s (ncu sectors per walk step x the live walk-step
-    rate) against the matching App. A.6 ceiling -- L2 when the walk graph fits the ~64 MB of L2
-    that random accesses can use, else DRAM -- plus SURVEY 8(d)'s algorithmic bytes against HBM."""
+def walk_roofline(prof, args, hbm, hbm_how, max_ms):
+    """K6's roofline, from the live walk-step rate and the committed ncu capture of K6 on this
+    config (profiles/ncu_k_walks_<config>_r02.json):
+      * walk graph L2-resident (packed arc records): bound = the L2's random 32-byte sector rate;
+        achieved = L1->L2 read sectors per step x steps/s, peak = the App. A.6 ceiling (independent
+        random 8-byte loads on a 48-64 MB buffer, profiles/sector_ubench_r02.jsonl);
+      * DRAM-resident: bound = HBM bandwidth.  A random DRAM miss moves a whole 128-byte line on
+        B200 (ncu on the ubench: ~127 DRAM bytes per random 8-byte load, whatever the load flavour or
+        the L2 fetch-granularity limit), so the binding quantity is DRAM bytes, not sectors:
+        achieved = ncu DRAM bytes per step x steps/s, peak = the measured copy bandwidth.
+    Plus SURVEY 8(d)'s algorithmic count (<= 3 random sectors = 96 B per step) against HBM."""
     launches = max(prof["walk_launches"], 1)
     walk_launch_ms = prof["walk_ms"] / launches
     steps_per_launch = prof["walk_steps"] / launches
@@ -298,33 +305,40 @@ def walk_roofline(prof, args, hbm, hbm_how, max_ms, walk_graph_bytes):
            "note": "SURVEY 8(d): <= 3 random 32-byte sectors per step (node record, column, y probe)"}
     ncu, nsrc = ncu_summary("k_walks", args.config)
     ceil = sector_ceilings()
-    l2_resident = walk_graph_bytes <= 64 * 2**20
+    layout = {0: "cols + node records", 1: "16-byte arc records", 2: "packed 8-byte arc records"}.get(
+        prof.get("walk_layout", -1), "?")
     out = {"kernel": "k_walks (K6, AMC walks)", "walk_steps_per_s": steps_s, "avg_launch_ms": walk_launch_ms,
            "walk_steps_per_launch": steps_per_launch, "walk_share_of_step": prof["walk_ms"] / max(max_ms, 1e-9),
-           "walk_graph_mb": walk_graph_bytes / 2**20, "hbm_algorithmic": alg}
-    if ncu and ceil:
-        if l2_resident and ceil["l2_g_sectors_per_s"]:
-            spp = float(ncu["l2_sectors_per_walk_step"])
-            peak_gs = ceil["l2_g_sectors_per_s"]
-            bound = "random_sector_l2"
+           "walk_graph_mb": prof["walk_graph_bytes"] / 2**20, "walk_layout": layout, "hbm_algorithmic": alg}
+    if ncu:
+        dram_ps = float(ncu["dram_bytes_per_walk_step"])
+        out["traffic"] = dram_ps * steps_per_launch
+        out["traffic_source"] = nsrc
+        out["ncu_per_step"] = {k: ncu.get(k) for k in ("dram_bytes_per_walk_step", "l2_sectors_per_walk_step",
+                                                        "l1_to_l2_sectors_per_walk_step")}
+        if prof.get("walk_layout") == 2 and ceil and ceil["l2_g_sectors_per_s"]:
+            spp = float(ncu["l1_to_l2_sectors_per_walk_step"])
+            ach = spp * steps_s * 32 / 1e9
+            out.update({"bound": "random_sector_l2", "achieved": ach, "peak": ceil["l2_g_sectors_per_s"] * 32,
+                        "unit": "GB/s", "frac": ach / (ceil["l2_g_sectors_per_s"] * 32),
+                        "achieved_g_sectors_per_s": spp * steps_s / 1e9,
+                        "peak_g_sectors_per_s": ceil["l2_g_sectors_per_s"],
+                        "peak_source": ceil["source"] + " (independent random 8-byte loads, 48-64 MB buffer)"})
         else:
-            spp = float(ncu["dram_bytes_per_walk_step"]) / 32.0
-            peak_gs = ceil["dram_g_sectors_per_s"]
-            bound = "random_sector_dram"
-        ach = spp * steps_s * 32 / 1e9
-        out.update({"bound": bound, "achieved": ach, "peak": peak_gs * 32, "unit": "GB/s",
-                    "frac": ach / (peak_gs * 32), "sectors_per_step": spp,
-                    "achieved_g_sectors_per_s": spp * steps_s / 1e9, "peak_g_sectors_per_s": peak_gs,
-                    "peak_source": ceil["source"] + " (independent random 32-byte sector reads, "
-                                   + ("48-64 MB buffer)" if bound == "random_sector_l2" else "16 GB buffer)"),
-                    "traffic": float(ncu["dram_bytes_per_walk_step"]) * steps_per_launch,
-                    "traffic_source": nsrc,
-                    "ncu": {k: ncu.get(k) for k in ("dram_bytes_per_walk_step", "l2_sectors_per_walk_step",
-                                                     "l1_to_l2_sectors_per_walk_step")}})
+            ach = dram_ps * steps_s / 1e9
+            out.update({"bound": "hbm", "achieved": ach, "peak": hbm, "peak_kind": hbm_how, "unit": "GB/s",
+                        "frac": ach / hbm,
+                        "note": "DRAM bytes per walk step (ncu) x live steps/s; a random DRAM miss moves a "
+                                "128-byte line"})
+            if ceil and ceil["dram_g_sectors_per_s"]:
+                out["random_dram_ceiling"] = {
+                    "g_random_loads_per_s": ceil["dram_g_sectors_per_s"], "source": ceil["source"],
+                    "note": "independent random 8-byte loads over 16 GB: 4.7 TB/s of DRAM lines; K6 exceeds it "
+                            "through L2 hits, so HBM bandwidth is the binding roof"}
     else:
         out.update({"bound": "hbm", "achieved": alg["achieved_gbs"], "peak": hbm, "unit": "GB/s",
                     "frac": alg["frac"], "traffic": None,
-                    "note": "no committed ncu summary / sector ceiling for this config: algorithmic bytes vs HBM"})
+                    "note": "no committed ncu summary for this config: algorithmic bytes vs HBM"})
     return out
 
 
@@ -579,8 +593,7 @@ def main():
     line = None
     if rank == 0:
         hbm, how = peaks()
-        walk_graph_bytes = prof["walk_graph_bytes"]
-        roof = walk_roofline(prof, args, hbm, how, max_ms, walk_graph_bytes)
+        roof = walk_roofline(prof, args, hbm, how, max_ms)
         smm_alg = 12.0 * prof["smm_pairs"]   # 4 B column + 8 B value per edge visit
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,

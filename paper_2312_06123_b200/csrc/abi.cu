@@ -272,12 +272,13 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         int layout = 0;  // 0 cols, 1 arcs16, 2 packed
         if (packable && pack_foot <= 0.75 * (double)l2) layout = 2;
         (void)cols_foot;
-        // DRAM-resident graphs keep cols + node records: a random DRAM access moves a 128-byte line
-        // whatever the record size (profiles/sector_ubench_r02.jsonl, ncu: 127 B per 8-byte load),
-        // so the smaller 4-byte column array wins by its higher L2 hit rate (LJ-shaped config:
-        // 495 vs 517 ms of walks per step, profiles/exp_layout_lj_r02.jsonl); its arc loads are
-        // evict-first in L2 so they do not push out the y-tables and node records
-        if (layout == 0) g->arc_policy = 1;
+        // DRAM-resident graphs keep cols + node records: a random DRAM access moves a whole line
+        // whatever the record size (profiles/sector_flavours_r02.txt), so the smaller 4-byte column
+        // array wins by its higher L2 hit rate (LJ-shaped config: 495 vs 517 ms of walks per step
+        // against 16-byte arc records); column loads are L2 evict-first (one-off random accesses
+        // must not push out the y-tables and node records) with the 64-byte L2 fetch size, node
+        // records 64-byte fetches (447 -> 418 ms; profiles/exp_walk_policy_r02.jsonl)
+        if (layout == 0) g->arc_policy = 4;
         if (const char *env = getenv("GEER_WALK_LAYOUT")) {
             if (!strcmp(env, "arcs")) layout = 1;
             if (!strcmp(env, "cols")) layout = 0;
@@ -292,8 +293,8 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_WALK_PERSIST")) g->walk_persist = atoi(env) != 0;
         if (const char *env = getenv("GEER_YTABLE")) g->ytable_force = !strcmp(env, "hash") ? 1 : !strcmp(env, "rank") ? 2 : 0;
         if (const char *env = getenv("GEER_Y_EVICT_FIRST")) g->y_evict_first = atoi(env) != 0;
-        if (const char *env = getenv("GEER_Y_POLICY")) g->y_evict_first = std::min(2, std::max(0, atoi(env)));
-        if (const char *env = getenv("GEER_ARC_POLICY")) g->arc_policy = std::min(2, std::max(0, atoi(env)));
+        if (const char *env = getenv("GEER_Y_POLICY")) g->y_evict_first = std::min(6, std::max(0, atoi(env)));
+        if (const char *env = getenv("GEER_ARC_POLICY")) g->arc_policy = std::min(4, std::max(0, atoi(env)));
         if (const char *env = getenv("GEER_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(env));
         if (const char *env = getenv("GEER_L2_PERSIST")) g->l2_persist = atoi(env) != 0;
         if (const char *env = getenv("GEER_OVERLAP_FRAC")) g->overlap_frac = std::min(1.0, std::max(0.1, atof(env)));

@@ -32,8 +32,10 @@ namespace {
 
 constexpr int BKT_NT = 256;                 // threads of the reduce CTA
 constexpr int BKT_NW = BKT_NT / 32;
-constexpr int BKT_TARGET = 1024;            // mean pairs per bucket a segment is cut for
-constexpr int BKT_CAP = 2048;               // largest bucket sorted in shared memory
+constexpr int BKT_TARGET = 256;             // mean pairs per bucket a segment is cut for
+constexpr int BKT_WCAP = 512;               // largest bucket reduced by one warp (k_bkt_reduce_warp)
+constexpr int BKT_WPB = 4;                  // warps per CTA of k_bkt_reduce_warp
+constexpr int BKT_CAP = 2048;               // largest bucket sorted in shared memory by one CTA
 constexpr int EMIT_PER = 4;                 // pairs per lane of the enumeration kernels
 
 struct BStat {
@@ -190,7 +192,12 @@ __device__ unsigned long long *cta_radix_sort(unsigned long long *a, unsigned lo
         const int sh = 8 * p;
         for (int i = lane; i < 256; i += 32) S.wh[warp][i] = 0u;
         __syncwarp();
-        for (int i = lo + lane; i < hi; i += 32) atomicAdd(&S.wh[warp][(src[i] >> sh) & 255u], 1u);
+        for (int base = lo; base < hi; base += 32) {   // warp-aggregated histogram
+            const int i = base + lane;
+            const unsigned d = i < hi ? (unsigned)((src[i] >> sh) & 255u) : 256u;
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            if (d < 256u && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&S.wh[warp][d], (unsigned)__popc(peers));
+        }
         __syncthreads();
         // a digit every key shares needs no pass
         const unsigned d0 = (unsigned)((src[0] >> sh) & 255u);
@@ -290,13 +297,7 @@ __global__ void __launch_bounds__(BKT_NT) k_bkt_reduce(
     const int32_t gl = bseg[b], g = g0 + gl;
     const int64_t base = boff[b];
     const int n = (int)(boff[b + 1] - base);
-    if (n == 0) {
-        if (tid == 0) {
-            ucnt[b] = 0;
-            bst[b] = BStat{0, 0ull, 0ull, 0, 0.0, 0.0, 0};
-        }
-        return;
-    }
+    if (n <= BKT_WCAP) return;   // k_bkt_reduce_warp
     const int sh = segsh[gl], eb = segeb[gl];
     const int64_t hi = b - segBoff[gl];
     unsigned long long *a, *bb;
@@ -380,6 +381,164 @@ __global__ void __launch_bounds__(BKT_NT) k_bkt_reduce(
     if (tid == 0) {
         ucnt[b] = U;
         bst[b] = BStat{V, M1, M2, C1, s_at[0], s_at[1], s_flags};
+    }
+}
+
+// 5a. reduce, small buckets (n <= BKT_WCAP): one WARP per bucket, warp-synchronous (no CTA
+// barriers), buckets handed out grid-stride.  Same result as k_bkt_reduce: stable LSD radix sort
+// of (u_low, e) keys, values gathered in sorted order, one lane per run of equal u summing its
+// values in ascending e, / d(u); statistics reduced over the warp.
+struct WarpSmem {
+    unsigned long long a[BKT_WCAP], b[BKT_WCAP];
+    unsigned int cnt[256];
+    int runs[BKT_WCAP];
+};
+
+// Stable LSD passes over key bits [lo, hi), 8 bits per pass (one warp).
+__device__ __forceinline__ unsigned long long *warp_radix_sort(unsigned long long *a, unsigned long long *b, int n,
+                                                               int lo, int hi, unsigned int *cnt)
+{
+    const int lane = threadIdx.x & 31;
+    const int npass = (hi - lo + 7) / 8;
+    unsigned long long *src = a, *dst = b;
+    for (int p = 0; p < npass; p++) {
+        const int sh = lo + 8 * p;
+        for (int i = lane; i < 256; i += 32) cnt[i] = 0u;
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) atomicAdd(&cnt[(src[i] >> sh) & 255u], 1u);
+        __syncwarp();
+        if (cnt[(src[0] >> sh) & 255u] == (unsigned)n) continue;   // a digit all keys share
+        unsigned v[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            v[j] = cnt[lane * 8 + j];
+            sum += v[j];
+        }
+        unsigned incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        unsigned run = incl - sum;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            cnt[lane * 8 + j] = run;
+            run += v[j];
+        }
+        __syncwarp();
+        for (int base = 0; base < n; base += 32) {
+            const int i = base + lane;
+            const bool valid = i < n;
+            const unsigned long long k = valid ? src[i] : 0ull;
+            const unsigned d = valid ? (unsigned)((k >> sh) & 255u) : 256u;
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            const unsigned lt = peers & ((1u << lane) - 1u);
+            if (valid) dst[cnt[d] + __popc(lt)] = k;
+            __syncwarp();
+            if (valid && lt == 0) cnt[d] += __popc(peers);
+            __syncwarp();
+        }
+        unsigned long long *t = src;
+        src = dst;
+        dst = t;
+    }
+    return src;
+}
+
+__global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
+    int32_t g0, const int64_t *__restrict__ dNB, const int32_t *__restrict__ bseg, const int64_t *__restrict__ segBoff,
+    const int32_t *__restrict__ segsh, const int32_t *__restrict__ segeb, const int64_t *__restrict__ boff,
+    const unsigned long long *__restrict__ keys, const int64_t *__restrict__ fr_off, const double *__restrict__ fr_val,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ act, const QState *__restrict__ qs,
+    int32_t *__restrict__ out_id, double *__restrict__ out_val, int64_t *__restrict__ ucnt, BStat *__restrict__ bst)
+{
+    __shared__ WarpSmem W[BKT_WPB];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpSmem &M = W[wib];
+    const int64_t NB = *dNB;
+    const unsigned full = 0xffffffffu;
+    for (int64_t b = (int64_t)blockIdx.x * BKT_WPB + wib; b < NB; b += (int64_t)gridDim.x * BKT_WPB) {
+        const int64_t base = boff[b];
+        const int n = (int)(boff[b + 1] - base);
+        if (n > BKT_WCAP) continue;   // k_bkt_reduce
+        if (n == 0) {
+            if (lane == 0) {
+                ucnt[b] = 0;
+                bst[b] = BStat{0, 0ull, 0ull, 0, 0.0, 0.0, 0};
+            }
+            continue;
+        }
+        const int32_t gl = bseg[b], g = g0 + gl;
+        const int sh = segsh[gl], eb = segeb[gl];
+        const int64_t hi = b - segBoff[gl];
+        for (int i = lane; i < n; i += 32) M.a[i] = keys[base + i];
+        __syncwarp();
+        unsigned long long *srt = warp_radix_sort(M.a, M.b, n, 0, sh + eb, M.cnt);
+        double *gv = reinterpret_cast<double *>(srt == M.a ? M.b : M.a);
+        const int64_t f0 = fr_off[g];
+        const unsigned long long emask = (1ull << eb) - 1ull;
+        for (int i = lane; i < n; i += 32) gv[i] = fr_val[f0 + (int64_t)(srt[i] & emask)];
+        // run heads and their ranks
+        int U = 0;
+        for (int t0 = 0; t0 < n; t0 += 32) {
+            const int i = t0 + lane;
+            const bool head = i < n && (i == 0 || (srt[i] >> eb) != (srt[i - 1] >> eb));
+            const unsigned bal = __ballot_sync(full, head);
+            if (head) M.runs[U + __popc(bal & ((1u << lane) - 1u))] = i;
+            U += __popc(bal);
+        }
+        __syncwarp();
+        const QState &Q = qs[act[g >> 1]];
+        long long vol = 0;
+        unsigned long long m1 = 0;
+        double at_s = 0.0, at_t = 0.0;
+        int flags = 0;
+        for (int r = lane; r < U; r += 32) {
+            const int i0 = M.runs[r], i1 = r + 1 < U ? M.runs[r + 1] : n;
+            double sum = 0.0;
+            for (int i = i0; i < i1; i++) sum += gv[i];   // ascending source order (R13)
+            const int32_t u = (int32_t)((hi << sh) | (int64_t)(srt[i0] >> eb));
+            const int64_t d = off[u + 1] - off[u];
+            const double x = sum / (double)d;
+            out_id[base + r] = u;
+            out_val[base + r] = x;
+            vol += d;
+            const unsigned long long xb = (unsigned long long)__double_as_longlong(x);
+            m1 = xb > m1 ? xb : m1;
+            if (u == Q.s) { at_s = x; flags |= 1; }
+            if (u == Q.t) { at_t = x; flags |= 2; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            vol += __shfl_xor_sync(full, vol, o);
+            const unsigned long long t = __shfl_xor_sync(full, m1, o);
+            m1 = t > m1 ? t : m1;
+        }
+        long long c1 = 0;
+        unsigned long long m2 = 0;
+        __syncwarp();
+        for (int r = lane; r < U; r += 32) {
+            const unsigned long long xb = (unsigned long long)__double_as_longlong(out_val[base + r]);
+            if (xb == m1) c1++;
+            else if (xb > m2) m2 = xb;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            c1 += __shfl_xor_sync(full, c1, o);
+            const unsigned long long t = __shfl_xor_sync(full, m2, o);
+            m2 = t > m2 ? t : m2;
+        }
+        // x(s), x(t): single writers -> the lane that has them
+        const unsigned bs = __ballot_sync(full, flags & 1), bt = __ballot_sync(full, flags & 2);
+        if (bs) at_s = __shfl_sync(full, at_s, __ffs(bs) - 1);
+        if (bt) at_t = __shfl_sync(full, at_t, __ffs(bt) - 1);
+        if (lane == 0) {
+            ucnt[b] = U;
+            bst[b] = BStat{vol, m1, m2, c1, at_s, at_t, (int64_t)((bs ? 1 : 0) | (bt ? 2 : 0))};
+        }
+        __syncwarp();
     }
 }
 
@@ -567,6 +726,11 @@ int smm_push_wave_a(Ctx &c, int32_t g0, int32_t ns, int64_t P0, int64_t E, const
         CK(cudaFuncSetAttribute(k_bkt_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
+    k_bkt_reduce_warp<<<(unsigned)std::min<int64_t>((NBmax + BKT_WPB - 1) / BKT_WPB, (int64_t)g->num_sms * 16),
+                        32 * BKT_WPB, 0, st>>>(g0, dNB, bseg, segBoff, segsh, segeb, boff, keys, fr_off,
+                                               ws.fr_val.as<double>(), g->d_off, ws.act.as<int32_t>(),
+                                               ws.qs.as<QState>(), out_id, out_val, ucnt, bst);
+    LAUNCHED(g);
     k_bkt_reduce<<<(unsigned)NBmax, BKT_NT, smem, st>>>(g0, dNB, bseg, segBoff, segsh, segeb, boff, keys,
                                                          ws.pk_alt.as<unsigned long long>(), fr_off,
                                                          ws.fr_val.as<double>(), g->d_off, ws.act.as<int32_t>(),

@@ -125,70 +125,100 @@ __device__ __forceinline__ uint64_t pol_evict_last()
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-// Walk-graph (arc) loads with an optional L2 policy (apol != 0) and, with na1, no L1 allocation:
-// on DRAM-resident graphs every arc load is a one-off random access, so it should not push the
-// y-tables of the queries being walked out of L2 (GEER_ARC_POLICY).
+// Walk-graph (arc) loads, by GEER_ARC_POLICY: 0 plain; 1 L2 evict-first (default on
+// DRAM-resident graphs: an arc load is a one-off random access, it should not push the y-tables
+// and node records out of L2); 2 evict-first + no L1 allocation; 3 the L2::64B fetch size (a
+// random DRAM miss otherwise moves a 128-byte line); 4 evict-first + L2::64B.
 template <class T>
-__device__ __forceinline__ T ld_arc(const T *p, uint64_t apol, int na1);
+__device__ __forceinline__ T ld_arc(const T *p, uint64_t apol, int am);
 template <>
-__device__ __forceinline__ uint4 ld_arc<uint4>(const uint4 *p, uint64_t apol, int na1)
+__device__ __forceinline__ uint4 ld_arc<uint4>(const uint4 *p, uint64_t apol, int am)
 {
-    if (!apol) return __ldg(p);
     uint4 r;
-    if (na1)
+    if (am == 0) return __ldg(p);
+    if (am == 1)
+        asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(apol));
+    else if (am == 2)
         asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
             : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(apol));
+    else if (am == 3)
+        asm("ld.global.nc.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
     else
-        asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        asm("ld.global.nc.L2::cache_hint.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
             : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(apol));
     return r;
 }
 template <>
 __device__ __forceinline__ unsigned long long ld_arc<unsigned long long>(const unsigned long long *p, uint64_t apol,
-                                                                         int na1)
+                                                                         int am)
 {
-    if (!apol) return __ldg(p);
     unsigned long long r;
-    if (na1) asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(apol));
-    else asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(apol));
+    if (am == 0) return __ldg(p);
+    if (am == 1) asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(apol));
+    else if (am == 2) asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(apol));
+    else if (am == 3) asm("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(r) : "l"(p));
+    else asm("ld.global.nc.L2::cache_hint.L2::64B.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(apol));
     return r;
 }
 template <>
-__device__ __forceinline__ int32_t ld_arc<int32_t>(const int32_t *p, uint64_t apol, int na1)
+__device__ __forceinline__ int32_t ld_arc<int32_t>(const int32_t *p, uint64_t apol, int am)
 {
-    if (!apol) return __ldg(p);
     int32_t r;
-    if (na1) asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(apol));
-    else asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(apol));
+    if (am == 0) return __ldg(p);
+    if (am == 1) asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(apol));
+    else if (am == 2) asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(apol));
+    else if (am == 3) asm("ld.global.nc.L2::64B.s32 %0, [%1];" : "=r"(r) : "l"(p));
+    else asm("ld.global.nc.L2::cache_hint.L2::64B.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(apol));
     return r;
 }
-__device__ __forceinline__ double ld_y(const double *p, uint64_t pol)
+
+// y-structure loads: optional L2 policy (pol != 0) and, with y64, the L2::64B fetch size.
+__device__ __forceinline__ double ld_y(const double *p, uint64_t pol, int y64)
 {
-    if (!pol) return __ldg(p);
     double r;
+    if (y64) {
+        if (pol) asm("ld.global.nc.L2::cache_hint.L2::64B.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+        else asm("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(r) : "l"(p));
+        return r;
+    }
+    if (!pol) return __ldg(p);
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
     return r;
 }
-__device__ __forceinline__ uint4 ld_y(const uint4 *p, uint64_t pol)
+__device__ __forceinline__ uint4 ld_y(const uint4 *p, uint64_t pol, int y64)
 {
-    if (!pol) return __ldg(p);
     uint4 r;
+    if (y64) {
+        if (pol)
+            asm("ld.global.nc.L2::cache_hint.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+        else
+            asm("ld.global.nc.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+        return r;
+    }
+    if (!pol) return __ldg(p);
     asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
         : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+    return r;
+}
+// node record {offset, degree} of the walk's current node
+__device__ __forceinline__ uint2 ld_rec(const uint2 *p, int r64)
+{
+    if (!r64) return __ldg(p);
+    uint2 r;
+    asm("ld.global.nc.L2::64B.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
 
 // Hash lookups: slot of v, or -1 when v is not in supp(y) (then y(v) = 0, Alg. 1 L7 outside
 // U_s and U_t).  Staged keys in shared memory, or the table in global memory (one 16-byte
 // bucket per probe).  ylookup_global_from continues a global probe at bucket bk.
-__device__ __forceinline__ int4 ld_bucket(const int32_t *keys, uint32_t bk, uint64_t pol)
+__device__ __forceinline__ int4 ld_bucket(const int32_t *keys, uint32_t bk, uint64_t pol, int y64 = 0)
 {
     const int4 *p = reinterpret_cast<const int4 *>(keys + (size_t)bk * YB);
-    if (!pol) return __ldg(p);
-    int4 a;
-    asm("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(p), "l"(pol));
-    return a;
+    const uint4 r = ld_y(reinterpret_cast<const uint4 *>(p), pol, y64);
+    return make_int4((int)r.x, (int)r.y, (int)r.z, (int)r.w);
 }
 __device__ __forceinline__ int64_t ylookup_smem(const int32_t *skeys, int lgb, int32_t v)
 {
@@ -266,7 +296,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
                                             const uint4 *__restrict__ yrec, const double *__restrict__ gvals,
                                             int lgb, int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b,
                                             const uint64_t *kk, uint32_t key0, uint32_t key1, double *acc,
-                                            int32_t *endv, uint64_t pol, uint64_t apol, int na1)
+                                            int32_t *endv, uint64_t pol, uint64_t apol, int na1, int y64)
 {
     constexpr int C = 2 * NP;
     uint2 R[C];
@@ -277,7 +307,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
 #pragma unroll
     for (int c = 0; c < C; c++) {
         v[c] = (c & 1) ? t : s;
-        R[c] = __ldg(rec + v[c]);
+        R[c] = ld_rec(rec + v[c], na1 >= 3);
         acc[c] = 0.0;
         pv[c] = 0.0;
         cz[c] = 0u;
@@ -311,19 +341,19 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
                 const int64_t idx = mode == YM_RANK ? rank_index(prec[c], v[c])
                                                     : ylookup_resolve(*reinterpret_cast<const int4 *>(&prec[c]),
                                                                       gkeys, lgb, v[c], pol);
-                if (idx >= 0) pv[c] = ld_y(gvals + idx, pol);
+                if (idx >= 0) pv[c] = ld_y(gvals + idx, pol, y64);
             }
             v[c] = (int32_t)A[c].x;
             if (ARC) R[c] = make_uint2(A[c].y, A[c].z);
-            else R[c] = __ldg(rec + v[c]);
+            else R[c] = ld_rec(rec + v[c], na1 >= 3);
             if (mode == YM_RANK) {
-                prec[c] = ld_y(yrec + (v[c] >> 6), pol);
+                prec[c] = ld_y(yrec + (v[c] >> 6), pol, y64);
             } else if (mode == YM_GLOBAL) {
-                const int4 bk = ld_bucket(gkeys, ybucket(v[c], lgb), pol);
+                const int4 bk = ld_bucket(gkeys, ybucket(v[c], lgb), pol, y64);
                 prec[c] = make_uint4((uint32_t)bk.x, (uint32_t)bk.y, (uint32_t)bk.z, (uint32_t)bk.w);
             } else {
                 const int64_t slot = ylookup_smem(skeys, lgb, v[c]);
-                if (slot >= 0) pv[c] = ld_y(gvals + slot, pol);
+                if (slot >= 0) pv[c] = ld_y(gvals + slot, pol, y64);
             }
         }
     }
@@ -334,7 +364,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
             const int64_t idx = mode == YM_RANK ? rank_index(prec[c], v[c])
                                                 : ylookup_resolve(*reinterpret_cast<const int4 *>(&prec[c]), gkeys,
                                                                   lgb, v[c], pol);
-            if (idx >= 0) acc[c] += ld_y(gvals + idx, pol);
+            if (idx >= 0) acc[c] += ld_y(gvals + idx, pol, y64);
         }
         endv[c] = v[c];
     }
@@ -350,7 +380,7 @@ __device__ __forceinline__ void walk_chunk(int64_t chunk, int32_t i, int mode, c
                                            const uint4 *__restrict__ arcs, const int32_t *__restrict__ cols,
                                            const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
                                            uint32_t key0, uint32_t key1, int reuse, uint64_t pol, uint64_t apol,
-                                           int na1, TilePart *__restrict__ parts)
+                                           int na1, int y64, TilePart *__restrict__ parts)
 {
     const int lane = threadIdx.x & 31;
     const QState &Q = qs[amc[i]];
@@ -372,7 +402,7 @@ __device__ __forceinline__ void walk_chunk(int64_t chunk, int32_t i, int mode, c
     uint64_t ck = 0ull;
     if (any) {
         walk_chains<ARC, NP>(rec, arcs, cols, parcs, pk, mode, skeys, Q.ykeys, Q.yrec, Q.yvals, Q.ylog2 - YB_LOG,
-                             Q.s, Q.t, Q.st.ell_f, q, bkey, kk, key0, key1, acc, endv, pol, apol, na1);
+                             Q.s, Q.t, Q.st.ell_f, q, bkey, kk, key0, key1, acc, endv, pol, apol, na1, y64);
 #pragma unroll
         for (int p = 0; p < NP; p++) {
             if (kk[p] < (uint64_t)eta) {
@@ -422,9 +452,10 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
     __shared__ int64_t s_tile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
-    const uint64_t pol = y_policy == 1 ? pol_evict_first() : y_policy == 2 ? pol_evict_last() : 0;
+    const int yp = y_policy & 3, y64 = y_policy >> 2;   // GEER_Y_POLICY: +4 = L2::64B fetch size
+    const uint64_t pol = yp == 1 ? pol_evict_first() : yp == 2 ? pol_evict_last() : 0;
     const uint64_t apol = arc_policy ? pol_evict_first() : 0;
-    const int na1 = arc_policy == 2;
+    const int na1 = arc_policy;   // the arc-load mode of ld_arc
     if (smem_words == 0) {
         int32_t i = 0;   // a warp's chunks only increase: its query index only moves forward
         for (int it = 0;; it++) {
@@ -437,7 +468,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             if (cincl[i] <= chunk) i += 1 + find_chunk_query(cincl + i + 1, na - i - 1, chunk);
             const int mode = qs[amc[i]].ymode == YT_RANK ? YM_RANK : YM_GLOBAL;
             walk_chunk<ARC, NP>(chunk, i, mode, nullptr, cincl, amc, qs, rec, arcs, cols, parcs, pk, b, key0, key1,
-                                reuse, pol, apol, na1, parts);
+                                reuse, pol, apol, na1, y64, parts);
         }
         return;
     }
@@ -482,7 +513,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
         __syncthreads();
         if (wvalid)
             walk_chunk<ARC, NP>(chunk, i, s_mode[warp], sm_words + s_soff[warp], cincl, amc, qs, rec, arcs, cols,
-                                parcs, pk, b, key0, key1, reuse, pol, apol, na1, parts);
+                                parcs, pk, b, key0, key1, reuse, pol, apol, na1, y64, parts);
         __syncthreads();
     }
 }

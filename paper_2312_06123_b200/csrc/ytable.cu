@@ -130,20 +130,38 @@ __device__ __forceinline__ void or_global(unsigned long long *p, unsigned long l
     asm volatile("red.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Hash find-or-insert of v; returns its slot, *found = v was already present.
-__device__ __forceinline__ int64_t hash_insert(int32_t *keys, int lgb, int32_t v, bool *found)
+// K5, hash layout: one CTA per leaving query builds its whole table -- in shared memory when it
+// has at most YH_SMEM_SLOTS slots (then copied out), else in place in global memory -- with the
+// same two passes as the rank path's owner rule: t* entries insert v with -(t*(v)/d_t), then s*
+// entries find-or-insert v and complete y = s*(v)/d_s + stored (IEEE a - b is a + (-b)), or
+// s*(v)/d_s - 0.0 when v is not in supp t*.  Every y(v) is written exactly once.
+constexpr int YH_SMEM_SLOTS = 8192;
+#define YH_SMEM_SLOTS_DEV 8192
+constexpr int YH_THREADS = 256;
+template <bool SMEM>
+__device__ __forceinline__ int32_t yh_cas(int32_t *p, int32_t cmp, int32_t val)
+{
+    if (SMEM) return atomicCAS(p, cmp, val);
+    return cas_global(p, cmp, val);
+}
+template <bool SMEM>
+__device__ __forceinline__ int32_t yh_load(const int32_t *p)
+{
+    if (SMEM) return *(volatile const int32_t *)p;
+    int32_t v;
+    asm volatile("ld.volatile.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+template <bool SMEM>
+__device__ __forceinline__ int64_t yh_insert(int32_t *keys, int lgb, int32_t v, bool *found)
 {
     const uint32_t bmask = (1u << lgb) - 1u;
     uint32_t bk = ybucket(v, lgb);
     while (true) {
-        const int4 *bp = reinterpret_cast<const int4 *>(keys + bk * YB);
-        int4 A;
-        asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(A.x), "=r"(A.y), "=r"(A.z), "=r"(A.w) : "l"(bp));
-        const int32_t kk[YB] = {A.x, A.y, A.z, A.w};
         for (int j = 0; j < YB; j++) {
             const uint32_t slot = bk * YB + j;
-            int32_t k = kk[j];
-            if (k == -1) k = cas_global(keys + slot, -1, v);
+            int32_t k = yh_load<SMEM>(keys + slot);
+            if (k == -1) k = yh_cas<SMEM>(keys + slot, -1, v);
             if (k == -1 || k == v) {
                 *found = k == v;
                 return slot;
@@ -152,9 +170,48 @@ __device__ __forceinline__ int64_t hash_insert(int32_t *keys, int lgb, int32_t v
         bk = (bk + 1) & bmask;
     }
 }
+template <bool SMEM>
+__device__ __forceinline__ void yh_build(int32_t *keys, const YDesc &D, const int32_t *__restrict__ id,
+                                         const double *__restrict__ val, int64_t s0, int64_t s1, int64_t t1)
+{
+    for (int64_t e = s1 + threadIdx.x; e < t1; e += YH_THREADS) {   // t* entries first
+        bool found;
+        const int64_t slot = yh_insert<SMEM>(keys, D.lgb, id[e], &found);
+        D.vals[slot] = -(val[e] / (double)D.dt);
+    }
+    __syncthreads();
+    for (int64_t e = s0 + threadIdx.x; e < s1; e += YH_THREADS) {
+        bool found;
+        const int64_t slot = yh_insert<SMEM>(keys, D.lgb, id[e], &found);
+        const double a = val[e] / (double)D.ds;
+        D.vals[slot] = found ? a + D.vals[slot] : a - 0.0;
+    }
+}
+__global__ void __launch_bounds__(YH_THREADS) k_yhash(int32_t na, const int64_t *__restrict__ segoff,
+                                                      const int32_t *__restrict__ id, const double *__restrict__ val,
+                                                      const YDesc *__restrict__ yd)
+{
+    __shared__ __align__(16) int32_t sk[YH_SMEM_SLOTS];
+    const int32_t i = blockIdx.x;
+    if (i >= na) return;
+    const YDesc D = yd[i];
+    if (D.mode != YT_HASH) return;
+    const int64_t s0 = segoff[2 * i], s1 = segoff[2 * i + 1], t1 = segoff[2 * i + 2];
+    const int cap = YB << D.lgb;
+    if (cap > YH_SMEM_SLOTS) return;   // k_yinsert (global CAS, one thread per entry)
+    {
+        for (int j = threadIdx.x; j < cap; j += YH_THREADS) sk[j] = -1;
+        __syncthreads();
+        yh_build<true>(sk, D, id, val, s0, s1, t1);
+        __syncthreads();
+        int4 *dst = reinterpret_cast<int4 *>(D.keys);
+        const int4 *src = reinterpret_cast<const int4 *>(sk);
+        for (int j = threadIdx.x; j < cap / 4; j += YH_THREADS) dst[j] = src[j];
+    }
+}
 
-// K5 over the support entries (frontier entry e: node id[e], value val[e], segment seg[e] =
-// 2 i + side; each segment sorted by node id) of the leaving queries.  Every node v of
+// K5, rank layout, over the support entries (frontier entry e: node id[e], value val[e], segment
+// seg[e] = 2 i + side; each segment sorted by node id) of the leaving queries.  Every node v of
 // U = supp(s*) u supp(t*) gets
 //     y(v) = s*(v)/d(s) - t*(v)/d(t)          (a side v is not on contributes 0.0 / d = 0.0)
 // written exactly once in its final form (Alg. 1 L7 with s = s*, t = t*), no searches:
@@ -196,9 +253,12 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
         D.vals[r.z + __popcll(ubits & below)] = y;
         return;
     }
+    // hash tables: small ones are built by k_yhash (one CTA per query, shared memory); the large
+    // ones here, by global CAS, with the same two passes
+    if ((YB << D.lgb) <= YH_SMEM_SLOTS_DEV) return;
     if (side != (pass == 0 ? 1 : 0)) return;
     bool found;
-    const int64_t slot = hash_insert(D.keys, D.lgb, v, &found);
+    const int64_t slot = yh_insert<false>(D.keys, D.lgb, v, &found);
     if (side == 1) {
         D.vals[slot] = -(val[e] / (double)D.dt);
     } else {
@@ -298,14 +358,20 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
     uint4 *recs = reinterpret_cast<uint4 *>(yb.as<char>() + o_rec);
     uint4 *aux = reinterpret_cast<uint4 *>(yb.as<char>() + o_aux);      // build-time {S bits, T bits}
     int32_t *keys = reinterpret_cast<int32_t *>(yb.as<char>() + o_key);   // 16-byte buckets: aligned region
-    k_yfill<<<blocks_for(std::max(H, R), 256), 256, 0, c.st>>>(H, keys, R, aux);
-    LAUNCHED(c.g);
+    if (H > 0 || R > 0) {   // (small hash tables are rewritten whole by k_yhash)
+        k_yfill<<<blocks_for(std::max(H, R), 256), 256, 0, c.st>>>(H, keys, R, aux);
+        LAUNCHED(c.g);
+    }
     ENSURE(ws.ydesc, sizeof(YDesc) * (na + 1), false);
     YDesc *yd = ws.ydesc.as<YDesc>();
     k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, sz, incl, keys, vals, recs, aux,
                                                       ws.qs.as<QState>(), yd);
     LAUNCHED(c.g);
-    for (int pass = 0; pass < 2; pass++) {
+    if (H > 0) {
+        k_yhash<<<na, YH_THREADS, 0, c.st>>>(na, segoff, id, val, yd);
+        LAUNCHED(c.g);
+    }
+    for (int pass = 0; pass < 2; pass++) {   // rank tables and large hash tables
         if (pass == 1 && R > 0) {
             k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, sz, yd);
             LAUNCHED(c.g);

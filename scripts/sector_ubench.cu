@@ -56,7 +56,7 @@ __device__ __forceinline__ uint64_t ldnc(const uint64_t *p)
     return v;
 }
 // load flavours (for the sector-granularity experiment): 0 nc, 1 ca, 2 cg, 3 cs, 4 lu, 5 cv,
-// 6 nc + L1::no_allocate, 7 ca + L1::no_allocate
+// 6 nc + L1::no_allocate, 7 ca + L1::no_allocate, 8-10 with the L2::64B prefetch-size qualifier
 template <int FL>
 __device__ __forceinline__ uint64_t ldf(const uint64_t *p)
 {
@@ -69,6 +69,9 @@ __device__ __forceinline__ uint64_t ldf(const uint64_t *p)
     if (FL == 5) asm volatile("ld.global.cv.u64 %0, [%1];" : "=l"(v) : "l"(p));
     if (FL == 6) asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
     if (FL == 7) asm volatile("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    if (FL == 8) asm volatile("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    if (FL == 9) asm volatile("ld.global.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    if (FL == 10) asm volatile("ld.global.nc.L1::no_allocate.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
     return v;
 }
 template <int FL>
@@ -202,7 +205,7 @@ int main(int argc, char **argv)
         if (getenv("UBENCH_FLAVOURS")) {
             const int iters = mb >= 1024 ? 64 : 256;
             const double loads = (double)blocks * threads * iters * 8;
-            double ms[8];
+            double ms[11];
             ms[0] = time_ms([&] { k_flavour<0><<<blocks, threads>>>(buf, nsect, iters, sink); });
             ms[1] = time_ms([&] { k_flavour<1><<<blocks, threads>>>(buf, nsect, iters, sink); });
             ms[2] = time_ms([&] { k_flavour<2><<<blocks, threads>>>(buf, nsect, iters, sink); });
@@ -211,8 +214,12 @@ int main(int argc, char **argv)
             ms[5] = time_ms([&] { k_flavour<5><<<blocks, threads>>>(buf, nsect, iters, sink); });
             ms[6] = time_ms([&] { k_flavour<6><<<blocks, threads>>>(buf, nsect, iters, sink); });
             ms[7] = time_ms([&] { k_flavour<7><<<blocks, threads>>>(buf, nsect, iters, sink); });
-            const char *nm[8] = {"nc", "ca", "cg", "cs", "lu", "cv", "nc_L1na", "ca_L1na"};
-            for (int f = 0; f < 8; f++)
+            ms[8] = time_ms([&] { k_flavour<8><<<blocks, threads>>>(buf, nsect, iters, sink); });
+            ms[9] = time_ms([&] { k_flavour<9><<<blocks, threads>>>(buf, nsect, iters, sink); });
+            ms[10] = time_ms([&] { k_flavour<10><<<blocks, threads>>>(buf, nsect, iters, sink); });
+            const char *nm[11] = {"nc", "ca", "cg", "cs", "lu", "cv", "nc_L1na", "ca_L1na", "nc_L2_64B", "ca_L2_64B",
+                                  "nc_L1na_L2_64B"};
+            for (int f = 0; f < 11; f++)
                 printf("{\"mode\": \"flavour\", \"flavour\": \"%s\", \"buffer_mb\": %.0f, \"ms\": %.4f, "
                        "\"g_sectors_per_s\": %.2f}\n", nm[f], mb, ms[f], loads / ms[f] / 1e6);
         }
