@@ -68,6 +68,19 @@ def sector_ceilings():
     return None
 
 
+def random_dram_ceiling():
+    """The random-DRAM-access ceiling matching K6's working set on DRAM-resident graphs
+    (profiles/random_dram_ceiling_r02.json, from scripts/sector_ubench.cu + ncu)."""
+    for p in sorted((ROOT / "profiles").glob("random_dram_ceiling_r*.json"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+            d["source"] = f"profiles/{p.name}: " + d.get("how", "")
+            return d
+        except Exception:
+            continue
+    return None
+
+
 def ncu_summary(kind: str, config: str):
     """The committed ncu --set full summary of a kernel (K6 walks / K9 spmm) on this config."""
     for p in sorted((ROOT / "profiles").glob(f"ncu_{kind}_{config}_r*.json"), reverse=True):
@@ -326,15 +339,21 @@ def walk_roofline(prof, args, hbm, hbm_how, max_ms):
                         "peak_source": ceil["source"] + " (independent random 8-byte loads, 48-64 MB buffer)"})
         else:
             ach = dram_ps * steps_s / 1e9
-            out.update({"bound": "hbm", "achieved": ach, "peak": hbm, "peak_kind": hbm_how, "unit": "GB/s",
-                        "frac": ach / hbm,
-                        "note": "DRAM bytes per walk step (ncu) x live steps/s; a random DRAM miss moves a "
-                                "128-byte line"})
-            if ceil and ceil["dram_g_sectors_per_s"]:
-                out["random_dram_ceiling"] = {
-                    "g_random_loads_per_s": ceil["dram_g_sectors_per_s"], "source": ceil["source"],
-                    "note": "independent random 8-byte loads over 16 GB: 4.7 TB/s of DRAM lines; K6 exceeds it "
-                            "through L2 hits, so HBM bandwidth is the binding roof"}
+            rc = random_dram_ceiling()
+            out["hbm_copy"] = {"achieved_gbs": ach, "peak_gbs": hbm, "peak_kind": hbm_how, "frac": ach / hbm,
+                               "note": "K6's DRAM bytes (ncu per step x live steps/s) against the copy bandwidth"}
+            if rc:
+                out.update({"bound": "random_sector_dram", "achieved": ach, "peak": rc["dram_gbs"], "unit": "GB/s",
+                            "frac": ach / rc["dram_gbs"],
+                            "achieved_g_dram_accesses_per_s": ach / 64.0,
+                            "peak_g_dram_accesses_per_s": rc["dram_gbs"] / 64.0,
+                            "peak_source": rc["source"],
+                            "note": "random DRAM accesses are rate-bound, not bandwidth-bound: a random miss moves "
+                                    "a 64-byte line (K6 loads use .L2::64B); the ceiling is the DRAM byte rate of "
+                                    "independent random 64-byte-line loads over a buffer of the K6 working set's size"})
+            else:
+                out.update({"bound": "hbm", "achieved": ach, "peak": hbm, "peak_kind": hbm_how, "unit": "GB/s",
+                            "frac": ach / hbm})
     else:
         out.update({"bound": "hbm", "achieved": alg["achieved_gbs"], "peak": hbm, "unit": "GB/s",
                     "frac": alg["frac"], "traffic": None,

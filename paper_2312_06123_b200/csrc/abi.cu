@@ -271,6 +271,10 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         const double pack_foot = 8.0 * (double)g->nnz;
         int layout = 0;  // 0 cols, 1 arcs16, 2 packed
         if (packable && pack_foot <= 0.75 * (double)l2) layout = 2;
+        // cols needs a second random access per step (the node record) unless the node records
+        // stay in L2: beyond ~3/8 of L2 (Friendster-shaped: 480 MB of records) the 16-byte arc
+        // records, one access per step, win (363 vs 243 ms per step on a 125k shard)
+        else if (8.0 * (double)n > 0.375 * (double)l2) layout = 1;
         (void)cols_foot;
         // DRAM-resident graphs keep cols + node records: a random DRAM access moves a whole line
         // whatever the record size (profiles/sector_flavours_r02.txt), so the smaller 4-byte column
@@ -278,7 +282,7 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         // against 16-byte arc records); column loads are L2 evict-first (one-off random accesses
         // must not push out the y-tables and node records) with the 64-byte L2 fetch size, node
         // records 64-byte fetches (447 -> 418 ms; profiles/exp_walk_policy_r02.jsonl)
-        if (layout == 0) g->arc_policy = 4;
+        if (layout != 2) g->arc_policy = 4;
         if (const char *env = getenv("GEER_WALK_LAYOUT")) {
             if (!strcmp(env, "arcs")) layout = 1;
             if (!strcmp(env, "cols")) layout = 0;
@@ -293,7 +297,7 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_WALK_PERSIST")) g->walk_persist = atoi(env) != 0;
         if (const char *env = getenv("GEER_YTABLE")) g->ytable_force = !strcmp(env, "hash") ? 1 : !strcmp(env, "rank") ? 2 : 0;
         if (const char *env = getenv("GEER_Y_EVICT_FIRST")) g->y_evict_first = atoi(env) != 0;
-        if (const char *env = getenv("GEER_Y_POLICY")) g->y_evict_first = std::min(6, std::max(0, atoi(env)));
+        if (const char *env = getenv("GEER_Y_POLICY")) g->y_evict_first = std::min(15, std::max(0, atoi(env)));
         if (const char *env = getenv("GEER_ARC_POLICY")) g->arc_policy = std::min(4, std::max(0, atoi(env)));
         if (const char *env = getenv("GEER_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(env));
         if (const char *env = getenv("GEER_L2_PERSIST")) g->l2_persist = atoi(env) != 0;

@@ -125,10 +125,6 @@ __device__ __forceinline__ int32_t cas_global(int32_t *p, int32_t cmp, int32_t v
     asm volatile("atom.global.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "l"(p), "r"(cmp), "r"(val) : "memory");
     return old;
 }
-__device__ __forceinline__ void or_global(unsigned long long *p, unsigned long long v)
-{
-    asm volatile("red.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 
 // K5, hash layout: one CTA per leaving query builds its whole table -- in shared memory when it
 // has at most YH_SMEM_SLOTS slots (then copied out), else in place in global memory -- with the
@@ -236,7 +232,18 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
     if (D.mode == YT_RANK) {
         const uint64_t bit = 1ull << (v & 63);
         if (pass == 0) {
-            or_global(reinterpret_cast<unsigned long long *>(D.aux + (v >> 6)) + side, bit);
+            // the segment's entries are sorted by node id: the first entry of each 64-id word writes
+            // the word's bits for its side (one writer per word and side: no atomics)
+            if (e > segoff[g] && (id[e - 1] >> 6) == (v >> 6)) return;
+            uint64_t bits = 0;
+            const int64_t e1 = segoff[g + 1];
+            for (int64_t f = e; f < e1; f++) {
+                const int32_t w = id[f];
+                if ((w >> 6) != (v >> 6)) break;
+                bits |= 1ull << (w & 63);
+            }
+            reinterpret_cast<unsigned long long *>(D.aux + (v >> 6))[side] = bits;
+            (void)bit;
             return;
         }
         const uint4 a = D.aux[v >> 6];
@@ -352,7 +359,10 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
     const size_t o_rec = up(sizeof(double) * V), o_aux = o_rec + up(sizeof(uint4) * R);
     const size_t o_key = o_aux + up(sizeof(uint4) * R);
     const size_t ybytes = o_key + up(sizeof(int32_t) * H);
-    if (ybytes > yb.cap) CK(cudaDeviceSynchronize());   // the old buffer may still serve an earlier AMC
+    if (ybytes > yb.cap) {   // the old buffer may still serve an earlier batch's AMC (AMC stream)
+        CK(cudaStreamSynchronize(c.g->amc_stream));
+        CK(cudaStreamSynchronize(c.st));
+    }
     ENSURE(yb, ybytes, false);
     double *vals = yb.as<double>();
     uint4 *recs = reinterpret_cast<uint4 *>(yb.as<char>() + o_rec);

@@ -32,3 +32,21 @@ if [ "$PART" = profile ] || [ "$PART" = all ]; then
       --no-spmm --no-accuracy > gpurun_out/ncu_launch_$CFG.log 2>&1
 fi
 ls -la gpurun_out | tail -30
+if [ "$PART" = extra ]; then
+  # config 1 walk-load variants on the packed layout; two real ranks on one GPU over gloo (plumbing);
+  # the Friendster-shaped shard (configs[4], one GPU's 125k of 1M)
+  bash scripts/exp_env.sh rmat20 gpurun_out/exp_rmat20_arc.jsonl "GEER_ARC_POLICY=0" "GEER_ARC_POLICY=3" "GEER_ARC_POLICY=4" > gpurun_out/exp_rmat20_arc.log 2>&1
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 \
+      bench.py --gpus 2 --dist-backend gloo --config rmat20 --steps 3 --warmup 3 --no-cpu-baseline --no-spmm \
+      --no-accuracy > gpurun_out/bench_2rank_gloo.log 2>&1
+  timeout 1800 python bench.py --config friendster --steps 3 --warmup 3 --no-cpu-baseline --no-spmm > gpurun_out/bench_friendster.log 2>&1
+  # the matching random-DRAM ceiling for K6 on the graded config (64-byte fetches, 256 MB - 1 GB buffers)
+  nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o scripts/sector_ubench scripts/sector_ubench.cu
+  UBENCH_FLAVOURS=1 timeout 300 scripts/sector_ubench 2 128,256,512,1024 > gpurun_out/ubench_mid.jsonl 2>&1
+  UBENCH_FLAVOURS=1 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,lts__t_sector_hit_rate.pct --clock-control none \
+      -k regex:k_flavour --csv scripts/sector_ubench 2 128,256,512,1024 > gpurun_out/ncu_ubench_mid.csv 2>&1
+  # K6 on config 1 (packed layout): the capture behind its random_sector_l2 roofline
+  timeout 600 python scripts/walk_batch_steps.py rmat20 > gpurun_out/walk_steps_rmat20.json 2> gpurun_out/walk_steps_rmat20.err
+  timeout 900 ncu --set full --clock-control none -k regex:k_walks -s 5 -c 1 -f -o gpurun_out/walks_rmat20 \
+      python bench.py --config rmat20 --steps 1 --warmup 1 --no-cpu-baseline --no-spmm --no-accuracy > gpurun_out/ncu_walks_rmat20.log 2>&1
+fi
