@@ -318,7 +318,8 @@ def walk_roofline(prof, args, hbm, hbm_how, max_ms):
            "note": "SURVEY 8(d): <= 3 random 32-byte sectors per step (node record, column, y probe)"}
     ncu, nsrc = ncu_summary("k_walks", args.config)
     ceil = sector_ceilings()
-    layout = {0: "cols + node records", 1: "16-byte arc records", 2: "packed 8-byte arc records"}.get(
+    layout = {0: "cols + node records", 1: "16-byte arc records", 2: "packed 8-byte arc records",
+              3: "24-bit cols (5 per 16 B) + node records"}.get(
         prof.get("walk_layout", -1), "?")
     out = {"kernel": "k_walks (K6, AMC walks)", "walk_steps_per_s": steps_s, "avg_launch_ms": walk_launch_ms,
            "walk_steps_per_launch": steps_per_launch, "walk_share_of_step": prof["walk_ms"] / max(max_ms, 1e-9),

@@ -37,8 +37,37 @@ static void clear_error()
     t_msg = "ok";
 }
 
+// The checks that need no pass over the columns (host, before the upload).
+static int validate_basic(int64_t n, const int64_t *off, const int32_t *cols)
+{
+    if (n < 2 || n > (int64_t)INT32_MAX) {
+        set_error(ER_EINVAL, "n must be in [2, 2^31-1]");
+        return ER_EINVAL;
+    }
+    if (!off || !cols) {
+        set_error(ER_EINVAL, "offsets/cols must be non-NULL");
+        return ER_EINVAL;
+    }
+    if (off[0] != 0) {
+        set_error(ER_EINVAL, "offsets[0] != 0");
+        return ER_EINVAL;
+    }
+    for (int64_t v = 0; v < n; v++) {
+        if (off[v + 1] < off[v]) {
+            set_error(ER_EINVAL, "offsets not non-decreasing at node " + std::to_string(v));
+            return ER_EINVAL;
+        }
+    }
+    if (off[n] >= ((int64_t)1 << 32)) {
+        set_error(ER_EINVAL, "graphs with 2^32 or more arcs are not supported (32-bit node records)");
+        return ER_EINVAL;
+    }
+    return ER_OK;
+}
+
 // Host-side validation of the CSR (graph creation is not on the query path; the
-// paper also loads and preprocesses graphs outside its timings).
+// paper also loads and preprocesses graphs outside its timings).  The device
+// validation (validate.cu) hands graphs with unsorted rows, or very deep BFS trees, to this one.
 static int validate(int64_t n, const int64_t *off, const int32_t *cols, bool *rows_sorted, int32_t *max_deg,
                     int *spectral_code, bool spmm_only)
 {
@@ -216,7 +245,15 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         set_error(ER_EINVAL, "unknown flags");
         return nullptr;
     }
-    if (validate(n, offsets, cols, &sorted, &md, &spec, (flags & ER_CREATE_SPMM_ONLY) != 0) != ER_OK) return nullptr;
+    const bool spmm_only = (flags & ER_CREATE_SPMM_ONLY) != 0;
+    if (validate_basic(n, offsets, cols) != ER_OK) return nullptr;
+    // input errors are reported whether or not a device is present: without one (or on request,
+    // GEER_HOST_VALIDATE=1) the whole validation runs on the host first
+    int ndev = 0;
+    const bool no_dev = cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0;
+    cudaGetLastError();
+    const bool host_val = no_dev || (getenv("GEER_HOST_VALIDATE") && atoi(getenv("GEER_HOST_VALIDATE")) != 0);
+    if (host_val && validate(n, offsets, cols, &sorted, &md, &spec, spmm_only) != ER_OK) return nullptr;
     er_graph *g = new (std::nothrow) er_graph();
     if (!g) {
         set_error(ER_ENOMEM, "host allocation failed");
@@ -241,9 +278,6 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
     }
     g->n = n;
     g->nnz = offsets[n];
-    g->rows_sorted = sorted;
-    g->max_deg = md;
-    g->query_block = spec;
     int nb = 1;
     while ((1ll << nb) < n) nb++;
     g->nbits = nb;
@@ -251,6 +285,31 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
     if (e == cudaSuccess) e = cudaMalloc(&g->d_cols, sizeof(int32_t) * std::max<int64_t>(g->nnz, 1));
     if (e == cudaSuccess) e = cudaMemcpy(g->d_off, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g->d_cols, cols, sizeof(int32_t) * g->nnz, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !host_val) {
+        // the checks over the columns run on the device (validate.cu); graphs with unsorted rows
+        // (or a BFS deeper than its level cap) fall back to the host validation
+        int code = ER_OK;
+        std::string msg;
+        if (geer::validate_device(g, &code, &msg, &spec, &sorted, &md) != 0) {
+            if (validate(n, offsets, cols, &sorted, &md, &spec, spmm_only) != ER_OK) {
+                er_graph_destroy(g);
+                return nullptr;
+            }
+        } else {
+            if (code == ER_OK && spec != ER_OK && !spmm_only) {
+                code = spec;
+                msg = spec == ER_EDISCONNECTED ? "graph is not connected" : "graph is bipartite (lambda = 1)";
+            }
+            if (code != ER_OK) {
+                er_graph_destroy(g);
+                set_error(code, msg);
+                return nullptr;
+            }
+        }
+    }
+    g->rows_sorted = sorted;
+    g->max_deg = md;
+    g->query_block = spec;
     if (e == cudaSuccess) {
         // 8-byte node records {offset, degree} for the walk kernel (one sector per step)
         std::vector<uint2> rec(n);
@@ -282,10 +341,14 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         // against 16-byte arc records); column loads are L2 evict-first (one-off random accesses
         // must not push out the y-tables and node records) with the 64-byte L2 fetch size, node
         // records 64-byte fetches (447 -> 418 ms; profiles/exp_walk_policy_r02.jsonl)
-        if (layout != 2) g->arc_policy = 4;
+        if (layout != 2) g->arc_policy = 4;   // (layouts 0, 1, 3: DRAM-resident)
+        // cols with node ids below 2^24: 24-bit columns, 5 per 16-byte chunk (3.2 B per arc instead of
+        // 4: a larger share of the random column loads hits L2)
+        if (layout == 0 && n <= (1 << 24)) layout = 3;
         if (const char *env = getenv("GEER_WALK_LAYOUT")) {
             if (!strcmp(env, "arcs")) layout = 1;
             if (!strcmp(env, "cols")) layout = 0;
+            if (!strcmp(env, "cols24") && n <= (1 << 24)) layout = 3;
             if (!strcmp(env, "packed") && packable) layout = 2;
         }
         // K6 scheduling: per-warp chunks when the walk graph is L2-resident (packed), CTA-tiles of
@@ -321,6 +384,10 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (layout == 2 && e == cudaSuccess) {
             e = cudaMalloc(&g->d_parcs, sizeof(unsigned long long) * std::max<int64_t>(g->nnz, 1));
             if (e == cudaSuccess) e = geer::build_parcs(g);
+        }
+        if (layout == 3 && e == cudaSuccess) {
+            e = cudaMalloc(&g->d_c24, sizeof(uint4) * std::max<int64_t>((g->nnz + 4) / 5, 1));
+            if (e == cudaSuccess) e = geer::build_c24(g);
         }
     }
     if (e == cudaSuccess && g->l2_persist) {
@@ -368,6 +435,7 @@ void er_graph_destroy(er_graph *g)
         if (g->d_rec) cudaFree(g->d_rec);
         if (g->d_arcs) cudaFree(g->d_arcs);
         if (g->d_parcs) cudaFree(g->d_parcs);
+        if (g->d_c24) cudaFree(g->d_c24);
         if (g->d_steps) cudaFree(g->d_steps);
         if (g->d_rowperm) cudaFree(g->d_rowperm);
         if (g->d_hseg) cudaFree(g->d_hseg);
@@ -578,8 +646,10 @@ int er_graph_profile_read(er_graph *g, er_profile *out)
     std::lock_guard<std::mutex> lk(g->mu);
     *out = g->prof;
     out->walk_ctas_per_sm = g->walk_occ;
-    out->walk_layout = g->d_parcs ? 2 : g->d_arcs ? 1 : 0;
-    out->walk_graph_bytes = g->d_parcs ? 8 * g->nnz : g->d_arcs ? 16 * g->nnz : 4 * g->nnz + 8 * g->n;
+    out->walk_layout = g->d_parcs ? 2 : g->d_c24 ? 3 : g->d_arcs ? 1 : 0;
+    out->walk_graph_bytes = g->d_parcs ? 8 * g->nnz
+                            : g->d_c24 ? 16 * ((g->nnz + 4) / 5) + 8 * g->n
+                            : g->d_arcs ? 16 * g->nnz : 4 * g->nnz + 8 * g->n;
     if (g->d_steps) {
         int64_t steps = 0;
         cudaError_t e = cudaMemcpy(&steps, g->d_steps, sizeof(int64_t), cudaMemcpyDeviceToHost);

@@ -135,6 +135,7 @@ struct er_graph {
     uint2 *d_rec = nullptr;       // {offset, degree} per node (offsets < 2^32)
     uint4 *d_arcs = nullptr;      // {u, offset(u), degree(u), 0} per arc, in CSR order (walk chain)
     unsigned long long *d_parcs = nullptr;  // packed 8-byte arc records (when they fit 64 bits)
+    uint4 *d_c24 = nullptr;       // 24-bit columns, 5 per 16-byte chunk (DRAM-resident graphs with n < 2^24)
     geer::PackSpec pack;
     int32_t max_deg = 0;
     bool rows_sorted = false;
@@ -202,5 +203,8 @@ int run_smm_series(er_graph *g, const int32_t *pairs, int64_t k, double tol, int
 int run_estimate_lambda(er_graph *g, int iters, double *lambda_out);
 cudaError_t build_arcs(er_graph *g);
 cudaError_t build_parcs(er_graph *g);
+cudaError_t build_c24(er_graph *g);
+// Device validation of the uploaded CSR (validate.cu): 1 = the host validation must decide.
+int validate_device(er_graph *g, int *code, std::string *msg, int *spectral, bool *rows_sorted, int32_t *max_deg);
 
 }  // namespace geer

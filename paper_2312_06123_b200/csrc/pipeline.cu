@@ -967,6 +967,39 @@ __global__ void k_build_parcs(int64_t nnz, const int32_t *__restrict__ cols, con
     parcs[e] = pk.pack((uint32_t)u, r.x, r.y);
 }
 
+// 24-bit columns (node ids < 2^24), 5 per 16-byte chunk: column e in chunk e / 5 at bytes
+// 3 (e mod 5) .. +2, little endian; the last 1 byte of each chunk is padding, so every column sits
+// inside one 16-byte load.
+__global__ void k_build_c24(int64_t nnz, const int32_t *__restrict__ cols, uint4 *__restrict__ c24)
+{
+    const int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ch * 5 >= nnz) return;
+    unsigned char b[16] = {0};
+    for (int j = 0; j < 5; j++) {
+        const int64_t e = ch * 5 + j;
+        const uint32_t u = e < nnz ? (uint32_t)cols[e] : 0u;
+        b[3 * j] = (unsigned char)(u & 255u);
+        b[3 * j + 1] = (unsigned char)((u >> 8) & 255u);
+        b[3 * j + 2] = (unsigned char)((u >> 16) & 255u);
+    }
+    uint4 q;
+    q.x = b[0] | (b[1] << 8) | (b[2] << 16) | ((uint32_t)b[3] << 24);
+    q.y = b[4] | (b[5] << 8) | (b[6] << 16) | ((uint32_t)b[7] << 24);
+    q.z = b[8] | (b[9] << 8) | (b[10] << 16) | ((uint32_t)b[11] << 24);
+    q.w = b[12] | (b[13] << 8) | (b[14] << 16) | ((uint32_t)b[15] << 24);
+    c24[ch] = q;
+}
+
+cudaError_t build_c24(er_graph *g)
+{
+    const int64_t nch = (g->nnz + 4) / 5;
+    k_build_c24<<<blocks_for(nch, 256), 256>>>(g->nnz, g->d_cols, g->d_c24);
+    g->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    return e;
+}
+
 cudaError_t build_parcs(er_graph *g)
 {
     k_build_parcs<<<blocks_for(g->nnz, 256), 256>>>(g->nnz, g->d_cols, g->d_rec, g->pack, g->d_parcs);

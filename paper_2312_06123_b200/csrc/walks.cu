@@ -267,6 +267,17 @@ __device__ __forceinline__ uint4 next_arc(const uint2 R, uint64_t r64, const uin
     const uint64_t e = (uint64_t)R.x + __umul64hi(r64, (uint64_t)R.y);   // idx = floor(r64 d / 2^64) (R10)
     if (ARC == 2) return pk.unpack(ld_arc(parcs + e, apol, na1));
     if (ARC == 1) return ld_arc(arcs + e, apol, na1);
+    if (ARC == 3) {   // 24-bit columns, 5 per 16-byte chunk (bytes 3p..3p+2 of the chunk)
+        const uint64_t ch = e / 5u;
+        const uint32_t p = (uint32_t)(e - 5u * ch);
+        const uint4 q = ld_arc(arcs + ch, apol, na1);
+        const uint32_t a = p <= 1 ? q.x : p == 2 ? q.y : p == 3 ? q.z : q.w;
+        const uint32_t b = p == 1 ? q.y : p == 2 ? q.z : 0u;
+        const uint32_t sh = p == 1 ? 24u : p == 2 ? 16u : p == 3 ? 8u : 0u;
+        uint4 A;
+        A.x = __funnelshift_r(a, b, sh) & 0xFFFFFFu;
+        return A;
+    }
     uint4 A;
     A.x = (uint32_t)ld_arc(cols + e, apol, na1);
     return A;
@@ -345,7 +356,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
                 if (idx >= 0) pv[c] = ld_y(gvals + idx, pol, y64);
             }
             v[c] = (int32_t)A[c].x;
-            if (ARC) R[c] = make_uint2(A[c].y, A[c].z);
+            if (ARC == 1 || ARC == 2) R[c] = make_uint2(A[c].y, A[c].z);
             else R[c] = ld_rec(rec + v[c], na1 >= 3);
             if (mode == YM_NONE) {
             } else if (mode == YM_RANK) {
@@ -625,7 +636,8 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
             CK(cudaEventRecord(e0, sb));
         }
 #define WALK_ARGS                                                                                         \
-    na, cincl, list, qs, g->d_rec, g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0, key1, smem_words,      \
+    na, cincl, list, qs, g->d_rec, g->d_c24 ? g->d_c24 : g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0,  \
+        key1, smem_words,                                                                                     \
         g->y_evict_first, g->arc_policy, P.reuse,                                                             \
         persist ? tctr + b : nullptr, parts
 #define WALK_LAUNCH(ARC, NP, MINB)                                                                          \
@@ -649,6 +661,7 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
 #define WALK_ARC(NP, MINB)                                   \
     do {                                                     \
         if (g->d_parcs) WALK_LAUNCH(2, NP, MINB);            \
+        else if (g->d_c24) WALK_LAUNCH(3, NP, MINB);         \
         else if (g->d_arcs) WALK_LAUNCH(1, NP, MINB);        \
         else WALK_LAUNCH(0, NP, MINB);                       \
     } while (0)

@@ -293,8 +293,8 @@ def test_unsorted_rows_parity(geer, tiny):
 
 @pytest.mark.parametrize("graph", ["tiny", "rmat20"])
 def test_walk_layouts_byte_identical(geer, tiny, rmat20, graph):
-    # node records + columns, 16-byte arc records and packed 8-byte arc records are three
-    # encodings of the same CSR: every output bit must agree
+    # node records + columns (32-bit or 24-bit, 5 per 16-byte chunk), 16-byte arc records and packed
+    # 8-byte arc records are four encodings of the same CSR: every output bit must agree
     import os
     if graph == "tiny":
         g, pairs = tiny
@@ -303,7 +303,7 @@ def test_walk_layouts_byte_identical(geer, tiny, rmat20, graph):
         g, pairs, _, _ = rmat20
         pairs = pairs[::20]
     outs = {}
-    for lay in ("cols", "arcs", "packed"):
+    for lay in ("cols", "cols24", "arcs", "packed"):
         os.environ["GEER_WALK_LAYOUT"] = lay
         try:
             h = geer.er_graph_create(g.n, g.offsets, g.cols)
@@ -313,7 +313,7 @@ def test_walk_layouts_byte_identical(geer, tiny, rmat20, graph):
         r, st = geer.er_query_batch_ex(h, pairs, 0.1, stats=True)
         outs[lay] = (r.tobytes(), st.tobytes())
         geer.er_graph_destroy(h)
-    assert outs["cols"] == outs["arcs"] == outs["packed"]
+    assert outs["cols"] == outs["cols24"] == outs["arcs"] == outs["packed"]
 
 
 def _hub_graph(n=3000, seed=5):
@@ -591,3 +591,54 @@ def test_split_waves_are_byte_identical(geer, rmat20):
                                    check=True, capture_output=True,
                                    cwd=str(W.Path(__file__).resolve().parents[1])).stdout)
     assert len(outs[0]) > 0 and outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("case", ["range", "selfloop", "dup", "asym", "disconnected", "bipartite", "ok", "unsorted"])
+def test_device_validation_matches_host(geer, case):
+    """er_graph_create validates on the device (validate.cu); GEER_HOST_VALIDATE=1 forces the host
+    validation.  Both give the same code (and message) on sorted-row graphs with one injected fault,
+    at a size where the device path does real work; unsorted rows go to the host either way."""
+    import os
+    g = W.random_small(11, 3000, 0.004)
+    off, cols = g.offsets.copy(), g.cols.copy()
+    d = g.degrees()
+    v = int(np.argmax(d))
+    if case == "range":
+        cols[off[v] + 1] = g.n + 7
+    elif case == "selfloop":
+        cols[off[v]] = v          # (row stays sorted only if v is its smallest neighbour: allow either)
+        cols[off[v]:off[v + 1]] = np.sort(cols[off[v]:off[v + 1]])
+    elif case == "dup":
+        cols[off[v] + 1] = cols[off[v]]
+    elif case == "asym":
+        # drop v from row u (u = v's first neighbour) by replacing it with another absent neighbour
+        u = int(cols[off[v]])
+        row = cols[off[u]:off[u + 1]]
+        cand = [w for w in range(g.n) if w != u and w not in set(row.tolist())]
+        row[row == v] = cand[0]
+        cols[off[u]:off[u + 1]] = np.sort(row)
+    elif case == "disconnected":
+        h = W.from_edges(20, [(i, i + 1) for i in range(9)] + [(0, 2)] + [(10 + i, 11 + i) for i in range(9)] + [(10, 12)])
+        off, cols = h.offsets, h.cols
+    elif case == "bipartite":
+        h = W.cycle(2000)
+        off, cols = h.offsets, h.cols
+    elif case == "unsorted":
+        cols[off[v]:off[v + 1]] = cols[off[v]:off[v + 1]][::-1]
+    n = len(off) - 1
+    res = {}
+    for host in ("0", "1"):
+        os.environ["GEER_HOST_VALIDATE"] = host
+        try:
+            try:
+                h = geer.er_graph_create(n, off, cols)
+                geer.er_graph_destroy(h)
+                res[host] = ("ok", "")
+            except geer.GeerError as e:
+                res[host] = (e.code, str(e))
+        finally:
+            del os.environ["GEER_HOST_VALIDATE"]
+    assert res["0"] == res["1"], res
+    want = {"range": geer.ER_EINVAL, "selfloop": geer.ER_ESELFLOOP, "dup": geer.ER_EDUP, "asym": geer.ER_EASYM,
+            "disconnected": geer.ER_EDISCONNECTED, "bipartite": geer.ER_EBIPARTITE, "ok": "ok", "unsorted": "ok"}[case]
+    assert res["0"][0] == want, res
