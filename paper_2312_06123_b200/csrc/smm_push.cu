@@ -34,7 +34,7 @@ constexpr int BKT_NT = 256;                 // threads of the reduce CTA
 constexpr int BKT_NW = BKT_NT / 32;
 constexpr int BKT_TARGET = 256;             // mean pairs per bucket a segment is cut for
 constexpr int BKT_WCAP = 512;               // largest bucket reduced by one warp (k_bkt_reduce_warp)
-constexpr int BKT_WPB = 4;                  // warps per CTA of k_bkt_reduce_warp
+constexpr int BKT_WPB = 8;                  // warps per CTA of k_bkt_reduce_warp
 constexpr int BKT_CAP = 2048;               // largest bucket sorted in shared memory by one CTA
 constexpr int EMIT_PER = 4;                 // pairs per lane of the enumeration kernels
 
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(BKT_NT) k_bkt_reduce(
     const int32_t gl = bseg[b], g = g0 + gl;
     const int64_t base = boff[b];
     const int n = (int)(boff[b + 1] - base);
-    if (n <= BKT_WCAP) return;   // k_bkt_reduce_warp
+    if (n <= BKT_WCAP && segsh[bseg[b]] + segeb[bseg[b]] <= 32) return;   // k_bkt_reduce_warp
     const int sh = segsh[gl], eb = segeb[gl];
     const int64_t hi = b - segBoff[gl];
     unsigned long long *a, *bb;
@@ -389,20 +389,20 @@ __global__ void __launch_bounds__(BKT_NT) k_bkt_reduce(
 // of (u_low, e) keys, values gathered in sorted order, one lane per run of equal u summing its
 // values in ascending e, / d(u); statistics reduced over the warp.
 struct WarpSmem {
-    unsigned long long a[BKT_WCAP], b[BKT_WCAP];
+    unsigned int a[BKT_WCAP], b[BKT_WCAP];   // 32-bit keys (buckets with wider keys: k_bkt_reduce)
     unsigned int cnt[256];
-    int runs[BKT_WCAP];
+    unsigned short runs[BKT_WCAP];
 };
 
-// Stable LSD passes over key bits [lo, hi), 8 bits per pass (one warp).
-__device__ __forceinline__ unsigned long long *warp_radix_sort(unsigned long long *a, unsigned long long *b, int n,
-                                                               int lo, int hi, unsigned int *cnt)
+// Stable LSD passes over key bits [0, bits), 8 bits per pass (one warp, 32-bit keys).
+__device__ __forceinline__ unsigned int *warp_radix_sort(unsigned int *a, unsigned int *b, int n, int bits,
+                                                         unsigned int *cnt)
 {
     const int lane = threadIdx.x & 31;
-    const int npass = (hi - lo + 7) / 8;
-    unsigned long long *src = a, *dst = b;
+    const int npass = (bits + 7) / 8;
+    unsigned int *src = a, *dst = b;
     for (int p = 0; p < npass; p++) {
-        const int sh = lo + 8 * p;
+        const int sh = 8 * p;
         for (int i = lane; i < 256; i += 32) cnt[i] = 0u;
         __syncwarp();
         for (int i = lane; i < n; i += 32) atomicAdd(&cnt[(src[i] >> sh) & 255u], 1u);
@@ -431,8 +431,8 @@ __device__ __forceinline__ unsigned long long *warp_radix_sort(unsigned long lon
         for (int base = 0; base < n; base += 32) {
             const int i = base + lane;
             const bool valid = i < n;
-            const unsigned long long k = valid ? src[i] : 0ull;
-            const unsigned d = valid ? (unsigned)((k >> sh) & 255u) : 256u;
+            const unsigned k = valid ? src[i] : 0u;
+            const unsigned d = valid ? ((k >> sh) & 255u) : 256u;
             const unsigned peers = __match_any_sync(0xffffffffu, d);
             const unsigned lt = peers & ((1u << lane) - 1u);
             if (valid) dst[cnt[d] + __popc(lt)] = k;
@@ -440,7 +440,7 @@ __device__ __forceinline__ unsigned long long *warp_radix_sort(unsigned long lon
             if (valid && lt == 0) cnt[d] += __popc(peers);
             __syncwarp();
         }
-        unsigned long long *t = src;
+        unsigned int *t = src;
         src = dst;
         dst = t;
     }
@@ -462,7 +462,9 @@ __global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
     for (int64_t b = (int64_t)blockIdx.x * BKT_WPB + wib; b < NB; b += (int64_t)gridDim.x * BKT_WPB) {
         const int64_t base = boff[b];
         const int n = (int)(boff[b + 1] - base);
-        if (n > BKT_WCAP) continue;   // k_bkt_reduce
+        const int32_t gl = bseg[b], g = g0 + gl;
+        const int sh = segsh[gl], eb = segeb[gl];
+        if (n > BKT_WCAP || sh + eb > 32) continue;   // k_bkt_reduce
         if (n == 0) {
             if (lane == 0) {
                 ucnt[b] = 0;
@@ -470,21 +472,17 @@ __global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
             }
             continue;
         }
-        const int32_t gl = bseg[b], g = g0 + gl;
-        const int sh = segsh[gl], eb = segeb[gl];
         const int64_t hi = b - segBoff[gl];
-        for (int i = lane; i < n; i += 32) M.a[i] = keys[base + i];
+        for (int i = lane; i < n; i += 32) M.a[i] = (unsigned)keys[base + i];
         __syncwarp();
-        unsigned long long *srt = warp_radix_sort(M.a, M.b, n, 0, sh + eb, M.cnt);
-        double *gv = reinterpret_cast<double *>(srt == M.a ? M.b : M.a);
-        const int64_t f0 = fr_off[g];
-        const unsigned long long emask = (1ull << eb) - 1ull;
-        for (int i = lane; i < n; i += 32) gv[i] = fr_val[f0 + (int64_t)(srt[i] & emask)];
+        const unsigned *srt = warp_radix_sort(M.a, M.b, n, sh + eb, M.cnt);
+        const double *__restrict__ fv = fr_val + fr_off[g];
+        const unsigned emask = eb >= 32 ? 0xffffffffu : (1u << eb) - 1u;
         // run heads and their ranks
         int U = 0;
         for (int t0 = 0; t0 < n; t0 += 32) {
             const int i = t0 + lane;
-            const bool head = i < n && (i == 0 || (srt[i] >> eb) != (srt[i - 1] >> eb));
+            const bool head = i < n && (i == 0 || (eb < 32 && (srt[i] >> eb) != (srt[i - 1] >> eb)));
             const unsigned bal = __ballot_sync(full, head);
             if (head) M.runs[U + __popc(bal & ((1u << lane) - 1u))] = i;
             U += __popc(bal);
@@ -498,8 +496,8 @@ __global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
         for (int r = lane; r < U; r += 32) {
             const int i0 = M.runs[r], i1 = r + 1 < U ? M.runs[r + 1] : n;
             double sum = 0.0;
-            for (int i = i0; i < i1; i++) sum += gv[i];   // ascending source order (R13)
-            const int32_t u = (int32_t)((hi << sh) | (int64_t)(srt[i0] >> eb));
+            for (int i = i0; i < i1; i++) sum += fv[srt[i] & emask];   // ascending source order (R13)
+            const int32_t u = (int32_t)((hi << sh) | (int64_t)(eb >= 32 ? 0u : srt[i0] >> eb));
             const int64_t d = off[u + 1] - off[u];
             const double x = sum / (double)d;
             out_id[base + r] = u;

@@ -284,7 +284,7 @@ __device__ __forceinline__ uint4 next_arc(const uint2 R, uint64_t r64, const uin
 }
 
 // y-lookup modes of a warp (its query's table layout and the tile's staging plan).
-enum { YM_GLOBAL = 0, YM_SMEM = 1, YM_RANK = 2, YM_NONE = 3 };   // YM_NONE: diagnostic only (no y, wrong results)
+enum { YM_GLOBAL = 0, YM_SMEM = 1, YM_RANK = 2 };
 
 // NP walk pairs per thread = 2 NP independent chains (S_k from s, T_k from t for each pair),
 // advanced in lock step so 2 NP arc loads are in flight per thread.  Per step and chain:
@@ -348,8 +348,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
         for (int c = 0; c < C; c++) {
             acc[c] += pv[c];   // y of an earlier step, in step order
             pv[c] = 0.0;
-            if (mode == YM_NONE) {
-            } else if (mode != YM_SMEM) {   // resolve the previous step's node (v[c])
+            if (mode != YM_SMEM) {   // resolve the previous step's node (v[c])
                 const int64_t idx = mode == YM_RANK ? rank_index(prec[c], v[c])
                                                     : ylookup_resolve(*reinterpret_cast<const int4 *>(&prec[c]),
                                                                       gkeys, lgb, v[c], pol);
@@ -358,8 +357,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
             v[c] = (int32_t)A[c].x;
             if (ARC == 1 || ARC == 2) R[c] = make_uint2(A[c].y, A[c].z);
             else R[c] = ld_rec(rec + v[c], na1 >= 3);
-            if (mode == YM_NONE) {
-            } else if (mode == YM_RANK) {
+            if (mode == YM_RANK) {
                 prec[c] = ld_y(yrec + (v[c] >> 6), pol, y64);
             } else if (mode == YM_GLOBAL) {
                 const int4 bk = ld_bucket(gkeys, ybucket(v[c], lgb), pol, y64);
@@ -373,7 +371,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
 #pragma unroll
     for (int c = 0; c < C; c++) {
         acc[c] += pv[c];
-        if (mode != YM_SMEM && mode != YM_NONE && lf > 0) {
+        if (mode != YM_SMEM && lf > 0) {
             const int64_t idx = mode == YM_RANK ? rank_index(prec[c], v[c])
                                                 : ylookup_resolve(*reinterpret_cast<const int4 *>(&prec[c]), gkeys,
                                                                   lgb, v[c], pol);
@@ -465,7 +463,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
     __shared__ int64_t s_tile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
-    const int yp = y_policy & 3, y64 = (y_policy >> 2) & 1;   // GEER_Y_POLICY: +4 = L2::64B fetch size, +8 = no y (diagnostic)
+    const int yp = y_policy & 3, y64 = (y_policy >> 2) & 1;   // GEER_Y_POLICY: +4 = L2::64B fetch size
     const uint64_t pol = yp == 1 ? pol_evict_first() : yp == 2 ? pol_evict_last() : 0;
     const uint64_t apol = arc_policy ? pol_evict_first() : 0;
     const int na1 = arc_policy;   // the arc-load mode of ld_arc
@@ -479,7 +477,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             chunk = __shfl_sync(0xffffffffu, chunk, 0);
             if (chunk >= nchunks) break;
             if (cincl[i] <= chunk) i += 1 + find_chunk_query(cincl + i + 1, na - i - 1, chunk);
-            const int mode = (y_policy & 8) ? YM_NONE : qs[amc[i]].ymode == YT_RANK ? YM_RANK : YM_GLOBAL;
+            const int mode = qs[amc[i]].ymode == YT_RANK ? YM_RANK : YM_GLOBAL;
             walk_chunk<ARC, NP>(chunk, i, mode, nullptr, cincl, amc, qs, rec, arcs, cols, parcs, pk, b, key0, key1,
                                 reuse, pol, apol, na1, y64, parts);
         }
