@@ -336,12 +336,10 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         else if (8.0 * (double)n > 0.375 * (double)l2) layout = 1;
         (void)cols_foot;
         // DRAM-resident graphs keep cols + node records: a random DRAM access moves a whole line
-        // whatever the record size (profiles/sector_flavours_r02.txt), so the smaller 4-byte column
-        // array wins by its higher L2 hit rate (LJ-shaped config: 495 vs 517 ms of walks per step
-        // against 16-byte arc records); column loads are L2 evict-first (one-off random accesses
-        // must not push out the y-tables and node records) with the 64-byte L2 fetch size, node
-        // records 64-byte fetches (447 -> 418 ms; profiles/exp_walk_policy_r02.jsonl)
-        if (layout != 2) g->arc_policy = 4;   // (layouts 0, 1, 3: DRAM-resident)
+        // whatever the record size (profiles/sector_flavours_r02.txt), so the smaller column array
+        // wins by its higher L2 hit rate (LJ-shaped config: 495 vs 517 ms of walks per step against
+        // 16-byte arc records); K6 then loads columns L2 evict-first with 64-byte fetches and node
+        // records with 64-byte fetches (walks.cu; 447 -> 418 ms, profiles/exp_walk_policy_r02.jsonl)
         // cols with node ids below 2^24: 24-bit columns, 5 per 16-byte chunk (3.2 B per arc instead of
         // 4: a larger share of the random column loads hits L2)
         if (layout == 0 && n <= (1 << 24)) layout = 3;
@@ -359,10 +357,6 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_AMC_OVERLAP")) g->amc_overlap = atoi(env) != 0;
         if (const char *env = getenv("GEER_WALK_PERSIST")) g->walk_persist = atoi(env) != 0;
         if (const char *env = getenv("GEER_YTABLE")) g->ytable_force = !strcmp(env, "hash") ? 1 : !strcmp(env, "rank") ? 2 : 0;
-        if (const char *env = getenv("GEER_Y_EVICT_FIRST")) g->y_evict_first = atoi(env) != 0;
-        if (const char *env = getenv("GEER_Y_POLICY")) g->y_evict_first = std::min(15, std::max(0, atoi(env)));
-        if (const char *env = getenv("GEER_ARC_POLICY")) g->arc_policy = std::min(4, std::max(0, atoi(env)));
-        if (const char *env = getenv("GEER_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(env));
         if (const char *env = getenv("GEER_L2_PERSIST")) g->l2_persist = atoi(env) != 0;
         if (const char *env = getenv("GEER_OVERLAP_FRAC")) g->overlap_frac = std::min(1.0, std::max(0.1, atof(env)));
         if (const char *env = getenv("GEER_MAX_SUB_BATCH")) g->max_sub_batch = std::max<int64_t>(1, atoll(env));

@@ -153,8 +153,6 @@ struct er_graph {
     int64_t rank_max_bytes = 960 << 10;  // ... and when the records take at most this, i.e. graphs up to
                                          // ~3.9M nodes (GEER_RANK_MAX_KB; measured on configs 1-4)
     int ytable_force = 0;  // y-table layout: 0 by footprint, 1 hash only, 2 rank bitmap only (GEER_YTABLE)
-    int y_evict_first = 0; // K6: L2 policy on y-table loads: 0 none, 1 evict-first, 2 evict-last (GEER_Y_POLICY)
-    int arc_policy = 0;    // K6: arc loads 0 plain, 1 L2 evict-first, 2 + no L1 allocation (GEER_ARC_POLICY)
     bool l2_persist = false; // K6: persisting-L2 access window over the walk graph (GEER_L2_PERSIST)
     size_t l2_window = 0, l2_persist_bytes = 0;
     int64_t max_sub_batch = 1 << 18;  // queries per internal sub-batch (GEER_MAX_SUB_BATCH)

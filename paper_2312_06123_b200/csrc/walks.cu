@@ -111,114 +111,61 @@ __device__ __forceinline__ int bucket_match(const int4 a, int32_t v, bool *empty
     return m;
 }
 
-// y-structure loads with an optional L2 evict-first policy (pol != 0): the tables stream past,
-// the walk graph's arc records should stay in L2.
+// L2 evict-first access policy (for the one-off random loads of a DRAM-resident walk graph).
 __device__ __forceinline__ uint64_t pol_evict_first()
 {
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ uint64_t pol_evict_last()
+// Walk-graph loads.  DL = the walk graph is DRAM-resident (every layout but the
+// packed one): column / arc loads are L2 evict-first (one-off random accesses must not push the
+// y-tables and node records out of L2) with the 64-byte L2 fetch size (a random DRAM miss
+// otherwise moves a 128-byte line), node records 64-byte fetches; L2-resident packed records:
+// plain loads.  (Measured alternatives: profiles/exp_walk_policy_r02.jsonl.)
+template <bool DL>
+__device__ __forceinline__ uint4 ld_arc_v4(const uint4 *p, uint64_t apol)
 {
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-// Walk-graph (arc) loads, by GEER_ARC_POLICY: 0 plain; 1 L2 evict-first (default on
-// DRAM-resident graphs: an arc load is a one-off random access, it should not push the y-tables
-// and node records out of L2); 2 evict-first + no L1 allocation; 3 the L2::64B fetch size (a
-// random DRAM miss otherwise moves a 128-byte line); 4 evict-first + L2::64B.
-template <class T>
-__device__ __forceinline__ T ld_arc(const T *p, uint64_t apol, int am);
-template <>
-__device__ __forceinline__ uint4 ld_arc<uint4>(const uint4 *p, uint64_t apol, int am)
-{
+    if (!DL) return __ldg(p);
     uint4 r;
-    if (am == 0) return __ldg(p);
-    if (am == 1)
-        asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(apol));
-    else if (am == 2)
-        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(apol));
-    else if (am == 3)
-        asm("ld.global.nc.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    else
-        asm("ld.global.nc.L2::cache_hint.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(apol));
+    asm("ld.global.nc.L2::cache_hint.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(apol));
     return r;
 }
-template <>
-__device__ __forceinline__ unsigned long long ld_arc<unsigned long long>(const unsigned long long *p, uint64_t apol,
-                                                                         int am)
+template <bool DL>
+__device__ __forceinline__ unsigned long long ld_arc_u64(const unsigned long long *p, uint64_t apol)
 {
+    if (!DL) return __ldg(p);
     unsigned long long r;
-    if (am == 0) return __ldg(p);
-    if (am == 1) asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(apol));
-    else if (am == 2) asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(apol));
-    else if (am == 3) asm("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(r) : "l"(p));
-    else asm("ld.global.nc.L2::cache_hint.L2::64B.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(apol));
+    asm("ld.global.nc.L2::cache_hint.L2::64B.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(apol));
     return r;
 }
-template <>
-__device__ __forceinline__ int32_t ld_arc<int32_t>(const int32_t *p, uint64_t apol, int am)
+template <bool DL>
+__device__ __forceinline__ int32_t ld_arc_s32(const int32_t *p, uint64_t apol)
 {
+    if (!DL) return __ldg(p);
     int32_t r;
-    if (am == 0) return __ldg(p);
-    if (am == 1) asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(apol));
-    else if (am == 2) asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(apol));
-    else if (am == 3) asm("ld.global.nc.L2::64B.s32 %0, [%1];" : "=r"(r) : "l"(p));
-    else asm("ld.global.nc.L2::cache_hint.L2::64B.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(apol));
-    return r;
-}
-
-// y-structure loads: optional L2 policy (pol != 0) and, with y64, the L2::64B fetch size.
-__device__ __forceinline__ double ld_y(const double *p, uint64_t pol, int y64)
-{
-    double r;
-    if (y64) {
-        if (pol) asm("ld.global.nc.L2::cache_hint.L2::64B.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
-        else asm("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(r) : "l"(p));
-        return r;
-    }
-    if (!pol) return __ldg(p);
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ uint4 ld_y(const uint4 *p, uint64_t pol, int y64)
-{
-    uint4 r;
-    if (y64) {
-        if (pol)
-            asm("ld.global.nc.L2::cache_hint.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
-        else
-            asm("ld.global.nc.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-        return r;
-    }
-    if (!pol) return __ldg(p);
-    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+    asm("ld.global.nc.L2::cache_hint.L2::64B.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(apol));
     return r;
 }
 // node record {offset, degree} of the walk's current node
-__device__ __forceinline__ uint2 ld_rec(const uint2 *p, int r64)
+template <bool DL>
+__device__ __forceinline__ uint2 ld_rec(const uint2 *p)
 {
-    if (!r64) return __ldg(p);
+    if (!DL) return __ldg(p);
     uint2 r;
     asm("ld.global.nc.L2::64B.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
+__device__ __forceinline__ double ld_y(const double *p) { return __ldg(p); }
+__device__ __forceinline__ uint4 ld_y(const uint4 *p) { return __ldg(p); }
 
 // Hash lookups: slot of v, or -1 when v is not in supp(y) (then y(v) = 0, Alg. 1 L7 outside
 // U_s and U_t).  Staged keys in shared memory, or the table in global memory (one 16-byte
 // bucket per probe).  ylookup_global_from continues a global probe at bucket bk.
-__device__ __forceinline__ int4 ld_bucket(const int32_t *keys, uint32_t bk, uint64_t pol, int y64 = 0)
+__device__ __forceinline__ int4 ld_bucket(const int32_t *keys, uint32_t bk)
 {
-    const int4 *p = reinterpret_cast<const int4 *>(keys + (size_t)bk * YB);
-    const uint4 r = ld_y(reinterpret_cast<const uint4 *>(p), pol, y64);
-    return make_int4((int)r.x, (int)r.y, (int)r.z, (int)r.w);
+    return __ldg(reinterpret_cast<const int4 *>(keys + (size_t)bk * YB));
 }
 __device__ __forceinline__ int64_t ylookup_smem(const int32_t *skeys, int lgb, int32_t v)
 {
@@ -233,12 +180,11 @@ __device__ __forceinline__ int64_t ylookup_smem(const int32_t *skeys, int lgb, i
         bk = (bk + 1) & bmask;
     }
 }
-__device__ __forceinline__ int64_t ylookup_global_from(const int32_t *keys, int lgb, int32_t v, uint32_t bk,
-                                                       uint64_t pol)
+__device__ __forceinline__ int64_t ylookup_global_from(const int32_t *keys, int lgb, int32_t v, uint32_t bk)
 {
     const uint32_t bmask = (1u << lgb) - 1u;
     while (true) {
-        const int4 a = ld_bucket(keys, bk, pol);
+        const int4 a = ld_bucket(keys, bk);
         bool empty;
         const int m = bucket_match(a, v, &empty);
         if (m >= 0) return (int64_t)bk * YB + m;
@@ -247,30 +193,29 @@ __device__ __forceinline__ int64_t ylookup_global_from(const int32_t *keys, int 
     }
 }
 // Resolve a global probe whose first bucket `a` (of node v) was loaded one step earlier.
-__device__ __forceinline__ int64_t ylookup_resolve(const int4 a, const int32_t *keys, int lgb, int32_t v,
-                                                   uint64_t pol)
+__device__ __forceinline__ int64_t ylookup_resolve(const int4 a, const int32_t *keys, int lgb, int32_t v)
 {
     bool empty;
     const int m = bucket_match(a, v, &empty);
     const uint32_t bk = ybucket(v, lgb);
     if (m >= 0) return (int64_t)bk * YB + m;
     if (empty) return -1;
-    return ylookup_global_from(keys, lgb, v, (bk + 1) & ((1u << lgb) - 1u), pol);   // full bucket: rare
+    return ylookup_global_from(keys, lgb, v, (bk + 1) & ((1u << lgb) - 1u));   // full bucket: rare
 }
 
 template <int ARC>
 __device__ __forceinline__ uint4 next_arc(const uint2 R, uint64_t r64, const uint4 *__restrict__ arcs,
                                           const int32_t *__restrict__ cols,
-                                          const unsigned long long *__restrict__ parcs, PackSpec pk, uint64_t apol,
-                                          int na1)
+                                          const unsigned long long *__restrict__ parcs, PackSpec pk, uint64_t apol)
 {
     const uint64_t e = (uint64_t)R.x + __umul64hi(r64, (uint64_t)R.y);   // idx = floor(r64 d / 2^64) (R10)
-    if (ARC == 2) return pk.unpack(ld_arc(parcs + e, apol, na1));
-    if (ARC == 1) return ld_arc(arcs + e, apol, na1);
+    constexpr bool DL = ARC != 2;
+    if (ARC == 2) return pk.unpack(ld_arc_u64<DL>(parcs + e, apol));
+    if (ARC == 1) return ld_arc_v4<DL>(arcs + e, apol);
     if (ARC == 3) {   // 24-bit columns, 5 per 16-byte chunk (bytes 3p..3p+2 of the chunk)
         const uint64_t ch = e / 5u;
         const uint32_t p = (uint32_t)(e - 5u * ch);
-        const uint4 q = ld_arc(arcs + ch, apol, na1);
+        const uint4 q = ld_arc_v4<DL>(arcs + ch, apol);
         const uint32_t a = p <= 1 ? q.x : p == 2 ? q.y : p == 3 ? q.z : q.w;
         const uint32_t b = p == 1 ? q.y : p == 2 ? q.z : 0u;
         const uint32_t sh = p == 1 ? 24u : p == 2 ? 16u : p == 3 ? 8u : 0u;
@@ -279,7 +224,7 @@ __device__ __forceinline__ uint4 next_arc(const uint2 R, uint64_t r64, const uin
         return A;
     }
     uint4 A;
-    A.x = (uint32_t)ld_arc(cols + e, apol, na1);
+    A.x = (uint32_t)ld_arc_s32<DL>(cols + e, apol);
     return A;
 }
 
@@ -307,7 +252,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
                                             const uint4 *__restrict__ yrec, const double *__restrict__ gvals,
                                             int lgb, int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b,
                                             const uint64_t *kk, uint32_t key0, uint32_t key1, double *acc,
-                                            int32_t *endv, uint64_t pol, uint64_t apol, int na1, int y64)
+                                            int32_t *endv, uint64_t apol)
 {
     constexpr int C = 2 * NP;
     uint2 R[C];
@@ -318,7 +263,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
 #pragma unroll
     for (int c = 0; c < C; c++) {
         v[c] = (c & 1) ? t : s;
-        R[c] = ld_rec(rec + v[c], na1 >= 3);
+        R[c] = ld_rec<ARC != 2>(rec + v[c]);
         acc[c] = 0.0;
         pv[c] = 0.0;
         cz[c] = 0u;
@@ -342,7 +287,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
             } else {
                 r64 = ((uint64_t)cw[c] << 32) | cz[c];
             }
-            A[c] = next_arc<ARC>(R[c], r64, arcs, cols, parcs, pk, apol, na1);
+            A[c] = next_arc<ARC>(R[c], r64, arcs, cols, parcs, pk, apol);
         }
 #pragma unroll
         for (int c = 0; c < C; c++) {
@@ -351,20 +296,20 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
             if (mode != YM_SMEM) {   // resolve the previous step's node (v[c])
                 const int64_t idx = mode == YM_RANK ? rank_index(prec[c], v[c])
                                                     : ylookup_resolve(*reinterpret_cast<const int4 *>(&prec[c]),
-                                                                      gkeys, lgb, v[c], pol);
-                if (idx >= 0) pv[c] = ld_y(gvals + idx, pol, y64);
+                                                                      gkeys, lgb, v[c]);
+                if (idx >= 0) pv[c] = ld_y(gvals + idx);
             }
             v[c] = (int32_t)A[c].x;
             if (ARC == 1 || ARC == 2) R[c] = make_uint2(A[c].y, A[c].z);
-            else R[c] = ld_rec(rec + v[c], na1 >= 3);
+            else R[c] = ld_rec<ARC != 2>(rec + v[c]);
             if (mode == YM_RANK) {
-                prec[c] = ld_y(yrec + (v[c] >> 6), pol, y64);
+                prec[c] = ld_y(yrec + (v[c] >> 6));
             } else if (mode == YM_GLOBAL) {
-                const int4 bk = ld_bucket(gkeys, ybucket(v[c], lgb), pol, y64);
+                const int4 bk = ld_bucket(gkeys, ybucket(v[c], lgb));
                 prec[c] = make_uint4((uint32_t)bk.x, (uint32_t)bk.y, (uint32_t)bk.z, (uint32_t)bk.w);
             } else {
                 const int64_t slot = ylookup_smem(skeys, lgb, v[c]);
-                if (slot >= 0) pv[c] = ld_y(gvals + slot, pol, y64);
+                if (slot >= 0) pv[c] = ld_y(gvals + slot);
             }
         }
     }
@@ -374,8 +319,8 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
         if (mode != YM_SMEM && lf > 0) {
             const int64_t idx = mode == YM_RANK ? rank_index(prec[c], v[c])
                                                 : ylookup_resolve(*reinterpret_cast<const int4 *>(&prec[c]), gkeys,
-                                                                  lgb, v[c], pol);
-            if (idx >= 0) acc[c] += ld_y(gvals + idx, pol, y64);
+                                                                  lgb, v[c]);
+            if (idx >= 0) acc[c] += ld_y(gvals + idx);
         }
         endv[c] = v[c];
     }
@@ -390,8 +335,8 @@ __device__ __forceinline__ void walk_chunk(int64_t chunk, int32_t i, int mode, c
                                            const QState *__restrict__ qs, const uint2 *__restrict__ rec,
                                            const uint4 *__restrict__ arcs, const int32_t *__restrict__ cols,
                                            const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
-                                           uint32_t key0, uint32_t key1, int reuse, uint64_t pol, uint64_t apol,
-                                           int na1, int y64, TilePart *__restrict__ parts)
+                                           uint32_t key0, uint32_t key1, int reuse, uint64_t apol,
+                                           TilePart *__restrict__ parts)
 {
     const int lane = threadIdx.x & 31;
     const QState &Q = qs[amc[i]];
@@ -413,7 +358,7 @@ __device__ __forceinline__ void walk_chunk(int64_t chunk, int32_t i, int mode, c
     uint64_t ck = 0ull;
     if (any) {
         walk_chains<ARC, NP>(rec, arcs, cols, parcs, pk, mode, skeys, Q.ykeys, Q.yrec, Q.yvals, Q.ylog2 - YB_LOG,
-                             Q.s, Q.t, Q.st.ell_f, q, bkey, kk, key0, key1, acc, endv, pol, apol, na1, y64);
+                             Q.s, Q.t, Q.st.ell_f, q, bkey, kk, key0, key1, acc, endv, apol);
 #pragma unroll
         for (int p = 0; p < NP; p++) {
             if (kk[p] < (uint64_t)eta) {
@@ -453,7 +398,7 @@ __global__ void __launch_bounds__(WALK_THREADS, MINB)
 k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict__ amc,
         const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
         const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
-        uint32_t key0, uint32_t key1, int32_t smem_words, int y_policy, int arc_policy, int reuse,
+        uint32_t key0, uint32_t key1, int32_t smem_words, int reuse,
         unsigned long long *__restrict__ tile_ctr, TilePart *__restrict__ parts)
 {
     extern __shared__ __align__(32) int32_t sm_words[];
@@ -463,10 +408,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
     __shared__ int64_t s_tile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
-    const int yp = y_policy & 3, y64 = (y_policy >> 2) & 1;   // GEER_Y_POLICY: +4 = L2::64B fetch size
-    const uint64_t pol = yp == 1 ? pol_evict_first() : yp == 2 ? pol_evict_last() : 0;
-    const uint64_t apol = arc_policy ? pol_evict_first() : 0;
-    const int na1 = arc_policy;   // the arc-load mode of ld_arc
+    const uint64_t apol = ARC != 2 ? pol_evict_first() : 0;
     if (smem_words == 0) {
         int32_t i = 0;   // a warp's chunks only increase: its query index only moves forward
         for (int it = 0;; it++) {
@@ -479,7 +421,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             if (cincl[i] <= chunk) i += 1 + find_chunk_query(cincl + i + 1, na - i - 1, chunk);
             const int mode = qs[amc[i]].ymode == YT_RANK ? YM_RANK : YM_GLOBAL;
             walk_chunk<ARC, NP>(chunk, i, mode, nullptr, cincl, amc, qs, rec, arcs, cols, parcs, pk, b, key0, key1,
-                                reuse, pol, apol, na1, y64, parts);
+                                reuse, apol, parts);
         }
         return;
     }
@@ -524,7 +466,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
         __syncthreads();
         if (wvalid)
             walk_chunk<ARC, NP>(chunk, i, s_mode[warp], sm_words + s_soff[warp], cincl, amc, qs, rec, arcs, cols,
-                                parcs, pk, b, key0, key1, reuse, pol, apol, na1, y64, parts);
+                                parcs, pk, b, key0, key1, reuse, apol, parts);
         __syncthreads();
     }
 }
@@ -636,7 +578,7 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
 #define WALK_ARGS                                                                                         \
     na, cincl, list, qs, g->d_rec, g->d_c24 ? g->d_c24 : g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0,  \
         key1, smem_words,                                                                                     \
-        g->y_evict_first, g->arc_policy, P.reuse,                                                             \
+        P.reuse,                                                                                              \
         persist ? tctr + b : nullptr, parts
 #define WALK_LAUNCH(ARC, NP, MINB)                                                                          \
     do {                                                                                                    \
