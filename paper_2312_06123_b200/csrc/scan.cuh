@@ -179,6 +179,26 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan_apply(const T *__restrict__ in
     scan_store_tile<T, IT>(out, n, blockIdx.x, stage, x);
 }
 
+// Small inputs (a few tiles): one CTA scans in place of the three launches.
+template <class T, class Op, int IT>
+__global__ void __launch_bounds__(SCAN_NT) k_scan_single(const T *__restrict__ in, int64_t n, T zero, Op op,
+                                                         T *__restrict__ out)
+{
+    __shared__ T stage[SCAN_NT * IT];
+    __shared__ T sh[SCAN_NT / 32];
+    T carry = zero;
+    const int64_t nt = (n + SCAN_NT * IT - 1) / (SCAN_NT * IT);
+    for (int64_t tt = 0; tt < nt; tt++) {
+        T x[IT];
+        scan_load_tile<T, IT>(in, n, tt, stage, x, zero);
+        const T tot = scan_tile_regs<T, Op, IT>(x, carry, sh, op, zero);
+        scan_store_tile<T, IT>(out, n, tt, stage, x);
+        carry = op(carry, tot);
+    }
+}
+
+constexpr int SCAN_SINGLE_TILES = 8;
+
 // Temporary bytes the scan of n elements of T needs.
 template <class T>
 inline size_t scan_tmp_bytes(int64_t n)
@@ -195,6 +215,10 @@ inline int scan_launch(cudaStream_t st, const T *in, T *out, int64_t n, T zero, 
     if (n <= 0) return 0;
     constexpr int IT = ScanItems<T>::v;
     const int64_t nt = (n + (int64_t)SCAN_NT * IT - 1) / ((int64_t)SCAN_NT * IT);
+    if (nt <= SCAN_SINGLE_TILES) {
+        k_scan_single<T, Op, IT><<<1, SCAN_NT, 0, st>>>(in, n, zero, op, out);
+        return 1;
+    }
     T *ts = reinterpret_cast<T *>(tmp);
     k_scan_tiles<T, Op, IT><<<(unsigned)nt, SCAN_NT, 0, st>>>(in, n, zero, op, ts);
     k_scan_carry<T, Op, IT><<<1, SCAN_NT, 0, st>>>(ts, nt, zero, op);

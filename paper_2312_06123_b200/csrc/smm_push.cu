@@ -72,11 +72,18 @@ __global__ void k_bkt_plan(int32_t nseg, const int64_t *__restrict__ fr_off, con
 }
 
 // Segment of every bucket.
-__global__ void k_bkt_seg(int32_t nseg, const int64_t *__restrict__ segBoff, int32_t *__restrict__ bseg)
+__global__ void k_bkt_seg(int32_t nseg, const int64_t *__restrict__ segBoff, const int64_t *__restrict__ dNB,
+                          int32_t *__restrict__ bseg)
 {
-    const int32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= nseg) return;
-    for (int64_t b = segBoff[g]; b < segBoff[g + 1]; b++) bseg[b] = g;
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one thread per bucket
+    if (b >= *dNB) return;
+    int32_t lo = 0, hi = nseg;   // segBoff[lo] <= b < segBoff[hi]
+    while (hi - lo > 1) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (segBoff[mid] <= b) lo = mid;
+        else hi = mid;
+    }
+    bseg[b] = lo;
 }
 
 // Pair enumeration shared by count and scatter over the chunk's pairs P0 + [0, E) (entries
@@ -581,20 +588,26 @@ __device__ __forceinline__ MStat mstat_shfl(const MStat &a, int o)
     r.at_t = __shfl_xor_sync(0xffffffffu, a.at_t, o);
     return r;
 }
-__global__ void k_bkt_merge(int32_t nseg, int32_t g0, const int64_t *__restrict__ segBoff, const BStat *__restrict__ bst,
-                            SegStat *__restrict__ ss)
+constexpr int MERGE_NT = 128;
+__global__ void __launch_bounds__(MERGE_NT) k_bkt_merge(int32_t nseg, int32_t g0, const int64_t *__restrict__ segBoff,
+                                                        const BStat *__restrict__ bst, SegStat *__restrict__ ss)
 {
-    const int32_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;   // local segment
-    const int lane = threadIdx.x & 31;
+    // one CTA per segment (a large segment has thousands of buckets)
+    __shared__ MStat sm[MERGE_NT / 32];
+    const int32_t g = blockIdx.x;   // local segment
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (g >= nseg) return;
     MStat m{0, 0, 0, 0ull, 0ull, 0.0, 0.0};
-    for (int64_t b = segBoff[g] + lane; b < segBoff[g + 1]; b += 32) {
+    for (int64_t b = segBoff[g] + threadIdx.x; b < segBoff[g + 1]; b += MERGE_NT) {
         const BStat B = bst[b];
         m = mstat_merge(m, MStat{B.vol, B.n1, B.flags, B.max1, B.max2, B.at_s, B.at_t});
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = mstat_merge(m, mstat_shfl(m, o));
-    if (lane == 0) {
+    if (lane == 0) sm[warp] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < MERGE_NT / 32; w++) m = mstat_merge(m, sm[w]);
         SegStat &S = ss[g0 + g];
         S.vol = m.vol;
         S.max1 = __longlong_as_double((long long)m.m1);
@@ -697,7 +710,7 @@ int smm_push_wave_a(Ctx &c, int32_t g0, int32_t ns, int64_t P0, int64_t E, const
     CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (NBmax + 1), st));
     CK(cudaMemsetAsync(cur, 0, sizeof(unsigned int) * (NBmax + 1), st));
     CK(cudaMemsetAsync(ucnt, 0, sizeof(int64_t) * (NBmax + 1), st));
-    k_bkt_seg<<<blocks_for(ns, 256), 256, 0, st>>>(ns, segBoff, bseg);
+    k_bkt_seg<<<blocks_for(NBmax, 256), 256, 0, st>>>(ns, segBoff, dNB, bseg);
     LAUNCHED(g);
     // entry range of the chunk (host copies of two frontier offsets are not needed: the kernels
     // search the whole frontier's ent_off, which is monotone)
@@ -750,7 +763,7 @@ int smm_push_wave_b(Ctx &c, int32_t g0, int32_t ns, int64_t *dU)
     const int64_t *dNB = v.segBoff + ns;
     double *out_val = ws.pk_out.as<double>();
     const int32_t *out_id = reinterpret_cast<const int32_t *>(out_val + ws.pk_e);
-    k_bkt_merge<<<blocks_for((int64_t)ns * 32, 256), 256, 0, st>>>(ns, g0, v.segBoff, v.bst, ws.segstat.as<SegStat>());
+    k_bkt_merge<<<(unsigned)ns, MERGE_NT, 0, st>>>(ns, g0, v.segBoff, v.bst, ws.segstat.as<SegStat>());
     LAUNCHED(g);
     k_bkt_gather<<<blocks_for(NBmax * 32, 256), 256, 0, st>>>(dNB, ns, g0, v.bseg, v.segBoff, v.boff, v.uoff, out_id,
                                                               out_val, ws.nf_id.as<int32_t>(), ws.nf_val.as<double>(),

@@ -214,10 +214,41 @@ __global__ void __launch_bounds__(YH_THREADS) k_yhash(int32_t na, const int64_t 
 //   hash  pass 0: t* entries insert v with -(t*(v)/d(t)) (= 0.0/d(s) - t*(v)/d(t) exactly);
 //         pass 1: s* entries find-or-insert v: y = s*(v)/d(s) + stored (= a - b exactly, IEEE
 //                 a - b is a + (-b)) if v was inserted by its t* entry, else s*(v)/d(s) - 0.0
-//   rank  pass 0: every entry sets its side's bit of v in the build-time aux records;
-//         (k_yrank between the passes: union bits, rank of U and rank of the t* side per record)
+//   rank  (k_ybits: every entry's side bit of v into the build-time aux records; k_yrank: union
+//         bits, rank of U and rank of the t* side per record)
 //         pass 1: v's owner (its s* entry, else its t* entry) finds v's t* entry by rank (segment
 //                 start + rank T + popc) and writes y at rank U + popc(U bits below v)
+// Rank tables, side bits: one thread per frontier entry; the entries of one 64-id word of one
+// segment are consecutive (segments sorted by node id), so a warp ORs each run of equal
+// (segment, word) by a segmented shuffle scan and the run's first lane sets the bits with one
+// 64-bit atomicOr (a word split across warps gets one atomic per warp).  aux is zeroed before.
+__global__ void k_ybits(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
+                        const int32_t *__restrict__ id, const YDesc *__restrict__ yd)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    unsigned long long key = ~0ull, bits = 0;
+    unsigned long long *dst = nullptr;
+    if (e < Fmax && (dF == nullptr || e < *dF)) {
+        const int32_t g = seg[e];
+        const YDesc D = yd[g >> 1];
+        if (D.mode == YT_RANK) {
+            const int32_t v = id[e];
+            key = ((unsigned long long)(uint32_t)g << 32) | (uint32_t)(v >> 6);
+            bits = 1ull << (v & 63);
+            dst = reinterpret_cast<unsigned long long *>(D.aux + (v >> 6)) + (g & 1);
+        }
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, d);
+        const unsigned long long ob = __shfl_down_sync(0xffffffffu, bits, d);
+        if (lane + d < 32 && ok == key) bits |= ob;
+    }
+    const unsigned long long pk = __shfl_up_sync(0xffffffffu, key, 1);
+    if (dst != nullptr && (lane == 0 || pk != key)) atomicOr(dst, bits);
+}
+
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                           const int32_t *__restrict__ id, const double *__restrict__ val,
                           const int64_t *__restrict__ segoff, const YDesc *__restrict__ yd, int pass)
@@ -231,21 +262,7 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
     const int32_t v = id[e];
     if (D.mode == YT_RANK) {
         const uint64_t bit = 1ull << (v & 63);
-        if (pass == 0) {
-            // the segment's entries are sorted by node id: the first entry of each 64-id word writes
-            // the word's bits for its side (one writer per word and side: no atomics)
-            if (e > segoff[g] && (id[e - 1] >> 6) == (v >> 6)) return;
-            uint64_t bits = 0;
-            const int64_t e1 = segoff[g + 1];
-            for (int64_t f = e; f < e1; f++) {
-                const int32_t w = id[f];
-                if ((w >> 6) != (v >> 6)) break;
-                bits |= 1ull << (w & 63);
-            }
-            reinterpret_cast<unsigned long long *>(D.aux + (v >> 6))[side] = bits;
-            (void)bit;
-            return;
-        }
+        if (pass == 0) return;   // bits: k_ybits
         const uint4 a = D.aux[v >> 6];
         const uint64_t sbits = ((uint64_t)a.y << 32) | a.x, tbits = ((uint64_t)a.w << 32) | a.z;
         if (side == 1 && (sbits & bit)) return;   // the side-0 entry owns v
@@ -381,11 +398,13 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
         k_yhash<<<na, YH_THREADS, 0, c.st>>>(na, segoff, id, val, yd);
         LAUNCHED(c.g);
     }
-    for (int pass = 0; pass < 2; pass++) {   // rank tables and large hash tables
-        if (pass == 1 && R > 0) {
-            k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, sz, yd);
-            LAUNCHED(c.g);
-        }
+    if (R > 0) {
+        k_ybits<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, yd);
+        LAUNCHED(c.g);
+        k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, sz, yd);
+        LAUNCHED(c.g);
+    }
+    for (int pass = H > 0 ? 0 : 1; pass < 2; pass++) {   // rank tables (values) and large hash tables
         k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, segoff, yd, pass);
         LAUNCHED(c.g);
     }

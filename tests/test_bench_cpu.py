@@ -58,3 +58,29 @@ def test_plumbing_check_two_ranks_gloo():
     assert len(lines) == 1, p.stdout
     d = json.loads(lines[0])
     assert d["plumbing_check"] is True and d["n_ranks"] == 2 and d["gathered_ok"] is True
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_bench_gpu_line_tiny():
+    """The GPU arm end to end on the tiny config: one JSON line with the contract's keys, the
+    roofline and cpu_baseline objects, e2e with the bytes copied, launches counted, a sampled
+    parity summary with no differences beyond 1e-9."""
+    p = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "tiny", "--steps", "3", "--warmup", "3",
+                        "--no-spmm"], capture_output=True, text=True, cwd=str(ROOT), timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    need = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+            "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"}
+    assert need <= set(d), need - set(d)
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 100 * 8 and d["e2e"]["d2h_bytes_per_step"] == 100 * 8
+    for k in ("bound", "achieved", "peak", "unit", "frac"):
+        assert k in d["roofline"], k
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    ps = d["parity_summary"]
+    assert ps["max_abs_diff_r"] <= 1e-9 and ps["ties"] == 0 and ps["walk_checksums_equal"] == ps["queries"]
