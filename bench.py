@@ -319,7 +319,8 @@ def walk_roofline(prof, args, hbm, hbm_how, max_ms):
     ncu, nsrc = ncu_summary("k_walks", args.config)
     ceil = sector_ceilings()
     layout = {0: "cols + node records", 1: "16-byte arc records", 2: "packed 8-byte arc records",
-              3: "24-bit cols (5 per 16 B) + node records"}.get(
+              3: "24-bit cols (5 per 16 B) + node records",
+              4: "degree-ordered 24-bit cols (5 per 16 B) + shared-memory degree-class tree"}.get(
         prof.get("walk_layout", -1), "?")
     out = {"kernel": "k_walks (K6, AMC walks)", "walk_steps_per_s": steps_s, "avg_launch_ms": walk_launch_ms,
            "walk_steps_per_launch": steps_per_launch, "walk_share_of_step": prof["walk_ms"] / max(max_ms, 1e-9),

@@ -249,7 +249,8 @@ typedef struct er_profile {
     double amc_span_ms;      /* first K6 launch start to last K6 launch end, per batch, summed (the
                                 part above walk_ms is the AMC loop's K7 / scan / launch gaps) */
     int64_t walk_graph_bytes; /* bytes of the walk graph K6 reads (layout below), for the roofline */
-    int32_t walk_layout;     /* 0: cols + node records, 1: 16-byte arc records, 2: packed 8-byte arc records */
+    int32_t walk_layout;     /* 0: cols + node records, 1: 16-byte arc records, 2: packed 8-byte arc records,
+                                3: 24-bit cols + node records, 4: degree-ordered 24-bit cols + class tree */
     int32_t pad_;
 } er_profile;
 int er_graph_profile(er_graph *g, int enable);

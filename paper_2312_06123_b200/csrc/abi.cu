@@ -343,11 +343,26 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         // cols with node ids below 2^24: 24-bit columns, 5 per 16-byte chunk (3.2 B per arc instead of
         // 4: a larger share of the random column loads hits L2)
         if (layout == 0 && n <= (1 << 24)) layout = 3;
+        // and renumbered by degree (layout 4, falls back to 3 when not applicable): the node
+        // record comes from a shared-memory tree of the degree classes instead of a dependent
+        // global load (LJ-shaped config)
+        if (layout == 3) layout = 4;
         if (const char *env = getenv("GEER_WALK_LAYOUT")) {
             if (!strcmp(env, "arcs")) layout = 1;
             if (!strcmp(env, "cols")) layout = 0;
             if (!strcmp(env, "cols24") && n <= (1 << 24)) layout = 3;
+            if (!strcmp(env, "dord") && n <= (1 << 24)) layout = 4;
             if (!strcmp(env, "packed") && packable) layout = 2;
+        }
+        if (layout == 4 && e == cudaSuccess) {
+            const int rc = geer::build_dord(g, offsets, cols);
+            if (rc < 0) e = cudaErrorMemoryAllocation;
+            if (rc == 1) layout = 3;
+            // K6 column loads: about half of L2 worth of the column lines evict-last (a fixed share
+            // of the random column loads then hits L2), the rest evict-first (LJ-shaped config:
+            // 373 -> 334 ms of walks per step, flat for 15-45 % of the 238 MB)
+            if (rc == 0 && !getenv("GEER_WALK_L2_KEEP"))
+                g->walk_l2_keep = (float)std::min(1.0, 0.5 * (double)l2 / (16.0 * (double)((g->nnz + 4) / 5)));
         }
         // K6 scheduling: per-warp chunks when the walk graph is L2-resident (packed), CTA-tiles of
         // 8 chunks when it is DRAM-resident (measured: 4.40 vs 4.56 ms on config 1, 544 vs 529 ms
@@ -358,6 +373,7 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_WALK_PERSIST")) g->walk_persist = atoi(env) != 0;
         if (const char *env = getenv("GEER_YTABLE")) g->ytable_force = !strcmp(env, "hash") ? 1 : !strcmp(env, "rank") ? 2 : 0;
         if (const char *env = getenv("GEER_L2_PERSIST")) g->l2_persist = atoi(env) != 0;
+        if (const char *env = getenv("GEER_WALK_L2_KEEP")) g->walk_l2_keep = (float)std::min(1.0, std::max(0.0, atof(env)));
         if (const char *env = getenv("GEER_OVERLAP_FRAC")) g->overlap_frac = std::min(1.0, std::max(0.1, atof(env)));
         if (const char *env = getenv("GEER_MAX_SUB_BATCH")) g->max_sub_batch = std::max<int64_t>(1, atoll(env));
         if (const char *env = getenv("GEER_WAVE_PAIRS_MAX")) g->wave_pairs_max = std::max<int64_t>(1, atoll(env));
@@ -430,6 +446,10 @@ void er_graph_destroy(er_graph *g)
         if (g->d_arcs) cudaFree(g->d_arcs);
         if (g->d_parcs) cudaFree(g->d_parcs);
         if (g->d_c24) cudaFree(g->d_c24);
+        if (g->d_perm) cudaFree(g->d_perm);
+        if (g->d_iperm) cudaFree(g->d_iperm);
+        if (g->d_cblk) cudaFree(g->d_cblk);
+        if (g->d_ccd) cudaFree(g->d_ccd);
         if (g->d_steps) cudaFree(g->d_steps);
         if (g->d_rowperm) cudaFree(g->d_rowperm);
         if (g->d_hseg) cudaFree(g->d_hseg);
@@ -640,8 +660,10 @@ int er_graph_profile_read(er_graph *g, er_profile *out)
     std::lock_guard<std::mutex> lk(g->mu);
     *out = g->prof;
     out->walk_ctas_per_sm = g->walk_occ;
-    out->walk_layout = g->d_parcs ? 2 : g->d_c24 ? 3 : g->d_arcs ? 1 : 0;
+    out->walk_layout = g->d_parcs ? 2 : g->d_cblk ? 4 : g->d_c24 ? 3 : g->d_arcs ? 1 : 0;
     out->walk_graph_bytes = g->d_parcs ? 8 * g->nnz
+                            : g->d_cblk ? 16 * ((g->nnz + 4) / 5) + 4 * g->n + 4 * g->dord_nv
+                                              + 2 * (int64_t)g->dord_nblk + 8 * (int64_t)g->dord_ncls
                             : g->d_c24 ? 16 * ((g->nnz + 4) / 5) + 8 * g->n
                             : g->d_arcs ? 16 * g->nnz : 4 * g->nnz + 8 * g->n;
     if (g->d_steps) {

@@ -40,6 +40,22 @@ struct QState {
 
 
 // 64-bit packed arc record: u | offset(u) | degree(u) in bu + bo + bd <= 64 bits.
+// Degree-ordered walk graph (K6 layout 4): nodes renumbered by descending degree
+// (ties by id), each maximal run of equal degree ("class" c, degree d_c) padded to a multiple of
+// 2^bshift ids, so every block of 2^bshift new ids lies inside one class and its rows are
+// contiguous in the renumbered CSR: off(v) = base_c + (v - vstart_c) d_c.  K6 stages blk (class of
+// each block, u16) and cd (per class {base_c - vstart_c d_c mod 2^32, d_c}) in shared memory and
+// gets (off, d) of v from two shared loads instead of a dependent global load of v's node
+// record.  perm: old id -> new id; iperm: new id -> old id (-1 on padding); nv: new id space.
+struct DOrdView {
+    const int32_t *perm = nullptr;
+    const int32_t *iperm = nullptr;
+    const uint16_t *blk = nullptr;   // [nblk]
+    const uint2 *cd = nullptr;       // [ncls]
+    int32_t nblk = 0, ncls = 0, bshift = 0;
+};
+constexpr int DORD_SMEM_BYTES = 24 * 1024;   // shared memory per K6 CTA for blk + cd
+
 struct PackSpec {
     int bo = 0, bd = 0;  // bit widths of offset and degree (u takes the high bits)
     __host__ __device__ unsigned long long pack(uint32_t u, uint32_t off, uint32_t deg) const
@@ -109,6 +125,7 @@ struct Workspace {
     DevBuf segstat;                                 // SegStat per segment
     DevBuf ycap, yoff;                              // y-table sizes and their scans (per leaving query)
     DevBuf ydesc;                                   // K5 build-time table descriptors (per leaving query)
+    DevBuf ywid;                                    // K5: walk ids of the frontier entries (layout 4)
     DevBuf cub_tmp;                                 // CUB temp storage
     DevBuf scalars;                                 // small device scalars
     DevBuf spmm_part;                               // K9 heavy-row segment sums
@@ -136,6 +153,13 @@ struct er_graph {
     uint4 *d_arcs = nullptr;      // {u, offset(u), degree(u), 0} per arc, in CSR order (walk chain)
     unsigned long long *d_parcs = nullptr;  // packed 8-byte arc records (when they fit 64 bits)
     uint4 *d_c24 = nullptr;       // 24-bit columns, 5 per 16-byte chunk (DRAM-resident graphs with n < 2^24)
+    // degree-ordered walk graph (layout 4): d_c24 then holds the renumbered CSR's columns
+    int32_t *d_perm = nullptr, *d_iperm = nullptr;
+    uint16_t *d_cblk = nullptr;
+    uint2 *d_ccd = nullptr;
+    int32_t dord_nblk = 0, dord_ncls = 0, dord_bshift = 0;
+    float walk_l2_keep = 0.f;   // K6 column loads: fraction of lines L2 evict-last (rest evict-first)
+    int64_t dord_nv = 0;   // new id space (n plus class padding)
     geer::PackSpec pack;
     int32_t max_deg = 0;
     bool rows_sorted = false;
@@ -202,6 +226,9 @@ int run_estimate_lambda(er_graph *g, int iters, double *lambda_out);
 cudaError_t build_arcs(er_graph *g);
 cudaError_t build_parcs(er_graph *g);
 cudaError_t build_c24(er_graph *g);
+// layout 4 from the host CSR (offsets, cols): 1 = not applicable (too many degree classes, n or
+// nnz too large), 0 = built, < 0 = CUDA / host allocation failure
+int build_dord(er_graph *g, const int64_t *offsets, const int32_t *cols);
 // Device validation of the uploaded CSR (validate.cu): 1 = the host validation must decide.
 int validate_device(er_graph *g, int *code, std::string *msg, int *spectral, bool *rows_sorted, int32_t *max_deg);
 

@@ -27,6 +27,8 @@
 #include "geer_device.cuh"
 #include "stages.h"
 
+#include <vector>
+
 namespace geer {
 
 // ============================================================================ kernels
@@ -468,7 +470,7 @@ void Workspace::release()
     DevBuf *all[] = {&qs, &pairs, &out, &stats, &act, &act2, &cont, &idx, &fr_id, &fr_val, &fr_seg, &fr_off,
                      &nf_id, &nf_val, &nf_seg, &nf_off, &ent_off, &keys, &vals, &keys2, &vals2,
                      &runstart, &segstat, &ycap, &yoff, &cub_tmp, &scalars, &ids, &seglen, &segbeg, &cont2,
-                     &idx2, &spmm_part, &qids, &dense_x, &dense_y, &dense_cnt, &ydesc, &pk_seg, &pk_bkt, &pk_keys,
+                     &idx2, &spmm_part, &qids, &dense_x, &dense_y, &dense_cnt, &ydesc, &ywid, &pk_seg, &pk_bkt, &pk_keys,
                      &pk_alt, &pk_out};
     for (DevBuf *b : all) b->release();
     for (DevBuf &b : ychunk) b.release();
@@ -998,6 +1000,90 @@ cudaError_t build_c24(er_graph *g)
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     return e;
+}
+
+int build_dord(er_graph *g, const int64_t *off, const int32_t *cols)
+{
+    const int64_t n = g->n, nnz = g->nnz;
+    if (n > (1ll << 24) || nnz >= (1ll << 32) || nnz == 0) return 1;
+    int64_t maxd = 0;
+    for (int64_t v = 0; v < n; v++) maxd = std::max(maxd, off[v + 1] - off[v]);
+    std::vector<int64_t> cnt(maxd + 1, 0);
+    for (int64_t v = 0; v < n; v++) cnt[off[v + 1] - off[v]]++;
+    std::vector<int64_t> cdeg;   // classes in descending degree
+    for (int64_t d = maxd; d >= 0; d--)
+        if (cnt[d] > 0) cdeg.push_back(d);
+    const int64_t K = (int64_t)cdeg.size();
+    if (K > 65535) return 1;
+    // the smallest block (least padding) whose tables fit the shared-memory budget
+    int bs = -1;
+    int64_t nv = 0;
+    for (int b = 4; b <= 16 && bs < 0; b++) {
+        int64_t v = 0;
+        for (int64_t c = 0; c < K; c++) v += ((cnt[cdeg[c]] + (1ll << b) - 1) >> b) << b;
+        if (v <= (1ll << 24) && 2 * (v >> b) + 8 * K <= DORD_SMEM_BYTES) { bs = b; nv = v; }
+    }
+    if (bs < 0) return 1;
+    const int64_t nblk = nv >> bs;
+    std::vector<int64_t> pos(maxd + 1, 0);
+    std::vector<uint16_t> blk(nblk);
+    std::vector<uint2> cd(K);
+    {
+        int64_t vstart = 0, arcs = 0;
+        for (int64_t c = 0; c < K; c++) {
+            const int64_t d = cdeg[c], size = ((cnt[d] + (1ll << bs) - 1) >> bs) << bs;
+            pos[d] = vstart;
+            cd[c] = make_uint2((uint32_t)arcs - (uint32_t)vstart * (uint32_t)d, (uint32_t)d);   // mod 2^32
+            for (int64_t k = vstart >> bs; k < (vstart + size) >> bs; k++) blk[k] = (uint16_t)c;
+            vstart += size;
+            arcs += cnt[d] * d;
+        }
+    }
+    // renumbering: by descending degree, ties by id (a stable counting sort)
+    std::vector<int32_t> perm(n), iperm(nv, -1);
+    for (int64_t v = 0; v < n; v++) {
+        const int64_t u = pos[off[v + 1] - off[v]]++;
+        perm[v] = (int32_t)u;
+        iperm[u] = (int32_t)v;
+    }
+    // the renumbered CSR: row perm[v] = perm of v's neighbours, in v's order (padding ids: no row)
+    std::vector<int32_t> ncols(nnz);
+    {
+        int64_t j = 0;
+        for (int64_t u = 0; u < nv; u++) {
+            const int32_t v = iperm[u];
+            if (v < 0) continue;
+            for (int64_t e = off[v]; e < off[v + 1]; e++) ncols[j++] = perm[cols[e]];
+        }
+    }
+    int32_t *dtmp = nullptr;
+    cudaError_t e = cudaMalloc(&g->d_c24, sizeof(uint4) * std::max<int64_t>((nnz + 4) / 5, 1));
+    if (e == cudaSuccess) e = cudaMalloc(&dtmp, sizeof(int32_t) * nnz);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_perm, sizeof(int32_t) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_iperm, sizeof(int32_t) * nv);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_cblk, sizeof(uint16_t) * nblk);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_ccd, sizeof(uint2) * K);
+    if (e == cudaSuccess) e = cudaMemcpy(dtmp, ncols.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_perm, perm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_iperm, iperm.data(), sizeof(int32_t) * nv, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_cblk, blk.data(), sizeof(uint16_t) * nblk, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_ccd, cd.data(), sizeof(uint2) * K, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        k_build_c24<<<blocks_for((nnz + 4) / 5, 256), 256>>>(nnz, dtmp, g->d_c24);
+        g->launches++;
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    if (dtmp) cudaFree(dtmp);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "er_graph_create (degree-ordered walk graph)");
+        return -1;
+    }
+    g->dord_nblk = (int32_t)nblk;
+    g->dord_ncls = (int32_t)K;
+    g->dord_bshift = bs;
+    g->dord_nv = nv;
+    return 0;
 }
 
 cudaError_t build_parcs(er_graph *g)

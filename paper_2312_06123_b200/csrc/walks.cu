@@ -118,6 +118,14 @@ __device__ __forceinline__ uint64_t pol_evict_first()
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+// Fraction `keep` of the lines (by address) L2 evict-last, the others evict-first: a fixed part
+// of a DRAM-resident walk graph stays in L2 while the rest streams past.
+__device__ __forceinline__ uint64_t pol_keep_fraction(float keep)
+{
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(p) : "f"(keep));
+    return p;
+}
 // Walk-graph loads.  DL = the walk graph is DRAM-resident (every layout but the
 // packed one): column / arc loads are L2 evict-first (one-off random accesses must not push the
 // y-tables and node records out of L2) with the 64-byte L2 fetch size (a random DRAM miss
@@ -203,25 +211,50 @@ __device__ __forceinline__ int64_t ylookup_resolve(const int4 a, const int32_t *
     return ylookup_global_from(keys, lgb, v, (bk + 1) & ((1u << lgb) - 1u));   // full bucket: rare
 }
 
+// Layout 4: node record {off(v), d(v)} of renumbered node v from the degree-class tables staged
+// in shared memory (geer_internal.h DOrdView): class of v's block, then the class's {base', d}.
+// 32-bit words of K6's layout-4 tables in shared memory (rounded to 16 bytes for the staging area)
+__host__ __device__ inline int32_t dord_smem_words(int32_t ncls, int32_t nblk)
+{
+    return ((2 * ncls + (nblk + 1) / 2) + 3) & ~3;
+}
+struct STree {
+    const uint16_t *blk;
+    const uint2 *cd;
+    int32_t bshift;
+};
+__device__ __forceinline__ uint2 class_rec(const STree &T, uint32_t v)
+{
+    const uint2 cd = T.cd[T.blk[v >> T.bshift]];
+    return make_uint2(cd.x + v * cd.y, cd.y);   // base_c + (v - vstart_c) d_c, exact mod 2^32 (off < 2^32)
+}
+
+// Column p (0..4) of a 24-bit chunk: bytes 3p..3p+2, i.e. bits 24p..24p+23 of the 128-bit chunk.
+// Branch-free (selects only), and applied only after every chain's chunk load has been issued:
+// a data-dependent branch between two chains' loads makes the second wait for the first.
+__device__ __forceinline__ uint32_t col24(const uint4 q, uint32_t p)
+{
+    const uint64_t lo = ((uint64_t)q.y << 32) | q.x, hi = ((uint64_t)q.w << 32) | q.z;
+    const uint32_t bo = 24u * p;   // 0, 24, 48, 72, 96
+    uint64_t v = (bo < 64u ? lo : hi) >> (bo & 63u);
+    v |= bo == 48u ? hi << 16 : 0ull;   // bits 48..71 straddle the two halves
+    return (uint32_t)v & 0xFFFFFFu;
+}
+
 template <int ARC>
 __device__ __forceinline__ uint4 next_arc(const uint2 R, uint64_t r64, const uint4 *__restrict__ arcs,
                                           const int32_t *__restrict__ cols,
-                                          const unsigned long long *__restrict__ parcs, PackSpec pk, uint64_t apol)
+                                          const unsigned long long *__restrict__ parcs, PackSpec pk, uint64_t apol,
+                                          uint32_t *p24)
 {
     const uint64_t e = (uint64_t)R.x + __umul64hi(r64, (uint64_t)R.y);   // idx = floor(r64 d / 2^64) (R10)
     constexpr bool DL = ARC != 2;
     if (ARC == 2) return pk.unpack(ld_arc_u64<DL>(parcs + e, apol));
     if (ARC == 1) return ld_arc_v4<DL>(arcs + e, apol);
-    if (ARC == 3) {   // 24-bit columns, 5 per 16-byte chunk (bytes 3p..3p+2 of the chunk)
+    if (ARC == 3 || ARC == 4) {   // 24-bit columns, 5 per 16-byte chunk: the raw chunk; *p24 = its slot
         const uint64_t ch = e / 5u;
-        const uint32_t p = (uint32_t)(e - 5u * ch);
-        const uint4 q = ld_arc_v4<DL>(arcs + ch, apol);
-        const uint32_t a = p <= 1 ? q.x : p == 2 ? q.y : p == 3 ? q.z : q.w;
-        const uint32_t b = p == 1 ? q.y : p == 2 ? q.z : 0u;
-        const uint32_t sh = p == 1 ? 24u : p == 2 ? 16u : p == 3 ? 8u : 0u;
-        uint4 A;
-        A.x = __funnelshift_r(a, b, sh) & 0xFFFFFFu;
-        return A;
+        *p24 = (uint32_t)(e - 5u * ch);
+        return ld_arc_v4<DL>(arcs + ch, apol);
     }
     uint4 A;
     A.x = (uint32_t)ld_arc_s32<DL>(cols + e, apol);
@@ -252,7 +285,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
                                             const uint4 *__restrict__ yrec, const double *__restrict__ gvals,
                                             int lgb, int32_t s, int32_t t, int32_t lf, uint32_t q, uint32_t b,
                                             const uint64_t *kk, uint32_t key0, uint32_t key1, double *acc,
-                                            int32_t *endv, uint64_t apol)
+                                            int32_t *endv, uint64_t apol, const STree &T)
 {
     constexpr int C = 2 * NP;
     uint2 R[C];
@@ -263,7 +296,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
 #pragma unroll
     for (int c = 0; c < C; c++) {
         v[c] = (c & 1) ? t : s;
-        R[c] = ld_rec<ARC != 2>(rec + v[c]);
+        R[c] = ARC == 4 ? class_rec(T, (uint32_t)v[c]) : ld_rec<ARC != 2>(rec + v[c]);
         acc[c] = 0.0;
         pv[c] = 0.0;
         cz[c] = 0u;
@@ -273,6 +306,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
     }
     for (int32_t j = 1; j <= lf; j++) {
         uint4 A[C];
+        uint32_t p24[C];
 #pragma unroll
         for (int c = 0; c < C; c++) {
             uint64_t r64;
@@ -287,7 +321,11 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
             } else {
                 r64 = ((uint64_t)cw[c] << 32) | cz[c];
             }
-            A[c] = next_arc<ARC>(R[c], r64, arcs, cols, parcs, pk, apol);
+            A[c] = next_arc<ARC>(R[c], r64, arcs, cols, parcs, pk, apol, &p24[c]);
+        }
+        if (ARC == 3 || ARC == 4) {
+#pragma unroll
+            for (int c = 0; c < C; c++) A[c].x = col24(A[c], p24[c]);
         }
 #pragma unroll
         for (int c = 0; c < C; c++) {
@@ -301,6 +339,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
             }
             v[c] = (int32_t)A[c].x;
             if (ARC == 1 || ARC == 2) R[c] = make_uint2(A[c].y, A[c].z);
+            else if (ARC == 4) R[c] = class_rec(T, (uint32_t)v[c]);
             else R[c] = ld_rec<ARC != 2>(rec + v[c]);
             if (mode == YM_RANK) {
                 prec[c] = ld_y(yrec + (v[c] >> 6));
@@ -336,7 +375,7 @@ __device__ __forceinline__ void walk_chunk(int64_t chunk, int32_t i, int mode, c
                                            const uint4 *__restrict__ arcs, const int32_t *__restrict__ cols,
                                            const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
                                            uint32_t key0, uint32_t key1, int reuse, uint64_t apol,
-                                           TilePart *__restrict__ parts)
+                                           TilePart *__restrict__ parts, const DOrdView &dv, const STree &T)
 {
     const int lane = threadIdx.x & 31;
     const QState &Q = qs[amc[i]];
@@ -357,8 +396,18 @@ __device__ __forceinline__ void walk_chunk(int64_t chunk, int32_t i, int mode, c
     double s1 = 0.0, s2 = 0.0;
     uint64_t ck = 0ull;
     if (any) {
+        // layout 4 walks (and its y-tables are keyed) in the renumbered ids; the end nodes go back
+        // to the caller's ids for the checksum
+        const int32_t s = ARC == 4 ? __ldg(dv.perm + Q.s) : Q.s, t = ARC == 4 ? __ldg(dv.perm + Q.t) : Q.t;
         walk_chains<ARC, NP>(rec, arcs, cols, parcs, pk, mode, skeys, Q.ykeys, Q.yrec, Q.yvals, Q.ylog2 - YB_LOG,
-                             Q.s, Q.t, Q.st.ell_f, q, bkey, kk, key0, key1, acc, endv, apol);
+                             s, t, Q.st.ell_f, q, bkey, kk, key0, key1, acc, endv, apol, T);
+#pragma unroll
+        for (int p = 0; p < NP; p++) {
+            if (ARC == 4 && kk[p] < (uint64_t)eta) {
+                endv[2 * p] = __ldg(dv.iperm + endv[2 * p]);
+                endv[2 * p + 1] = __ldg(dv.iperm + endv[2 * p + 1]);
+            }
+        }
 #pragma unroll
         for (int p = 0; p < NP; p++) {
             if (kk[p] < (uint64_t)eta) {
@@ -399,16 +448,28 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
         const QState *__restrict__ qs, const uint2 *__restrict__ rec, const uint4 *__restrict__ arcs,
         const int32_t *__restrict__ cols, const unsigned long long *__restrict__ parcs, PackSpec pk, int b,
         uint32_t key0, uint32_t key1, int32_t smem_words, int reuse,
-        unsigned long long *__restrict__ tile_ctr, TilePart *__restrict__ parts)
+        unsigned long long *__restrict__ tile_ctr, TilePart *__restrict__ parts, DOrdView dv, float keep)
 {
-    extern __shared__ __align__(32) int32_t sm_words[];
+    extern __shared__ __align__(32) int32_t sm_dyn[];
     __shared__ int32_t s_qi[WALK_WARPS];
     __shared__ int32_t s_soff[WALK_WARPS];
     __shared__ int32_t s_mode[WALK_WARPS];
     __shared__ int64_t s_tile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nchunks = cincl[na - 1];   // read on the device: no host round trip per batch
-    const uint64_t apol = ARC != 2 ? pol_evict_first() : 0;
+    const uint64_t apol = ARC == 2 ? 0 : keep > 0.f ? pol_keep_fraction(keep) : pol_evict_first();
+    // layout 4: the degree-class tables first in dynamic shared memory (cd, then blk), staging after
+    STree T{nullptr, nullptr, 0};
+    int32_t *sm_words = sm_dyn;
+    if (ARC == 4) {
+        uint2 *scd = reinterpret_cast<uint2 *>(sm_dyn);
+        uint16_t *sblk = reinterpret_cast<uint16_t *>(scd + dv.ncls);
+        for (int32_t k = threadIdx.x; k < dv.ncls; k += WALK_THREADS) scd[k] = __ldg(dv.cd + k);
+        for (int32_t k = threadIdx.x; k < dv.nblk; k += WALK_THREADS) sblk[k] = __ldg(dv.blk + k);
+        __syncthreads();
+        T = STree{sblk, scd, dv.bshift};
+        sm_words = sm_dyn + dord_smem_words(dv.ncls, dv.nblk);
+    }
     if (smem_words == 0) {
         int32_t i = 0;   // a warp's chunks only increase: its query index only moves forward
         for (int it = 0;; it++) {
@@ -421,7 +482,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
             if (cincl[i] <= chunk) i += 1 + find_chunk_query(cincl + i + 1, na - i - 1, chunk);
             const int mode = qs[amc[i]].ymode == YT_RANK ? YM_RANK : YM_GLOBAL;
             walk_chunk<ARC, NP>(chunk, i, mode, nullptr, cincl, amc, qs, rec, arcs, cols, parcs, pk, b, key0, key1,
-                                reuse, apol, parts);
+                                reuse, apol, parts, dv, T);
         }
         return;
     }
@@ -466,7 +527,7 @@ k_walks(int32_t na, const int64_t *__restrict__ cincl, const int32_t *__restrict
         __syncthreads();
         if (wvalid)
             walk_chunk<ARC, NP>(chunk, i, s_mode[warp], sm_words + s_soff[warp], cincl, amc, qs, rec, arcs, cols,
-                                parcs, pk, b, key0, key1, reuse, apol, parts);
+                                parcs, pk, b, key0, key1, reuse, apol, parts, dv, T);
         __syncthreads();
     }
 }
@@ -579,7 +640,7 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
     na, cincl, list, qs, g->d_rec, g->d_c24 ? g->d_c24 : g->d_arcs, g->d_cols, g->d_parcs, g->pack, b, key0,  \
         key1, smem_words,                                                                                     \
         P.reuse,                                                                                              \
-        persist ? tctr + b : nullptr, parts
+        persist ? tctr + b : nullptr, parts, dv, g->walk_l2_keep
 #define WALK_LAUNCH(ARC, NP, MINB)                                                                          \
     do {                                                                                                    \
         CK(cudaFuncSetAttribute(k_walks<ARC, NP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
@@ -601,6 +662,7 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
 #define WALK_ARC(NP, MINB)                                   \
     do {                                                     \
         if (g->d_parcs) WALK_LAUNCH(2, NP, MINB);            \
+        else if (g->d_cblk) WALK_LAUNCH(4, NP, MINB);        \
         else if (g->d_c24) WALK_LAUNCH(3, NP, MINB);         \
         else if (g->d_arcs) WALK_LAUNCH(1, NP, MINB);        \
         else WALK_LAUNCH(0, NP, MINB);                       \
@@ -611,7 +673,19 @@ int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs
         // fraction of the resident-CTA slots so head kernels always find room on every SM
         const bool persist = g->walk_persist;
         const double slot_frac = g->amc_overlap ? g->overlap_frac : 1.0;
-        const size_t smem_bytes = sizeof(int32_t) * (size_t)std::max(smem_words, 0);
+        DOrdView dv;
+        size_t tree_bytes = 0;
+        if (g->d_cblk) {
+            dv.perm = g->d_perm;
+            dv.iperm = g->d_iperm;
+            dv.blk = g->d_cblk;
+            dv.cd = g->d_ccd;
+            dv.nblk = g->dord_nblk;
+            dv.ncls = g->dord_ncls;
+            dv.bshift = g->dord_bshift;
+            tree_bytes = sizeof(int32_t) * (size_t)dord_smem_words(dv.ncls, dv.nblk);
+        }
+        const size_t smem_bytes = tree_bytes + sizeof(int32_t) * (size_t)std::max(smem_words, 0);
         if (g->walk_np == 1) {
             if (g->walk_minb == 3) WALK_ARC(1, 3);
             else if (g->walk_minb == 5) WALK_ARC(1, 5);

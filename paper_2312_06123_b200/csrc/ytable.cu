@@ -8,6 +8,13 @@
 
 namespace geer {
 
+// The node id the walk kernel uses for node v (its y-table key): the degree-ordered renumbering
+// of walk layout 4 (geer_internal.h DOrdView), else v.
+__device__ __forceinline__ int32_t walk_id(const int32_t *__restrict__ perm, int32_t v)
+{
+    return perm != nullptr ? __ldg(perm + v) : v;
+}
+
 // y-tables (K5): y(v) = s*(v)/d(s) - t*(v)/d(t) on U = supp(s*) u supp(t*) for each query that
 // leaves the SMM head for AMC in this wave (Alg. 1 L7 with s = s*, t = t*).  Two layouts,
 // chosen per query by footprint:
@@ -168,24 +175,25 @@ __device__ __forceinline__ int64_t yh_insert(int32_t *keys, int lgb, int32_t v, 
 }
 template <bool SMEM>
 __device__ __forceinline__ void yh_build(int32_t *keys, const YDesc &D, const int32_t *__restrict__ id,
-                                         const double *__restrict__ val, int64_t s0, int64_t s1, int64_t t1)
+                                         const int32_t *__restrict__ perm, const double *__restrict__ val, int64_t s0,
+                                         int64_t s1, int64_t t1)
 {
     for (int64_t e = s1 + threadIdx.x; e < t1; e += YH_THREADS) {   // t* entries first
         bool found;
-        const int64_t slot = yh_insert<SMEM>(keys, D.lgb, id[e], &found);
+        const int64_t slot = yh_insert<SMEM>(keys, D.lgb, walk_id(perm, id[e]), &found);
         D.vals[slot] = -(val[e] / (double)D.dt);
     }
     __syncthreads();
     for (int64_t e = s0 + threadIdx.x; e < s1; e += YH_THREADS) {
         bool found;
-        const int64_t slot = yh_insert<SMEM>(keys, D.lgb, id[e], &found);
+        const int64_t slot = yh_insert<SMEM>(keys, D.lgb, walk_id(perm, id[e]), &found);
         const double a = val[e] / (double)D.ds;
         D.vals[slot] = found ? a + D.vals[slot] : a - 0.0;
     }
 }
 __global__ void __launch_bounds__(YH_THREADS) k_yhash(int32_t na, const int64_t *__restrict__ segoff,
-                                                      const int32_t *__restrict__ id, const double *__restrict__ val,
-                                                      const YDesc *__restrict__ yd)
+                                                      const int32_t *__restrict__ id, const int32_t *__restrict__ perm,
+                                                      const double *__restrict__ val, const YDesc *__restrict__ yd)
 {
     __shared__ __align__(16) int32_t sk[YH_SMEM_SLOTS];
     const int32_t i = blockIdx.x;
@@ -198,7 +206,7 @@ __global__ void __launch_bounds__(YH_THREADS) k_yhash(int32_t na, const int64_t 
     {
         for (int j = threadIdx.x; j < cap; j += YH_THREADS) sk[j] = -1;
         __syncthreads();
-        yh_build<true>(sk, D, id, val, s0, s1, t1);
+        yh_build<true>(sk, D, id, perm, val, s0, s1, t1);
         __syncthreads();
         int4 *dst = reinterpret_cast<int4 *>(D.keys);
         const int4 *src = reinterpret_cast<const int4 *>(sk);
@@ -206,24 +214,24 @@ __global__ void __launch_bounds__(YH_THREADS) k_yhash(int32_t na, const int64_t 
     }
 }
 
-// K5, rank layout, over the support entries (frontier entry e: node id[e], value val[e], segment
-// seg[e] = 2 i + side; each segment sorted by node id) of the leaving queries.  Every node v of
+// K5 over the support entries (frontier entry e: node id[e], value val[e], segment seg[e] = 2 i +
+// side) of the leaving queries.  Tables are keyed by the walk kernel's node ids (walk_id: the
+// degree-ordered renumbering of walk layout 4, else the ids themselves).  Every node v of
 // U = supp(s*) u supp(t*) gets
 //     y(v) = s*(v)/d(s) - t*(v)/d(t)          (a side v is not on contributes 0.0 / d = 0.0)
-// written exactly once in its final form (Alg. 1 L7 with s = s*, t = t*), no searches:
-//   hash  pass 0: t* entries insert v with -(t*(v)/d(t)) (= 0.0/d(s) - t*(v)/d(t) exactly);
-//         pass 1: s* entries find-or-insert v: y = s*(v)/d(s) + stored (= a - b exactly, IEEE
-//                 a - b is a + (-b)) if v was inserted by its t* entry, else s*(v)/d(s) - 0.0
-//   rank  (k_ybits: every entry's side bit of v into the build-time aux records; k_yrank: union
-//         bits, rank of U and rank of the t* side per record)
-//         pass 1: v's owner (its s* entry, else its t* entry) finds v's t* entry by rank (segment
-//                 start + rank T + popc) and writes y at rank U + popc(U bits below v)
-// Rank tables, side bits: one thread per frontier entry; the entries of one 64-id word of one
-// segment are consecutive (segments sorted by node id), so a warp ORs each run of equal
-// (segment, word) by a segmented shuffle scan and the run's first lane sets the bits with one
-// 64-bit atomicOr (a word split across warps gets one atomic per warp).  aux is zeroed before.
+// in two passes, no searches and no floating-point atomics (Alg. 1 L7 with s = s*, t = t*):
+//   pass 0: t* entries store -(t*(v)/d(t)) (= 0.0/d(s) - t*(v)/d(t) exactly);
+//   pass 1: s* entries: y = s*(v)/d(s) + stored (= a - b exactly, IEEE a - b is a + (-b)) if v
+//           has a t* entry, else s*(v)/d(s) - 0.0.
+// hash: the slot of v by find-or-insert; rank: the slot at rank U + popc(U bits below v) (k_ybits:
+// every entry's side bit of v into the build-time aux records; k_yrank: union bits and ranks).
+// Rank tables, side bits: one thread per frontier entry; a warp ORs each run of equal (segment,
+// 64-id word) by a segmented shuffle scan and the run's first lane sets the bits with one 64-bit
+// atomicOr (segments are sorted by node id: without renumbering a word's entries are consecutive,
+// one atomic per word and warp).  aux is zeroed before.
 __global__ void k_ybits(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
-                        const int32_t *__restrict__ id, const YDesc *__restrict__ yd)
+                        const int32_t *__restrict__ id, const int32_t *__restrict__ perm,
+                        const YDesc *__restrict__ yd)
 {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
@@ -233,7 +241,7 @@ __global__ void k_ybits(int64_t Fmax, const int64_t *__restrict__ dF, const int3
         const int32_t g = seg[e];
         const YDesc D = yd[g >> 1];
         if (D.mode == YT_RANK) {
-            const int32_t v = id[e];
+            const int32_t v = walk_id(perm, id[e]);
             key = ((unsigned long long)(uint32_t)g << 32) | (uint32_t)(v >> 6);
             bits = 1ull << (v & 63);
             dst = reinterpret_cast<unsigned long long *>(D.aux + (v >> 6)) + (g & 1);
@@ -249,9 +257,21 @@ __global__ void k_ybits(int64_t Fmax, const int64_t *__restrict__ dF, const int3
     if (dst != nullptr && (lane == 0 || pk != key)) atomicOr(dst, bits);
 }
 
+// Layout 4: the walk id (renumbered node id) of every frontier entry of a leaving query, once, so
+// the build passes read ids sequentially instead of each looking up perm.
+__global__ void k_ywid(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
+                       const int32_t *__restrict__ id, const int32_t *__restrict__ perm,
+                       const YDesc *__restrict__ yd, int32_t *__restrict__ wid)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
+    if (yd[seg[e] >> 1].mode < 0) return;
+    wid[e] = __ldg(perm + id[e]);
+}
+
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
-                          const int32_t *__restrict__ id, const double *__restrict__ val,
-                          const int64_t *__restrict__ segoff, const YDesc *__restrict__ yd, int pass)
+                          const int32_t *__restrict__ id, const int32_t *__restrict__ perm,
+                          const double *__restrict__ val, const YDesc *__restrict__ yd, int pass)
 {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
@@ -259,28 +279,24 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
     const YDesc D = yd[g >> 1];
     if (D.mode < 0) return;
     const int side = g & 1;
-    const int32_t v = id[e];
+    if (side != (pass == 0 ? 1 : 0)) return;
+    // hash tables of <= YH_SMEM_SLOTS slots are built by k_yhash (one CTA per query, shared memory)
+    if (D.mode == YT_HASH && (YB << D.lgb) <= YH_SMEM_SLOTS_DEV) return;
+    const int32_t v = walk_id(perm, id[e]);
     if (D.mode == YT_RANK) {
         const uint64_t bit = 1ull << (v & 63);
-        if (pass == 0) return;   // bits: k_ybits
-        const uint4 a = D.aux[v >> 6];
-        const uint64_t sbits = ((uint64_t)a.y << 32) | a.x, tbits = ((uint64_t)a.w << 32) | a.z;
-        if (side == 1 && (sbits & bit)) return;   // the side-0 entry owns v
         const uint4 r = D.rec[v >> 6];
-        const uint64_t below = bit - 1ull;
-        double xt = 0.0;
-        if (side == 1) xt = val[e];
-        else if (tbits & bit) xt = val[segoff[g ^ 1] + r.w + __popcll(tbits & below)];   // v's t* entry
-        const double xs = side == 0 ? val[e] : 0.0;
-        const double y = xs / (double)D.ds - xt / (double)D.dt;
         const uint64_t ubits = ((uint64_t)r.y << 32) | r.x;
-        D.vals[r.z + __popcll(ubits & below)] = y;
+        double *slot = D.vals + r.z + __popcll(ubits & (bit - 1ull));
+        if (side == 1) {
+            *slot = -(val[e] / (double)D.dt);
+        } else {
+            const uint64_t tbits = reinterpret_cast<const unsigned long long *>(D.aux + (v >> 6))[1];
+            const double a = val[e] / (double)D.ds;
+            *slot = (tbits & bit) ? a + *slot : a - 0.0;
+        }
         return;
     }
-    // hash tables: small ones are built by k_yhash (one CTA per query, shared memory); the large
-    // ones here, by global CAS, with the same two passes
-    if ((YB << D.lgb) <= YH_SMEM_SLOTS_DEV) return;
-    if (side != (pass == 0 ? 1 : 0)) return;
     bool found;
     const int64_t slot = yh_insert<false>(D.keys, D.lgb, v, &found);
     if (side == 1) {
@@ -348,7 +364,7 @@ int ytable_plan(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, con
     ENSURE(ws.ycap, sizeof(YSizes) * (na + 1), false);
     ENSURE(ws.yoff, sizeof(YSizes) * (na + 1), false);
     YSizes *sz = ws.ycap.as<YSizes>(), *incl = ws.yoff.as<YSizes>();
-    const int64_t nrec = (c.g->n + 63) / 64;
+    const int64_t nrec = ((c.g->d_cblk ? c.g->dord_nv : c.g->n) + 63) / 64;   // over the walk kernel's ids
     k_ycap<<<blocks_for(na, 256), 256, 0, c.st>>>(na, act, ws.qs.as<QState>(), cont, segoff, nrec, c.g->ytable_force,
                                                   c.g->rank_min_cap, c.g->rank_ratio, c.g->rank_max_bytes, sz);
     LAUNCHED(c.g);
@@ -365,6 +381,7 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
 {
     Workspace &ws = c.ws;
     const YSizes *sz = ws.ycap.as<YSizes>(), *incl = ws.yoff.as<YSizes>();
+    const int32_t *perm = c.g->d_cblk ? c.g->d_perm : nullptr;   // keys in the walk kernel's ids
     if (V == 0) return ER_OK;
     if (c.g->profiling) {
         c.g->prof.ytable_slots += H;
@@ -394,18 +411,26 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
     k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, sz, incl, keys, vals, recs, aux,
                                                       ws.qs.as<QState>(), yd);
     LAUNCHED(c.g);
+    if (perm != nullptr) {   // key by walk ids: map once, then build as without renumbering
+        ENSURE(ws.ywid, sizeof(int32_t) * std::max<int64_t>(Fmax, 1), false);
+        int32_t *wid = ws.ywid.as<int32_t>();
+        k_ywid<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, perm, yd, wid);
+        LAUNCHED(c.g);
+        id = wid;
+        perm = nullptr;
+    }
     if (H > 0) {
-        k_yhash<<<na, YH_THREADS, 0, c.st>>>(na, segoff, id, val, yd);
+        k_yhash<<<na, YH_THREADS, 0, c.st>>>(na, segoff, id, perm, val, yd);
         LAUNCHED(c.g);
     }
     if (R > 0) {
-        k_ybits<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, yd);
+        k_ybits<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, perm, yd);
         LAUNCHED(c.g);
         k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, sz, yd);
         LAUNCHED(c.g);
     }
-    for (int pass = H > 0 ? 0 : 1; pass < 2; pass++) {   // rank tables (values) and large hash tables
-        k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, val, segoff, yd, pass);
+    for (int pass = 0; pass < 2; pass++) {   // rank tables and large hash tables: t* entries, then s*
+        k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, perm, val, yd, pass);
         LAUNCHED(c.g);
     }
     return ER_OK;

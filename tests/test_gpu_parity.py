@@ -293,8 +293,10 @@ def test_unsorted_rows_parity(geer, tiny):
 
 @pytest.mark.parametrize("graph", ["tiny", "rmat20"])
 def test_walk_layouts_byte_identical(geer, tiny, rmat20, graph):
-    # node records + columns (32-bit or 24-bit, 5 per 16-byte chunk), 16-byte arc records and packed
-    # 8-byte arc records are four encodings of the same CSR: every output bit must agree
+    # node records + columns (32-bit or 24-bit, 5 per 16-byte chunk), 16-byte arc records, packed
+    # 8-byte arc records and the degree-ordered renumbering (24-bit columns + a class tree, y-tables
+    # keyed by the new ids) are five encodings of the same CSR: every output bit must agree
+    #
     import os
     if graph == "tiny":
         g, pairs = tiny
@@ -303,17 +305,19 @@ def test_walk_layouts_byte_identical(geer, tiny, rmat20, graph):
         g, pairs, _, _ = rmat20
         pairs = pairs[::20]
     outs = {}
-    for lay in ("cols", "cols24", "arcs", "packed"):
+    code = {"cols": 0, "arcs": 1, "packed": 2, "cols24": 3, "dord": 4}
+    for lay in ("cols", "cols24", "arcs", "packed", "dord"):
         os.environ["GEER_WALK_LAYOUT"] = lay
         try:
             h = geer.er_graph_create(g.n, g.offsets, g.cols)
         finally:
             del os.environ["GEER_WALK_LAYOUT"]
+        assert geer.er_graph_profile_read(h)["walk_layout"] == code[lay]
         geer.er_graph_set_lambda(h, g.lam)
         r, st = geer.er_query_batch_ex(h, pairs, 0.1, stats=True)
         outs[lay] = (r.tobytes(), st.tobytes())
         geer.er_graph_destroy(h)
-    assert outs["cols"] == outs["cols24"] == outs["arcs"] == outs["packed"]
+    assert outs["cols"] == outs["cols24"] == outs["arcs"] == outs["packed"] == outs["dord"]
 
 
 def _hub_graph(n=3000, seed=5):
@@ -461,7 +465,9 @@ def test_ytable_layouts_and_kernel_variants_byte_identical(graph, tiny, rmat20):
                 {"GEER_WALK_SMEM_KB": "8"}, {"GEER_WALK_SMEM_KB": "24", "GEER_YTABLE": "hash"},
                 {"GEER_WALK_TILES": "1"}, {"GEER_WALK_LAYOUT": "arcs"}, {"GEER_WALK_LAYOUT": "cols"},
                 {"GEER_WALK_NP": "2"}, {"GEER_WALK_NP": "2", "GEER_WALK_MINB": "3"}, {"GEER_WALK_PERSIST": "0"},
-                {"GEER_AMC_OVERLAP": "1"}):
+                {"GEER_AMC_OVERLAP": "1"}, {"GEER_WALK_LAYOUT": "dord"},
+                {"GEER_WALK_LAYOUT": "dord", "GEER_YTABLE": "rank"}, {"GEER_WALK_LAYOUT": "dord", "GEER_YTABLE": "hash"},
+                {"GEER_WALK_LAYOUT": "dord", "GEER_RANK_MAX_KB": "0"}, {"GEER_WALK_LAYOUT": "dord", "GEER_WALK_SMEM_KB": "8"}):
         e = dict(os.environ, **env)
         outs[str(env)] = subprocess.run([sys.executable, "-c", code, repr(g.lam)], env=e, check=True,
                                         capture_output=True, cwd=str(W.Path(__file__).resolve().parents[1])).stdout
