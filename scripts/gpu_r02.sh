@@ -33,9 +33,9 @@ if [ "$PART" = profile ] || [ "$PART" = all ]; then
 fi
 ls -la gpurun_out | tail -30
 if [ "$PART" = extra ]; then
-  # config 1 walk-load variants on the packed layout; two real ranks on one GPU over gloo (plumbing);
-  # the Friendster-shaped shard (configs[4], one GPU's 125k of 1M)
-  bash scripts/exp_env.sh rmat20 gpurun_out/exp_rmat20_arc.jsonl "GEER_ARC_POLICY=0" "GEER_ARC_POLICY=3" "GEER_ARC_POLICY=4" > gpurun_out/exp_rmat20_arc.log 2>&1
+  # the Orkut-shaped config; two real ranks on one GPU over gloo (plumbing); the Friendster-shaped
+  # shard (configs[4], one GPU's 125k of 1M)
+  timeout 900 python bench.py --config orkut_full --steps 3 --warmup 3 --no-cpu-baseline --no-spmm > gpurun_out/bench_orkut.log 2>&1
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 \
       bench.py --gpus 2 --dist-backend gloo --config rmat20 --steps 3 --warmup 3 --no-cpu-baseline --no-spmm \
       --no-accuracy > gpurun_out/bench_2rank_gloo.log 2>&1
