@@ -354,6 +354,7 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
             if (!strcmp(env, "dord") && n <= (1 << 24)) layout = 4;
             if (!strcmp(env, "packed") && packable) layout = 2;
         }
+        if (const char *env = getenv("GEER_DORD_SMEM_KB")) g->dord_smem_bytes = 1024 * std::min(96, std::max(0, atoi(env)));
         if (layout == 4 && e == cudaSuccess) {
             const int rc = geer::build_dord(g, offsets, cols);
             if (rc < 0) e = cudaErrorMemoryAllocation;

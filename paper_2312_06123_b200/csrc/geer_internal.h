@@ -54,7 +54,7 @@ struct DOrdView {
     const uint2 *cd = nullptr;       // [ncls]
     int32_t nblk = 0, ncls = 0, bshift = 0;
 };
-constexpr int DORD_SMEM_BYTES = 24 * 1024;   // shared memory per K6 CTA for blk + cd
+constexpr int DORD_SMEM_BYTES = 24 * 1024;   // default shared memory per K6 CTA for blk + cd
 
 struct PackSpec {
     int bo = 0, bd = 0;  // bit widths of offset and degree (u takes the high bits)
@@ -160,6 +160,7 @@ struct er_graph {
     int32_t dord_nblk = 0, dord_ncls = 0, dord_bshift = 0;
     float walk_l2_keep = 0.f;   // K6 column loads: fraction of lines L2 evict-last (rest evict-first)
     int64_t dord_nv = 0;   // new id space (n plus class padding)
+    int32_t dord_smem_bytes = geer::DORD_SMEM_BYTES;   // budget for blk + cd (GEER_DORD_SMEM_KB)
     geer::PackSpec pack;
     int32_t max_deg = 0;
     bool rows_sorted = false;

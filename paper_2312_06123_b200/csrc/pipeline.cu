@@ -1021,7 +1021,7 @@ int build_dord(er_graph *g, const int64_t *off, const int32_t *cols)
     for (int b = 4; b <= 16 && bs < 0; b++) {
         int64_t v = 0;
         for (int64_t c = 0; c < K; c++) v += ((cnt[cdeg[c]] + (1ll << b) - 1) >> b) << b;
-        if (v <= (1ll << 24) && 2 * (v >> b) + 8 * K <= DORD_SMEM_BYTES) { bs = b; nv = v; }
+        if (v <= (1ll << 24) && 2 * (v >> b) + 8 * K <= g->dord_smem_bytes) { bs = b; nv = v; }
     }
     if (bs < 0) return 1;
     const int64_t nblk = nv >> bs;

@@ -320,6 +320,30 @@ def test_walk_layouts_byte_identical(geer, tiny, rmat20, graph):
     assert outs["cols"] == outs["cols24"] == outs["arcs"] == outs["packed"] == outs["dord"]
 
 
+def test_degree_ordered_layout_budget(geer, rmat20):
+    # layout 4's class tables must fit the shared-memory budget: a smaller budget takes a larger
+    # block (more padding ids, a different renumbering), a budget nothing fits falls back to the
+    # 24-bit columns; every output bit stays the same
+    import os
+    g, pairs, _, _ = rmat20
+    pairs = pairs[::10]
+    outs = {}
+    for kb, want in (("24", 4), ("8", 4), ("0", 3)):
+        os.environ.update({"GEER_WALK_LAYOUT": "dord", "GEER_DORD_SMEM_KB": kb})
+        try:
+            h = geer.er_graph_create(g.n, g.offsets, g.cols)
+        finally:
+            del os.environ["GEER_WALK_LAYOUT"], os.environ["GEER_DORD_SMEM_KB"]
+        prof = geer.er_graph_profile_read(h)
+        assert prof["walk_layout"] == want, (kb, prof["walk_layout"])
+        geer.er_graph_set_lambda(h, g.lam)
+        r, st = geer.er_query_batch_ex(h, pairs, 0.1, stats=True)
+        outs[kb] = (r.tobytes(), st.tobytes(), prof["walk_graph_bytes"])
+        geer.er_graph_destroy(h)
+    assert outs["24"][:2] == outs["8"][:2] == outs["0"][:2]
+    assert outs["8"][2] >= outs["24"][2]   # more padding ids, larger perm tables
+
+
 def _hub_graph(n=3000, seed=5):
     """Hubs of degree n-1 and 1500 (K9 rows cut into SPMM_SEG = 512 segments) over a sparse
     random graph, plus rows of degree exactly 512 and 513 (the segment boundary)."""
