@@ -31,8 +31,8 @@ struct QState {
     int32_t ymode;         // y-table layout: 0 hash (ykeys, ylog2), 1 rank bitmap (yrec)
     int32_t pad2;
     const int32_t *ykeys;  // hash keys (YT_HASH)
-    const uint4 *yrec;     // rank records {U bits lo, U bits hi, rank U, rank t*-side} per 64 node ids (YT_RANK)
-    const uint4 *yaux;     // build-time {s*-side bits, t*-side bits} per 64 node ids (YT_RANK)
+    const uint4 *yrec;     // rank records {U bits 0-31, 32-63, 64-95, rank U} per 96 node ids (YT_RANK)
+    const uint4 *yaux;     // build-time {s*-side bits, 0}, {t*-side bits, 0} per 96 node ids (YT_RANK)
     const double *yvals;   // values (by slot, or by rank)
     double z;              // last batch mean Z (= r_f)
     double s1acc, s2acc;   // running sums of Z_k, Z_k^2 (reuse variant)
@@ -174,7 +174,7 @@ struct er_graph {
     int walk_occ = 0;    // K6 resident CTAs per SM at the last launch (occupancy API)
     bool walk_persist = true;   // K6 persistent grid + atomic tile counter (GEER_WALK_PERSIST=1) or one tile per CTA
     int64_t rank_min_cap = 4096;  // K5: rank bitmap only for tables above this many hash slots (GEER_RANK_MIN_CAP)
-    int64_t rank_ratio = 24;      // ... and when 16 B x records < rank_ratio x slots (GEER_RANK_RATIO)
+    int64_t rank_ratio = 12;      // ... and when 16 B x records < rank_ratio x slots (GEER_RANK_RATIO)
     int64_t rank_max_bytes = 960 << 10;  // ... and when the records take at most this, i.e. graphs up to
                                          // ~3.9M nodes (GEER_RANK_MAX_KB; measured on configs 1-4)
     int ytable_force = 0;  // y-table layout: 0 by footprint, 1 hash only, 2 rank bitmap only (GEER_YTABLE)

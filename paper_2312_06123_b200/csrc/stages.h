@@ -36,14 +36,17 @@ constexpr int YT_HASH = 0;
 constexpr int YT_RANK = 1;
 constexpr int WALK_KEY_SLOTS = 4096;        // largest hash table staged in shared memory
 
-// Rank-bitmap lookup: record r = {U bits lo, U bits hi, rank U, rank T} of the 64 node ids
-// around v; position of y(v) in the value array, or -1 when v is not in U.
+// Rank-bitmap records: one 16-byte record {U bits 0-31, 32-63, 64-95; rank U} per RANK_IDS = 96
+// consecutive node ids (three 32-id words and the number of U members before the record).
+constexpr uint32_t RANK_IDS = 96;
+__device__ __forceinline__ uint32_t rank_rec(int32_t v) { return (uint32_t)v / RANK_IDS; }
+// Position of y(v) in the value array, or -1 when v is not in U (r = v's record).
 __device__ __forceinline__ int64_t rank_index(const uint4 r, int32_t v)
 {
-    const unsigned long long bits = ((unsigned long long)r.y << 32) | r.x;
-    const int b = v & 63;
-    if (!((bits >> b) & 1ull)) return -1;
-    return (int64_t)r.z + __popcll(bits & ((1ull << b) - 1ull));
+    const uint32_t b = (uint32_t)v - RANK_IDS * rank_rec(v), wd = b >> 5, m = 1u << (b & 31u);
+    const uint32_t word = wd == 0 ? r.x : wd == 1 ? r.y : r.z;
+    if (!(word & m)) return -1;
+    return (int64_t)r.w + __popc(word & (m - 1u)) + (wd > 0 ? __popc(r.x) : 0) + (wd > 1 ? __popc(r.y) : 0);
 }
 
 // Walk pairs of AMC batch b: the first walk index drawn in batch b -- all eta_b = eta0 2^b fresh

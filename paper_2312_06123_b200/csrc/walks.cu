@@ -342,7 +342,7 @@ __device__ __forceinline__ void walk_chains(const uint2 *__restrict__ rec, const
             else if (ARC == 4) R[c] = class_rec(T, (uint32_t)v[c]);
             else R[c] = ld_rec<ARC != 2>(rec + v[c]);
             if (mode == YM_RANK) {
-                prec[c] = ld_y(yrec + (v[c] >> 6));
+                prec[c] = ld_y(yrec + rank_rec(v[c]));
             } else if (mode == YM_GLOBAL) {
                 const int4 bk = ld_bucket(gkeys, ybucket(v[c], lgb));
                 prec[c] = make_uint4((uint32_t)bk.x, (uint32_t)bk.y, (uint32_t)bk.z, (uint32_t)bk.w);

@@ -22,9 +22,9 @@ __device__ __forceinline__ int32_t walk_id(const int32_t *__restrict__ perm, int
 //    capacity = next power of two >= 2 (|supp s*| + |supp t*|) (load <= 1/2), >= one bucket;
 //    values fp64 by slot.  (Tables of <= WALK_KEY_SLOTS keys can be staged whole in the walk
 //    kernel's shared memory, GEER_WALK_SMEM_KB; off by default.)
-//  * rank bitmap (YT_RANK): one 16-byte record {U bits (64); rank U; rank T} per 64 node ids
-//    (bit v of U; ranks = |U| and |supp t*| below the record), values fp64 by rank: y(v) is at
-//    vals[rank U + popc(U bits below v)].  Exact membership in one 16-byte load, no probing;
+//  * rank bitmap (YT_RANK): one 16-byte record {U bits (96); rank U} per 96 node ids
+//    (stages.h rank_rec / rank_index; rank U = |U| below the record), values fp64 by rank: y(v)
+//    is at vals[rank U + popc(U bits below v)].  Exact membership in one 16-byte load, no probing;
 //    used for tables too large to stage whose records take less than twice the hash layout's
 //    12 B/slot (keys + values).
 // Per leaving query i: h hash slots, v value slots, r rank records (0 for queries that stay).
@@ -68,8 +68,8 @@ __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState
 // indexed by i: K5 reaches it in one load from the entry's segment).
 struct YDesc {
     int32_t *keys;     // YT_HASH: 2^(lgb + YB_LOG) int32 keys
-    uint4 *rec;        // YT_RANK: walk records {U bits, rank U, rank T}
-    uint4 *aux;        // YT_RANK: build-time records {S bits, T bits}
+    uint4 *rec;        // YT_RANK: walk records {U bits 0-95, rank U}
+    uint4 *aux;        // YT_RANK: build-time {s* side bits 0-95, 0}, {t* side bits 0-95, 0} per record
     double *vals;      // y values (by slot or by rank)
     int32_t mode;      // -1: the query does not leave now; YT_HASH / YT_RANK
     int32_t lgb;       // YT_HASH: log2 of the bucket count
@@ -99,7 +99,7 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const YSi
         if (n.r > 0) {
             D.mode = Q.ymode = YT_RANK;
             D.rec = rbase + (c.r - n.r);
-            D.aux = abase + (c.r - n.r);
+            D.aux = abase + 2 * (c.r - n.r);   // two aux records per walk record
             Q.yrec = D.rec;
             Q.yaux = D.aux;
             Q.ykeys = nullptr;
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(YH_THREADS) k_yhash(int32_t na, const int64_t 
 // hash: the slot of v by find-or-insert; rank: the slot at rank U + popc(U bits below v) (k_ybits:
 // every entry's side bit of v into the build-time aux records; k_yrank: union bits and ranks).
 // Rank tables, side bits: one thread per frontier entry; a warp ORs each run of equal (segment,
-// 64-id word) by a segmented shuffle scan and the run's first lane sets the bits with one 64-bit
+// 32-id word) by a segmented shuffle scan and the run's first lane sets the bits with one 32-bit
 // atomicOr (segments are sorted by node id: without renumbering a word's entries are consecutive,
 // one atomic per word and warp).  aux is zeroed before.
 __global__ void k_ybits(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
@@ -235,22 +235,24 @@ __global__ void k_ybits(int64_t Fmax, const int64_t *__restrict__ dF, const int3
 {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    unsigned long long key = ~0ull, bits = 0;
-    unsigned long long *dst = nullptr;
+    unsigned long long key = ~0ull;
+    unsigned int bits = 0;
+    unsigned int *dst = nullptr;
     if (e < Fmax && (dF == nullptr || e < *dF)) {
         const int32_t g = seg[e];
         const YDesc D = yd[g >> 1];
         if (D.mode == YT_RANK) {
             const int32_t v = walk_id(perm, id[e]);
-            key = ((unsigned long long)(uint32_t)g << 32) | (uint32_t)(v >> 6);
-            bits = 1ull << (v & 63);
-            dst = reinterpret_cast<unsigned long long *>(D.aux + (v >> 6)) + (g & 1);
+            // 32-id word v >> 5 = word (v >> 5) mod 3 of record v / 96 (96 = 3 x 32)
+            key = ((unsigned long long)(uint32_t)g << 32) | (uint32_t)(v >> 5);
+            bits = 1u << (v & 31);
+            dst = reinterpret_cast<unsigned int *>(D.aux + 2 * rank_rec(v) + (g & 1)) + ((uint32_t)(v >> 5) % 3u);
         }
     }
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, d);
-        const unsigned long long ob = __shfl_down_sync(0xffffffffu, bits, d);
+        const unsigned int ob = __shfl_down_sync(0xffffffffu, bits, d);
         if (lane + d < 32 && ok == key) bits |= ob;
     }
     const unsigned long long pk = __shfl_up_sync(0xffffffffu, key, 1);
@@ -284,16 +286,14 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
     if (D.mode == YT_HASH && (YB << D.lgb) <= YH_SMEM_SLOTS_DEV) return;
     const int32_t v = walk_id(perm, id[e]);
     if (D.mode == YT_RANK) {
-        const uint64_t bit = 1ull << (v & 63);
-        const uint4 r = D.rec[v >> 6];
-        const uint64_t ubits = ((uint64_t)r.y << 32) | r.x;
-        double *slot = D.vals + r.z + __popcll(ubits & (bit - 1ull));
+        const uint32_t w = rank_rec(v);
+        double *slot = D.vals + rank_index(D.rec[w], v);   // v is in U: its entry set the bit
         if (side == 1) {
             *slot = -(val[e] / (double)D.dt);
         } else {
-            const uint64_t tbits = reinterpret_cast<const unsigned long long *>(D.aux + (v >> 6))[1];
+            const uint32_t tw = reinterpret_cast<const unsigned int *>(D.aux + 2 * w + 1)[(uint32_t)(v >> 5) % 3u];
             const double a = val[e] / (double)D.ds;
-            *slot = (tbits & bit) ? a + *slot : a - 0.0;
+            *slot = ((tw >> (v & 31)) & 1u) ? a + *slot : a - 0.0;
         }
         return;
     }
@@ -320,34 +320,26 @@ k_yrank(int32_t na, const YSizes *__restrict__ sz, const YDesc *__restrict__ yd)
     const uint4 *aux = yd[i].aux;
     const int64_t R = sz[i].r;
     static_assert(YRANK_THREADS == SCAN_NT, "k_yrank uses the CTA scan of scan.cuh");
-    __shared__ unsigned long long sh[SCAN_NT / 32];
-    unsigned long long carry = 0;   // (rank U << 32) | rank T
+    __shared__ uint32_t sh[SCAN_NT / 32];
+    uint32_t carry = 0;   // rank U
     for (int64_t base = 0; base < R; base += YRANK_THREADS * YRANK_ITEMS) {
         const int64_t w0 = base + (int64_t)threadIdx.x * YRANK_ITEMS;
-        uint4 a[YRANK_ITEMS];
-        unsigned long long c[YRANK_ITEMS];
+        uint4 u[YRANK_ITEMS];
+        uint32_t c[YRANK_ITEMS], sum = 0;
 #pragma unroll
         for (int j = 0; j < YRANK_ITEMS; j++) {
-            a[j] = w0 + j < R ? aux[w0 + j] : make_uint4(0u, 0u, 0u, 0u);
-            c[j] = ((unsigned long long)(__popc(a[j].x | a[j].z) + __popc(a[j].y | a[j].w)) << 32) |
-                   (unsigned long long)(__popc(a[j].z) + __popc(a[j].w));
+            const uint4 a = w0 + j < R ? aux[2 * (w0 + j)] : make_uint4(0u, 0u, 0u, 0u);
+            const uint4 t = w0 + j < R ? aux[2 * (w0 + j) + 1] : make_uint4(0u, 0u, 0u, 0u);
+            u[j] = make_uint4(a.x | t.x, a.y | t.y, a.z | t.z, 0u);
+            c[j] = __popc(u[j].x) + __popc(u[j].y) + __popc(u[j].z);
+            sum += c[j];
         }
-        unsigned long long excl[YRANK_ITEMS], tot, sum = 0;
-#pragma unroll
-        for (int j = 0; j < YRANK_ITEMS; j++) sum += c[j];
-        unsigned long long run;
-        cta_scan(sum, sh, ScanAdd<unsigned long long>(), 0ull, &run, &tot);
+        uint32_t run, tot;
+        cta_scan(sum, sh, ScanAdd<uint32_t>(), 0u, &run, &tot);
 #pragma unroll
         for (int j = 0; j < YRANK_ITEMS; j++) {
-            excl[j] = run;
+            if (w0 + j < R) recs[w0 + j] = make_uint4(u[j].x, u[j].y, u[j].z, carry + run);
             run += c[j];
-        }
-#pragma unroll
-        for (int j = 0; j < YRANK_ITEMS; j++) {
-            if (w0 + j < R) {
-                const unsigned long long rk = carry + excl[j];
-                recs[w0 + j] = make_uint4(a[j].x | a[j].z, a[j].y | a[j].w, (uint32_t)(rk >> 32), (uint32_t)rk);
-            }
         }
         carry += tot;
         __syncthreads();
@@ -364,7 +356,7 @@ int ytable_plan(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, con
     ENSURE(ws.ycap, sizeof(YSizes) * (na + 1), false);
     ENSURE(ws.yoff, sizeof(YSizes) * (na + 1), false);
     YSizes *sz = ws.ycap.as<YSizes>(), *incl = ws.yoff.as<YSizes>();
-    const int64_t nrec = ((c.g->d_cblk ? c.g->dord_nv : c.g->n) + 63) / 64;   // over the walk kernel's ids
+    const int64_t nrec = ((c.g->d_cblk ? c.g->dord_nv : c.g->n) + RANK_IDS - 1) / RANK_IDS;   // over the walk ids
     k_ycap<<<blocks_for(na, 256), 256, 0, c.st>>>(na, act, ws.qs.as<QState>(), cont, segoff, nrec, c.g->ytable_force,
                                                   c.g->rank_min_cap, c.g->rank_ratio, c.g->rank_max_bytes, sz);
     LAUNCHED(c.g);
@@ -391,7 +383,7 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
     DevBuf &yb = ws.ychunk[wave];
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };   // 256-byte aligned regions
     const size_t o_rec = up(sizeof(double) * V), o_aux = o_rec + up(sizeof(uint4) * R);
-    const size_t o_key = o_aux + up(sizeof(uint4) * R);
+    const size_t o_key = o_aux + up(2 * sizeof(uint4) * R);   // aux: two records per walk record
     const size_t ybytes = o_key + up(sizeof(int32_t) * H);
     if (ybytes > yb.cap) {   // the old buffer may still serve an earlier batch's AMC (AMC stream)
         CK(cudaStreamSynchronize(c.g->amc_stream));
@@ -403,7 +395,7 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
     uint4 *aux = reinterpret_cast<uint4 *>(yb.as<char>() + o_aux);      // build-time {S bits, T bits}
     int32_t *keys = reinterpret_cast<int32_t *>(yb.as<char>() + o_key);   // 16-byte buckets: aligned region
     if (H > 0 || R > 0) {   // (small hash tables are rewritten whole by k_yhash)
-        k_yfill<<<blocks_for(std::max(H, R), 256), 256, 0, c.st>>>(H, keys, R, aux);
+        k_yfill<<<blocks_for(std::max(H, 2 * R), 256), 256, 0, c.st>>>(H, keys, 2 * R, aux);
         LAUNCHED(c.g);
     }
     ENSURE(ws.ydesc, sizeof(YDesc) * (na + 1), false);

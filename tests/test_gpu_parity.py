@@ -283,12 +283,19 @@ def test_unsorted_rows_parity(geer, tiny):
         a, b = g0.offsets[v], g0.offsets[v + 1]
         cols[a:b] = rng.permutation(cols[a:b])
     g = W.Graph(g0.n, g0.offsets.copy(), cols, "tiny_shuffled", g0.lam)
-    h = geer.er_graph_create(g.n, g.offsets, g.cols)
-    geer.er_graph_set_lambda(h, g.lam)
-    for eps in (0.1, 0.3):
-        r, st, ro, so = run_both(geer, h, g, pairs, eps)
-        compare(g, pairs, r, st, ro, so, sorted_adj=False)
-    geer.er_graph_destroy(h)
+    import os
+    for layout in ("", "dord"):   # default walk layout, and the degree-ordered one (row order kept)
+        if layout:
+            os.environ["GEER_WALK_LAYOUT"] = layout
+        try:
+            h = geer.er_graph_create(g.n, g.offsets, g.cols)
+        finally:
+            os.environ.pop("GEER_WALK_LAYOUT", None)
+        geer.er_graph_set_lambda(h, g.lam)
+        for eps in (0.1, 0.3):
+            r, st, ro, so = run_both(geer, h, g, pairs, eps)
+            compare(g, pairs, r, st, ro, so, sorted_adj=False)
+        geer.er_graph_destroy(h)
 
 
 @pytest.mark.parametrize("graph", ["tiny", "rmat20"])
