@@ -175,8 +175,8 @@ struct er_graph {
     bool walk_persist = true;   // K6 persistent grid + atomic tile counter (GEER_WALK_PERSIST=1) or one tile per CTA
     int64_t rank_min_cap = 4096;  // K5: rank bitmap only for tables above this many hash slots (GEER_RANK_MIN_CAP)
     int64_t rank_ratio = 12;      // ... and when 16 B x records < rank_ratio x slots (GEER_RANK_RATIO)
-    int64_t rank_max_bytes = 960 << 10;  // ... and when the records take at most this, i.e. graphs up to
-                                         // ~3.9M nodes (GEER_RANK_MAX_KB; measured on configs 1-4)
+    int64_t rank_max_bytes = 960 << 10;  // ... and when the records take at most this, i.e. walk ids up to
+                                         // ~5.9M (96 per record; GEER_RANK_MAX_KB; configs 1-4)
     int ytable_force = 0;  // y-table layout: 0 by footprint, 1 hash only, 2 rank bitmap only (GEER_YTABLE)
     bool l2_persist = false; // K6: persisting-L2 access window over the walk graph (GEER_L2_PERSIST)
     size_t l2_window = 0, l2_persist_bytes = 0;
