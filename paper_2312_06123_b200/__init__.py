@@ -14,12 +14,14 @@ Arrays may be numpy arrays (host) or torch CUDA tensors (device pointers).
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libgeer.so"
+# GEER_LIB: an alternative build of this library (A/B experiments, scripts/build_variant.py)
+LIB_PATH = Path(os.environ["GEER_LIB"]).resolve() if os.environ.get("GEER_LIB") else _PKG / "libgeer.so"
 
 ER_OK, ER_EINVAL, ER_ESELFLOOP, ER_EDUP, ER_EASYM, ER_EDISCONNECTED, ER_EBIPARTITE, ER_ESPECTRAL, \
     ER_ENOMEM, ER_ECUDA = range(10)

@@ -32,7 +32,6 @@ struct QState {
     int32_t pad2;
     const int32_t *ykeys;  // hash keys (YT_HASH)
     const uint4 *yrec;     // rank records {U bits 0-31, 32-63, 64-95, rank U} per 96 node ids (YT_RANK)
-    const uint4 *yaux;     // build-time {s*-side bits, 0}, {t*-side bits, 0} per 96 node ids (YT_RANK)
     const double *yvals;   // values (by slot, or by rank)
     double z;              // last batch mean Z (= r_f)
     double s1acc, s2acc;   // running sums of Z_k, Z_k^2 (reuse variant)

@@ -86,9 +86,26 @@ __global__ void k_bkt_seg(int32_t nseg, const int64_t *__restrict__ segBoff, con
     bseg[b] = lo;
 }
 
+// Largest index lo in [lo, hi) with a[lo] <= x, given a[lo] <= x and (a[hi] > x or hi the end),
+// a monotone: the 32 lanes of the (converged) warp probe 32 evenly spaced points per round, so the
+// range shrinks 32-fold per round (6 rounds for 10^8 entries instead of 27 dependent loads).
+__device__ __forceinline__ int64_t warp_search(const int64_t *__restrict__ a, int64_t lo, int64_t hi, int64_t x)
+{
+    const int lane = threadIdx.x & 31;
+    while (hi - lo > 1) {
+        const int64_t step = (hi - lo + 31) >> 5;   // >= 1
+        const int64_t q = lo + (int64_t)(lane + 1) * step;
+        const bool le = q < hi && a[q] <= x;        // true for a prefix of the lanes
+        const int c = __popc(__ballot_sync(0xffffffffu, le));
+        lo += (int64_t)c * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
+
 // Pair enumeration shared by count and scatter over the chunk's pairs P0 + [0, E) (entries
-// [e_lo, e_hi)): warp = 32 * EMIT_PER consecutive positions, lane 0 binary-searches the entry of
-// the warp's first position, lanes step forward from it.  f(live, local position, entry, j):
+// [e_lo, e_hi)): warp = 32 * EMIT_PER consecutive positions, the warp searches the entry of its
+// first position (warp_search), lanes step forward from it.  f(live, local position, entry, j):
 // the pair is the j-th neighbour of the entry's node.
 template <class Fn>
 __device__ __forceinline__ void for_pairs(int64_t P0, int64_t E, int64_t e_lo, int64_t e_hi,
@@ -97,17 +114,7 @@ __device__ __forceinline__ void for_pairs(int64_t P0, int64_t E, int64_t e_lo, i
     const int lane = threadIdx.x & 31;
     const int64_t base = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * EMIT_PER;
     if (base >= E) return;
-    int64_t e0 = 0;
-    if (lane == 0) {
-        int64_t lo = e_lo, hi = e_hi;   // ent_off[lo] <= P0 + base < ent_off[hi]
-        while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (ent_off[mid] <= P0 + base) lo = mid;
-            else hi = mid;
-        }
-        e0 = lo;
-    }
-    int64_t e = __shfl_sync(0xffffffffu, e0, 0);
+    int64_t e = warp_search(ent_off, e_lo, e_hi, P0 + base);
     int64_t start = ent_off[e], next = ent_off[e + 1];
 #pragma unroll
     for (int i = 0; i < EMIT_PER; i++) {
@@ -283,28 +290,21 @@ __device__ __forceinline__ long long cta_sum_i64(long long v, long long *sh)
     return r;
 }
 
-// 5. reduce: one CTA per bucket (grid >= the bucket count; extra CTAs exit).
-__global__ void __launch_bounds__(BKT_NT) k_bkt_reduce(
-    int32_t g0, const int64_t *__restrict__ dNB, const int32_t *__restrict__ bseg, const int64_t *__restrict__ segBoff,
+// 5. reduce, large buckets (more than BKT_WCAP pairs -- a hub's run, or skew -- or keys wider than
+// 32 bits): one CTA per bucket of the list k_bkt_reduce_warp collected, persistent CTAs.
+__device__ __forceinline__ void reduce_big_bucket(
+    int64_t b, int32_t g0, const int32_t *__restrict__ bseg, const int64_t *__restrict__ segBoff,
     const int32_t *__restrict__ segsh, const int32_t *__restrict__ segeb, const int64_t *__restrict__ boff,
     unsigned long long *__restrict__ keys, unsigned long long *__restrict__ alt, const int64_t *__restrict__ fr_off,
-    const double *__restrict__ fr_val, const int64_t *__restrict__ off, const int32_t *__restrict__ act,
+    const double *__restrict__ fr_val, const uint2 *__restrict__ rec, const int32_t *__restrict__ act,
     const QState *__restrict__ qs, int32_t *__restrict__ out_id, double *__restrict__ out_val,
-    int32_t *__restrict__ gruns, int64_t *__restrict__ ucnt, BStat *__restrict__ bst)
+    int32_t *__restrict__ gruns, int64_t *__restrict__ ucnt, BStat *__restrict__ bst, unsigned long long *smk,
+    SortSmem &S, int *s_runs, unsigned long long *s_red, double *s_at, int *s_flags)
 {
-    extern __shared__ __align__(16) unsigned long long smk[];   // 2 * BKT_CAP keys, BKT_CAP run starts
-    __shared__ SortSmem S;
-    __shared__ int s_runs[BKT_NT];
-    __shared__ unsigned long long s_red[BKT_NW];
-    __shared__ double s_at[2];
-    __shared__ int s_flags;
-    const int64_t b = blockIdx.x;
-    if (b >= *dNB) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t gl = bseg[b], g = g0 + gl;
     const int64_t base = boff[b];
     const int n = (int)(boff[b + 1] - base);
-    if (n <= BKT_WCAP && segsh[bseg[b]] + segeb[bseg[b]] <= 32) return;   // k_bkt_reduce_warp
     const int sh = segsh[gl], eb = segeb[gl];
     const int64_t hi = b - segBoff[gl];
     unsigned long long *a, *bb;
@@ -313,12 +313,12 @@ __global__ void __launch_bounds__(BKT_NT) k_bkt_reduce(
         bb = smk + BKT_CAP;
         for (int i = tid; i < n; i += BKT_NT) a[i] = keys[base + i];
         __syncthreads();
-    } else {   // large bucket (a hub's run, or skew): sorted in place in global memory
+    } else {   // sorted in place in global memory
         a = keys + base;
         bb = alt + base;
     }
     if (tid == 0) {
-        s_flags = 0;
+        *s_flags = 0;
         s_at[0] = s_at[1] = 0.0;
     }
     unsigned long long *srt = cta_radix_sort(a, bb, n, sh + eb, S);
@@ -354,10 +354,10 @@ __global__ void __launch_bounds__(BKT_NT) k_bkt_reduce(
     unsigned long long m1 = 0;
     for (int r = tid; r < U; r += BKT_NT) {
         const int i0 = runs[r], i1 = r + 1 < U ? runs[r + 1] : n;
+        const int32_t u = (int32_t)((hi << sh) | (int64_t)(srt[i0] >> eb));
+        const uint32_t d = __ldg(&rec[u].y);
         double sum = 0.0;
         for (int i = i0; i < i1; i++) sum += gv[i];
-        const int32_t u = (int32_t)((hi << sh) | (int64_t)(srt[i0] >> eb));
-        const int64_t d = off[u + 1] - off[u];
         const double x = sum / (double)d;
         out_id[base + r] = u;
         out_val[base + r] = x;
@@ -366,11 +366,11 @@ __global__ void __launch_bounds__(BKT_NT) k_bkt_reduce(
         m1 = xb > m1 ? xb : m1;
         if (u == Q.s) {   // single writers: u occurs once in the bucket
             s_at[0] = x;
-            atomicOr(&s_flags, 1);
+            atomicOr(s_flags, 1);
         }
         if (u == Q.t) {
             s_at[1] = x;
-            atomicOr(&s_flags, 2);
+            atomicOr(s_flags, 2);
         }
     }
     __syncthreads();
@@ -387,8 +387,29 @@ __global__ void __launch_bounds__(BKT_NT) k_bkt_reduce(
     const unsigned long long M2 = cta_max_u64(m2, s_red);
     if (tid == 0) {
         ucnt[b] = U;
-        bst[b] = BStat{V, M1, M2, C1, s_at[0], s_at[1], s_flags};
+        bst[b] = BStat{V, M1, M2, C1, s_at[0], s_at[1], *s_flags};
     }
+    __syncthreads();   // the shared buffers serve the CTA's next bucket
+}
+
+__global__ void __launch_bounds__(BKT_NT) k_bkt_reduce(
+    int32_t g0, const int64_t *__restrict__ nbig, const int64_t *__restrict__ big, const int32_t *__restrict__ bseg,
+    const int64_t *__restrict__ segBoff, const int32_t *__restrict__ segsh, const int32_t *__restrict__ segeb,
+    const int64_t *__restrict__ boff, unsigned long long *__restrict__ keys, unsigned long long *__restrict__ alt,
+    const int64_t *__restrict__ fr_off, const double *__restrict__ fr_val, const uint2 *__restrict__ rec,
+    const int32_t *__restrict__ act, const QState *__restrict__ qs, int32_t *__restrict__ out_id,
+    double *__restrict__ out_val, int32_t *__restrict__ gruns, int64_t *__restrict__ ucnt, BStat *__restrict__ bst)
+{
+    extern __shared__ __align__(16) unsigned long long smk[];   // 2 * BKT_CAP keys, BKT_CAP run starts
+    __shared__ SortSmem S;
+    __shared__ int s_runs[BKT_NT];
+    __shared__ unsigned long long s_red[BKT_NW];
+    __shared__ double s_at[2];
+    __shared__ int s_flags;
+    const int64_t NBig = *nbig;
+    for (int64_t li = blockIdx.x; li < NBig; li += gridDim.x)
+        reduce_big_bucket(big[li], g0, bseg, segBoff, segsh, segeb, boff, keys, alt, fr_off, fr_val, rec, act, qs,
+                          out_id, out_val, gruns, ucnt, bst, smk, S, s_runs, s_red, s_at, &s_flags);
 }
 
 // 5a. reduce, small buckets (n <= BKT_WCAP): one WARP per bucket, warp-synchronous (no CTA
@@ -458,8 +479,9 @@ __global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
     int32_t g0, const int64_t *__restrict__ dNB, const int32_t *__restrict__ bseg, const int64_t *__restrict__ segBoff,
     const int32_t *__restrict__ segsh, const int32_t *__restrict__ segeb, const int64_t *__restrict__ boff,
     const unsigned long long *__restrict__ keys, const int64_t *__restrict__ fr_off, const double *__restrict__ fr_val,
-    const int64_t *__restrict__ off, const int32_t *__restrict__ act, const QState *__restrict__ qs,
-    int32_t *__restrict__ out_id, double *__restrict__ out_val, int64_t *__restrict__ ucnt, BStat *__restrict__ bst)
+    const uint2 *__restrict__ rec, const int32_t *__restrict__ act, const QState *__restrict__ qs,
+    int32_t *__restrict__ out_id, double *__restrict__ out_val, int64_t *__restrict__ ucnt, BStat *__restrict__ bst,
+    unsigned long long *__restrict__ nbig, int64_t *__restrict__ big)
 {
     __shared__ WarpSmem W[BKT_WPB];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -471,7 +493,10 @@ __global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
         const int n = (int)(boff[b + 1] - base);
         const int32_t gl = bseg[b], g = g0 + gl;
         const int sh = segsh[gl], eb = segeb[gl];
-        if (n > BKT_WCAP || sh + eb > 32) continue;   // k_bkt_reduce
+        if (n > BKT_WCAP || sh + eb > 32) {   // listed for k_bkt_reduce
+            if (lane == 0) big[atomicAdd(nbig, 1ull)] = b;
+            continue;
+        }
         if (n == 0) {
             if (lane == 0) {
                 ucnt[b] = 0;
@@ -496,8 +521,8 @@ __global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
         }
         __syncwarp();
         const QState &Q = qs[act[g >> 1]];
-        long long vol = 0;
-        unsigned long long m1 = 0;
+        long long vol = 0, c1 = 0;
+        unsigned long long m1 = 0, m2 = 0;   // top-2 with multiplicity, streamed per lane
         double at_s = 0.0, at_t = 0.0;
         int flags = 0;
         for (int r = lane; r < U; r += 32) {
@@ -505,35 +530,40 @@ __global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
             double sum = 0.0;
             for (int i = i0; i < i1; i++) sum += fv[srt[i] & emask];   // ascending source order (R13)
             const int32_t u = (int32_t)((hi << sh) | (int64_t)(eb >= 32 ? 0u : srt[i0] >> eb));
-            const int64_t d = off[u + 1] - off[u];
+            const uint32_t d = __ldg(&rec[u].y);
             const double x = sum / (double)d;
             out_id[base + r] = u;
             out_val[base + r] = x;
             vol += d;
             const unsigned long long xb = (unsigned long long)__double_as_longlong(x);
-            m1 = xb > m1 ? xb : m1;
+            if (xb > m1) {
+                m2 = m1;
+                m1 = xb;
+                c1 = 1;
+            } else if (xb == m1) {
+                c1++;
+            } else if (xb > m2) {
+                m2 = xb;
+            }
             if (u == Q.s) { at_s = x; flags |= 1; }
             if (u == Q.t) { at_t = x; flags |= 2; }
         }
+        // exact merges (integer sums, maxima on the bits of x >= 0): the tree order does not matter
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             vol += __shfl_xor_sync(full, vol, o);
-            const unsigned long long t = __shfl_xor_sync(full, m1, o);
-            m1 = t > m1 ? t : m1;
-        }
-        long long c1 = 0;
-        unsigned long long m2 = 0;
-        __syncwarp();
-        for (int r = lane; r < U; r += 32) {
-            const unsigned long long xb = (unsigned long long)__double_as_longlong(out_val[base + r]);
-            if (xb == m1) c1++;
-            else if (xb > m2) m2 = xb;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            c1 += __shfl_xor_sync(full, c1, o);
-            const unsigned long long t = __shfl_xor_sync(full, m2, o);
-            m2 = t > m2 ? t : m2;
+            const unsigned long long om1 = __shfl_xor_sync(full, m1, o), om2 = __shfl_xor_sync(full, m2, o);
+            const long long oc1 = __shfl_xor_sync(full, c1, o);
+            if (om1 > m1) {
+                m2 = m1 > om2 ? m1 : om2;   // max(m2, m1, om2) = max(m1, om2): m1 > m2
+                m1 = om1;
+                c1 = oc1;
+            } else if (om1 == m1) {
+                c1 += oc1;
+                m2 = m2 > om2 ? m2 : om2;
+            } else {
+                m2 = m2 > om1 ? m2 : om1;
+            }
         }
         // x(s), x(t): single writers -> the lane that has them
         const unsigned bs = __ballot_sync(full, flags & 1), bt = __ballot_sync(full, flags & 2);
@@ -664,6 +694,8 @@ struct PushView {
     BStat *bst;
     int32_t *bseg;
     unsigned int *cur;
+    unsigned long long *nbig;   // count of the buckets listed for k_bkt_reduce
+    int64_t *big;               // their indices
 };
 PushView push_view(Workspace &ws, int32_t nseg, int64_t NBmax)
 {
@@ -679,6 +711,8 @@ PushView push_view(Workspace &ws, int32_t nseg, int64_t NBmax)
     v.bst = reinterpret_cast<BStat *>(v.uoff + (NBmax + 2));
     v.bseg = reinterpret_cast<int32_t *>(v.bst + (NBmax + 1));
     v.cur = reinterpret_cast<unsigned int *>(v.bseg + (NBmax + 1));
+    v.nbig = reinterpret_cast<unsigned long long *>(v.cur + ((NBmax + 2) & ~(int64_t)1));   // 8-byte aligned
+    v.big = reinterpret_cast<int64_t *>(v.nbig + 1);
     return v;
 }
 }  // namespace
@@ -695,7 +729,7 @@ int smm_push_wave_a(Ctx &c, int32_t g0, int32_t ns, int64_t P0, int64_t E, const
     ws.pk_nbmax = NBmax;
     ws.pk_e = E;
     ENSURE(ws.pk_seg, (sizeof(int64_t) * 2 + sizeof(int32_t) * 2) * (size_t)(ns + 2), false);
-    ENSURE(ws.pk_bkt, (sizeof(int64_t) * 4 + sizeof(BStat) + sizeof(int32_t) * 2) * (size_t)(NBmax + 2), false);
+    ENSURE(ws.pk_bkt, (sizeof(int64_t) * 5 + sizeof(BStat) + sizeof(int32_t) * 2) * (size_t)(NBmax + 2) + 16, false);
     const PushView v = push_view(ws, ns, NBmax);
     int64_t *segB = v.segB, *segBoff = v.segBoff, *cnt = v.cnt, *boff = v.boff, *ucnt = v.ucnt, *uoff = v.uoff;
     int32_t *segsh = v.segsh, *segeb = v.segeb, *bseg = v.bseg;
@@ -710,6 +744,7 @@ int smm_push_wave_a(Ctx &c, int32_t g0, int32_t ns, int64_t P0, int64_t E, const
     CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (NBmax + 1), st));
     CK(cudaMemsetAsync(cur, 0, sizeof(unsigned int) * (NBmax + 1), st));
     CK(cudaMemsetAsync(ucnt, 0, sizeof(int64_t) * (NBmax + 1), st));
+    CK(cudaMemsetAsync(v.nbig, 0, sizeof(unsigned long long), st));
     k_bkt_seg<<<blocks_for(NBmax, 256), 256, 0, st>>>(ns, segBoff, dNB, bseg);
     LAUNCHED(g);
     // entry range of the chunk (host copies of two frontier offsets are not needed: the kernels
@@ -739,13 +774,14 @@ int smm_push_wave_a(Ctx &c, int32_t g0, int32_t ns, int64_t P0, int64_t E, const
     }
     k_bkt_reduce_warp<<<(unsigned)std::min<int64_t>((NBmax + BKT_WPB - 1) / BKT_WPB, (int64_t)g->num_sms * 16),
                         32 * BKT_WPB, 0, st>>>(g0, dNB, bseg, segBoff, segsh, segeb, boff, keys, fr_off,
-                                               ws.fr_val.as<double>(), g->d_off, ws.act.as<int32_t>(),
-                                               ws.qs.as<QState>(), out_id, out_val, ucnt, bst);
+                                               ws.fr_val.as<double>(), g->d_rec, ws.act.as<int32_t>(),
+                                               ws.qs.as<QState>(), out_id, out_val, ucnt, bst, v.nbig, v.big);
     LAUNCHED(g);
-    k_bkt_reduce<<<(unsigned)NBmax, BKT_NT, smem, st>>>(g0, dNB, bseg, segBoff, segsh, segeb, boff, keys,
-                                                         ws.pk_alt.as<unsigned long long>(), fr_off,
-                                                         ws.fr_val.as<double>(), g->d_off, ws.act.as<int32_t>(),
-                                                         ws.qs.as<QState>(), out_id, out_val, gruns, ucnt, bst);
+    // the listed buckets: persistent CTAs over the list (its length stays on the device)
+    k_bkt_reduce<<<(unsigned)std::min<int64_t>(NBmax, (int64_t)g->num_sms * 4), BKT_NT, smem, st>>>(
+        g0, reinterpret_cast<const int64_t *>(v.nbig), v.big, bseg, segBoff, segsh, segeb, boff, keys,
+        ws.pk_alt.as<unsigned long long>(), fr_off, ws.fr_val.as<double>(), g->d_rec, ws.act.as<int32_t>(),
+        ws.qs.as<QState>(), out_id, out_val, gruns, ucnt, bst);
     LAUNCHED(g);
     rc = scan_offsets(c, ucnt, uoff, NBmax);
     if (rc) return rc;

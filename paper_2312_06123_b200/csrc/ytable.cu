@@ -38,6 +38,9 @@ struct YSizesPlus {
     }
 };
 
+constexpr int YH_SMEM_SLOTS = 8192;   // larger hash tables: global CAS (k_yinsert)
+#define YH_SMEM_SLOTS_DEV 8192
+
 __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState *__restrict__ qs,
                        const int32_t *__restrict__ cont, const int64_t *__restrict__ segoff, int64_t nrec,
                        int force, int64_t min_cap, int64_t ratio, int64_t max_bytes, YSizes *__restrict__ sz)
@@ -69,7 +72,6 @@ __global__ void k_ycap(int32_t na, const int32_t *__restrict__ act, const QState
 struct YDesc {
     int32_t *keys;     // YT_HASH: 2^(lgb + YB_LOG) int32 keys
     uint4 *rec;        // YT_RANK: walk records {U bits 0-95, rank U}
-    uint4 *aux;        // YT_RANK: build-time {s* side bits 0-95, 0}, {t* side bits 0-95, 0} per record
     double *vals;      // y values (by slot or by rank)
     int32_t mode;      // -1: the query does not leave now; YT_HASH / YT_RANK
     int32_t lgb;       // YT_HASH: log2 of the bucket count
@@ -78,7 +80,7 @@ struct YDesc {
 
 __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const YSizes *__restrict__ sz,
                           const YSizes *__restrict__ incl, int32_t *kbase, double *vbase, uint4 *rbase,
-                          uint4 *abase, QState *__restrict__ qs, YDesc *__restrict__ yd)
+                          QState *__restrict__ qs, YDesc *__restrict__ yd)
 {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
@@ -86,7 +88,7 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const YSi
     YDesc D;
     D.mode = -1;
     D.keys = nullptr;
-    D.rec = D.aux = nullptr;
+    D.rec = nullptr;
     D.vals = nullptr;
     D.lgb = 0;
     D.ds = D.dt = 1;
@@ -99,9 +101,7 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const YSi
         if (n.r > 0) {
             D.mode = Q.ymode = YT_RANK;
             D.rec = rbase + (c.r - n.r);
-            D.aux = abase + 2 * (c.r - n.r);   // two aux records per walk record
             Q.yrec = D.rec;
-            Q.yaux = D.aux;
             Q.ykeys = nullptr;
             Q.ylog2 = 0;
         } else {
@@ -119,12 +119,15 @@ __global__ void k_yassign(int32_t na, const int32_t *__restrict__ act, const YSi
     yd[i] = D;
 }
 
-__global__ void k_yfill(int64_t H, int32_t *__restrict__ keys, int64_t R, uint4 *__restrict__ aux)
+__global__ void k_yfill(int64_t H, int32_t *__restrict__ keys, int64_t R, uint4 *__restrict__ rec)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j < H) keys[j] = -1;
-    if (j < R) aux[j] = make_uint4(0u, 0u, 0u, 0u);   // the records themselves are written by k_yrank
+    if (j < R) rec[j] = make_uint4(0u, 0u, 0u, 0u);   // bits by k_ybits, ranks by k_yrank
 }
+
+// Rank tables: a value slot not yet written by a t* entry holds this NaN (no y value is a NaN).
+constexpr unsigned long long Y_UNSET = 0x7FF4000000005E47ull;
 
 __device__ __forceinline__ int32_t cas_global(int32_t *p, int32_t cmp, int32_t val)
 {
@@ -138,8 +141,6 @@ __device__ __forceinline__ int32_t cas_global(int32_t *p, int32_t cmp, int32_t v
 // same two passes as the rank path's owner rule: t* entries insert v with -(t*(v)/d_t), then s*
 // entries find-or-insert v and complete y = s*(v)/d_s + stored (IEEE a - b is a + (-b)), or
 // s*(v)/d_s - 0.0 when v is not in supp t*.  Every y(v) is written exactly once.
-constexpr int YH_SMEM_SLOTS = 8192;
-#define YH_SMEM_SLOTS_DEV 8192
 constexpr int YH_THREADS = 256;
 template <bool SMEM>
 __device__ __forceinline__ int32_t yh_cas(int32_t *p, int32_t cmp, int32_t val)
@@ -191,6 +192,22 @@ __device__ __forceinline__ void yh_build(int32_t *keys, const YDesc &D, const in
         D.vals[slot] = found ? a + D.vals[slot] : a - 0.0;
     }
 }
+// One query's hash table built in the shared-memory array sk (cap slots), then copied out.
+__device__ __forceinline__ void yh_build_smem(int32_t *sk, int32_t i, const int64_t *__restrict__ segoff,
+                                              const int32_t *__restrict__ id, const int32_t *__restrict__ perm,
+                                              const double *__restrict__ val, const YDesc &D)
+{
+    const int64_t s0 = segoff[2 * i], s1 = segoff[2 * i + 1], t1 = segoff[2 * i + 2];
+    const int cap = YB << D.lgb;
+    for (int j = threadIdx.x; j < cap; j += YH_THREADS) sk[j] = -1;
+    __syncthreads();
+    yh_build<true>(sk, D, id, perm, val, s0, s1, t1);
+    __syncthreads();
+    int4 *dst = reinterpret_cast<int4 *>(D.keys);
+    const int4 *src = reinterpret_cast<const int4 *>(sk);
+    for (int j = threadIdx.x; j < cap / 4; j += YH_THREADS) dst[j] = src[j];
+}
+// Tables of <= YH_SMEM_SLOTS slots: one CTA per leaving query (static shared memory).
 __global__ void __launch_bounds__(YH_THREADS) k_yhash(int32_t na, const int64_t *__restrict__ segoff,
                                                       const int32_t *__restrict__ id, const int32_t *__restrict__ perm,
                                                       const double *__restrict__ val, const YDesc *__restrict__ yd)
@@ -199,21 +216,9 @@ __global__ void __launch_bounds__(YH_THREADS) k_yhash(int32_t na, const int64_t 
     const int32_t i = blockIdx.x;
     if (i >= na) return;
     const YDesc D = yd[i];
-    if (D.mode != YT_HASH) return;
-    const int64_t s0 = segoff[2 * i], s1 = segoff[2 * i + 1], t1 = segoff[2 * i + 2];
-    const int cap = YB << D.lgb;
-    if (cap > YH_SMEM_SLOTS) return;   // k_yinsert (global CAS, one thread per entry)
-    {
-        for (int j = threadIdx.x; j < cap; j += YH_THREADS) sk[j] = -1;
-        __syncthreads();
-        yh_build<true>(sk, D, id, perm, val, s0, s1, t1);
-        __syncthreads();
-        int4 *dst = reinterpret_cast<int4 *>(D.keys);
-        const int4 *src = reinterpret_cast<const int4 *>(sk);
-        for (int j = threadIdx.x; j < cap / 4; j += YH_THREADS) dst[j] = src[j];
-    }
+    if (D.mode != YT_HASH || (YB << D.lgb) > YH_SMEM_SLOTS) return;
+    yh_build_smem(sk, i, segoff, id, perm, val, D);
 }
-
 // K5 over the support entries (frontier entry e: node id[e], value val[e], segment seg[e] = 2 i +
 // side) of the leaving queries.  Tables are keyed by the walk kernel's node ids (walk_id: the
 // degree-ordered renumbering of walk layout 4, else the ids themselves).  Every node v of
@@ -224,14 +229,17 @@ __global__ void __launch_bounds__(YH_THREADS) k_yhash(int32_t na, const int64_t 
 //   pass 1: s* entries: y = s*(v)/d(s) + stored (= a - b exactly, IEEE a - b is a + (-b)) if v
 //           has a t* entry, else s*(v)/d(s) - 0.0.
 // hash: the slot of v by find-or-insert; rank: the slot at rank U + popc(U bits below v) (k_ybits:
-// every entry's side bit of v into the build-time aux records; k_yrank: union bits and ranks).
-// Rank tables, side bits: one thread per frontier entry; a warp ORs each run of equal (segment,
-// 32-id word) by a segmented shuffle scan and the run's first lane sets the bits with one 32-bit
+// every entry's bit of v into its query's records; k_yrank: the ranks, and every value slot set to
+// Y_UNSET, so pass 1 tells "v in supp t*" by the slot's content).
+// Rank tables, bits: one thread per frontier entry; a warp ORs each run of equal (query, 32-id
+// word) by a segmented shuffle scan and the run's first lane sets the bits with one 32-bit
 // atomicOr (segments are sorted by node id: without renumbering a word's entries are consecutive,
-// one atomic per word and warp).  aux is zeroed before.
+// one atomic per word and warp).  The records are zeroed before.
+// With wid != nullptr (walk layout 4) the same pass stores every leaving entry's walk id in wid, for
+// the hash builds and the value passes.
 __global__ void k_ybits(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                         const int32_t *__restrict__ id, const int32_t *__restrict__ perm,
-                        const YDesc *__restrict__ yd)
+                        const YDesc *__restrict__ yd, int32_t *__restrict__ wid)
 {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
@@ -241,12 +249,16 @@ __global__ void k_ybits(int64_t Fmax, const int64_t *__restrict__ dF, const int3
     if (e < Fmax && (dF == nullptr || e < *dF)) {
         const int32_t g = seg[e];
         const YDesc D = yd[g >> 1];
+        int32_t v = 0;
+        if (D.mode >= 0) {
+            v = walk_id(perm, id[e]);
+            if (wid != nullptr) wid[e] = v;
+        }
         if (D.mode == YT_RANK) {
-            const int32_t v = walk_id(perm, id[e]);
             // 32-id word v >> 5 = word (v >> 5) mod 3 of record v / 96 (96 = 3 x 32)
-            key = ((unsigned long long)(uint32_t)g << 32) | (uint32_t)(v >> 5);
+            key = ((unsigned long long)(uint32_t)(g >> 1) << 32) | (uint32_t)(v >> 5);   // both sides: U bits
             bits = 1u << (v & 31);
-            dst = reinterpret_cast<unsigned int *>(D.aux + 2 * rank_rec(v) + (g & 1)) + ((uint32_t)(v >> 5) % 3u);
+            dst = reinterpret_cast<unsigned int *>(D.rec + rank_rec(v)) + ((uint32_t)(v >> 5) % 3u);
         }
     }
 #pragma unroll
@@ -257,18 +269,6 @@ __global__ void k_ybits(int64_t Fmax, const int64_t *__restrict__ dF, const int3
     }
     const unsigned long long pk = __shfl_up_sync(0xffffffffu, key, 1);
     if (dst != nullptr && (lane == 0 || pk != key)) atomicOr(dst, bits);
-}
-
-// Layout 4: the walk id (renumbered node id) of every frontier entry of a leaving query, once, so
-// the build passes read ids sequentially instead of each looking up perm.
-__global__ void k_ywid(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
-                       const int32_t *__restrict__ id, const int32_t *__restrict__ perm,
-                       const YDesc *__restrict__ yd, int32_t *__restrict__ wid)
-{
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
-    if (yd[seg[e] >> 1].mode < 0) return;
-    wid[e] = __ldg(perm + id[e]);
 }
 
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
@@ -291,9 +291,8 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
         if (side == 1) {
             *slot = -(val[e] / (double)D.dt);
         } else {
-            const uint32_t tw = reinterpret_cast<const unsigned int *>(D.aux + 2 * w + 1)[(uint32_t)(v >> 5) % 3u];
-            const double a = val[e] / (double)D.ds;
-            *slot = ((tw >> (v & 31)) & 1u) ? a + *slot : a - 0.0;
+            const double a = val[e] / (double)D.ds, y = *slot;   // Y_UNSET: v is not in supp t*
+            *slot = (unsigned long long)__double_as_longlong(y) == Y_UNSET ? a - 0.0 : a + y;
         }
         return;
     }
@@ -307,8 +306,9 @@ __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const in
     }
 }
 
-// Ranks of the rank-bitmap tables: rank(record w) = popcount of all records before w.  One CTA
-// per leaving query (non-rank queries exit); YRANK_ITEMS consecutive records per thread per pass.
+// Ranks of the rank-bitmap tables: rank(record w) = popcount of all records before w, stored in the
+// record's fourth word; and the value slots set to Y_UNSET for the value passes.  One CTA per
+// leaving query (non-rank queries exit); YRANK_ITEMS consecutive records per thread per pass.
 constexpr int YRANK_THREADS = 256;
 constexpr int YRANK_ITEMS = 4;
 __global__ void __launch_bounds__(YRANK_THREADS)
@@ -317,33 +317,31 @@ k_yrank(int32_t na, const YSizes *__restrict__ sz, const YDesc *__restrict__ yd)
     const int32_t i = blockIdx.x;
     if (i >= na || sz[i].r == 0) return;
     uint4 *recs = yd[i].rec;
-    const uint4 *aux = yd[i].aux;
     const int64_t R = sz[i].r;
     static_assert(YRANK_THREADS == SCAN_NT, "k_yrank uses the CTA scan of scan.cuh");
     __shared__ uint32_t sh[SCAN_NT / 32];
     uint32_t carry = 0;   // rank U
     for (int64_t base = 0; base < R; base += YRANK_THREADS * YRANK_ITEMS) {
         const int64_t w0 = base + (int64_t)threadIdx.x * YRANK_ITEMS;
-        uint4 u[YRANK_ITEMS];
         uint32_t c[YRANK_ITEMS], sum = 0;
 #pragma unroll
         for (int j = 0; j < YRANK_ITEMS; j++) {
-            const uint4 a = w0 + j < R ? aux[2 * (w0 + j)] : make_uint4(0u, 0u, 0u, 0u);
-            const uint4 t = w0 + j < R ? aux[2 * (w0 + j) + 1] : make_uint4(0u, 0u, 0u, 0u);
-            u[j] = make_uint4(a.x | t.x, a.y | t.y, a.z | t.z, 0u);
-            c[j] = __popc(u[j].x) + __popc(u[j].y) + __popc(u[j].z);
+            const uint4 u = w0 + j < R ? recs[w0 + j] : make_uint4(0u, 0u, 0u, 0u);
+            c[j] = __popc(u.x) + __popc(u.y) + __popc(u.z);
             sum += c[j];
         }
         uint32_t run, tot;
         cta_scan(sum, sh, ScanAdd<uint32_t>(), 0u, &run, &tot);
 #pragma unroll
         for (int j = 0; j < YRANK_ITEMS; j++) {
-            if (w0 + j < R) recs[w0 + j] = make_uint4(u[j].x, u[j].y, u[j].z, carry + run);
+            if (w0 + j < R) recs[w0 + j].w = carry + run;
             run += c[j];
         }
         carry += tot;
         __syncthreads();
     }
+    unsigned long long *vals = reinterpret_cast<unsigned long long *>(yd[i].vals);
+    for (uint32_t k = threadIdx.x; k < carry; k += YRANK_THREADS) vals[k] = Y_UNSET;
 }
 
 // ---------------------------------------------------------------------------- host side
@@ -382,8 +380,7 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
     if ((int)ws.ychunk.size() <= wave) ws.ychunk.resize(wave + 1);
     DevBuf &yb = ws.ychunk[wave];
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };   // 256-byte aligned regions
-    const size_t o_rec = up(sizeof(double) * V), o_aux = o_rec + up(sizeof(uint4) * R);
-    const size_t o_key = o_aux + up(2 * sizeof(uint4) * R);   // aux: two records per walk record
+    const size_t o_rec = up(sizeof(double) * V), o_key = o_rec + up(sizeof(uint4) * R);
     const size_t ybytes = o_key + up(sizeof(int32_t) * H);
     if (ybytes > yb.cap) {   // the old buffer may still serve an earlier batch's AMC (AMC stream)
         CK(cudaStreamSynchronize(c.g->amc_stream));
@@ -392,22 +389,28 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
     ENSURE(yb, ybytes, false);
     double *vals = yb.as<double>();
     uint4 *recs = reinterpret_cast<uint4 *>(yb.as<char>() + o_rec);
-    uint4 *aux = reinterpret_cast<uint4 *>(yb.as<char>() + o_aux);      // build-time {S bits, T bits}
     int32_t *keys = reinterpret_cast<int32_t *>(yb.as<char>() + o_key);   // 16-byte buckets: aligned region
     if (H > 0 || R > 0) {   // (small hash tables are rewritten whole by k_yhash)
-        k_yfill<<<blocks_for(std::max(H, 2 * R), 256), 256, 0, c.st>>>(H, keys, 2 * R, aux);
+        k_yfill<<<blocks_for(std::max(H, R), 256), 256, 0, c.st>>>(H, keys, R, recs);
         LAUNCHED(c.g);
     }
     ENSURE(ws.ydesc, sizeof(YDesc) * (na + 1), false);
     YDesc *yd = ws.ydesc.as<YDesc>();
-    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, sz, incl, keys, vals, recs, aux,
+    k_yassign<<<blocks_for(na, 128), 128, 0, c.st>>>(na, act, sz, incl, keys, vals, recs,
                                                       ws.qs.as<QState>(), yd);
     LAUNCHED(c.g);
-    if (perm != nullptr) {   // key by walk ids: map once, then build as without renumbering
+    // rank bits; under layout 4 the same pass maps every leaving entry to its walk id once, then the
+    // builds run as without renumbering
+    int32_t *wid = nullptr;
+    if (perm != nullptr) {
         ENSURE(ws.ywid, sizeof(int32_t) * std::max<int64_t>(Fmax, 1), false);
-        int32_t *wid = ws.ywid.as<int32_t>();
-        k_ywid<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, perm, yd, wid);
+        wid = ws.ywid.as<int32_t>();
+    }
+    if (R > 0 || wid != nullptr) {
+        k_ybits<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, perm, yd, wid);
         LAUNCHED(c.g);
+    }
+    if (wid != nullptr) {
         id = wid;
         perm = nullptr;
     }
@@ -416,8 +419,6 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
         LAUNCHED(c.g);
     }
     if (R > 0) {
-        k_ybits<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, perm, yd);
-        LAUNCHED(c.g);
         k_yrank<<<na, YRANK_THREADS, 0, c.st>>>(na, sz, yd);
         LAUNCHED(c.g);
     }
