@@ -236,73 +236,127 @@ __global__ void __launch_bounds__(YH_THREADS) k_yhash(int32_t na, const int64_t 
 // atomicOr (segments are sorted by node id: without renumbering a word's entries are consecutive,
 // one atomic per word and warp).  The records are zeroed before.
 // With wid != nullptr (walk layout 4) the same pass stores every leaving entry's walk id in wid, for
-// the hash builds and the value passes.
+// the hash builds and the value passes.  YB_EPT entries per thread (stride blockDim.x), their
+// loads staged level by level as in k_yinsert.
+#ifndef YB_EPT
+#define YB_EPT 2
+#endif
 __global__ void k_ybits(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                         const int32_t *__restrict__ id, const int32_t *__restrict__ perm,
                         const YDesc *__restrict__ yd, int32_t *__restrict__ wid)
 {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t F = dF != nullptr ? min(Fmax, *dF) : Fmax;
+    const int64_t e0 = (int64_t)blockIdx.x * blockDim.x * YB_EPT + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    unsigned long long key = ~0ull;
-    unsigned int bits = 0;
-    unsigned int *dst = nullptr;
-    if (e < Fmax && (dF == nullptr || e < *dF)) {
-        const int32_t g = seg[e];
-        const YDesc D = yd[g >> 1];
-        int32_t v = 0;
-        if (D.mode >= 0) {
-            v = walk_id(perm, id[e]);
-            if (wid != nullptr) wid[e] = v;
-        }
-        if (D.mode == YT_RANK) {
-            // 32-id word v >> 5 = word (v >> 5) mod 3 of record v / 96 (96 = 3 x 32)
-            key = ((unsigned long long)(uint32_t)(g >> 1) << 32) | (uint32_t)(v >> 5);   // both sides: U bits
-            bits = 1u << (v & 31);
-            dst = reinterpret_cast<unsigned int *>(D.rec + rank_rec(v)) + ((uint32_t)(v >> 5) % 3u);
+    int32_t g[YB_EPT], mode[YB_EPT], v[YB_EPT];
+    uint4 *rec[YB_EPT];
+#pragma unroll
+    for (int k = 0; k < YB_EPT; k++) {
+        const int64_t e = e0 + (int64_t)k * blockDim.x;
+        g[k] = e < F ? seg[e] : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < YB_EPT; k++) {
+        const int64_t e = e0 + (int64_t)k * blockDim.x;
+        mode[k] = g[k] >= 0 ? yd[g[k] >> 1].mode : -1;
+        if (mode[k] >= 0) {
+            v[k] = walk_id(perm, id[e]);
+            rec[k] = yd[g[k] >> 1].rec;
         }
     }
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, d);
-        const unsigned int ob = __shfl_down_sync(0xffffffffu, bits, d);
-        if (lane + d < 32 && ok == key) bits |= ob;
+    for (int k = 0; k < YB_EPT; k++) {
+        const int64_t e = e0 + (int64_t)k * blockDim.x;
+        unsigned long long key = ~0ull;
+        unsigned int bits = 0;
+        unsigned int *dst = nullptr;
+        if (mode[k] >= 0 && wid != nullptr) wid[e] = v[k];
+        if (mode[k] == YT_RANK) {
+            // 32-id word v >> 5 = word (v >> 5) mod 3 of record v / 96 (96 = 3 x 32)
+            key = ((unsigned long long)(uint32_t)(g[k] >> 1) << 32) | (uint32_t)(v[k] >> 5);   // both sides: U bits
+            bits = 1u << (v[k] & 31);
+            dst = reinterpret_cast<unsigned int *>(rec[k] + rank_rec(v[k])) + ((uint32_t)(v[k] >> 5) % 3u);
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, d);
+            const unsigned int ob = __shfl_down_sync(0xffffffffu, bits, d);
+            if (lane + d < 32 && ok == key) bits |= ob;
+        }
+        const unsigned long long pk = __shfl_up_sync(0xffffffffu, key, 1);
+        if (dst != nullptr && (lane == 0 || pk != key)) atomicOr(dst, bits);
     }
-    const unsigned long long pk = __shfl_up_sync(0xffffffffu, key, 1);
-    if (dst != nullptr && (lane == 0 || pk != key)) atomicOr(dst, bits);
 }
 
+// YI_EPT entries per thread (stride blockDim.x), staged so that each level of the dependent loads
+// (segment -> descriptor and walk id -> rank record -> value slot) is in flight for all of them at
+// once; stores come last, after every load (the value slots of one pass are distinct: every y(v)
+// has one writer per pass).
+#ifndef YI_EPT
+#define YI_EPT 2
+#endif
 __global__ void k_yinsert(int64_t Fmax, const int64_t *__restrict__ dF, const int32_t *__restrict__ seg,
                           const int32_t *__restrict__ id, const int32_t *__restrict__ perm,
                           const double *__restrict__ val, const YDesc *__restrict__ yd, int pass)
 {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= Fmax || (dF != nullptr && e >= *dF)) return;
-    const int32_t g = seg[e];
-    const YDesc D = yd[g >> 1];
-    if (D.mode < 0) return;
-    const int side = g & 1;
-    if (side != (pass == 0 ? 1 : 0)) return;
-    // hash tables of <= YH_SMEM_SLOTS slots are built by k_yhash (one CTA per query, shared memory)
-    if (D.mode == YT_HASH && (YB << D.lgb) <= YH_SMEM_SLOTS_DEV) return;
-    const int32_t v = walk_id(perm, id[e]);
-    if (D.mode == YT_RANK) {
-        const uint32_t w = rank_rec(v);
-        double *slot = D.vals + rank_index(D.rec[w], v);   // v is in U: its entry set the bit
-        if (side == 1) {
-            *slot = -(val[e] / (double)D.dt);
-        } else {
-            const double a = val[e] / (double)D.ds, y = *slot;   // Y_UNSET: v is not in supp t*
-            *slot = (unsigned long long)__double_as_longlong(y) == Y_UNSET ? a - 0.0 : a + y;
-        }
-        return;
+    const int64_t F = dF != nullptr ? min(Fmax, *dF) : Fmax;
+    const int64_t e0 = (int64_t)blockIdx.x * blockDim.x * YI_EPT + threadIdx.x;
+    const int want = pass == 0 ? 1 : 0;   // side of this pass: t* entries, then s* entries
+    int32_t q[YI_EPT];   // leaving query index, or -1
+#pragma unroll
+    for (int k = 0; k < YI_EPT; k++) {
+        const int64_t e = e0 + (int64_t)k * blockDim.x;
+        const int32_t g = e < F ? seg[e] : -1;
+        q[k] = g >= 0 && (g & 1) == want ? g >> 1 : -1;
     }
-    bool found;
-    const int64_t slot = yh_insert<false>(D.keys, D.lgb, v, &found);
-    if (side == 1) {
-        D.vals[slot] = -(val[e] / (double)D.dt);
-    } else {
-        const double a = val[e] / (double)D.ds;
-        D.vals[slot] = found ? a + D.vals[slot] : a - 0.0;
+    int32_t mode[YI_EPT], v[YI_EPT];
+    const uint4 *rec[YI_EPT];
+#pragma unroll
+    for (int k = 0; k < YI_EPT; k++) {
+        const int64_t e = e0 + (int64_t)k * blockDim.x;
+        mode[k] = q[k] >= 0 ? yd[q[k]].mode : -1;
+        if (mode[k] == YT_HASH && (YB << yd[q[k]].lgb) <= YH_SMEM_SLOTS_DEV) mode[k] = -1;   // k_yhash
+        if (mode[k] >= 0) {
+            v[k] = walk_id(perm, id[e]);
+            rec[k] = yd[q[k]].rec;
+        }
+    }
+    uint4 r[YI_EPT];
+#pragma unroll
+    for (int k = 0; k < YI_EPT; k++)
+        if (mode[k] == YT_RANK) r[k] = rec[k][rank_rec(v[k])];
+    double *slot[YI_EPT];
+    double y[YI_EPT];
+#pragma unroll
+    for (int k = 0; k < YI_EPT; k++) {
+        if (mode[k] == YT_RANK) {
+            slot[k] = yd[q[k]].vals + rank_index(r[k], v[k]);   // v is in U: its entry set the bit
+            if (want == 0) y[k] = *slot[k];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < YI_EPT; k++) {
+        if (mode[k] < 0) continue;
+        const int64_t e = e0 + (int64_t)k * blockDim.x;
+        const YDesc &D = yd[q[k]];
+        const double x = val[e];
+        if (mode[k] == YT_RANK) {
+            if (want == 1) {
+                *slot[k] = -(x / (double)D.dt);
+            } else {
+                const double a = x / (double)D.ds;   // Y_UNSET: v is not in supp t*
+                *slot[k] = (unsigned long long)__double_as_longlong(y[k]) == Y_UNSET ? a - 0.0 : a + y[k];
+            }
+        } else {   // large hash tables (tables of <= YH_SMEM_SLOTS slots: k_yhash, shared memory)
+            bool found;
+            const int64_t hs = yh_insert<false>(D.keys, D.lgb, v[k], &found);
+            if (want == 1) {
+                D.vals[hs] = -(x / (double)D.dt);
+            } else {
+                const double a = x / (double)D.ds;
+                D.vals[hs] = found ? a + D.vals[hs] : a - 0.0;
+            }
+        }
     }
 }
 
@@ -407,7 +461,7 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
         wid = ws.ywid.as<int32_t>();
     }
     if (R > 0 || wid != nullptr) {
-        k_ybits<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, perm, yd, wid);
+        k_ybits<<<blocks_for((Fmax + YB_EPT - 1) / YB_EPT, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, perm, yd, wid);
         LAUNCHED(c.g);
     }
     if (wid != nullptr) {
@@ -423,7 +477,8 @@ int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, 
         LAUNCHED(c.g);
     }
     for (int pass = 0; pass < 2; pass++) {   // rank tables and large hash tables: t* entries, then s*
-        k_yinsert<<<blocks_for(Fmax, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, perm, val, yd, pass);
+        k_yinsert<<<blocks_for((Fmax + YI_EPT - 1) / YI_EPT, 256), 256, 0, c.st>>>(Fmax, dF, seg, id, perm, val, yd,
+                                                                                     pass);
         LAUNCHED(c.g);
     }
     return ER_OK;
