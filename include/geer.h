@@ -117,6 +117,21 @@ int64_t er_graph_num_arcs(const er_graph *g);        /* offsets[n] = 2m */
 /* Kernels launched by this handle since creation (all of them are this library's). */
 int64_t er_graph_kernel_launches(const er_graph *g);
 
+/*
+ * er_probe_random_loads -- the random-access ceiling of the running device that K6's roofline is
+ * quoted against: 8-byte loads at independent, uniformly random
+ * 32-byte sectors of a freshly allocated buffer of `bytes`, 8 in flight per thread, every SM at
+ * full occupancy; the best of 3 timed launches after one warm-up.  Not on the query path
+ * (diagnostic; synchronous; allocates and frees the buffer).
+ *   bytes          buffer size, >= 1 MiB (L2-resident below ~64 MB, DRAM-resident above)
+ *   flavour        0: ld.global.nc (K6's packed-record load), 1: ld.global.nc.L2::64B (K6's
+ *                  column load on DRAM-resident walk graphs: 64-byte L2 fills)
+ *   iters          8-load rounds per thread (the launch length)
+ *   g_loads_per_s  out: 10^9 loads per second
+ * Errors: ER_EINVAL (arguments), ER_ECUDA (allocation or launch).
+ */
+int er_probe_random_loads(int64_t bytes, int32_t flavour, int32_t iters, double *g_loads_per_s);
+
 typedef struct er_opts {
     int32_t tau;               /* batches of AMC, 1..8 (default 5) */
     int32_t force_ell_b;       /* -1: Eq. 15 decides ell_b (default); >= 0: exactly min(force, ell)

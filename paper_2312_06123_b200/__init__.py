@@ -44,7 +44,7 @@ EXPORTED = ["er_graph_create", "er_graph_create_ex", "er_graph_destroy", "er_que
             "er_last_error_message", "er_graph_lambda", "er_graph_set_lambda",
             "er_graph_estimate_lambda", "er_graph_num_nodes", "er_graph_num_arcs",
             "er_graph_kernel_launches", "er_opts_default", "er_query_batch_ex", "er_spmm",
-            "er_graph_profile", "er_graph_profile_read", "er_smm_series", "er_spmm_ex"]
+            "er_graph_profile", "er_graph_profile_read", "er_smm_series", "er_spmm_ex", "er_probe_random_loads"]
 
 
 class er_opts(ctypes.Structure):
@@ -103,6 +103,8 @@ def _load():
     L.er_spmm.restype = ctypes.c_int
     L.er_spmm_ex.argtypes = [vp, vp, vp, i32, i32, vp]
     L.er_spmm_ex.restype = ctypes.c_int
+    L.er_probe_random_loads.argtypes = [i64, i32, i32, ctypes.POINTER(dbl)]
+    L.er_probe_random_loads.restype = ctypes.c_int
     L.er_smm_series.argtypes = [vp, vp, i64, dbl, i32, vp, vp]
     L.er_smm_series.restype = ctypes.c_int
     L.er_graph_profile.argtypes = [vp, ctypes.c_int]
@@ -183,6 +185,13 @@ def er_graph_estimate_lambda(g, iters: int = 0) -> float:
 
 def er_graph_kernel_launches(g) -> int:
     return int(_get().er_graph_kernel_launches(g))
+
+
+def er_probe_random_loads(nbytes: int, flavour: int, iters: int = 64) -> float:
+    """10^9 random 8-byte loads per second on the current device (include/geer.h)."""
+    out = ctypes.c_double()
+    _raise(_get().er_probe_random_loads(int(nbytes), int(flavour), int(iters), ctypes.byref(out)))
+    return out.value
 
 
 def er_graph_num_nodes(g) -> int:

@@ -12,7 +12,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgeer.so"
-SOURCES = ["pipeline.cu", "smm_push.cu", "validate.cu", "ytable.cu", "walks.cu", "dense.cu", "abi.cu", "lambda.cu", "spmm.cu"]
+SOURCES = ["pipeline.cu", "smm_push.cu", "validate.cu", "ytable.cu", "walks.cu", "dense.cu", "abi.cu", "lambda.cu", "spmm.cu", "probe.cu"]
 HEADERS = ["geer_internal.h", "geer_device.cuh", "stages.h", "scan.cuh"]
 INCLUDE = PKG.parent / "include" / "geer.h"
 
