@@ -20,16 +20,16 @@ __device__ __forceinline__ uint64_t probe_mix(uint64_t x)
     return x;
 }
 
-template <int FL>
+template <int FL, int U>
 __global__ void __launch_bounds__(256) k_probe_loads(const uint64_t *__restrict__ buf, uint64_t nsect, int iters,
                                                      unsigned long long *__restrict__ sink)
 {
     uint64_t x = probe_mix((uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1) | 1ull;
     uint64_t acc = 0;
     for (int it = 0; it < iters; it++) {
-        uint64_t v[8];
+        uint64_t v[U];
 #pragma unroll
-        for (int u = 0; u < 8; u++) {   // xorshift64: the next sector, independent of every load
+        for (int u = 0; u < U; u++) {   // xorshift64: the next sector, independent of every load
             x ^= x << 13;
             x ^= x >> 7;
             x ^= x << 17;
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) k_probe_loads(const uint64_t *__restrict_
             else asm volatile("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(v[u]) : "l"(p));
         }
 #pragma unroll
-        for (int u = 0; u < 8; u++) acc += v[u];
+        for (int u = 0; u < U; u++) acc += v[u];
     }
     if (acc == 0x5E47ull) atomicAdd(sink, 1ull);   // keeps the loads
 }
@@ -68,20 +68,22 @@ extern "C" int er_probe_random_loads(int64_t bytes, int32_t flavour, int32_t ite
     const uint64_t nsect = (uint64_t)bytes / 32;
     for (int rep = 0; rep < 4 && e == cudaSuccess; rep++) {      // rep 0 warms up
         cudaEventRecord(e0);
-        if (flavour == 0) k_probe_loads<0><<<blocks, threads>>>(buf, nsect, iters, sink);
-        else k_probe_loads<1><<<blocks, threads>>>(buf, nsect, iters, sink);
+        if (flavour == 0) k_probe_loads<0, 8><<<blocks, threads>>>(buf, nsect, iters, sink);
+        else k_probe_loads<1, 8><<<blocks, threads>>>(buf, nsect, iters, sink);
         cudaEventRecord(e1);
         e = cudaEventSynchronize(e1);
         float ms = 0.f;
         if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
         if (rep > 0 && (best == 0.f || ms < best)) best = ms;
     }
+    const double per_thread = 8.0;   // loads in flight per thread (4 and 16 measure the same rate:
+                                     // profiles/probe_sweep_r02.jsonl)
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
     if (buf) cudaFree(buf);
     if (sink) cudaFree(sink);
     if (e != cudaSuccess) return geer::cuda_fail(e, "er_probe_random_loads");
-    *g_loads_per_s = (double)blocks * threads * iters * 8.0 / (best * 1e-3) / 1e9;
+    *g_loads_per_s = (double)blocks * threads * iters * per_thread / (best * 1e-3) / 1e9;
     return ER_OK;
 }

@@ -683,3 +683,16 @@ def test_device_validation_matches_host(geer, case):
     want = {"range": geer.ER_EINVAL, "selfloop": geer.ER_ESELFLOOP, "dup": geer.ER_EDUP, "asym": geer.ER_EASYM,
             "disconnected": geer.ER_EDISCONNECTED, "bipartite": geer.ER_EBIPARTITE, "ok": "ok", "unsorted": "ok"}[case]
     assert res["0"][0] == want, res
+
+
+@pytest.mark.gpu
+def test_probe_random_loads(geer):
+    # the live ceiling bench.py quotes K6 against: an L2-resident buffer serves random
+    # sectors several times faster than a DRAM-resident one; bad arguments fail with ER_EINVAL
+    l2 = geer.er_probe_random_loads(48 << 20, 0, 16)
+    dram = geer.er_probe_random_loads(256 << 20, 1, 16)
+    assert 100.0 < l2 < 1000.0 and 10.0 < dram < 200.0 and l2 > 2.0 * dram, (l2, dram)
+    with pytest.raises(geer.GeerError):
+        geer.er_probe_random_loads(1024, 0, 1)
+    with pytest.raises(geer.GeerError):
+        geer.er_probe_random_loads(48 << 20, 2, 1)
