@@ -379,6 +379,11 @@ er_graph *er_graph_create_ex(int64_t n, const int64_t *offsets, const int32_t *c
         if (const char *env = getenv("GEER_MAX_SUB_BATCH")) g->max_sub_batch = std::max<int64_t>(1, atoll(env));
         if (const char *env = getenv("GEER_WAVE_PAIRS_MAX")) g->wave_pairs_max = std::max<int64_t>(1, atoll(env));
         if (const char *env = getenv("GEER_WALK_NP")) g->walk_np = atoi(env) == 1 ? 1 : 2;
+        {   // ER_ENOMEM fault injection (tests): the N-th workspace growth from here on fails once
+            const char *env = getenv("GEER_FAULT_ALLOC");
+            geer::g_fault_count = 0;
+            geer::g_fault_target = env ? std::max<int64_t>(0, atoll(env)) : 0;
+        }
         if (const char *env = getenv("GEER_HUB_CB")) { const int v = atoi(env); g->hub_cb = (v == 8 || v == 16) ? v : 32; }
         if (const char *env = getenv("GEER_WALK_SMEM_KB")) g->walk_smem_words = 256 * std::min(48, std::max(0, atoi(env)));
         if (const char *env = getenv("GEER_RANK_MIN_CAP")) g->rank_min_cap = std::max<int64_t>(0, atoll(env));

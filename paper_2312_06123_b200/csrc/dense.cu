@@ -112,6 +112,7 @@ bool dense_wave_pays(const er_graph *g, int32_t na, int64_t E)
 
 int smm_dense_wave(Ctx &c, int32_t na, int64_t F, const int32_t *act, int64_t *dU)
 {
+    NvtxRange nvtx_("geer/smm_dense");
     er_graph *g = c.g;
     Workspace &ws = c.ws;
     cudaStream_t st = c.st;

@@ -3,8 +3,10 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -102,6 +104,15 @@ struct BatchParams {
     uint64_t seed;
     int64_t qbase;          // global index of query 0
     int64_t n;
+};
+
+// NVTX range for the host-side stages (visible in nsys / ncu --nvtx; a no-op without a tool
+// attached): "geer/batch", "geer/smm_wave", "geer/ytable", "geer/amc", "geer/spmm", ...
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
 };
 
 // Grow-only device buffer.
@@ -212,6 +223,8 @@ struct er_graph {
 namespace geer {
 
 void set_error(int code, const std::string &msg);
+// ER_ENOMEM fault injection (pipeline.cu): the g_fault_target-th workspace growth fails.
+extern std::atomic<int64_t> g_fault_target, g_fault_count;
 int cuda_fail(cudaError_t e, const char *what);
 
 // Pipeline entry (pipeline.cu).

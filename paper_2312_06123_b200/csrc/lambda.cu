@@ -195,6 +195,7 @@ static bool tridiag_ql(int m, std::vector<double> a, std::vector<double> b, std:
 
 int run_estimate_lambda(er_graph *g, int iters, double *lambda_out)
 {
+    NvtxRange nvtx_("geer/lambda");
     const int64_t n = g->n;
     cudaStream_t st = g->stream;
     const int64_t by_mem = (int64_t)(LZ_BASIS_BYTES / (8.0 * (double)n)) - 1;

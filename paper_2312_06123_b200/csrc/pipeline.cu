@@ -25,6 +25,8 @@
 #include <cstring>
 
 #include "geer_device.cuh"
+#include <atomic>
+
 #include "stages.h"
 
 #include <vector>
@@ -430,9 +432,14 @@ __global__ void k_select(int32_t n, const int32_t *__restrict__ in, const int32_
 
 // ============================================================================ host side
 
+// ER_ENOMEM fault injection (tests): GEER_FAULT_ALLOC=N, read at er_graph_create, makes the N-th
+// workspace growth after it fail like an out-of-memory cudaMalloc (once).
+std::atomic<int64_t> g_fault_target{0}, g_fault_count{0};
+
 cudaError_t DevBuf::ensure(size_t bytes, bool keep, cudaStream_t st)
 {
     if (bytes <= cap) return cudaSuccess;
+    if (g_fault_target.load() > 0 && ++g_fault_count == g_fault_target.load()) return cudaErrorMemoryAllocation;
     size_t ncap = std::max(bytes, cap + cap / 2);
     ncap = (ncap + 255) & ~(size_t)255;
     void *np = nullptr;
@@ -507,6 +514,7 @@ int select_list(Ctx &c, const int32_t *ids, const int32_t *flag, int32_t n, int3
 int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, double p_fail, const er_opts &o,
                     double *out_r, er_query_stats *stats)
 {
+    NvtxRange nvtx_("geer/batch");
     Workspace &ws = g->ws;
     // The batch runs on the handle's high-priority head stream (so SMM-head kernels are scheduled
     // ahead of AMC walk CTAs when both are queued), forked from and joined back into the
@@ -690,6 +698,7 @@ int run_query_batch(er_graph *g, const int32_t *pairs, int64_t k, double eps, do
         const cudaStream_t ystream = overlap ? nullptr : g->ybuild_stream;
         bool y_pending = false;
         while (na > 0) {
+            NvtxRange nvtx_wave("geer/smm_wave");
             const int32_t nseg = (int32_t)(2 * na);
             // emission offsets
             ENSURE(ws.ent_off, sizeof(int64_t) * (2 * F + 2), false);

@@ -721,6 +721,7 @@ PushView push_view(Workspace &ws, int32_t nseg, int64_t NBmax)
 // wave's pair enumeration ent_off.
 int smm_push_wave_a(Ctx &c, int32_t g0, int32_t ns, int64_t P0, int64_t E, const int64_t *ent_off)
 {
+    NvtxRange nvtx_("geer/smm_push");
     Workspace &ws = c.ws;
     er_graph *g = c.g;
     const cudaStream_t st = c.st;

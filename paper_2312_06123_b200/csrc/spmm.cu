@@ -343,6 +343,7 @@ void launch_rows(er_graph *g, const double *X, double *Y, double *part, int32_t 
 
 int run_spmm(er_graph *g, const double *X, double *Y, int32_t q, int32_t normalize, cudaStream_t st, bool exact)
 {
+    NvtxRange nvtx_("geer/spmm");
     if (!g->d_rowperm) {
         const int rc = build_spmm_plan(g, g->stream);
         if (rc) return rc;
@@ -430,6 +431,7 @@ __global__ void k_series_acc(int32_t q, int32_t i, const int32_t *__restrict__ p
 int run_smm_series(er_graph *g, const int32_t *pairs, int64_t k, double tol, int32_t max_iters, double *out_r,
                    int32_t *ells)
 {
+    NvtxRange nvtx_("geer/smm_series");
     const int64_t n = g->n;
     const int32_t QB = 64;
     cudaStream_t st = g->stream;

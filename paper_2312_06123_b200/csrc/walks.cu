@@ -594,6 +594,7 @@ __global__ void k_amc_reduce(int32_t na, const int32_t *__restrict__ amc, const 
 int launch_amc_group(er_graph *g, cudaStream_t sb, const AmcGroup &G, QState *qs, const BatchParams &P, bool prof,
                      BatchRes &R)
 {
+    NvtxRange nvtx_("geer/amc");
     const int32_t na = G.na;
     if (na == 0) return ER_OK;
     // per-group buffers (stream ordered on the AMC stream)

@@ -423,6 +423,7 @@ int ytable_plan(Ctx &c, int32_t na, const int32_t *act, const int32_t *cont, con
 int ytable_build(Ctx &c, int32_t na, const int32_t *act, const int64_t *segoff, const int32_t *id, const double *val,
                  const int32_t *seg, int64_t Fmax, const int64_t *dF, int wave, int64_t H, int64_t V, int64_t R)
 {
+    NvtxRange nvtx_("geer/ytable");
     Workspace &ws = c.ws;
     const YSizes *sz = ws.ycap.as<YSizes>(), *incl = ws.yoff.as<YSizes>();
     const int32_t *perm = c.g->d_cblk ? c.g->d_perm : nullptr;   // keys in the walk kernel's ids

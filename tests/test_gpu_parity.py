@@ -696,3 +696,37 @@ def test_probe_random_loads(geer):
         geer.er_probe_random_loads(1024, 0, 1)
     with pytest.raises(geer.GeerError):
         geer.er_probe_random_loads(48 << 20, 2, 1)
+
+
+@pytest.mark.gpu
+def test_enomem_fault_injection_recovers(geer, tiny):
+    # GEER_FAULT_ALLOC=N makes the N-th workspace growth after er_graph_create fail like an
+    # out-of-memory cudaMalloc: the batch fails with ER_ENOMEM (or succeeds when N is past the last
+    # growth), and the same handle then answers the batch bit-identically to an unfaulted run
+    import os
+    g, pairs = tiny
+    h = geer.er_graph_create(g.n, g.offsets, g.cols)
+    geer.er_graph_set_lambda(h, g.lam)
+    ref = geer.er_query_batch(h, pairs, 0.1, 0.01)
+    geer.er_graph_destroy(h)
+    failed = 0
+    try:
+        for n in (1, 2, 3, 5, 8, 13, 21, 34, 55):
+            os.environ["GEER_FAULT_ALLOC"] = str(n)
+            h = geer.er_graph_create(g.n, g.offsets, g.cols)
+            try:
+                geer.er_graph_set_lambda(h, g.lam)
+                try:
+                    geer.er_query_batch(h, pairs, 0.1, 0.01)
+                except geer.GeerError as e:
+                    assert e.code == geer.ER_ENOMEM, e
+                    failed += 1
+                r = geer.er_query_batch(h, pairs, 0.1, 0.01)
+                assert r.tobytes() == ref.tobytes(), n
+            finally:
+                geer.er_graph_destroy(h)
+    finally:
+        os.environ.pop("GEER_FAULT_ALLOC", None)
+        h = geer.er_graph_create(g.n, g.offsets, g.cols)   # resets the injection
+        geer.er_graph_destroy(h)
+    assert failed >= 3
