@@ -4,6 +4,16 @@
 
 #include "stages.h"
 
+// Column chunk loads of DRAM-resident walk graphs skip L1 (they are never reused; the y records
+// keep the L1 lines: LJ-shaped walks 361.4 -> 357.2 ms on one box); y loads with L1 evict_last
+// measured slower (366.8 ms).  Both are compile-time switches for A/B builds.
+#ifndef GEER_COL_L1NA
+#define GEER_COL_L1NA 1
+#endif
+#ifndef GEER_Y_L1EL
+#define GEER_Y_L1EL 0
+#endif
+
 namespace geer {
 
 // Chunks of walk pairs of batch b per AMC query, and the AMC sort key (descending ell_f) used to
@@ -136,8 +146,13 @@ __device__ __forceinline__ uint4 ld_arc_v4(const uint4 *p, uint64_t apol)
 {
     if (!DL) return __ldg(p);
     uint4 r;
+#if GEER_COL_L1NA
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(apol));
+#else
     asm("ld.global.nc.L2::cache_hint.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
         : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(apol));
+#endif
     return r;
 }
 template <bool DL>
@@ -165,8 +180,24 @@ __device__ __forceinline__ uint2 ld_rec(const uint2 *p)
     asm("ld.global.nc.L2::64B.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
+
+#if GEER_Y_L1EL
+__device__ __forceinline__ double ld_y(const double *p)
+{
+    double v;
+    asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_y(const uint4 *p)
+{
+    uint4 r;
+    asm("ld.global.nc.L1::evict_last.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+#else
 __device__ __forceinline__ double ld_y(const double *p) { return __ldg(p); }
 __device__ __forceinline__ uint4 ld_y(const uint4 *p) { return __ldg(p); }
+#endif
 
 // Hash lookups: slot of v, or -1 when v is not in supp(y) (then y(v) = 0, Alg. 1 L7 outside
 // U_s and U_t).  Staged keys in shared memory, or the table in global memory (one 16-byte
