@@ -81,6 +81,22 @@ def random_dram_ceiling():
     return None
 
 
+def head_spmm(alg_bytes: float, head_ms: float, config: str):
+    """SURVEY 8(d)'s SpMM GB/s of the GEER head, two ways: algorithmic (12 B per push pair) and the
+    DRAM bytes of the head's kernels in one call (committed ncu launch list,
+    profiles/ncu_smm_head_<config>_r*.json), both over the live head time."""
+    out = {"algorithmic_bytes_per_step": alg_bytes, "algorithmic_gbs": alg_bytes / max(head_ms / 1e3, 1e-12) / 1e9,
+           "note": "SURVEY 8(d): 12 B per push pair (column + value), over the SMM head's event time (push, "
+                   "grouping, stats, y-tables)"}
+    nc, src = ncu_summary("smm_head", config)
+    if nc:
+        out.update({"ncu_dram_bytes_per_step": nc["dram_bytes_per_call"],
+                    "dram_gbs": nc["dram_bytes_per_call"] / max(head_ms / 1e3, 1e-12) / 1e9,
+                    "dram_over_algorithmic": nc["dram_bytes_per_call"] / max(alg_bytes, 1.0),
+                    "ncu_source": src})
+    return out
+
+
 def live_probe(nbytes: int, flavour: int):
     """The random-load ceiling of this device (G loads/s, er_probe_random_loads), or None."""
     try:
@@ -657,10 +673,7 @@ def main():
                                    "walk_ctas_per_sm": prof["walk_ctas_per_sm"],
                                    "smm_waves_per_step": prof["smm_waves"] / args.steps,
                                    "smm_dense_waves_per_step": prof["smm_dense_waves"] / args.steps},
-            "smm_head_spmm": {"algorithmic_bytes_per_step": smm_alg / args.steps,
-                              "algorithmic_gbs": smm_alg / max(prof["smm_ms"] / 1e3, 1e-12) / 1e9,
-                              "note": "SURVEY 8(d): 12 B per push pair (column + value), over the SMM head's "
-                                      "event time (push, grouping, stats, y-tables)"},
+            "smm_head_spmm": head_spmm(smm_alg / args.steps, prof["smm_ms"], args.config),
             "queries_split": split,
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(pairs.nbytes),
                     "d2h_bytes_per_step": int(nq * 8)},
