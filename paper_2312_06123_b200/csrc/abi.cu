@@ -461,6 +461,7 @@ void er_graph_destroy(er_graph *g)
         if (g->d_hseg) cudaFree(g->d_hseg);
         if (g->d_seg_e0) cudaFree(g->d_seg_e0);
         if (g->d_seg_row) cudaFree(g->d_seg_row);
+        if (g->d_spmm_desc) cudaFree(g->d_spmm_desc);
         if (g->amc_stream) cudaStreamSynchronize(g->amc_stream);
         if (g->stream) cudaStreamDestroy(g->stream);
         if (g->amc_stream) cudaStreamDestroy(g->amc_stream);

@@ -214,6 +214,7 @@ struct er_graph {
     int64_t *d_hseg = nullptr;     // K9: first segment of each heavy row (n_heavy + 1)
     int64_t *d_seg_e0 = nullptr;   // K9: first arc of each segment
     int32_t *d_seg_row = nullptr;  // K9: row of each segment
+    int4 *d_spmm_desc = nullptr;   // K9: work items {first arc (2 words), length, row | -1 - segment}
     int hub_cb = 32;                     // K9 exact: columns per heavy-row CTA (GEER_HUB_CB 8/16/32)
     cudaStream_t spmm_stream = nullptr;  // K9 exact: heavy rows concurrent with the light rows
     cudaEvent_t spmm_fork = nullptr, spmm_join = nullptr;

@@ -22,7 +22,10 @@
 //  * one sub-warp of LPR lanes per item; lane l owns the 16-byte column vectors l, l+LPR, ...
 //    of the row (128-bit loads of X rows, coalesced across the sub-warp); the neighbour loop is
 //    unrolled by 8 so 8 independent gathers are in flight per lane, then added in CSR order;
-//  * heavy-row segment sums go to a scratch block and a second kernel adds them per row.
+//  * heavy-row segment sums go to a scratch block and a second kernel adds them per row;
+//  * q <= 64 (one column vector per lane): k_spmm_items, the same items and sums pipelined
+//    across items (precomputed item descriptors, the next item's neighbour ids loaded during the
+//    current item's last round of gathers).
 // No tensor cores: the contraction has one nonzero per (row, neighbour) and fp64 accumulation.
 
 
@@ -37,7 +40,12 @@ namespace geer {
 namespace {
 
 constexpr int SPMM_THREADS = 256;
-constexpr int SPMM_UNROLL = 8;
+#ifndef SPMM_UNROLL
+#define SPMM_UNROLL 8   // k_spmm_rows: neighbours (X gathers) in flight per lane and round
+#endif
+#ifndef SPMM_PUNROLL
+#define SPMM_PUNROLL 6  // k_spmm_items: the same (A/B on the LJ-shaped graph: 6 beats 4 and 8)
+#endif
 
 inline unsigned blocks_for(int64_t n, int per) { return (unsigned)((n + per - 1) / per); }
 
@@ -112,6 +120,92 @@ k_spmm_rows(int64_t nseg, int64_t nitems, const int64_t *__restrict__ seg_e0, co
         }
         if (norm) vdiv(acc, dv);
         out[cv] = acc;
+    }
+}
+
+// The same items and sums, software-pipelined across items (q <= 2 LPR VEC: one column vector
+// per lane).  Persistent sub-warps take items it, it + nsub, ... (round-robin over the
+// degree-descending item order); an item is a precomputed descriptor {first arc, length, row or
+// segment} (one coalesced 16-byte load, no dependent off[] load), loaded two items ahead; the
+// last round of an item loads the NEXT item's first neighbour ids while its own X gathers are in
+// flight, so a row costs one dependent round trip per round of SPMM_PUNROLL neighbours instead of
+// rows -> off -> cols -> X.  Sums and their order are those of k_spmm_rows (bit-identical).
+#ifndef SPMM_PIPE
+#define SPMM_PIPE 1   // 0: k_spmm_rows only; 2: descriptors one item ahead (A/B variants)
+#endif
+__device__ __forceinline__ int64_t desc_e0(const int4 d)
+{
+    return (int64_t)(((uint64_t)(uint32_t)d.y << 32) | (uint64_t)(uint32_t)d.x);
+}
+template <int LPR, int VEC>
+__global__ void __launch_bounds__(SPMM_THREADS, SPMM_MINB)
+k_spmm_items(int64_t nitems, const int4 *__restrict__ desc, const int32_t *__restrict__ cols,
+             const double *__restrict__ X, double *__restrict__ Y, double *__restrict__ part, int32_t q, int normalize)
+{
+    using V = typename VecT<VEC>::T;
+    const int64_t nsub = (int64_t)gridDim.x * (SPMM_THREADS / LPR);
+    int64_t it = ((int64_t)blockIdx.x * SPMM_THREADS + threadIdx.x) / LPR;
+    const int l = threadIdx.x % LPR;
+    const int32_t nvec = q / VEC;
+    if (it >= nitems || l >= nvec) return;   // no cross-lane operations below
+    const V *__restrict__ Xv = reinterpret_cast<const V *>(X);
+    const int4 zero = make_int4(0, 0, 0, 0);
+    int4 d = desc[it];
+    int64_t itn = it + nsub;
+#if SPMM_PIPE != 2
+    int4 dn = itn < nitems ? desc[itn] : zero;
+#endif
+    int32_t w[SPMM_PUNROLL];
+    {
+        const int64_t e0 = desc_e0(d);
+#pragma unroll
+        for (int j = 0; j < SPMM_PUNROLL; j++) w[j] = j < d.z ? __ldg(cols + e0 + j) : 0;
+    }
+    while (true) {
+        const int64_t itn2 = itn + nsub;
+#if SPMM_PIPE == 2
+        const int4 dn = itn < nitems ? desc[itn] : zero;      // one item ahead
+#else
+        const int4 dn2 = itn2 < nitems ? desc[itn2] : zero;   // two items ahead
+#endif
+        const int64_t e0 = desc_e0(d), en0 = desc_e0(dn);
+        const int32_t len = d.z, lenn = dn.z;   // lenn = 0 past the end
+        V acc;
+        vzero(acc);
+        for (int32_t e = 0; e < len; e += SPMM_PUNROLL) {
+            const int32_t rem = len - e;
+            V x[SPMM_PUNROLL];
+#pragma unroll
+            for (int j = 0; j < SPMM_PUNROLL; j++)
+                if (j < rem) x[j] = __ldg(Xv + (int64_t)w[j] * nvec + l);
+            if (rem > SPMM_PUNROLL) {   // this item's next round
+#pragma unroll
+                for (int j = 0; j < SPMM_PUNROLL; j++)
+                    w[j] = SPMM_PUNROLL + j < rem ? __ldg(cols + e0 + e + SPMM_PUNROLL + j) : 0;
+            } else {                   // the next item's first round
+#pragma unroll
+                for (int j = 0; j < SPMM_PUNROLL; j++) w[j] = j < lenn ? __ldg(cols + en0 + j) : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < SPMM_PUNROLL; j++)
+                if (j < rem) vadd(acc, x[j]);   // CSR order (R13)
+        }
+        if (len == 0) {
+#pragma unroll
+            for (int j = 0; j < SPMM_PUNROLL; j++) w[j] = j < lenn ? __ldg(cols + en0 + j) : 0;
+        }
+        if (d.w >= 0) {   // a light row: Y[v] (the full row)
+            if (normalize) vdiv(acc, (double)len);
+            reinterpret_cast<V *>(Y)[(int64_t)d.w * nvec + l] = acc;
+        } else {          // a heavy-row segment: its partial sum
+            reinterpret_cast<V *>(part)[(int64_t)(-1 - d.w) * nvec + l] = acc;
+        }
+        if (itn >= nitems) break;
+        itn = itn2;
+        d = dn;
+#if SPMM_PIPE != 2
+        dn = dn2;
+#endif
     }
 }
 
@@ -308,6 +402,24 @@ int build_spmm_plan(er_graph *g, cudaStream_t st)
         CK(cudaMemcpy(g->d_seg_e0, seg_e0.data(), sizeof(int64_t) * g->n_seg, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(g->d_seg_row, seg_row.data(), sizeof(int32_t) * g->n_seg, cudaMemcpyHostToDevice));
     }
+    // item descriptors of k_spmm_items: the segments, then the light rows (degree-descending)
+    {
+        const int64_t ni = g->n_seg + (n - nh);
+        std::vector<int4> desc(std::max<int64_t>(ni, 1));
+        auto mk = [](int64_t e0, int64_t len, int32_t dst) {
+            return make_int4((int)(uint32_t)(uint64_t)e0, (int)(uint32_t)((uint64_t)e0 >> 32), (int)len, dst);
+        };
+        for (int64_t p = 0; p < g->n_seg; p++) {
+            const int32_t v = seg_row[p];
+            desc[p] = mk(seg_e0[p], std::min<int64_t>(SPMM_SEG, off[v + 1] - seg_e0[p]), (int32_t)(-1 - p));
+        }
+        for (int64_t r = nh; r < n; r++) {
+            const int32_t v = perm[r];
+            desc[g->n_seg + (r - nh)] = mk(off[v], off[v + 1] - off[v], v);
+        }
+        CK(cudaMalloc(&g->d_spmm_desc, sizeof(int4) * desc.size()));
+        CK(cudaMemcpy(g->d_spmm_desc, desc.data(), sizeof(int4) * desc.size(), cudaMemcpyHostToDevice));
+    }
     return ER_OK;
 }
 
@@ -322,6 +434,24 @@ void launch_rows(er_graph *g, const double *X, double *Y, double *part, int32_t 
     const int64_t nseg = exact ? 0 : g->n_seg;
     const int64_t nitems = nseg + (g->n - g->n_heavy);
     if (nitems == 0) return;
+    if (SPMM_PIPE && nvec <= lpr) {   // one column vector per lane: the pipelined item kernel
+        const int4 *desc = g->d_spmm_desc + (exact ? g->n_seg : 0);
+        const unsigned pgrid = (unsigned)std::min<int64_t>(blocks_for(nitems * lpr, SPMM_THREADS),
+                                                           (int64_t)g->num_sms * SPMM_MINB);
+#define P(LPR)                                                                                                  \
+    k_spmm_items<LPR, VEC><<<pgrid, SPMM_THREADS, 0, st>>>(nitems, desc, g->d_cols, X, Y, part, q, normalize)
+        switch (lpr) {
+            case 1: P(1); break;
+            case 2: P(2); break;
+            case 4: P(4); break;
+            case 8: P(8); break;
+            case 16: P(16); break;
+            default: P(32); break;
+        }
+#undef P
+        g->launches++;
+        return;
+    }
     const unsigned grid = blocks_for(nitems * lpr, SPMM_THREADS);
 #define L(LPR)                                                                                               \
     k_spmm_rows<LPR, VEC><<<grid, SPMM_THREADS, 0, st>>>(nseg, nitems, g->d_seg_e0, g->d_seg_row,              \

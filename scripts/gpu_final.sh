@@ -21,9 +21,9 @@ for CFG in lj_full rmat20; do
   python scripts/ncu_summary.py walks gpurun_out/walks_$CFG.ncu-rep $CFG gpurun_out/walk_steps_$CFG.json \
       > gpurun_out/ncu_k_walks_${CFG}_final.json 2> gpurun_out/ncu_summary_$CFG.err
 done
-timeout 900 ncu --set full --clock-control none -k regex:k_spmm_rows -s 3 -c 1 -f -o gpurun_out/spmm16_rmat20 \
+timeout 900 ncu --set full --clock-control none -k 'regex:k_spmm_(rows|items)' -s 3 -c 1 -f -o gpurun_out/spmm16_rmat20 \
     python scripts/spmm_probe.py rmat20 > gpurun_out/ncu_spmm16_rmat20.log 2>&1
-timeout 900 ncu --set full --clock-control none -k regex:k_spmm_rows -s 11 -c 1 -f -o gpurun_out/spmm64_rmat20 \
+timeout 900 ncu --set full --clock-control none -k 'regex:k_spmm_(rows|items)' -s 11 -c 1 -f -o gpurun_out/spmm64_rmat20 \
     python scripts/spmm_probe.py rmat20 > gpurun_out/ncu_spmm64_rmat20.log 2>&1
 python scripts/ncu_summary.py spmm gpurun_out/spmm16_rmat20.ncu-rep rmat20 16 > gpurun_out/ncu_k_spmm_q16_rmat20.json 2>/dev/null
 python scripts/ncu_summary.py spmm gpurun_out/spmm64_rmat20.ncu-rep rmat20 64 > gpurun_out/ncu_k_spmm_q64_rmat20.json 2>/dev/null

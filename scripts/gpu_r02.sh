@@ -23,9 +23,9 @@ if [ "$PART" = profile ] || [ "$PART" = all ]; then
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_walks -s 5 -c 1 -f \
       -o gpurun_out/walks_$CFG python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-spmm \
       --no-accuracy > gpurun_out/ncu_walks_$CFG.log 2>&1
-  timeout 900 ncu --set full --clock-control none -k regex:k_spmm_rows -s 3 -c 1 -f -o gpurun_out/spmm16_$CFG \
+  timeout 900 ncu --set full --clock-control none -k 'regex:k_spmm_(rows|items)' -s 3 -c 1 -f -o gpurun_out/spmm16_$CFG \
       python scripts/spmm_probe.py $CFG > gpurun_out/ncu_spmm16_$CFG.log 2>&1
-  timeout 900 ncu --set full --clock-control none -k regex:k_spmm_rows -s 11 -c 1 -f -o gpurun_out/spmm64_$CFG \
+  timeout 900 ncu --set full --clock-control none -k 'regex:k_spmm_(rows|items)' -s 11 -c 1 -f -o gpurun_out/spmm64_$CFG \
       python scripts/spmm_probe.py $CFG > gpurun_out/ncu_spmm64_$CFG.log 2>&1
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 800 --csv \
       --log-file gpurun_out/launches_$CFG.csv python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline \

@@ -20,7 +20,8 @@ h = G.er_graph_create(g.n, g.offsets, g.cols)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 out = {"lib": os.environ.get("GEER_LIB", "in-tree"), "config": cfg}
 for q in (16, 64):
-    X = torch.rand((g.n, q), dtype=torch.float64, device="cuda")
+    X = torch.rand((g.n, q), dtype=torch.float64, device="cuda",
+                   generator=torch.Generator(device="cuda").manual_seed(q))   # same X for every variant
     Y = torch.empty_like(X)
     ts = []
     for i in range(8):
