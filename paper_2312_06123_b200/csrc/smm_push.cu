@@ -417,10 +417,13 @@ __global__ void __launch_bounds__(BKT_NT) k_bkt_reduce(
 // of (u_low, e) keys, values gathered in sorted order, one lane per run of equal u summing its
 // values in ascending e, / d(u); statistics reduced over the warp.
 struct WarpSmem {
-    unsigned int a[BKT_WCAP], b[BKT_WCAP];   // 32-bit keys (buckets with wider keys: k_bkt_reduce)
+    unsigned int a[BKT_WCAP], b[BKT_WCAP];   // 32-bit keys (buckets with wider keys: k_bkt_reduce);
+                                             // after the sort the other buffer holds the run heads
     unsigned int cnt[256];
-    unsigned short runs[BKT_WCAP];
 };
+#ifndef BKT_RW_MINB
+#define BKT_RW_MINB 4   // resident CTAs per SM k_bkt_reduce_warp is compiled for (64 registers)
+#endif
 
 // Stable LSD passes over key bits [0, bits), 8 bits per pass (one warp, 32-bit keys).
 __device__ __forceinline__ unsigned int *warp_radix_sort(unsigned int *a, unsigned int *b, int n, int bits,
@@ -475,7 +478,7 @@ __device__ __forceinline__ unsigned int *warp_radix_sort(unsigned int *a, unsign
     return src;
 }
 
-__global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
+__global__ void __launch_bounds__(32 * BKT_WPB, BKT_RW_MINB) k_bkt_reduce_warp(
     int32_t g0, const int64_t *__restrict__ dNB, const int32_t *__restrict__ bseg, const int64_t *__restrict__ segBoff,
     const int32_t *__restrict__ segsh, const int32_t *__restrict__ segeb, const int64_t *__restrict__ boff,
     const unsigned long long *__restrict__ keys, const int64_t *__restrict__ fr_off, const double *__restrict__ fr_val,
@@ -508,6 +511,7 @@ __global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
         for (int i = lane; i < n; i += 32) M.a[i] = (unsigned)keys[base + i];
         __syncwarp();
         const unsigned *srt = warp_radix_sort(M.a, M.b, n, sh + eb, M.cnt);
+        unsigned int *runs = srt == M.a ? M.b : M.a;
         const double *__restrict__ fv = fr_val + fr_off[g];
         const unsigned emask = eb >= 32 ? 0xffffffffu : (1u << eb) - 1u;
         // run heads and their ranks
@@ -516,7 +520,7 @@ __global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
             const int i = t0 + lane;
             const bool head = i < n && (i == 0 || (eb < 32 && (srt[i] >> eb) != (srt[i - 1] >> eb)));
             const unsigned bal = __ballot_sync(full, head);
-            if (head) M.runs[U + __popc(bal & ((1u << lane) - 1u))] = i;
+            if (head) runs[U + __popc(bal & ((1u << lane) - 1u))] = i;
             U += __popc(bal);
         }
         __syncwarp();
@@ -526,7 +530,7 @@ __global__ void __launch_bounds__(32 * BKT_WPB) k_bkt_reduce_warp(
         double at_s = 0.0, at_t = 0.0;
         int flags = 0;
         for (int r = lane; r < U; r += 32) {
-            const int i0 = M.runs[r], i1 = r + 1 < U ? M.runs[r + 1] : n;
+            const int i0 = runs[r], i1 = r + 1 < U ? runs[r + 1] : n;
             double sum = 0.0;
             for (int i = i0; i < i1; i++) sum += fv[srt[i] & emask];   // ascending source order (R13)
             const int32_t u = (int32_t)((hi << sh) | (int64_t)(eb >= 32 ? 0u : srt[i0] >> eb));
