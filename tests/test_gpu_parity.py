@@ -411,6 +411,39 @@ def test_spmm_k9_every_column(geer, q):
         geer.er_graph_destroy(h)
 
 
+@pytest.mark.parametrize("q", [2, 6, 16, 64])
+def test_spmm_k9_item_pipeline_row_lengths(geer, q):
+    """k_spmm_items (q <= 64) hands each sub-warp rows one after another, loading the next row's
+    first neighbour ids during the current row's last gather round: rows of every degree 1..60
+    (around multiples of the 6 gathers per round), interleaved in id order, bit-identical to the
+    oracle's sequential pull, in both the exact and the segmented mode."""
+    import torch
+    E, nxt = [], 60
+    for c in range(60):                     # star centre c: c + 1 leaves, chained to c + 1
+        for _ in range(c):
+            E.append((c, nxt))
+            nxt += 1
+        if c + 1 < 60:
+            E.append((c, c + 1))
+    E += [(0, nxt), (nxt, nxt + 1)]         # degree 2
+    g = W.from_edges(nxt + 2, E, "stars")
+    assert set(range(1, 61)) <= set(g.degrees().tolist())
+    h = geer.er_graph_create(g.n, g.offsets, g.cols, flags=geer.ER_CREATE_SPMM_ONLY)
+    try:
+        X = np.random.default_rng(40 + q).random((g.n, q))
+        Xd = torch.from_numpy(X).cuda()
+        for exact_ in (False, True):
+            for normalize in (True, False):
+                Y = torch.full((g.n, q), np.nan, dtype=torch.float64, device="cuda")
+                geer.er_spmm(h, Xd, Y, normalize=normalize, exact=exact_)
+                Yh = Y.cpu().numpy()
+                for c in range(q) if q <= 16 else (0, 31, q - 1):
+                    want = oracle.propagate_dense(g, X[:, c], normalize=normalize)
+                    assert np.array_equal(Yh[:, c], want), (q, c, exact_, normalize)
+    finally:
+        geer.er_graph_destroy(h)
+
+
 def test_spmm_k9_unaligned_block(geer):
     """A block whose base is only 8-byte aligned takes the scalar path; same bits."""
     import torch
