@@ -673,7 +673,7 @@ def main():
                                    "walk_ctas_per_sm": prof["walk_ctas_per_sm"],
                                    "smm_waves_per_step": prof["smm_waves"] / args.steps,
                                    "smm_dense_waves_per_step": prof["smm_dense_waves"] / args.steps},
-            "smm_head_spmm": head_spmm(smm_alg / args.steps, prof["smm_ms"], args.config),
+            "smm_head_spmm": head_spmm(smm_alg / args.steps, prof["smm_ms"] / args.steps, args.config),
             "queries_split": split,
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(pairs.nbytes),
                     "d2h_bytes_per_step": int(nq * 8)},
