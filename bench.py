@@ -184,7 +184,11 @@ WORKLOAD_NAMES = {
 def config_dict(g, args, world):
     import workloads as W
     gseed = W.CONFIGS[args.config][1]["seed"]
-    return {"workload": f"{WORKLOAD_NAMES.get(args.config, args.config)}, {args.queries} queries/GPU "
+    if args.scaling == "strong":
+        nq_label = f"{W.CONFIGS[args.config][2]} queries in all (one global list, cost-model partition over {world} GPU(s))"
+    else:
+        nq_label = f"{args.queries} queries/GPU"
+    return {"workload": f"{WORKLOAD_NAMES.get(args.config, args.config)}, {nq_label} "
                         f"(50% random pairs, 50% edges), eps={args.eps}, delta=0.01, tau=5",
             "baseline_config_index": {"tiny": 0, "rmat20": 1, "lj_full": 2, "orkut_full": 3,
                                       "friendster": 4}.get(args.config),
@@ -192,13 +196,15 @@ def config_dict(g, args, world):
             "lambda": float(g.lam) if g.lam is not None else None,
             "lambda_source": "workloads.lambda_for (ARPACK <= 2^24 arcs, else torch Lanczos with full "
                              "re-orthogonalisation), pinned on both arms",
-            "queries_per_gpu": args.queries, "eps": args.eps, "delta": 0.01, "tau": 5,
+            "queries_per_gpu": args.queries if args.scaling == "weak" else None,
+            "queries_total": args.queries * world if args.scaling == "weak" else W.CONFIGS[args.config][2],
+            "eps": args.eps, "delta": 0.01, "tau": 5,
             "parallelism": f"queries sharded over {world} GPU(s) ({args.scaling} scaling), CSR replicated",
             "l2": "flushed between steps (256 MiB device write outside the timed events); the graph and "
                   "walk state exceed L2",
             "switch_ratio": args.switch_ratio,
             "smm_mode": {0: "auto (cost model)", 1: "frontier push", 2: "dense pull"}[args.smm_mode],
-            "seeds": {"graph": gseed, "queries": "graph seed + 1 + rank", "walks": "0x2312061232DEC0DE"}}
+            "seeds": {"graph": gseed, "queries": "graph seed + 1 + rank" if args.scaling == "weak" else "graph seed + 1 (global list)", "walks": "0x2312061232DEC0DE"}}
 
 
 def load_workload(args):
