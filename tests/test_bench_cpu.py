@@ -84,3 +84,23 @@ def test_bench_gpu_line_tiny():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     ps = d["parity_summary"]
     assert ps["max_abs_diff_r"] <= 1e-9 and ps["ties"] == 0 and ps["walk_checksums_equal"] == ps["queries"]
+
+
+@pytest.mark.gpu
+def test_bench_gpu_line_tiny_strong_scaling():
+    """`--scaling strong` at N = 1: the global query list goes through dist.partition, query_ids and
+    the partition-order results; the line names the global list (no per-GPU count) and its sampled
+    parity against the oracle is clean."""
+    p = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "tiny", "--steps", "3", "--warmup", "3",
+                        "--no-spmm", "--scaling", "strong"], capture_output=True, text=True, cwd=str(ROOT),
+                       timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["scaling"] == "strong" and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["config"]["queries_total"] == 100 and d["config"]["queries_per_gpu"] is None
+    assert "queries in all" in d["config"]["workload"]
+    ps = d.get("parity_summary")
+    if ps:
+        assert ps["max_abs_diff_r"] <= 1e-9 and ps["walk_checksums_equal"] == ps["queries"]
