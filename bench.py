@@ -399,6 +399,22 @@ def walk_roofline(prof, args, hbm, hbm_how, max_ms):
                             "note": "random DRAM accesses are rate-bound, not bandwidth-bound: a random miss moves "
                                     "a 64-byte line (K6 loads use .L2::64B); the ceiling is the DRAM byte rate of "
                                     "independent random 64-byte-line loads over a buffer of the K6 working set's size"})
+                # context for walk graphs larger than the ceiling's buffer: the committed rate of the
+                # same loads over a buffer as large as the walk graph (lower: fewer L2 hits, TLB reach).
+                # peak stays the larger, 256 MB figure, so frac is never flattered by this.
+                tab = {int(k): v for k, v in (rc.get("g_loads_per_s_by_buffer_mb") or {}).items()}
+                wmb = prof["walk_graph_bytes"] / 2**20
+                fit = [k for k in tab if k <= wmb and k > rc["buffer_mb"]]
+                if fit:
+                    kmb = max(fit)
+                    out["ceiling_at_working_set"] = {
+                        "buffer_mb": kmb, "g_random_loads_per_s": tab[kmb], "dram_bytes_per_load": 63.8,
+                        "dram_gbs": tab[kmb] * 63.8,
+                        "note": "uniform random .L2::64B loads over the largest measured buffer <= the walk graph "
+                                "(profiles/sector_ubench_r02.jsonl, 63.8 DRAM bytes per load: "
+                                "profiles/sector_flavours_r02.txt); K6 can exceed it -- the first steps of a "
+                                "query's walks share s's and t's rows and hub rows stay in L2 -- so it is quoted "
+                                "beside the roofline, not as its peak"}
             else:
                 out.update({"bound": "hbm", "achieved": ach, "peak": hbm, "peak_kind": hbm_how, "unit": "GB/s",
                             "frac": ach / hbm})
